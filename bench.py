@@ -1,0 +1,337 @@
+"""bench.py — PCG iterations/s of the B200 hot path on BASELINE.json's config 5.
+
+One step = the whole hot path on the c5 workload
+(uniform 256x128x128 H8, 4.19M elements, 12.83M DOFs, x ~ U(0.001, 1)):
+SIMP scale, Jacobi diagonal, projected rhs, exactly 500 PCG iterations,
+recovery, sensitivities + compliance, Eq. 5 filter (rmin = 2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): every rank solves its own replica of the workload, no
+collective on the data path ("scaling": "weak"); value = total iterations/s.
+--impl reference times the oracle (plain numpy/scipy CPU program) on a
+bounded sample of the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_HBM_GBS = 6650.0
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(mx)) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _cpu_baseline(budget_s=15.0, sample_dims=(48, 24, 24)):
+    """The oracle as it stands (assembled CSR + textbook Jacobi-PCG, scipy, 1
+    thread) on a c5-recipe sub-box; PCG iterations/s scaled to the c5 DOF
+    count (cost per iteration is linear in DOFs for this sparse operator)."""
+    from inputs import config
+    from oracle import fe, mesh as omesh, solve
+    prob = config("c5", nx=sample_dims[0], ny=sample_dims[1], nz=sample_dims[2])
+    om = omesh.build_mesh(prob, with_filter=False)
+    x = om.density
+    K = fe.assemble_K(om, x, prob.penal, prob.E0, prob.Emin, prob.nu)
+    A, b, C = fe.projected_system(om, K)
+    its = 5
+    t0 = time.perf_counter()
+    solve.pcg_jacobi(A, b, fixed_iters=its)
+    dt = time.perf_counter() - t0
+    its = max(5, int(budget_s / max(dt / its, 1e-6)))
+    t0 = time.perf_counter()
+    solve.pcg_jacobi(A, b, fixed_iters=its)
+    dt = time.perf_counter() - t0
+    full = config("c5")
+    n_dof_full = 3 * (full.base[0] + 1) * (full.base[1] + 1) * (full.base[2] + 1)
+    it_s_sample = its / dt
+    return {
+        "value": it_s_sample * om.n_dof / n_dof_full,
+        "unit": "iterations/s",
+        "cores": 1,
+        "kind": "oracle",
+        "sample": (f"oracle Jacobi-PCG ({its} iterations, {dt:.1f} s) on a c5-recipe "
+                   f"{sample_dims[0]}x{sample_dims[1]}x{sample_dims[2]} sub-box ({om.n_dof} DOFs); "
+                   f"{it_s_sample:.2f} it/s there, scaled by DOF count to c5"),
+    }
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    steps, warm = args.steps, args.warmup
+    cb = None
+    times = []
+    for i in range(warm + steps):
+        t0 = time.perf_counter()
+        cb = _cpu_baseline(budget_s=args.ref_budget)
+        if i >= warm:
+            times.append(time.perf_counter() - t0)
+    val = cb["value"]
+    line = {
+        "impl": "reference", "metric": "pcg_iterations_per_sec", "value": val, "unit": "iterations/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": 1000.0 * float(np.mean(times)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "c5_uniform3d_256x128x128", "iters_per_solve": 500},
+        "cpu_baseline": cb,
+        "e2e": {"value": val, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import paper_1009_4975_b200 as pb
+    from inputs import config, density_at
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    prob = config(args.config) if args.config != "c5" else config("c5")
+    iters = prob.fixed_iters or 500
+    t_prep = time.perf_counter()
+    hm = pb.prepare(prob)
+    t_prep = time.perf_counter() - t_prep
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        m = pb.Mesh(hm, E0=prob.E0, Emin=prob.Emin, nu=prob.nu, rmin=prob.rmin, device=local, stream=stream)
+        x_host = torch.from_numpy(density_at(prob, hm.elem_level, hm.elem_anchor)).pin_memory()
+        x = x_host.to(dev, non_blocking=True)
+        if prob.presmooth_rmin is not None:
+            xs = torch.empty_like(x)
+            m.to_filter(pb.TO_FILTER_DENS, x, x, xs, stream=stream)
+            x = xs
+        u = torch.zeros(hm.n_dof, dtype=torch.float64, device=dev)
+        dc = torch.empty(hm.n_el, dtype=torch.float64, device=dev)
+        dcf = torch.empty_like(dc)
+    flags = pb.TO_FIXED_ITERS | pb.TO_NO_TRUE_RES
+
+    def step(profile=False):
+        st = m.tosolve_cg(prob.penal, x, u, rtol=0.0, max_iter=iters,
+                          flags=flags | (pb.TO_PROFILE if profile else 0), stream=stream)
+        m.to_sensitivity(prob.penal, x, u, dc, stream=stream)
+        m.to_filter(pb.TO_FILTER_SENS, x, dc, dcf, stream=stream)
+        return st
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # ---- device-timed region (inputs resident in HBM) -------------------------------
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    launches = 0
+    prof = {"apply_ms": 0.0, "alpha_ms": 0.0, "u1_ms": 0.0, "u2_ms": 0.0, "iters": 0}
+    for _ in range(args.steps):
+        st = step(profile=True)
+        launches += m.info()["kernel_launches"] + 2
+        p = m.profile()
+        for k in prof:
+            prof[k] += p[k]
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    ms_per_step = ms / args.steps
+    value = ws * iters * args.steps / (ms / 1000.0)
+
+    # ---- end-to-end through the C ABI with host buffers -------------------------------
+    dcf_host = torch.empty(hm.n_el, dtype=torch.float64).pin_memory()
+    raw_host = torch.from_numpy(density_at(prob, hm.elem_level, hm.elem_anchor)).pin_memory()
+    xr = torch.empty(hm.n_el, dtype=torch.float64, device=dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    t_wall = time.perf_counter()
+    e2.record(stream)
+    comp = 0.0
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            xr.copy_(raw_host, non_blocking=True)
+        xin = xr
+        if prob.presmooth_rmin is not None:
+            m.to_filter(pb.TO_FILTER_DENS, xr, xr, x, stream=stream)
+            xin = x
+        m.tosolve_cg(prob.penal, xin, u, rtol=0.0, max_iter=iters, flags=flags, stream=stream)
+        comp = m.to_sensitivity(prob.penal, xin, u, dc, compliance=True, stream=stream)
+        m.to_filter(pb.TO_FILTER_SENS, xin, dc, dcf, stream=stream)
+        with torch.cuda.stream(stream):
+            dcf_host.copy_(dcf, non_blocking=True)
+    e3.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = e2.elapsed_time(e3)
+    e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_t.item())
+
+    # ---- roofline of the dominant kernel (the operator apply) -------------------------
+    hbm, peak_kind = _peaks()
+    nc = 1 << hm.dim
+    bytes_per_apply = hm.n_el * (8 + 4 * nc) + hm.n_dof * 16     # s_e, conn, p read, q write
+    apply_ms = prof["apply_ms"] / max(1, prof["iters"])
+    achieved = bytes_per_apply / (apply_ms / 1000.0) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.config, {}).get("apply_dram_bytes")
+        except Exception:
+            traffic = None
+    total_prof = prof["apply_ms"] + prof["alpha_ms"] + prof["u1_ms"] + prof["u2_ms"]
+    info = m.info()
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = _cpu_baseline(budget_s=args.ref_budget)
+
+    if rank == 0:
+        line = {
+            "metric": "pcg_iterations_per_sec", "value": value, "unit": "iterations/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": prob.name, "n_elem": hm.n_el, "n_dof": hm.n_dof,
+                       "iters_per_solve": iters, "step": "simp+diag+rhs+500 PCG its+recover+sens+filter",
+                       "l2": "inputs larger than L2 (CG working set ~1.3 GB vs 126 MB L2)",
+                       "parallelism": f"replicas{ws}"},
+            "dof_matvecs_per_sec": value * hm.n_dof,
+            "e2e": {"value": ws * iters * args.steps / (e2e_ms / 1000.0), "unit": "iterations/s",
+                    "h2d_bytes_per_step": hm.n_el * 8, "d2h_bytes_per_step": hm.n_el * 8 + 8},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "kernel": "operator apply q = A p (+ p.q)",
+                         "algorithmic_bytes_per_launch": bytes_per_apply,
+                         "avg_launch_ms": apply_ms, "peak_source": peak_kind,
+                         "share_of_iteration": prof["apply_ms"] / total_prof if total_prof else None},
+            "kernel_ms_per_iter": {k: prof[k] / max(1, prof["iters"]) for k in ("apply_ms", "alpha_ms", "u1_ms", "u2_ms")},
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "gpu_launches": launches,
+            "host_prepare_s": t_prep,
+            "matvec_variant": info["matvec_variant"],
+            "compliance": comp,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--ref-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,204 @@
+/*
+ * tomesh.h — C ABI of the B200 (sm_100a) hot path of
+ *   Wang, de Sturler & Paulino, "Dynamic Adaptive Mesh Refinement for
+ *   Topology Optimization", arXiv:1009.4975 (reference text: PAPER.md).
+ *
+ * What the calls compute (citations are PAPER.md line : section / equation):
+ *
+ *   tomesh_upload   the FE mesh of the current adaptive quadtree/octree
+ *                   (:564-571 §6; hanging-node interpolation P of Eq. 6,
+ *                   :653-663), Dirichlet region Omega_0 (Eq. 1, :300-301),
+ *                   loads f (Eq. 1) and the filter neighbourhoods (Eq. 4,
+ *                   :600-609), copied to the device.
+ *   tosolve_cg      u solving K(x) u = f (Eq. 1, :296-304) with the SIMP
+ *                   modulus E_min + x^p (E0 - E_min) (Eq. 2, :322-324), via
+ *                   the projected system with unit diagonal on constrained
+ *                   DOFs (Eq. 8, :678-682), Dirichlet DOFs eliminated
+ *                   symmetrically, solved by CG on the diagonally rescaled
+ *                   system D^-1/2 A D^-1/2 (:511-523) = Jacobi-PCG, then the
+ *                   recovery u = [I 0; P 0] u_hat (Eq. 9, :683-686).
+ *   to_sensitivity  dc_e = -p x_e^(p-1) (E0 - E_min) u_e^T K0(h_e) u_e
+ *                   (sensitivity analysis, :343-346; formula per north_star,
+ *                   DESIGN.md reading R2) and optionally c = f^T u (Eq. 1).
+ *   to_filter       Eq. 5 (:613-616), Stainko's volume-weighted Sigmund
+ *                   filter, with H_de of Eq. 4; or its density variant
+ *                   (reading R10).
+ *   to_apply_A / to_jacobi_diag / to_project_rhs / to_recover
+ *                   the individual operators of Eqs. 7-9, exposed for
+ *                   operator-level parity checks.
+ *
+ * Conventions shared by every call
+ *   - dim = 2 (Q4 plane stress, unit thickness) or 3 (H8).  Local corner of
+ *     an element c = cx + 2 cy + 4 cz, local DOF = dim*c + component; global
+ *     DOF = dim*node + component.  Vectors over DOFs have
+ *     length dim*n_node and keep hanging and fixed DOFs.
+ *   - All floating point is IEEE fp64.
+ *   - Device pointers are raw CUDA device addresses on the handle's device
+ *     (e.g. torch.Tensor.data_ptr() of a contiguous float64 CUDA tensor).
+ *     They stay owned by the caller; the library never frees or retains them.
+ *   - cuda_stream is a cudaStream_t (NULL = legacy default stream).  Calls
+ *     that fill host outputs synchronise that stream before returning; the
+ *     others are asynchronous with respect to the host.
+ *   - Errors: every call returns a status (0 = OK, >0 = result usable with a
+ *     warning, <0 = failure).  No exception or abort crosses the ABI.  The
+ *     thread-local message of the last failure is to_last_error().
+ *   - A handle is not thread-safe; distinct handles are independent.
+ */
+#ifndef TOMESH_H
+#define TOMESH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct to_mesh to_mesh;
+
+enum {
+  TO_OK = 0,
+  TO_NOT_CONVERGED = 1,   /* max_iter reached above rtol; stats and u filled   */
+  TO_EINVAL = -1,         /* bad argument (NULL pointer, bad size, x <= 0 ...) */
+  TO_ECUDA = -2,          /* CUDA runtime error                                */
+  TO_ENOMEM = -3,         /* device allocation failed                          */
+  TO_EMESH = -4,          /* inconsistent mesh arrays (see to_last_error)      */
+  TO_ENAN = -5,           /* NaN/Inf appeared in the CG recurrences            */
+  TO_EBREAKDOWN = -6,     /* p^T A p <= 0                                      */
+  TO_ENONPOS_DIAG = -7    /* a free DOF has a non-positive diagonal            */
+};
+
+/* tosolve_cg flags */
+enum {
+  TO_WARM = 1,            /* u_dev holds the initial guess  */
+  TO_FIXED_ITERS = 2,     /* run exactly max_iter iterations, ignore rtol      */
+  TO_HISTORY = 4,         /* record ||r_k||/||b|| into the handle's history    */
+  TO_NO_TRUE_RES = 8,     /* skip the extra matvec for relres_true             */
+  TO_PROFILE = 16         /* time every iteration kernel with CUDA events      */
+};
+
+/* to_filter modes */
+enum { TO_FILTER_SENS = 0, TO_FILTER_DENS = 1 };
+
+/* Mesh description (host memory; copied by tomesh_upload).
+ * Lattice: finest level L = max_level, lattice unit h_L = h0 / 2^L; a leaf
+ * with level l has edge s = 2^(L-l) lattice units, anchor = its minimum
+ * corner in lattice units.  Arrays must follow the canonical contract of
+ * SURVEY.md §8(b) C1-C9 (Morton element and node order, ascending hanging and
+ * fixed lists, ascending parents per hanging node). */
+typedef struct {
+  int32_t dim;                 /* 2 or 3                                         */
+  int32_t max_level;           /* L >= 0                                         */
+  double  h0;                  /* level-0 cell edge (physical length)            */
+  int64_t n_elem, n_node;
+  const int32_t *elem_node;    /* [n_elem][2^dim] node ids, C4 corner order      */
+  const int32_t *elem_anchor;  /* [n_elem][dim]  lattice anchors                 */
+  const int8_t  *elem_level;   /* [n_elem]                                       */
+  int64_t n_hang;              /* hanging nodes (Eq. 6 "constrained DOFs")       */
+  const int32_t *hang_node;    /* [n_hang] ascending node ids                    */
+  const int32_t *hang_ptr;     /* [n_hang+1]                                     */
+  const int32_t *hang_parent;  /* [hang_ptr[n_hang]] ascending within a row      */
+  const double  *hang_weight;  /* [hang_ptr[n_hang]] rows sum to 1 (1/2 or 1/4)  */
+  int64_t n_fixed;
+  const int64_t *fixed_dof;    /* [n_fixed] ascending DOF ids, no hanging DOF;
+                                  prescribed value u0 = 0                        */
+  const double  *load;         /* [dim*n_node] consistent nodal loads f, before
+                                  the projection C^T (hanging loads allowed)     */
+  double E0, Emin, nu;         /* SIMP E_min + x^p (E0 - E_min); Poisson ratio   */
+  double rmin;                 /* filter radius (physical); 0 = no filter        */
+  int64_t filt_nnz;
+  const int64_t *filt_ptr;     /* [n_elem+1] or NULL when rmin == 0              */
+  const int32_t *filt_idx;     /* [filt_nnz] neighbours with |c_d-c_e| < rmin,
+                                  ascending, self included (C9)                  */
+} to_mesh_desc;
+
+typedef struct {
+  int32_t iters;               /* CG iterations performed                        */
+  int32_t status;              /* same code as the return value                  */
+  double  relres;              /* recurrence ||r_k||_2 / ||b||_2                 */
+  double  relres_true;         /* ||b - A x||_2 / ||b||_2 at exit (-1 if skipped)*/
+  double  ms;                  /* device time of the whole call (CUDA events)    */
+  double  bnorm;               /* ||b||_2                                        */
+} to_cg_stats;
+
+typedef struct {
+  int32_t dim, structured;     /* structured = 1: uniform-grid fast path chosen  */
+  int64_t n_elem, n_node, n_dof, n_hang, n_fixed, filt_nnz;
+  int64_t grid[3];             /* element grid when structured                   */
+  int64_t device_bytes;        /* device memory held by the handle               */
+  int32_t kernel_launches;     /* kernels launched by the last tosolve_cg        */
+  int32_t matvec_variant;      /* id of the operator kernel in use               */
+} to_mesh_info;
+
+/* Validate, copy to `device`, derive device encodings, allocate the CG
+ * workspace.  Rejects with TO_EMESH: out-of-range indices, a constraint
+ * parent that is itself hanging, a hanging DOF listed as fixed, hanging
+ * weights not summing to 1, unsorted lists.  On success *out owns all device
+ * memory until tomesh_free. */
+int  tomesh_upload(const to_mesh_desc *desc, int device, void *cuda_stream, to_mesh **out);
+void tomesh_free(to_mesh *m);
+int  tomesh_get_info(const to_mesh *m, to_mesh_info *info);
+
+/* Solve A u_hat = b (Eq. 8 + Dirichlet rows) by Jacobi-PCG and write
+ * u = C u_hat (Eq. 9) to u_dev[dim*n_node] (fixed DOFs = 0).
+ *   penal      SIMP exponent p (> 0; continuation is the caller's business)
+ *   x_dev      [n_elem] densities in (0, 1]
+ *   u_dev      [dim*n_node] output; input guess when flags & TO_WARM
+ *   rtol       stop when ||r_k||/||b|| <= rtol (ignored with TO_FIXED_ITERS)
+ *   max_iter   iteration cap (exact count with TO_FIXED_ITERS)
+ *   st         nullable host stats
+ * Synchronises cuda_stream.  Returns TO_NOT_CONVERGED (> 0) if the cap was
+ * reached, TO_EBREAKDOWN / TO_ENAN / TO_ENONPOS_DIAG on numerical failure. */
+int  tosolve_cg(to_mesh *m, double penal, const double *x_dev, double *u_dev,
+                double rtol, int32_t max_iter, uint32_t flags, to_cg_stats *st,
+                void *cuda_stream);
+
+/* Residual history of the last TO_HISTORY solve: copies min(n, iters)
+ * values of ||r_k||/||b|| (k = 1..iters) to host `out`; returns the count. */
+int  tosolve_history(const to_mesh *m, double *out, int32_t n);
+
+/* Per-kernel device time of the last TO_PROFILE solve, in ms, summed over
+ * its iterations: out[0] operator apply (q = A p, with p.q), out[1] the
+ * alpha reduction (0 when fused into the apply), out[2] r update + (r.z,
+ * r.r), out[3] x/p update, out[4] number of iterations profiled.  n >= 5. */
+int  tosolve_profile(const to_mesh *m, double *out, int32_t n);
+
+/* dc_dev[n_elem] = -p x^(p-1) (E0-Emin) u_e^T K0(h_e) u_e with u_e the element
+ * gather of u_dev (already recovered, hanging values included).  If
+ * compliance_host != NULL also computes f^T u and synchronises. */
+int  to_sensitivity(to_mesh *m, double penal, const double *x_dev, const double *u_dev,
+                    double *dc_dev, double *compliance_host, void *cuda_stream);
+
+/* TO_FILTER_SENS: out_e = sum_d x_d H_de V_d in_d / (x_e sum_d H_de V_d)  (Eq. 5)
+ * TO_FILTER_DENS: out_e = sum_d H_de V_d in_d / sum_d H_de V_d
+ * H_de = rmin - |c_d - c_e| over the uploaded neighbour lists (Eq. 4).
+ * out_dev must not alias in_dev or x_dev.  Asynchronous. */
+int  to_filter(to_mesh *m, int32_t mode, const double *x_dev, const double *in_dev,
+               double *out_dev, void *cuda_stream);
+
+/* Operator-level entry points (parity and diagnostics; asynchronous).
+ * to_apply_A:      q = A v,  A = Pi_F C^T K(x) C Pi_F + (I - Pi_F)  (Eq. 8)
+ * to_jacobi_diag:  d = diag(A)  (1 on hanging and fixed DOFs)
+ * to_project_rhs:  b = Pi_F C^T f  (Eq. 7 right-hand side)
+ * to_recover:      u = C v  (Eq. 9); in place allowed (u_dev == v_dev) */
+int  to_apply_A(to_mesh *m, double penal, const double *x_dev, const double *v_dev,
+                double *q_dev, void *cuda_stream);
+int  to_jacobi_diag(to_mesh *m, double penal, const double *x_dev, double *d_dev,
+                    void *cuda_stream);
+int  to_project_rhs(to_mesh *m, double *b_dev, void *cuda_stream);
+int  to_recover(to_mesh *m, const double *v_dev, double *u_dev, void *cuda_stream);
+
+/* Host-only diagnostics (no GPU needed): the unit element matrix K0 the
+ * kernels use (E = 1, h = 1, closed form of csrc/element.cpp), dim*2^dim
+ * square, row-major, local DOF = dim*corner + component; and, for dim = 3,
+ * its Hadamard factorisation (diag[3][8], off[3][3][8], see csrc/element.h).
+ * Returns 0, or the number of entries violating the factorisation pattern. */
+int  to_element_matrix(int32_t dim, double nu, double *K_host);
+int  to_element_hadamard(double nu, double *diag_host, double *off_host);
+
+/* Thread-local message describing the last failure ("" if none). */
+const char *to_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOMESH_H */

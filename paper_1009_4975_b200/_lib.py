@@ -1,0 +1,122 @@
+"""ctypes declarations of libtomesh.so (include/tomesh.h, include/tomesh_host.h).
+
+Loading fails loudly: there is no CPU fallback anywhere in this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libtomesh.so")
+
+TO_OK, TO_NOT_CONVERGED = 0, 1
+TO_EINVAL, TO_ECUDA, TO_ENOMEM, TO_EMESH, TO_ENAN, TO_EBREAKDOWN, TO_ENONPOS_DIAG = -1, -2, -3, -4, -5, -6, -7
+TO_WARM, TO_FIXED_ITERS, TO_HISTORY, TO_NO_TRUE_RES, TO_PROFILE = 1, 2, 4, 8, 16
+TO_FILTER_SENS, TO_FILTER_DENS = 0, 1
+TOH_LOAD_POINT, TOH_LOAD_LINE, TOH_LOAD_FACE = 0, 1, 2
+
+STATUS_NAMES = {0: "TO_OK", 1: "TO_NOT_CONVERGED", -1: "TO_EINVAL", -2: "TO_ECUDA", -3: "TO_ENOMEM",
+                -4: "TO_EMESH", -5: "TO_ENAN", -6: "TO_EBREAKDOWN", -7: "TO_ENONPOS_DIAG"}
+
+P = C.c_void_p
+
+
+class ToMeshDesc(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int32), ("max_level", C.c_int32), ("h0", C.c_double),
+        ("n_elem", C.c_int64), ("n_node", C.c_int64),
+        ("elem_node", P), ("elem_anchor", P), ("elem_level", P),
+        ("n_hang", C.c_int64), ("hang_node", P), ("hang_ptr", P), ("hang_parent", P), ("hang_weight", P),
+        ("n_fixed", C.c_int64), ("fixed_dof", P),
+        ("load", P),
+        ("E0", C.c_double), ("Emin", C.c_double), ("nu", C.c_double),
+        ("rmin", C.c_double), ("filt_nnz", C.c_int64), ("filt_ptr", P), ("filt_idx", P),
+    ]
+
+
+class ToCgStats(C.Structure):
+    _fields_ = [("iters", C.c_int32), ("status", C.c_int32), ("relres", C.c_double),
+                ("relres_true", C.c_double), ("ms", C.c_double), ("bnorm", C.c_double)]
+
+
+class ToMeshInfo(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("structured", C.c_int32),
+                ("n_elem", C.c_int64), ("n_node", C.c_int64), ("n_dof", C.c_int64), ("n_hang", C.c_int64),
+                ("n_fixed", C.c_int64), ("filt_nnz", C.c_int64), ("grid", C.c_int64 * 3),
+                ("device_bytes", C.c_int64), ("kernel_launches", C.c_int32), ("matvec_variant", C.c_int32)]
+
+
+class HostSpec(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int32), ("max_level", C.c_int32), ("base", C.c_int32 * 3), ("h0", C.c_double),
+        ("n_leaf", C.c_int64), ("leaf_level", P), ("leaf_anchor", P),
+        ("n_fixed_box", C.c_int32), ("fixed_box", P), ("fixed_mask", P),
+        ("n_load", C.c_int32), ("load_kind", P), ("load_box", P), ("load_vec", P),
+        ("rmin", C.c_double),
+    ]
+
+
+class HostArrays(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int32), ("max_level", C.c_int32), ("h0", C.c_double),
+        ("n_elem", C.c_int64), ("n_node", C.c_int64), ("n_hang", C.c_int64), ("n_hang_nnz", C.c_int64),
+        ("n_fixed", C.c_int64), ("filt_nnz", C.c_int64),
+        ("elem_node", P), ("elem_anchor", P), ("elem_level", P), ("node_coord", P),
+        ("hang_node", P), ("hang_ptr", P), ("hang_parent", P), ("hang_weight", P),
+        ("fixed_dof", P), ("load", P), ("filt_ptr", P), ("filt_idx", P),
+    ]
+
+
+EXPORTS = {
+    # name: (restype, argtypes)
+    "tomesh_upload": (C.c_int, [C.POINTER(ToMeshDesc), C.c_int, P, C.POINTER(P)]),
+    "tomesh_free": (None, [P]),
+    "tomesh_get_info": (C.c_int, [P, C.POINTER(ToMeshInfo)]),
+    "tosolve_cg": (C.c_int, [P, C.c_double, P, P, C.c_double, C.c_int32, C.c_uint32, C.POINTER(ToCgStats), P]),
+    "tosolve_history": (C.c_int, [P, P, C.c_int32]),
+    "tosolve_profile": (C.c_int, [P, P, C.c_int32]),
+    "to_sensitivity": (C.c_int, [P, C.c_double, P, P, P, C.POINTER(C.c_double), P]),
+    "to_filter": (C.c_int, [P, C.c_int32, P, P, P, P]),
+    "to_apply_A": (C.c_int, [P, C.c_double, P, P, P, P]),
+    "to_jacobi_diag": (C.c_int, [P, C.c_double, P, P, P]),
+    "to_project_rhs": (C.c_int, [P, P, P]),
+    "to_recover": (C.c_int, [P, P, P, P]),
+    "to_element_matrix": (C.c_int, [C.c_int32, C.c_double, P]),
+    "to_element_hadamard": (C.c_int, [C.c_double, P, P]),
+    "to_last_error": (C.c_char_p, []),
+    "tomesh_host_build": (C.c_int, [C.POINTER(HostSpec), C.POINTER(P)]),
+    "tomesh_host_get": (C.c_int, [P, C.POINTER(HostArrays)]),
+    "tomesh_host_filter": (C.c_int, [P, C.c_double]),
+    "tomesh_host_free": (None, [P]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libtomesh.so not built ({LIB_PATH}); run __graft_entry__.build() "
+                              "or python -m paper_1009_4975_b200.build — there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in EXPORTS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+class TomeshError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        msg = lib().to_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {STATUS_NAMES.get(code, code)} ({code}): {msg}")
+        self.code = code
+
+
+def check(code: int, where: str, ok_positive: bool = True) -> int:
+    if code < 0 or (code > 0 and not ok_positive):
+        raise TomeshError(code, where)
+    return code

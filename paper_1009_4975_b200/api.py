@@ -1,0 +1,269 @@
+"""Thin Python binding of libtomesh (argument marshalling only).
+
+Every step of the hot path runs in the library's CUDA kernels (device
+calls) or its C++ host builder (mesh preparation).  torch is used for device
+memory and streams only.  Names follow include/tomesh.h.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib as L
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def _copy(ptr, dtype, count, shape=None):
+    if count == 0 or not ptr:
+        out = np.zeros(0 if shape is None else (0,) + tuple(shape[1:]), dtype=dtype)
+        return out
+    buf = (C.c_byte * (count * np.dtype(dtype).itemsize)).from_address(ptr)
+    out = np.frombuffer(buf, dtype=dtype, count=count).copy()
+    return out.reshape(shape) if shape is not None else out
+
+
+# ---------------------------------------------------------------------------
+# host mesh preparation (C++ host builder, include/tomesh_host.h)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class HostMesh:
+    dim: int
+    L: int
+    h0: float
+    elem_node: np.ndarray
+    elem_anchor: np.ndarray
+    elem_level: np.ndarray
+    node_coord: np.ndarray
+    hang_node: np.ndarray
+    hang_ptr: np.ndarray
+    hang_parent: np.ndarray
+    hang_weight: np.ndarray
+    fixed_dof: np.ndarray
+    load: np.ndarray
+    filt_ptr: Optional[np.ndarray]
+    filt_idx: Optional[np.ndarray]
+    rmin: float
+
+    @property
+    def n_el(self):
+        return int(self.elem_level.shape[0])
+
+    @property
+    def n_node(self):
+        return int(self.node_coord.shape[0])
+
+    @property
+    def n_dof(self):
+        return self.dim * self.n_node
+
+    @property
+    def hL(self):
+        return self.h0 / (1 << self.L)
+
+
+_KIND = {"point": L.TOH_LOAD_POINT, "line": L.TOH_LOAD_LINE, "face": L.TOH_LOAD_FACE}
+
+
+def tomesh_host_build(dim, max_level, base, h0, leaf_level, leaf_anchor, fixed, loads, rmin) -> HostMesh:
+    """fixed: [(lo, hi, mask)], loads: [(kind, lo, hi, vec)] (lattice boxes, inclusive)."""
+    lib = L.lib()
+    leaf_level = np.ascontiguousarray(leaf_level, dtype=np.int8)
+    leaf_anchor = np.ascontiguousarray(leaf_anchor, dtype=np.int32).reshape(-1, dim)
+    fb = np.ascontiguousarray([list(lo) + list(hi) for lo, hi, _ in fixed] or [[0] * 2 * dim], dtype=np.int32)
+    fm = np.ascontiguousarray([m for _, _, m in fixed] or [0], dtype=np.int32)
+    lk = np.ascontiguousarray([_KIND[k] for k, _, _, _ in loads] or [0], dtype=np.int32)
+    lb = np.ascontiguousarray([list(lo) + list(hi) for _, lo, hi, _ in loads] or [[0] * 2 * dim], dtype=np.int32)
+    lv = np.ascontiguousarray([list(v) for _, _, _, v in loads] or [[0.0] * dim], dtype=np.float64)
+    spec = L.HostSpec()
+    spec.dim = dim
+    spec.max_level = max_level
+    for c in range(3):
+        spec.base[c] = int(base[c]) if c < dim else 1
+    spec.h0 = h0
+    spec.n_leaf = leaf_level.shape[0]
+    spec.leaf_level = _ptr(leaf_level)
+    spec.leaf_anchor = _ptr(leaf_anchor)
+    spec.n_fixed_box = len(fixed)
+    spec.fixed_box = _ptr(fb)
+    spec.fixed_mask = _ptr(fm)
+    spec.n_load = len(loads)
+    spec.load_kind = _ptr(lk)
+    spec.load_box = _ptr(lb)
+    spec.load_vec = _ptr(lv)
+    spec.rmin = float(rmin)
+    h = C.c_void_p()
+    L.check(lib.tomesh_host_build(C.byref(spec), C.byref(h)), "tomesh_host_build")
+    try:
+        a = L.HostArrays()
+        L.check(lib.tomesh_host_get(h, C.byref(a)), "tomesh_host_get")
+        nc = 1 << dim
+        ne, nn = a.n_elem, a.n_node
+        return HostMesh(
+            dim=dim, L=max_level, h0=h0,
+            elem_node=_copy(a.elem_node, np.int32, ne * nc, (ne, nc)),
+            elem_anchor=_copy(a.elem_anchor, np.int32, ne * dim, (ne, dim)),
+            elem_level=_copy(a.elem_level, np.int8, ne),
+            node_coord=_copy(a.node_coord, np.int32, nn * dim, (nn, dim)),
+            hang_node=_copy(a.hang_node, np.int32, a.n_hang),
+            hang_ptr=_copy(a.hang_ptr, np.int32, a.n_hang + 1),
+            hang_parent=_copy(a.hang_parent, np.int32, a.n_hang_nnz),
+            hang_weight=_copy(a.hang_weight, np.float64, a.n_hang_nnz),
+            fixed_dof=_copy(a.fixed_dof, np.int64, a.n_fixed),
+            load=_copy(a.load, np.float64, nn * dim),
+            filt_ptr=_copy(a.filt_ptr, np.int64, ne + 1) if a.filt_ptr else None,
+            filt_idx=_copy(a.filt_idx, np.int32, a.filt_nnz) if a.filt_ptr else None,
+            rmin=float(rmin),
+        )
+    finally:
+        lib.tomesh_host_free(h)
+
+
+def prepare(problem) -> HostMesh:
+    """Host mesh for an ``inputs.Problem`` (its pre-balance leaves and predicates)."""
+    p = problem
+    return tomesh_host_build(p.dim, p.L, p.base, p.h0, p.leaf_level, p.leaf_anchor, p.fixed, p.loads, p.rmin)
+
+
+# ---------------------------------------------------------------------------
+# device handle (include/tomesh.h)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class CgStats:
+    iters: int
+    status: int
+    relres: float
+    relres_true: float
+    ms: float
+    bnorm: float
+
+
+def _dptr(t):
+    import torch
+    if t is None:
+        return None
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise ValueError("expected a contiguous float64 CUDA tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+class Mesh:
+    """Device copy of a mesh + CG workspace (tomesh_upload / tomesh_free)."""
+
+    def __init__(self, host: HostMesh, E0=1.0, Emin=1e-9, nu=0.3, rmin=None, device=0, stream=None):
+        import torch
+        self.host = host
+        self.device = torch.device("cuda", device)
+        self.dim = host.dim
+        self.n_el, self.n_node, self.n_dof = host.n_el, host.n_node, host.n_dof
+        self.E0, self.Emin, self.nu = E0, Emin, nu
+        rmin = host.rmin if rmin is None else rmin
+        keep = []
+
+        def arr(a, dt):
+            a = np.ascontiguousarray(a, dtype=dt)
+            keep.append(a)
+            return _ptr(a)
+
+        d = L.ToMeshDesc()
+        d.dim = host.dim
+        d.max_level = host.L
+        d.h0 = host.h0
+        d.n_elem = host.n_el
+        d.n_node = host.n_node
+        d.elem_node = arr(host.elem_node, np.int32)
+        d.elem_anchor = arr(host.elem_anchor, np.int32)
+        d.elem_level = arr(host.elem_level, np.int8)
+        d.n_hang = host.hang_node.shape[0]
+        d.hang_node = arr(host.hang_node, np.int32)
+        d.hang_ptr = arr(host.hang_ptr, np.int32)
+        d.hang_parent = arr(host.hang_parent, np.int32)
+        d.hang_weight = arr(host.hang_weight, np.float64)
+        d.n_fixed = host.fixed_dof.shape[0]
+        d.fixed_dof = arr(host.fixed_dof, np.int64)
+        d.load = arr(host.load, np.float64)
+        d.E0, d.Emin, d.nu = E0, Emin, nu
+        d.rmin = rmin if host.filt_ptr is not None else 0.0
+        if host.filt_ptr is not None and rmin > 0:
+            d.filt_nnz = host.filt_idx.shape[0]
+            d.filt_ptr = arr(host.filt_ptr, np.int64)
+            d.filt_idx = arr(host.filt_idx, np.int32)
+        self._h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            L.check(L.lib().tomesh_upload(C.byref(d), device, _stream(stream), C.byref(self._h)), "tomesh_upload")
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            L.lib().tomesh_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        i = L.ToMeshInfo()
+        L.check(L.lib().tomesh_get_info(self._h, C.byref(i)), "tomesh_get_info")
+        return {f: (list(getattr(i, f)) if f == "grid" else getattr(i, f)) for f, _ in L.ToMeshInfo._fields_}
+
+    # -- the four calls of the boundary --------------------------------------------------
+    def tosolve_cg(self, penal, x, u, rtol=1e-10, max_iter=20000, flags=0, stream=None) -> CgStats:
+        st = L.ToCgStats()
+        rc = L.lib().tosolve_cg(self._h, float(penal), _dptr(x), _dptr(u), float(rtol), int(max_iter),
+                                int(flags), C.byref(st), _stream(stream))
+        L.check(rc, "tosolve_cg")
+        return CgStats(st.iters, st.status, st.relres, st.relres_true, st.ms, st.bnorm)
+
+    def history(self, n):
+        out = np.zeros(max(1, n))
+        k = L.lib().tosolve_history(self._h, _ptr(out), int(n))
+        L.check(k, "tosolve_history")
+        return out[:k]
+
+    def profile(self):
+        out = np.zeros(5)
+        L.check(L.lib().tosolve_profile(self._h, _ptr(out), 5), "tosolve_profile")
+        return {"apply_ms": out[0], "alpha_ms": out[1], "u1_ms": out[2], "u2_ms": out[3], "iters": int(out[4])}
+
+    def to_sensitivity(self, penal, x, u, dc, compliance=False, stream=None):
+        c = C.c_double(0.0)
+        L.check(L.lib().to_sensitivity(self._h, float(penal), _dptr(x), _dptr(u), _dptr(dc),
+                                       C.byref(c) if compliance else None, _stream(stream)), "to_sensitivity")
+        return c.value if compliance else None
+
+    def to_filter(self, mode, x, inp, out, stream=None):
+        L.check(L.lib().to_filter(self._h, int(mode), _dptr(x), _dptr(inp), _dptr(out), _stream(stream)),
+                "to_filter")
+        return out
+
+    # -- operator-level calls -------------------------------------------------------------
+    def to_apply_A(self, penal, x, v, q, stream=None):
+        L.check(L.lib().to_apply_A(self._h, float(penal), _dptr(x), _dptr(v), _dptr(q), _stream(stream)), "to_apply_A")
+        return q
+
+    def to_jacobi_diag(self, penal, x, d, stream=None):
+        L.check(L.lib().to_jacobi_diag(self._h, float(penal), _dptr(x), _dptr(d), _stream(stream)), "to_jacobi_diag")
+        return d
+
+    def to_project_rhs(self, b, stream=None):
+        L.check(L.lib().to_project_rhs(self._h, _dptr(b), _stream(stream)), "to_project_rhs")
+        return b
+
+    def to_recover(self, v, u, stream=None):
+        L.check(L.lib().to_recover(self._h, _dptr(v), _dptr(u), _stream(stream)), "to_recover")
+        return u

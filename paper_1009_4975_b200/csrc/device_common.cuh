@@ -1,0 +1,100 @@
+// Device-side helpers: reductions, scalar block of the CG loop.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tomesh {
+
+constexpr int kNumSMs = 148;          // B200
+constexpr int kBlock = 256;
+
+// Device-resident state of one Jacobi-PCG solve.  Every scalar of the
+// recurrences lives here so that no iteration needs the host.
+struct CgScalars {
+  double rho;        // r_k . z_k
+  double alpha;      // rho / (p . A p)
+  double beta;       // rho_{k+1} / rho_k
+  double rr;         // ||r_k||^2
+  double bnorm2;     // ||b||^2
+  double thresh2;    // rtol^2 ||b||^2
+  double tmp[4];     // scratch reductions (true residual, compliance, ...)
+  int32_t iter;      // completed iterations
+  int32_t max_iter;
+  int32_t fixed;     // 1: ignore rtol
+  int32_t done;      // 1: stop now (set on breakdown / before the first iteration)
+  int32_t done_next; // 1: stop after the x/p update of the current iteration
+  int32_t status;    // TO_OK or a negative code
+  int32_t history;   // record ||r||/||b|| per iteration
+  int32_t pad;
+  uint32_t counter[8];   // last-block-done counters, one per reduction site
+};
+
+enum { CNT_PQ = 0, CNT_U1 = 1, CNT_INIT = 2, CNT_MISC = 3, CNT_MISC2 = 4 };
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum of NV values; the result is valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV]) {
+  __shared__ double sh[NV][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) sh[k][wid] = v[k];
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double t = lane < nw ? sh[k][lane] : 0.0;
+      v[k] = warp_sum(t);
+    }
+  }
+}
+
+// Grid-wide deterministic sum: every block deposits its partial, the last
+// block to arrive adds the partials in a fixed order.  Returns true in
+// thread 0 of the last block, with the totals in `v`.
+template <int NV>
+__device__ __forceinline__ bool grid_sum(double (&v)[NV], double *partials, uint32_t *counter) {
+  __shared__ bool s_last;
+  block_sum<NV>(v);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) partials[(size_t)blockIdx.x * NV + k] = v[k];
+    __threadfence();
+    uint32_t t = atomicAdd(counter, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  double acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] += __ldcg(&partials[(size_t)b * NV + k]);
+  }
+  block_sum<NV>(acc);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = acc[k];
+    *counter = 0u;
+  }
+  return threadIdx.x == 0;
+}
+
+__device__ __forceinline__ bool cg_stopped(const CgScalars *S) {
+  return *((volatile const int32_t *)&S->done) | *((volatile const int32_t *)&S->done_next);
+}
+
+}  // namespace tomesh

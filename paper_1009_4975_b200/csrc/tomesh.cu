@@ -1,0 +1,628 @@
+// libtomesh — C ABI entry points (include/tomesh.h) and the host side of the
+// device path: validation, upload, the PCG driver loop, sensitivities, filter.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "../../include/tomesh.h"
+#include "common.h"
+#include "device_common.cuh"
+#include "element.h"
+#include "kernels_cg.cuh"
+#include "kernels_general.cuh"
+
+using namespace tomesh;
+
+namespace {
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct to_mesh {
+  int dim = 0, L = 0, device = 0;
+  double h0 = 1.0, hL = 1.0, E0 = 1.0, Emin = 1e-9, nu = 0.3, rmin = 0.0;
+  int64_t n_el = 0, n_node = 0, n_dof = 0, n_hang = 0, n_fixed = 0, filt_nnz = 0;
+  std::vector<DevBuf> bufs;
+  int64_t dev_bytes = 0;
+  // mesh
+  int32_t *elem_node = nullptr, *elem_anchor = nullptr, *node_hang = nullptr;
+  int8_t *elem_level = nullptr;
+  int32_t *hang_ptr = nullptr, *hang_parent = nullptr, *child_ptr = nullptr, *child_hang = nullptr;
+  double *hang_weight = nullptr, *child_weight = nullptr, *load = nullptr;
+  uint8_t *free_dof = nullptr;
+  int64_t *filt_ptr = nullptr;
+  int32_t *filt_idx = nullptr;
+  // workspace
+  double *s = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *dinv = nullptr, *D = nullptr;
+  double *partials = nullptr, *hist = nullptr;
+  int32_t hist_len = 0, hist_cap = 0;
+  CgScalars *S = nullptr;
+  CgScalars *S_host = nullptr;   // pinned mirror
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  K0Dense2 K2{};
+  K0Dense3 K3{};
+  int last_launches = 0;
+  int matvec_variant = 0;
+  std::vector<cudaEvent_t> prof_ev;   // TO_PROFILE: 5 events per iteration
+  double prof_ms[5] = {0, 0, 0, 0, 0};
+
+  MeshView view() const {
+    MeshView M;
+    M.n_el = n_el;
+    M.n_node = n_node;
+    M.elem_node = elem_node;
+    M.elem_level = elem_level;
+    M.elem_anchor = elem_anchor;
+    M.node_hang = node_hang;
+    M.hang_ptr = hang_ptr;
+    M.hang_parent = hang_parent;
+    M.hang_weight = hang_weight;
+    M.child_ptr = child_ptr;
+    M.child_hang = child_hang;
+    M.child_weight = child_weight;
+    M.free_dof = free_dof;
+    M.L = L;
+    M.hL = hL;
+    return M;
+  }
+
+  template <typename T>
+  int alloc(T **ptr, size_t count) {
+    *ptr = nullptr;
+    if (count == 0) count = 1;
+    void *d = nullptr;
+    if (cudaMalloc(&d, count * sizeof(T)) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("cudaMalloc of %zu bytes failed", count * sizeof(T));
+      return TO_ENOMEM;
+    }
+    bufs.push_back({d, count * sizeof(T)});
+    dev_bytes += (int64_t)(count * sizeof(T));
+    *ptr = (T *)d;
+    return 0;
+  }
+  ~to_mesh() {
+    for (auto &b : bufs) cudaFree(b.p);
+    if (S_host) cudaFreeHost(S_host);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    for (auto e : prof_ev) cudaEventDestroy(e);
+  }
+};
+
+namespace {
+
+#define CK(call)                                                                 \
+  do {                                                                           \
+    cudaError_t _e = (call);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      set_error("%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, __LINE__); \
+      return TO_ECUDA;                                                           \
+    }                                                                            \
+  } while (0)
+
+#define RC(call)                 \
+  do {                           \
+    int _rc = (call);            \
+    if (_rc != 0) return _rc;    \
+  } while (0)
+
+inline int grid_for(int64_t n, int per_block = kBlock, int max_waves = 8) {
+  int64_t g = (n + per_block - 1) / per_block;
+  g = std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)kNumSMs * max_waves));
+  return (int)g;
+}
+
+constexpr int kMaxPartialBlocks = kNumSMs * 8;
+
+int check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("kernel launch failed: %s", cudaGetErrorString(e));
+    return TO_ECUDA;
+  }
+  return 0;
+}
+
+int validate(const to_mesh_desc *d) {
+  if (d->dim != 2 && d->dim != 3) { set_error("dim must be 2 or 3"); return TO_EINVAL; }
+  if (d->n_elem <= 0 || d->n_node <= 0) { set_error("empty mesh"); return TO_EINVAL; }
+  if (d->max_level < 0 || d->max_level > 20) { set_error("max_level out of range"); return TO_EINVAL; }
+  if (!d->elem_node || !d->elem_anchor || !d->elem_level || !d->load) { set_error("NULL mesh array"); return TO_EINVAL; }
+  if (d->n_node * d->dim >= (1LL << 31)) { set_error("too many DOFs for int32 node ids"); return TO_EINVAL; }
+  if (!(d->h0 > 0.0) || !(d->E0 > 0.0) || !(d->Emin >= 0.0) || !(d->nu > -1.0 && d->nu < 0.5)) {
+    set_error("bad material or geometry constants");
+    return TO_EINVAL;
+  }
+  const int nc = 1 << d->dim;
+  for (int64_t i = 0; i < d->n_elem * nc; ++i)
+    if (d->elem_node[i] < 0 || d->elem_node[i] >= d->n_node) {
+      set_error("elem_node[%lld] = %d out of range", (long long)i, d->elem_node[i]);
+      return TO_EMESH;
+    }
+  for (int64_t e = 0; e < d->n_elem; ++e)
+    if (d->elem_level[e] < 0 || d->elem_level[e] > d->max_level) { set_error("elem_level out of range"); return TO_EMESH; }
+  if (d->n_hang < 0 || (d->n_hang > 0 && (!d->hang_node || !d->hang_ptr || !d->hang_parent || !d->hang_weight))) {
+    set_error("bad hanging arrays");
+    return TO_EINVAL;
+  }
+  std::vector<char> hang(d->n_node, 0);
+  for (int64_t h = 0; h < d->n_hang; ++h) {
+    int32_t n = d->hang_node[h];
+    if (n < 0 || n >= d->n_node || (h > 0 && n <= d->hang_node[h - 1])) { set_error("hang_node not ascending / out of range"); return TO_EMESH; }
+    hang[n] = 1;
+  }
+  if (d->n_hang > 0 && d->hang_ptr[0] != 0) { set_error("hang_ptr[0] != 0"); return TO_EMESH; }
+  for (int64_t h = 0; h < d->n_hang; ++h) {
+    int32_t a = d->hang_ptr[h], b = d->hang_ptr[h + 1];
+    if (b <= a || b - a > 4) { set_error("hanging node %lld has %d parents", (long long)h, b - a); return TO_EMESH; }
+    double wsum = 0.0;
+    for (int32_t k = a; k < b; ++k) {
+      int32_t p = d->hang_parent[k];
+      if (p < 0 || p >= d->n_node) { set_error("hang_parent out of range"); return TO_EMESH; }
+      if (hang[p]) { set_error("constraint parent %d of hanging node %d is itself hanging", p, d->hang_node[h]); return TO_EMESH; }
+      if (k > a && p <= d->hang_parent[k - 1]) { set_error("hang_parent not ascending"); return TO_EMESH; }
+      wsum += d->hang_weight[k];
+    }
+    if (std::fabs(wsum - 1.0) > 1e-12) { set_error("hanging weights of node %d sum to %.17g", d->hang_node[h], wsum); return TO_EMESH; }
+  }
+  if (d->n_fixed < 0 || (d->n_fixed > 0 && !d->fixed_dof)) { set_error("bad fixed_dof"); return TO_EINVAL; }
+  for (int64_t i = 0; i < d->n_fixed; ++i) {
+    int64_t f = d->fixed_dof[i];
+    if (f < 0 || f >= d->n_node * d->dim || (i > 0 && f <= d->fixed_dof[i - 1])) { set_error("fixed_dof not ascending / out of range"); return TO_EMESH; }
+    if (hang[f / d->dim]) { set_error("fixed DOF %lld is on a hanging node", (long long)f); return TO_EMESH; }
+  }
+  if (d->rmin > 0.0) {
+    if (!d->filt_ptr || !d->filt_idx) { set_error("rmin > 0 but no filter lists"); return TO_EINVAL; }
+    if (d->filt_ptr[0] != 0 || d->filt_ptr[d->n_elem] != d->filt_nnz) { set_error("bad filt_ptr"); return TO_EMESH; }
+    for (int64_t e = 0; e < d->n_elem; ++e)
+      if (d->filt_ptr[e + 1] < d->filt_ptr[e]) { set_error("filt_ptr not monotone"); return TO_EMESH; }
+    for (int64_t k = 0; k < d->filt_nnz; ++k)
+      if (d->filt_idx[k] < 0 || d->filt_idx[k] >= d->n_elem) { set_error("filt_idx out of range"); return TO_EMESH; }
+  }
+  return 0;
+}
+
+template <typename T>
+int upload_array(to_mesh *m, T **dst, const T *src, size_t count, cudaStream_t st) {
+  RC(m->alloc(dst, count));
+  if (count) CK(cudaMemcpyAsync(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice, st));
+  return 0;
+}
+
+int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
+  CK(cudaSetDevice(device));
+  m->device = device;
+  m->dim = d->dim;
+  m->L = d->max_level;
+  m->h0 = d->h0;
+  m->hL = d->h0 / (double)(1 << d->max_level);
+  m->E0 = d->E0;
+  m->Emin = d->Emin;
+  m->nu = d->nu;
+  m->rmin = d->rmin;
+  m->n_el = d->n_elem;
+  m->n_node = d->n_node;
+  m->n_dof = d->n_node * d->dim;
+  m->n_hang = d->n_hang;
+  m->n_fixed = d->n_fixed;
+  m->filt_nnz = d->rmin > 0.0 ? d->filt_nnz : 0;
+  const int dim = d->dim, nc = 1 << dim;
+
+  // host-derived encodings
+  std::vector<int32_t> node_hang(m->n_node, -1);
+  for (int64_t h = 0; h < d->n_hang; ++h) node_hang[d->hang_node[h]] = (int32_t)h;
+  std::vector<uint8_t> free_dof(m->n_dof, 1);
+  for (int64_t h = 0; h < d->n_hang; ++h)
+    for (int c = 0; c < dim; ++c) free_dof[(int64_t)d->hang_node[h] * dim + c] = 0;
+  for (int64_t i = 0; i < d->n_fixed; ++i) free_dof[d->fixed_dof[i]] = 0;
+  // parent -> hanging children (transpose of P), children ascending
+  std::vector<int32_t> cptr(m->n_node + 1, 0), chang, ccount(m->n_node, 0);
+  std::vector<double> cw;
+  if (d->n_hang > 0) {
+    for (int64_t h = 0; h < d->n_hang; ++h)
+      for (int32_t k = d->hang_ptr[h]; k < d->hang_ptr[h + 1]; ++k) cptr[d->hang_parent[k] + 1]++;
+    for (int64_t n = 0; n < m->n_node; ++n) cptr[n + 1] += cptr[n];
+    chang.resize(cptr[m->n_node]);
+    cw.resize(cptr[m->n_node]);
+    for (int64_t h = 0; h < d->n_hang; ++h)
+      for (int32_t k = d->hang_ptr[h]; k < d->hang_ptr[h + 1]; ++k) {
+        int32_t p = d->hang_parent[k];
+        int32_t pos = cptr[p] + ccount[p]++;
+        chang[pos] = d->hang_node[h];
+        cw[pos] = d->hang_weight[k];
+      }
+  }
+
+  RC(upload_array(m, &m->elem_node, d->elem_node, (size_t)m->n_el * nc, st));
+  RC(upload_array(m, &m->elem_anchor, d->elem_anchor, (size_t)m->n_el * dim, st));
+  RC(upload_array(m, &m->elem_level, d->elem_level, (size_t)m->n_el, st));
+  RC(upload_array(m, &m->node_hang, node_hang.data(), node_hang.size(), st));
+  RC(upload_array(m, &m->free_dof, free_dof.data(), free_dof.size(), st));
+  RC(upload_array(m, &m->load, d->load, (size_t)m->n_dof, st));
+  if (d->n_hang > 0) {
+    const size_t nnz = (size_t)d->hang_ptr[d->n_hang];
+    RC(upload_array(m, &m->hang_ptr, d->hang_ptr, (size_t)d->n_hang + 1, st));
+    RC(upload_array(m, &m->hang_parent, d->hang_parent, nnz, st));
+    RC(upload_array(m, &m->hang_weight, d->hang_weight, nnz, st));
+    RC(upload_array(m, &m->child_ptr, cptr.data(), cptr.size(), st));
+    RC(upload_array(m, &m->child_hang, chang.data(), chang.size(), st));
+    RC(upload_array(m, &m->child_weight, cw.data(), cw.size(), st));
+  }
+  if (m->filt_nnz > 0 || d->rmin > 0.0) {
+    RC(upload_array(m, &m->filt_ptr, d->filt_ptr, (size_t)m->n_el + 1, st));
+    RC(upload_array(m, &m->filt_idx, d->filt_idx, (size_t)std::max<int64_t>(1, m->filt_nnz), st));
+  }
+  // workspace
+  RC(m->alloc(&m->s, m->n_el));
+  RC(m->alloc(&m->x, m->n_dof));
+  RC(m->alloc(&m->r, m->n_dof));
+  RC(m->alloc(&m->p, m->n_dof));
+  RC(m->alloc(&m->q, m->n_dof));
+  RC(m->alloc(&m->dinv, m->n_dof));
+  RC(m->alloc(&m->D, m->n_dof));
+  RC(m->alloc(&m->partials, (size_t)kMaxPartialBlocks * 4));
+  RC(m->alloc(&m->S, 1));
+  CK(cudaMemsetAsync(m->S, 0, sizeof(CgScalars), st));
+  CK(cudaMallocHost(&m->S_host, sizeof(CgScalars)));
+  CK(cudaEventCreate(&m->ev0));
+  CK(cudaEventCreate(&m->ev1));
+  // element matrices (closed form, element.cpp)
+  build_K0(2, d->nu, m->K2.K);
+  build_K0(3, d->nu, m->K3.K);
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+// ---- operator pieces -------------------------------------------------------------------
+
+int launch_simp(to_mesh *m, double penal, const double *x, cudaStream_t st) {
+  int g = grid_for(m->n_el);
+  if (m->dim == 2)
+    k_simp<2><<<g, kBlock, 0, st>>>(m->n_el, x, m->elem_level, penal, m->E0, m->Emin, m->L, m->hL, m->s, m->S);
+  else
+    k_simp<3><<<g, kBlock, 0, st>>>(m->n_el, x, m->elem_level, penal, m->E0, m->Emin, m->L, m->hL, m->s, m->S);
+  m->last_launches++;
+  return check_launch();
+}
+
+// D = diag(Pi_F C^T K C Pi_F) from s; Dinv (free mask) and optional diag(A).
+int launch_diag(to_mesh *m, double *d_out, cudaStream_t st) {
+  CK(cudaMemsetAsync(m->D, 0, sizeof(double) * m->n_dof, st));
+  int g = grid_for(m->n_el);
+  if (m->dim == 2) k_diag<2><<<g, kBlock, 0, st>>>(m->view(), m->s, m->D, m->K2);
+  else k_diag<3><<<g, kBlock, 0, st>>>(m->view(), m->s, m->D, m->K3);
+  k_dinv<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->free_dof, m->D, m->dinv, d_out, m->S);
+  m->last_launches += 2;
+  return check_launch();
+}
+
+int launch_rhs(to_mesh *m, double *b, cudaStream_t st) {
+  int g = grid_for(m->n_node);
+  if (m->dim == 2) k_rhs<2><<<g, kBlock, 0, st>>>(m->view(), m->load, b);
+  else k_rhs<3><<<g, kBlock, 0, st>>>(m->view(), m->load, b);
+  m->last_launches++;
+  return check_launch();
+}
+
+// q = C^T K C p for p vanishing on non-free DOFs (values on non-free DOFs of q
+// are not meaningful; callers mask).  S == nullptr: unconditional.
+int launch_matvec(to_mesh *m, const double *p, double *q, const CgScalars *S, cudaStream_t st) {
+  CK(cudaMemsetAsync(q, 0, sizeof(double) * m->n_dof, st));
+  int g = grid_for(m->n_el, kBlock, 16);
+  if (m->dim == 2) k_matvec_atomic<2><<<g, kBlock, 0, st>>>(m->view(), m->s, p, q, m->K2, S);
+  else k_matvec_atomic<3><<<g, kBlock, 0, st>>>(m->view(), m->s, p, q, m->K3, S);
+  m->last_launches++;
+  return check_launch();
+}
+
+int launch_recover(to_mesh *m, const double *v, double *u, cudaStream_t st) {
+  int g = grid_for(m->n_node);
+  if (m->dim == 2) k_recover<2><<<g, kBlock, 0, st>>>(m->view(), v, u);
+  else k_recover<3><<<g, kBlock, 0, st>>>(m->view(), v, u);
+  m->last_launches++;
+  return check_launch();
+}
+
+int reset_scalars(to_mesh *m, int max_iter, bool fixed, bool history, cudaStream_t st) {
+  CgScalars h;
+  std::memset(&h, 0, sizeof(h));
+  h.max_iter = max_iter;
+  h.fixed = fixed ? 1 : 0;
+  h.history = history ? 1 : 0;
+  *m->S_host = h;
+  CK(cudaMemcpyAsync(m->S, m->S_host, sizeof(CgScalars), cudaMemcpyHostToDevice, st));
+  return 0;
+}
+
+int read_scalars(to_mesh *m, cudaStream_t st) {
+  CK(cudaMemcpyAsync(m->S_host, m->S, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double rtol, int32_t max_iter,
+          uint32_t flags, to_cg_stats *st_out, cudaStream_t st) {
+  const bool fixed = (flags & TO_FIXED_ITERS) != 0;
+  const bool warm = (flags & TO_WARM) != 0;
+  const bool hist = (flags & TO_HISTORY) != 0;
+  const int64_t n = m->n_dof;
+  m->last_launches = 0;
+  if (hist && max_iter > m->hist_cap) {
+    RC(m->alloc(&m->hist, (size_t)max_iter));
+    m->hist_cap = max_iter;
+  }
+  CK(cudaEventRecord(m->ev0, st));
+  RC(reset_scalars(m, max_iter, fixed, hist, st));
+  RC(launch_simp(m, penal, x_dev, st));
+  RC(launch_diag(m, nullptr, st));
+  RC(launch_rhs(m, m->r, st));
+  const int gv = grid_for(n);
+  k_norm2_b<<<gv, kBlock, 0, st>>>(n, m->r, m->partials, m->S);
+  m->last_launches++;
+  if (warm) {
+    k_mask_copy<<<gv, kBlock, 0, st>>>(n, u_dev, m->dinv, m->x);
+    RC(launch_matvec(m, m->x, m->q, nullptr, st));
+    k_sub_masked<<<gv, kBlock, 0, st>>>(n, m->q, m->dinv, m->r);
+    m->last_launches += 2;
+  } else {
+    CK(cudaMemsetAsync(m->x, 0, sizeof(double) * n, st));
+  }
+  k_init<<<gv, kBlock, 0, st>>>(n, m->r, m->dinv, m->p, m->partials, m->S, rtol);
+  m->last_launches++;
+  RC(check_launch());
+
+  const bool prof = (flags & TO_PROFILE) != 0;
+  if (prof) {
+    size_t need = (size_t)5 * std::max(1, max_iter);
+    while (m->prof_ev.size() < need) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      m->prof_ev.push_back(e);
+    }
+  }
+  int launched = 0;
+  int chunk = fixed ? std::max(1, max_iter) : 16;
+  RC(read_scalars(m, st));
+  bool stop = m->S_host->done != 0;
+  while (!stop && launched < max_iter) {
+    int cnt = std::min(chunk, max_iter - launched);
+    for (int k = 0; k < cnt; ++k) {
+      cudaEvent_t *E = prof ? &m->prof_ev[(size_t)5 * (launched + k)] : nullptr;
+      if (prof) CK(cudaEventRecord(E[0], st));
+      RC(launch_matvec(m, m->p, m->q, m->S, st));
+      if (prof) CK(cudaEventRecord(E[1], st));
+      k_pq<<<gv, kBlock, 0, st>>>(n, m->p, m->q, m->partials, m->S);
+      if (prof) CK(cudaEventRecord(E[2], st));
+      k_u1<<<gv, kBlock, 0, st>>>(n, m->q, m->dinv, m->r, m->partials, m->S, m->hist);
+      if (prof) CK(cudaEventRecord(E[3], st));
+      k_u2<<<gv, kBlock, 0, st>>>(n, m->r, m->dinv, m->p, m->x, m->S);
+      if (prof) CK(cudaEventRecord(E[4], st));
+      m->last_launches += 3;
+    }
+    RC(check_launch());
+    launched += cnt;
+    if (!fixed) {
+      RC(read_scalars(m, st));
+      stop = m->S_host->done || m->S_host->done_next;
+      chunk = std::min(chunk * 2, 256);
+    }
+  }
+  RC(read_scalars(m, st));
+  CgScalars res = *m->S_host;
+  if (prof) {
+    for (int j = 0; j < 5; ++j) m->prof_ms[j] = 0.0;
+    int nit = std::min(launched, res.iter);
+    for (int it = 0; it < nit; ++it)
+      for (int j = 0; j < 4; ++j) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, m->prof_ev[(size_t)5 * it + j], m->prof_ev[(size_t)5 * it + j + 1]));
+        m->prof_ms[j] += t;
+      }
+    m->prof_ms[4] = nit;
+  }
+  double relres_true = -1.0;
+  if (!(flags & TO_NO_TRUE_RES) && res.status == 0) {
+    RC(launch_rhs(m, m->r, st));          // r := b
+    RC(launch_matvec(m, m->x, m->p, nullptr, st));   // p := C^T K C x
+    k_resid2<<<gv, kBlock, 0, st>>>(n, m->r, m->p, m->free_dof, m->partials, m->S);
+    m->last_launches++;
+    RC(read_scalars(m, st));
+    relres_true = res.bnorm2 > 0.0 ? std::sqrt(m->S_host->tmp[0] / res.bnorm2) : 0.0;
+  }
+  RC(launch_recover(m, m->x, u_dev, st));
+  CK(cudaEventRecord(m->ev1, st));
+  CK(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
+  m->hist_len = hist ? res.iter : 0;
+  int rc = res.status;
+  if (rc == 0 && !fixed && !(res.rr <= res.thresh2) && res.bnorm2 > 0.0) rc = TO_NOT_CONVERGED;
+  if (st_out) {
+    st_out->iters = res.iter;
+    st_out->status = rc;
+    st_out->relres = res.bnorm2 > 0.0 ? std::sqrt(res.rr / res.bnorm2) : 0.0;
+    st_out->relres_true = relres_true;
+    st_out->ms = ms;
+    st_out->bnorm = std::sqrt(res.bnorm2);
+  }
+  if (rc < 0) {
+    const char *why = rc == TO_EBREAKDOWN ? "CG breakdown (p^T A p <= 0)"
+                      : rc == TO_ENAN     ? "NaN/Inf in the CG recurrences"
+                      : rc == TO_ENONPOS_DIAG ? "non-positive diagonal on a free DOF"
+                      : rc == TO_EINVAL   ? "density outside (0, 1]"
+                                          : "solver failure";
+    set_error("%s", why);
+  }
+  return rc;
+}
+
+}  // namespace
+
+// ======================================================================================
+// C ABI
+// ======================================================================================
+
+extern "C" int tomesh_upload(const to_mesh_desc *desc, int device, void *cuda_stream, to_mesh **out) {
+  clear_error();
+  if (!desc || !out) { set_error("NULL argument"); return TO_EINVAL; }
+  *out = nullptr;
+  int rc = validate(desc);
+  if (rc) return rc;
+  to_mesh *m = new (std::nothrow) to_mesh();
+  if (!m) { set_error("out of host memory"); return TO_ENOMEM; }
+  try {
+    rc = do_upload(desc, device, (cudaStream_t)cuda_stream, m);
+  } catch (...) {
+    set_error("out of host memory during upload");
+    rc = TO_ENOMEM;
+  }
+  if (rc) { delete m; return rc; }
+  *out = m;
+  return 0;
+}
+
+extern "C" void tomesh_free(to_mesh *m) {
+  if (!m) return;
+  cudaSetDevice(m->device);
+  delete m;
+}
+
+extern "C" int tomesh_get_info(const to_mesh *m, to_mesh_info *info) {
+  if (!m || !info) { set_error("NULL argument"); return TO_EINVAL; }
+  std::memset(info, 0, sizeof(*info));
+  info->dim = m->dim;
+  info->structured = 0;
+  info->n_elem = m->n_el;
+  info->n_node = m->n_node;
+  info->n_dof = m->n_dof;
+  info->n_hang = m->n_hang;
+  info->n_fixed = m->n_fixed;
+  info->filt_nnz = m->filt_nnz;
+  info->device_bytes = m->dev_bytes;
+  info->kernel_launches = m->last_launches;
+  info->matvec_variant = m->matvec_variant;
+  return 0;
+}
+
+extern "C" int tosolve_cg(to_mesh *m, double penal, const double *x_dev, double *u_dev, double rtol,
+                          int32_t max_iter, uint32_t flags, to_cg_stats *st, void *cuda_stream) {
+  clear_error();
+  if (!m || !x_dev || !u_dev) { set_error("NULL argument"); return TO_EINVAL; }
+  if (!(penal > 0.0) || max_iter < 0 || (!(flags & TO_FIXED_ITERS) && !(rtol >= 0.0))) {
+    set_error("bad solver parameters");
+    return TO_EINVAL;
+  }
+  if (cudaSetDevice(m->device) != cudaSuccess) { set_error("cudaSetDevice failed"); return TO_ECUDA; }
+  return solve(m, penal, x_dev, u_dev, rtol, max_iter, flags, st, (cudaStream_t)cuda_stream);
+}
+
+extern "C" int tosolve_history(const to_mesh *m, double *out, int32_t n) {
+  if (!m || !out || n < 0) { set_error("NULL argument"); return TO_EINVAL; }
+  int cnt = std::min(n, m->hist_len);
+  if (cnt > 0 && cudaMemcpy(out, m->hist, sizeof(double) * cnt, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    set_error("history copy failed");
+    return TO_ECUDA;
+  }
+  return cnt;
+}
+
+extern "C" int tosolve_profile(const to_mesh *m, double *out, int32_t n) {
+  if (!m || !out || n < 5) { set_error("bad argument"); return TO_EINVAL; }
+  for (int j = 0; j < 5; ++j) out[j] = m->prof_ms[j];
+  return 0;
+}
+
+extern "C" int to_sensitivity(to_mesh *m, double penal, const double *x_dev, const double *u_dev, double *dc_dev,
+                              double *compliance_host, void *cuda_stream) {
+  clear_error();
+  if (!m || !x_dev || !u_dev || !dc_dev) { set_error("NULL argument"); return TO_EINVAL; }
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  int g = grid_for(m->n_el);
+  if (m->dim == 2) k_sens<2><<<g, kBlock, 0, st>>>(m->view(), x_dev, u_dev, penal, m->E0, m->Emin, dc_dev, m->K2);
+  else k_sens<3><<<g, kBlock, 0, st>>>(m->view(), x_dev, u_dev, penal, m->E0, m->Emin, dc_dev, m->K3);
+  RC(check_launch());
+  if (compliance_host) {
+    k_dot<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->load, u_dev, m->partials, m->S, 1);
+    RC(check_launch());
+    CK(cudaMemcpyAsync(m->S_host, m->S, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *compliance_host = m->S_host->tmp[1];
+  }
+  return 0;
+}
+
+extern "C" int to_filter(to_mesh *m, int32_t mode, const double *x_dev, const double *in_dev, double *out_dev,
+                         void *cuda_stream) {
+  clear_error();
+  if (!m || !in_dev || !out_dev || (mode == TO_FILTER_SENS && !x_dev)) { set_error("NULL argument"); return TO_EINVAL; }
+  if (mode != TO_FILTER_SENS && mode != TO_FILTER_DENS) { set_error("bad filter mode"); return TO_EINVAL; }
+  if (out_dev == in_dev || out_dev == x_dev) { set_error("out_dev aliases an input"); return TO_EINVAL; }
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (!(m->rmin > 0.0)) {   // filter deactivated: identity
+    CK(cudaMemcpyAsync(out_dev, in_dev, sizeof(double) * m->n_el, cudaMemcpyDeviceToDevice, st));
+    return 0;
+  }
+  int g = grid_for(m->n_el);
+  if (m->dim == 2) k_filter<2><<<g, kBlock, 0, st>>>(m->view(), m->filt_ptr, m->filt_idx, m->rmin, mode, x_dev, in_dev, out_dev);
+  else k_filter<3><<<g, kBlock, 0, st>>>(m->view(), m->filt_ptr, m->filt_idx, m->rmin, mode, x_dev, in_dev, out_dev);
+  return check_launch();
+}
+
+extern "C" int to_apply_A(to_mesh *m, double penal, const double *x_dev, const double *v_dev, double *q_dev,
+                          void *cuda_stream) {
+  clear_error();
+  if (!m || !x_dev || !v_dev || !q_dev || q_dev == v_dev) { set_error("bad argument"); return TO_EINVAL; }
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  RC(reset_scalars(m, 0, false, false, st));
+  RC(launch_simp(m, penal, x_dev, st));
+  int gv = grid_for(m->n_dof);
+  k_mask_free<<<gv, kBlock, 0, st>>>(m->n_dof, m->free_dof, v_dev, m->p);
+  RC(launch_matvec(m, m->p, q_dev, nullptr, st));
+  k_fix_nonfree<<<gv, kBlock, 0, st>>>(m->n_dof, m->free_dof, v_dev, q_dev);
+  return check_launch();
+}
+
+extern "C" int to_jacobi_diag(to_mesh *m, double penal, const double *x_dev, double *d_dev, void *cuda_stream) {
+  clear_error();
+  if (!m || !x_dev || !d_dev) { set_error("NULL argument"); return TO_EINVAL; }
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  RC(reset_scalars(m, 0, false, false, st));
+  RC(launch_simp(m, penal, x_dev, st));
+  return launch_diag(m, d_dev, st);
+}
+
+extern "C" int to_project_rhs(to_mesh *m, double *b_dev, void *cuda_stream) {
+  clear_error();
+  if (!m || !b_dev) { set_error("NULL argument"); return TO_EINVAL; }
+  return launch_rhs(m, b_dev, (cudaStream_t)cuda_stream);
+}
+
+extern "C" int to_recover(to_mesh *m, const double *v_dev, double *u_dev, void *cuda_stream) {
+  clear_error();
+  if (!m || !v_dev || !u_dev) { set_error("NULL argument"); return TO_EINVAL; }
+  return launch_recover(m, v_dev, u_dev, (cudaStream_t)cuda_stream);
+}
+
+extern "C" int to_element_matrix(int32_t dim, double nu, double *K_host) {
+  if ((dim != 2 && dim != 3) || !K_host) { set_error("bad argument"); return TO_EINVAL; }
+  build_K0(dim, nu, K_host);
+  return 0;
+}
+
+extern "C" int to_element_hadamard(double nu, double *diag_host, double *off_host) {
+  if (!diag_host || !off_host) { set_error("NULL argument"); return TO_EINVAL; }
+  K0Had3 h;
+  int bad = build_K0_hadamard(nu, &h);
+  std::memcpy(diag_host, h.diag, sizeof(h.diag));
+  std::memcpy(off_host, h.off, sizeof(h.off));
+  return bad;
+}

@@ -1,0 +1,131 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle on the same
+seeded inputs.  Tolerances: L1 operator outputs 1e-12
+relative L2 (fp64 rounding of a few hundred terms), converged u, compliance,
+dc and filtered dc 1e-8 relative L2 (north_star), certificate <= 10 rtol."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from inputs import config
+from oracle import fe, mesh as omesh, pipeline, topopt
+from tests.gpu_helpers import cuda, host, product_input_density, product_mesh, rel
+from tests.helpers import cantilever2d, cantilever3d, refine_some
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "c1": lambda: config("c1"),
+    "c2": lambda: config("c2"),
+    "c3s": lambda: config("c3", nx=16, ny=8, nz=8),
+    "c4s": lambda: config("c4", base=(6, 3, 3), L=3, n_gauss=12),
+    "c5s": lambda: config("c5", nx=20, ny=10, nz=10),
+    "amr2d": lambda: cantilever2d((5, 3), L=3, leaves=refine_some(2, (5, 3), 3, [(1, 1), (3, 0)]), rmin=0.3),
+    "amr3d": lambda: cantilever3d((3, 2, 2), L=2, leaves=refine_some(3, (3, 2, 2), 2, [(1, 1, 0)]), rmin=0.4),
+}
+
+_cache = {}
+
+
+def _setup(name):
+    if name not in _cache:
+        prob = CASES[name]()
+        om = omesh.build_mesh(prob)
+        hm, m = product_mesh(prob)
+        x_dev = product_input_density(prob, hm, m)
+        _cache[name] = (prob, om, hm, m, x_dev)
+    return _cache[name]
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_L1_operators(name):
+    prob, om, hm, m, x_dev = _setup(name)
+    x = pipeline.input_density(prob, om)
+    assert rel(host(x_dev), x) <= 1e-12                       # includes the c3 DENS pass
+    xd = cuda(x)
+    K = fe.assemble_K(om, x, prob.penal, prob.E0, prob.Emin, prob.nu)
+    A, b, C = fe.projected_system(om, K)
+    rng = np.random.default_rng(7)
+    v = rng.standard_normal(om.n_dof)
+    q = torch.empty(om.n_dof, dtype=torch.float64, device="cuda")
+    m.to_apply_A(prob.penal, xd, cuda(v), q)
+    assert rel(host(q), A @ v) <= 1e-12
+    d = torch.empty_like(q)
+    m.to_jacobi_diag(prob.penal, xd, d)
+    assert rel(host(d), A.diagonal()) <= 1e-12
+    bd = torch.empty_like(q)
+    m.to_project_rhs(bd)
+    assert rel(host(bd), b) <= 1e-14
+    u = torch.empty_like(q)
+    m.to_recover(cuda(v), u)
+    assert rel(host(u), C @ v) <= 1e-14
+    # sensitivities and compliance from an identical u
+    uu = C @ v
+    dc = torch.empty(om.n_el, dtype=torch.float64, device="cuda")
+    c = m.to_sensitivity(prob.penal, xd, cuda(uu), dc, compliance=True)
+    dco = topopt.sensitivities(om, x, uu, prob.penal, prob.E0, prob.Emin, prob.nu)
+    assert rel(host(dc), dco) <= 1e-12
+    assert abs(c - fe.compliance(om.load, uu)) <= 1e-12 * max(1.0, abs(c))
+    # filter from identical (x, dc)
+    out = torch.empty_like(dc)
+    m.to_filter(0, xd, cuda(dco), out)
+    assert rel(host(out), topopt.filter_sens(om, prob.rmin, x, dco)) <= 1e-12
+    m.to_filter(1, xd, cuda(dco), out)
+    assert rel(host(out), topopt.filter_dens(om, prob.rmin, dco)) <= 1e-12
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_L2_converged_solve(name):
+    prob, om, hm, m, x_dev = _setup(name)
+    x = pipeline.input_density(prob, om)
+    ref = pipeline.run(prob, rtol=1e-10, m=om, x=x)
+    xd = cuda(x)
+    u = torch.zeros(om.n_dof, dtype=torch.float64, device="cuda")
+    st = m.tosolve_cg(prob.penal, xd, u, rtol=1e-10, max_iter=50000)
+    assert st.status == 0 and st.relres <= 1e-10
+    ud = host(u)
+    assert rel(ud, ref.u) <= 1e-8
+    dc = torch.empty(om.n_el, dtype=torch.float64, device="cuda")
+    c = m.to_sensitivity(prob.penal, xd, u, dc, compliance=True)
+    assert abs(c - ref.compliance) <= 1e-8 * abs(ref.compliance)
+    assert rel(host(dc), ref.dc) <= 1e-8
+    out = torch.empty_like(dc)
+    m.to_filter(0, xd, dc, out)
+    assert rel(host(out), ref.dc_filtered) <= 1e-8
+    # L3 certificate: the oracle's own A, b judge the device solution
+    uhat = ud.copy()
+    for k, hn in enumerate(om.hang_node):
+        uhat[om.dim * hn:om.dim * hn + om.dim] = 0.0
+    cert = np.linalg.norm(ref.b - ref.A @ uhat) / np.linalg.norm(ref.b)
+    assert cert <= 10 * 1e-10
+    assert abs(st.relres_true - cert) <= 1e-11
+    # iteration counts of two correct fp64 PCGs differ by rounding only
+    assert abs(st.iters - ref.cg.iters) <= max(5, 0.05 * ref.cg.iters)
+
+
+def test_warm_start_and_fixed_iterations():
+    prob, om, hm, m, x_dev = _setup("c2")
+    u = torch.zeros(om.n_dof, dtype=torch.float64, device="cuda")
+    st = m.tosolve_cg(prob.penal, x_dev, u, rtol=1e-10, max_iter=50000)
+    st2 = m.tosolve_cg(prob.penal, x_dev, u, rtol=1e-8, max_iter=50000, flags=1)   # TO_WARM
+    assert st2.iters <= 1
+    u2 = torch.zeros_like(u)
+    st3 = m.tosolve_cg(prob.penal, x_dev, u2, rtol=1e-30, max_iter=37, flags=2 | 4)  # FIXED | HISTORY
+    assert st3.iters == 37 and st3.status == 0
+    h = m.history(100)
+    assert h.shape[0] == 37 and np.all(np.isfinite(h))
+    # same 37 iterations again: deterministic (atomic-free reductions in fixed order)
+    u3 = torch.zeros_like(u)
+    m.tosolve_cg(prob.penal, x_dev, u3, rtol=1e-30, max_iter=37, flags=2)
+    if m.info()["matvec_variant"] != 0:
+        assert torch.equal(u2, u3)
+
+
+def test_zero_load_gives_zero_solution():
+    prob = cantilever2d((4, 2))
+    prob.loads = []
+    hm, m = product_mesh(prob)
+    x = cuda(np.full(hm.n_el, 0.5))
+    u = torch.full((hm.n_dof,), 3.0, dtype=torch.float64, device="cuda")
+    st = m.tosolve_cg(3.0, x, u, rtol=1e-10, max_iter=100)
+    assert st.iters == 0 and torch.count_nonzero(u) == 0
