@@ -38,11 +38,15 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // Block-wide sum of NV values; the result is valid in thread 0.
+__device__ __forceinline__ int lin_tid() { return threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z); }
+__device__ __forceinline__ int lin_nthr() { return blockDim.x * blockDim.y * blockDim.z; }
+
 template <int NV>
 __device__ __forceinline__ void block_sum(double (&v)[NV]) {
   __shared__ double sh[NV][32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nw = (blockDim.x + 31) >> 5;
+  const int tid = lin_tid();
+  const int lane = tid & 31, wid = tid >> 5;
+  const int nw = (lin_nthr() + 31) >> 5;
 #pragma unroll
   for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
   __syncthreads();
@@ -67,7 +71,8 @@ template <int NV>
 __device__ __forceinline__ bool grid_sum(double (&v)[NV], double *partials, uint32_t *counter) {
   __shared__ bool s_last;
   block_sum<NV>(v);
-  if (threadIdx.x == 0) {
+  const int tid = lin_tid();
+  if (tid == 0) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) partials[(size_t)blockIdx.x * NV + k] = v[k];
     __threadfence();
@@ -80,21 +85,30 @@ __device__ __forceinline__ bool grid_sum(double (&v)[NV], double *partials, uint
   double acc[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+  for (int b = tid; b < (int)gridDim.x; b += lin_nthr()) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) acc[k] += __ldcg(&partials[(size_t)b * NV + k]);
   }
   block_sum<NV>(acc);
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) v[k] = acc[k];
     *counter = 0u;
   }
-  return threadIdx.x == 0;
+  return tid == 0;
 }
 
 __device__ __forceinline__ bool cg_stopped(const CgScalars *S) {
   return *((volatile const int32_t *)&S->done) | *((volatile const int32_t *)&S->done_next);
+}
+
+// Called by the first kernel of every iteration (the operator apply).  When
+// the previous iteration converged (done_next), promote it to `done` so that
+// the x/p update kernel of this overshoot iteration is skipped as well.
+__device__ __forceinline__ bool cg_stop_at_apply(CgScalars *S) {
+  if (!cg_stopped(S)) return false;
+  if (blockIdx.x == 0 && threadIdx.x == 0) S->done = 1;
+  return true;
 }
 
 }  // namespace tomesh

@@ -227,9 +227,9 @@ template <int DIM>
 __global__ void k_matvec_atomic(MeshView M, const double *__restrict__ s, const double *__restrict__ p,
                                 double *__restrict__ q,
                                 const __grid_constant__ typename std::conditional<DIM == 2, K0Dense2, K0Dense3>::type K0,
-                                const CgScalars *S) {
+                                CgScalars *S) {
   constexpr int NC = 1 << DIM, ND = DIM * NC;
-  if (S && cg_stopped(S)) return;
+  if (S && cg_stop_at_apply(S)) return;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M.n_el; e += (int64_t)gridDim.x * blockDim.x) {
     double ue[ND], ye[ND];
     int node[NC], hang[NC];

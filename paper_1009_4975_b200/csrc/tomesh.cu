@@ -14,8 +14,13 @@
 #include "element.h"
 #include "kernels_cg.cuh"
 #include "kernels_general.cuh"
+#include "kernels_struct3d.cuh"
 
 using namespace tomesh;
+
+namespace tomesh {
+constexpr int kS3TYW = 8;   // warps per CTA (node rows + 1) of the structured H8 apply
+}
 
 namespace {
 
@@ -49,6 +54,13 @@ struct to_mesh {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   K0Dense2 K2{};
   K0Dense3 K3{};
+  K0Had3 KH{};
+  // structured fast path (uniform H8 box)
+  bool structured = false, force_general = false;
+  GridView G{};
+  int32_t *perm_el = nullptr, *perm_node = nullptr;
+  uint8_t *free_lex = nullptr;
+  double k0d = 0.0, h_struct = 1.0;
   int last_launches = 0;
   int matvec_variant = 0;
   std::vector<cudaEvent_t> prof_ev;   // TO_PROFILE: 5 events per iteration
@@ -198,6 +210,74 @@ int upload_array(to_mesh *m, T **dst, const T *src, size_t count, cudaStream_t s
   return 0;
 }
 
+// Uniform 3D meshes (one level, leaves tiling a box, no hanging nodes) use the
+// structured fast path: lexicographic internal vectors, implicit connectivity.
+int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof, cudaStream_t st, to_mesh *m) {
+  m->structured = false;
+  if (d->dim != 3 || d->n_hang != 0 || m->force_general) return 0;
+  const int8_t lev0 = d->elem_level[0];
+  for (int64_t e = 1; e < d->n_elem; ++e)
+    if (d->elem_level[e] != lev0) return 0;
+  const int32_t sz = 1 << (d->max_level - lev0);
+  int64_t ext[3] = {0, 0, 0};
+  for (int64_t e = 0; e < d->n_elem; ++e)
+    for (int c = 0; c < 3; ++c) ext[c] = std::max<int64_t>(ext[c], d->elem_anchor[e * 3 + c] / sz + 1);
+  if (ext[0] * ext[1] * ext[2] != d->n_elem) return 0;
+  if ((ext[0] + 1) * (ext[1] + 1) * (ext[2] + 1) != d->n_node) return 0;
+  if (ext[0] + 1 >= (1 << 30) / 4) return 0;
+  GridView G;
+  G.EX = (int)ext[0]; G.EY = (int)ext[1]; G.EZ = (int)ext[2];
+  G.NX = G.EX + 1; G.NY = G.EY + 1; G.NZ = G.EZ + 1;
+  G.ntx = (G.NX + 30) / 31;
+  G.nty = (G.NY + kS3TYW - 2) / (kS3TYW - 1);
+  // z segmentation: balance full waves (2 CTAs/SM) against the one recomputed layer per segment
+  {
+    const int64_t base = (int64_t)G.ntx * G.nty, slots = (int64_t)kNumSMs * 2;
+    double best = 1e300;
+    int best_n = 1;
+    for (int nz = 1; nz <= G.NZ; ++nz) {
+      int zlen = (G.NZ + nz - 1) / nz;
+      int nseg = (G.NZ + zlen - 1) / zlen;
+      double waves = std::ceil((double)(base * nseg) / (double)slots);
+      double cost = waves * (zlen + 1);
+      if (cost < best - 1e-9) { best = cost; best_n = nseg; }
+    }
+    G.zlen = (G.NZ + best_n - 1) / best_n;
+    G.nzs = (G.NZ + G.zlen - 1) / G.zlen;
+  }
+  // all 24 diagonal entries of the cube's K0 are equal (symmetry); Dinv uses one
+  for (int a = 1; a < 24; ++a)
+    if (std::fabs(m->K3.K[a * 24 + a] - m->K3.K[0]) > 1e-14 * std::fabs(m->K3.K[0])) return 0;
+  std::vector<int32_t> perm_el(d->n_elem), perm_node(d->n_node, -1);
+  for (int64_t e = 0; e < d->n_elem; ++e) {
+    const int32_t *a = d->elem_anchor + e * 3;
+    const int64_t ei = a[0] / sz, ej = a[1] / sz, ek = a[2] / sz;
+    perm_el[e] = (int32_t)(ei + G.EX * (ej + (int64_t)G.EY * ek));
+    for (int c = 0; c < 8; ++c) {
+      const int64_t ni = ei + (c & 1), nj = ej + ((c >> 1) & 1), nk = ek + (c >> 2);
+      perm_node[d->elem_node[e * 8 + c]] = (int32_t)(ni + G.NX * (nj + (int64_t)G.NY * nk));
+    }
+  }
+  std::vector<uint8_t> free_lex(m->n_dof, 0);
+  for (int64_t n = 0; n < d->n_node; ++n) {
+    if (perm_node[n] < 0) return 0;
+    for (int c = 0; c < 3; ++c) free_lex[(int64_t)perm_node[n] * 3 + c] = free_dof[n * 3 + c];
+  }
+  RC(upload_array(m, &m->perm_el, perm_el.data(), perm_el.size(), st));
+  RC(upload_array(m, &m->perm_node, perm_node.data(), perm_node.size(), st));
+  RC(upload_array(m, &m->free_lex, free_lex.data(), free_lex.size(), st));
+  const int64_t grid = (int64_t)G.ntx * G.nty * G.nzs;
+  if (grid > kMaxPartialBlocks) RC(m->alloc(&m->partials, (size_t)grid * 4));
+  m->G = G;
+  m->k0d = m->K3.K[0];
+  m->h_struct = m->hL * (double)sz;
+  m->structured = true;
+  m->matvec_variant = 1;
+  const size_t smem = sizeof(S3Smem<kS3TYW>);
+  CK(cudaFuncSetAttribute(k_apply_s3<kS3TYW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return 0;
+}
+
 int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
   CK(cudaSetDevice(device));
   m->device = device;
@@ -278,6 +358,8 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
   // element matrices (closed form, element.cpp)
   build_K0(2, d->nu, m->K2.K);
   build_K0(3, d->nu, m->K3.K);
+  if (build_K0_hadamard(d->nu, &m->KH) != 0) { set_error("Hadamard factorisation check failed"); return TO_EINVAL; }
+  RC(setup_structured(d, free_dof, st, m));
   CK(cudaStreamSynchronize(st));
   return 0;
 }
@@ -315,7 +397,7 @@ int launch_rhs(to_mesh *m, double *b, cudaStream_t st) {
 
 // q = C^T K C p for p vanishing on non-free DOFs (values on non-free DOFs of q
 // are not meaningful; callers mask).  S == nullptr: unconditional.
-int launch_matvec(to_mesh *m, const double *p, double *q, const CgScalars *S, cudaStream_t st) {
+int launch_matvec(to_mesh *m, const double *p, double *q, CgScalars *S, cudaStream_t st) {
   CK(cudaMemsetAsync(q, 0, sizeof(double) * m->n_dof, st));
   int g = grid_for(m->n_el, kBlock, 16);
   if (m->dim == 2) k_matvec_atomic<2><<<g, kBlock, 0, st>>>(m->view(), m->s, p, q, m->K2, S);
@@ -349,6 +431,71 @@ int read_scalars(to_mesh *m, cudaStream_t st) {
   return 0;
 }
 
+// ---- internal-order operations --------------------------------------------------------
+// The CG vectors are in "internal" order: lexicographic for the structured path,
+// canonical (Morton, C3) otherwise.
+
+const uint8_t *free_int(const to_mesh *m) { return m->structured ? m->free_lex : m->free_dof; }
+
+// s_e and Dinv (internal order); d_int (optional) = diag(A) in internal order.
+int op_scale_and_diag(to_mesh *m, double penal, const double *x, double *d_int, cudaStream_t st) {
+  if (!m->structured) {
+    RC(launch_simp(m, penal, x, st));
+    return launch_diag(m, d_int, st);
+  }
+  k_simp_s3<<<grid_for(m->n_el), kBlock, 0, st>>>(m->n_el, x, m->perm_el, penal, m->E0, m->Emin, m->h_struct,
+                                                   m->s, m->S);
+  k_diag_s3<<<grid_for(m->n_node), kBlock, 0, st>>>(m->G, m->s, m->free_lex, m->k0d, m->dinv, d_int, m->S);
+  m->last_launches += 2;
+  return check_launch();
+}
+
+// b = Pi_F C^T f in internal order
+int op_rhs(to_mesh *m, double *b_int, cudaStream_t st) {
+  if (!m->structured) return launch_rhs(m, b_int, st);
+  k_to_lex<<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->perm_node, m->load, m->free_dof, b_int);
+  m->last_launches++;
+  return check_launch();
+}
+
+// out = C^T K C in (in vanishing on non-free DOFs).  With S: CG mode (stop
+// check, alpha = rho / in.out on the device).
+int op_apply(to_mesh *m, const double *in, double *out, CgScalars *S, cudaStream_t st) {
+  if (!m->structured) {
+    RC(launch_matvec(m, in, out, S, st));
+    if (S) {
+      k_pq<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, in, out, m->partials, S);
+      m->last_launches++;
+    }
+    return check_launch();
+  }
+  const GridView &G = m->G;
+  dim3 block(32, kS3TYW);
+  int grid = G.ntx * G.nty * G.nzs;
+  k_apply_s3<kS3TYW><<<grid, block, sizeof(S3Smem<kS3TYW>), st>>>(G, m->s, in, out, m->KH, S, m->partials);
+  m->last_launches++;
+  return check_launch();
+}
+
+// dst = Pi_F u (canonical -> internal), used for warm starts
+int op_masked_in(to_mesh *m, const double *u_canon, double *dst, cudaStream_t st) {
+  if (!m->structured) {
+    k_mask_free<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->free_dof, u_canon, dst);
+  } else {
+    k_to_lex<<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->perm_node, u_canon, m->free_dof, dst);
+  }
+  m->last_launches++;
+  return check_launch();
+}
+
+// u = C v (internal -> canonical, hanging DOFs interpolated, Eq. 9)
+int op_recover_out(to_mesh *m, const double *v_int, double *u_canon, cudaStream_t st) {
+  if (!m->structured) return launch_recover(m, v_int, u_canon, st);
+  k_from_lex<<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->perm_node, v_int, u_canon);
+  m->last_launches++;
+  return check_launch();
+}
+
 int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double rtol, int32_t max_iter,
           uint32_t flags, to_cg_stats *st_out, cudaStream_t st) {
   const bool fixed = (flags & TO_FIXED_ITERS) != 0;
@@ -362,17 +509,16 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   }
   CK(cudaEventRecord(m->ev0, st));
   RC(reset_scalars(m, max_iter, fixed, hist, st));
-  RC(launch_simp(m, penal, x_dev, st));
-  RC(launch_diag(m, nullptr, st));
-  RC(launch_rhs(m, m->r, st));
+  RC(op_scale_and_diag(m, penal, x_dev, nullptr, st));
+  RC(op_rhs(m, m->r, st));
   const int gv = grid_for(n);
   k_norm2_b<<<gv, kBlock, 0, st>>>(n, m->r, m->partials, m->S);
   m->last_launches++;
   if (warm) {
-    k_mask_copy<<<gv, kBlock, 0, st>>>(n, u_dev, m->dinv, m->x);
-    RC(launch_matvec(m, m->x, m->q, nullptr, st));
+    RC(op_masked_in(m, u_dev, m->x, st));
+    RC(op_apply(m, m->x, m->q, nullptr, st));
     k_sub_masked<<<gv, kBlock, 0, st>>>(n, m->q, m->dinv, m->r);
-    m->last_launches += 2;
+    m->last_launches++;
   } else {
     CK(cudaMemsetAsync(m->x, 0, sizeof(double) * n, st));
   }
@@ -382,7 +528,7 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
 
   const bool prof = (flags & TO_PROFILE) != 0;
   if (prof) {
-    size_t need = (size_t)5 * std::max(1, max_iter);
+    size_t need = (size_t)4 * std::max(1, max_iter);
     while (m->prof_ev.size() < need) {
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
@@ -396,17 +542,15 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   while (!stop && launched < max_iter) {
     int cnt = std::min(chunk, max_iter - launched);
     for (int k = 0; k < cnt; ++k) {
-      cudaEvent_t *E = prof ? &m->prof_ev[(size_t)5 * (launched + k)] : nullptr;
+      cudaEvent_t *E = prof ? &m->prof_ev[(size_t)4 * (launched + k)] : nullptr;
       if (prof) CK(cudaEventRecord(E[0], st));
-      RC(launch_matvec(m, m->p, m->q, m->S, st));
+      RC(op_apply(m, m->p, m->q, m->S, st));
       if (prof) CK(cudaEventRecord(E[1], st));
-      k_pq<<<gv, kBlock, 0, st>>>(n, m->p, m->q, m->partials, m->S);
-      if (prof) CK(cudaEventRecord(E[2], st));
       k_u1<<<gv, kBlock, 0, st>>>(n, m->q, m->dinv, m->r, m->partials, m->S, m->hist);
-      if (prof) CK(cudaEventRecord(E[3], st));
+      if (prof) CK(cudaEventRecord(E[2], st));
       k_u2<<<gv, kBlock, 0, st>>>(n, m->r, m->dinv, m->p, m->x, m->S);
-      if (prof) CK(cudaEventRecord(E[4], st));
-      m->last_launches += 3;
+      if (prof) CK(cudaEventRecord(E[3], st));
+      m->last_launches += 2;
     }
     RC(check_launch());
     launched += cnt;
@@ -421,24 +565,26 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   if (prof) {
     for (int j = 0; j < 5; ++j) m->prof_ms[j] = 0.0;
     int nit = std::min(launched, res.iter);
-    for (int it = 0; it < nit; ++it)
-      for (int j = 0; j < 4; ++j) {
+    for (int it = 0; it < nit; ++it) {
+      const int slot[3] = {0, 2, 3};   // apply(+alpha), r update, x/p update
+      for (int j = 0; j < 3; ++j) {
         float t = 0.f;
-        CK(cudaEventElapsedTime(&t, m->prof_ev[(size_t)5 * it + j], m->prof_ev[(size_t)5 * it + j + 1]));
-        m->prof_ms[j] += t;
+        CK(cudaEventElapsedTime(&t, m->prof_ev[(size_t)4 * it + j], m->prof_ev[(size_t)4 * it + j + 1]));
+        m->prof_ms[slot[j]] += t;
       }
+    }
     m->prof_ms[4] = nit;
   }
   double relres_true = -1.0;
   if (!(flags & TO_NO_TRUE_RES) && res.status == 0) {
-    RC(launch_rhs(m, m->r, st));          // r := b
-    RC(launch_matvec(m, m->x, m->p, nullptr, st));   // p := C^T K C x
-    k_resid2<<<gv, kBlock, 0, st>>>(n, m->r, m->p, m->free_dof, m->partials, m->S);
+    RC(op_rhs(m, m->r, st));                      // r := b
+    RC(op_apply(m, m->x, m->p, nullptr, st));     // p := C^T K C x
+    k_resid2<<<gv, kBlock, 0, st>>>(n, m->r, m->p, free_int(m), m->partials, m->S);
     m->last_launches++;
     RC(read_scalars(m, st));
     relres_true = res.bnorm2 > 0.0 ? std::sqrt(m->S_host->tmp[0] / res.bnorm2) : 0.0;
   }
-  RC(launch_recover(m, m->x, u_dev, st));
+  RC(op_recover_out(m, m->x, u_dev, st));
   CK(cudaEventRecord(m->ev1, st));
   CK(cudaStreamSynchronize(st));
   float ms = 0.f;
@@ -583,10 +729,16 @@ extern "C" int to_apply_A(to_mesh *m, double penal, const double *x_dev, const d
   if (!m || !x_dev || !v_dev || !q_dev || q_dev == v_dev) { set_error("bad argument"); return TO_EINVAL; }
   cudaStream_t st = (cudaStream_t)cuda_stream;
   RC(reset_scalars(m, 0, false, false, st));
-  RC(launch_simp(m, penal, x_dev, st));
+  RC(op_scale_and_diag(m, penal, x_dev, nullptr, st));
   int gv = grid_for(m->n_dof);
-  k_mask_free<<<gv, kBlock, 0, st>>>(m->n_dof, m->free_dof, v_dev, m->p);
-  RC(launch_matvec(m, m->p, q_dev, nullptr, st));
+  if (!m->structured) {
+    k_mask_free<<<gv, kBlock, 0, st>>>(m->n_dof, m->free_dof, v_dev, m->p);
+    RC(op_apply(m, m->p, q_dev, nullptr, st));
+  } else {
+    RC(op_masked_in(m, v_dev, m->p, st));           // Pi_F v, internal order
+    RC(op_apply(m, m->p, m->q, nullptr, st));
+    RC(op_recover_out(m, m->q, q_dev, st));         // back to canonical order
+  }
   k_fix_nonfree<<<gv, kBlock, 0, st>>>(m->n_dof, m->free_dof, v_dev, q_dev);
   return check_launch();
 }
@@ -596,8 +748,9 @@ extern "C" int to_jacobi_diag(to_mesh *m, double penal, const double *x_dev, dou
   if (!m || !x_dev || !d_dev) { set_error("NULL argument"); return TO_EINVAL; }
   cudaStream_t st = (cudaStream_t)cuda_stream;
   RC(reset_scalars(m, 0, false, false, st));
-  RC(launch_simp(m, penal, x_dev, st));
-  return launch_diag(m, d_dev, st);
+  if (!m->structured) return op_scale_and_diag(m, penal, x_dev, d_dev, st);
+  RC(op_scale_and_diag(m, penal, x_dev, m->D, st));
+  return op_recover_out(m, m->D, d_dev, st);
 }
 
 extern "C" int to_project_rhs(to_mesh *m, double *b_dev, void *cuda_stream) {
