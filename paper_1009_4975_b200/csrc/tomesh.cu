@@ -35,6 +35,7 @@ struct to_mesh {
   int dim = 0, L = 0, device = 0;
   double h0 = 1.0, hL = 1.0, E0 = 1.0, Emin = 1e-9, nu = 0.3, rmin = 0.0;
   int64_t n_el = 0, n_node = 0, n_dof = 0, n_hang = 0, n_fixed = 0, filt_nnz = 0;
+  int64_t n_int = 0;   // length of the internal CG vectors (n_dof, or padded rows when structured)
   std::vector<DevBuf> bufs;
   int64_t dev_bytes = 0;
   // mesh
@@ -228,6 +229,8 @@ int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof
   GridView G;
   G.EX = (int)ext[0]; G.EY = (int)ext[1]; G.EZ = (int)ext[2];
   G.NX = G.EX + 1; G.NY = G.EY + 1; G.NZ = G.EZ + 1;
+  G.RS = 3 * G.NX + ((3 * G.NX) & 1);     // even row stride: every node row 16-byte aligned
+  if ((int64_t)G.RS * G.NY * G.NZ >= (1LL << 31) - kS3PadBack) return 0;
   G.ntx = (G.NX + 30) / 31;
   G.nty = (G.NY + kS3TYW - 2) / (kS3TYW - 1);
   // z segmentation: balance full waves (2 CTAs/SM) against the one recomputed layer per segment
@@ -255,13 +258,14 @@ int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof
     perm_el[e] = (int32_t)(ei + G.EX * (ej + (int64_t)G.EY * ek));
     for (int c = 0; c < 8; ++c) {
       const int64_t ni = ei + (c & 1), nj = ej + ((c >> 1) & 1), nk = ek + (c >> 2);
-      perm_node[d->elem_node[e * 8 + c]] = (int32_t)(ni + G.NX * (nj + (int64_t)G.NY * nk));
+      perm_node[d->elem_node[e * 8 + c]] = (int32_t)((nj + (int64_t)G.NY * nk) * G.RS + 3 * ni);
     }
   }
-  std::vector<uint8_t> free_lex(m->n_dof, 0);
+  m->n_int = (int64_t)G.RS * G.NY * G.NZ;
+  std::vector<uint8_t> free_lex(m->n_int, 0);
   for (int64_t n = 0; n < d->n_node; ++n) {
     if (perm_node[n] < 0) return 0;
-    for (int c = 0; c < 3; ++c) free_lex[(int64_t)perm_node[n] * 3 + c] = free_dof[n * 3 + c];
+    for (int c = 0; c < 3; ++c) free_lex[(int64_t)perm_node[n] + c] = free_dof[n * 3 + c];
   }
   RC(upload_array(m, &m->perm_el, perm_el.data(), perm_el.size(), st));
   RC(upload_array(m, &m->perm_node, perm_node.data(), perm_node.size(), st));
@@ -341,14 +345,6 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
     RC(upload_array(m, &m->filt_ptr, d->filt_ptr, (size_t)m->n_el + 1, st));
     RC(upload_array(m, &m->filt_idx, d->filt_idx, (size_t)std::max<int64_t>(1, m->filt_nnz), st));
   }
-  // workspace
-  RC(m->alloc(&m->s, m->n_el));
-  RC(m->alloc(&m->x, m->n_dof));
-  RC(m->alloc(&m->r, m->n_dof));
-  RC(m->alloc(&m->p, m->n_dof));
-  RC(m->alloc(&m->q, m->n_dof));
-  RC(m->alloc(&m->dinv, m->n_dof));
-  RC(m->alloc(&m->D, m->n_dof));
   RC(m->alloc(&m->partials, (size_t)kMaxPartialBlocks * 4));
   RC(m->alloc(&m->S, 1));
   CK(cudaMemsetAsync(m->S, 0, sizeof(CgScalars), st));
@@ -359,7 +355,17 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
   build_K0(2, d->nu, m->K2.K);
   build_K0(3, d->nu, m->K3.K);
   if (build_K0_hadamard(d->nu, &m->KH) != 0) { set_error("Hadamard factorisation check failed"); return TO_EINVAL; }
+  m->n_int = m->n_dof;
   RC(setup_structured(d, free_dof, st, m));
+  // workspace: internal-order vectors with zero pads on both sides (the
+  // structured kernels read whole aligned row windows)
+  RC(m->alloc(&m->s, m->n_el));
+  for (double **v : {&m->x, &m->r, &m->p, &m->q, &m->dinv, &m->D}) {
+    double *base = nullptr;
+    RC(m->alloc(&base, (size_t)(m->n_int + kS3PadFront + kS3PadBack)));
+    CK(cudaMemsetAsync(base, 0, sizeof(double) * (m->n_int + kS3PadFront + kS3PadBack), st));
+    *v = base + kS3PadFront;
+  }
   CK(cudaStreamSynchronize(st));
   return 0;
 }
@@ -453,7 +459,7 @@ int op_scale_and_diag(to_mesh *m, double penal, const double *x, double *d_int, 
 // b = Pi_F C^T f in internal order
 int op_rhs(to_mesh *m, double *b_int, cudaStream_t st) {
   if (!m->structured) return launch_rhs(m, b_int, st);
-  k_to_lex<<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->perm_node, m->load, m->free_dof, b_int);
+  k_to_int<<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->perm_node, m->load, m->free_dof, b_int);
   m->last_launches++;
   return check_launch();
 }
@@ -482,7 +488,7 @@ int op_masked_in(to_mesh *m, const double *u_canon, double *dst, cudaStream_t st
   if (!m->structured) {
     k_mask_free<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->free_dof, u_canon, dst);
   } else {
-    k_to_lex<<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->perm_node, u_canon, m->free_dof, dst);
+    k_to_int<<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->perm_node, u_canon, m->free_dof, dst);
   }
   m->last_launches++;
   return check_launch();
@@ -491,7 +497,7 @@ int op_masked_in(to_mesh *m, const double *u_canon, double *dst, cudaStream_t st
 // u = C v (internal -> canonical, hanging DOFs interpolated, Eq. 9)
 int op_recover_out(to_mesh *m, const double *v_int, double *u_canon, cudaStream_t st) {
   if (!m->structured) return launch_recover(m, v_int, u_canon, st);
-  k_from_lex<<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->perm_node, v_int, u_canon);
+  k_from_int<<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->perm_node, v_int, u_canon);
   m->last_launches++;
   return check_launch();
 }
@@ -501,7 +507,7 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   const bool fixed = (flags & TO_FIXED_ITERS) != 0;
   const bool warm = (flags & TO_WARM) != 0;
   const bool hist = (flags & TO_HISTORY) != 0;
-  const int64_t n = m->n_dof;
+  const int64_t n = m->n_int;
   m->last_launches = 0;
   if (hist && max_iter > m->hist_cap) {
     RC(m->alloc(&m->hist, (size_t)max_iter));

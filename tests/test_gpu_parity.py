@@ -18,7 +18,7 @@ CASES = {
     "c1": lambda: config("c1"),
     "c2": lambda: config("c2"),
     "c3s": lambda: config("c3", nx=16, ny=8, nz=8),
-    "c4s": lambda: config("c4", base=(6, 3, 3), L=3, n_gauss=12),
+    "c4s": lambda: config("c4", base=(12, 6, 6), L=2, n_gauss=60),
     "c5s": lambda: config("c5", nx=20, ny=10, nz=10),
     "amr2d": lambda: cantilever2d((5, 3), L=3, leaves=refine_some(2, (5, 3), 3, [(1, 1), (3, 0)]), rmin=0.3),
     "amr3d": lambda: cantilever3d((3, 2, 2), L=2, leaves=refine_some(3, (3, 2, 2), 2, [(1, 1, 0)]), rmin=0.4),

@@ -101,7 +101,7 @@ def test_host_builder_bit_exact_vs_oracle(case):
     elif case == "c5s":
         prob = config("c5", nx=16, ny=8, nz=8)
     elif case == "c4s":
-        prob = config("c4", base=(6, 3, 3), L=3, n_gauss=12)
+        prob = config("c4", base=(12, 6, 6), L=2, n_gauss=60)
     elif case == "amr2d":
         prob = cantilever2d((5, 3), L=3, leaves=refine_some(2, (5, 3), 3, [(1, 1), (3, 0)]), rmin=0.3)
     elif case == "amr3d":
