@@ -1,13 +1,17 @@
-// Fused Jacobi-PCG vector kernels (textbook Hestenes-Stiefel recurrences on
-// the rescaled system, PAPER.md:511-523 with SURVEY reading Q3).
+// Jacobi-PCG vector kernels (textbook Hestenes-Stiefel recurrences on the
+// rescaled system, PAPER.md:511-523 with reading Q3), fused so that every
+// iteration makes one pass of the operator and one pass of the r update:
 //
-// Per iteration (V = 12 fp64 vector passes):
-//   matvec            q = A p                         (p read, q written)
-//   k_pq              alpha = rho / (p.q)             (p, q read) [v0 only; fused later]
-//   k_u1              r -= alpha q; rho' = r.(Dinv r); rr = r.r      (r, q, Dinv -> r)
-//   k_u2              x += alpha p;  p = Dinv r + beta p            (r, Dinv, p, x -> p, x)
-// Dinv == 0 marks hanging and fixed DOFs: r, p, x stay 0 there (A is the
-// identity on them and b vanishes there, so this is exact).
+//   K1  p_k = Dinv r_k + beta_{k-1} p_{k-1};  x += alpha_{k-1} p_{k-1}
+//       q = A p_k;  alpha_k = rho_k / (p_k . q)
+//   K2  r_{k+1} = r_k - alpha_k q;  rho_{k+1} = r.Dinv r;  rr = r.r
+//       beta_k = rho_{k+1} / rho_k;  stop test on rr
+//   after the loop: x += alpha_last p_last (k_xfinal)
+//
+// p ping-pongs between two buffers (iteration k reads pbuf[(k+1)&1] and
+// writes pbuf[k&1]) because K1 reads p_{k-1} at neighbours' nodes while they
+// write p_k.  Dinv == 0 marks hanging and fixed DOFs: r, p, x stay 0 there
+// (A is the identity on them and b vanishes there, so this is exact).
 #pragma once
 #include "device_common.cuh"
 
@@ -16,6 +20,38 @@ namespace tomesh {
 #define GRID_STRIDE(i, n) \
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
+// Scalars after the initial residual: rho0 = r0.z0, rr0, thresholds.
+__device__ __forceinline__ void cg_init_scalars(CgScalars *S, double rho, double rr, double rtol) {
+  S->rho = rho;
+  S->rr = rr;
+  S->thresh2 = rtol * rtol * S->bnorm2;
+  S->alpha = 0.0;
+  S->beta = 0.0;
+  if (S->bnorm2 == 0.0 || S->status != 0) S->done = 1;
+  if (!S->fixed && rr <= S->thresh2) S->done = 1;
+  if (S->max_iter <= 0) S->done = 1;
+  if (!(rho == rho) || !(rr == rr)) {
+    S->status = -5;
+    S->done = 1;
+  }
+}
+
+// Scalars after the r update of iteration k (one completed iteration).
+__device__ __forceinline__ void cg_after_rupdate(CgScalars *S, double rz, double rr, double *hist) {
+  const int it = S->iter + 1;
+  S->iter = it;
+  if (!(rz == rz) || !(rr == rr)) {
+    S->status = -5;
+    S->done = 1;
+    return;
+  }
+  S->beta = rz / S->rho;
+  S->rho = rz;
+  S->rr = rr;
+  if (S->history && hist) hist[it - 1] = sqrt(rr / S->bnorm2);
+  if ((!S->fixed && rr <= S->thresh2) || it >= S->max_iter) S->done_next = 1;
+}
+
 // ||v||^2 -> S->bnorm2 (used for b).
 __global__ void k_norm2_b(int64_t n, const double *__restrict__ v, double *partials, CgScalars *S) {
   double acc[1] = {0.0};
@@ -23,96 +59,60 @@ __global__ void k_norm2_b(int64_t n, const double *__restrict__ v, double *parti
   if (grid_sum<1>(acc, partials, &S->counter[CNT_MISC])) S->bnorm2 = acc[0];
 }
 
-// x = Pi_F u (warm start), masked copy using Dinv as the free mask.
-__global__ void k_mask_copy(int64_t n, const double *__restrict__ u, const double *__restrict__ Dinv,
-                            double *__restrict__ x) {
-  GRID_STRIDE(i, n) { x[i] = (Dinv[i] != 0.0) ? u[i] : 0.0; }
-}
-
-// r = r - q on free DOFs (warm start: r = b - A x0).
-__global__ void k_sub_masked(int64_t n, const double *__restrict__ q, const double *__restrict__ Dinv,
+// r = r - q on free DOFs (warm start: r = b - A x0); `free` per DOF.
+__global__ void k_sub_masked(int64_t n, const double *__restrict__ q, const uint8_t *__restrict__ free_dof,
                              double *__restrict__ r) {
-  GRID_STRIDE(i, n) { r[i] = (Dinv[i] != 0.0) ? r[i] - q[i] : 0.0; }
+  GRID_STRIDE(i, n) { r[i] = free_dof[i] ? r[i] - q[i] : 0.0; }
 }
 
-// z = Dinv r; p = z; rho = r.z; rr = r.r; thresholds.
-__global__ void k_init(int64_t n, const double *__restrict__ r, const double *__restrict__ Dinv,
-                       double *__restrict__ p, double *partials, CgScalars *S, double rtol) {
+// General path K1, elementwise half: p_k, deferred x update, q = 0 (the
+// atomic operator kernel accumulates into q next).
+__global__ void k_pre_g(int64_t n, const double *__restrict__ r, const double *__restrict__ Dinv,
+                        const double *__restrict__ po, double *__restrict__ pn, double *__restrict__ x,
+                        double *__restrict__ q, CgScalars *S) {
+  if (cg_stop_at_apply(S)) return;
+  const double beta = __ldcg(&S->beta), alpha_old = __ldcg(&S->alpha);
+  GRID_STRIDE(i, n) {
+    const double pold = po[i];
+    const double pv = (beta != 0.0) ? beta * pold : 0.0;
+    pn[i] = fma(Dinv[i], r[i], pv);
+    if (alpha_old != 0.0) x[i] = fma(alpha_old, pold, x[i]);
+    q[i] = 0.0;
+  }
+}
+
+// General path K2 (per-DOF Dinv).  INIT: rho0, rr0 only.
+template <bool INIT>
+__global__ void k_rupd(int64_t n, const double *__restrict__ q, const double *__restrict__ Dinv,
+                       double *__restrict__ r, double *partials, CgScalars *S, double *hist, double rtol) {
+  if (!INIT && cg_stopped(S)) return;
+  const double alpha = INIT ? 0.0 : __ldcg(&S->alpha);
   double acc[2] = {0.0, 0.0};
   GRID_STRIDE(i, n) {
-    double ri = r[i], z = Dinv[i] * ri;
-    p[i] = z;
-    acc[0] = fma(ri, z, acc[0]);
-    acc[1] = fma(ri, ri, acc[1]);
-  }
-  if (grid_sum<2>(acc, partials, &S->counter[CNT_INIT])) {
-    S->rho = acc[0];
-    S->rr = acc[1];
-    S->thresh2 = rtol * rtol * S->bnorm2;
-    S->alpha = 0.0;
-    S->beta = 0.0;
-    if (S->bnorm2 == 0.0 || S->status != 0) S->done = 1;
-    if (!S->fixed && acc[1] <= S->thresh2) S->done = 1;
-    if (S->max_iter <= 0) S->done = 1;
-  }
-}
-
-// alpha = rho / (p . q)
-__global__ void k_pq(int64_t n, const double *__restrict__ p, const double *__restrict__ q, double *partials,
-                     CgScalars *S) {
-  if (cg_stopped(S)) return;
-  double acc[1] = {0.0};
-  GRID_STRIDE(i, n) { acc[0] = fma(p[i], q[i], acc[0]); }
-  if (grid_sum<1>(acc, partials, &S->counter[CNT_PQ])) {
-    double pq = acc[0];
-    if (!(pq > 0.0)) {
-      S->status = (pq != pq) ? -5 : -6;   // TO_ENAN / TO_EBREAKDOWN
-      S->done = 1;
-    } else {
-      S->alpha = S->rho / pq;
-    }
-  }
-}
-
-__global__ void k_u1(int64_t n, const double *__restrict__ q, const double *__restrict__ Dinv,
-                     double *__restrict__ r, double *partials, CgScalars *S, double *hist) {
-  if (cg_stopped(S)) return;
-  const double alpha = S->alpha;
-  double acc[2] = {0.0, 0.0};
-  GRID_STRIDE(i, n) {
-    double di = Dinv[i];
+    const double di = Dinv[i];
     double ri = r[i];
-    if (di != 0.0) ri = fma(-alpha, q[i], ri);
-    r[i] = ri;
+    if (!INIT) {
+      if (di != 0.0) ri = fma(-alpha, q[i], ri);
+      r[i] = ri;
+    }
     acc[0] = fma(ri, di * ri, acc[0]);
     acc[1] = fma(ri, ri, acc[1]);
   }
-  if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) {
-    double rz = acc[0], rr = acc[1];
-    int it = S->iter + 1;
-    S->iter = it;
-    if (!(rz == rz) || !(rr == rr)) {
-      S->status = -5;
-      S->done = 1;
-      return;
-    }
-    S->beta = rz / S->rho;
-    S->rho = rz;
-    S->rr = rr;
-    if (S->history && hist) hist[it - 1] = sqrt(rr / S->bnorm2);
-    if ((!S->fixed && rr <= S->thresh2) || it >= S->max_iter) S->done_next = 1;
+  if (INIT) {
+    if (grid_sum<2>(acc, partials, &S->counter[CNT_INIT])) cg_init_scalars(S, acc[0], acc[1], rtol);
+  } else {
+    if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) cg_after_rupdate(S, acc[0], acc[1], hist);
   }
 }
 
-__global__ void k_u2(int64_t n, const double *__restrict__ r, const double *__restrict__ Dinv,
-                     double *__restrict__ p, double *__restrict__ x, const CgScalars *S) {
-  if (*((volatile const int32_t *)&S->done)) return;
-  const double alpha = S->alpha, beta = S->beta;
-  GRID_STRIDE(i, n) {
-    double pi = p[i];
-    x[i] = fma(alpha, pi, x[i]);
-    p[i] = fma(beta, pi, Dinv[i] * r[i]);
-  }
+// x += alpha_last p_last after the loop (iteration iter-1 wrote pbuf[(iter-1)&1]).
+__global__ void k_xfinal(int64_t n, double *__restrict__ x, const double *__restrict__ p0,
+                         const double *__restrict__ p1, const CgScalars *S) {
+  const int it = S->iter;
+  if (it <= 0 || S->status != 0) return;
+  const double alpha = S->alpha;
+  const double *p = ((it - 1) & 1) ? p1 : p0;
+  GRID_STRIDE(i, n) { x[i] = fma(alpha, p[i], x[i]); }
 }
 
 // sum over free DOFs of (b - t)^2 -> S->tmp[0]

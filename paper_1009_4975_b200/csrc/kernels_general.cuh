@@ -203,39 +203,91 @@ __device__ __forceinline__ void wht8x3(double (&v)[24]) {
   }
 }
 
-// y = K0 x for H8 via the Hadamard factorisation (element.h).
-__device__ __forceinline__ void had_apply(const K0Had3 &H, double (&x)[24], double (&y)[24]) {
-  wht8x3(x);
+// One output of the Hadamard-basis product: yhat(m,i) = diag[i][m] xhat(m,i) +
+// sum_{j != i, bit_i(m) != bit_j(m)} off[i][j][m] xhat(m ^ e_i ^ e_j, j).
+__device__ __forceinline__ double had_mid_one(const K0Had3 &H, const double (&x)[24], int m, int i) {
+  double acc = H.diag[i][m] * x[3 * m + i];
 #pragma unroll
-  for (int m = 0; m < 8; ++m) {
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      double acc = (m == 0) ? 0.0 : H.diag[i][m] * x[3 * m + i];
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        if (j == i || ((m >> i) & 1) == ((m >> j) & 1)) continue;
-        acc = fma(H.off[i][j][m], x[3 * (m ^ ((1 << i) | (1 << j))) + j], acc);
-      }
-      y[3 * m + i] = acc;
-    }
+  for (int j = 0; j < 3; ++j) {
+    if (j == i || ((m >> i) & 1) == ((m >> j) & 1)) continue;
+    acc = fma(H.off[i][j][m], x[3 * (m ^ ((1 << i) | (1 << j))) + j], acc);
   }
-  wht8x3(y);
+  return acc;
 }
 
-// ---- operator apply, atomic scatter (v0 reference kernel) ---------------------------
+// xhat := Khat xhat in place.  The coupling (m,i) -> (m ^ e_i ^ e_j, j) splits
+// the 24 Hadamard coordinates into closed groups: two triples, six pairs,
+// three singletons (m = 7) and the rigid-translation mode m = 0, whose
+// output is zero.  Each group is evaluated from its inputs before it is
+// written back, so no second 24-vector is live (register pressure).
+__device__ __forceinline__ void had_mid_inplace(const K0Had3 &H, double (&x)[24]) {
+#define HAD_G3(m0, i0, m1, i1, m2, i2)                                                                      \
+  {                                                                                                         \
+    const double a = had_mid_one(H, x, m0, i0), b = had_mid_one(H, x, m1, i1), c = had_mid_one(H, x, m2, i2); \
+    x[3 * m0 + i0] = a;                                                                                     \
+    x[3 * m1 + i1] = b;                                                                                     \
+    x[3 * m2 + i2] = c;                                                                                     \
+  }
+#define HAD_G2(m0, i0, m1, i1)                                                   \
+  {                                                                              \
+    const double a = had_mid_one(H, x, m0, i0), b = had_mid_one(H, x, m1, i1); \
+    x[3 * m0 + i0] = a;                                                          \
+    x[3 * m1 + i1] = b;                                                          \
+  }
+  HAD_G3(1, 0, 2, 1, 4, 2)
+  HAD_G2(1, 1, 2, 0)
+  HAD_G2(1, 2, 4, 0)
+  HAD_G2(2, 2, 4, 1)
+  HAD_G3(6, 0, 5, 1, 3, 2)
+  HAD_G2(6, 1, 5, 0)
+  HAD_G2(6, 2, 3, 0)
+  HAD_G2(5, 2, 3, 1)
+#pragma unroll
+  for (int i = 0; i < 3; ++i) x[21 + i] *= H.diag[i][7];
+  x[0] = x[1] = x[2] = 0.0;
+#undef HAD_G3
+#undef HAD_G2
+}
+
+// x := K0 x for H8 via the Hadamard factorisation (element.h), in place.
+__device__ __forceinline__ void had_apply_inplace(const K0Had3 &H, double (&x)[24]) {
+  wht8x3(x);
+  had_mid_inplace(H, x);
+  wht8x3(x);
+}
+
+// y = K0 x (x is destroyed).
+__device__ __forceinline__ void had_apply(const K0Had3 &H, double (&x)[24], double (&y)[24]) {
+  had_apply_inplace(H, x);
+#pragma unroll
+  for (int a = 0; a < 24; ++a) y[a] = x[a];
+}
+
+// ---- operator apply, atomic scatter ------------------------------------------------------
+// q += C^T (s_e K0) C p per element (q zeroed by the caller).  With S (CG
+// mode): p^T A p = sum_e s_e pbar_e^T K0 pbar_e (pbar_e = C_e p, p vanishing
+// on non-free DOFs) is reduced in the same pass and the last block forms
+// alpha_k = rho_k / p^T A p, so no separate p.q pass is needed.
 template <int DIM>
 __global__ void k_matvec_atomic(MeshView M, const double *__restrict__ s, const double *__restrict__ p,
                                 double *__restrict__ q,
                                 const __grid_constant__ typename std::conditional<DIM == 2, K0Dense2, K0Dense3>::type K0,
-                                CgScalars *S) {
+                                CgScalars *S, double *partials) {
   constexpr int NC = 1 << DIM, ND = DIM * NC;
-  if (S && cg_stop_at_apply(S)) return;
+  if (S && cg_stopped(S)) return;
+  double pq = 0.0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M.n_el; e += (int64_t)gridDim.x * blockDim.x) {
     double ue[ND], ye[ND];
     int node[NC], hang[NC];
     gather_C<DIM>(M, e, p, ue, node, hang);
     dense_apply<ND>(K0.K, ue, ye);
     const double se = s[e];
+    if (S) {
+      double en = 0.0;
+#pragma unroll
+      for (int a = 0; a < ND; ++a) en = fma(ue[a], ye[a], en);
+      pq = fma(se, en, pq);
+    }
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       if (hang[c] < 0) {
@@ -249,6 +301,17 @@ __global__ void k_matvec_atomic(MeshView M, const double *__restrict__ s, const 
 #pragma unroll
           for (int i = 0; i < DIM; ++i) atomicAdd(&q[pn * DIM + i], w * ye[DIM * c + i]);
         }
+      }
+    }
+  }
+  if (S) {
+    double v[1] = {pq};
+    if (grid_sum<1>(v, partials, &S->counter[CNT_PQ])) {
+      if (!(v[0] > 0.0)) {
+        S->status = (v[0] != v[0]) ? -5 : -6;
+        S->done = 1;
+      } else {
+        S->alpha = S->rho / v[0];
       }
     }
   }

@@ -4,12 +4,24 @@
 // and the work decomposition change:
 //
 //  * CG vectors live in "internal" order: lexicographic nodes (i fastest),
-//    3 interleaved doubles per node, each node row padded to an even number
-//    of doubles (RS) so every row starts 16-byte aligned, plus zero pads in
-//    front of and behind the vector.  The canonical Morton numbering (C3) is
+//    NXP = NX rounded up to even nodes per row, 3 interleaved doubles per
+//    node (row stride RS = 3 NXP doubles, 16-byte aligned), plus zero pads
+//    in front of and behind the vector.  Node-valued arrays (the Jacobi
+//    inverse diagonal Dinv, one value per node because the 24 diagonal
+//    entries of the cube's K0 are equal and Dirichlet conditions clamp whole
+//    nodes) use the same node order.  The canonical Morton numbering (C3) is
 //    applied once per solve at the boundary (f in, u out).  Connectivity is
 //    implicit: element (i,j,k) has corner c at node (i+cx, j+cy, k+cz).
-//  * s_e lives in lexicographic element order.
+//  * One PCG iteration is two kernels (textbook Hestenes-Stiefel recurrences,
+//    PAPER.md:511-523 with reading Q3, the x update deferred by one
+//    iteration so that it rides on the operator kernel):
+//      K1 k_apply_s3<CG>  p_k = Dinv r_k + beta_{k-1} p_{k-1}   (all staged nodes)
+//                         x  += alpha_{k-1} p_{k-1}              (owned nodes)
+//                         q   = A p_k,  p_k . q -> alpha_k        (owned nodes)
+//      K2 k_rupd_s3       r  -= alpha_k q;  r.Dinv r, r.r -> beta_k, stop test
+//    and after the loop k_xfinal adds the last alpha p.  Vector traffic per
+//    iteration: K1 reads r, p_{k-1}, x (+ s, Dinv/3) and writes p_k, q, x; K2
+//    reads r, q (+ Dinv/3) and writes r: 9.67 passes instead of 12.
 //  * One CTA owns a (31 x (TYW-1)) patch of node columns and a range of node
 //    planes; it sweeps the element layers in z.  Thread (tx, ty) computes the
 //    element whose minimum corner is node (i0+tx-1, j0+ty-1) and accumulates
@@ -19,16 +31,18 @@
 //    every node is written by exactly one thread, so the result is
 //    deterministic.  The halo element row/column of each patch is recomputed
 //    instead of exchanged.
-//  * The p plane tile (33 x (TYW+1) nodes) arrives by TMA 1D bulk copies
-//    (cp.async.bulk, one 800-byte row each, issued by one thread, completion
-//    on an mbarrier), NBUF-deep so the copy of plane k+3 overlaps the
-//    compute of layer k.  The lower plane of each element is carried in
-//    registers, so each layer reads one plane from shared memory.
+//  * The r, p_{k-1} and Dinv plane tiles (33 x (TYW+1) nodes) arrive by TMA
+//    1D bulk copies (cp.async.bulk, one row each, issued by one thread,
+//    completion on an mbarrier), NBUF planes ahead of the compute.  p_k is
+//    formed from them in shared memory (two planes live), so the gather of
+//    the element corners never touches global memory.
 //  * The element product uses the Hadamard factorisation of K0 (element.h):
 //    ~215 fp64 operations instead of 576 FMAs.
 //  * p.q of the owned nodes is reduced in the same kernel (last-block-done),
 //    and the last block forms alpha = rho / p.q (CG scalars stay on device).
 #pragma once
+#include <cuda.h>
+
 #include "device_common.cuh"
 #include "element.h"
 #include "kernels_cg.cuh"
@@ -39,25 +53,37 @@ namespace tomesh {
 struct GridView {
   int EX, EY, EZ;        // elements per axis
   int NX, NY, NZ;        // nodes per axis
-  int RS;                // doubles per node row in the internal layout (even)
+  int NXP;               // nodes per internal row (NX rounded up to even)
+  int RS;                // doubles per node row in the internal layout (3 NXP)
   int ntx, nty, nzs;     // CTA tiles in x, y and z segments
   int zlen;              // node planes per z segment
 };
 
-constexpr int kS3PadFront = 16;    // doubles before / after an internal vector
-constexpr int kS3PadBack = 128;
+constexpr int kS3PadFront = 16;    // doubles (or nodes) before an internal vector
+constexpr int kS3PadBack = 128;    // doubles (or nodes) after it
 constexpr int kS3RowD = 100;       // doubles staged per node row: 33 nodes + alignment (800 B)
-constexpr int kS3NBuf = 4;
+constexpr int kS3RowN = 34;        // node values staged per row: 33 + alignment (272 B)
+constexpr int kS3NBuf = 4;         // staging depth (planes in flight ~ NBUF - 1 layers ahead)
 
 __device__ __forceinline__ int64_t s3_row(const GridView &G, int j, int k) {
   return ((int64_t)j + (int64_t)G.NY * k) * G.RS;
 }
+__device__ __forceinline__ int64_t s3_nrow(const GridView &G, int j, int k) {
+  return ((int64_t)j + (int64_t)G.NY * k) * G.NXP;
+}
+
+constexpr int s3_pad128(int doubles) { return (doubles + 15) / 16 * 16; }   // 128-byte multiple
 
 template <int TYW>
 struct S3Smem {
-  static constexpr int PY = TYW + 1;                // node rows staged
-  double plane[kS3NBuf][PY][kS3RowD];
-  double xch[TYW][6][32];                           // y-exchange: 2 planes x 3 components
+  static constexpr int PY = TYW + 1;                          // node rows staged
+  static constexpr int PD = s3_pad128(PY * kS3RowD);          // doubles per staged DOF plane
+  static constexpr int PN = s3_pad128(PY * kS3RowN);          // doubles per staged node plane
+  double r[kS3NBuf][PD];                                      // r_k (CG) or v (plain apply), TMA box
+  double po[kS3NBuf][PD];                                     // p_{k-1}, TMA box
+  double dn[kS3NBuf][PN];                                     // Dinv per node, TMA box
+  double pn[3][PY][kS3RowD];                                  // p_k ring: planes k mod 3
+  double xch[2][TYW][6][32];                                  // y-exchange (layer parity): 2 planes x 3 comps
   unsigned long long mbar[kS3NBuf];
 };
 
@@ -81,71 +107,154 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
+// 3D tiled TMA load of one box (OOB elements zero-filled; the transaction
+// count is always the full box).
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                            unsigned long long *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
-// One thread: copy the node rows of plane k (tile origin i0-1, j0-1) into buffer b.
-// Rows outside the mesh are skipped (they only feed elements outside the mesh,
-// whose s_e is 0; their stale values are finite).
-template <int TYW>
-__device__ __forceinline__ void s3_issue_plane(S3Smem<TYW> &sm, int b, const GridView &G, const double *p, int i0,
-                                               int j0, int k, int off) {
+// One thread: stage plane k (tile origin node (i0-1, j0-1)) into buffer b:
+// one TMA box per array.  Rows and columns outside the vector come back as 0.
+template <int TYW, bool CG>
+__device__ __forceinline__ void s3_issue_plane(S3Smem<TYW> &sm, int b, const CUtensorMap *ta, const CUtensorMap *tb,
+                                               const CUtensorMap *tc, int i0, int j0, int k, int off, int noff) {
   constexpr int PY = TYW + 1;
-  unsigned bytes = 0;
-  const bool kin = (k >= 0 && k < G.NZ);
-  if (kin)
-    for (int row = 0; row < PY; ++row) {
-      const int j = j0 - 1 + row;
-      if (j >= 0 && j < G.NY) bytes += kS3RowD * 8;
-    }
+  constexpr unsigned bytes = PY * kS3RowD * 8 * (CG ? 2 : 1) + (CG ? PY * kS3RowN * 8 : 0);
   fence_proxy_async();
   mbar_arrive_expect_tx(&sm.mbar[b], bytes);
-  if (kin)
-    for (int row = 0; row < PY; ++row) {
-      const int j = j0 - 1 + row;
-      if (j < 0 || j >= G.NY) continue;
-      const double *src = p + s3_row(G, j, k) + 3 * (i0 - 1) - off;
-      bulk_g2s(&sm.plane[b][row][0], src, kS3RowD * 8, &sm.mbar[b]);
-    }
+  tma_load_3d(sm.r[b], ta, 3 * (i0 - 1) - off, j0 - 1, k, &sm.mbar[b]);
+  if (CG) {
+    tma_load_3d(sm.po[b], tb, 3 * (i0 - 1) - off, j0 - 1, k, &sm.mbar[b]);
+    tma_load_3d(sm.dn[b], tc, (i0 - 1) - noff, j0 - 1, k, &sm.mbar[b]);
+  }
 }
 
-template <int TYW>
+// p_k of node (col, row) of staged plane k: CG: Dinv r + beta p_{k-1}; plain: v.
+template <int TYW, bool CG>
+__device__ __forceinline__ void s3_form_node(const S3Smem<TYW> &sm, int b, int row, int col, int off, int noff,
+                                             double beta, bool pin, double (&v)[3]) {
+  const double *rr = &sm.r[b][row * kS3RowD + off + 3 * col];
+  const double *pp = &sm.po[b][row * kS3RowD + off + 3 * col];
+  const double dv = CG ? sm.dn[b][row * kS3RowN + noff + col] : 0.0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    double t = pin ? rr[d] : 0.0;
+    if (CG && pin) t = fma(dv, t, (beta != 0.0) ? beta * pp[d] : 0.0);
+    v[d] = t;
+  }
+}
+
+// K1.  CG = true: the fused PCG operator step (see the header comment).
+// CG = false: q = C^T K C v for a v that vanishes on non-free DOFs (ta maps v;
+// tb, tc, pnew, x, S unused).
+//
+// Per CTA the layers ek = k_lo-1 .. k_hi-1 run with one barrier each:
+//   1. element ek from p planes ek, ek+1 (ring slots ek%3, (ek+1)%3) -> y-exchange write
+//   2. barrier
+//   3. y-exchange read, q and p.q of node plane ek (owned); refill the staging
+//      buffer of plane ek+2 with plane ek+2+NBUF (warp 0, one elected lane)
+//   4. wait for plane ek+3, form p of it into ring slot (ek+3)%3 (= ek%3, free
+//      since step 2); owners write p_k there and update x
+// Plane P is issued during layer P-2-NBUF, waited for during layer P-3.
+template <int TYW, bool CG>
 __global__ void __launch_bounds__(32 * TYW, 2)
-k_apply_s3(GridView G, const double *__restrict__ s, const double *__restrict__ p, double *__restrict__ q,
+k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ CUtensorMap ta,
+           const __grid_constant__ CUtensorMap tb, const __grid_constant__ CUtensorMap tc,
+           double *__restrict__ pnew, double *__restrict__ x, double *__restrict__ q,
            const __grid_constant__ K0Had3 H, CgScalars *S, double *partials) {
-  if (S && cg_stop_at_apply(S)) return;
+  if (CG && cg_stop_at_apply(S)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   S3Smem<TYW> &sm = *reinterpret_cast<S3Smem<TYW> *>(smem_raw);
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = tx + 32 * ty;
-  int b = blockIdx.x;
-  const int zs = b % G.nzs;
-  b /= G.nzs;
-  const int ty_t = b % G.nty;
-  const int tx_t = b / G.nty;
+  int bid = blockIdx.x;
+  const int zs = bid % G.nzs;
+  bid /= G.nzs;
+  const int ty_t = bid % G.nty;
+  const int tx_t = bid / G.nty;
   const int i0 = tx_t * 31, j0 = ty_t * (TYW - 1);
   const int k_lo = zs * G.zlen;
   const int k_hi = min(G.NZ, k_lo + G.zlen);
-  const int off = (i0 - 1) & 1;                         // window starts on an even double
+  const int off = (i0 - 1) & 1;                         // DOF window starts on an even double
+  const int noff = (i0 - 1) & 1;                        // node window starts on an even node
   const int ei = i0 - 1 + tx, ej = j0 - 1 + ty;        // this thread's element column / node column
   const bool col_el = (ei >= 0 && ei < G.EX && ej >= 0 && ej < G.EY);
   const bool owner = (tx >= 1 && ty >= 1 && ei < G.NX && ej < G.NY);
+  const double beta = CG ? __ldcg(&S->beta) : 0.0;
+  const double alpha_old = CG ? __ldcg(&S->alpha) : 0.0;
+  const bool xupd = CG && owner && alpha_old != 0.0;
+  const int64_t plane_d = (int64_t)G.NY * G.RS;        // doubles per node plane
 
-  // zero the staging buffers once (rows that are never copied must hold finite values)
-  for (int t = tid; t < kS3NBuf * (TYW + 1) * kS3RowD; t += 32 * TYW) (&sm.plane[0][0][0])[t] = 0.0;
-  if (tid == 0)
+  if (tid == 0) {
     for (int bb = 0; bb < kS3NBuf; ++bb) mbar_init(&sm.mbar[bb], 1);
-  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   __syncthreads();
-  // prologue: planes k_lo-1, k_lo, k_lo+1
+  auto buf_of = [&](int k) { return (k - (k_lo - 1)) % kS3NBuf; };
+  auto staged = [&](int k) { return k >= 0 && k < G.NZ && k <= k_hi; };
+  // prologue: issue planes k_lo-1 .. k_lo-2+NBUF
   if (tid == 0)
-    for (int t = 0; t < 3; ++t) s3_issue_plane<TYW>(sm, t, G, p, i0, j0, k_lo - 1 + t, off);
+    for (int k = k_lo - 1; k < k_lo - 1 + kS3NBuf; ++k)
+      if (staged(k)) s3_issue_plane<TYW, CG>(sm, buf_of(k), &ta, &tb, &tc, i0, j0, k, off, noff);
   unsigned phase = 0;                                   // parity bit per buffer
+
+  double xr[3] = {0.0, 0.0, 0.0};                       // x of the owned node of the next plane to form
+  if (xupd && k_lo < k_hi) {
+    const int64_t dof = s3_row(G, ej, k_lo) + 3 * ei;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) xr[d] = __ldcs(&x[dof + d]);
+  }
+
+  // form p of plane k into ring slot k%3.  Every thread forms its own node
+  // (tx, ty), which is the node it owns (if it owns one); the 41 halo nodes of
+  // column 32 and row TYW are spread over lanes 0-5 of all warps so that every
+  // warp does at most two rounds.
+  const int xe = tx * TYW + ty;                         // this thread's extra halo node, if < 33 + TYW
+  const int xe_row = xe < 33 ? TYW : xe - 33, xe_col = xe < 33 ? xe : 32;
+  auto form_plane = [&](int k) {
+    const bool pin = k >= 0 && k < G.NZ;
+    const int bb = buf_of(k);
+    if (pin) {
+      mbar_wait(&sm.mbar[bb], (phase >> bb) & 1);
+      phase ^= 1u << bb;
+    }
+    double(*dst)[kS3RowD] = sm.pn[(k + 3) % 3];
+    double v[3];
+    s3_form_node<TYW, CG>(sm, bb, ty, tx, off, noff, beta, pin, v);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) dst[ty][off + 3 * tx + d] = v[d];
+    if (CG && owner && k >= k_lo && k < k_hi) {
+      const int64_t dof = s3_row(G, ej, k) + 3 * ei;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) __stcs(&pnew[dof + d], v[d]);
+      if (xupd) {
+        const double *pp = &sm.po[bb][ty * kS3RowD + off + 3 * tx];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) __stcs(&x[dof + d], fma(alpha_old, pp[d], xr[d]));
+        if (k + 1 < k_hi) {
+#pragma unroll
+          for (int d = 0; d < 3; ++d) xr[d] = __ldcs(&x[dof + plane_d + d]);
+        }
+      }
+    }
+    if (xe < 33 + TYW) {
+      s3_form_node<TYW, CG>(sm, bb, xe_row, xe_col, off, noff, beta, pin, v);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) dst[xe_row][off + 3 * xe_col + d] = v[d];
+    }
+  };
+  for (int k = k_lo - 1; k <= min(k_lo + 1, k_hi); ++k) form_plane(k);
+  __syncthreads();
+  // the buffers of planes k_lo-1 and k_lo are free again
+  if (tid == 0)
+    for (int k = k_lo - 1 + kS3NBuf; k <= k_lo + kS3NBuf; ++k)
+      if (staged(k)) s3_issue_plane<TYW, CG>(sm, buf_of(k), &ta, &tb, &tc, i0, j0, k, off, noff);
 
   double pq = 0.0;
   double acc_cur[3] = {0.0, 0.0, 0.0};                  // node plane ek (owned column)
@@ -158,22 +267,16 @@ k_apply_s3(GridView G, const double *__restrict__ s, const double *__restrict__ 
   }
 
   for (int ek = k_lo - 1; ek < k_hi; ++ek) {
-    const int bo = (ek - (k_lo - 1)) % kS3NBuf;         // buffer of plane ek
-    const int bn = (bo + 1) % kS3NBuf;                  // buffer of plane ek+1
-    // keep the copy engine NBUF-1 planes ahead: plane ek+3 into the buffer of plane ek-1
-    if (tid == 0 && ek + 3 <= k_hi) s3_issue_plane<TYW>(sm, (bo + 3) % kS3NBuf, G, p, i0, j0, ek + 3, off);
-    if (ek == k_lo - 1) {
-      mbar_wait(&sm.mbar[bo], (phase >> bo) & 1);
-      phase ^= 1u << bo;
-    }
-    mbar_wait(&sm.mbar[bn], (phase >> bn) & 1);
-    phase ^= 1u << bn;
     const double se = s_next;
     s_idx += s_stride;
     {
       const int ekn = ek + 1;
       s_next = (col_el && ekn >= 0 && ekn < G.EZ && ekn < k_hi) ? __ldg(&s[s_idx]) : 0.0;
     }
+    const int slo = (ek + 3) % 3, shi = (ek + 4) % 3;
+    double p_own[3];                                    // p_k at the owned node of plane ek
+#pragma unroll
+    for (int d = 0; d < 3; ++d) p_own[d] = sm.pn[slo][ty][off + 3 * tx + d];
     const bool el = col_el && ek >= 0 && ek < G.EZ;
     double y[24];
     if (el) {
@@ -181,13 +284,13 @@ k_apply_s3(GridView G, const double *__restrict__ s, const double *__restrict__ 
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
-        const double *row = &sm.plane[cz ? bn : bo][ty + cy][off + 3 * (tx + cx)];
+        const double *row = &sm.pn[cz ? shi : slo][ty + cy][off + 3 * (tx + cx)];
 #pragma unroll
         for (int d = 0; d < 3; ++d) xv[3 * c + d] = row[d];
       }
-      had_apply(H, xv, y);
+      had_apply_inplace(H, xv);
 #pragma unroll
-      for (int a = 0; a < 24; ++a) y[a] *= se;
+      for (int a = 0; a < 24; ++a) y[a] = xv[a] * se;
     } else {
 #pragma unroll
       for (int a = 0; a < 24; ++a) y[a] = 0.0;
@@ -208,13 +311,15 @@ k_apply_s3(GridView G, const double *__restrict__ s, const double *__restrict__ 
 #pragma unroll
     for (int cz = 0; cz < 2; ++cz)
 #pragma unroll
-      for (int d = 0; d < 3; ++d) sm.xch[ty][3 * cz + d][tx] = a_row[1][cz][d];
-    __syncthreads();
+      for (int d = 0; d < 3; ++d) sm.xch[ek & 1][ty][3 * cz + d][tx] = a_row[1][cz][d];
+    __syncthreads();                                    // the one barrier of the layer
+    if (tid == 0 && staged(ek + 2 + kS3NBuf))
+      s3_issue_plane<TYW, CG>(sm, buf_of(ek + 2 + kS3NBuf), &ta, &tb, &tc, i0, j0, ek + 2 + kS3NBuf, off, noff);
     double tot[2][3];
 #pragma unroll
     for (int cz = 0; cz < 2; ++cz)
 #pragma unroll
-      for (int d = 0; d < 3; ++d) tot[cz][d] = a_row[0][cz][d] + (ty > 0 ? sm.xch[ty - 1][3 * cz + d][tx] : 0.0);
+      for (int d = 0; d < 3; ++d) tot[cz][d] = a_row[0][cz][d] + (ty > 0 ? sm.xch[ek & 1][ty - 1][3 * cz + d][tx] : 0.0);
     // node plane ek is complete: cz=1 part of layer ek-1 (acc_cur) + cz=0 part of layer ek
     if (ek >= k_lo && owner) {
       const int64_t dof = s3_row(G, ej, ek) + 3 * ei;
@@ -222,13 +327,14 @@ k_apply_s3(GridView G, const double *__restrict__ s, const double *__restrict__ 
       for (int d = 0; d < 3; ++d) {
         const double qv = acc_cur[d] + tot[0][d];
         q[dof + d] = qv;
-        pq = fma(sm.plane[bo][ty][off + 3 * tx + d], qv, pq);
+        if (CG) pq = fma(p_own[d], qv, pq);
       }
     }
 #pragma unroll
     for (int d = 0; d < 3; ++d) acc_cur[d] = tot[1][d];
+    if (ek + 3 <= k_hi) form_plane(ek + 3);
   }
-  if (S) {
+  if (CG) {
     double v[1] = {pq};
     if (grid_sum<1>(v, partials, &S->counter[CNT_PQ])) {
       if (!(v[0] > 0.0)) {
@@ -238,6 +344,60 @@ k_apply_s3(GridView G, const double *__restrict__ s, const double *__restrict__ 
         S->alpha = S->rho / v[0];
       }
     }
+  }
+}
+
+// ---- vector kernels of the structured path -----------------------------------------------
+// Coalesced double2 streams over the internal vector; Dinv is gathered per
+// node (node = DOF / 3, an L1 hit: a warp's 64 doubles of r span 22 nodes).
+
+// K2: r -= alpha q on free nodes; rho' = r.Dinv r, rr = r.r -> beta, stop test.
+// INIT: no update (r = r0); rho0, rr0 and the thresholds.
+template <bool INIT>
+__global__ void __launch_bounds__(256) k_rupd_s3(int64_t n, const double *__restrict__ q, const double *__restrict__ dn,
+                          double *__restrict__ r, double *partials, CgScalars *S, double *hist, double rtol) {
+  if (!INIT && cg_stopped(S)) return;
+  constexpr int U = 4;
+  const double alpha = INIT ? 0.0 : __ldcg(&S->alpha);
+  double acc[2] = {0.0, 0.0};
+  const int64_t n2 = n >> 1;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  double2 *r2 = reinterpret_cast<double2 *>(r);
+  const double2 *q2 = reinterpret_cast<const double2 *>(q);
+  for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < n2; j0 += U * T) {
+    double2 rv[U], qv[U];
+    double d0[U], d1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + u * T;
+      if (j < n2) {
+        rv[u] = __ldcs(&r2[j]);
+        qv[u] = INIT ? make_double2(0.0, 0.0) : __ldcs(&q2[j]);
+        d0[u] = __ldg(&dn[(2 * j) / 3]);
+        d1[u] = __ldg(&dn[(2 * j + 1) / 3]);
+      } else {
+        rv[u] = qv[u] = make_double2(0.0, 0.0);
+        d0[u] = d1[u] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + u * T;
+      if (!INIT) {
+        if (d0[u] != 0.0) rv[u].x = fma(-alpha, qv[u].x, rv[u].x);
+        if (d1[u] != 0.0) rv[u].y = fma(-alpha, qv[u].y, rv[u].y);
+        if (j < n2) __stcs(&r2[j], rv[u]);
+      }
+      acc[0] = fma(rv[u].x, d0[u] * rv[u].x, acc[0]);
+      acc[0] = fma(rv[u].y, d1[u] * rv[u].y, acc[0]);
+      acc[1] = fma(rv[u].x, rv[u].x, acc[1]);
+      acc[1] = fma(rv[u].y, rv[u].y, acc[1]);
+    }
+  }
+  if (INIT) {
+    if (grid_sum<2>(acc, partials, &S->counter[CNT_INIT])) cg_init_scalars(S, acc[0], acc[1], rtol);
+  } else {
+    if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) cg_after_rupdate(S, acc[0], acc[1], hist);
   }
 }
 
@@ -255,9 +415,10 @@ __global__ void k_simp_s3(int64_t n, const double *__restrict__ x, const int32_t
 }
 
 // D = K0_diag * sum of s over the <= 8 elements around each node (all 24
-// diagonal entries of the cube's K0 are equal); Dinv = free ? 1/D : 0.
-__global__ void k_diag_s3(GridView G, const double *__restrict__ s_lex, const uint8_t *__restrict__ free_int,
-                          double k0d, double *__restrict__ Dinv, double *__restrict__ d_out, CgScalars *S) {
+// diagonal entries of the cube's K0 are equal); Dinv = free ? 1/D : 0 per
+// node; d_out (optional, per DOF) = diag(A) with 1 on non-free DOFs.
+__global__ void k_diag_s3(GridView G, const double *__restrict__ s_lex, const uint8_t *__restrict__ free_node,
+                          double k0d, double *__restrict__ dn, double *__restrict__ d_out, CgScalars *S) {
   const int64_t nn = (int64_t)G.NX * G.NY * G.NZ;
   GRID_STRIDE(n, nn) {
     int i = (int)(n % G.NX);
@@ -272,18 +433,14 @@ __global__ void k_diag_s3(GridView G, const double *__restrict__ s_lex, const ui
         acc += s_lex[(int64_t)ei + (int64_t)G.EX * ((int64_t)ej + (int64_t)G.EY * ek)];
     }
     const double d = k0d * acc;
-    const int64_t base = s3_row(G, j, k) + 3 * i;
+    const int64_t node = s3_nrow(G, j, k) + i;
+    const bool fr = free_node[node] != 0;
+    if (fr && !(d > 0.0)) S->status = -7;
+    if (dn) dn[node] = fr ? 1.0 / d : 0.0;
+    if (d_out) {
+      const int64_t base = s3_row(G, j, k) + 3 * i;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const int64_t dof = base + c;
-      if (free_int[dof]) {
-        if (!(d > 0.0)) S->status = -7;
-        if (Dinv) Dinv[dof] = 1.0 / d;
-        if (d_out) d_out[dof] = d;
-      } else {
-        if (Dinv) Dinv[dof] = 0.0;
-        if (d_out) d_out[dof] = 1.0;
-      }
+      for (int c = 0; c < 3; ++c) d_out[base + c] = fr ? d : 1.0;
     }
   }
 }

@@ -1,9 +1,12 @@
 // libtomesh — C ABI entry points (include/tomesh.h) and the host side of the
 // device path: validation, upload, the PCG driver loop, sensitivities, filter.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -47,7 +50,9 @@ struct to_mesh {
   int64_t *filt_ptr = nullptr;
   int32_t *filt_idx = nullptr;
   // workspace
-  double *s = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *dinv = nullptr, *D = nullptr;
+  double *s = nullptr, *x = nullptr, *r = nullptr, *q = nullptr, *dinv = nullptr, *D = nullptr;
+  double *pb[2] = {nullptr, nullptr};   // p ping-pong: iteration k writes pb[k & 1]
+  double *dn = nullptr;                 // structured: Dinv per node (internal node order)
   double *partials = nullptr, *hist = nullptr;
   int32_t hist_len = 0, hist_cap = 0;
   CgScalars *S = nullptr;
@@ -60,8 +65,13 @@ struct to_mesh {
   bool structured = false, force_general = false;
   GridView G{};
   int32_t *perm_el = nullptr, *perm_node = nullptr;
-  uint8_t *free_lex = nullptr;
+  uint8_t *free_lex = nullptr;         // per DOF, internal order
+  uint8_t *free_node_lex = nullptr;    // per node, internal order
+  int64_t n_int_nodes = 0;
   double k0d = 0.0, h_struct = 1.0;
+  // TMA tensor maps of the internal vectors (structured path): [NZ][NY][RS] doubles
+  // (boxes of TYW+1 rows x 100 doubles) and the node array Dinv [NZ][NY][NXP].
+  CUtensorMap tm_r, tm_x, tm_pb[2], tm_dn;
   int last_launches = 0;
   int matvec_variant = 0;
   std::vector<cudaEvent_t> prof_ev;   // TO_PROFILE: 5 events per iteration
@@ -211,6 +221,36 @@ int upload_array(to_mesh *m, T **dst, const T *src, size_t count, cudaStream_t s
   return 0;
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+// 3D fp64 tensor map over [d2][d1][d0] with a (b0 x b1 x 1) box; OOB reads are 0.
+int make_tensor_map(CUtensorMap *map, const double *base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0,
+                    uint32_t b1) {
+  auto enc = tensor_map_encoder();
+  if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return TO_ECUDA; }
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {d0 * 8, d0 * d1 * 8};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)base, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d)", (int)r); return TO_ECUDA; }
+  return 0;
+}
+
 // Uniform 3D meshes (one level, leaves tiling a box, no hanging nodes) use the
 // structured fast path: lexicographic internal vectors, implicit connectivity.
 int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof, cudaStream_t st, to_mesh *m) {
@@ -229,7 +269,8 @@ int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof
   GridView G;
   G.EX = (int)ext[0]; G.EY = (int)ext[1]; G.EZ = (int)ext[2];
   G.NX = G.EX + 1; G.NY = G.EY + 1; G.NZ = G.EZ + 1;
-  G.RS = 3 * G.NX + ((3 * G.NX) & 1);     // even row stride: every node row 16-byte aligned
+  G.NXP = G.NX + (G.NX & 1);              // even node count per row: node pairs never straddle rows
+  G.RS = 3 * G.NXP;                       // every node row 16-byte aligned
   if ((int64_t)G.RS * G.NY * G.NZ >= (1LL << 31) - kS3PadBack) return 0;
   G.ntx = (G.NX + 30) / 31;
   G.nty = (G.NY + kS3TYW - 2) / (kS3TYW - 1);
@@ -251,6 +292,9 @@ int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof
   // all 24 diagonal entries of the cube's K0 are equal (symmetry); Dinv uses one
   for (int a = 1; a < 24; ++a)
     if (std::fabs(m->K3.K[a * 24 + a] - m->K3.K[0]) > 1e-14 * std::fabs(m->K3.K[0])) return 0;
+  // Dirichlet conditions must clamp whole nodes (one Dinv per node)
+  for (int64_t n = 0; n < d->n_node; ++n)
+    if (free_dof[n * 3] != free_dof[n * 3 + 1] || free_dof[n * 3] != free_dof[n * 3 + 2]) return 0;
   std::vector<int32_t> perm_el(d->n_elem), perm_node(d->n_node, -1);
   for (int64_t e = 0; e < d->n_elem; ++e) {
     const int32_t *a = d->elem_anchor + e * 3;
@@ -262,14 +306,24 @@ int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof
     }
   }
   m->n_int = (int64_t)G.RS * G.NY * G.NZ;
-  std::vector<uint8_t> free_lex(m->n_int, 0);
+  m->n_int_nodes = (int64_t)G.NXP * G.NY * G.NZ;
+  std::vector<uint8_t> free_lex(m->n_int, 0), free_node(m->n_int_nodes, 0);
   for (int64_t n = 0; n < d->n_node; ++n) {
     if (perm_node[n] < 0) return 0;
     for (int c = 0; c < 3; ++c) free_lex[(int64_t)perm_node[n] + c] = free_dof[n * 3 + c];
+    free_node[perm_node[n] / 3] = free_dof[n * 3];
   }
   RC(upload_array(m, &m->perm_el, perm_el.data(), perm_el.size(), st));
   RC(upload_array(m, &m->perm_node, perm_node.data(), perm_node.size(), st));
   RC(upload_array(m, &m->free_lex, free_lex.data(), free_lex.size(), st));
+  RC(upload_array(m, &m->free_node_lex, free_node.data(), free_node.size(), st));
+  {
+    double *base = nullptr;
+    const size_t cnt = (size_t)(m->n_int_nodes + kS3PadFront + kS3PadBack);
+    RC(m->alloc(&base, cnt));
+    CK(cudaMemsetAsync(base, 0, sizeof(double) * cnt, st));
+    m->dn = base + kS3PadFront;
+  }
   const int64_t grid = (int64_t)G.ntx * G.nty * G.nzs;
   if (grid > kMaxPartialBlocks) RC(m->alloc(&m->partials, (size_t)grid * 4));
   m->G = G;
@@ -278,7 +332,8 @@ int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof
   m->structured = true;
   m->matvec_variant = 1;
   const size_t smem = sizeof(S3Smem<kS3TYW>);
-  CK(cudaFuncSetAttribute(k_apply_s3<kS3TYW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(k_apply_s3<kS3TYW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(k_apply_s3<kS3TYW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   return 0;
 }
 
@@ -356,15 +411,26 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
   build_K0(3, d->nu, m->K3.K);
   if (build_K0_hadamard(d->nu, &m->KH) != 0) { set_error("Hadamard factorisation check failed"); return TO_EINVAL; }
   m->n_int = m->n_dof;
+  // diagnostics: TOMESH_FORCE_GENERAL=1 keeps uniform H8 meshes on the general path
+  m->force_general = std::getenv("TOMESH_FORCE_GENERAL") != nullptr;
   RC(setup_structured(d, free_dof, st, m));
   // workspace: internal-order vectors with zero pads on both sides (the
   // structured kernels read whole aligned row windows)
   RC(m->alloc(&m->s, m->n_el));
-  for (double **v : {&m->x, &m->r, &m->p, &m->q, &m->dinv, &m->D}) {
+  for (double **v : {&m->x, &m->r, &m->pb[0], &m->pb[1], &m->q, &m->dinv, &m->D}) {
     double *base = nullptr;
     RC(m->alloc(&base, (size_t)(m->n_int + kS3PadFront + kS3PadBack)));
     CK(cudaMemsetAsync(base, 0, sizeof(double) * (m->n_int + kS3PadFront + kS3PadBack), st));
     *v = base + kS3PadFront;
+  }
+  if (m->structured) {
+    const GridView &G = m->G;
+    const uint32_t PY = kS3TYW + 1;
+    RC(make_tensor_map(&m->tm_r, m->r, G.RS, G.NY, G.NZ, kS3RowD, PY));
+    RC(make_tensor_map(&m->tm_x, m->x, G.RS, G.NY, G.NZ, kS3RowD, PY));
+    RC(make_tensor_map(&m->tm_pb[0], m->pb[0], G.RS, G.NY, G.NZ, kS3RowD, PY));
+    RC(make_tensor_map(&m->tm_pb[1], m->pb[1], G.RS, G.NY, G.NZ, kS3RowD, PY));
+    RC(make_tensor_map(&m->tm_dn, m->dn, G.NXP, G.NY, G.NZ, kS3RowN, PY));
   }
   CK(cudaStreamSynchronize(st));
   return 0;
@@ -402,12 +468,12 @@ int launch_rhs(to_mesh *m, double *b, cudaStream_t st) {
 }
 
 // q = C^T K C p for p vanishing on non-free DOFs (values on non-free DOFs of q
-// are not meaningful; callers mask).  S == nullptr: unconditional.
-int launch_matvec(to_mesh *m, const double *p, double *q, CgScalars *S, cudaStream_t st) {
+// are not meaningful; callers mask).  Plain apply (no CG scalars).
+int launch_matvec(to_mesh *m, const double *p, double *q, cudaStream_t st) {
   CK(cudaMemsetAsync(q, 0, sizeof(double) * m->n_dof, st));
   int g = grid_for(m->n_el, kBlock, 16);
-  if (m->dim == 2) k_matvec_atomic<2><<<g, kBlock, 0, st>>>(m->view(), m->s, p, q, m->K2, S);
-  else k_matvec_atomic<3><<<g, kBlock, 0, st>>>(m->view(), m->s, p, q, m->K3, S);
+  if (m->dim == 2) k_matvec_atomic<2><<<g, kBlock, 0, st>>>(m->view(), m->s, p, q, m->K2, nullptr, nullptr);
+  else k_matvec_atomic<3><<<g, kBlock, 0, st>>>(m->view(), m->s, p, q, m->K3, nullptr, nullptr);
   m->last_launches++;
   return check_launch();
 }
@@ -451,7 +517,7 @@ int op_scale_and_diag(to_mesh *m, double penal, const double *x, double *d_int, 
   }
   k_simp_s3<<<grid_for(m->n_el), kBlock, 0, st>>>(m->n_el, x, m->perm_el, penal, m->E0, m->Emin, m->h_struct,
                                                    m->s, m->S);
-  k_diag_s3<<<grid_for(m->n_node), kBlock, 0, st>>>(m->G, m->s, m->free_lex, m->k0d, m->dinv, d_int, m->S);
+  k_diag_s3<<<grid_for(m->n_node), kBlock, 0, st>>>(m->G, m->s, m->free_node_lex, m->k0d, m->dn, d_int, m->S);
   m->last_launches += 2;
   return check_launch();
 }
@@ -464,23 +530,53 @@ int op_rhs(to_mesh *m, double *b_int, cudaStream_t st) {
   return check_launch();
 }
 
-// out = C^T K C in (in vanishing on non-free DOFs).  With S: CG mode (stop
-// check, alpha = rho / in.out on the device).
-int op_apply(to_mesh *m, const double *in, double *out, CgScalars *S, cudaStream_t st) {
-  if (!m->structured) {
-    RC(launch_matvec(m, in, out, S, st));
-    if (S) {
-      k_pq<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, in, out, m->partials, S);
-      m->last_launches++;
-    }
-    return check_launch();
-  }
-  const GridView &G = m->G;
+int s3_grid(const to_mesh *m) { return m->G.ntx * m->G.nty * m->G.nzs; }
+
+// out = C^T K C in (in vanishing on non-free DOFs), plain apply.  Structured:
+// `in` must be one of the handle's TMA-mapped vectors (x or pb[0]).
+int op_apply(to_mesh *m, const double *in, double *out, cudaStream_t st) {
+  if (!m->structured) return launch_matvec(m, in, out, st);
+  const CUtensorMap *tin = in == m->x ? &m->tm_x : in == m->pb[0] ? &m->tm_pb[0] : in == m->r ? &m->tm_r : nullptr;
+  if (!tin) { set_error("internal: unmapped apply input"); return TO_EINVAL; }
   dim3 block(32, kS3TYW);
-  int grid = G.ntx * G.nty * G.nzs;
-  k_apply_s3<kS3TYW><<<grid, block, sizeof(S3Smem<kS3TYW>), st>>>(G, m->s, in, out, m->KH, S, m->partials);
+  k_apply_s3<kS3TYW, false><<<s3_grid(m), block, sizeof(S3Smem<kS3TYW>), st>>>(
+      m->G, m->s, *tin, *tin, m->tm_dn, nullptr, nullptr, out, m->KH, nullptr, nullptr);
   m->last_launches++;
   return check_launch();
+}
+
+// K1 of CG iteration k: p_k into pb[k & 1] from pb[(k+1) & 1], deferred x
+// update, q = A p_k, alpha_k.
+int op_cg_k1(to_mesh *m, int k, cudaStream_t st) {
+  const double *po = m->pb[(k + 1) & 1];
+  double *pn = m->pb[k & 1];
+  if (!m->structured) {
+    k_pre_g<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->r, m->dinv, po, pn, m->x, m->q, m->S);
+    int g = grid_for(m->n_el, kBlock, 16);
+    if (m->dim == 2) k_matvec_atomic<2><<<g, kBlock, 0, st>>>(m->view(), m->s, pn, m->q, m->K2, m->S, m->partials);
+    else k_matvec_atomic<3><<<g, kBlock, 0, st>>>(m->view(), m->s, pn, m->q, m->K3, m->S, m->partials);
+    m->last_launches += 2;
+    return 0;
+  }
+  dim3 block(32, kS3TYW);
+  k_apply_s3<kS3TYW, true><<<s3_grid(m), block, sizeof(S3Smem<kS3TYW>), st>>>(
+      m->G, m->s, m->tm_r, m->tm_pb[(k + 1) & 1], m->tm_dn, pn, m->x, m->q, m->KH, m->S, m->partials);
+  m->last_launches++;
+  return 0;
+}
+
+// K2 (INIT: rho0, rr0 and thresholds only).
+template <bool INIT>
+int op_cg_k2(to_mesh *m, double rtol, cudaStream_t st) {
+  if (!m->structured) {
+    k_rupd<INIT><<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->q, m->dinv, m->r, m->partials, m->S, m->hist,
+                                                        rtol);
+  } else {
+    k_rupd_s3<INIT><<<grid_for(m->n_int / 8), kBlock, 0, st>>>(m->n_int, m->q, m->dn, m->r, m->partials, m->S,
+                                                                m->hist, rtol);
+  }
+  m->last_launches++;
+  return 0;
 }
 
 // dst = Pi_F u (canonical -> internal), used for warm starts
@@ -522,19 +618,18 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   m->last_launches++;
   if (warm) {
     RC(op_masked_in(m, u_dev, m->x, st));
-    RC(op_apply(m, m->x, m->q, nullptr, st));
-    k_sub_masked<<<gv, kBlock, 0, st>>>(n, m->q, m->dinv, m->r);
+    RC(op_apply(m, m->x, m->q, st));
+    k_sub_masked<<<gv, kBlock, 0, st>>>(n, m->q, free_int(m), m->r);
     m->last_launches++;
   } else {
     CK(cudaMemsetAsync(m->x, 0, sizeof(double) * n, st));
   }
-  k_init<<<gv, kBlock, 0, st>>>(n, m->r, m->dinv, m->p, m->partials, m->S, rtol);
-  m->last_launches++;
+  RC(op_cg_k2<true>(m, rtol, st));
   RC(check_launch());
 
   const bool prof = (flags & TO_PROFILE) != 0;
   if (prof) {
-    size_t need = (size_t)4 * std::max(1, max_iter);
+    size_t need = (size_t)3 * std::max(1, max_iter);
     while (m->prof_ev.size() < need) {
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
@@ -548,15 +643,12 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   while (!stop && launched < max_iter) {
     int cnt = std::min(chunk, max_iter - launched);
     for (int k = 0; k < cnt; ++k) {
-      cudaEvent_t *E = prof ? &m->prof_ev[(size_t)4 * (launched + k)] : nullptr;
+      cudaEvent_t *E = prof ? &m->prof_ev[(size_t)3 * (launched + k)] : nullptr;
       if (prof) CK(cudaEventRecord(E[0], st));
-      RC(op_apply(m, m->p, m->q, m->S, st));
+      RC(op_cg_k1(m, launched + k, st));
       if (prof) CK(cudaEventRecord(E[1], st));
-      k_u1<<<gv, kBlock, 0, st>>>(n, m->q, m->dinv, m->r, m->partials, m->S, m->hist);
+      RC(op_cg_k2<false>(m, rtol, st));
       if (prof) CK(cudaEventRecord(E[2], st));
-      k_u2<<<gv, kBlock, 0, st>>>(n, m->r, m->dinv, m->p, m->x, m->S);
-      if (prof) CK(cudaEventRecord(E[3], st));
-      m->last_launches += 2;
     }
     RC(check_launch());
     launched += cnt;
@@ -566,16 +658,19 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
       chunk = std::min(chunk * 2, 256);
     }
   }
+  k_xfinal<<<gv, kBlock, 0, st>>>(n, m->x, m->pb[0], m->pb[1], m->S);
+  m->last_launches++;
+  RC(check_launch());
   RC(read_scalars(m, st));
   CgScalars res = *m->S_host;
   if (prof) {
     for (int j = 0; j < 5; ++j) m->prof_ms[j] = 0.0;
     int nit = std::min(launched, res.iter);
     for (int it = 0; it < nit; ++it) {
-      const int slot[3] = {0, 2, 3};   // apply(+alpha), r update, x/p update
-      for (int j = 0; j < 3; ++j) {
+      const int slot[2] = {0, 2};   // K1 (p/x update + apply + alpha), K2 (r update + reductions)
+      for (int j = 0; j < 2; ++j) {
         float t = 0.f;
-        CK(cudaEventElapsedTime(&t, m->prof_ev[(size_t)4 * it + j], m->prof_ev[(size_t)4 * it + j + 1]));
+        CK(cudaEventElapsedTime(&t, m->prof_ev[(size_t)3 * it + j], m->prof_ev[(size_t)3 * it + j + 1]));
         m->prof_ms[slot[j]] += t;
       }
     }
@@ -584,8 +679,8 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   double relres_true = -1.0;
   if (!(flags & TO_NO_TRUE_RES) && res.status == 0) {
     RC(op_rhs(m, m->r, st));                      // r := b
-    RC(op_apply(m, m->x, m->p, nullptr, st));     // p := C^T K C x
-    k_resid2<<<gv, kBlock, 0, st>>>(n, m->r, m->p, free_int(m), m->partials, m->S);
+    RC(op_apply(m, m->x, m->q, st));              // q := C^T K C x
+    k_resid2<<<gv, kBlock, 0, st>>>(n, m->r, m->q, free_int(m), m->partials, m->S);
     m->last_launches++;
     RC(read_scalars(m, st));
     relres_true = res.bnorm2 > 0.0 ? std::sqrt(m->S_host->tmp[0] / res.bnorm2) : 0.0;
@@ -652,7 +747,10 @@ extern "C" int tomesh_get_info(const to_mesh *m, to_mesh_info *info) {
   if (!m || !info) { set_error("NULL argument"); return TO_EINVAL; }
   std::memset(info, 0, sizeof(*info));
   info->dim = m->dim;
-  info->structured = 0;
+  info->structured = m->structured ? 1 : 0;
+  info->grid[0] = m->structured ? m->G.EX : 0;
+  info->grid[1] = m->structured ? m->G.EY : 0;
+  info->grid[2] = m->structured ? m->G.EZ : 0;
   info->n_elem = m->n_el;
   info->n_node = m->n_node;
   info->n_dof = m->n_dof;
@@ -738,12 +836,12 @@ extern "C" int to_apply_A(to_mesh *m, double penal, const double *x_dev, const d
   RC(op_scale_and_diag(m, penal, x_dev, nullptr, st));
   int gv = grid_for(m->n_dof);
   if (!m->structured) {
-    k_mask_free<<<gv, kBlock, 0, st>>>(m->n_dof, m->free_dof, v_dev, m->p);
-    RC(op_apply(m, m->p, q_dev, nullptr, st));
+    k_mask_free<<<gv, kBlock, 0, st>>>(m->n_dof, m->free_dof, v_dev, m->pb[0]);
+    RC(op_apply(m, m->pb[0], q_dev, st));
   } else {
-    RC(op_masked_in(m, v_dev, m->p, st));           // Pi_F v, internal order
-    RC(op_apply(m, m->p, m->q, nullptr, st));
-    RC(op_recover_out(m, m->q, q_dev, st));         // back to canonical order
+    RC(op_masked_in(m, v_dev, m->pb[0], st));        // Pi_F v, internal order
+    RC(op_apply(m, m->pb[0], m->q, st));
+    RC(op_recover_out(m, m->q, q_dev, st));          // back to canonical order
   }
   k_fix_nonfree<<<gv, kBlock, 0, st>>>(m->n_dof, m->free_dof, v_dev, q_dev);
   return check_launch();

@@ -2,6 +2,8 @@
 seeded inputs.  Tolerances: L1 operator outputs 1e-12
 relative L2 (fp64 rounding of a few hundred terms), converged u, compliance,
 dc and filtered dc 1e-8 relative L2 (north_star), certificate <= 10 rtol."""
+import os
+
 import numpy as np
 import pytest
 
@@ -20,6 +22,8 @@ CASES = {
     "c3s": lambda: config("c3", nx=16, ny=8, nz=8),
     "c4s": lambda: config("c4", base=(12, 6, 6), L=2, n_gauss=60),
     "c5s": lambda: config("c5", nx=20, ny=10, nz=10),
+    "c5s_general": lambda: config("c5", nx=20, ny=10, nz=10),     # uniform H8 forced onto the general path
+    "c3s_ragged": lambda: config("c3", nx=37, ny=9, nz=13),       # several CTA tiles + ragged tails in x, y, z
     "amr2d": lambda: cantilever2d((5, 3), L=3, leaves=refine_some(2, (5, 3), 3, [(1, 1), (3, 0)]), rmin=0.3),
     "amr3d": lambda: cantilever3d((3, 2, 2), L=2, leaves=refine_some(3, (3, 2, 2), 2, [(1, 1, 0)]), rmin=0.4),
 }
@@ -31,7 +35,14 @@ def _setup(name):
     if name not in _cache:
         prob = CASES[name]()
         om = omesh.build_mesh(prob)
-        hm, m = product_mesh(prob)
+        if name.endswith("_general"):
+            os.environ["TOMESH_FORCE_GENERAL"] = "1"
+        try:
+            hm, m = product_mesh(prob)
+        finally:
+            os.environ.pop("TOMESH_FORCE_GENERAL", None)
+        if name.startswith(("c3s", "c5s")):
+            assert m.info()["structured"] == (0 if name.endswith("_general") else 1)
         x_dev = product_input_density(prob, hm, m)
         _cache[name] = (prob, om, hm, m, x_dev)
     return _cache[name]
