@@ -91,6 +91,35 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def kernel_bytes(dim, n_el, n_node, n_dof, structured):
+    """Algorithmic bytes per launch of the two PCG kernels.
+
+    K1 (structured): s (8/elem) + Dinv (8/node) + read r, p_{k-1}, x and write
+    p_k, q, x (6 x 8/DOF).  General path: the elementwise pre-pass (read r,
+    Dinv, p, x; write p, x, q: 7 x 8/DOF) + the operator (s + connectivity per
+    element, gather of p, scatter of q: 2 x 8/DOF).
+    K2: read r, q, write r (3 x 8/DOF) + Dinv (8/node structured, 8/DOF general)."""
+    nc = 1 << dim
+    if structured:
+        k1 = 8 * n_el + 8 * n_node + 48 * n_dof
+        k2 = 24 * n_dof + 8 * n_node
+    else:
+        k1 = 56 * n_dof + n_el * (8 + 4 * nc) + 16 * n_dof
+        k2 = 32 * n_dof
+    return {"k1": k1, "k2": k2}
+
+
+def max_over_ranks(value, ws, device=None):
+    """Max of a per-rank float over all ranks (identity when ws == 1)."""
+    if ws <= 1:
+        return float(value)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -223,12 +252,7 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     barrier()
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        import torch.distributed as dist
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms = float(ms_t.item())
+    ms = max_over_ranks(e0.elapsed_time(e1), ws, dev)
     ms_per_step = ms / args.steps
     value = ws * iters * args.steps / (ms / 1000.0)
 
@@ -257,28 +281,23 @@ def run_ours(args):
             dcf_host.copy_(dcf, non_blocking=True)
     e3.record(stream)
     torch.cuda.synchronize(dev)
-    e2e_ms = e2.elapsed_time(e3)
-    e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        import torch.distributed as dist
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(e2e_t.item())
+    e2e_ms = max_over_ranks(e2.elapsed_time(e3), ws, dev)
 
-    # ---- roofline of the dominant kernel (the operator apply) -------------------------
+    # ---- roofline of the dominant kernel (K1: p update + operator + x update) ---------
     hbm, peak_kind = _peaks()
-    nc = 1 << hm.dim
-    bytes_per_apply = hm.n_el * (8 + 4 * nc) + hm.n_dof * 16     # s_e, conn, p read, q write
-    apply_ms = prof["apply_ms"] / max(1, prof["iters"])
-    achieved = bytes_per_apply / (apply_ms / 1000.0) / 1e9
+    info = m.info()
+    kb = kernel_bytes(hm.dim, hm.n_el, hm.n_node, hm.n_dof, bool(info["structured"]))
+    k1_ms = prof["apply_ms"] / max(1, prof["iters"])
+    k2_ms = prof["u1_ms"] / max(1, prof["iters"])
+    achieved = kb["k1"] / (k1_ms / 1000.0) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(args.config, {}).get("apply_dram_bytes")
+            traffic = json.load(open(tf)).get(prob.name, {}).get("k1_dram_bytes")
         except Exception:
             traffic = None
     total_prof = prof["apply_ms"] + prof["alpha_ms"] + prof["u1_ms"] + prof["u2_ms"]
-    info = m.info()
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -299,11 +318,17 @@ def run_ours(args):
                     "h2d_bytes_per_step": hm.n_el * 8, "d2h_bytes_per_step": hm.n_el * 8 + 8},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
-                         "kernel": "operator apply q = A p (+ p.q)",
-                         "algorithmic_bytes_per_launch": bytes_per_apply,
-                         "avg_launch_ms": apply_ms, "peak_source": peak_kind,
+                         "kernel": "K1 k_apply_s3<CG>: p = Dinv r + beta p, x += alpha p, q = A p, p.q",
+                         "algorithmic_bytes_per_launch": kb["k1"], "avg_launch_ms": k1_ms,
+                         "peak_source": peak_kind,
                          "share_of_iteration": prof["apply_ms"] / total_prof if total_prof else None},
-            "kernel_ms_per_iter": {k: prof[k] / max(1, prof["iters"]) for k in ("apply_ms", "alpha_ms", "u1_ms", "u2_ms")},
+            "kernels": {
+                "k1_apply": {"ms": k1_ms, "bytes": kb["k1"], "gbs": kb["k1"] / (k1_ms / 1000.0) / 1e9},
+                "k2_rupdate": {"ms": k2_ms, "bytes": kb["k2"],
+                               "gbs": kb["k2"] / (k2_ms / 1000.0) / 1e9 if k2_ms > 0 else None},
+                "iteration": {"ms": k1_ms + k2_ms, "bytes": kb["k1"] + kb["k2"],
+                              "gbs": (kb["k1"] + kb["k2"]) / ((k1_ms + k2_ms) / 1000.0) / 1e9},
+            },
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": launches,

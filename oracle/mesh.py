@@ -23,7 +23,9 @@ def morton(coords: np.ndarray) -> np.ndarray:
     coords = np.asarray(coords, dtype=np.int64)
     d = coords.shape[1]
     key = np.zeros(coords.shape[0], dtype=np.int64)
-    for b in range(21):
+    top = int(coords.max()) if coords.size else 0
+    assert coords.size == 0 or (int(coords.min()) >= 0 and top < (1 << 21))
+    for b in range(max(1, top.bit_length())):          # higher bits are all zero
         for c in range(d):
             key |= ((coords[:, c] >> b) & 1) << (d * b + c)
     return key
@@ -241,19 +243,21 @@ def build_mesh(prob: Problem, with_filter: bool = True, density: bool = True) ->
             sel &= (anc[:, c] == lo[c]) | (anc[:, c] + size == lo[c])
         for c in span:
             sel &= (anc[:, c] >= lo[c]) & (anc[:, c] + size <= hi[c])
-        for e in np.nonzero(sel)[0].tolist():
-            s = int(size[e])
-            measure = (s * hL) ** len(span)
-            npts = 1 << len(span)
-            for m in range(npts):
-                p = np.empty(dim, dtype=np.int64)
-                for c in fixed_axes:
-                    p[c] = lo[c]
-                for t, c in enumerate(span):
-                    p[c] = anc[e, c] + ((m >> t) & 1) * s
-                nid = _node_lookup(node_keys, p[None, :])[0]
-                assert nid >= 0
-                load[dim * nid:dim * nid + dim] += vec * (measure / npts)
+        # each boundary piece spreads vec * measure equally over its 2^len(span) corners
+        es = np.nonzero(sel)[0]
+        s = size[es].astype(np.int64)
+        measure = (s.astype(np.float64) * hL) ** len(span)
+        npts = 1 << len(span)
+        for m in range(npts):
+            p = np.empty((es.shape[0], dim), dtype=np.int64)
+            for c in fixed_axes:
+                p[:, c] = lo[c]
+            for t, c in enumerate(span):
+                p[:, c] = anc[es, c] + ((m >> t) & 1) * s
+            nid = _node_lookup(node_keys, p)
+            assert np.all(nid >= 0)
+            for c in range(dim):
+                np.add.at(load, dim * nid.astype(np.int64) + c, vec[c] * (measure / npts))
 
     mesh = OracleMesh(dim=dim, L=L, hL=hL, elem_level=lev.astype(np.int8),
                       elem_anchor=anc.astype(np.int32), elem_node=elem_node,

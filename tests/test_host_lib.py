@@ -89,13 +89,15 @@ def _compare(prob):
 
 
 @pytest.mark.parametrize("case", [
-    "c1", "c2", "c3s", "c5s", "c4s",
+    "c1", "c2", "c3", "c4", "c3s", "c5s", "c4s",
     "amr2d", "amr3d", "ripple2d"])
 def test_host_builder_bit_exact_vs_oracle(case):
     if case == "c1":
         prob = config("c1")
     elif case == "c2":
         prob = config("c2")
+    elif case in ("c3", "c4"):
+        prob = config(case)                            # full BASELINE.json sizes
     elif case == "c3s":
         prob = config("c3", nx=12, ny=6, nz=6)
     elif case == "c5s":
@@ -109,7 +111,7 @@ def test_host_builder_bit_exact_vs_oracle(case):
     else:
         prob = cantilever2d((4, 4), L=4, leaves=refine_some(2, (4, 4), 4, [(1, 1)]), rmin=0.2)
     hm, om = _compare(prob)
-    if case in ("c2", "c4s", "amr2d", "amr3d", "ripple2d"):
+    if case in ("c2", "c4", "c4s", "amr2d", "amr3d", "ripple2d"):
         assert hm.hang_node.size > 0
 
 
