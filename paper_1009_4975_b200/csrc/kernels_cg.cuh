@@ -52,6 +52,63 @@ __device__ __forceinline__ void cg_after_rupdate(CgScalars *S, double rz, double
   if ((!S->fixed && rr <= S->thresh2) || it >= S->max_iter) S->done_next = 1;
 }
 
+// Structured path, end of the single-kernel iteration k (last block).
+// d = {rho_k = r_k.Dinv r_k, rr_k = r_k.r_k, p_k.q_k, q_k.z_k, q_k.Dinv q_k},
+// all exact dots of the vectors formed in this kernel.  x_k is complete.
+//   stop if rr_k <= rtol^2 ||b||^2 (x_k is the answer, k iterations);
+//   alpha_k = rho_k / p_k.q_k;
+//   rho_{k+1} = (r_k - alpha q).Dinv (r_k - alpha q)
+//             = rho_k - 2 alpha q.z_k + alpha^2 q.Dinv q   (one-step expansion:
+//     the next kernel needs beta_k = rho_{k+1}/rho_k before it can form r_{k+1};
+//     its own exact rho_{k+1} then feeds alpha_{k+1}, so the expansion error,
+//     ~eps rho_k / rho_{k+1}, enters beta_k only and does not accumulate).
+__device__ __forceinline__ void cg_single_step(CgScalars *S, int k, const double (&d)[5], double rtol, double *hist) {
+  const double rho = d[0], rr = d[1], pq = d[2], qz = d[3], qdq = d[4];
+  if (k == 0) {
+    S->thresh2 = rtol * rtol * S->bnorm2;
+    if (S->status != 0) {
+      S->done = 1;
+      return;
+    }
+  }
+  S->iter = k;
+  S->rho = rho;
+  S->rr = rr;
+  if (!(rho == rho) || !(rr == rr) || !(pq == pq) || !(qz == qz) || !(qdq == qdq)) {
+    S->status = -5;
+    S->done = 1;
+    return;
+  }
+  if (S->history && hist && k >= 1) hist[k - 1] = sqrt(rr / S->bnorm2);
+  if ((!S->fixed && rr <= S->thresh2) || S->bnorm2 == 0.0) {
+    S->done = 1;
+    return;
+  }
+  if (!(pq > 0.0)) {
+    S->status = -6;
+    S->done = 1;
+    return;
+  }
+  const double alpha = rho / pq;
+  const double rho_next = fma(alpha * alpha, qdq, fma(-2.0 * alpha, qz, rho));
+  S->alpha = alpha;
+  S->beta = rho_next / rho;
+}
+
+// Structured path, final step after N = max_iter iterations (or 0): r_N =
+// r_{N-1} - alpha q_{N-1}, x_N = x_{N-1} + alpha p_{N-1}, rho_N, rr_N.
+// Elementwise over node pairs (no operator needed).
+__device__ __forceinline__ void cg_final_step(CgScalars *S, int n_iter, double rho, double rr, double rtol,
+                                              double *hist) {
+  if (n_iter == 0) S->thresh2 = rtol * rtol * S->bnorm2;
+  S->iter = n_iter;
+  S->rho = rho;
+  S->rr = rr;
+  if (!(rho == rho) || !(rr == rr)) S->status = -5;
+  if (S->history && hist && n_iter >= 1) hist[n_iter - 1] = sqrt(rr / S->bnorm2);
+  S->done = 1;
+}
+
 // ||v||^2 -> S->bnorm2 (used for b).
 __global__ void k_norm2_b(int64_t n, const double *__restrict__ v, double *partials, CgScalars *S) {
   double acc[1] = {0.0};

@@ -12,16 +12,20 @@
 //    nodes) use the same node order.  The canonical Morton numbering (C3) is
 //    applied once per solve at the boundary (f in, u out).  Connectivity is
 //    implicit: element (i,j,k) has corner c at node (i+cx, j+cy, k+cz).
-//  * One PCG iteration is two kernels (textbook Hestenes-Stiefel recurrences,
-//    PAPER.md:511-523 with reading Q3, the x update deferred by one
-//    iteration so that it rides on the operator kernel):
-//      K1 k_apply_s3<CG>  p_k = Dinv r_k + beta_{k-1} p_{k-1}   (all staged nodes)
-//                         x  += alpha_{k-1} p_{k-1}              (owned nodes)
-//                         q   = A p_k,  p_k . q -> alpha_k        (owned nodes)
-//      K2 k_rupd_s3       r  -= alpha_k q;  r.Dinv r, r.r -> beta_k, stop test
-//    and after the loop k_xfinal adds the last alpha p.  Vector traffic per
-//    iteration: K1 reads r, p_{k-1}, x (+ s, Dinv/3) and writes p_k, q, x; K2
-//    reads r, q (+ Dinv/3) and writes r: 9.67 passes instead of 12.
+//  * One PCG iteration is ONE kernel (k_apply_s3<S3_CG>, Hestenes-Stiefel
+//    recurrences on the rescaled system, PAPER.md:511-523 with reading Q3):
+//      r_k = r_{k-1} - alpha_{k-1} q_{k-1}      (all staged nodes)
+//      p_k = Dinv r_k + beta_{k-1} p_{k-1}      (all staged nodes)
+//      x  += alpha_{k-1} p_{k-1}               (owned nodes)
+//      q_k = A p_k                              (owned nodes)
+//      one grid reduction of r_k.Dinv r_k, r_k.r_k, p_k.q_k, q_k.z_k, q_k.Dinv q_k
+//    after which the last block forms alpha_k and beta_k (cg_single_step, with
+//    rho_{k+1} from the one-step expansion) and tests rr_k.  r, p and q
+//    ping-pong between two buffers each (iteration k reads buffer (k+1)&1 at
+//    neighbours' nodes while they write buffer k&1).  k_final_s3 completes
+//    x_N after exactly N iterations.  Vector traffic per iteration: read r,
+//    q, p, x, write r, p, q, x (+ s, Dinv/3): 8.67 passes (12 for the
+//    unfused textbook scheme).
 //  * One CTA owns a (31 x (TYW-1)) patch of node columns and a range of node
 //    planes; it sweeps the element layers in z.  Thread (tx, ty) computes the
 //    element whose minimum corner is node (i0+tx-1, j0+ty-1) and accumulates
@@ -63,7 +67,7 @@ constexpr int kS3PadFront = 16;    // doubles (or nodes) before an internal vect
 constexpr int kS3PadBack = 128;    // doubles (or nodes) after it
 constexpr int kS3RowD = 100;       // doubles staged per node row: 33 nodes + alignment (800 B)
 constexpr int kS3RowN = 34;        // node values staged per row: 33 + alignment (272 B)
-constexpr int kS3NBuf = 4;         // staging depth (planes in flight ~ NBUF - 1 layers ahead)
+constexpr int kS3NBuf = 2;         // staging depth: plane P is issued ~1.5 layers before it is formed
 
 __device__ __forceinline__ int64_t s3_row(const GridView &G, int j, int k) {
   return ((int64_t)j + (int64_t)G.NY * k) * G.RS;
@@ -74,16 +78,20 @@ __device__ __forceinline__ int64_t s3_nrow(const GridView &G, int j, int k) {
 
 constexpr int s3_pad128(int doubles) { return (doubles + 15) / 16 * 16; }   // 128-byte multiple
 
+enum { S3_PLAIN = 0, S3_CG = 1 };
+
 template <int TYW>
 struct S3Smem {
   static constexpr int PY = TYW + 1;                          // node rows staged
   static constexpr int PD = s3_pad128(PY * kS3RowD);          // doubles per staged DOF plane
   static constexpr int PN = s3_pad128(PY * kS3RowN);          // doubles per staged node plane
-  double r[kS3NBuf][PD];                                      // r_k (CG) or v (plain apply), TMA box
-  double po[kS3NBuf][PD];                                     // p_{k-1}, TMA box
+  double ra[kS3NBuf][PD];                                     // r_{k-1} (CG) or v (plain), TMA box
+  double qa[kS3NBuf][PD];                                     // q_{k-1}, TMA box
+  double pa[kS3NBuf][PD];                                     // p_{k-1}, TMA box
   double dn[kS3NBuf][PN];                                     // Dinv per node, TMA box
   double pn[3][PY][kS3RowD];                                  // p_k ring: planes k mod 3
-  double xch[2][TYW][6][32];                                  // y-exchange (layer parity): 2 planes x 3 comps
+  double own[3][4][TYW * 32];                                 // owned node of plane k mod 3: z_k (3), Dinv
+  double xch[2][TYW][3][32];                                  // y-exchange (layer parity)
   unsigned long long mbar[kS3NBuf];
 };
 
@@ -119,56 +127,74 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
+struct S3Maps {           // TMA maps of the arrays one K1 launch stages
+  CUtensorMap a, q, p, d;   // r_{k-1} (or v), q_{k-1}, p_{k-1}, Dinv
+};
+
 // One thread: stage plane k (tile origin node (i0-1, j0-1)) into buffer b:
 // one TMA box per array.  Rows and columns outside the vector come back as 0.
-template <int TYW, bool CG>
-__device__ __forceinline__ void s3_issue_plane(S3Smem<TYW> &sm, int b, const CUtensorMap *ta, const CUtensorMap *tb,
-                                               const CUtensorMap *tc, int i0, int j0, int k, int off, int noff) {
+template <int TYW, int MODE>
+__device__ __forceinline__ void s3_issue_plane(S3Smem<TYW> &sm, int b, const S3Maps &M, int i0, int j0, int k,
+                                               int off, int noff) {
   constexpr int PY = TYW + 1;
-  constexpr unsigned bytes = PY * kS3RowD * 8 * (CG ? 2 : 1) + (CG ? PY * kS3RowN * 8 : 0);
+  constexpr bool CG = MODE == S3_CG;
+  constexpr unsigned bytes = PY * kS3RowD * 8 * (CG ? 3 : 1) + (CG ? PY * kS3RowN * 8 : 0);
   fence_proxy_async();
   mbar_arrive_expect_tx(&sm.mbar[b], bytes);
-  tma_load_3d(sm.r[b], ta, 3 * (i0 - 1) - off, j0 - 1, k, &sm.mbar[b]);
+  tma_load_3d(sm.ra[b], &M.a, 3 * (i0 - 1) - off, j0 - 1, k, &sm.mbar[b]);
   if (CG) {
-    tma_load_3d(sm.po[b], tb, 3 * (i0 - 1) - off, j0 - 1, k, &sm.mbar[b]);
-    tma_load_3d(sm.dn[b], tc, (i0 - 1) - noff, j0 - 1, k, &sm.mbar[b]);
+    tma_load_3d(sm.qa[b], &M.q, 3 * (i0 - 1) - off, j0 - 1, k, &sm.mbar[b]);
+    tma_load_3d(sm.pa[b], &M.p, 3 * (i0 - 1) - off, j0 - 1, k, &sm.mbar[b]);
+    tma_load_3d(sm.dn[b], &M.d, (i0 - 1) - noff, j0 - 1, k, &sm.mbar[b]);
   }
 }
 
-// p_k of node (col, row) of staged plane k: CG: Dinv r + beta p_{k-1}; plain: v.
-template <int TYW, bool CG>
+// r_k and p_k of node (col, row) of staged plane k.  CG:
+//   r_k = r_{k-1} - alpha_{k-1} q_{k-1}   (free nodes, Dinv != 0; r stays 0 elsewhere)
+//   p_k = Dinv r_k + beta_{k-1} p_{k-1}
+// plain: p = the staged v.  pin = false (plane outside the mesh): zeros.
+template <int TYW, int MODE>
 __device__ __forceinline__ void s3_form_node(const S3Smem<TYW> &sm, int b, int row, int col, int off, int noff,
-                                             double beta, bool pin, double (&v)[3]) {
-  const double *rr = &sm.r[b][row * kS3RowD + off + 3 * col];
-  const double *pp = &sm.po[b][row * kS3RowD + off + 3 * col];
-  const double dv = CG ? sm.dn[b][row * kS3RowN + noff + col] : 0.0;
+                                             double alpha, double beta, bool pin, double (&rv)[3], double (&pv)[3],
+                                             double &dv) {
+  const int o = row * kS3RowD + off + 3 * col;
+  dv = (MODE == S3_CG && pin) ? sm.dn[b][row * kS3RowN + noff + col] : 0.0;
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    double t = pin ? rr[d] : 0.0;
-    if (CG && pin) t = fma(dv, t, (beta != 0.0) ? beta * pp[d] : 0.0);
-    v[d] = t;
+    double r = pin ? sm.ra[b][o + d] : 0.0;
+    double p = r;
+    if (MODE == S3_CG) {
+      if (pin && alpha != 0.0 && dv != 0.0) r = fma(-alpha, sm.qa[b][o + d], r);
+      p = fma(dv, r, (pin && beta != 0.0) ? beta * sm.pa[b][o + d] : 0.0);
+    }
+    rv[d] = r;
+    pv[d] = p;
   }
 }
 
-// K1.  CG = true: the fused PCG operator step (see the header comment).
-// CG = false: q = C^T K C v for a v that vanishes on non-free DOFs (ta maps v;
-// tb, tc, pnew, x, S unused).
+// K1.  MODE = S3_CG: iteration k of the single-kernel Jacobi-PCG (header comment):
+//   form r_k, p_k on every staged node; owners write r_k, p_k and do
+//   x += alpha_{k-1} p_{k-1}; q_k = A p_k (owners write it); reduce
+//   rho_k = r_k.Dinv r_k, rr_k = r_k.r_k, p_k.q_k, q_k.z_k, q_k.Dinv q_k; the
+//   last block forms alpha_k, beta_k (rho_{k+1} by the one-step expansion)
+//   and the stop test on rr_k.
+// MODE = S3_PLAIN: q = C^T K C v for a v that vanishes on non-free DOFs.
 //
 // Per CTA the layers ek = k_lo-1 .. k_hi-1 run with one barrier each:
 //   1. element ek from p planes ek, ek+1 (ring slots ek%3, (ek+1)%3) -> y-exchange write
 //   2. barrier
-//   3. y-exchange read, q and p.q of node plane ek (owned); refill the staging
-//      buffer of plane ek+2 with plane ek+2+NBUF (warp 0, one elected lane)
-//   4. wait for plane ek+3, form p of it into ring slot (ek+3)%3 (= ek%3, free
-//      since step 2); owners write p_k there and update x
+//   3. y-exchange read, q of node plane ek (owned) and its dot products;
+//      refill the staging buffer of plane ek+2 with plane ek+2+NBUF
+//   4. wait for plane ek+3, form it into ring slot (ek+3)%3 (= ek%3, free
+//      since step 2); owners write r_k, p_k, update x, keep z_k, Dinv for step 3
 // Plane P is issued during layer P-2-NBUF, waited for during layer P-3.
-template <int TYW, bool CG>
+template <int TYW, int MODE>
 __global__ void __launch_bounds__(32 * TYW, 2)
-k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ CUtensorMap ta,
-           const __grid_constant__ CUtensorMap tb, const __grid_constant__ CUtensorMap tc,
+k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3Maps M, double *__restrict__ rnew,
            double *__restrict__ pnew, double *__restrict__ x, double *__restrict__ q,
-           const __grid_constant__ K0Had3 H, CgScalars *S, double *partials) {
-  if (CG && cg_stop_at_apply(S)) return;
+           const __grid_constant__ K0Had3 H, CgScalars *S, double *partials, int kit, double rtol, double *hist) {
+  constexpr bool CG = MODE == S3_CG;
+  if (CG && cg_stopped(S)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   S3Smem<TYW> &sm = *reinterpret_cast<S3Smem<TYW> *>(smem_raw);
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -201,7 +227,7 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ CUt
   // prologue: issue planes k_lo-1 .. k_lo-2+NBUF
   if (tid == 0)
     for (int k = k_lo - 1; k < k_lo - 1 + kS3NBuf; ++k)
-      if (staged(k)) s3_issue_plane<TYW, CG>(sm, buf_of(k), &ta, &tb, &tc, i0, j0, k, off, noff);
+      if (staged(k)) s3_issue_plane<TYW, MODE>(sm, buf_of(k), M, i0, j0, k, off, noff);
   unsigned phase = 0;                                   // parity bit per buffer
 
   double xr[3] = {0.0, 0.0, 0.0};                       // x of the owned node of the next plane to form
@@ -210,8 +236,9 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ CUt
 #pragma unroll
     for (int d = 0; d < 3; ++d) xr[d] = __ldcs(&x[dof + d]);
   }
+  double dots[5] = {0.0, 0.0, 0.0, 0.0, 0.0};           // rho, rr, p.q, q.z, q.Dinv q
 
-  // form p of plane k into ring slot k%3.  Every thread forms its own node
+  // form plane k into ring slot k%3.  Every thread forms its own node
   // (tx, ty), which is the node it owns (if it owns one); the 41 halo nodes of
   // column 32 and row TYW are spread over lanes 0-5 of all warps so that every
   // warp does at most two rounds.
@@ -224,76 +251,86 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ CUt
       mbar_wait(&sm.mbar[bb], (phase >> bb) & 1);
       phase ^= 1u << bb;
     }
-    double(*dst)[kS3RowD] = sm.pn[(k + 3) % 3];
-    double v[3];
-    s3_form_node<TYW, CG>(sm, bb, ty, tx, off, noff, beta, pin, v);
+    const int slot = (k + 3) % 3;
+    double(*dst)[kS3RowD] = sm.pn[slot];
+    double rv[3], pv[3], dv;
+    s3_form_node<TYW, MODE>(sm, bb, ty, tx, off, noff, alpha_old, beta, pin, rv, pv, dv);
 #pragma unroll
-    for (int d = 0; d < 3; ++d) dst[ty][off + 3 * tx + d] = v[d];
-    if (CG && owner && k >= k_lo && k < k_hi) {
-      const int64_t dof = s3_row(G, ej, k) + 3 * ei;
+    for (int d = 0; d < 3; ++d) dst[ty][off + 3 * tx + d] = pv[d];
+    if (CG) {
+      const bool mine = owner && k >= k_lo && k < k_hi;
 #pragma unroll
-      for (int d = 0; d < 3; ++d) __stcs(&pnew[dof + d], v[d]);
-      if (xupd) {
-        const double *pp = &sm.po[bb][ty * kS3RowD + off + 3 * tx];
+      for (int d = 0; d < 3; ++d) sm.own[slot][d][tid] = mine ? dv * rv[d] : 0.0;
+      sm.own[slot][3][tid] = mine ? dv : 0.0;
+      if (mine) {
+        const int64_t dof = s3_row(G, ej, k) + 3 * ei;
 #pragma unroll
-        for (int d = 0; d < 3; ++d) __stcs(&x[dof + d], fma(alpha_old, pp[d], xr[d]));
-        if (k + 1 < k_hi) {
+        for (int d = 0; d < 3; ++d) {
+          __stcs(&rnew[dof + d], rv[d]);
+          __stcs(&pnew[dof + d], pv[d]);
+          dots[0] = fma(dv * rv[d], rv[d], dots[0]);
+          dots[1] = fma(rv[d], rv[d], dots[1]);
+        }
+        if (xupd) {
+          const double *pp = &sm.pa[bb][ty * kS3RowD + off + 3 * tx];
 #pragma unroll
-          for (int d = 0; d < 3; ++d) xr[d] = __ldcs(&x[dof + plane_d + d]);
+          for (int d = 0; d < 3; ++d) __stcs(&x[dof + d], fma(alpha_old, pp[d], xr[d]));
+          if (k + 1 < k_hi) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) xr[d] = __ldcs(&x[dof + plane_d + d]);
+          }
         }
       }
     }
     if (xe < 33 + TYW) {
-      s3_form_node<TYW, CG>(sm, bb, xe_row, xe_col, off, noff, beta, pin, v);
+      s3_form_node<TYW, MODE>(sm, bb, xe_row, xe_col, off, noff, alpha_old, beta, pin, rv, pv, dv);
 #pragma unroll
-      for (int d = 0; d < 3; ++d) dst[xe_row][off + 3 * xe_col + d] = v[d];
+      for (int d = 0; d < 3; ++d) dst[xe_row][off + 3 * xe_col + d] = pv[d];
     }
   };
-  for (int k = k_lo - 1; k <= min(k_lo + 1, k_hi); ++k) form_plane(k);
-  __syncthreads();
-  // the buffers of planes k_lo-1 and k_lo are free again
-  if (tid == 0)
-    for (int k = k_lo - 1 + kS3NBuf; k <= k_lo + kS3NBuf; ++k)
-      if (staged(k)) s3_issue_plane<TYW, CG>(sm, buf_of(k), &ta, &tb, &tc, i0, j0, k, off, noff);
-
-  double pq = 0.0;
-  double acc_cur[3] = {0.0, 0.0, 0.0};                  // node plane ek (owned column)
-  int64_t s_idx = (int64_t)ei + (int64_t)G.EX * ((int64_t)ej + (int64_t)G.EY * (k_lo - 1));
-  const int64_t s_stride = (int64_t)G.EX * G.EY;
-  double s_next = 0.0;
-  {
-    const int ek = k_lo - 1;
-    if (col_el && ek >= 0 && ek < G.EZ) s_next = __ldg(&s[s_idx]);
+  // prologue forms planes k_lo-1 .. k_lo+1; the loop's layer ek issues plane
+  // ek+2+NBUF, so the prologue issues every plane up to k_lo+NBUF, each once
+  // the plane NBUF below it (same buffer) has been formed by all threads
+  for (int k = k_lo - 1; k <= min(k_lo + 1, k_hi); ++k) {
+    form_plane(k);
+    __syncthreads();
+    const int kn = k + kS3NBuf;
+    if (tid == 0 && kn <= k_lo + kS3NBuf && staged(kn)) s3_issue_plane<TYW, MODE>(sm, buf_of(kn), M, i0, j0, kn, off, noff);
   }
 
+  // per-layer carries: contributions of layer ek-1's upper corners
+  double own_carry[3] = {0.0, 0.0, 0.0};                // to node (ei, ej, ek)
+  double up_carry[3] = {0.0, 0.0, 0.0};                 // to node (ei, ej+1, ek), sent to row ty+1
+  // s_e of this thread's element column, loaded two layers ahead (register ring)
+  const int64_t s_stride = (int64_t)G.EX * G.EY;
+  const int64_t s_col = (int64_t)ei + (int64_t)G.EX * ej;
+  auto load_s = [&](int ek) {
+    return (col_el && ek >= 0 && ek < G.EZ && ek < k_hi) ? __ldg(&s[s_col + s_stride * ek]) : 0.0;
+  };
+  double s_n1 = load_s(k_lo - 1), s_n2 = load_s(k_lo);
+
   for (int ek = k_lo - 1; ek < k_hi; ++ek) {
-    const double se = s_next;
-    s_idx += s_stride;
-    {
-      const int ekn = ek + 1;
-      s_next = (col_el && ekn >= 0 && ekn < G.EZ && ekn < k_hi) ? __ldg(&s[s_idx]) : 0.0;
-    }
+    const double se = s_n1;
+    s_n1 = s_n2;
+    s_n2 = load_s(ek + 2);
     const int slo = (ek + 3) % 3, shi = (ek + 4) % 3;
     double p_own[3];                                    // p_k at the owned node of plane ek
 #pragma unroll
     for (int d = 0; d < 3; ++d) p_own[d] = sm.pn[slo][ty][off + 3 * tx + d];
     const bool el = col_el && ek >= 0 && ek < G.EZ;
     double y[24];
-    if (el) {
-      double xv[24];
+    {
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
         const double *row = &sm.pn[cz ? shi : slo][ty + cy][off + 3 * (tx + cx)];
 #pragma unroll
-        for (int d = 0; d < 3; ++d) xv[3 * c + d] = row[d];
+        for (int d = 0; d < 3; ++d) y[3 * c + d] = row[d];
       }
-      had_apply_inplace(H, xv);
+      had_apply_inplace(H, y);
+      const double sc = el ? se : 0.0;
 #pragma unroll
-      for (int a = 0; a < 24; ++a) y[a] = xv[a] * se;
-    } else {
-#pragma unroll
-      for (int a = 0; a < 24; ++a) y[a] = 0.0;
+      for (int a = 0; a < 24; ++a) y[a] *= sc;
     }
     // x routing: corner (1,cy,cz) of element ei goes to node ei+1 (lane + 1)
     double a_row[2][2][3];   // [cy][cz][comp] after the x merge, at node column ei
@@ -307,98 +344,74 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ CUt
           if (tx == 0) from_left = 0.0;
           a_row[cy][cz][d] = y[3 * (2 * cy + 4 * cz) + d] + from_left;
         }
-    // y routing: row ty's (cy = 1) part goes to row ty+1
+    // y routing: node (ei, ej+1, ek) collects this layer's (cy=1, cz=0) part and
+    // the previous layer's (cy=1, cz=1) part; row ty+1 owns it
 #pragma unroll
-    for (int cz = 0; cz < 2; ++cz)
-#pragma unroll
-      for (int d = 0; d < 3; ++d) sm.xch[ek & 1][ty][3 * cz + d][tx] = a_row[1][cz][d];
+    for (int d = 0; d < 3; ++d) sm.xch[ek & 1][ty][d][tx] = a_row[1][0][d] + up_carry[d];
     __syncthreads();                                    // the one barrier of the layer
     if (tid == 0 && staged(ek + 2 + kS3NBuf))
-      s3_issue_plane<TYW, CG>(sm, buf_of(ek + 2 + kS3NBuf), &ta, &tb, &tc, i0, j0, ek + 2 + kS3NBuf, off, noff);
-    double tot[2][3];
-#pragma unroll
-    for (int cz = 0; cz < 2; ++cz)
-#pragma unroll
-      for (int d = 0; d < 3; ++d) tot[cz][d] = a_row[0][cz][d] + (ty > 0 ? sm.xch[ek & 1][ty - 1][3 * cz + d][tx] : 0.0);
-    // node plane ek is complete: cz=1 part of layer ek-1 (acc_cur) + cz=0 part of layer ek
+      s3_issue_plane<TYW, MODE>(sm, buf_of(ek + 2 + kS3NBuf), M, i0, j0, ek + 2 + kS3NBuf, off, noff);
+    // node plane ek is complete: (cz=0) parts of layer ek + (cz=1) parts of layer ek-1
     if (ek >= k_lo && owner) {
       const int64_t dof = s3_row(G, ej, ek) + 3 * ei;
+      const int slot = (ek + 3) % 3;
+      const double dv = CG ? sm.own[slot][3][tid] : 0.0;
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
-        const double qv = acc_cur[d] + tot[0][d];
-        q[dof + d] = qv;
-        if (CG) pq = fma(p_own[d], qv, pq);
+        const double qv = a_row[0][0][d] + own_carry[d] + (ty > 0 ? sm.xch[ek & 1][ty - 1][d][tx] : 0.0);
+        __stcs(&q[dof + d], qv);
+        if (CG) {
+          dots[2] = fma(p_own[d], qv, dots[2]);
+          dots[3] = fma(sm.own[slot][d][tid], qv, dots[3]);
+          dots[4] = fma(dv * qv, qv, dots[4]);
+        }
       }
     }
 #pragma unroll
-    for (int d = 0; d < 3; ++d) acc_cur[d] = tot[1][d];
+    for (int d = 0; d < 3; ++d) {
+      own_carry[d] = a_row[0][1][d];
+      up_carry[d] = a_row[1][1][d];
+    }
     if (ek + 3 <= k_hi) form_plane(ek + 3);
   }
   if (CG) {
-    double v[1] = {pq};
-    if (grid_sum<1>(v, partials, &S->counter[CNT_PQ])) {
-      if (!(v[0] > 0.0)) {
-        S->status = (v[0] != v[0]) ? -5 : -6;
-        S->done = 1;
-      } else {
-        S->alpha = S->rho / v[0];
-      }
-    }
+    if (grid_sum<5>(dots, partials, &S->counter[CNT_PQ])) cg_single_step(S, kit, dots, rtol, hist);
   }
 }
 
-// ---- vector kernels of the structured path -----------------------------------------------
-// Coalesced double2 streams over the internal vector; Dinv is gathered per
-// node (node = DOF / 3, an L1 hit: a warp's 64 doubles of r span 22 nodes).
-
-// K2: r -= alpha q on free nodes; rho' = r.Dinv r, rr = r.r -> beta, stop test.
-// INIT: no update (r = r0); rho0, rr0 and the thresholds.
-template <bool INIT>
-__global__ void __launch_bounds__(256) k_rupd_s3(int64_t n, const double *__restrict__ q, const double *__restrict__ dn,
-                          double *__restrict__ r, double *partials, CgScalars *S, double *hist, double rtol) {
-  if (!INIT && cg_stopped(S)) return;
-  constexpr int U = 4;
-  const double alpha = INIT ? 0.0 : __ldcg(&S->alpha);
+// ---- final step of a structured solve (after N iterations) ----------------------------
+// r_N = r_{N-1} - alpha q_{N-1} (free nodes), x_N = x_{N-1} + alpha p_{N-1},
+// rho_N, rr_N -> cg_final_step.  Coalesced double2 streams; Dinv gathered
+// per node (node = DOF / 3, an L1 hit).  r_N itself is not stored.
+__global__ void __launch_bounds__(512) k_final_s3(int n, const double *__restrict__ ro, const double *__restrict__ qo,
+                                                  const double *__restrict__ po, const double *__restrict__ dn,
+                                                  double *__restrict__ x, double *partials, CgScalars *S, int n_iter,
+                                                  double rtol, double *hist) {
+  if (cg_stopped(S)) return;
+  const double alpha = __ldcg(&S->alpha);
   double acc[2] = {0.0, 0.0};
-  const int64_t n2 = n >> 1;
-  const int64_t T = (int64_t)gridDim.x * blockDim.x;
-  double2 *r2 = reinterpret_cast<double2 *>(r);
-  const double2 *q2 = reinterpret_cast<const double2 *>(q);
-  for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < n2; j0 += U * T) {
-    double2 rv[U], qv[U];
-    double d0[U], d1[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t j = j0 + u * T;
-      if (j < n2) {
-        rv[u] = __ldcs(&r2[j]);
-        qv[u] = INIT ? make_double2(0.0, 0.0) : __ldcs(&q2[j]);
-        d0[u] = __ldg(&dn[(2 * j) / 3]);
-        d1[u] = __ldg(&dn[(2 * j + 1) / 3]);
-      } else {
-        rv[u] = qv[u] = make_double2(0.0, 0.0);
-        d0[u] = d1[u] = 0.0;
-      }
+  const int n2 = n >> 1;
+  const double2 *r2 = reinterpret_cast<const double2 *>(ro);
+  const double2 *q2 = reinterpret_cast<const double2 *>(qo);
+  const double2 *p2 = reinterpret_cast<const double2 *>(po);
+  double2 *x2 = reinterpret_cast<double2 *>(x);
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n2; j += gridDim.x * blockDim.x) {
+    double2 rv = __ldcs(&r2[j]);
+    const unsigned e = 2u * (unsigned)j;
+    const double d0 = __ldg(&dn[e / 3u]), d1 = __ldg(&dn[(e + 1u) / 3u]);
+    if (alpha != 0.0) {
+      const double2 qv = __ldcs(&q2[j]), pv = __ldcs(&p2[j]);
+      double2 xv = x2[j];
+      if (d0 != 0.0) rv.x = fma(-alpha, qv.x, rv.x);
+      if (d1 != 0.0) rv.y = fma(-alpha, qv.y, rv.y);
+      xv.x = fma(alpha, pv.x, xv.x);
+      xv.y = fma(alpha, pv.y, xv.y);
+      x2[j] = xv;
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t j = j0 + u * T;
-      if (!INIT) {
-        if (d0[u] != 0.0) rv[u].x = fma(-alpha, qv[u].x, rv[u].x);
-        if (d1[u] != 0.0) rv[u].y = fma(-alpha, qv[u].y, rv[u].y);
-        if (j < n2) __stcs(&r2[j], rv[u]);
-      }
-      acc[0] = fma(rv[u].x, d0[u] * rv[u].x, acc[0]);
-      acc[0] = fma(rv[u].y, d1[u] * rv[u].y, acc[0]);
-      acc[1] = fma(rv[u].x, rv[u].x, acc[1]);
-      acc[1] = fma(rv[u].y, rv[u].y, acc[1]);
-    }
+    acc[0] = fma(rv.x, d0 * rv.x, fma(rv.y, d1 * rv.y, acc[0]));
+    acc[1] = fma(rv.x, rv.x, fma(rv.y, rv.y, acc[1]));
   }
-  if (INIT) {
-    if (grid_sum<2>(acc, partials, &S->counter[CNT_INIT])) cg_init_scalars(S, acc[0], acc[1], rtol);
-  } else {
-    if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) cg_after_rupdate(S, acc[0], acc[1], hist);
-  }
+  if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) cg_final_step(S, n_iter, acc[0], acc[1], rtol, hist);
 }
 
 // ---- setup kernels of the structured path ------------------------------------------------

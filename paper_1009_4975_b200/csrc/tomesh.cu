@@ -52,6 +52,8 @@ struct to_mesh {
   // workspace
   double *s = nullptr, *x = nullptr, *r = nullptr, *q = nullptr, *dinv = nullptr, *D = nullptr;
   double *pb[2] = {nullptr, nullptr};   // p ping-pong: iteration k writes pb[k & 1]
+  double *rb[2] = {nullptr, nullptr};   // structured: r ping-pong (rb[0] = r)
+  double *qb[2] = {nullptr, nullptr};   // structured: q ping-pong (qb[0] = q)
   double *dn = nullptr;                 // structured: Dinv per node (internal node order)
   double *partials = nullptr, *hist = nullptr;
   int32_t hist_len = 0, hist_cap = 0;
@@ -71,7 +73,7 @@ struct to_mesh {
   double k0d = 0.0, h_struct = 1.0;
   // TMA tensor maps of the internal vectors (structured path): [NZ][NY][RS] doubles
   // (boxes of TYW+1 rows x 100 doubles) and the node array Dinv [NZ][NY][NXP].
-  CUtensorMap tm_r, tm_x, tm_pb[2], tm_dn;
+  CUtensorMap tm_x, tm_rb[2], tm_qb[2], tm_pb[2], tm_dn;
   int last_launches = 0;
   int matvec_variant = 0;
   std::vector<cudaEvent_t> prof_ev;   // TO_PROFILE: 5 events per iteration
@@ -332,8 +334,8 @@ int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof
   m->structured = true;
   m->matvec_variant = 1;
   const size_t smem = sizeof(S3Smem<kS3TYW>);
-  CK(cudaFuncSetAttribute(k_apply_s3<kS3TYW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  CK(cudaFuncSetAttribute(k_apply_s3<kS3TYW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(k_apply_s3<kS3TYW, S3_CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(k_apply_s3<kS3TYW, S3_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   return 0;
 }
 
@@ -417,19 +419,28 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
   // workspace: internal-order vectors with zero pads on both sides (the
   // structured kernels read whole aligned row windows)
   RC(m->alloc(&m->s, m->n_el));
-  for (double **v : {&m->x, &m->r, &m->pb[0], &m->pb[1], &m->q, &m->dinv, &m->D}) {
+  std::vector<double **> vecs = {&m->x, &m->r, &m->pb[0], &m->pb[1], &m->q, &m->dinv, &m->D};
+  if (m->structured) {
+    vecs.push_back(&m->rb[1]);
+    vecs.push_back(&m->qb[1]);
+  }
+  for (double **v : vecs) {
     double *base = nullptr;
     RC(m->alloc(&base, (size_t)(m->n_int + kS3PadFront + kS3PadBack)));
     CK(cudaMemsetAsync(base, 0, sizeof(double) * (m->n_int + kS3PadFront + kS3PadBack), st));
     *v = base + kS3PadFront;
   }
+  m->rb[0] = m->r;
+  m->qb[0] = m->q;
   if (m->structured) {
     const GridView &G = m->G;
     const uint32_t PY = kS3TYW + 1;
-    RC(make_tensor_map(&m->tm_r, m->r, G.RS, G.NY, G.NZ, kS3RowD, PY));
     RC(make_tensor_map(&m->tm_x, m->x, G.RS, G.NY, G.NZ, kS3RowD, PY));
-    RC(make_tensor_map(&m->tm_pb[0], m->pb[0], G.RS, G.NY, G.NZ, kS3RowD, PY));
-    RC(make_tensor_map(&m->tm_pb[1], m->pb[1], G.RS, G.NY, G.NZ, kS3RowD, PY));
+    for (int b = 0; b < 2; ++b) {
+      RC(make_tensor_map(&m->tm_rb[b], m->rb[b], G.RS, G.NY, G.NZ, kS3RowD, PY));
+      RC(make_tensor_map(&m->tm_qb[b], m->qb[b], G.RS, G.NY, G.NZ, kS3RowD, PY));
+      RC(make_tensor_map(&m->tm_pb[b], m->pb[b], G.RS, G.NY, G.NZ, kS3RowD, PY));
+    }
     RC(make_tensor_map(&m->tm_dn, m->dn, G.NXP, G.NY, G.NZ, kS3RowN, PY));
   }
   CK(cudaStreamSynchronize(st));
@@ -533,48 +544,66 @@ int op_rhs(to_mesh *m, double *b_int, cudaStream_t st) {
 int s3_grid(const to_mesh *m) { return m->G.ntx * m->G.nty * m->G.nzs; }
 
 // out = C^T K C in (in vanishing on non-free DOFs), plain apply.  Structured:
-// `in` must be one of the handle's TMA-mapped vectors (x or pb[0]).
+// `in` must be one of the handle's TMA-mapped vectors (x, pb[0], rb[*]).
 int op_apply(to_mesh *m, const double *in, double *out, cudaStream_t st) {
   if (!m->structured) return launch_matvec(m, in, out, st);
-  const CUtensorMap *tin = in == m->x ? &m->tm_x : in == m->pb[0] ? &m->tm_pb[0] : in == m->r ? &m->tm_r : nullptr;
+  const CUtensorMap *tin = in == m->x        ? &m->tm_x
+                           : in == m->pb[0]  ? &m->tm_pb[0]
+                           : in == m->rb[0]  ? &m->tm_rb[0]
+                           : in == m->rb[1]  ? &m->tm_rb[1]
+                                             : nullptr;
   if (!tin) { set_error("internal: unmapped apply input"); return TO_EINVAL; }
+  S3Maps M;
+  M.a = M.q = M.p = M.d = *tin;
   dim3 block(32, kS3TYW);
-  k_apply_s3<kS3TYW, false><<<s3_grid(m), block, sizeof(S3Smem<kS3TYW>), st>>>(
-      m->G, m->s, *tin, *tin, m->tm_dn, nullptr, nullptr, out, m->KH, nullptr, nullptr);
+  k_apply_s3<kS3TYW, S3_PLAIN><<<s3_grid(m), block, sizeof(S3Smem<kS3TYW>), st>>>(
+      m->G, m->s, M, nullptr, nullptr, nullptr, out, m->KH, nullptr, nullptr, 0, 0.0, nullptr);
   m->last_launches++;
   return check_launch();
 }
 
-// K1 of CG iteration k: p_k into pb[k & 1] from pb[(k+1) & 1], deferred x
-// update, q = A p_k, alpha_k.
+// General path, iteration k part 1: p_k into pb[k & 1] from pb[(k+1) & 1],
+// deferred x update, q = A p_k, alpha_k.
 int op_cg_k1(to_mesh *m, int k, cudaStream_t st) {
   const double *po = m->pb[(k + 1) & 1];
   double *pn = m->pb[k & 1];
-  if (!m->structured) {
-    k_pre_g<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->r, m->dinv, po, pn, m->x, m->q, m->S);
-    int g = grid_for(m->n_el, kBlock, 16);
-    if (m->dim == 2) k_matvec_atomic<2><<<g, kBlock, 0, st>>>(m->view(), m->s, pn, m->q, m->K2, m->S, m->partials);
-    else k_matvec_atomic<3><<<g, kBlock, 0, st>>>(m->view(), m->s, pn, m->q, m->K3, m->S, m->partials);
-    m->last_launches += 2;
-    return 0;
-  }
+  k_pre_g<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->r, m->dinv, po, pn, m->x, m->q, m->S);
+  int g = grid_for(m->n_el, kBlock, 16);
+  if (m->dim == 2) k_matvec_atomic<2><<<g, kBlock, 0, st>>>(m->view(), m->s, pn, m->q, m->K2, m->S, m->partials);
+  else k_matvec_atomic<3><<<g, kBlock, 0, st>>>(m->view(), m->s, pn, m->q, m->K3, m->S, m->partials);
+  m->last_launches += 2;
+  return 0;
+}
+
+// Structured path, the whole iteration k in one kernel (kernels_struct3d.cuh).
+int op_cg_s3(to_mesh *m, int k, double rtol, cudaStream_t st) {
+  const int o = (k + 1) & 1, w = k & 1;
+  S3Maps M;
+  M.a = m->tm_rb[o];
+  M.q = m->tm_qb[o];
+  M.p = m->tm_pb[o];
+  M.d = m->tm_dn;
   dim3 block(32, kS3TYW);
-  k_apply_s3<kS3TYW, true><<<s3_grid(m), block, sizeof(S3Smem<kS3TYW>), st>>>(
-      m->G, m->s, m->tm_r, m->tm_pb[(k + 1) & 1], m->tm_dn, pn, m->x, m->q, m->KH, m->S, m->partials);
+  k_apply_s3<kS3TYW, S3_CG><<<s3_grid(m), block, sizeof(S3Smem<kS3TYW>), st>>>(
+      m->G, m->s, M, m->rb[w], m->pb[w], m->x, m->qb[w], m->KH, m->S, m->partials, k, rtol, m->hist);
   m->last_launches++;
   return 0;
 }
 
-// K2 (INIT: rho0, rr0 and thresholds only).
+// Structured path, x_N and the final residual after N iterations.
+int op_final_s3(to_mesh *m, int n_iter, double rtol, cudaStream_t st) {
+  const int o = (n_iter + 1) & 1;
+  k_final_s3<<<kNumSMs * 4, 512, 0, st>>>((int)m->n_int, m->rb[o], m->qb[o], m->pb[o], m->dn, m->x, m->partials,
+                                          m->S, n_iter, rtol, m->hist);
+  m->last_launches++;
+  return check_launch();
+}
+
+// General path K2 (INIT: rho0, rr0 and thresholds only).
 template <bool INIT>
 int op_cg_k2(to_mesh *m, double rtol, cudaStream_t st) {
-  if (!m->structured) {
-    k_rupd<INIT><<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->q, m->dinv, m->r, m->partials, m->S, m->hist,
-                                                        rtol);
-  } else {
-    k_rupd_s3<INIT><<<grid_for(m->n_int / 8), kBlock, 0, st>>>(m->n_int, m->q, m->dn, m->r, m->partials, m->S,
-                                                                m->hist, rtol);
-  }
+  k_rupd<INIT><<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->q, m->dinv, m->r, m->partials, m->S, m->hist,
+                                                      rtol);
   m->last_launches++;
   return 0;
 }
@@ -612,19 +641,21 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   CK(cudaEventRecord(m->ev0, st));
   RC(reset_scalars(m, max_iter, fixed, hist, st));
   RC(op_scale_and_diag(m, penal, x_dev, nullptr, st));
-  RC(op_rhs(m, m->r, st));
+  // r0 = b: the structured kernel of iteration 0 reads r from rb[1]
+  double *r0 = m->structured ? m->rb[1] : m->r;
+  RC(op_rhs(m, r0, st));
   const int gv = grid_for(n);
-  k_norm2_b<<<gv, kBlock, 0, st>>>(n, m->r, m->partials, m->S);
+  k_norm2_b<<<gv, kBlock, 0, st>>>(n, r0, m->partials, m->S);
   m->last_launches++;
   if (warm) {
     RC(op_masked_in(m, u_dev, m->x, st));
     RC(op_apply(m, m->x, m->q, st));
-    k_sub_masked<<<gv, kBlock, 0, st>>>(n, m->q, free_int(m), m->r);
+    k_sub_masked<<<gv, kBlock, 0, st>>>(n, m->q, free_int(m), r0);
     m->last_launches++;
   } else {
     CK(cudaMemsetAsync(m->x, 0, sizeof(double) * n, st));
   }
-  RC(op_cg_k2<true>(m, rtol, st));
+  if (!m->structured) RC(op_cg_k2<true>(m, rtol, st));
   RC(check_launch());
 
   const bool prof = (flags & TO_PROFILE) != 0;
@@ -638,17 +669,26 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   }
   int launched = 0;
   int chunk = fixed ? std::max(1, max_iter) : 16;
-  RC(read_scalars(m, st));
-  bool stop = m->S_host->done != 0;
+  bool stop = false;
+  if (!m->structured) {
+    RC(read_scalars(m, st));
+    stop = m->S_host->done != 0;
+  }
   while (!stop && launched < max_iter) {
     int cnt = std::min(chunk, max_iter - launched);
     for (int k = 0; k < cnt; ++k) {
       cudaEvent_t *E = prof ? &m->prof_ev[(size_t)3 * (launched + k)] : nullptr;
       if (prof) CK(cudaEventRecord(E[0], st));
-      RC(op_cg_k1(m, launched + k, st));
-      if (prof) CK(cudaEventRecord(E[1], st));
-      RC(op_cg_k2<false>(m, rtol, st));
-      if (prof) CK(cudaEventRecord(E[2], st));
+      if (m->structured) {
+        RC(op_cg_s3(m, launched + k, rtol, st));
+        if (prof) CK(cudaEventRecord(E[1], st));
+        if (prof) CK(cudaEventRecord(E[2], st));
+      } else {
+        RC(op_cg_k1(m, launched + k, st));
+        if (prof) CK(cudaEventRecord(E[1], st));
+        RC(op_cg_k2<false>(m, rtol, st));
+        if (prof) CK(cudaEventRecord(E[2], st));
+      }
     }
     RC(check_launch());
     launched += cnt;
@@ -658,8 +698,12 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
       chunk = std::min(chunk * 2, 256);
     }
   }
-  k_xfinal<<<gv, kBlock, 0, st>>>(n, m->x, m->pb[0], m->pb[1], m->S);
-  m->last_launches++;
+  if (m->structured) {
+    RC(op_final_s3(m, max_iter, rtol, st));       // no-op if an iteration already converged
+  } else {
+    k_xfinal<<<gv, kBlock, 0, st>>>(n, m->x, m->pb[0], m->pb[1], m->S);
+    m->last_launches++;
+  }
   RC(check_launch());
   RC(read_scalars(m, st));
   CgScalars res = *m->S_host;

@@ -114,8 +114,9 @@ def test_L2_converged_solve(name):
     assert abs(st.iters - ref.cg.iters) <= max(5, 0.05 * ref.cg.iters)
 
 
-def test_warm_start_and_fixed_iterations():
-    prob, om, hm, m, x_dev = _setup("c2")
+@pytest.mark.parametrize("name", ["c2", "c5s"])
+def test_warm_start_and_fixed_iterations(name):
+    prob, om, hm, m, x_dev = _setup(name)
     u = torch.zeros(om.n_dof, dtype=torch.float64, device="cuda")
     st = m.tosolve_cg(prob.penal, x_dev, u, rtol=1e-10, max_iter=50000)
     st2 = m.tosolve_cg(prob.penal, x_dev, u, rtol=1e-8, max_iter=50000, flags=1)   # TO_WARM

@@ -57,9 +57,9 @@ def test_kernel_bytes_formula():
     import bench
     # c5: 4,194,304 elements, 4,276,737 nodes, 12,830,211 DOFs
     kb = bench.kernel_bytes(3, 4194304, 4276737, 12830211, True)
-    assert kb["k1"] == 8 * 4194304 + 8 * 4276737 + 48 * 12830211
-    assert abs(kb["k1"] / 1e6 - 683.6) < 0.1
-    assert abs(kb["k2"] / 1e6 - 342.1) < 0.1
+    assert kb["k1"] == 8 * 4194304 + 8 * 4276737 + 64 * 12830211
+    assert abs(kb["k1"] / 1e6 - 888.9) < 0.1
+    assert kb["k2"] == 0
 
 
 def test_reference_arm_json_contract():

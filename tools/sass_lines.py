@@ -41,18 +41,25 @@ def sass_line_map(mangled_substr):
     return funcs[keys[0]] if keys else None
 
 
-def main(rep, kname, n=30):
+def main(rep, kname, n=30, which=-1):
+    """which: index among the report's launches whose demangled name contains
+    the kernel's short name (default: the last one)."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
-    lines = out.splitlines()
-    rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
-    hdr = rows[0]
+    rows = list(csv.reader(io.StringIO(out)))
+    blocks, cur = [], None
+    for r in rows:
+        if r and r[0] == "Kernel Name":
+            cur = {"name": r[1], "rows": []}
+            blocks.append(cur)
+        elif cur is not None:
+            cur["rows"].append(r)
+    short = re.sub(r"I.*", "", re.sub(r"^_ZN\d+tomesh\d+", "", kname))
+    cand = [b for b in blocks if short in b["name"]]
+    blk = cand[which]
+    hdr = blk["rows"][0]
     ci = {h: i for i, h in enumerate(hdr)}
     stall_cols = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
-    body = []
-    for r in rows[1:]:
-        if not r or r[0] in ("Address", "Kernel Name"):
-            break
-        body.append(r)
+    body = blk["rows"][1:]
     base = int(body[0][ci["Address"]], 16)
     fmap = sass_line_map(kname)
     bymap = {off: ln for off, ln, _ in fmap} if fmap else {}
@@ -78,4 +85,5 @@ def main(rep, kname, n=30):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 30)
+    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 30,
+         int(sys.argv[4]) if len(sys.argv) > 4 else -1)
