@@ -19,6 +19,7 @@ HEADERS = ["common.h", "device_common.cuh", "element.h", "kernels_cg.cuh", "kern
            "kernels_struct3d.cuh", "kernels_struct2d.cuh"]
 
 NVCC_FLAGS = [
+    *([f"-DTOMESH_S3_TYW={os.environ['TOMESH_S3_TYW']}"] if os.environ.get("TOMESH_S3_TYW") else []),
     "-O3", "-std=c++17", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-Xcompiler", "-fPIC,-fopenmp,-O3",

@@ -78,6 +78,8 @@ __device__ __forceinline__ int64_t s3_nrow(const GridView &G, int j, int k) {
 
 constexpr int s3_pad128(int doubles) { return (doubles + 15) / 16 * 16; }   // 128-byte multiple
 
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
 enum { S3_PLAIN = 0, S3_CG = 1 };
 
 template <int TYW>
@@ -91,11 +93,10 @@ struct S3Smem {
   double dn[kS3NBuf][PN];                                     // Dinv per node, TMA box
   double pn[3][PY][kS3RowD];                                  // p_k ring: planes k mod 3
   double own[3][4][TYW * 32];                                 // owned node of plane k mod 3: z_k (3), Dinv
-  double xch[2][TYW][3][32];                                  // y-exchange (layer parity)
+  double xch[2][TYW - 1][3][32];                              // y-exchange (layer parity); row TYW-1 sends to nobody
   unsigned long long mbar[kS3NBuf];
+  int fcnt[kS3NBuf];                                          // warps done forming from each staging buffer
 };
-
-__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
@@ -157,15 +158,24 @@ template <int TYW, int MODE>
 __device__ __forceinline__ void s3_form_node(const S3Smem<TYW> &sm, int b, int row, int col, int off, int noff,
                                              double alpha, double beta, bool pin, double (&rv)[3], double (&pv)[3],
                                              double &dv) {
+  // The staged q and p are finite (every buffer is zeroed at upload and only
+  // ever holds finite iterates), so alpha = 0 / beta = 0 need no special case.
   const int o = row * kS3RowD + off + 3 * col;
-  dv = (MODE == S3_CG && pin) ? sm.dn[b][row * kS3RowN + noff + col] : 0.0;
+  if (!pin) {
+    dv = 0.0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) rv[d] = pv[d] = 0.0;
+    return;
+  }
+  dv = MODE == S3_CG ? sm.dn[b][row * kS3RowN + noff + col] : 0.0;
+  const double a_eff = dv != 0.0 ? -alpha : 0.0;   // r changes on free nodes only
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    double r = pin ? sm.ra[b][o + d] : 0.0;
+    double r = sm.ra[b][o + d];
     double p = r;
     if (MODE == S3_CG) {
-      if (pin && alpha != 0.0 && dv != 0.0) r = fma(-alpha, sm.qa[b][o + d], r);
-      p = fma(dv, r, (pin && beta != 0.0) ? beta * sm.pa[b][o + d] : 0.0);
+      r = fma(a_eff, sm.qa[b][o + d], r);
+      p = fma(dv, r, beta * sm.pa[b][o + d]);
     }
     rv[d] = r;
     pv[d] = p;
@@ -180,16 +190,18 @@ __device__ __forceinline__ void s3_form_node(const S3Smem<TYW> &sm, int b, int r
 //   and the stop test on rr_k.
 // MODE = S3_PLAIN: q = C^T K C v for a v that vanishes on non-free DOFs.
 //
-// Per CTA the layers ek = k_lo-1 .. k_hi-1 run with one barrier each:
-//   1. element ek from p planes ek, ek+1 (ring slots ek%3, (ek+1)%3) -> y-exchange write
+// Per CTA the layers ek = k_lo-1 .. k_hi-1 run with one CTA barrier each:
+//   1. element ek from p planes ek, ek+1 (ring slots ek%3, (ek+1)%3); x routing
+//      by warp shuffle; upper-row corners to the y-exchange (layer parity)
 //   2. barrier
-//   3. y-exchange read, q of node plane ek (owned) and its dot products;
-//      refill the staging buffer of plane ek+2 with plane ek+2+NBUF
-//   4. wait for plane ek+3, form it into ring slot (ek+3)%3 (= ek%3, free
-//      since step 2); owners write r_k, p_k, update x, keep z_k, Dinv for step 3
-// Plane P is issued during layer P-2-NBUF, waited for during layer P-3.
+//   3. y-exchange read: q and the dots of the owned node of plane ek
+//   4. form plane ek+3 into ring slot ek%3 (free since step 2) from the TMA
+//      staging; owners write r_k, p_k, update x, keep z_k, Dinv for step 3.
+//      The last warp done with a staging buffer issues its next plane (+NBUF).
+// (A variant with neighbour-only progress counters instead of the barrier was
+// measured 18% slower: the counter handshakes cost more than the barrier.)
 template <int TYW, int MODE>
-__global__ void __launch_bounds__(32 * TYW, 2)
+__global__ void __launch_bounds__(32 * TYW, TYW <= 8 ? 2 : 1)
 k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3Maps M, double *__restrict__ rnew,
            double *__restrict__ pnew, double *__restrict__ x, double *__restrict__ q,
            const __grid_constant__ K0Had3 H, CgScalars *S, double *partials, int kit, double rtol, double *hist) {
@@ -217,24 +229,34 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
   const bool xupd = CG && owner && alpha_old != 0.0;
   const int64_t plane_d = (int64_t)G.NY * G.RS;        // doubles per node plane
 
+  auto buf_of = [&](int k) { return (k - (k_lo - 1)) % kS3NBuf; };
+  auto staged = [&](int k) { return k >= 0 && k < G.NZ && k <= k_hi; };
   if (tid == 0) {
-    for (int bb = 0; bb < kS3NBuf; ++bb) mbar_init(&sm.mbar[bb], 1);
+    for (int bb = 0; bb < kS3NBuf; ++bb) {
+      mbar_init(&sm.mbar[bb], 1);
+      sm.fcnt[bb] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  auto buf_of = [&](int k) { return (k - (k_lo - 1)) % kS3NBuf; };
-  auto staged = [&](int k) { return k >= 0 && k < G.NZ && k <= k_hi; };
-  // prologue: issue planes k_lo-1 .. k_lo-2+NBUF
+  // initial staging: planes k_lo-1 .. k_lo-2+NBUF; afterwards plane P is
+  // issued by the last warp to finish forming plane P-NBUF (same buffer)
   if (tid == 0)
     for (int k = k_lo - 1; k < k_lo - 1 + kS3NBuf; ++k)
       if (staged(k)) s3_issue_plane<TYW, MODE>(sm, buf_of(k), M, i0, j0, k, off, noff);
   unsigned phase = 0;                                   // parity bit per buffer
 
-  double xr[3] = {0.0, 0.0, 0.0};                       // x of the owned node of the next plane to form
-  if (xupd && k_lo < k_hi) {
+  // x of the owned node, two planes ahead: slot xa holds planes k_lo, k_lo+2,
+  // ..., slot xb planes k_lo+1, k_lo+3, ... (each slot is a fixed register
+  // triple: the 2x-unrolled layer loop alternates them)
+  double xa[3] = {0.0, 0.0, 0.0}, xb[3] = {0.0, 0.0, 0.0};
+  if (xupd) {
     const int64_t dof = s3_row(G, ej, k_lo) + 3 * ei;
 #pragma unroll
-    for (int d = 0; d < 3; ++d) xr[d] = __ldcs(&x[dof + d]);
+    for (int d = 0; d < 3; ++d) {
+      if (k_lo < k_hi) xa[d] = __ldcs(&x[dof + d]);
+      if (k_lo + 1 < k_hi) xb[d] = __ldcs(&x[dof + plane_d + d]);
+    }
   }
   double dots[5] = {0.0, 0.0, 0.0, 0.0, 0.0};           // rho, rr, p.q, q.z, q.Dinv q
 
@@ -244,7 +266,7 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
   // warp does at most two rounds.
   const int xe = tx * TYW + ty;                         // this thread's extra halo node, if < 33 + TYW
   const int xe_row = xe < 33 ? TYW : xe - 33, xe_col = xe < 33 ? xe : 32;
-  auto form_plane = [&](int k) {
+  auto form_plane = [&](int k, double(&xs)[3]) {
     const bool pin = k >= 0 && k < G.NZ;
     const int bb = buf_of(k);
     if (pin) {
@@ -260,8 +282,8 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
     if (CG) {
       const bool mine = owner && k >= k_lo && k < k_hi;
 #pragma unroll
-      for (int d = 0; d < 3; ++d) sm.own[slot][d][tid] = mine ? dv * rv[d] : 0.0;
-      sm.own[slot][3][tid] = mine ? dv : 0.0;
+      for (int d = 0; d < 3; ++d) sm.own[slot][d][tid] = dv * rv[d];   // read back only if mine
+      sm.own[slot][3][tid] = dv;
       if (mine) {
         const int64_t dof = s3_row(G, ej, k) + 3 * ei;
 #pragma unroll
@@ -274,10 +296,10 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
         if (xupd) {
           const double *pp = &sm.pa[bb][ty * kS3RowD + off + 3 * tx];
 #pragma unroll
-          for (int d = 0; d < 3; ++d) __stcs(&x[dof + d], fma(alpha_old, pp[d], xr[d]));
-          if (k + 1 < k_hi) {
+          for (int d = 0; d < 3; ++d) __stcs(&x[dof + d], fma(alpha_old, pp[d], xs[d]));
+          if (k + 2 < k_hi) {
 #pragma unroll
-            for (int d = 0; d < 3; ++d) xr[d] = __ldcs(&x[dof + plane_d + d]);
+            for (int d = 0; d < 3; ++d) xs[d] = __ldcs(&x[dof + 2 * plane_d + d]);
           }
         }
       }
@@ -287,37 +309,43 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
 #pragma unroll
       for (int d = 0; d < 3; ++d) dst[xe_row][off + 3 * xe_col + d] = pv[d];
     }
+    // staging buffer bb: the last warp done with plane k refills it with
+    // plane k+NBUF (monotone count: round r completes at TYW (r+1))
+    if (tx == 0) {
+      const int round = (k - (k_lo - 1)) / kS3NBuf;
+      int old;
+      asm volatile("atom.acq_rel.cta.shared.add.u32 %0, [%1], 1;\n" : "=r"(old) : "r"(smem_u32(&sm.fcnt[bb])) : "memory");
+      if (old == TYW * (round + 1) - 1 && staged(k + kS3NBuf))
+        s3_issue_plane<TYW, MODE>(sm, bb, M, i0, j0, k + kS3NBuf, off, noff);
+    }
+    __syncwarp();
   };
-  // prologue forms planes k_lo-1 .. k_lo+1; the loop's layer ek issues plane
-  // ek+2+NBUF, so the prologue issues every plane up to k_lo+NBUF, each once
-  // the plane NBUF below it (same buffer) has been formed by all threads
-  for (int k = k_lo - 1; k <= min(k_lo + 1, k_hi); ++k) {
-    form_plane(k);
-    __syncthreads();
-    const int kn = k + kS3NBuf;
-    if (tid == 0 && kn <= k_lo + kS3NBuf && staged(kn)) s3_issue_plane<TYW, MODE>(sm, buf_of(kn), M, i0, j0, kn, off, noff);
-  }
+  // prologue: planes k_lo-1 .. k_lo+1 (no element has read a ring slot yet)
+  for (int k = k_lo - 1; k <= min(k_lo + 1, k_hi); ++k) form_plane(k, k == k_lo + 1 ? xb : xa);
+  __syncthreads();
 
   // per-layer carries: contributions of layer ek-1's upper corners
   double own_carry[3] = {0.0, 0.0, 0.0};                // to node (ei, ej, ek)
   double up_carry[3] = {0.0, 0.0, 0.0};                 // to node (ei, ej+1, ek), sent to row ty+1
   // s_e of this thread's element column, loaded two layers ahead (register ring)
   const int64_t s_stride = (int64_t)G.EX * G.EY;
-  const int64_t s_col = (int64_t)ei + (int64_t)G.EX * ej;
-  auto load_s = [&](int ek) {
-    return (col_el && ek >= 0 && ek < G.EZ && ek < k_hi) ? __ldg(&s[s_col + s_stride * ek]) : 0.0;
-  };
-  double s_n1 = load_s(k_lo - 1), s_n2 = load_s(k_lo);
+  // the load itself is unconditional (clamped to a valid element) so that no
+  // select waits on it; the validity mask is applied two layers later
+  const int64_t s_col_c = (int64_t)min(max(ei, 0), G.EX - 1) + (int64_t)G.EX * min(max(ej, 0), G.EY - 1);
+  auto load_s = [&](int ek) { return __ldg(&s[s_col_c + s_stride * min(max(ek, 0), G.EZ - 1)]); };
+  auto s_valid = [&](int ek) { return col_el && ek >= 0 && ek < G.EZ && ek < k_hi; };
+  // two slots, used alternately by even/odd layers of the 2x-unrolled loop
+  // below, so the prefetch lands in its own register (no rotation moves that
+  // would wait on the load)
+  double s_a = load_s(k_lo - 1), s_b = load_s(k_lo);
 
-  for (int ek = k_lo - 1; ek < k_hi; ++ek) {
-    const double se = s_n1;
-    s_n1 = s_n2;
-    s_n2 = load_s(ek + 2);
+  // One layer; no CTA barrier: warp w synchronises with rows w-1 and w+1 only
+  // through the progress counters (it reads row w+1 of the p ring, sends its
+  // upper corners to row w+1 and receives row w-1's).
+  auto layer = [&](const int ek, double &s_slot, double(&x_slot)[3]) {
+    const double se = s_valid(ek) ? s_slot : 0.0;
+    s_slot = load_s(ek + 2);
     const int slo = (ek + 3) % 3, shi = (ek + 4) % 3;
-    double p_own[3];                                    // p_k at the owned node of plane ek
-#pragma unroll
-    for (int d = 0; d < 3; ++d) p_own[d] = sm.pn[slo][ty][off + 3 * tx + d];
-    const bool el = col_el && ek >= 0 && ek < G.EZ;
     double y[24];
     {
 #pragma unroll
@@ -327,11 +355,10 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
 #pragma unroll
         for (int d = 0; d < 3; ++d) y[3 * c + d] = row[d];
       }
-      had_apply_inplace(H, y);
-      const double sc = el ? se : 0.0;
-#pragma unroll
-      for (int a = 0; a < 24; ++a) y[a] *= sc;
     }
+    had_apply_inplace(H, y);
+#pragma unroll
+    for (int a = 0; a < 24; ++a) y[a] *= se;            // se = 0 for elements outside the mesh / segment
     // x routing: corner (1,cy,cz) of element ei goes to node ei+1 (lane + 1)
     double a_row[2][2][3];   // [cy][cz][comp] after the x merge, at node column ei
 #pragma unroll
@@ -340,30 +367,33 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
       for (int cz = 0; cz < 2; ++cz)
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-          double from_left = __shfl_up_sync(0xffffffffu, y[3 * (1 + 2 * cy + 4 * cz) + d], 1);
-          if (tx == 0) from_left = 0.0;
+          // lane 0 receives its own value: garbage, but lane 0 is the halo
+          // column (never an owner), so it needs no select
+          const double from_left = __shfl_up_sync(0xffffffffu, y[3 * (1 + 2 * cy + 4 * cz) + d], 1);
           a_row[cy][cz][d] = y[3 * (2 * cy + 4 * cz) + d] + from_left;
         }
     // y routing: node (ei, ej+1, ek) collects this layer's (cy=1, cz=0) part and
     // the previous layer's (cy=1, cz=1) part; row ty+1 owns it
+    if (ty < TYW - 1) {
 #pragma unroll
-    for (int d = 0; d < 3; ++d) sm.xch[ek & 1][ty][d][tx] = a_row[1][0][d] + up_carry[d];
-    __syncthreads();                                    // the one barrier of the layer
-    if (tid == 0 && staged(ek + 2 + kS3NBuf))
-      s3_issue_plane<TYW, MODE>(sm, buf_of(ek + 2 + kS3NBuf), M, i0, j0, ek + 2 + kS3NBuf, off, noff);
+      for (int d = 0; d < 3; ++d) sm.xch[ek & 1][ty][d][tx] = a_row[1][0][d] + up_carry[d];
+    }
+    __syncthreads();                                    // the one CTA barrier of the layer
     // node plane ek is complete: (cz=0) parts of layer ek + (cz=1) parts of layer ek-1
-    if (ek >= k_lo && owner) {
-      const int64_t dof = s3_row(G, ej, ek) + 3 * ei;
-      const int slot = (ek + 3) % 3;
-      const double dv = CG ? sm.own[slot][3][tid] : 0.0;
+    {
+      if (ek >= k_lo && owner) {
+        const int64_t dof = s3_row(G, ej, ek) + 3 * ei;
+        const int slot = (ek + 3) % 3;
+        const double dv = CG ? sm.own[slot][3][tid] : 0.0;
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double qv = a_row[0][0][d] + own_carry[d] + (ty > 0 ? sm.xch[ek & 1][ty - 1][d][tx] : 0.0);
-        __stcs(&q[dof + d], qv);
-        if (CG) {
-          dots[2] = fma(p_own[d], qv, dots[2]);
-          dots[3] = fma(sm.own[slot][d][tid], qv, dots[3]);
-          dots[4] = fma(dv * qv, qv, dots[4]);
+        for (int d = 0; d < 3; ++d) {
+          const double qv = a_row[0][0][d] + own_carry[d] + sm.xch[ek & 1][ty - 1][d][tx];
+          __stcs(&q[dof + d], qv);
+          if (CG) {
+            dots[2] = fma(sm.pn[slot][ty][off + 3 * tx + d], qv, dots[2]);   // p_k of the own node (this thread formed it)
+            dots[3] = fma(sm.own[slot][d][tid], qv, dots[3]);
+            dots[4] = fma(dv * qv, qv, dots[4]);
+          }
         }
       }
     }
@@ -372,7 +402,14 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
       own_carry[d] = a_row[0][1][d];
       up_carry[d] = a_row[1][1][d];
     }
-    if (ek + 3 <= k_hi) form_plane(ek + 3);
+    if (ek + 3 <= k_hi) {
+      form_plane(ek + 3, x_slot);                       // slot ek%3: free since the barrier
+    }
+  };
+  // ek = k_lo-1+2t forms plane k_lo+2+2t (x slot xa); ek+1 forms k_lo+3+2t (xb)
+  for (int ek = k_lo - 1; ek < k_hi; ek += 2) {
+    layer(ek, s_a, xa);
+    if (ek + 1 < k_hi) layer(ek + 1, s_b, xb);
   }
   if (CG) {
     if (grid_sum<5>(dots, partials, &S->counter[CNT_PQ])) cg_single_step(S, kit, dots, rtol, hist);

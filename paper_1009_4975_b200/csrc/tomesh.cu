@@ -22,7 +22,11 @@
 using namespace tomesh;
 
 namespace tomesh {
-constexpr int kS3TYW = 8;   // warps per CTA (node rows + 1) of the structured H8 apply
+#ifndef TOMESH_S3_TYW
+#define TOMESH_S3_TYW 8
+#endif
+constexpr int kS3TYW = TOMESH_S3_TYW;   // warps per CTA (node rows + 1) of the structured H8 kernel
+constexpr int kS3CtasPerSM = kS3TYW <= 8 ? 2 : 1;
 }
 
 namespace {
@@ -278,7 +282,7 @@ int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof
   G.nty = (G.NY + kS3TYW - 2) / (kS3TYW - 1);
   // z segmentation: balance full waves (2 CTAs/SM) against the one recomputed layer per segment
   {
-    const int64_t base = (int64_t)G.ntx * G.nty, slots = (int64_t)kNumSMs * 2;
+    const int64_t base = (int64_t)G.ntx * G.nty, slots = (int64_t)kNumSMs * kS3CtasPerSM;
     double best = 1e300;
     int best_n = 1;
     for (int nz = 1; nz <= G.NZ; ++nz) {

@@ -87,3 +87,32 @@ def main(rep, kname, n=30, which=-1):
 if __name__ == "__main__":
     main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 30,
          int(sys.argv[4]) if len(sys.argv) > 4 else -1)
+
+
+def top_instructions(rep, kname, line_suffix, n=10, which=-1):
+    """The SASS instructions of one source line with the most samples."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    blocks, cur = [], None
+    for r in rows:
+        if r and r[0] == "Kernel Name":
+            cur = {"name": r[1], "rows": []}
+            blocks.append(cur)
+        elif cur is not None:
+            cur["rows"].append(r)
+    short = re.sub(r"I.*", "", re.sub(r"^_ZN\d+tomesh\d+", "", kname))
+    blk = [b for b in blocks if short in b["name"]][which]
+    hdr = blk["rows"][0]
+    ci = {h: i for i, h in enumerate(hdr)}
+    body = blk["rows"][1:]
+    base = int(body[0][ci["Address"]], 16)
+    fmap = sass_line_map(kname)
+    bymap = {off: (ln, ins) for off, ln, ins in fmap}
+    res = []
+    for r in body:
+        off = int(r[ci["Address"]], 16) - base
+        ln, ins = bymap.get(off, ("?", "?"))
+        if ln.endswith(line_suffix):
+            res.append((int(r[ci["Warp Stall Sampling (All Samples)"]] or 0), hex(off), ins))
+    for t in sorted(res, reverse=True)[:n]:
+        print(t)
