@@ -83,4 +83,32 @@ int build_K0_hadamard(double nu, K0Had3 *out) {
   return bad;
 }
 
+int build_K0_hadamard_sym(const K0Had3 &h, K0HadSym *out) {
+  auto pop = [](int m) { return (m & 1) + ((m >> 1) & 1) + ((m >> 2) & 1); };
+  bool set_d[2][3] = {}, set_o[2][2] = {};
+  for (int i = 0; i < 3; ++i)
+    for (int m = 1; m < 8; ++m) {
+      const int b = (m >> i) & 1, n = pop(m) - b;
+      if (!set_d[b][n]) { out->d[b][n] = h.diag[i][m]; set_d[b][n] = true; }
+      for (int j = 0; j < 3; ++j) {
+        if (j == i || ((m >> j) & 1) == b) continue;
+        const int t = ((m >> (3 - i - j)) & 1);
+        if (!set_o[b][t]) { out->o[b][t] = h.off[i][j][m]; set_o[b][t] = true; }
+      }
+    }
+  out->d[0][0] = 0.0;
+  int bad = 0;
+  auto differs = [](double a, double c) { return std::fabs(a - c) > 1e-15 * std::fmax(std::fabs(c), 1e-300); };
+  for (int i = 0; i < 3; ++i)
+    for (int m = 1; m < 8; ++m) {
+      const int b = (m >> i) & 1, n = pop(m) - b;
+      if (differs(h.diag[i][m], out->d[b][n])) ++bad;
+      for (int j = 0; j < 3; ++j) {
+        if (j == i || ((m >> j) & 1) == b) continue;
+        if (differs(h.off[i][j][m], out->o[b][(m >> (3 - i - j)) & 1])) ++bad;
+      }
+    }
+  return bad;
+}
+
 }  // namespace tomesh

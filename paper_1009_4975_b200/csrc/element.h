@@ -36,7 +36,22 @@ struct K0Had3 {
   double off[3][3][8];
 };
 
+// The 45 nonzero Hadamard coefficients take only 9 distinct values:
+//   diag[i][m] = d[b][n],  b = bit i of m, n = number of the other bits of m set
+//                (d[0][0] = 0: the rigid translation mode);
+//   off[i][j][m] = o[b][t], b = bit i of m (bit j differs), t = bit 3-i-j of m.
+// (Per axis the Hadamard images of the 1D mass, stiffness and gradient
+// matrices are diag(1, 1/3), diag(0, 4) and -2 e1 e0^T, so every coefficient
+// is a product of these per-axis factors with lambda or mu.)
+struct K0HadSym {
+  double d[2][3];
+  double o[2][2];
+};
+
 void build_K0(int dim, double nu, double *K);      // E = 1, h = 1
+// Class values of `h`; returns the number of coefficients that differ from
+// their class value by more than 1e-15 relative (0 expected).
+int build_K0_hadamard_sym(const K0Had3 &h, K0HadSym *out);
 int build_K0_hadamard(double nu, K0Had3 *out);     // returns 0 if the structure check passes
 
 }  // namespace tomesh

@@ -1,17 +1,10 @@
-// Jacobi-PCG vector kernels (textbook Hestenes-Stiefel recurrences on the
-// rescaled system, PAPER.md:511-523 with reading Q3), fused so that every
-// iteration makes one pass of the operator and one pass of the r update:
-//
-//   K1  p_k = Dinv r_k + beta_{k-1} p_{k-1};  x += alpha_{k-1} p_{k-1}
-//       q = A p_k;  alpha_k = rho_k / (p_k . q)
-//   K2  r_{k+1} = r_k - alpha_k q;  rho_{k+1} = r.Dinv r;  rr = r.r
-//       beta_k = rho_{k+1} / rho_k;  stop test on rr
-//   after the loop: x += alpha_last p_last (k_xfinal)
-//
-// p ping-pongs between two buffers (iteration k reads pbuf[(k+1)&1] and
-// writes pbuf[k&1]) because K1 reads p_{k-1} at neighbours' nodes while they
-// write p_k.  Dinv == 0 marks hanging and fixed DOFs: r, p, x stay 0 there
-// (A is the identity on them and b vanishes there, so this is exact).
+// Jacobi-PCG scalar logic and vector kernels shared by both paths (textbook
+// Hestenes-Stiefel recurrences on the rescaled system, PAPER.md:511-523 with
+// reading Q3).  The iteration kernels themselves live in kernels_struct3d.cuh
+// (uniform H8: one kernel per iteration) and kernels_general.cuh (AMR: an
+// element pass and a node pass per iteration).  Dinv == 0 marks hanging and
+// fixed DOFs: r, p, x stay 0 there (A is the identity on them and b vanishes
+// there, so this is exact).
 #pragma once
 #include "device_common.cuh"
 
@@ -122,22 +115,6 @@ __global__ void k_sub_masked(int64_t n, const double *__restrict__ q, const uint
   GRID_STRIDE(i, n) { r[i] = free_dof[i] ? r[i] - q[i] : 0.0; }
 }
 
-// General path K1, elementwise half: p_k, deferred x update, q = 0 (the
-// atomic operator kernel accumulates into q next).
-__global__ void k_pre_g(int64_t n, const double *__restrict__ r, const double *__restrict__ Dinv,
-                        const double *__restrict__ po, double *__restrict__ pn, double *__restrict__ x,
-                        double *__restrict__ q, CgScalars *S) {
-  if (cg_stop_at_apply(S)) return;
-  const double beta = __ldcg(&S->beta), alpha_old = __ldcg(&S->alpha);
-  GRID_STRIDE(i, n) {
-    const double pold = po[i];
-    const double pv = (beta != 0.0) ? beta * pold : 0.0;
-    pn[i] = fma(Dinv[i], r[i], pv);
-    if (alpha_old != 0.0) x[i] = fma(alpha_old, pold, x[i]);
-    q[i] = 0.0;
-  }
-}
-
 // General path K2 (per-DOF Dinv).  INIT: rho0, rr0 only.
 template <bool INIT>
 __global__ void k_rupd(int64_t n, const double *__restrict__ q, const double *__restrict__ Dinv,
@@ -160,16 +137,6 @@ __global__ void k_rupd(int64_t n, const double *__restrict__ q, const double *__
   } else {
     if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) cg_after_rupdate(S, acc[0], acc[1], hist);
   }
-}
-
-// x += alpha_last p_last after the loop (iteration iter-1 wrote pbuf[(iter-1)&1]).
-__global__ void k_xfinal(int64_t n, double *__restrict__ x, const double *__restrict__ p0,
-                         const double *__restrict__ p1, const CgScalars *S) {
-  const int it = S->iter;
-  if (it <= 0 || S->status != 0) return;
-  const double alpha = S->alpha;
-  const double *p = ((it - 1) & 1) ? p1 : p0;
-  GRID_STRIDE(i, n) { x[i] = fma(alpha, p[i], x[i]); }
 }
 
 // sum over free DOFs of (b - t)^2 -> S->tmp[0]

@@ -4,13 +4,14 @@
 //   k_simp        a1  s_e = (E_min + x_e^p (E0 - E_min)) h_e^(d-2)       (Eq. 2)
 //   k_diag_*      a2  D = diag(Pi_F C^T K C Pi_F) (cross terms included)  (:515-521)
 //   k_rhs         a3  b = Pi_F C^T f                                      (Eq. 7 rhs)
-//   k_matvec_*    a4  q = C^T K C p for p vanishing on non-free DOFs       (Eq. 8)
+//   k_elem_pass + k_node_pass  a4-a6  one PCG iteration (or q = C^T K C p)  (Eq. 8)
 //   k_recover     a8  u = C u_hat                                         (Eq. 9)
 //   k_sens        a10 dc_e = -p x^(p-1)(E0-Emin) h^(d-2) u_e^T K0 u_e    (:343-346)
 //   k_filter      a11 Eq. 5 / density variant                             (:613-616)
 #pragma once
 #include "device_common.cuh"
 #include "element.h"
+#include "kernels_cg.cuh"
 
 namespace tomesh {
 
@@ -43,51 +44,47 @@ __global__ void k_simp(int64_t n, const double *__restrict__ x, const int8_t *__
 }
 
 // ---- Jacobi diagonal (a2) ---------------------------------------------------------
+// D_(n,i) = sum_e s_e sum_{a,b} w_a w_b K0[(a,i),(b,i)] over the corners a, b of
+// element e that map to node n (directly with w = 1, or as a hanging corner
+// with its Eq. 6 weight): the diagonal of C^T K C with the cross terms of two
+// hanging corners sharing a parent (reading Q4).  Node-centric over the
+// incidence CSR (entries of one element are consecutive): no atomics, so D is
+// bit-reproducible.
 template <int DIM>
-__global__ void k_diag(MeshView M, const double *__restrict__ s, double *__restrict__ D,
-                       const __grid_constant__ typename std::conditional<DIM == 2, K0Dense2, K0Dense3>::type K0) {
+__global__ void k_diag_node(int64_t n_node, const int64_t *__restrict__ inc_ptr, const uint32_t *__restrict__ inc,
+                            const double *__restrict__ s,
+                            const __grid_constant__ typename std::conditional<DIM == 2, K0Dense2, K0Dense3>::type K0,
+                            double *__restrict__ D) {
   constexpr int NC = 1 << DIM, ND = DIM * NC;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M.n_el; e += (int64_t)gridDim.x * blockDim.x) {
-    const double se = s[e];
-    int tgt[NC * 4], cor[NC * 4];
-    double w[NC * 4];
-    int nt = 0;
-    bool any_h = false;
-    for (int c = 0; c < NC; ++c) {
-      int n = M.elem_node[e * NC + c];
-      int h = M.node_hang[n];
-      if (h < 0) {
-        tgt[nt] = n; cor[nt] = c; w[nt] = 1.0; ++nt;
-      } else {
-        any_h = true;
-        for (int k = M.hang_ptr[h]; k < M.hang_ptr[h + 1]; ++k) {
-          tgt[nt] = M.hang_parent[k]; cor[nt] = c; w[nt] = M.hang_weight[k]; ++nt;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_node; n += (int64_t)gridDim.x * blockDim.x) {
+    double acc[DIM];
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) acc[i] = 0.0;
+    const int64_t k1 = inc_ptr[n + 1];
+    int64_t k = inc_ptr[n];
+    while (k < k1) {
+      const uint32_t e = (inc[k] & 0x3fffffffu) / NC;
+      int64_t kend = k;
+      while (kend < k1 && (inc[kend] & 0x3fffffffu) / NC == e) ++kend;   // this element's corners
+      double el[DIM];
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) el[i] = 0.0;
+      for (int64_t a = k; a < kend; ++a)
+        for (int64_t b = k; b < kend; ++b) {
+          const uint32_t ta = inc[a], tb = inc[b];
+          const int ca = (int)((ta & 0x3fffffffu) % NC), cb = (int)((tb & 0x3fffffffu) % NC);
+          const double wa = (ta >> 30) == 0 ? 1.0 : (ta >> 30) == 1 ? 0.5 : 0.25;
+          const double wb = (tb >> 30) == 0 ? 1.0 : (tb >> 30) == 1 ? 0.5 : 0.25;
+#pragma unroll
+          for (int i = 0; i < DIM; ++i) el[i] += wa * wb * K0.K[(DIM * ca + i) * ND + DIM * cb + i];
         }
-      }
+      const double se = s[e];
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) acc[i] = fma(se, el[i], acc[i]);
+      k = kend;
     }
-    if (!any_h) {
-      for (int c = 0; c < NC; ++c)
-        for (int i = 0; i < DIM; ++i)
-          atomicAdd(&D[(int64_t)tgt[c] * DIM + i], se * K0.K[(DIM * c + i) * ND + DIM * c + i]);
-      continue;
-    }
-    for (int t1 = 0; t1 < nt; ++t1) {
-      bool first = true;
-      for (int t0 = 0; t0 < t1; ++t0)
-        if (tgt[t0] == tgt[t1]) first = false;
-      if (!first) continue;
-      for (int i = 0; i < DIM; ++i) {
-        double acc = 0.0;
-        for (int a = 0; a < nt; ++a) {
-          if (tgt[a] != tgt[t1]) continue;
-          for (int b = 0; b < nt; ++b) {
-            if (tgt[b] != tgt[t1]) continue;
-            acc += w[a] * w[b] * K0.K[(DIM * cor[a] + i) * ND + DIM * cor[b] + i];
-          }
-        }
-        atomicAdd(&D[(int64_t)tgt[t1] * DIM + i], se * acc);
-      }
-    }
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) D[n * DIM + i] = acc[i];
   }
 }
 
@@ -220,7 +217,8 @@ __device__ __forceinline__ double had_mid_one(const K0Had3 &H, const double (&x)
 // three singletons (m = 7) and the rigid-translation mode m = 0, whose
 // output is zero.  Each group is evaluated from its inputs before it is
 // written back, so no second 24-vector is live (register pressure).
-__device__ __forceinline__ void had_mid_inplace(const K0Had3 &H, double (&x)[24]) {
+template <typename HC>
+__device__ __forceinline__ void had_mid_inplace(const HC &H, double (&x)[24]) {
 #define HAD_G3(m0, i0, m1, i1, m2, i2)                                                                      \
   {                                                                                                         \
     const double a = had_mid_one(H, x, m0, i0), b = had_mid_one(H, x, m1, i1), c = had_mid_one(H, x, m2, i2); \
@@ -243,14 +241,67 @@ __device__ __forceinline__ void had_mid_inplace(const K0Had3 &H, double (&x)[24]
   HAD_G2(6, 2, 3, 0)
   HAD_G2(5, 2, 3, 1)
 #pragma unroll
-  for (int i = 0; i < 3; ++i) x[21 + i] *= H.diag[i][7];
+  for (int i = 0; i < 3; ++i) x[21 + i] = had_mid_one(H, x, 7, i);
   x[0] = x[1] = x[2] = 0.0;
 #undef HAD_G3
 #undef HAD_G2
 }
 
+// Same products with the 9 class values of the coefficients (element.h
+// K0HadSym): the compiler keeps 9 doubles live instead of reloading 45.
+__device__ __forceinline__ double had_mid_one(const K0HadSym &H, const double (&x)[24], int m, int i) {
+  const int b = (m >> i) & 1;
+  const int n = (m & 1) + ((m >> 1) & 1) + ((m >> 2) & 1) - b;
+  double acc = H.d[b][n] * x[3 * m + i];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    if (j == i || ((m >> j) & 1) == b) continue;
+    acc = fma(H.o[b][(m >> (3 - i - j)) & 1], x[3 * (m ^ ((1 << i) | (1 << j))) + j], acc);
+  }
+  return acc;
+}
+
+// In-place middle product that also accumulates x^T K0 x = sum xhat . yhat
+// (K0 = H Khat H with the 1/64 folded into Khat), group by group.
+template <typename HC>
+__device__ __forceinline__ void had_mid_inplace_energy(const HC &H, double (&x)[24], double &en) {
+#define HAD_E3(m0, i0, m1, i1, m2, i2)                                                                      \
+  {                                                                                                         \
+    const double a = had_mid_one(H, x, m0, i0), b = had_mid_one(H, x, m1, i1), c = had_mid_one(H, x, m2, i2); \
+    en = fma(a, x[3 * m0 + i0], fma(b, x[3 * m1 + i1], fma(c, x[3 * m2 + i2], en)));                         \
+    x[3 * m0 + i0] = a;                                                                                     \
+    x[3 * m1 + i1] = b;                                                                                     \
+    x[3 * m2 + i2] = c;                                                                                     \
+  }
+#define HAD_E2(m0, i0, m1, i1)                                                   \
+  {                                                                              \
+    const double a = had_mid_one(H, x, m0, i0), b = had_mid_one(H, x, m1, i1); \
+    en = fma(a, x[3 * m0 + i0], fma(b, x[3 * m1 + i1], en));                     \
+    x[3 * m0 + i0] = a;                                                          \
+    x[3 * m1 + i1] = b;                                                          \
+  }
+  HAD_E3(1, 0, 2, 1, 4, 2)
+  HAD_E2(1, 1, 2, 0)
+  HAD_E2(1, 2, 4, 0)
+  HAD_E2(2, 2, 4, 1)
+  HAD_E3(6, 0, 5, 1, 3, 2)
+  HAD_E2(6, 1, 5, 0)
+  HAD_E2(6, 2, 3, 0)
+  HAD_E2(5, 2, 3, 1)
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double a = had_mid_one(H, x, 7, i);
+    en = fma(a, x[21 + i], en);
+    x[21 + i] = a;
+  }
+  x[0] = x[1] = x[2] = 0.0;
+#undef HAD_E3
+#undef HAD_E2
+}
+
 // x := K0 x for H8 via the Hadamard factorisation (element.h), in place.
-__device__ __forceinline__ void had_apply_inplace(const K0Had3 &H, double (&x)[24]) {
+template <typename HC>
+__device__ __forceinline__ void had_apply_inplace(const HC &H, double (&x)[24]) {
   wht8x3(x);
   had_mid_inplace(H, x);
   wht8x3(x);
@@ -263,48 +314,77 @@ __device__ __forceinline__ void had_apply(const K0Had3 &H, double (&x)[24], doub
   for (int a = 0; a < 24; ++a) y[a] = x[a];
 }
 
-// ---- operator apply, atomic scatter ------------------------------------------------------
-// q += C^T (s_e K0) C p per element (q zeroed by the caller).  With S (CG
-// mode): p^T A p = sum_e s_e pbar_e^T K0 pbar_e (pbar_e = C_e p, p vanishing
-// on non-free DOFs) is reduced in the same pass and the last block forms
-// alpha_k = rho_k / p^T A p, so no separate p.q pass is needed.
-template <int DIM>
-__global__ void k_matvec_atomic(MeshView M, const double *__restrict__ s, const double *__restrict__ p,
-                                double *__restrict__ q,
-                                const __grid_constant__ typename std::conditional<DIM == 2, K0Dense2, K0Dense3>::type K0,
-                                CgScalars *S, double *partials) {
+// ---- general path, one PCG iteration = element pass + node pass --------------------------
+// Deterministic and atomic-free (the paper's operator, Eq. 8, assembled on
+// the fly): the element pass stores y_e = s_e K0 (C_e p)_e per element; the
+// node pass sums, for each node, the (element, corner, weight) incidences of
+// the precomputed CSR (weights 1, or the hanging-node interpolation weights of
+// Eq. 6 for the parents of a hanging corner), i.e. q = C^T K C p.
+enum { G_PLAIN = 0, G_CG = 1 };
+
+// p of DOF d: CG: Dinv r + beta p_{k-1} (formed on the fly; the node pass
+// stores the same value); plain: v.
+template <int MODE>
+__device__ __forceinline__ double g_p(const double *__restrict__ r, const double *__restrict__ Dinv,
+                                      const double *__restrict__ po, double beta, int64_t d) {
+  if (MODE == G_PLAIN) return po[d];
+  return fma(Dinv[d], r[d], beta * po[d]);
+}
+
+template <int DIM, int MODE>
+__global__ void __launch_bounds__(256) k_elem_pass(MeshView M, const double *__restrict__ s,
+                                                   const double *__restrict__ r, const double *__restrict__ Dinv,
+                                                   const double *__restrict__ po, double *__restrict__ ye,
+                                                   const __grid_constant__ K0Dense2 K2, const __grid_constant__ K0HadSym H,
+                                                   CgScalars *S, double *partials) {
   constexpr int NC = 1 << DIM, ND = DIM * NC;
-  if (S && cg_stopped(S)) return;
+  if (MODE == G_CG && cg_stopped(S)) return;
+  const double beta = MODE == G_CG ? __ldcg(&S->beta) : 0.0;
   double pq = 0.0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M.n_el; e += (int64_t)gridDim.x * blockDim.x) {
-    double ue[ND], ye[ND];
-    int node[NC], hang[NC];
-    gather_C<DIM>(M, e, p, ue, node, hang);
-    dense_apply<ND>(K0.K, ue, ye);
-    const double se = s[e];
-    if (S) {
-      double en = 0.0;
-#pragma unroll
-      for (int a = 0; a < ND; ++a) en = fma(ue[a], ye[a], en);
-      pq = fma(se, en, pq);
-    }
+    double y[ND];
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-      if (hang[c] < 0) {
+      const int n = M.elem_node[e * NC + c];
+      const int h = M.node_hang[n];
+      if (h < 0) {
 #pragma unroll
-        for (int i = 0; i < DIM; ++i) atomicAdd(&q[(int64_t)node[c] * DIM + i], se * ye[DIM * c + i]);
+        for (int i = 0; i < DIM; ++i) y[DIM * c + i] = g_p<MODE>(r, Dinv, po, beta, (int64_t)n * DIM + i);
       } else {
-        int h = hang[c];
-        for (int k = M.hang_ptr[h]; k < M.hang_ptr[h + 1]; ++k) {
-          double w = se * M.hang_weight[k];
-          int64_t pn = M.hang_parent[k];
+        double acc[DIM];
 #pragma unroll
-          for (int i = 0; i < DIM; ++i) atomicAdd(&q[pn * DIM + i], w * ye[DIM * c + i]);
+        for (int i = 0; i < DIM; ++i) acc[i] = 0.0;
+        for (int k = M.hang_ptr[h]; k < M.hang_ptr[h + 1]; ++k) {
+          const double w = M.hang_weight[k];
+          const int64_t pn = M.hang_parent[k];
+#pragma unroll
+          for (int i = 0; i < DIM; ++i) acc[i] = fma(w, g_p<MODE>(r, Dinv, po, beta, pn * DIM + i), acc[i]);
         }
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) y[DIM * c + i] = acc[i];
       }
     }
+    const double se = s[e];
+    double en = 0.0;
+    if constexpr (DIM == 3) {
+      wht8x3(y);
+      had_mid_inplace_energy(H, y, en);
+      wht8x3(y);
+    } else {
+      double t[ND];
+      dense_apply<ND>(K2.K, y, t);
+#pragma unroll
+      for (int a = 0; a < ND; ++a) {
+        en = fma(y[a], t[a], en);
+        y[a] = t[a];
+      }
+    }
+    pq = fma(se, en, pq);
+    double2 *dst = reinterpret_cast<double2 *>(ye + e * ND);
+#pragma unroll
+    for (int a = 0; a < ND / 2; ++a) dst[a] = make_double2(se * y[2 * a], se * y[2 * a + 1]);
   }
-  if (S) {
+  if (MODE == G_CG) {
     double v[1] = {pq};
     if (grid_sum<1>(v, partials, &S->counter[CNT_PQ])) {
       if (!(v[0] > 0.0)) {
@@ -317,7 +397,85 @@ __global__ void k_matvec_atomic(MeshView M, const double *__restrict__ s, const 
   }
 }
 
+// Node pass.  q_n = sum over the incidences of n of w * y_e[corner] (packed
+// entry: element*2^DIM + corner in bits 0-29, weight code in bits 30-31:
+// 0 -> 1, 1 -> 1/2, 2 -> 1/4).
+//   plain: q_out = q (all DOFs; the caller masks);
+//   CG (iteration k, alpha_k known): on free DOFs p_k = Dinv r_k + beta p_{k-1}
+//   (stored in place), x += alpha_k p_k, r -= alpha_k q; reduce
+//   rho_{k+1} = r.Dinv r and rr -> beta_k and the stop test.
+template <int DIM, int MODE>
+__global__ void __launch_bounds__(256) k_node_pass(int64_t n_node, const int64_t *__restrict__ inc_ptr,
+                                                   const uint32_t *__restrict__ inc, const double *__restrict__ ye,
+                                                   double *__restrict__ r, const double *__restrict__ Dinv,
+                                                   double *__restrict__ p, double *__restrict__ x,
+                                                   double *__restrict__ q_out, double *partials, CgScalars *S,
+                                                   double *hist) {
+  if (MODE == G_CG && cg_stopped(S)) return;
+  const double beta = MODE == G_CG ? __ldcg(&S->beta) : 0.0;
+  const double alpha = MODE == G_CG ? __ldcg(&S->alpha) : 0.0;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_node; n += (int64_t)gridDim.x * blockDim.x) {
+    double qv[DIM];
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) qv[i] = 0.0;
+    const int64_t k1 = inc_ptr[n + 1];
+    for (int64_t k = inc_ptr[n]; k < k1; ++k) {
+      const uint32_t t = __ldg(&inc[k]);
+      const double w = (t >> 30) == 0 ? 1.0 : (t >> 30) == 1 ? 0.5 : 0.25;
+      const double *src = ye + (int64_t)(t & 0x3fffffffu) * DIM;
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) qv[i] = fma(w, __ldg(&src[i]), qv[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) {
+      const int64_t d = n * DIM + i;
+      if (MODE == G_PLAIN) {
+        q_out[d] = qv[i];
+      } else {
+        const double di = Dinv[d];
+        if (di != 0.0) {
+          const double pk = fma(di, r[d], beta * p[d]);
+          p[d] = pk;
+          x[d] = fma(alpha, pk, x[d]);
+          const double rn = fma(-alpha, qv[i], r[d]);
+          r[d] = rn;
+          acc[0] = fma(rn, di * rn, acc[0]);
+          acc[1] = fma(rn, rn, acc[1]);
+        }
+      }
+    }
+  }
+  if (MODE == G_CG) {
+    if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) {
+      cg_after_rupdate(S, acc[0], acc[1], hist);
+      if (S->done_next) S->done = 1;                 // x is already complete
+    }
+  }
+}
+
 // ---- sensitivities (a10) ----------------------------------------------------------------
+// 3D: u_e^T K0 u_e from the Hadamard middle product (sum xhat . yhat).
+__global__ void __launch_bounds__(256) k_sens_had3(MeshView M, const double *__restrict__ x,
+                                                   const double *__restrict__ u, double penal, double E0, double Emin,
+                                                   double *__restrict__ dc, const __grid_constant__ K0HadSym H) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M.n_el; e += (int64_t)gridDim.x * blockDim.x) {
+    double ue[24];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int64_t n = M.elem_node[e * 8 + c];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) ue[3 * c + i] = u[n * 3 + i];
+    }
+    wht8x3(ue);
+    double en = 0.0;
+    had_mid_inplace_energy(H, ue, en);
+    const double h = M.hL * (double)(1 << (M.L - M.elem_level[e]));
+    const double xe = x[e];
+    dc[e] = -penal * pow(xe, penal - 1.0) * (E0 - Emin) * h * en;
+  }
+}
+
 template <int DIM>
 __global__ void k_sens(MeshView M, const double *__restrict__ x, const double *__restrict__ u, double penal,
                        double E0, double Emin, double *__restrict__ dc,

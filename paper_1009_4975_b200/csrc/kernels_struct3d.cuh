@@ -204,7 +204,7 @@ template <int TYW, int MODE>
 __global__ void __launch_bounds__(32 * TYW, TYW <= 8 ? 2 : 1)
 k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3Maps M, double *__restrict__ rnew,
            double *__restrict__ pnew, double *__restrict__ x, double *__restrict__ q,
-           const __grid_constant__ K0Had3 H, CgScalars *S, double *partials, int kit, double rtol, double *hist) {
+           const __grid_constant__ K0HadSym H, CgScalars *S, double *partials, int kit, double rtol, double *hist) {
   constexpr bool CG = MODE == S3_CG;
   if (CG && cg_stopped(S)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];

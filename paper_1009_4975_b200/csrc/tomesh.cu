@@ -52,6 +52,9 @@ struct to_mesh {
   double *hang_weight = nullptr, *child_weight = nullptr, *load = nullptr;
   uint8_t *free_dof = nullptr;
   int64_t *filt_ptr = nullptr;
+  int64_t *inc_ptr = nullptr;          // general path: node -> (element, corner, weight) incidences
+  uint32_t *inc = nullptr;
+  double *ye = nullptr;                // general path: element vectors s_e K0 C_e p
   int32_t *filt_idx = nullptr;
   // workspace
   double *s = nullptr, *x = nullptr, *r = nullptr, *q = nullptr, *dinv = nullptr, *D = nullptr;
@@ -67,6 +70,7 @@ struct to_mesh {
   K0Dense2 K2{};
   K0Dense3 K3{};
   K0Had3 KH{};
+  K0HadSym KS{};
   // structured fast path (uniform H8 box)
   bool structured = false, force_general = false;
   GridView G{};
@@ -343,6 +347,47 @@ int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof
   return 0;
 }
 
+
+// General path: node -> (element, corner, weight) incidence CSR, the transpose
+// of the gather C_e P_e: a non-hanging corner contributes to its node with
+// weight 1, a hanging corner to each parent with the Eq. 6 weight.  Entries
+// per node in ascending (element, corner) order (deterministic sums).
+int setup_incidence(const to_mesh_desc *d, const std::vector<int32_t> &node_hang, cudaStream_t st, to_mesh *m) {
+  const int nc = 1 << d->dim;
+  if ((int64_t)d->n_elem * nc >= (1LL << 30)) { set_error("mesh too large for the packed incidence list"); return TO_EINVAL; }
+  std::vector<int64_t> ptr(d->n_node + 1, 0);
+  for (int64_t e = 0; e < d->n_elem; ++e)
+    for (int c = 0; c < nc; ++c) {
+      const int32_t n = d->elem_node[e * nc + c];
+      const int32_t h = node_hang[n];
+      if (h < 0) ptr[n + 1]++;
+      else
+        for (int32_t k = d->hang_ptr[h]; k < d->hang_ptr[h + 1]; ++k) ptr[d->hang_parent[k] + 1]++;
+    }
+  for (int64_t n = 0; n < d->n_node; ++n) ptr[n + 1] += ptr[n];
+  std::vector<uint32_t> inc(ptr[d->n_node]);
+  std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+  auto code = [](double w) -> uint32_t { return w == 1.0 ? 0u : w == 0.5 ? 1u : 2u; };
+  for (int64_t e = 0; e < d->n_elem; ++e)
+    for (int c = 0; c < nc; ++c) {
+      const int32_t n = d->elem_node[e * nc + c];
+      const int32_t h = node_hang[n];
+      const uint32_t idx = (uint32_t)(e * nc + c);
+      if (h < 0) inc[fill[n]++] = idx;
+      else
+        for (int32_t k = d->hang_ptr[h]; k < d->hang_ptr[h + 1]; ++k) {
+          const double w = d->hang_weight[k];
+          if (w != 1.0 && w != 0.5 && w != 0.25) { set_error("hanging weight %g not in {1, 1/2, 1/4}", w); return TO_EMESH; }
+          inc[fill[d->hang_parent[k]]++] = idx | (code(w) << 30);
+        }
+    }
+  RC(upload_array(m, &m->inc_ptr, ptr.data(), ptr.size(), st));
+  RC(upload_array(m, &m->inc, inc.data(), inc.size(), st));
+  RC(m->alloc(&m->ye, (size_t)d->n_elem * nc * d->dim));
+  CK(cudaMemsetAsync(m->ye, 0, sizeof(double) * (size_t)d->n_elem * nc * d->dim, st));
+  return 0;
+}
+
 int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
   CK(cudaSetDevice(device));
   m->device = device;
@@ -416,10 +461,12 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
   build_K0(2, d->nu, m->K2.K);
   build_K0(3, d->nu, m->K3.K);
   if (build_K0_hadamard(d->nu, &m->KH) != 0) { set_error("Hadamard factorisation check failed"); return TO_EINVAL; }
+  if (build_K0_hadamard_sym(m->KH, &m->KS) != 0) { set_error("Hadamard coefficient classes check failed"); return TO_EINVAL; }
   m->n_int = m->n_dof;
   // diagnostics: TOMESH_FORCE_GENERAL=1 keeps uniform H8 meshes on the general path
   m->force_general = std::getenv("TOMESH_FORCE_GENERAL") != nullptr;
   RC(setup_structured(d, free_dof, st, m));
+  if (!m->structured) RC(setup_incidence(d, node_hang, st, m));
   // workspace: internal-order vectors with zero pads on both sides (the
   // structured kernels read whole aligned row windows)
   RC(m->alloc(&m->s, m->n_el));
@@ -465,10 +512,9 @@ int launch_simp(to_mesh *m, double penal, const double *x, cudaStream_t st) {
 
 // D = diag(Pi_F C^T K C Pi_F) from s; Dinv (free mask) and optional diag(A).
 int launch_diag(to_mesh *m, double *d_out, cudaStream_t st) {
-  CK(cudaMemsetAsync(m->D, 0, sizeof(double) * m->n_dof, st));
-  int g = grid_for(m->n_el);
-  if (m->dim == 2) k_diag<2><<<g, kBlock, 0, st>>>(m->view(), m->s, m->D, m->K2);
-  else k_diag<3><<<g, kBlock, 0, st>>>(m->view(), m->s, m->D, m->K3);
+  const int g = grid_for(m->n_node);
+  if (m->dim == 2) k_diag_node<2><<<g, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->s, m->K2, m->D);
+  else k_diag_node<3><<<g, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->s, m->K3, m->D);
   k_dinv<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->free_dof, m->D, m->dinv, d_out, m->S);
   m->last_launches += 2;
   return check_launch();
@@ -483,13 +529,19 @@ int launch_rhs(to_mesh *m, double *b, cudaStream_t st) {
 }
 
 // q = C^T K C p for p vanishing on non-free DOFs (values on non-free DOFs of q
-// are not meaningful; callers mask).  Plain apply (no CG scalars).
+// are not meaningful; callers mask).  Plain apply: element pass + node pass.
 int launch_matvec(to_mesh *m, const double *p, double *q, cudaStream_t st) {
-  CK(cudaMemsetAsync(q, 0, sizeof(double) * m->n_dof, st));
-  int g = grid_for(m->n_el, kBlock, 16);
-  if (m->dim == 2) k_matvec_atomic<2><<<g, kBlock, 0, st>>>(m->view(), m->s, p, q, m->K2, nullptr, nullptr);
-  else k_matvec_atomic<3><<<g, kBlock, 0, st>>>(m->view(), m->s, p, q, m->K3, nullptr, nullptr);
-  m->last_launches++;
+  const int ge = grid_for(m->n_el, kBlock, 16), gn = grid_for(m->n_node, kBlock, 16);
+  if (m->dim == 2) {
+    k_elem_pass<2, G_PLAIN><<<ge, kBlock, 0, st>>>(m->view(), m->s, nullptr, nullptr, p, m->ye, m->K2, m->KS, nullptr, nullptr);
+    k_node_pass<2, G_PLAIN><<<gn, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, nullptr, nullptr, nullptr,
+                                                   nullptr, q, nullptr, nullptr, nullptr);
+  } else {
+    k_elem_pass<3, G_PLAIN><<<ge, kBlock, 0, st>>>(m->view(), m->s, nullptr, nullptr, p, m->ye, m->K2, m->KS, nullptr, nullptr);
+    k_node_pass<3, G_PLAIN><<<gn, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, nullptr, nullptr, nullptr,
+                                                   nullptr, q, nullptr, nullptr, nullptr);
+  }
+  m->last_launches += 2;
   return check_launch();
 }
 
@@ -561,20 +613,25 @@ int op_apply(to_mesh *m, const double *in, double *out, cudaStream_t st) {
   M.a = M.q = M.p = M.d = *tin;
   dim3 block(32, kS3TYW);
   k_apply_s3<kS3TYW, S3_PLAIN><<<s3_grid(m), block, sizeof(S3Smem<kS3TYW>), st>>>(
-      m->G, m->s, M, nullptr, nullptr, nullptr, out, m->KH, nullptr, nullptr, 0, 0.0, nullptr);
+      m->G, m->s, M, nullptr, nullptr, nullptr, out, m->KS, nullptr, nullptr, 0, 0.0, nullptr);
   m->last_launches++;
   return check_launch();
 }
 
-// General path, iteration k part 1: p_k into pb[k & 1] from pb[(k+1) & 1],
-// deferred x update, q = A p_k, alpha_k.
-int op_cg_k1(to_mesh *m, int k, cudaStream_t st) {
-  const double *po = m->pb[(k + 1) & 1];
-  double *pn = m->pb[k & 1];
-  k_pre_g<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->r, m->dinv, po, pn, m->x, m->q, m->S);
-  int g = grid_for(m->n_el, kBlock, 16);
-  if (m->dim == 2) k_matvec_atomic<2><<<g, kBlock, 0, st>>>(m->view(), m->s, pn, m->q, m->K2, m->S, m->partials);
-  else k_matvec_atomic<3><<<g, kBlock, 0, st>>>(m->view(), m->s, pn, m->q, m->K3, m->S, m->partials);
+// General path, iteration k: element pass (p_k formed on the fly, y_e,
+// p^T A p -> alpha_k) + node pass (q, r, x, p_k in place, rho, rr -> beta_k).
+int op_cg_general(to_mesh *m, cudaStream_t st) {
+  const int ge = grid_for(m->n_el, kBlock, 16), gn = grid_for(m->n_node, kBlock, 16);
+  double *p = m->pb[0];
+  if (m->dim == 2) {
+    k_elem_pass<2, G_CG><<<ge, kBlock, 0, st>>>(m->view(), m->s, m->r, m->dinv, p, m->ye, m->K2, m->KS, m->S, m->partials);
+    k_node_pass<2, G_CG><<<gn, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, m->r, m->dinv, p, m->x, nullptr,
+                                                m->partials, m->S, m->hist);
+  } else {
+    k_elem_pass<3, G_CG><<<ge, kBlock, 0, st>>>(m->view(), m->s, m->r, m->dinv, p, m->ye, m->K2, m->KS, m->S, m->partials);
+    k_node_pass<3, G_CG><<<gn, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, m->r, m->dinv, p, m->x, nullptr,
+                                                m->partials, m->S, m->hist);
+  }
   m->last_launches += 2;
   return 0;
 }
@@ -589,7 +646,7 @@ int op_cg_s3(to_mesh *m, int k, double rtol, cudaStream_t st) {
   M.d = m->tm_dn;
   dim3 block(32, kS3TYW);
   k_apply_s3<kS3TYW, S3_CG><<<s3_grid(m), block, sizeof(S3Smem<kS3TYW>), st>>>(
-      m->G, m->s, M, m->rb[w], m->pb[w], m->x, m->qb[w], m->KH, m->S, m->partials, k, rtol, m->hist);
+      m->G, m->s, M, m->rb[w], m->pb[w], m->x, m->qb[w], m->KS, m->S, m->partials, k, rtol, m->hist);
   m->last_launches++;
   return 0;
 }
@@ -688,9 +745,8 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
         if (prof) CK(cudaEventRecord(E[1], st));
         if (prof) CK(cudaEventRecord(E[2], st));
       } else {
-        RC(op_cg_k1(m, launched + k, st));
+        RC(op_cg_general(m, st));
         if (prof) CK(cudaEventRecord(E[1], st));
-        RC(op_cg_k2<false>(m, rtol, st));
         if (prof) CK(cudaEventRecord(E[2], st));
       }
     }
@@ -702,12 +758,7 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
       chunk = std::min(chunk * 2, 256);
     }
   }
-  if (m->structured) {
-    RC(op_final_s3(m, max_iter, rtol, st));       // no-op if an iteration already converged
-  } else {
-    k_xfinal<<<gv, kBlock, 0, st>>>(n, m->x, m->pb[0], m->pb[1], m->S);
-    m->last_launches++;
-  }
+  if (m->structured) RC(op_final_s3(m, max_iter, rtol, st));   // no-op if an iteration already converged
   RC(check_launch());
   RC(read_scalars(m, st));
   CgScalars res = *m->S_host;
@@ -846,7 +897,7 @@ extern "C" int to_sensitivity(to_mesh *m, double penal, const double *x_dev, con
   cudaStream_t st = (cudaStream_t)cuda_stream;
   int g = grid_for(m->n_el);
   if (m->dim == 2) k_sens<2><<<g, kBlock, 0, st>>>(m->view(), x_dev, u_dev, penal, m->E0, m->Emin, dc_dev, m->K2);
-  else k_sens<3><<<g, kBlock, 0, st>>>(m->view(), x_dev, u_dev, penal, m->E0, m->Emin, dc_dev, m->K3);
+  else k_sens_had3<<<g, kBlock, 0, st>>>(m->view(), x_dev, u_dev, penal, m->E0, m->Emin, dc_dev, m->KS);
   RC(check_launch());
   if (compliance_host) {
     k_dot<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->load, u_dev, m->partials, m->S, 1);

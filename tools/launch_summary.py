@@ -11,6 +11,8 @@ def main(path):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     hdr = rows[0]
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    mi = hdr.index("Metric Name")
+    rows = [rows[0]] + [r for r in rows[1:] if r[mi] == "gpu__time_duration.sum"]
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in rows[1:]:
         try:

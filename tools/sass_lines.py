@@ -116,3 +116,38 @@ def top_instructions(rep, kname, line_suffix, n=10, which=-1):
             res.append((int(r[ci["Warp Stall Sampling (All Samples)"]] or 0), hex(off), ins))
     for t in sorted(res, reverse=True)[:n]:
         print(t)
+
+
+def inst_by_line(rep, kname, n=40, which=-1):
+    """Executed warp instructions per source line and opcode (one launch)."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    blocks, cur = [], None
+    for r in rows:
+        if r and r[0] == "Kernel Name":
+            cur = {"name": r[1], "rows": []}
+            blocks.append(cur)
+        elif cur is not None:
+            cur["rows"].append(r)
+    short = re.sub(r"I.*", "", re.sub(r"^_ZN\d+tomesh\d+", "", kname))
+    blk = [b for b in blocks if short in b["name"]][which]
+    hdr = blk["rows"][0]
+    ci = {h: i for i, h in enumerate(hdr)}
+    body = blk["rows"][1:]
+    base = int(body[0][ci["Address"]], 16)
+    fmap = sass_line_map(kname)
+    bymap = {off: (ln, ins) for off, ln, ins in fmap}
+    agg = collections.defaultdict(collections.Counter)
+    tot = collections.Counter()
+    for r in body:
+        off = int(r[ci["Address"]], 16) - base
+        ln, ins = bymap.get(off, ("?", "?"))
+        ex = int(r[ci["Instructions Executed"]] or 0)
+        op = re.sub(r"^@!?U?P\w+\s+", "", ins.strip()).split()[0].split(".")[0] if ins.strip() else "?"
+        agg[ln][op] += ex
+        tot[op] += ex
+    allx = sum(tot.values())
+    print(f"total executed {allx}")
+    for ln, c in sorted(agg.items(), key=lambda t: -sum(t[1].values()))[:n]:
+        sm = sum(c.values())
+        print(f"{sm:10d} {100 * sm / allx:5.1f}%  {ln:30s} {c.most_common(4)}")
