@@ -332,25 +332,41 @@ __device__ __forceinline__ double g_p(const double *__restrict__ r, const double
 }
 
 template <int DIM, int MODE>
-__global__ void __launch_bounds__(256) k_elem_pass(MeshView M, const double *__restrict__ s,
-                                                   const double *__restrict__ r, const double *__restrict__ Dinv,
-                                                   const double *__restrict__ po, double *__restrict__ ye,
-                                                   const __grid_constant__ K0Dense2 K2, const __grid_constant__ K0HadSym H,
-                                                   CgScalars *S, double *partials) {
+__global__ void __launch_bounds__(256, 3) k_elem_pass(MeshView M, const double *__restrict__ s,
+                                                      const double *__restrict__ r, const double *__restrict__ Dinv,
+                                                      const double *__restrict__ po, double *__restrict__ ye,
+                                                      const __grid_constant__ K0Dense2 K2,
+                                                      const __grid_constant__ K0HadSym H, const uint8_t *__restrict__ hmask,
+                                                      CgScalars *S, double *partials) {
   constexpr int NC = 1 << DIM, ND = DIM * NC;
   if (MODE == G_CG && cg_stopped(S)) return;
   const double beta = MODE == G_CG ? __ldcg(&S->beta) : 0.0;
   double pq = 0.0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M.n_el; e += (int64_t)gridDim.x * blockDim.x) {
+    // corner nodes in one or two 16-byte loads; hmask (bit c: corner c is a
+    // hanging node) avoids the dependent node_hang lookups on most elements
+    int node[NC];
+    {
+      const int4 *en4 = reinterpret_cast<const int4 *>(M.elem_node + e * NC);
+#pragma unroll
+      for (int h = 0; h < NC / 4; ++h) {
+        const int4 t = __ldg(&en4[h]);
+        node[4 * h] = t.x;
+        node[4 * h + 1] = t.y;
+        node[4 * h + 2] = t.z;
+        node[4 * h + 3] = t.w;
+      }
+    }
+    const unsigned hm = hmask[e];
     double y[ND];
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-      const int n = M.elem_node[e * NC + c];
-      const int h = M.node_hang[n];
-      if (h < 0) {
+      const int n = node[c];
+      if (!((hm >> c) & 1)) {
 #pragma unroll
         for (int i = 0; i < DIM; ++i) y[DIM * c + i] = g_p<MODE>(r, Dinv, po, beta, (int64_t)n * DIM + i);
       } else {
+        const int h = M.node_hang[n];
         double acc[DIM];
 #pragma unroll
         for (int i = 0; i < DIM; ++i) acc[i] = 0.0;
@@ -420,12 +436,24 @@ __global__ void __launch_bounds__(256) k_node_pass(int64_t n_node, const int64_t
 #pragma unroll
     for (int i = 0; i < DIM; ++i) qv[i] = 0.0;
     const int64_t k1 = inc_ptr[n + 1];
-    for (int64_t k = inc_ptr[n]; k < k1; ++k) {
-      const uint32_t t = __ldg(&inc[k]);
-      const double w = (t >> 30) == 0 ? 1.0 : (t >> 30) == 1 ? 0.5 : 0.25;
-      const double *src = ye + (int64_t)(t & 0x3fffffffu) * DIM;
+    // batches of 8 incidences: all index loads, then all element-vector loads
+    for (int64_t k0 = inc_ptr[n]; k0 < k1; k0 += 8) {
+      uint32_t t[8];
 #pragma unroll
-      for (int i = 0; i < DIM; ++i) qv[i] = fma(w, __ldg(&src[i]), qv[i]);
+      for (int j = 0; j < 8; ++j) t[j] = (k0 + j < k1) ? __ldg(&inc[k0 + j]) : 0xffffffffu;
+      double v[8][DIM];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double *src = ye + (int64_t)(t[j] & 0x3fffffffu) * DIM;
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) v[j][i] = (t[j] != 0xffffffffu) ? __ldg(&src[i]) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double w = (t[j] >> 30) == 0 ? 1.0 : (t[j] >> 30) == 1 ? 0.5 : 0.25;
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) qv[i] = fma(w, v[j][i], qv[i]);
+      }
     }
 #pragma unroll
     for (int i = 0; i < DIM; ++i) {

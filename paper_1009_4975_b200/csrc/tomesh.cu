@@ -55,6 +55,7 @@ struct to_mesh {
   int64_t *inc_ptr = nullptr;          // general path: node -> (element, corner, weight) incidences
   uint32_t *inc = nullptr;
   double *ye = nullptr;                // general path: element vectors s_e K0 C_e p
+  uint8_t *hmask = nullptr;            // general path: bit c = corner c of the element is hanging
   int32_t *filt_idx = nullptr;
   // workspace
   double *s = nullptr, *x = nullptr, *r = nullptr, *q = nullptr, *dinv = nullptr, *D = nullptr;
@@ -381,6 +382,11 @@ int setup_incidence(const to_mesh_desc *d, const std::vector<int32_t> &node_hang
           inc[fill[d->hang_parent[k]]++] = idx | (code(w) << 30);
         }
     }
+  std::vector<uint8_t> hmask(d->n_elem, 0);
+  for (int64_t e = 0; e < d->n_elem; ++e)
+    for (int c = 0; c < nc; ++c)
+      if (node_hang[d->elem_node[e * nc + c]] >= 0) hmask[e] |= (uint8_t)(1u << c);
+  RC(upload_array(m, &m->hmask, hmask.data(), hmask.size(), st));
   RC(upload_array(m, &m->inc_ptr, ptr.data(), ptr.size(), st));
   RC(upload_array(m, &m->inc, inc.data(), inc.size(), st));
   RC(m->alloc(&m->ye, (size_t)d->n_elem * nc * d->dim));
@@ -533,11 +539,11 @@ int launch_rhs(to_mesh *m, double *b, cudaStream_t st) {
 int launch_matvec(to_mesh *m, const double *p, double *q, cudaStream_t st) {
   const int ge = grid_for(m->n_el, kBlock, 16), gn = grid_for(m->n_node, kBlock, 16);
   if (m->dim == 2) {
-    k_elem_pass<2, G_PLAIN><<<ge, kBlock, 0, st>>>(m->view(), m->s, nullptr, nullptr, p, m->ye, m->K2, m->KS, nullptr, nullptr);
+    k_elem_pass<2, G_PLAIN><<<ge, kBlock, 0, st>>>(m->view(), m->s, nullptr, nullptr, p, m->ye, m->K2, m->KS, m->hmask, nullptr, nullptr);
     k_node_pass<2, G_PLAIN><<<gn, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, nullptr, nullptr, nullptr,
                                                    nullptr, q, nullptr, nullptr, nullptr);
   } else {
-    k_elem_pass<3, G_PLAIN><<<ge, kBlock, 0, st>>>(m->view(), m->s, nullptr, nullptr, p, m->ye, m->K2, m->KS, nullptr, nullptr);
+    k_elem_pass<3, G_PLAIN><<<ge, kBlock, 0, st>>>(m->view(), m->s, nullptr, nullptr, p, m->ye, m->K2, m->KS, m->hmask, nullptr, nullptr);
     k_node_pass<3, G_PLAIN><<<gn, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, nullptr, nullptr, nullptr,
                                                    nullptr, q, nullptr, nullptr, nullptr);
   }
@@ -624,11 +630,11 @@ int op_cg_general(to_mesh *m, cudaStream_t st) {
   const int ge = grid_for(m->n_el, kBlock, 16), gn = grid_for(m->n_node, kBlock, 16);
   double *p = m->pb[0];
   if (m->dim == 2) {
-    k_elem_pass<2, G_CG><<<ge, kBlock, 0, st>>>(m->view(), m->s, m->r, m->dinv, p, m->ye, m->K2, m->KS, m->S, m->partials);
+    k_elem_pass<2, G_CG><<<ge, kBlock, 0, st>>>(m->view(), m->s, m->r, m->dinv, p, m->ye, m->K2, m->KS, m->hmask, m->S, m->partials);
     k_node_pass<2, G_CG><<<gn, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, m->r, m->dinv, p, m->x, nullptr,
                                                 m->partials, m->S, m->hist);
   } else {
-    k_elem_pass<3, G_CG><<<ge, kBlock, 0, st>>>(m->view(), m->s, m->r, m->dinv, p, m->ye, m->K2, m->KS, m->S, m->partials);
+    k_elem_pass<3, G_CG><<<ge, kBlock, 0, st>>>(m->view(), m->s, m->r, m->dinv, p, m->ye, m->K2, m->KS, m->hmask, m->S, m->partials);
     k_node_pass<3, G_CG><<<gn, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, m->r, m->dinv, p, m->x, nullptr,
                                                 m->partials, m->S, m->hist);
   }
