@@ -324,9 +324,12 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
   for (int k = k_lo - 1; k <= min(k_lo + 1, k_hi); ++k) form_plane(k, k == k_lo + 1 ? xb : xa);
   __syncthreads();
 
-  // per-layer carries: contributions of layer ek-1's upper corners
-  double own_carry[3] = {0.0, 0.0, 0.0};                // to node (ei, ej, ek)
-  double up_carry[3] = {0.0, 0.0, 0.0};                 // to node (ei, ej+1, ek), sent to row ty+1
+  // z carry at the face level: the top-face half of layer ek-1's inverse
+  // transform (still in the x-y Hadamard basis of the 4 face nodes), added to
+  // layer ek's bottom-face half before the face's own inverse x-y transform
+  double gcar[12];
+#pragma unroll
+  for (int t = 0; t < 12; ++t) gcar[t] = 0.0;
   // s_e of this thread's element column, loaded two layers ahead (register ring)
   const int64_t s_stride = (int64_t)G.EX * G.EY;
   // the load itself is unconditional (clamped to a valid element) so that no
@@ -356,27 +359,50 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
         for (int d = 0; d < 3; ++d) y[3 * c + d] = row[d];
       }
     }
-    had_apply_inplace(H, y);
+    // element product in the Hadamard basis (mode m = mx + 2 my + 4 mz), scaled
+    wht8x3(y);
+    had_mid_inplace(H, y);
 #pragma unroll
     for (int a = 0; a < 24; ++a) y[a] *= se;            // se = 0 for elements outside the mesh / segment
-    // x routing: corner (1,cy,cz) of element ei goes to node ei+1 (lane + 1)
-    double a_row[2][2][3];   // [cy][cz][comp] after the x merge, at node column ei
+    // inverse transform, z stage: bottom face (plane ek) and top face (plane ek+1)
+    double face[12];
+#pragma unroll
+    for (int t = 0; t < 12; ++t) {
+      const double a = y[t], b = y[12 + t];
+      face[t] = a + b + gcar[t];                        // plane ek: this layer's bottom + last layer's top
+      gcar[t] = a - b;
+    }
+    // inverse y stage then x stage on the 4 face nodes (corner cx + 2 cy)
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double a = face[3 * m + d], b = face[3 * (m + 2) + d];
+        face[3 * m + d] = a + b;
+        face[3 * (m + 2) + d] = a - b;
+      }
+#pragma unroll
+    for (int m = 0; m < 4; m += 2)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double a = face[3 * m + d], b = face[3 * (m + 1) + d];
+        face[3 * m + d] = a + b;
+        face[3 * (m + 1) + d] = a - b;
+      }
+    // x routing: corner (1, cy) of element column ei goes to node ei+1 (lane + 1);
+    // lane 0 receives its own value: garbage, but lane 0 is the halo column
+    double a_row[2][3];                                 // [cy][comp] at node column ei, plane ek
 #pragma unroll
     for (int cy = 0; cy < 2; ++cy)
 #pragma unroll
-      for (int cz = 0; cz < 2; ++cz)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          // lane 0 receives its own value: garbage, but lane 0 is the halo
-          // column (never an owner), so it needs no select
-          const double from_left = __shfl_up_sync(0xffffffffu, y[3 * (1 + 2 * cy + 4 * cz) + d], 1);
-          a_row[cy][cz][d] = y[3 * (2 * cy + 4 * cz) + d] + from_left;
-        }
-    // y routing: node (ei, ej+1, ek) collects this layer's (cy=1, cz=0) part and
-    // the previous layer's (cy=1, cz=1) part; row ty+1 owns it
+      for (int d = 0; d < 3; ++d) {
+        const double from_left = __shfl_up_sync(0xffffffffu, face[3 * (1 + 2 * cy) + d], 1);
+        a_row[cy][d] = face[3 * (2 * cy) + d] + from_left;
+      }
+    // y routing: the cy = 1 row goes to node row ty+1
     if (ty < TYW - 1) {
 #pragma unroll
-      for (int d = 0; d < 3; ++d) sm.xch[ek & 1][ty][d][tx] = a_row[1][0][d] + up_carry[d];
+      for (int d = 0; d < 3; ++d) sm.xch[ek & 1][ty][d][tx] = a_row[1][d];
     }
     __syncthreads();                                    // the one CTA barrier of the layer
     // node plane ek is complete: (cz=0) parts of layer ek + (cz=1) parts of layer ek-1
@@ -387,7 +413,7 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
         const double dv = CG ? sm.own[slot][3][tid] : 0.0;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-          const double qv = a_row[0][0][d] + own_carry[d] + sm.xch[ek & 1][ty - 1][d][tx];
+          const double qv = a_row[0][d] + sm.xch[ek & 1][ty - 1][d][tx];
           __stcs(&q[dof + d], qv);
           if (CG) {
             dots[2] = fma(sm.pn[slot][ty][off + 3 * tx + d], qv, dots[2]);   // p_k of the own node (this thread formed it)
@@ -396,11 +422,6 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
           }
         }
       }
-    }
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      own_carry[d] = a_row[0][1][d];
-      up_carry[d] = a_row[1][1][d];
     }
     if (ek + 3 <= k_hi) {
       form_plane(ek + 3, x_slot);                       // slot ek%3: free since the barrier
