@@ -211,11 +211,14 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
   S3Smem<TYW> &sm = *reinterpret_cast<S3Smem<TYW> *>(smem_raw);
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = tx + 32 * ty;
+  // x tiles fastest: the CTAs resident together cover whole node rows of the
+  // same z range, so their TMA boxes (and stores) of a plane are adjacent in
+  // memory (DRAM page locality)
   int bid = blockIdx.x;
-  const int zs = bid % G.nzs;
-  bid /= G.nzs;
+  const int tx_t = bid % G.ntx;
+  bid /= G.ntx;
   const int ty_t = bid % G.nty;
-  const int tx_t = bid / G.nty;
+  const int zs = bid / G.nty;
   const int i0 = tx_t * 31, j0 = ty_t * (TYW - 1);
   const int k_lo = zs * G.zlen;
   const int k_hi = min(G.NZ, k_lo + G.zlen);
