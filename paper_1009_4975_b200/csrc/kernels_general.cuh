@@ -9,6 +9,8 @@
 //   k_sens        a10 dc_e = -p x^(p-1)(E0-Emin) h^(d-2) u_e^T K0 u_e    (:343-346)
 //   k_filter      a11 Eq. 5 / density variant                             (:613-616)
 #pragma once
+#include <cooperative_groups.h>
+
 #include "device_common.cuh"
 #include "element.h"
 #include "kernels_cg.cuh"
@@ -322,13 +324,149 @@ __device__ __forceinline__ void had_apply(const K0Had3 &H, double (&x)[24], doub
 // Eq. 6 for the parents of a hanging corner), i.e. q = C^T K C p.
 enum { G_PLAIN = 0, G_CG = 1 };
 
+// Loads of vectors the same kernel may have written (persistent solver): a
+// plain cached global load (ld.global.ca: the grid barrier's acquire makes
+// the other blocks' writes visible; the non-coherent read-only path must not
+// be used for them); otherwise the read-only path.
+template <bool COH>
+__device__ __forceinline__ double g_ld(const double *p) {
+  if (!COH) return __ldg(p);
+  double v;
+  asm volatile("ld.global.ca.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // p of DOF d: CG: Dinv r + beta p_{k-1} (formed on the fly; the node pass
 // stores the same value); plain: v.
-template <int MODE>
+template <int MODE, bool COH>
 __device__ __forceinline__ double g_p(const double *__restrict__ r, const double *__restrict__ Dinv,
                                       const double *__restrict__ po, double beta, int64_t d) {
-  if (MODE == G_PLAIN) return po[d];
-  return fma(Dinv[d], r[d], beta * po[d]);
+  if (MODE == G_PLAIN) return g_ld<COH>(po + d);
+  return fma(__ldg(Dinv + d), g_ld<COH>(r + d), beta * g_ld<COH>(po + d));
+}
+
+// One element of the element pass: y_e = s_e K0 C_e p into ye; returns
+// s_e pbar^T K0 pbar (its share of p^T A p).
+template <int DIM, int MODE, bool COH>
+__device__ __forceinline__ double g_elem_one(const MeshView &M, int64_t e, const double *__restrict__ s,
+                                             const double *__restrict__ r, const double *__restrict__ Dinv,
+                                             const double *__restrict__ po, double *__restrict__ ye,
+                                             const K0Dense2 &K2, const K0HadSym &H, const uint8_t *__restrict__ hmask,
+                                             double beta) {
+  constexpr int NC = 1 << DIM, ND = DIM * NC;
+  // corner nodes in one or two 16-byte loads; hmask (bit c: corner c is a
+  // hanging node) avoids the dependent node_hang lookups on most elements
+  int node[NC];
+#pragma unroll
+  for (int h = 0; h < NC / 4; ++h) {
+    const int4 t = __ldg(reinterpret_cast<const int4 *>(M.elem_node + e * NC) + h);
+    node[4 * h] = t.x;
+    node[4 * h + 1] = t.y;
+    node[4 * h + 2] = t.z;
+    node[4 * h + 3] = t.w;
+  }
+  const unsigned hm = hmask[e];
+  // all corners unconditionally (branch-free, so all the gathers are in
+  // flight together); hanging corners (rare) are then replaced by the Eq. 6
+  // interpolation of their parents
+  double y[ND];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) y[DIM * c + i] = g_p<MODE, COH>(r, Dinv, po, beta, (int64_t)node[c] * DIM + i);
+  if (hm) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      if (!((hm >> c) & 1)) continue;
+      const int h = M.node_hang[node[c]];
+      double acc[DIM];
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) acc[i] = 0.0;
+      for (int k = M.hang_ptr[h]; k < M.hang_ptr[h + 1]; ++k) {
+        const double w = M.hang_weight[k];
+        const int64_t pn = M.hang_parent[k];
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) acc[i] = fma(w, g_p<MODE, COH>(r, Dinv, po, beta, pn * DIM + i), acc[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) y[DIM * c + i] = acc[i];
+    }
+  }
+  const double se = __ldg(s + e);
+  double en = 0.0;
+  if constexpr (DIM == 3) {
+    wht8x3(y);
+    had_mid_inplace_energy(H, y, en);
+    wht8x3(y);
+  } else {
+    double t[ND];
+    dense_apply<ND>(K2.K, y, t);
+#pragma unroll
+    for (int a = 0; a < ND; ++a) {
+      en = fma(y[a], t[a], en);
+      y[a] = t[a];
+    }
+  }
+  double2 *dst = reinterpret_cast<double2 *>(ye + e * ND);
+#pragma unroll
+  for (int a = 0; a < ND / 2; ++a) dst[a] = make_double2(se * y[2 * a], se * y[2 * a + 1]);
+  return se * en;
+}
+
+// One node of the node pass.  q_n = sum over the incidences of n of w *
+// y_e[corner] (packed entry: element*2^DIM + corner in bits 0-29, weight
+// code in bits 30-31: 0 -> 1, 1 -> 1/2, 2 -> 1/4).
+//   plain: q_out = q (all DOFs; the caller masks);
+//   CG (iteration k, alpha_k known): on free DOFs p_k = Dinv r_k + beta p_{k-1}
+//   (stored in place), x += alpha_k p_k, r -= alpha_k q; accumulates
+//   rho_{k+1} = r.Dinv r and rr into acc.
+template <int DIM, int MODE, bool COH>
+__device__ __forceinline__ void g_node_one(int64_t n, const int64_t *__restrict__ inc_ptr,
+                                           const uint32_t *__restrict__ inc, const double *__restrict__ ye,
+                                           double *__restrict__ r, const double *__restrict__ Dinv,
+                                           double *__restrict__ p, double *__restrict__ x, double *__restrict__ q_out,
+                                           double alpha, double beta, double (&acc)[2]) {
+  double qv[DIM];
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) qv[i] = 0.0;
+  const int64_t k1 = inc_ptr[n + 1];
+  // batches of 8 incidences: all index loads, then all element-vector loads
+  for (int64_t k0 = inc_ptr[n]; k0 < k1; k0 += 8) {
+    uint32_t t[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t[j] = (k0 + j < k1) ? __ldg(&inc[k0 + j]) : 0xffffffffu;
+    double v[8][DIM];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double *src = ye + (int64_t)(t[j] & 0x3fffffffu) * DIM;
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) v[j][i] = (t[j] != 0xffffffffu) ? g_ld<COH>(src + i) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double w = (t[j] >> 30) == 0 ? 1.0 : (t[j] >> 30) == 1 ? 0.5 : 0.25;
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) qv[i] = fma(w, v[j][i], qv[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) {
+    const int64_t d = n * DIM + i;
+    if (MODE == G_PLAIN) {
+      q_out[d] = qv[i];
+    } else {
+      const double di = __ldg(Dinv + d);
+      if (di != 0.0) {
+        const double pk = fma(di, r[d], beta * p[d]);
+        p[d] = pk;
+        x[d] = fma(alpha, pk, x[d]);
+        const double rn = fma(-alpha, qv[i], r[d]);
+        r[d] = rn;
+        acc[0] = fma(rn, di * rn, acc[0]);
+        acc[1] = fma(rn, rn, acc[1]);
+      }
+    }
+  }
 }
 
 template <int DIM, int MODE>
@@ -338,68 +476,11 @@ __global__ void __launch_bounds__(256, 3) k_elem_pass(MeshView M, const double *
                                                       const __grid_constant__ K0Dense2 K2,
                                                       const __grid_constant__ K0HadSym H, const uint8_t *__restrict__ hmask,
                                                       CgScalars *S, double *partials) {
-  constexpr int NC = 1 << DIM, ND = DIM * NC;
   if (MODE == G_CG && cg_stopped(S)) return;
   const double beta = MODE == G_CG ? __ldcg(&S->beta) : 0.0;
   double pq = 0.0;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M.n_el; e += (int64_t)gridDim.x * blockDim.x) {
-    // corner nodes in one or two 16-byte loads; hmask (bit c: corner c is a
-    // hanging node) avoids the dependent node_hang lookups on most elements
-    int node[NC];
-    {
-      const int4 *en4 = reinterpret_cast<const int4 *>(M.elem_node + e * NC);
-#pragma unroll
-      for (int h = 0; h < NC / 4; ++h) {
-        const int4 t = __ldg(&en4[h]);
-        node[4 * h] = t.x;
-        node[4 * h + 1] = t.y;
-        node[4 * h + 2] = t.z;
-        node[4 * h + 3] = t.w;
-      }
-    }
-    const unsigned hm = hmask[e];
-    double y[ND];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int n = node[c];
-      if (!((hm >> c) & 1)) {
-#pragma unroll
-        for (int i = 0; i < DIM; ++i) y[DIM * c + i] = g_p<MODE>(r, Dinv, po, beta, (int64_t)n * DIM + i);
-      } else {
-        const int h = M.node_hang[n];
-        double acc[DIM];
-#pragma unroll
-        for (int i = 0; i < DIM; ++i) acc[i] = 0.0;
-        for (int k = M.hang_ptr[h]; k < M.hang_ptr[h + 1]; ++k) {
-          const double w = M.hang_weight[k];
-          const int64_t pn = M.hang_parent[k];
-#pragma unroll
-          for (int i = 0; i < DIM; ++i) acc[i] = fma(w, g_p<MODE>(r, Dinv, po, beta, pn * DIM + i), acc[i]);
-        }
-#pragma unroll
-        for (int i = 0; i < DIM; ++i) y[DIM * c + i] = acc[i];
-      }
-    }
-    const double se = s[e];
-    double en = 0.0;
-    if constexpr (DIM == 3) {
-      wht8x3(y);
-      had_mid_inplace_energy(H, y, en);
-      wht8x3(y);
-    } else {
-      double t[ND];
-      dense_apply<ND>(K2.K, y, t);
-#pragma unroll
-      for (int a = 0; a < ND; ++a) {
-        en = fma(y[a], t[a], en);
-        y[a] = t[a];
-      }
-    }
-    pq = fma(se, en, pq);
-    double2 *dst = reinterpret_cast<double2 *>(ye + e * ND);
-#pragma unroll
-    for (int a = 0; a < ND / 2; ++a) dst[a] = make_double2(se * y[2 * a], se * y[2 * a + 1]);
-  }
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M.n_el; e += (int64_t)gridDim.x * blockDim.x)
+    pq += g_elem_one<DIM, MODE, false>(M, e, s, r, Dinv, po, ye, K2, H, hmask, beta);
   if (MODE == G_CG) {
     double v[1] = {pq};
     if (grid_sum<1>(v, partials, &S->counter[CNT_PQ])) {
@@ -413,13 +494,6 @@ __global__ void __launch_bounds__(256, 3) k_elem_pass(MeshView M, const double *
   }
 }
 
-// Node pass.  q_n = sum over the incidences of n of w * y_e[corner] (packed
-// entry: element*2^DIM + corner in bits 0-29, weight code in bits 30-31:
-// 0 -> 1, 1 -> 1/2, 2 -> 1/4).
-//   plain: q_out = q (all DOFs; the caller masks);
-//   CG (iteration k, alpha_k known): on free DOFs p_k = Dinv r_k + beta p_{k-1}
-//   (stored in place), x += alpha_k p_k, r -= alpha_k q; reduce
-//   rho_{k+1} = r.Dinv r and rr -> beta_k and the stop test.
 template <int DIM, int MODE>
 __global__ void __launch_bounds__(256) k_node_pass(int64_t n_node, const int64_t *__restrict__ inc_ptr,
                                                    const uint32_t *__restrict__ inc, const double *__restrict__ ye,
@@ -431,54 +505,117 @@ __global__ void __launch_bounds__(256) k_node_pass(int64_t n_node, const int64_t
   const double beta = MODE == G_CG ? __ldcg(&S->beta) : 0.0;
   const double alpha = MODE == G_CG ? __ldcg(&S->alpha) : 0.0;
   double acc[2] = {0.0, 0.0};
-  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_node; n += (int64_t)gridDim.x * blockDim.x) {
-    double qv[DIM];
-#pragma unroll
-    for (int i = 0; i < DIM; ++i) qv[i] = 0.0;
-    const int64_t k1 = inc_ptr[n + 1];
-    // batches of 8 incidences: all index loads, then all element-vector loads
-    for (int64_t k0 = inc_ptr[n]; k0 < k1; k0 += 8) {
-      uint32_t t[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) t[j] = (k0 + j < k1) ? __ldg(&inc[k0 + j]) : 0xffffffffu;
-      double v[8][DIM];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const double *src = ye + (int64_t)(t[j] & 0x3fffffffu) * DIM;
-#pragma unroll
-        for (int i = 0; i < DIM; ++i) v[j][i] = (t[j] != 0xffffffffu) ? __ldg(&src[i]) : 0.0;
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const double w = (t[j] >> 30) == 0 ? 1.0 : (t[j] >> 30) == 1 ? 0.5 : 0.25;
-#pragma unroll
-        for (int i = 0; i < DIM; ++i) qv[i] = fma(w, v[j][i], qv[i]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < DIM; ++i) {
-      const int64_t d = n * DIM + i;
-      if (MODE == G_PLAIN) {
-        q_out[d] = qv[i];
-      } else {
-        const double di = Dinv[d];
-        if (di != 0.0) {
-          const double pk = fma(di, r[d], beta * p[d]);
-          p[d] = pk;
-          x[d] = fma(alpha, pk, x[d]);
-          const double rn = fma(-alpha, qv[i], r[d]);
-          r[d] = rn;
-          acc[0] = fma(rn, di * rn, acc[0]);
-          acc[1] = fma(rn, rn, acc[1]);
-        }
-      }
-    }
-  }
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_node; n += (int64_t)gridDim.x * blockDim.x)
+    g_node_one<DIM, MODE, false>(n, inc_ptr, inc, ye, r, Dinv, p, x, q_out, alpha, beta, acc);
   if (MODE == G_CG) {
     if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) {
       cg_after_rupdate(S, acc[0], acc[1], hist);
       if (S->done_next) S->done = 1;                 // x is already complete
     }
+  }
+}
+
+// The whole general-path PCG loop in one cooperative (persistent) kernel:
+// per iteration an element pass, a grid barrier, the alpha reduction summed
+// by every block in the same order (identical values everywhere), a node
+// pass, a grid barrier, the beta reduction.  For the latency-bound AMR and
+// small meshes (c1, c2, c4) this removes the two launches and the host
+// polling per iteration.  Requires all blocks co-resident (cooperative launch).
+// Sum of the per-block partials, computed by warp 0 of every block in the same
+// fixed order (lane-strided partial sums, then the xor-shuffle tree) and
+// broadcast through shared memory: every block obtains bit-identical totals.
+template <int NV>
+__device__ __forceinline__ void g_sum_partials(const double *part, int nb, double (&out)[NV]) {
+  if (nb <= 32) {                                       // small grids: every thread, same order
+#pragma unroll
+    for (int k = 0; k < NV; ++k) out[k] = 0.0;
+    for (int b = 0; b < nb; ++b)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) out[k] += __ldcg(&part[NV * b + k]);
+    return;
+  }
+  __shared__ double bc[NV];
+  if (threadIdx.x < 32) {
+    double a[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) a[k] = 0.0;
+    for (int b = threadIdx.x; b < nb; b += 32)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) a[k] += __ldcg(&part[NV * b + k]);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) a[k] = warp_sum(a[k]);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) bc[k] = a[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = bc[k];
+  __syncthreads();
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(256, 2) k_cg_general_persistent(
+    MeshView M, const double *__restrict__ s, double *__restrict__ r, const double *__restrict__ Dinv,
+    double *__restrict__ p, double *__restrict__ x, double *__restrict__ ye, const int64_t *__restrict__ inc_ptr,
+    const uint32_t *__restrict__ inc, const __grid_constant__ K0Dense2 K2, const __grid_constant__ K0HadSym H,
+    const uint8_t *__restrict__ hmask, CgScalars *S, double *part_a, double *part_b, double *hist) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  const int nb = gridDim.x;
+  // scalars after the initial residual (k_rupd<true>), identical in every block
+  double rho = __ldcg(&S->rho), rr = __ldcg(&S->rr);
+  const double thresh2 = __ldcg(&S->thresh2), bnorm2 = __ldcg(&S->bnorm2);
+  const int max_iter = S->max_iter, fixed = S->fixed, history = S->history;
+  int status = __ldcg(&S->status);
+  bool done = __ldcg(&S->done) != 0;
+  double beta = 0.0;
+  int it = 0;
+  const int64_t tid0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)nb * blockDim.x;
+  while (!done && it < max_iter) {
+    double v1[1] = {0.0};
+    for (int64_t e = tid0; e < M.n_el; e += stride)
+      v1[0] += g_elem_one<DIM, G_CG, true>(M, e, s, r, Dinv, p, ye, K2, H, hmask, beta);
+    block_sum<1>(v1);
+    if (threadIdx.x == 0) __stcg(&part_a[blockIdx.x], v1[0]);
+    grid.sync();
+    double tot1[1];
+    g_sum_partials<1>(part_a, nb, tot1);
+    const double pq = tot1[0];
+    if (!(pq > 0.0)) {
+      status = (pq != pq) ? -5 : -6;
+      break;
+    }
+    const double alpha = rho / pq;
+    double v2[2] = {0.0, 0.0};
+    for (int64_t n = tid0; n < M.n_node; n += stride)
+      g_node_one<DIM, G_CG, true>(n, inc_ptr, inc, ye, r, Dinv, p, x, nullptr, alpha, beta, v2);
+    block_sum<2>(v2);
+    if (threadIdx.x == 0) {
+      __stcg(&part_b[2 * blockIdx.x], v2[0]);
+      __stcg(&part_b[2 * blockIdx.x + 1], v2[1]);
+    }
+    grid.sync();
+    double tot2[2];
+    g_sum_partials<2>(part_b, nb, tot2);
+    const double rz = tot2[0], rn = tot2[1];
+    ++it;
+    if (!(rz == rz) || !(rn == rn)) {
+      status = -5;
+      break;
+    }
+    beta = rz / rho;
+    rho = rz;
+    rr = rn;
+    if (history && hist && blockIdx.x == 0 && threadIdx.x == 0) hist[it - 1] = sqrt(rr / bnorm2);
+    if (!fixed && rr <= thresh2) done = true;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    S->iter = it;
+    S->rho = rho;
+    S->rr = rr;
+    S->beta = beta;
+    S->status = status;
+    S->done = 1;
   }
 }
 

@@ -56,6 +56,7 @@ struct to_mesh {
   uint32_t *inc = nullptr;
   double *ye = nullptr;                // general path: element vectors s_e K0 C_e p
   uint8_t *hmask = nullptr;            // general path: bit c = corner c of the element is hanging
+  int coop_blocks = 0;                 // general path: grid of the persistent cooperative solver (0 = off)
   int32_t *filt_idx = nullptr;
   // workspace
   double *s = nullptr, *x = nullptr, *r = nullptr, *q = nullptr, *dinv = nullptr, *D = nullptr;
@@ -472,7 +473,22 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
   // diagnostics: TOMESH_FORCE_GENERAL=1 keeps uniform H8 meshes on the general path
   m->force_general = std::getenv("TOMESH_FORCE_GENERAL") != nullptr;
   RC(setup_structured(d, free_dof, st, m));
-  if (!m->structured) RC(setup_incidence(d, node_hang, st, m));
+  if (!m->structured) {
+    RC(setup_incidence(d, node_hang, st, m));
+    // persistent cooperative solver: as many co-resident blocks as the work needs
+    int coop = 0;
+    CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+    // (latency-bound small meshes only: on large ones the separate element and
+    // node kernels run at higher occupancy)
+    if (coop && !std::getenv("TOMESH_NO_PERSISTENT") && d->n_elem <= 100000) {
+      int per_sm = 0;
+      if (d->dim == 2) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_general_persistent<2>, kBlock, 0));
+      else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_general_persistent<3>, kBlock, 0));
+      const int64_t need = (std::max<int64_t>(d->n_elem, d->n_node) + kBlock - 1) / kBlock;
+      m->coop_blocks = (int)std::min<int64_t>(need, (int64_t)per_sm * kNumSMs);
+      if (m->coop_blocks * 3 > kMaxPartialBlocks * 4) m->coop_blocks = kMaxPartialBlocks * 4 / 3;
+    }
+  }
   // workspace: internal-order vectors with zero pads on both sides (the
   // structured kernels read whole aligned row windows)
   RC(m->alloc(&m->s, m->n_el));
@@ -741,6 +757,22 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
     RC(read_scalars(m, st));
     stop = m->S_host->done != 0;
   }
+  if (!m->structured && m->coop_blocks > 0 && !stop) {
+    // the whole loop in one cooperative kernel (no host polling)
+    if (prof) CK(cudaEventRecord(m->prof_ev[0], st));
+    double *pa = m->partials, *pb_ = m->partials + kMaxPartialBlocks;
+    double *p = m->pb[0];
+    MeshView V = m->view();
+    void *args3[] = {&V, &m->s, &m->r, &m->dinv, &p, &m->x, &m->ye, &m->inc_ptr, &m->inc, &m->K2, &m->KS,
+                     &m->hmask, &m->S, &pa, &pb_, &m->hist};
+    const void *fn = m->dim == 2 ? (const void *)k_cg_general_persistent<2> : (const void *)k_cg_general_persistent<3>;
+    CK(cudaLaunchCooperativeKernel(fn, dim3(m->coop_blocks), dim3(kBlock), args3, 0, st));
+    m->last_launches++;
+    if (prof) CK(cudaEventRecord(m->prof_ev[1], st));
+    if (prof) CK(cudaEventRecord(m->prof_ev[2], st));
+    stop = true;
+    launched = max_iter;
+  }
   while (!stop && launched < max_iter) {
     int cnt = std::min(chunk, max_iter - launched);
     for (int k = 0; k < cnt; ++k) {
@@ -771,7 +803,8 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   if (prof) {
     for (int j = 0; j < 5; ++j) m->prof_ms[j] = 0.0;
     int nit = std::min(launched, res.iter);
-    for (int it = 0; it < nit; ++it) {
+    const bool persistent = !m->structured && m->coop_blocks > 0;
+    for (int it = 0; it < (persistent ? std::min(nit, 1) : nit); ++it) {
       const int slot[2] = {0, 2};   // K1 (p/x update + apply + alpha), K2 (r update + reductions)
       for (int j = 0; j < 2; ++j) {
         float t = 0.f;

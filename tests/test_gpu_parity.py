@@ -24,6 +24,7 @@ CASES = {
     "c5s": lambda: config("c5", nx=20, ny=10, nz=10),
     "c5s_general": lambda: config("c5", nx=20, ny=10, nz=10),     # uniform H8 forced onto the general path
     "c3s_ragged": lambda: config("c3", nx=37, ny=9, nz=13),       # several CTA tiles + ragged tails in x, y, z
+    "c2_launches": lambda: config("c2"),     # general path with per-iteration launches (no persistent kernel)
     "amr2d": lambda: cantilever2d((5, 3), L=3, leaves=refine_some(2, (5, 3), 3, [(1, 1), (3, 0)]), rmin=0.3),
     "amr3d": lambda: cantilever3d((3, 2, 2), L=2, leaves=refine_some(3, (3, 2, 2), 2, [(1, 1, 0)]), rmin=0.4),
 }
@@ -37,10 +38,13 @@ def _setup(name):
         om = omesh.build_mesh(prob)
         if name.endswith("_general"):
             os.environ["TOMESH_FORCE_GENERAL"] = "1"
+        if name.endswith("_launches"):
+            os.environ["TOMESH_NO_PERSISTENT"] = "1"
         try:
             hm, m = product_mesh(prob)
         finally:
             os.environ.pop("TOMESH_FORCE_GENERAL", None)
+            os.environ.pop("TOMESH_NO_PERSISTENT", None)
         if name.startswith(("c3s", "c5s")):
             assert m.info()["structured"] == (0 if name.endswith("_general") else 1)
         x_dev = product_input_density(prob, hm, m)
@@ -114,7 +118,7 @@ def test_L2_converged_solve(name):
     assert abs(st.iters - ref.cg.iters) <= max(5, 0.05 * ref.cg.iters)
 
 
-@pytest.mark.parametrize("name", ["c2", "c5s"])
+@pytest.mark.parametrize("name", ["c2", "c2_launches", "c5s"])
 def test_warm_start_and_fixed_iterations(name):
     prob, om, hm, m, x_dev = _setup(name)
     u = torch.zeros(om.n_dof, dtype=torch.float64, device="cuda")
