@@ -336,21 +336,37 @@ __device__ __forceinline__ double g_ld(const double *p) {
   return v;
 }
 
-// p of DOF d: CG: Dinv r + beta p_{k-1} (formed on the fly; the node pass
-// stores the same value); plain: v.
-template <int MODE, bool COH>
-__device__ __forceinline__ double g_p(const double *__restrict__ r, const double *__restrict__ Dinv,
-                                      const double *__restrict__ po, double beta, int64_t d) {
-  if (MODE == G_PLAIN) return g_ld<COH>(po + d);
-  return fma(__ldg(Dinv + d), g_ld<COH>(r + d), beta * g_ld<COH>(po + d));
+// Node record of the general-path CG: zp[n] = {z_k = Dinv r_k (DIM), p_{k-1}
+// (DIM)}, written by the node pass, so that a corner gather is one contiguous
+// 16*DIM-byte record instead of separate r, Dinv and p loads.
+// p of node n (all DIM components): CG: z_k + beta p_{k-1} (formed on the fly;
+// the node pass forms the same value); plain: v.
+template <int DIM, int MODE, bool COH>
+__device__ __forceinline__ void g_pnode(const double *__restrict__ zp, const double *__restrict__ v, double beta,
+                                        int64_t n, double (&out)[DIM]) {
+  if (MODE == G_PLAIN) {
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) out[i] = g_ld<COH>(v + n * DIM + i);
+    return;
+  }
+  const double2 *rec = reinterpret_cast<const double2 *>(zp + n * 2 * DIM);
+  double t[2 * DIM];
+#pragma unroll
+  for (int h = 0; h < DIM; ++h) {
+    const double2 w = COH ? __ldcg(rec + h) : __ldg(rec + h);
+    t[2 * h] = w.x;
+    t[2 * h + 1] = w.y;
+  }
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) out[i] = fma(beta, t[DIM + i], t[i]);
 }
 
 // One element of the element pass: y_e = s_e K0 C_e p into ye; returns
 // s_e pbar^T K0 pbar (its share of p^T A p).
 template <int DIM, int MODE, bool COH>
 __device__ __forceinline__ double g_elem_one(const MeshView &M, int64_t e, const double *__restrict__ s,
-                                             const double *__restrict__ r, const double *__restrict__ Dinv,
-                                             const double *__restrict__ po, double *__restrict__ ye,
+                                             const double *__restrict__ zp, const double *__restrict__ po,
+                                             double *__restrict__ ye,
                                              const K0Dense2 &K2, const K0HadSym &H, const uint8_t *__restrict__ hmask,
                                              double beta) {
   constexpr int NC = 1 << DIM, ND = DIM * NC;
@@ -371,9 +387,12 @@ __device__ __forceinline__ double g_elem_one(const MeshView &M, int64_t e, const
   // interpolation of their parents
   double y[ND];
 #pragma unroll
-  for (int c = 0; c < NC; ++c)
+  for (int c = 0; c < NC; ++c) {
+    double t[DIM];
+    g_pnode<DIM, MODE, COH>(zp, po, beta, node[c], t);
 #pragma unroll
-    for (int i = 0; i < DIM; ++i) y[DIM * c + i] = g_p<MODE, COH>(r, Dinv, po, beta, (int64_t)node[c] * DIM + i);
+    for (int i = 0; i < DIM; ++i) y[DIM * c + i] = t[i];
+  }
   if (hm) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -384,9 +403,10 @@ __device__ __forceinline__ double g_elem_one(const MeshView &M, int64_t e, const
       for (int i = 0; i < DIM; ++i) acc[i] = 0.0;
       for (int k = M.hang_ptr[h]; k < M.hang_ptr[h + 1]; ++k) {
         const double w = M.hang_weight[k];
-        const int64_t pn = M.hang_parent[k];
+        double t[DIM];
+        g_pnode<DIM, MODE, COH>(zp, po, beta, M.hang_parent[k], t);
 #pragma unroll
-        for (int i = 0; i < DIM; ++i) acc[i] = fma(w, g_p<MODE, COH>(r, Dinv, po, beta, pn * DIM + i), acc[i]);
+        for (int i = 0; i < DIM; ++i) acc[i] = fma(w, t[i], acc[i]);
       }
 #pragma unroll
       for (int i = 0; i < DIM; ++i) y[DIM * c + i] = acc[i];
@@ -424,7 +444,7 @@ template <int DIM, int MODE, bool COH>
 __device__ __forceinline__ void g_node_one(int64_t n, const int64_t *__restrict__ inc_ptr,
                                            const uint32_t *__restrict__ inc, const double *__restrict__ ye,
                                            double *__restrict__ r, const double *__restrict__ Dinv,
-                                           double *__restrict__ p, double *__restrict__ x, double *__restrict__ q_out,
+                                           double *__restrict__ zp, double *__restrict__ x, double *__restrict__ q_out,
                                            double alpha, double beta, double (&acc)[2]) {
   double qv[DIM];
 #pragma unroll
@@ -449,30 +469,46 @@ __device__ __forceinline__ void g_node_one(int64_t n, const int64_t *__restrict_
       for (int i = 0; i < DIM; ++i) qv[i] = fma(w, v[j][i], qv[i]);
     }
   }
+  if (MODE == G_PLAIN) {
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) q_out[n * DIM + i] = qv[i];
+    return;
+  }
+  // own record: z_k, p_{k-1} -> p_k; x += alpha p_k; r -= alpha q on free
+  // DOFs; new record {z_{k+1} = Dinv r_{k+1}, p_k}
+  double2 *rec = reinterpret_cast<double2 *>(zp + n * 2 * DIM);
+  double t[2 * DIM];
+#pragma unroll
+  for (int h = 0; h < DIM; ++h) {
+    const double2 w = COH ? __ldcg(rec + h) : rec[h];
+    t[2 * h] = w.x;
+    t[2 * h + 1] = w.y;
+  }
 #pragma unroll
   for (int i = 0; i < DIM; ++i) {
     const int64_t d = n * DIM + i;
-    if (MODE == G_PLAIN) {
-      q_out[d] = qv[i];
-    } else {
-      const double di = __ldg(Dinv + d);
-      if (di != 0.0) {
-        const double pk = fma(di, r[d], beta * p[d]);
-        p[d] = pk;
-        x[d] = fma(alpha, pk, x[d]);
-        const double rn = fma(-alpha, qv[i], r[d]);
-        r[d] = rn;
-        acc[0] = fma(rn, di * rn, acc[0]);
-        acc[1] = fma(rn, rn, acc[1]);
-      }
+    const double di = __ldg(Dinv + d);
+    const double pk = fma(beta, t[DIM + i], t[i]);      // 0 on non-free DOFs (z = p = 0 there)
+    double zn = 0.0;
+    if (di != 0.0) {
+      x[d] = fma(alpha, pk, x[d]);
+      const double rn = fma(-alpha, qv[i], r[d]);
+      r[d] = rn;
+      zn = di * rn;
+      acc[0] = fma(rn, zn, acc[0]);
+      acc[1] = fma(rn, rn, acc[1]);
     }
+    t[i] = zn;
+    t[DIM + i] = pk;
   }
+#pragma unroll
+  for (int h = 0; h < DIM; ++h) rec[h] = make_double2(t[2 * h], t[2 * h + 1]);
 }
 
 template <int DIM, int MODE>
 __global__ void __launch_bounds__(256, 3) k_elem_pass(MeshView M, const double *__restrict__ s,
-                                                      const double *__restrict__ r, const double *__restrict__ Dinv,
-                                                      const double *__restrict__ po, double *__restrict__ ye,
+                                                      const double *__restrict__ zp, const double *__restrict__ po,
+                                                      double *__restrict__ ye,
                                                       const __grid_constant__ K0Dense2 K2,
                                                       const __grid_constant__ K0HadSym H, const uint8_t *__restrict__ hmask,
                                                       CgScalars *S, double *partials) {
@@ -480,7 +516,7 @@ __global__ void __launch_bounds__(256, 3) k_elem_pass(MeshView M, const double *
   const double beta = MODE == G_CG ? __ldcg(&S->beta) : 0.0;
   double pq = 0.0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M.n_el; e += (int64_t)gridDim.x * blockDim.x)
-    pq += g_elem_one<DIM, MODE, false>(M, e, s, r, Dinv, po, ye, K2, H, hmask, beta);
+    pq += g_elem_one<DIM, MODE, false>(M, e, s, zp, po, ye, K2, H, hmask, beta);
   if (MODE == G_CG) {
     double v[1] = {pq};
     if (grid_sum<1>(v, partials, &S->counter[CNT_PQ])) {
@@ -498,7 +534,7 @@ template <int DIM, int MODE>
 __global__ void __launch_bounds__(256) k_node_pass(int64_t n_node, const int64_t *__restrict__ inc_ptr,
                                                    const uint32_t *__restrict__ inc, const double *__restrict__ ye,
                                                    double *__restrict__ r, const double *__restrict__ Dinv,
-                                                   double *__restrict__ p, double *__restrict__ x,
+                                                   double *__restrict__ zp, double *__restrict__ x,
                                                    double *__restrict__ q_out, double *partials, CgScalars *S,
                                                    double *hist) {
   if (MODE == G_CG && cg_stopped(S)) return;
@@ -506,7 +542,215 @@ __global__ void __launch_bounds__(256) k_node_pass(int64_t n_node, const int64_t
   const double alpha = MODE == G_CG ? __ldcg(&S->alpha) : 0.0;
   double acc[2] = {0.0, 0.0};
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_node; n += (int64_t)gridDim.x * blockDim.x)
-    g_node_one<DIM, MODE, false>(n, inc_ptr, inc, ye, r, Dinv, p, x, q_out, alpha, beta, acc);
+    g_node_one<DIM, MODE, false>(n, inc_ptr, inc, ye, r, Dinv, zp, x, q_out, alpha, beta, acc);
+  if (MODE == G_CG) {
+    if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) {
+      cg_after_rupdate(S, acc[0], acc[1], hist);
+      if (S->done_next) S->done = 1;                 // x is already complete
+    }
+  }
+}
+
+// ---- lane-per-corner variants (latency-bound AMR meshes) --------------------------------
+// A group of 2^DIM lanes handles one element: lane c gathers corner c (with
+// the Eq. 6 interpolation if it is hanging), the element product runs across
+// the group with warp shuffles, lane c stores y_e[corner c].  In 3D the
+// Walsh-Hadamard stages are xor-shuffles and lane c holds Hadamard mode c.
+template <int DIM, int MODE, bool COH>
+__device__ __forceinline__ double g_elem_lane(const MeshView &M, int64_t e, int c, const double *__restrict__ s,
+                                              const double *__restrict__ zp, const double *__restrict__ po,
+                                              double *__restrict__ ye,
+                                              const K0Dense2 &K2, const K0HadSym &H,
+                                              const uint8_t *__restrict__ hmask, double beta, bool live) {
+  constexpr int NC = 1 << DIM;
+  const int n = __ldg(M.elem_node + e * NC + c);
+  double v[DIM];
+  g_pnode<DIM, MODE, COH>(zp, po, beta, n, v);
+  if ((__ldg(hmask + e) >> c) & 1) {
+    const int h = M.node_hang[n];
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) v[i] = 0.0;
+    for (int k = M.hang_ptr[h]; k < M.hang_ptr[h + 1]; ++k) {
+      const double w = M.hang_weight[k];
+      double t[DIM];
+      g_pnode<DIM, MODE, COH>(zp, po, beta, M.hang_parent[k], t);
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) v[i] = fma(w, t[i], v[i]);
+    }
+  }
+  const double se = __ldg(s + e);
+  double en = 0.0, y[DIM];
+  if constexpr (DIM == 3) {
+    // forward WHT over the group: stage b pairs lanes c and c ^ b
+#pragma unroll
+    for (int b = 1; b < 8; b <<= 1)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double o = __shfl_xor_sync(0xffffffffu, v[i], b);
+        v[i] = (c & b) ? o - v[i] : v[i] + o;
+      }
+    // middle: mode m = c; coupling to lane m ^ e_i ^ e_j, component j
+    const int m = c;
+    const int bit[3] = {m & 1, (m >> 1) & 1, (m >> 2) & 1};
+    const int pop = bit[0] + bit[1] + bit[2];
+    double xo[3][3];                                    // xo[i][j] = xhat(m ^ e_i ^ e_j, j)
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = i + 1; j < 3; ++j) {
+        const int mask = (1 << i) | (1 << j);
+        xo[i][j] = __shfl_xor_sync(0xffffffffu, v[j], mask);
+        xo[j][i] = __shfl_xor_sync(0xffffffffu, v[i], mask);
+      }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int b = bit[i], nn = pop - b;
+      const double dco = b ? (nn == 0 ? H.d[1][0] : nn == 1 ? H.d[1][1] : H.d[1][2])
+                           : (nn == 0 ? 0.0 : nn == 1 ? H.d[0][1] : H.d[0][2]);
+      double acc = dco * v[i];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        if (j == i) continue;
+        const int t = 3 - i - j;
+        const double oco = b ? (bit[t] ? H.o[1][1] : H.o[1][0]) : (bit[t] ? H.o[0][1] : H.o[0][0]);
+        acc = (bit[j] != b) ? fma(oco, xo[i][j], acc) : acc;
+      }
+      y[i] = acc;
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) en = fma(v[i], y[i], en);
+    // inverse WHT over the group
+#pragma unroll
+    for (int b = 1; b < 8; b <<= 1)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double o = __shfl_xor_sync(0xffffffffu, y[i], b);
+        y[i] = (c & b) ? o - y[i] : y[i] + o;
+      }
+  } else {
+    // 2D: y(c,i) = sum_{c',j} K0[(c,i),(c',j)] v(c',j), the other corners by shuffles
+    const int base = (threadIdx.x & 31) & ~(NC - 1);
+    double vv[NC][2];
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) vv[cc][j] = __shfl_sync(0xffffffffu, v[j], base + cc);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc = fma(K2.K[(2 * c + i) * 8 + 2 * cc + j], vv[cc][j], acc);
+      y[i] = acc;
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) en = fma(v[i], y[i], en);
+  }
+  if (live) {
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) ye[(e * NC + c) * DIM + i] = se * y[i];
+  }
+  return live ? se * en : 0.0;
+}
+
+template <int DIM, int MODE>
+__global__ void __launch_bounds__(256) k_elem_pass_lanes(MeshView M, const double *__restrict__ s,
+                                                         const double *__restrict__ zp, const double *__restrict__ po,
+                                                         double *__restrict__ ye,
+                                                         const __grid_constant__ K0Dense2 K2,
+                                                         const __grid_constant__ K0HadSym H,
+                                                         const uint8_t *__restrict__ hmask, CgScalars *S,
+                                                         double *partials) {
+  constexpr int NC = 1 << DIM;
+  if (MODE == G_CG && cg_stopped(S)) return;
+  const double beta = MODE == G_CG ? __ldcg(&S->beta) : 0.0;
+  const int c = threadIdx.x & (NC - 1);
+  const int64_t groups = ((int64_t)gridDim.x * blockDim.x) / NC;
+  double pq = 0.0;
+  // the loop bound is uniform per warp (whole groups), so the shuffles stay converged
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / NC - (threadIdx.x & 31) / NC;
+       base < M.n_el; base += groups) {
+    const int64_t e = base + (threadIdx.x & 31) / NC;
+    const bool live = e < M.n_el;
+    pq += g_elem_lane<DIM, MODE, false>(M, live ? e : M.n_el - 1, c, s, zp, po, ye, K2, H, hmask, beta, live);
+  }
+  if (MODE == G_CG) {
+    double v[1] = {pq};
+    if (grid_sum<1>(v, partials, &S->counter[CNT_PQ])) {
+      if (!(v[0] > 0.0)) {
+        S->status = (v[0] != v[0]) ? -5 : -6;
+        S->done = 1;
+      } else {
+        S->alpha = S->rho / v[0];
+      }
+    }
+  }
+}
+
+// Node pass with a group of 4 lanes per node: lane l sums incidences l, l+4,
+// ... of the node, an xor-shuffle tree completes q_n in every lane of the
+// group, and lane i < DIM updates component i of the node (record, x, r).
+template <int DIM, int MODE>
+__global__ void __launch_bounds__(256) k_node_pass_lanes(int64_t n_node, const int64_t *__restrict__ inc_ptr,
+                                                         const uint32_t *__restrict__ inc, const double *__restrict__ ye,
+                                                         double *__restrict__ r, const double *__restrict__ Dinv,
+                                                         double *__restrict__ zp, double *__restrict__ x,
+                                                         double *__restrict__ q_out, double *partials, CgScalars *S,
+                                                         double *hist) {
+  constexpr int G = 4;
+  if (MODE == G_CG && cg_stopped(S)) return;
+  const double beta = MODE == G_CG ? __ldcg(&S->beta) : 0.0;
+  const double alpha = MODE == G_CG ? __ldcg(&S->alpha) : 0.0;
+  const int l = threadIdx.x & (G - 1);
+  const int64_t groups = ((int64_t)gridDim.x * blockDim.x) / G;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G - (threadIdx.x & 31) / G; base < n_node;
+       base += groups) {
+    const int64_t n = base + (threadIdx.x & 31) / G;
+    const bool live = n < n_node;
+    double qv[DIM];
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) qv[i] = 0.0;
+    if (live) {
+      const int64_t k1 = inc_ptr[n + 1];
+      for (int64_t k = inc_ptr[n] + l; k < k1; k += G) {
+        const uint32_t t = __ldg(&inc[k]);
+        const double w = (t >> 30) == 0 ? 1.0 : (t >> 30) == 1 ? 0.5 : 0.25;
+        const double *src = ye + (int64_t)(t & 0x3fffffffu) * DIM;
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) qv[i] = fma(w, __ldg(src + i), qv[i]);
+      }
+    }
+#pragma unroll
+    for (int b = 1; b < G; b <<= 1)
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) qv[i] += __shfl_xor_sync(0xffffffffu, qv[i], b);
+    if (!live || l >= DIM) continue;
+    // lane l < DIM: component l
+    double qc = qv[0];
+#pragma unroll
+    for (int i = 1; i < DIM; ++i) qc = (l == i) ? qv[i] : qc;
+    const int64_t d = n * DIM + l;
+    if (MODE == G_PLAIN) {
+      q_out[d] = qc;
+      continue;
+    }
+    double *rec = zp + n * 2 * DIM;
+    const double di = __ldg(Dinv + d);
+    const double pk = fma(beta, rec[DIM + l], rec[l]);
+    double zn = 0.0;
+    if (di != 0.0) {
+      x[d] = fma(alpha, pk, x[d]);
+      const double rn = fma(-alpha, qc, r[d]);
+      r[d] = rn;
+      zn = di * rn;
+      acc[0] = fma(rn, zn, acc[0]);
+      acc[1] = fma(rn, rn, acc[1]);
+    }
+    rec[l] = zn;
+    rec[DIM + l] = pk;
+  }
   if (MODE == G_CG) {
     if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) {
       cg_after_rupdate(S, acc[0], acc[1], hist);
@@ -557,7 +801,7 @@ __device__ __forceinline__ void g_sum_partials(const double *part, int nb, doubl
 template <int DIM>
 __global__ void __launch_bounds__(256, 2) k_cg_general_persistent(
     MeshView M, const double *__restrict__ s, double *__restrict__ r, const double *__restrict__ Dinv,
-    double *__restrict__ p, double *__restrict__ x, double *__restrict__ ye, const int64_t *__restrict__ inc_ptr,
+    double *__restrict__ zp, double *__restrict__ x, double *__restrict__ ye, const int64_t *__restrict__ inc_ptr,
     const uint32_t *__restrict__ inc, const __grid_constant__ K0Dense2 K2, const __grid_constant__ K0HadSym H,
     const uint8_t *__restrict__ hmask, CgScalars *S, double *part_a, double *part_b, double *hist) {
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
@@ -574,7 +818,7 @@ __global__ void __launch_bounds__(256, 2) k_cg_general_persistent(
   while (!done && it < max_iter) {
     double v1[1] = {0.0};
     for (int64_t e = tid0; e < M.n_el; e += stride)
-      v1[0] += g_elem_one<DIM, G_CG, true>(M, e, s, r, Dinv, p, ye, K2, H, hmask, beta);
+      v1[0] += g_elem_one<DIM, G_CG, true>(M, e, s, zp, nullptr, ye, K2, H, hmask, beta);
     block_sum<1>(v1);
     if (threadIdx.x == 0) __stcg(&part_a[blockIdx.x], v1[0]);
     grid.sync();
@@ -588,7 +832,7 @@ __global__ void __launch_bounds__(256, 2) k_cg_general_persistent(
     const double alpha = rho / pq;
     double v2[2] = {0.0, 0.0};
     for (int64_t n = tid0; n < M.n_node; n += stride)
-      g_node_one<DIM, G_CG, true>(n, inc_ptr, inc, ye, r, Dinv, p, x, nullptr, alpha, beta, v2);
+      g_node_one<DIM, G_CG, true>(n, inc_ptr, inc, ye, r, Dinv, zp, x, nullptr, alpha, beta, v2);
     block_sum<2>(v2);
     if (threadIdx.x == 0) {
       __stcg(&part_b[2 * blockIdx.x], v2[0]);
@@ -617,6 +861,18 @@ __global__ void __launch_bounds__(256, 2) k_cg_general_persistent(
     S->status = status;
     S->done = 1;
   }
+}
+
+// zp[n] = {Dinv r0, 0}: the record before the first general-path iteration.
+template <int DIM>
+__global__ void k_zp_init(int64_t n_node, const double *__restrict__ r, const double *__restrict__ Dinv,
+                          double *__restrict__ zp) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_node; n += (int64_t)gridDim.x * blockDim.x)
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) {
+      zp[n * 2 * DIM + i] = Dinv[n * DIM + i] * r[n * DIM + i];
+      zp[n * 2 * DIM + DIM + i] = 0.0;
+    }
 }
 
 // ---- sensitivities (a10) ----------------------------------------------------------------

@@ -56,6 +56,7 @@ struct to_mesh {
   uint32_t *inc = nullptr;
   double *ye = nullptr;                // general path: element vectors s_e K0 C_e p
   uint8_t *hmask = nullptr;            // general path: bit c = corner c of the element is hanging
+  double *zp = nullptr;                // general path: node records {Dinv r, p}
   int coop_blocks = 0;                 // general path: grid of the persistent cooperative solver (0 = off)
   int32_t *filt_idx = nullptr;
   // workspace
@@ -391,6 +392,7 @@ int setup_incidence(const to_mesh_desc *d, const std::vector<int32_t> &node_hang
   RC(upload_array(m, &m->inc_ptr, ptr.data(), ptr.size(), st));
   RC(upload_array(m, &m->inc, inc.data(), inc.size(), st));
   RC(m->alloc(&m->ye, (size_t)d->n_elem * nc * d->dim));
+  RC(m->alloc(&m->zp, (size_t)d->n_node * 2 * d->dim));
   CK(cudaMemsetAsync(m->ye, 0, sizeof(double) * (size_t)d->n_elem * nc * d->dim, st));
   return 0;
 }
@@ -555,11 +557,11 @@ int launch_rhs(to_mesh *m, double *b, cudaStream_t st) {
 int launch_matvec(to_mesh *m, const double *p, double *q, cudaStream_t st) {
   const int ge = grid_for(m->n_el, kBlock, 16), gn = grid_for(m->n_node, kBlock, 16);
   if (m->dim == 2) {
-    k_elem_pass<2, G_PLAIN><<<ge, kBlock, 0, st>>>(m->view(), m->s, nullptr, nullptr, p, m->ye, m->K2, m->KS, m->hmask, nullptr, nullptr);
+    k_elem_pass<2, G_PLAIN><<<ge, kBlock, 0, st>>>(m->view(), m->s, nullptr, p, m->ye, m->K2, m->KS, m->hmask, nullptr, nullptr);
     k_node_pass<2, G_PLAIN><<<gn, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, nullptr, nullptr, nullptr,
                                                    nullptr, q, nullptr, nullptr, nullptr);
   } else {
-    k_elem_pass<3, G_PLAIN><<<ge, kBlock, 0, st>>>(m->view(), m->s, nullptr, nullptr, p, m->ye, m->K2, m->KS, m->hmask, nullptr, nullptr);
+    k_elem_pass<3, G_PLAIN><<<ge, kBlock, 0, st>>>(m->view(), m->s, nullptr, p, m->ye, m->K2, m->KS, m->hmask, nullptr, nullptr);
     k_node_pass<3, G_PLAIN><<<gn, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, nullptr, nullptr, nullptr,
                                                    nullptr, q, nullptr, nullptr, nullptr);
   }
@@ -643,15 +645,18 @@ int op_apply(to_mesh *m, const double *in, double *out, cudaStream_t st) {
 // General path, iteration k: element pass (p_k formed on the fly, y_e,
 // p^T A p -> alpha_k) + node pass (q, r, x, p_k in place, rho, rr -> beta_k).
 int op_cg_general(to_mesh *m, cudaStream_t st) {
-  const int ge = grid_for(m->n_el, kBlock, 16), gn = grid_for(m->n_node, kBlock, 16);
+  // one resident wave (3 blocks of 256 per SM): several elements / nodes per
+  // thread, so the end-of-kernel reduction barrier is amortised
+  const int ge4 = grid_for(m->n_el * 4, kBlock, 8), ge8 = grid_for(m->n_el * 8, kBlock, 8);
+  const int gn4 = grid_for(m->n_node * 4, kBlock, 8);
   double *p = m->pb[0];
   if (m->dim == 2) {
-    k_elem_pass<2, G_CG><<<ge, kBlock, 0, st>>>(m->view(), m->s, m->r, m->dinv, p, m->ye, m->K2, m->KS, m->hmask, m->S, m->partials);
-    k_node_pass<2, G_CG><<<gn, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, m->r, m->dinv, p, m->x, nullptr,
+    k_elem_pass_lanes<2, G_CG><<<ge4, kBlock, 0, st>>>(m->view(), m->s, m->zp, nullptr, m->ye, m->K2, m->KS, m->hmask, m->S, m->partials);
+    k_node_pass_lanes<2, G_CG><<<gn4, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, m->r, m->dinv, m->zp, m->x, nullptr,
                                                 m->partials, m->S, m->hist);
   } else {
-    k_elem_pass<3, G_CG><<<ge, kBlock, 0, st>>>(m->view(), m->s, m->r, m->dinv, p, m->ye, m->K2, m->KS, m->hmask, m->S, m->partials);
-    k_node_pass<3, G_CG><<<gn, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, m->r, m->dinv, p, m->x, nullptr,
+    k_elem_pass_lanes<3, G_CG><<<ge8, kBlock, 0, st>>>(m->view(), m->s, m->zp, nullptr, m->ye, m->K2, m->KS, m->hmask, m->S, m->partials);
+    k_node_pass_lanes<3, G_CG><<<gn4, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, m->r, m->dinv, m->zp, m->x, nullptr,
                                                 m->partials, m->S, m->hist);
   }
   m->last_launches += 2;
@@ -738,7 +743,12 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   } else {
     CK(cudaMemsetAsync(m->x, 0, sizeof(double) * n, st));
   }
-  if (!m->structured) RC(op_cg_k2<true>(m, rtol, st));
+  if (!m->structured) {
+    RC(op_cg_k2<true>(m, rtol, st));
+    if (m->dim == 2) k_zp_init<2><<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->r, m->dinv, m->zp);
+    else k_zp_init<3><<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->r, m->dinv, m->zp);
+    m->last_launches++;
+  }
   RC(check_launch());
 
   const bool prof = (flags & TO_PROFILE) != 0;
@@ -763,7 +773,7 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
     double *pa = m->partials, *pb_ = m->partials + kMaxPartialBlocks;
     double *p = m->pb[0];
     MeshView V = m->view();
-    void *args3[] = {&V, &m->s, &m->r, &m->dinv, &p, &m->x, &m->ye, &m->inc_ptr, &m->inc, &m->K2, &m->KS,
+    void *args3[] = {&V, &m->s, &m->r, &m->dinv, &m->zp, &m->x, &m->ye, &m->inc_ptr, &m->inc, &m->K2, &m->KS,
                      &m->hmask, &m->S, &pa, &pb_, &m->hist};
     const void *fn = m->dim == 2 ? (const void *)k_cg_general_persistent<2> : (const void *)k_cg_general_persistent<3>;
     CK(cudaLaunchCooperativeKernel(fn, dim3(m->coop_blocks), dim3(kBlock), args3, 0, st));
