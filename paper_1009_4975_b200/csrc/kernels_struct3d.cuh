@@ -475,6 +475,44 @@ __global__ void __launch_bounds__(512) k_final_s3(int n, const double *__restric
   if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) cg_final_step(S, n_iter, acc[0], acc[1], rtol, hist);
 }
 
+// ---- filter on the uniform lattice (a11; Eqs. 3-5) --------------------
+// On a uniform grid H_de = rmin - |c_d - c_e| depends only on the lattice
+// offset d - e, so the neighbour set of C9 is a fixed stencil of offsets with
+// |offset|^2 h^2 < rmin^2 (exact on these dyadic values), truncated at the
+// box boundary; V_d = h^3 for every element.  Two passes: the filtered
+// quantity (x in for SENS, in for DENS) is scattered to lexicographic order,
+// then each element (canonical order) sums its stencil.
+struct S3FilterOffset {
+  int di, dj, dk;
+  double w;          // H * V
+};
+
+__global__ void k_filter_s3_scatter(int64_t n, const int32_t *__restrict__ perm_el, int mode,
+                                    const double *__restrict__ x, const double *__restrict__ in,
+                                    double *__restrict__ t_lex) {
+  GRID_STRIDE(e, n) { t_lex[perm_el[e]] = mode == 0 ? x[e] * in[e] : in[e]; }
+}
+
+__global__ void k_filter_s3(GridView G, int64_t n, const int32_t *__restrict__ perm_el,
+                            const S3FilterOffset *__restrict__ offs, int n_off, int mode,
+                            const double *__restrict__ x, const double *__restrict__ t_lex, double *__restrict__ out) {
+  GRID_STRIDE(e, n) {
+    const int64_t l = perm_el[e];
+    const int i = (int)(l % G.EX);
+    const int64_t rest = l / G.EX;
+    const int j = (int)(rest % G.EY), k = (int)(rest / G.EY);
+    double num = 0.0, den = 0.0;
+    for (int o = 0; o < n_off; ++o) {
+      const S3FilterOffset f = offs[o];
+      const int ii = i + f.di, jj = j + f.dj, kk = k + f.dk;
+      if (ii < 0 || ii >= G.EX || jj < 0 || jj >= G.EY || kk < 0 || kk >= G.EZ) continue;
+      num = fma(f.w, __ldg(&t_lex[ii + (int64_t)G.EX * (jj + (int64_t)G.EY * kk)]), num);
+      den += f.w;
+    }
+    out[e] = mode == 0 ? num / (x[e] * den) : num / den;
+  }
+}
+
 // ---- setup kernels of the structured path ------------------------------------------------
 
 // s in lexicographic element order from x in canonical (Morton) element order.

@@ -52,6 +52,9 @@ struct to_mesh {
   double *hang_weight = nullptr, *child_weight = nullptr, *load = nullptr;
   uint8_t *free_dof = nullptr;
   int64_t *filt_ptr = nullptr;
+  S3FilterOffset *foffs = nullptr;     // structured filter stencil
+  int n_foffs = 0;
+  double *ftmp = nullptr;              // structured filter: lexicographic temporary
   int64_t *inc_ptr = nullptr;          // general path: node -> (element, corner, weight) incidences
   uint32_t *inc = nullptr;
   double *ye = nullptr;                // general path: element vectors s_e K0 C_e p
@@ -456,10 +459,7 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
     RC(upload_array(m, &m->child_hang, chang.data(), chang.size(), st));
     RC(upload_array(m, &m->child_weight, cw.data(), cw.size(), st));
   }
-  if (m->filt_nnz > 0 || d->rmin > 0.0) {
-    RC(upload_array(m, &m->filt_ptr, d->filt_ptr, (size_t)m->n_el + 1, st));
-    RC(upload_array(m, &m->filt_idx, d->filt_idx, (size_t)std::max<int64_t>(1, m->filt_nnz), st));
-  }
+
   RC(m->alloc(&m->partials, (size_t)kMaxPartialBlocks * 4));
   RC(m->alloc(&m->S, 1));
   CK(cudaMemsetAsync(m->S, 0, sizeof(CgScalars), st));
@@ -475,6 +475,25 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
   // diagnostics: TOMESH_FORCE_GENERAL=1 keeps uniform H8 meshes on the general path
   m->force_general = std::getenv("TOMESH_FORCE_GENERAL") != nullptr;
   RC(setup_structured(d, free_dof, st, m));
+  // (the structured path filters with a lattice stencil and needs no lists)
+  if ((m->filt_nnz > 0 || d->rmin > 0.0) && !m->structured) {
+    RC(upload_array(m, &m->filt_ptr, d->filt_ptr, (size_t)m->n_el + 1, st));
+    RC(upload_array(m, &m->filt_idx, d->filt_idx, (size_t)std::max<int64_t>(1, m->filt_nnz), st));
+  }
+  if (d->rmin > 0.0 && m->structured) {
+    const double h = m->h_struct, r2 = d->rmin * d->rmin, V = h * h * h;
+    const int R = (int)std::ceil(d->rmin / h) + 1;
+    std::vector<S3FilterOffset> offs;
+    for (int dk = -R; dk <= R; ++dk)
+      for (int dj = -R; dj <= R; ++dj)
+        for (int di = -R; di <= R; ++di) {
+          const double d2 = (double)(di * di + dj * dj + dk * dk) * h * h;   // exact: integer times h^2
+          if (d2 < r2) offs.push_back({di, dj, dk, (d->rmin - std::sqrt(d2)) * V});
+        }
+    m->n_foffs = (int)offs.size();
+    RC(upload_array(m, &m->foffs, offs.data(), offs.size(), st));
+    RC(m->alloc(&m->ftmp, (size_t)m->n_el));
+  }
   if (!m->structured) {
     RC(setup_incidence(d, node_hang, st, m));
     // persistent cooperative solver: as many co-resident blocks as the work needs
@@ -970,6 +989,11 @@ extern "C" int to_filter(to_mesh *m, int32_t mode, const double *x_dev, const do
     return 0;
   }
   int g = grid_for(m->n_el);
+  if (m->structured) {
+    k_filter_s3_scatter<<<g, kBlock, 0, st>>>(m->n_el, m->perm_el, mode, x_dev, in_dev, m->ftmp);
+    k_filter_s3<<<g, kBlock, 0, st>>>(m->G, m->n_el, m->perm_el, m->foffs, m->n_foffs, mode, x_dev, m->ftmp, out_dev);
+    return check_launch();
+  }
   if (m->dim == 2) k_filter<2><<<g, kBlock, 0, st>>>(m->view(), m->filt_ptr, m->filt_idx, m->rmin, mode, x_dev, in_dev, out_dev);
   else k_filter<3><<<g, kBlock, 0, st>>>(m->view(), m->filt_ptr, m->filt_idx, m->rmin, mode, x_dev, in_dev, out_dev);
   return check_launch();
