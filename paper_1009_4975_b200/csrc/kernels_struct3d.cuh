@@ -91,7 +91,7 @@ struct S3Smem {
   double qa[kS3NBuf][PD];                                     // q_{k-1}, TMA box
   double pa[kS3NBuf][PD];                                     // p_{k-1}, TMA box
   double dn[kS3NBuf][PN];                                     // Dinv per node, TMA box
-  double pn[3][PY][kS3RowD];                                  // p_k ring: planes k mod 3
+  double pn[4][PY][kS3RowD];                                  // p_k ring: planes k mod 4
   double own[3][4][TYW * 32];                                 // owned node of plane k mod 3: z_k (3), Dinv
   double xch[2][TYW - 1][3][32];                              // y-exchange (layer parity); row TYW-1 sends to nobody
   unsigned long long mbar[kS3NBuf];
@@ -191,13 +191,15 @@ __device__ __forceinline__ void s3_form_node(const S3Smem<TYW> &sm, int b, int r
 // MODE = S3_PLAIN: q = C^T K C v for a v that vanishes on non-free DOFs.
 //
 // Per CTA the layers ek = k_lo-1 .. k_hi-1 run with one CTA barrier each:
-//   1. element ek from p planes ek, ek+1 (ring slots ek%3, (ek+1)%3); x routing
+//   1. element ek from p planes ek, ek+1 (ring slots ek%4, (ek+1)%4); x routing
 //      by warp shuffle; upper-row corners to the y-exchange (layer parity)
-//   2. barrier
-//   3. y-exchange read: q and the dots of the owned node of plane ek
-//   4. form plane ek+3 into ring slot ek%3 (free since step 2) from the TMA
-//      staging; owners write r_k, p_k, update x, keep z_k, Dinv for step 3.
-//      The last warp done with a staging buffer issues its next plane (+NBUF).
+//   2. form plane ek+3 into ring slot (ek+3)%4 (last read by layer ek-1,
+//      before the previous barrier) from the TMA staging; owners write r_k,
+//      p_k, update x, keep z_k, Dinv.  The last warp done with a staging buffer
+//      issues its next plane (+NBUF).  Runs before the barrier, overlapping
+//      the other warps' element work.
+//   3. barrier
+//   4. y-exchange read: q and the dots of the owned node of plane ek
 // (A variant with neighbour-only progress counters instead of the barrier was
 // measured 18% slower: the counter handshakes cost more than the barrier.)
 template <int TYW, int MODE>
@@ -276,8 +278,8 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
       mbar_wait(&sm.mbar[bb], (phase >> bb) & 1);
       phase ^= 1u << bb;
     }
-    const int slot = (k + 3) % 3;
-    double(*dst)[kS3RowD] = sm.pn[slot];
+    const int slot = (k + 3) % 3;                       // own ring slot
+    double(*dst)[kS3RowD] = sm.pn[(k + 4) & 3];
     double rv[3], pv[3], dv;
     s3_form_node<TYW, MODE>(sm, bb, ty, tx, off, noff, alpha_old, beta, pin, rv, pv, dv);
 #pragma unroll
@@ -351,7 +353,7 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
   auto layer = [&](const int ek, double &s_slot, double(&x_slot)[3]) {
     const double se = s_valid(ek) ? s_slot : 0.0;
     s_slot = load_s(ek + 2);
-    const int slo = (ek + 3) % 3, shi = (ek + 4) % 3;
+    const int slo = (ek + 4) & 3, shi = (ek + 5) & 3;
     double y[24];
     {
 #pragma unroll
@@ -407,27 +409,34 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
 #pragma unroll
       for (int d = 0; d < 3; ++d) sm.xch[ek & 1][ty][d][tx] = a_row[1][d];
     }
+    // the owned node's z_k and Dinv for plane ek (own ring slot ek%3, which the
+    // form of plane ek+3 below overwrites)
+    const bool qmine = ek >= k_lo && owner;
+    double zown[3] = {0.0, 0.0, 0.0}, dvown = 0.0;
+    if (CG && qmine) {
+      const int os = (ek + 3) % 3;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) zown[d] = sm.own[os][d][tid];
+      dvown = sm.own[os][3][tid];
+    }
+    // plane ek+3 goes to ring slot (ek+3)%4, last read by layer ek-1's elements
+    // (before the previous barrier), so the form runs before this layer's
+    // barrier and overlaps the other warps' element work
+    if (ek + 3 <= k_hi) form_plane(ek + 3, x_slot);
     __syncthreads();                                    // the one CTA barrier of the layer
     // node plane ek is complete: (cz=0) parts of layer ek + (cz=1) parts of layer ek-1
-    {
-      if (ek >= k_lo && owner) {
-        const int64_t dof = s3_row(G, ej, ek) + 3 * ei;
-        const int slot = (ek + 3) % 3;
-        const double dv = CG ? sm.own[slot][3][tid] : 0.0;
+    if (qmine) {
+      const int64_t dof = s3_row(G, ej, ek) + 3 * ei;
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          const double qv = a_row[0][d] + sm.xch[ek & 1][ty - 1][d][tx];
-          __stcs(&q[dof + d], qv);
-          if (CG) {
-            dots[2] = fma(sm.pn[slot][ty][off + 3 * tx + d], qv, dots[2]);   // p_k of the own node (this thread formed it)
-            dots[3] = fma(sm.own[slot][d][tid], qv, dots[3]);
-            dots[4] = fma(dv * qv, qv, dots[4]);
-          }
+      for (int d = 0; d < 3; ++d) {
+        const double qv = a_row[0][d] + sm.xch[ek & 1][ty - 1][d][tx];
+        __stcs(&q[dof + d], qv);
+        if (CG) {
+          dots[2] = fma(sm.pn[slo][ty][off + 3 * tx + d], qv, dots[2]);   // p_k of the own node (this thread formed it)
+          dots[3] = fma(zown[d], qv, dots[3]);
+          dots[4] = fma(dvown * qv, qv, dots[4]);
         }
       }
-    }
-    if (ek + 3 <= k_hi) {
-      form_plane(ek + 3, x_slot);                       // slot ek%3: free since the barrier
     }
   };
   // ek = k_lo-1+2t forms plane k_lo+2+2t (x slot xa); ek+1 forms k_lo+3+2t (xb)

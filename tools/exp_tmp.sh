@@ -1,4 +1,6 @@
 cd $GRAFT_REPO_ROOT
-sed -i 's|^NVCC_FLAGS = \[.*|NVCC_FLAGS = ["-DTOMESH_EXP_FIXED_SCALARS", "-DTOMESH_EXP_NO_ELEMENT",|' paper_1009_4975_b200/build.py
-python -c "from paper_1009_4975_b200 import build; build.build(force=True)"
-python tools/prof_run.py c5 3 && ncu --set full --import-source on --clock-control none -k regex:k_apply_s3 -s 2 -c 1 -o gpurun_out/noelem python tools/prof_run.py c5 3 > /dev/null 2>&1; ls gpurun_out
+for FL in "" "-DTOMESH_EXP_ONE_CTA"; do
+  sed -i "s|^NVCC_FLAGS = \[.*|NVCC_FLAGS = [\"-DEXPDUMMY\", $(for f in $FL; do printf '"%s", ' $f; done)|" paper_1009_4975_b200/build.py
+  python -c "from paper_1009_4975_b200 import build; build.build(force=True)"
+  echo "FLAGS: $FL"; python tools/microbench.py c5 | cut -c1-200
+done
