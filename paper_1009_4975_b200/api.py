@@ -160,6 +160,42 @@ def _stream(stream):
     return C.c_void_p(s.cuda_stream)
 
 
+def make_desc(host: HostMesh, E0, Emin, nu, rmin):
+    """to_mesh_desc of a host mesh (argument marshalling only); returns the
+    struct and the numpy arrays it points into (keep them alive)."""
+    keep = []
+
+    def arr(a, dt):
+        a = np.ascontiguousarray(a, dtype=dt)
+        keep.append(a)
+        return _ptr(a)
+
+    d = L.ToMeshDesc()
+    d.dim = host.dim
+    d.max_level = host.L
+    d.h0 = host.h0
+    d.n_elem = host.n_el
+    d.n_node = host.n_node
+    d.elem_node = arr(host.elem_node, np.int32)
+    d.elem_anchor = arr(host.elem_anchor, np.int32)
+    d.elem_level = arr(host.elem_level, np.int8)
+    d.n_hang = host.hang_node.shape[0]
+    d.hang_node = arr(host.hang_node, np.int32)
+    d.hang_ptr = arr(host.hang_ptr, np.int32)
+    d.hang_parent = arr(host.hang_parent, np.int32)
+    d.hang_weight = arr(host.hang_weight, np.float64)
+    d.n_fixed = host.fixed_dof.shape[0]
+    d.fixed_dof = arr(host.fixed_dof, np.int64)
+    d.load = arr(host.load, np.float64)
+    d.E0, d.Emin, d.nu = E0, Emin, nu
+    d.rmin = rmin if host.filt_ptr is not None else 0.0
+    if host.filt_ptr is not None and rmin > 0:
+        d.filt_nnz = host.filt_idx.shape[0]
+        d.filt_ptr = arr(host.filt_ptr, np.int64)
+        d.filt_idx = arr(host.filt_idx, np.int32)
+    return d, keep
+
+
 class Mesh:
     """Device copy of a mesh + CG workspace (tomesh_upload / tomesh_free)."""
 
@@ -171,36 +207,7 @@ class Mesh:
         self.n_el, self.n_node, self.n_dof = host.n_el, host.n_node, host.n_dof
         self.E0, self.Emin, self.nu = E0, Emin, nu
         rmin = host.rmin if rmin is None else rmin
-        keep = []
-
-        def arr(a, dt):
-            a = np.ascontiguousarray(a, dtype=dt)
-            keep.append(a)
-            return _ptr(a)
-
-        d = L.ToMeshDesc()
-        d.dim = host.dim
-        d.max_level = host.L
-        d.h0 = host.h0
-        d.n_elem = host.n_el
-        d.n_node = host.n_node
-        d.elem_node = arr(host.elem_node, np.int32)
-        d.elem_anchor = arr(host.elem_anchor, np.int32)
-        d.elem_level = arr(host.elem_level, np.int8)
-        d.n_hang = host.hang_node.shape[0]
-        d.hang_node = arr(host.hang_node, np.int32)
-        d.hang_ptr = arr(host.hang_ptr, np.int32)
-        d.hang_parent = arr(host.hang_parent, np.int32)
-        d.hang_weight = arr(host.hang_weight, np.float64)
-        d.n_fixed = host.fixed_dof.shape[0]
-        d.fixed_dof = arr(host.fixed_dof, np.int64)
-        d.load = arr(host.load, np.float64)
-        d.E0, d.Emin, d.nu = E0, Emin, nu
-        d.rmin = rmin if host.filt_ptr is not None else 0.0
-        if host.filt_ptr is not None and rmin > 0:
-            d.filt_nnz = host.filt_idx.shape[0]
-            d.filt_ptr = arr(host.filt_ptr, np.int64)
-            d.filt_idx = arr(host.filt_idx, np.int32)
+        d, self._keep = make_desc(host, E0, Emin, nu, rmin)
         self._h = C.c_void_p()
         with torch.cuda.device(self.device):
             L.check(L.lib().tomesh_upload(C.byref(d), device, _stream(stream), C.byref(self._h)), "tomesh_upload")

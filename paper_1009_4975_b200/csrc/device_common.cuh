@@ -98,6 +98,12 @@ __device__ __forceinline__ bool grid_sum(double (&v)[NV], double *partials, uint
   return tid == 0;
 }
 
+// Record a failure status; the first one wins (an invalid density makes the
+// diagonal and then the recurrences NaN too, and the user needs the cause).
+__device__ __forceinline__ void cg_fail(CgScalars *S, int code) {
+  atomicCAS(reinterpret_cast<int *>(&S->status), 0, code);
+}
+
 __device__ __forceinline__ bool cg_stopped(const CgScalars *S) {
   return *((volatile const int32_t *)&S->done) | *((volatile const int32_t *)&S->done_next);
 }

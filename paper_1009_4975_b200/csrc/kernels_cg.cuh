@@ -24,7 +24,7 @@ __device__ __forceinline__ void cg_init_scalars(CgScalars *S, double rho, double
   if (!S->fixed && rr <= S->thresh2) S->done = 1;
   if (S->max_iter <= 0) S->done = 1;
   if (!(rho == rho) || !(rr == rr)) {
-    S->status = -5;
+    cg_fail(S, -5);
     S->done = 1;
   }
 }
@@ -34,7 +34,7 @@ __device__ __forceinline__ void cg_after_rupdate(CgScalars *S, double rz, double
   const int it = S->iter + 1;
   S->iter = it;
   if (!(rz == rz) || !(rr == rr)) {
-    S->status = -5;
+    cg_fail(S, -5);
     S->done = 1;
     return;
   }
@@ -68,7 +68,7 @@ __device__ __forceinline__ void cg_single_step(CgScalars *S, int k, const double
   S->rho = rho;
   S->rr = rr;
   if (!(rho == rho) || !(rr == rr) || !(pq == pq) || !(qz == qz) || !(qdq == qdq)) {
-    S->status = -5;
+    cg_fail(S, -5);
     S->done = 1;
     return;
   }
@@ -78,7 +78,7 @@ __device__ __forceinline__ void cg_single_step(CgScalars *S, int k, const double
     return;
   }
   if (!(pq > 0.0)) {
-    S->status = -6;
+    cg_fail(S, -6);
     S->done = 1;
     return;
   }
@@ -97,7 +97,7 @@ __device__ __forceinline__ void cg_final_step(CgScalars *S, int n_iter, double r
   S->iter = n_iter;
   S->rho = rho;
   S->rr = rr;
-  if (!(rho == rho) || !(rr == rr)) S->status = -5;
+  if (!(rho == rho) || !(rr == rr)) cg_fail(S, -5);
   if (S->history && hist && n_iter >= 1) hist[n_iter - 1] = sqrt(rr / S->bnorm2);
   S->done = 1;
 }

@@ -38,7 +38,7 @@ __global__ void k_simp(int64_t n, const double *__restrict__ x, const int8_t *__
                        double *__restrict__ s, CgScalars *S) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     double xe = x[e];
-    if (!(xe > 0.0) || !(xe <= 1.0)) S->status = -1;  // TO_EINVAL
+    if (!(xe > 0.0) || !(xe <= 1.0)) cg_fail(S, -1);  // TO_EINVAL
     double v = Emin + pow(xe, penal) * (E0 - Emin);
     if (DIM == 3) v *= hL * (double)(1 << (L - lev[e]));
     s[e] = v;
@@ -97,7 +97,7 @@ __global__ void k_dinv(int64_t ndof, const uint8_t *__restrict__ free_dof, const
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ndof; i += (int64_t)gridDim.x * blockDim.x) {
     double d = D[i];
     if (free_dof[i]) {
-      if (!(d > 0.0)) S->status = -7;  // TO_ENONPOS_DIAG
+      if (!(d > 0.0)) cg_fail(S, -7);  // TO_ENONPOS_DIAG
       if (Dinv) Dinv[i] = 1.0 / d;
       if (d_out) d_out[i] = d;
     } else {
@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(256, 3) k_elem_pass(MeshView M, const double *
     double v[1] = {pq};
     if (grid_sum<1>(v, partials, &S->counter[CNT_PQ])) {
       if (!(v[0] > 0.0)) {
-        S->status = (v[0] != v[0]) ? -5 : -6;
+        cg_fail(S, (v[0] != v[0]) ? -5 : -6);
         S->done = 1;
       } else {
         S->alpha = S->rho / v[0];
@@ -679,7 +679,7 @@ __global__ void __launch_bounds__(256) k_elem_pass_lanes(MeshView M, const doubl
     double v[1] = {pq};
     if (grid_sum<1>(v, partials, &S->counter[CNT_PQ])) {
       if (!(v[0] > 0.0)) {
-        S->status = (v[0] != v[0]) ? -5 : -6;
+        cg_fail(S, (v[0] != v[0]) ? -5 : -6);
         S->done = 1;
       } else {
         S->alpha = S->rho / v[0];

@@ -530,7 +530,7 @@ __global__ void k_simp_s3(int64_t n, const double *__restrict__ x, const int32_t
                           CgScalars *S) {
   GRID_STRIDE(e, n) {
     double xe = x[e];
-    if (!(xe > 0.0) || !(xe <= 1.0)) S->status = -1;
+    if (!(xe > 0.0) || !(xe <= 1.0)) cg_fail(S, -1);
     s_lex[perm_el[e]] = (Emin + pow(xe, penal) * (E0 - Emin)) * h;
   }
 }
@@ -556,7 +556,7 @@ __global__ void k_diag_s3(GridView G, const double *__restrict__ s_lex, const ui
     const double d = k0d * acc;
     const int64_t node = s3_nrow(G, j, k) + i;
     const bool fr = free_node[node] != 0;
-    if (fr && !(d > 0.0)) S->status = -7;
+    if (fr && !(d > 0.0)) cg_fail(S, -7);
     if (dn) dn[node] = fr ? 1.0 / d : 0.0;
     if (d_out) {
       const int64_t base = s3_row(G, j, k) + 3 * i;

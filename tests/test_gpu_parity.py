@@ -144,3 +144,28 @@ def test_zero_load_gives_zero_solution():
     u = torch.full((hm.n_dof,), 3.0, dtype=torch.float64, device="cuda")
     st = m.tosolve_cg(3.0, x, u, rtol=1e-10, max_iter=100)
     assert st.iters == 0 and torch.count_nonzero(u) == 0
+
+
+@pytest.mark.parametrize("name", ["c2", "c5s"])
+def test_solver_edge_cases(name):
+    """Status codes of include/tomesh.h on both paths: densities outside (0, 1]
+    (incl. NaN) -> TO_EINVAL; max_iter = 0 -> no iteration, TO_NOT_CONVERGED, u
+    = 0; a too small iteration cap -> TO_NOT_CONVERGED with a usable iterate
+    whose recurrence residual matches the true one."""
+    import paper_1009_4975_b200 as pb
+    from paper_1009_4975_b200._lib import TomeshError
+    prob, om, hm, m, x_dev = _setup(name)
+    u = torch.zeros(om.n_dof, dtype=torch.float64, device="cuda")
+    for bad in (0.0, -0.5, 1.5, float("nan")):
+        xb = x_dev.clone()
+        xb[om.n_el // 2] = bad
+        with pytest.raises(TomeshError) as ei:
+            m.tosolve_cg(prob.penal, xb, u, rtol=1e-8, max_iter=100)
+        assert ei.value.code == pb.TO_EINVAL
+    st = m.tosolve_cg(prob.penal, x_dev, u, rtol=1e-10, max_iter=0)
+    assert st.iters == 0 and st.status == pb.TO_NOT_CONVERGED and torch.count_nonzero(u) == 0
+    assert abs(st.relres - 1.0) < 1e-12                 # r0 = b
+    st = m.tosolve_cg(prob.penal, x_dev, u, rtol=1e-12, max_iter=7)
+    assert st.iters == 7 and st.status == pb.TO_NOT_CONVERGED
+    assert np.isfinite(host(u)).all()
+    assert abs(st.relres_true - st.relres) <= 1e-6 * st.relres
