@@ -126,7 +126,10 @@ typedef struct {
   int64_t grid[3];             /* element grid when structured                   */
   int64_t device_bytes;        /* device memory held by the handle               */
   int32_t kernel_launches;     /* kernels launched by the last tosolve_cg        */
-  int32_t matvec_variant;      /* id of the operator kernel in use               */
+  int32_t matvec_variant;      /* operator path: 1 structured H8, 2 general
+                                  (launched passes), 3 general persistent       */
+  int64_t launches_total;      /* kernels launched by every call on this handle
+                                  since upload (monotone counter)               */
 } to_mesh_info;
 
 /* Validate, copy to `device`, derive device encodings, allocate the CG

@@ -44,7 +44,8 @@ class ToMeshInfo(C.Structure):
     _fields_ = [("dim", C.c_int32), ("structured", C.c_int32),
                 ("n_elem", C.c_int64), ("n_node", C.c_int64), ("n_dof", C.c_int64), ("n_hang", C.c_int64),
                 ("n_fixed", C.c_int64), ("filt_nnz", C.c_int64), ("grid", C.c_int64 * 3),
-                ("device_bytes", C.c_int64), ("kernel_launches", C.c_int32), ("matvec_variant", C.c_int32)]
+                ("device_bytes", C.c_int64), ("kernel_launches", C.c_int32), ("matvec_variant", C.c_int32),
+                ("launches_total", C.c_int64)]
 
 
 class HostSpec(C.Structure):

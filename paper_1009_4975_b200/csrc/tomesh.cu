@@ -90,6 +90,7 @@ struct to_mesh {
   CUtensorMap tm_x, tm_rb[2], tm_qb[2], tm_pb[2], tm_dn;
   int last_launches = 0;
   int matvec_variant = 0;
+  int64_t launches_total = 0;          // every kernel launched on this handle
   std::vector<cudaEvent_t> prof_ev;   // TO_PROFILE: 5 events per iteration
   double prof_ms[5] = {0, 0, 0, 0, 0};
 
@@ -879,6 +880,16 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   return rc;
 }
 
+// Adds the kernels an operator-level entry point launched (via last_launches)
+// to the handle's monotone counter, on every return path.
+struct LaunchCounter {
+  to_mesh *m;
+  int l0;
+  ~LaunchCounter() {
+    if (m) m->launches_total += m->last_launches - l0;
+  }
+};
+
 }  // namespace
 
 // ======================================================================================
@@ -926,7 +937,8 @@ extern "C" int tomesh_get_info(const to_mesh *m, to_mesh_info *info) {
   info->filt_nnz = m->filt_nnz;
   info->device_bytes = m->dev_bytes;
   info->kernel_launches = m->last_launches;
-  info->matvec_variant = m->matvec_variant;
+  info->matvec_variant = m->structured ? 1 : (m->coop_blocks > 0 ? 3 : 2);
+  info->launches_total = m->launches_total;
   return 0;
 }
 
@@ -939,7 +951,9 @@ extern "C" int tosolve_cg(to_mesh *m, double penal, const double *x_dev, double 
     return TO_EINVAL;
   }
   if (cudaSetDevice(m->device) != cudaSuccess) { set_error("cudaSetDevice failed"); return TO_ECUDA; }
-  return solve(m, penal, x_dev, u_dev, rtol, max_iter, flags, st, (cudaStream_t)cuda_stream);
+  const int rc = solve(m, penal, x_dev, u_dev, rtol, max_iter, flags, st, (cudaStream_t)cuda_stream);
+  m->launches_total += m->last_launches;
+  return rc;
 }
 
 extern "C" int tosolve_history(const to_mesh *m, double *out, int32_t n) {
@@ -966,8 +980,10 @@ extern "C" int to_sensitivity(to_mesh *m, double penal, const double *x_dev, con
   int g = grid_for(m->n_el);
   if (m->dim == 2) k_sens<2><<<g, kBlock, 0, st>>>(m->view(), x_dev, u_dev, penal, m->E0, m->Emin, dc_dev, m->K2);
   else k_sens_had3<<<g, kBlock, 0, st>>>(m->view(), x_dev, u_dev, penal, m->E0, m->Emin, dc_dev, m->KS);
+  m->launches_total++;
   RC(check_launch());
   if (compliance_host) {
+    m->launches_total++;
     k_dot<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->load, u_dev, m->partials, m->S, 1);
     RC(check_launch());
     CK(cudaMemcpyAsync(m->S_host, m->S, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
@@ -992,8 +1008,10 @@ extern "C" int to_filter(to_mesh *m, int32_t mode, const double *x_dev, const do
   if (m->structured) {
     k_filter_s3_scatter<<<g, kBlock, 0, st>>>(m->n_el, m->perm_el, mode, x_dev, in_dev, m->ftmp);
     k_filter_s3<<<g, kBlock, 0, st>>>(m->G, m->n_el, m->perm_el, m->foffs, m->n_foffs, mode, x_dev, m->ftmp, out_dev);
+    m->launches_total += 2;
     return check_launch();
   }
+  m->launches_total++;
   if (m->dim == 2) k_filter<2><<<g, kBlock, 0, st>>>(m->view(), m->filt_ptr, m->filt_idx, m->rmin, mode, x_dev, in_dev, out_dev);
   else k_filter<3><<<g, kBlock, 0, st>>>(m->view(), m->filt_ptr, m->filt_idx, m->rmin, mode, x_dev, in_dev, out_dev);
   return check_launch();
@@ -1001,6 +1019,7 @@ extern "C" int to_filter(to_mesh *m, int32_t mode, const double *x_dev, const do
 
 extern "C" int to_apply_A(to_mesh *m, double penal, const double *x_dev, const double *v_dev, double *q_dev,
                           void *cuda_stream) {
+  LaunchCounter lc_{m, m ? m->last_launches : 0};
   clear_error();
   if (!m || !x_dev || !v_dev || !q_dev || q_dev == v_dev) { set_error("bad argument"); return TO_EINVAL; }
   cudaStream_t st = (cudaStream_t)cuda_stream;
@@ -1009,6 +1028,7 @@ extern "C" int to_apply_A(to_mesh *m, double penal, const double *x_dev, const d
   int gv = grid_for(m->n_dof);
   if (!m->structured) {
     k_mask_free<<<gv, kBlock, 0, st>>>(m->n_dof, m->free_dof, v_dev, m->pb[0]);
+    m->last_launches++;
     RC(op_apply(m, m->pb[0], q_dev, st));
   } else {
     RC(op_masked_in(m, v_dev, m->pb[0], st));        // Pi_F v, internal order
@@ -1016,10 +1036,12 @@ extern "C" int to_apply_A(to_mesh *m, double penal, const double *x_dev, const d
     RC(op_recover_out(m, m->q, q_dev, st));          // back to canonical order
   }
   k_fix_nonfree<<<gv, kBlock, 0, st>>>(m->n_dof, m->free_dof, v_dev, q_dev);
+  m->last_launches++;
   return check_launch();
 }
 
 extern "C" int to_jacobi_diag(to_mesh *m, double penal, const double *x_dev, double *d_dev, void *cuda_stream) {
+  LaunchCounter lc_{m, m ? m->last_launches : 0};
   clear_error();
   if (!m || !x_dev || !d_dev) { set_error("NULL argument"); return TO_EINVAL; }
   cudaStream_t st = (cudaStream_t)cuda_stream;
@@ -1030,12 +1052,14 @@ extern "C" int to_jacobi_diag(to_mesh *m, double penal, const double *x_dev, dou
 }
 
 extern "C" int to_project_rhs(to_mesh *m, double *b_dev, void *cuda_stream) {
+  LaunchCounter lc_{m, m ? m->last_launches : 0};
   clear_error();
   if (!m || !b_dev) { set_error("NULL argument"); return TO_EINVAL; }
   return launch_rhs(m, b_dev, (cudaStream_t)cuda_stream);
 }
 
 extern "C" int to_recover(to_mesh *m, const double *v_dev, double *u_dev, void *cuda_stream) {
+  LaunchCounter lc_{m, m ? m->last_launches : 0};
   clear_error();
   if (!m || !v_dev || !u_dev) { set_error("NULL argument"); return TO_EINVAL; }
   return launch_recover(m, v_dev, u_dev, (cudaStream_t)cuda_stream);
