@@ -22,6 +22,9 @@ solve    textbook Jacobi-PCG (PAPER.md:511-523 rescaling reading), CG on the
          explicitly rescaled system, dense direct solve.
 topopt   sensitivities, Sigmund/Stainko filter
          (Eqs. 3-5) and the DENS variant, brute-force twins.
+oc       OC design update with the bisection on the volume multiplier
+         (reading R18) and the Fig. 1 loop with
+         p-continuation (reading R19).
 sample   one-by-one evaluation of rows of A, sensitivities and filter outputs
          for full-size configurations (parity on sampled outputs).
 
