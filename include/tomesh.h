@@ -23,6 +23,11 @@
  *   to_filter       Eq. 5 (:613-616), Stainko's volume-weighted Sigmund
  *                   filter, with H_de of Eq. 4; or its density variant
  *                   (reading R10).
+ *   to_oc_update    the design update of the Fig. 1 loop (:350-354 §3, "we
+ *                   use Optimality Criteria (OC)"; formula not printed, read
+ *                   as Bendsoe's heuristic OC step, reading R18)
+ *                   with the volume constraint of Eq. 1 (:296-304) met by a
+ *                   bisection on its multiplier, entirely on the device.
  *   to_apply_A / to_jacobi_diag / to_project_rhs / to_recover
  *                   the individual operators of Eqs. 7-9, exposed for
  *                   operator-level parity checks.
@@ -177,6 +182,65 @@ int  to_sensitivity(to_mesh *m, double penal, const double *x_dev, const double 
  * out_dev must not alias in_dev or x_dev.  Asynchronous. */
 int  to_filter(to_mesh *m, int32_t mode, const double *x_dev, const double *in_dev,
                double *out_dev, void *cuda_stream);
+
+/* OC design update (reading R18), element-wise with V_e = (2^(L-l_e) h_L)^dim:
+ *   x_new_e(lam) = min(min(1, x_e + move), max(max(rho_o, x_e - move),
+ *                      x_e (max(-dc_e, 0) / (lam V_e))^eta))
+ * with lam >= 0 such that sum_e V_e x_new_e = volfrac sum_e V_e: lam = 0 when
+ * even the lam -> 0+ limit stays within the budget ("inactive"); else the
+ * bracket [0, 1e9] (upper end widened x1e3 while still too much volume, up
+ * to 1e300; if that never suffices: "infeasible", lam = the last upper end)
+ * is bisected until l2 - l1 <= 1e-12 (l1 + l2) or 200 bisections.
+ *   x_dev, dc_dev  [n_elem] densities (in [rho_o, 1]) and filtered
+ *                  sensitivities (<= 0; positive values act as 0)
+ *   volfrac        V0 in (0, 1]; move >= 0; eta > 0; rho_o in (0, 1)
+ *   x_new_dev      [n_elem] output; may alias x_dev, must not alias dc_dev
+ *   st             nullable; filled after synchronising cuda_stream
+ * Returns TO_EINVAL for bad arguments, TO_ENAN if x or dc holds NaN/Inf. */
+typedef struct {
+  double  lambda;              /* volume multiplier (0 when inactive)            */
+  double  volume;              /* sum V x_new / sum V                            */
+  double  change;              /* max |x_new - x| (Condition 1)*/
+  double  ms;                  /* device time of the call (CUDA events)          */
+  int32_t steps;               /* bracket widenings + bisections                 */
+  int32_t state;               /* 0 active, 1 inactive, 2 infeasible             */
+  int32_t passes;              /* passes over the elements (grid-wide sums)      */
+} to_oc_stats;
+int  to_oc_update(to_mesh *m, const double *x_dev, const double *dc_dev, double volfrac,
+                  double move, double eta, double rho_o, double *x_new_dev,
+                  to_oc_stats *st, void *cuda_stream);
+
+/* The Fig. 1 optimization loop on the uploaded (fixed) mesh:
+ * per step  tosolve_cg (warm-started from the previous u, :541-543) ->
+ * to_sensitivity (+ compliance) -> to_filter SENS (Eq. 5, if filter and
+ * rmin > 0) -> to_oc_update written in place into x_dev.  p-continuation
+ * (:331-333, reading R19): p starts at penal0 and rises by
+ * penal_step (capped at penal_max) after a step whose design change is
+ * < change_tol (Condition 1, :431-434) or after stage_steps steps at the
+ * current p.  With stop_on_converge the loop ends after the first step at
+ * p = penal_max with change < change_tol.  Mesh adaptation (Fig. 1's
+ * refine/derefine branch) is not part of this call.
+ *   x_dev      [n_elem] in: initial design; out: the final design
+ *   u_dev      [dim*n_node] out: displacement of the last solve
+ *   hist       nullable [n_steps] per-step record; *steps_done = steps run
+ * Synchronises cuda_stream every step.  Returns the first failing status of
+ * a step (< 0), TO_NOT_CONVERGED if some solve hit max_iter, else TO_OK. */
+typedef struct {
+  double  volfrac, move, eta, rho_o;        /* to_oc_update (reading R18)        */
+  double  penal0, penal_max, penal_step;    /* continuation (reading R19)        */
+  int32_t stage_steps, stop_on_converge;
+  double  change_tol;                       /* Condition 1 (0.01)                */
+  double  rtol;                             /* per solve                         */
+  int32_t max_iter, filter;                 /* filter = 1: Eq. 5 on dc           */
+} to_opt_params;
+typedef struct {
+  double  compliance;          /* f^T u at the design entering the step          */
+  double  penal, volume, change, lambda;
+  double  solve_ms, oc_ms;     /* device times (CUDA events)                     */
+  int32_t cg_iters, status;    /* solve iterations and status                    */
+} to_opt_step;
+int  to_optimize(to_mesh *m, const to_opt_params *params, int32_t n_steps, double *x_dev,
+                 double *u_dev, to_opt_step *hist, int32_t *steps_done, void *cuda_stream);
 
 /* Operator-level entry points (parity and diagnostics; asynchronous).
  * to_apply_A:      q = A v,  A = Pi_F C^T K(x) C Pi_F + (I - Pi_F)  (Eq. 8)

@@ -128,8 +128,10 @@ def solve_u(mesh: OracleMesh, x, penal, E0=1.0, Emin=1e-9, nu=0.3):
 
 
 def optimize(mesh: OracleMesh, x0, volfrac, n_steps, rmin, penal0=1.0, penal_max=3.0, penal_step=0.5,
-             stage_steps=30, E0=1.0, Emin=1e-9, nu=0.3, move=MOVE, eta=ETA, rho_o=RHO_O):
-    """The Fig. 1 loop on a fixed mesh for n_steps design updates."""
+             stage_steps=30, E0=1.0, Emin=1e-9, nu=0.3, move=MOVE, eta=ETA, rho_o=RHO_O,
+             stop_on_converge=False, change_tol=0.01):
+    """The Fig. 1 loop on a fixed mesh for n_steps design updates (or until
+    converged at penal_max when stop_on_converge)."""
     x = np.asarray(x0, dtype=np.float64).copy()
     V = mesh.volumes()
     H = LoopHistory()
@@ -148,6 +150,8 @@ def optimize(mesh: OracleMesh, x0, volfrac, n_steps, rmin, penal0=1.0, penal_max
         H.lam.append(r.lam)
         x = r.x
         at_stage += 1
-        if penal < penal_max and (converged(r.change) or at_stage >= stage_steps):
+        if stop_on_converge and penal >= penal_max and converged(r.change, change_tol):
+            break
+        if penal < penal_max and (converged(r.change, change_tol) or at_stage >= stage_steps):
             penal, at_stage = min(penal_max, penal + penal_step), 0
     return x, H

@@ -48,6 +48,24 @@ class ToMeshInfo(C.Structure):
                 ("launches_total", C.c_int64)]
 
 
+class ToOcStats(C.Structure):
+    _fields_ = [("lambda_", C.c_double), ("volume", C.c_double), ("change", C.c_double), ("ms", C.c_double),
+                ("steps", C.c_int32), ("state", C.c_int32), ("passes", C.c_int32)]
+
+
+class ToOptParams(C.Structure):
+    _fields_ = [("volfrac", C.c_double), ("move", C.c_double), ("eta", C.c_double), ("rho_o", C.c_double),
+                ("penal0", C.c_double), ("penal_max", C.c_double), ("penal_step", C.c_double),
+                ("stage_steps", C.c_int32), ("stop_on_converge", C.c_int32), ("change_tol", C.c_double),
+                ("rtol", C.c_double), ("max_iter", C.c_int32), ("filter", C.c_int32)]
+
+
+class ToOptStep(C.Structure):
+    _fields_ = [("compliance", C.c_double), ("penal", C.c_double), ("volume", C.c_double),
+                ("change", C.c_double), ("lambda_", C.c_double), ("solve_ms", C.c_double), ("oc_ms", C.c_double),
+                ("cg_iters", C.c_int32), ("status", C.c_int32)]
+
+
 class HostSpec(C.Structure):
     _fields_ = [
         ("dim", C.c_int32), ("max_level", C.c_int32), ("base", C.c_int32 * 3), ("h0", C.c_double),
@@ -79,6 +97,10 @@ EXPORTS = {
     "tosolve_profile": (C.c_int, [P, P, C.c_int32]),
     "to_sensitivity": (C.c_int, [P, C.c_double, P, P, P, C.POINTER(C.c_double), P]),
     "to_filter": (C.c_int, [P, C.c_int32, P, P, P, P]),
+    "to_oc_update": (C.c_int, [P, P, P, C.c_double, C.c_double, C.c_double, C.c_double, P,
+                               C.POINTER(ToOcStats), P]),
+    "to_optimize": (C.c_int, [P, C.POINTER(ToOptParams), C.c_int32, P, P, C.POINTER(ToOptStep),
+                              C.POINTER(C.c_int32), P]),
     "to_apply_A": (C.c_int, [P, C.c_double, P, P, P, P]),
     "to_jacobi_diag": (C.c_int, [P, C.c_double, P, P, P]),
     "to_project_rhs": (C.c_int, [P, P, P]),

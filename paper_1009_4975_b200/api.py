@@ -145,6 +145,17 @@ class CgStats:
     bnorm: float
 
 
+@dataclass
+class OcStats:
+    lam: float
+    volume: float
+    change: float
+    ms: float
+    steps: int
+    state: int          # 0 active, 1 inactive, 2 infeasible
+    passes: int         # passes over the elements
+
+
 def _dptr(t):
     import torch
     if t is None:
@@ -257,6 +268,31 @@ class Mesh:
         L.check(L.lib().to_filter(self._h, int(mode), _dptr(x), _dptr(inp), _dptr(out), _stream(stream)),
                 "to_filter")
         return out
+
+    # -- the design update and the Fig. 1 loop ----------------------------------------------
+    def to_oc_update(self, x, dc, volfrac, x_new, move=0.2, eta=0.5, rho_o=1e-3, stream=None) -> OcStats:
+        st = L.ToOcStats()
+        L.check(L.lib().to_oc_update(self._h, _dptr(x), _dptr(dc), float(volfrac), float(move), float(eta),
+                                     float(rho_o), _dptr(x_new), C.byref(st), _stream(stream)), "to_oc_update")
+        return OcStats(st.lambda_, st.volume, st.change, st.ms, st.steps, st.state, st.passes)
+
+    def to_optimize(self, x, u, n_steps, volfrac, penal0=1.0, penal_max=3.0, penal_step=0.5, stage_steps=30,
+                    stop_on_converge=False, change_tol=0.01, move=0.2, eta=0.5, rho_o=1e-3, rtol=1e-10,
+                    max_iter=20000, filter=True, stream=None):
+        """Runs the Fig. 1 loop in the library; x is updated in place.  Returns
+        (status, list of per-step dicts)."""
+        P = L.ToOptParams(volfrac=volfrac, move=move, eta=eta, rho_o=rho_o, penal0=penal0, penal_max=penal_max,
+                          penal_step=penal_step, stage_steps=stage_steps, stop_on_converge=int(stop_on_converge),
+                          change_tol=change_tol, rtol=rtol, max_iter=max_iter, filter=int(filter))
+        hist = (L.ToOptStep * max(1, n_steps))()
+        done = C.c_int32(0)
+        rc = L.lib().to_optimize(self._h, C.byref(P), int(n_steps), _dptr(x), _dptr(u), hist, C.byref(done),
+                                 _stream(stream))
+        L.check(rc, "to_optimize")
+        out = [{f: getattr(hist[k], f) for f, _ in L.ToOptStep._fields_} for k in range(done.value)]
+        for h in out:
+            h["lam"] = h.pop("lambda_")
+        return rc, out
 
     # -- operator-level calls -------------------------------------------------------------
     def to_apply_A(self, penal, x, v, q, stream=None):

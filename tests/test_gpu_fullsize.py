@@ -4,12 +4,10 @@ cannot assemble these systems quickly, so it evaluates the operator element
 by element (oracle/sample.py), sensitivities and filter outputs on sampled
 elements, and the residual certificate of the device's own solution.
 
-Tolerances: operator, compliance and filter from identical inputs 1e-12
-relative (fp64 rounding of sums of <= a few hundred terms); sensitivities
-1e-10: u_e^T K0 u_e is a quadratic form whose value is 1e2-1e4 times smaller
-than sum |u_a K0_ab u_b| when u_e is dominated by rigid-body motion (K0's
-null space), so the rounding of the two evaluation orders is amplified by
-that cancellation ratio;
+Tolerances: operator, compliance and filter from identical seeded inputs
+1e-12 relative (fp64 rounding of sums of <= a few hundred terms);
+sensitivities of a seeded u 1e-11 (a quadratic form of 24 terms per element);
+OC update as in test_gpu_oc.py (lam 1e-10, x_new 1e-11);
 converged solves: the oracle's ||b - A u_dev|| / ||b|| <= 10 rtol (SURVEY
 §8(c) L3); the fixed-500-iteration c5 solve (not converged, so compared by
 properties): the device's reported true residual equals the oracle's to
@@ -22,7 +20,7 @@ import pytest
 torch = pytest.importorskip("torch")
 
 from inputs import config
-from oracle import fe, mesh as omesh, pipeline, sample, topopt
+from oracle import fe, mesh as omesh, oc, pipeline, sample, topopt
 from tests.gpu_helpers import cuda, host, product_mesh, rel
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
@@ -89,16 +87,27 @@ def test_fullsize_solve_sensitivities_filter(name):
         assert st.status == 0 and st.relres <= 1e-10
         cert = sample.residual_norm(om, x, host(u), prob.penal, prob.E0, prob.Emin, prob.nu)
         assert cert <= 10 * 1e-10
-    ud = host(u)
-    dc = torch.empty(om.n_el, dtype=torch.float64, device="cuda")
-    c = m.to_sensitivity(prob.penal, xd, u, dc, compliance=True)
-    assert abs(c - fe.compliance(om.load, ud)) <= 1e-12 * abs(c)
+    # sensitivities, compliance, filter and OC update on seeded inputs (never
+    # device outputs) at the full size, in the bench's handle configuration
     rng = np.random.default_rng(13)
+    us = rng.standard_normal(om.n_dof)
+    dc = torch.empty(om.n_el, dtype=torch.float64, device="cuda")
+    c = m.to_sensitivity(prob.penal, xd, cuda(us), dc, compliance=True)
+    assert abs(c - fe.compliance(om.load, us)) <= 1e-12 * abs(c)
     els = rng.choice(om.n_el, size=2000, replace=False)
-    dco = topopt.sensitivities(om, x, ud, prob.penal, prob.E0, prob.Emin, prob.nu, elems=els)
-    assert rel(host(dc)[els], dco) <= 1e-10
+    dco = topopt.sensitivities(om, x, us, prob.penal, prob.E0, prob.Emin, prob.nu, elems=els)
+    assert rel(host(dc)[els], dco) <= 1e-11
+    V = om.volumes()
+    dcs = -np.exp(rng.uniform(-6, 2, om.n_el)) * V
     out = torch.empty_like(dc)
-    m.to_filter(0, xd, dc, out)
+    m.to_filter(0, xd, cuda(dcs), out)
     fe_ = els[:100]
-    ref = sample.filter_rows(om, prob.rmin, x, host(dc), fe_, mode="sens")
+    ref = sample.filter_rows(om, prob.rmin, x, dcs, fe_, mode="sens")
     assert rel(host(out)[fe_], ref) <= 1e-12
+    vf = float(np.sum(V * x) / V.sum()) - 0.05          # a budget just below the current volume
+    r = oc.oc_update(x, dcs, V, vf)
+    st = m.to_oc_update(xd, cuda(dcs), vf, out)
+    assert st.state == 0 and r.status == "active"
+    assert abs(st.lam - r.lam) <= 1e-10 * r.lam and abs(st.steps - r.steps) <= 2
+    np.testing.assert_allclose(host(out), r.x, rtol=1e-11, atol=1e-15)
+    assert abs(st.volume - vf) <= 1e-10 and abs(st.change - r.change) <= 1e-11

@@ -46,13 +46,14 @@ def test_struct_layouts_match_header(tmp_path):
         pytest.skip("no g++")
     structs = {"to_mesh_desc": _lib.ToMeshDesc, "to_cg_stats": _lib.ToCgStats,
                "to_mesh_info": _lib.ToMeshInfo, "tomesh_host_spec": _lib.HostSpec,
-               "tomesh_host_arrays": _lib.HostArrays}
+               "tomesh_host_arrays": _lib.HostArrays, "to_oc_stats": _lib.ToOcStats,
+               "to_opt_params": _lib.ToOptParams, "to_opt_step": _lib.ToOptStep}
     lines = ['#include <cstdio>', '#include <cstddef>', '#include "tomesh.h"', '#include "tomesh_host.h"',
              "int main(){"]
     for cname, cls in structs.items():
         lines.append(f'printf("{cname} sizeof %zu\\n", sizeof({cname}));')
         for f, _ in cls._fields_:
-            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f.rstrip("_")}));')
     lines.append("return 0;}")
     src = tmp_path / "abi.cpp"
     src.write_text("\n".join(lines))
