@@ -25,6 +25,9 @@ topopt   sensitivities, Sigmund/Stainko filter
 oc       OC design update with the bisection on the volume multiplier
          (reading R18) and the Fig. 1 loop with
          p-continuation (reading R19).
+amr      the dynamic AMR strategy: adaptation trigger,
+         marking with r_amr, the two compatibility sweeps, refine/derefine
+         with density transfer (readings R21-R23), and Fig. 1 with AMR.
 sample   one-by-one evaluation of rows of A, sensitivities and filter outputs
          for full-size configurations (parity on sampled outputs).
 
