@@ -28,6 +28,9 @@
  *                   as Bendsoe's heuristic OC step, reading R18)
  *                   with the volume constraint of Eq. 1 (:296-304) met by a
  *                   bisection on its multiplier, entirely on the device.
+ *   to_amr_mark     the refinement/derefinement marks of the dynamic AMR
+ *                   strategy (:458-463 §4); the mesh update itself is host
+ *                   code (tomesh_host_adapt in tomesh_host.h).
  *   to_apply_A / to_jacobi_diag / to_project_rhs / to_recover
  *                   the individual operators of Eqs. 7-9, exposed for
  *                   operator-level parity checks.
@@ -210,6 +213,18 @@ int  to_oc_update(to_mesh *m, const double *x_dev, const double *dc_dev, double 
                   double move, double eta, double rho_o, double *x_new_dev,
                   to_oc_stats *st, void *cuda_stream);
 
+/* Dynamic AMR marking (§4, reading R21), one
+ * int8 per element into marks_dev (device memory, [n_elem]):
+ *   +1  a solid element (x_d >= rho_s) lies within r_amr of e (centre
+ *       distance < r_amr, e itself included) and e is below max_level;
+ *   -1  no solid element within r_amr and e is above level 0;
+ *    0  otherwise.
+ * r_amr is the handle's filter radius rmin ("we use rmin = r_amr",
+ * PAPER.md:606-607), evaluated on the same neighbour lists / stencil as
+ * to_filter; rmin = 0 means the element alone.  The marks feed
+ * tomesh_host_adapt (include/tomesh_host.h).  Asynchronous. */
+int  to_amr_mark(to_mesh *m, const double *x_dev, double rho_s, int8_t *marks_dev, void *cuda_stream);
+
 /* The Fig. 1 optimization loop on the uploaded (fixed) mesh:
  * per step  tosolve_cg (warm-started from the previous u, :541-543) ->
  * to_sensitivity (+ compliance) -> to_filter SENS (Eq. 5, if filter and
@@ -223,7 +238,10 @@ int  to_oc_update(to_mesh *m, const double *x_dev, const double *dc_dev, double 
  *   x_dev      [n_elem] in: initial design; out: the final design
  *   u_dev      [dim*n_node] out: displacement of the last solve
  *   hist       nullable [n_steps] per-step record; *steps_done = steps run
- * Synchronises cuda_stream every step.  Returns the first failing status of
+ *   state      nullable continuation / adaptation state carried across calls
+ *              (NULL: start at penal0 with fresh counters)
+ * The first solve of a call starts from zero (after an adaptation the mesh
+ * changed); later ones are warm-started.  Synchronises cuda_stream every step.  Returns the first failing status of
  * a step (< 0), TO_NOT_CONVERGED if some solve hit max_iter, else TO_OK. */
 typedef struct {
   double  volfrac, move, eta, rho_o;        /* to_oc_update (reading R18)        */
@@ -232,7 +250,19 @@ typedef struct {
   double  change_tol;                       /* Condition 1 (0.01)                */
   double  rtol;                             /* per solve                         */
   int32_t max_iter, filter;                 /* filter = 1: Eq. 5 on dc           */
+  int32_t adapt_min_steps, adapt_max_steps; /* > 0: stop after the step at which
+                                               the AMR trigger fires (PAPER.md:
+                                               421-446, reading R23): change <
+                                               change_tol and >= min steps since
+                                               the last adaptation, or >= max   */
 } to_opt_params;
+typedef struct {
+  double  penal;          /* in/out: current SIMP exponent                       */
+  int32_t at_stage;       /* in/out: steps taken at the current exponent         */
+  int32_t since_adapt;    /* in/out: steps since the last mesh adaptation        */
+  int32_t adapt_due;      /* out: 1 = stopped because the AMR trigger fired      */
+  int32_t converged;      /* out: 1 = stopped by stop_on_converge                */
+} to_opt_state;
 typedef struct {
   double  compliance;          /* f^T u at the design entering the step          */
   double  penal, volume, change, lambda;
@@ -240,7 +270,8 @@ typedef struct {
   int32_t cg_iters, status;    /* solve iterations and status                    */
 } to_opt_step;
 int  to_optimize(to_mesh *m, const to_opt_params *params, int32_t n_steps, double *x_dev,
-                 double *u_dev, to_opt_step *hist, int32_t *steps_done, void *cuda_stream);
+                 double *u_dev, to_opt_step *hist, int32_t *steps_done, to_opt_state *state,
+                 void *cuda_stream);
 
 /* Operator-level entry points (parity and diagnostics; asynchronous).
  * to_apply_A:      q = A v,  A = Pi_F C^T K(x) C Pi_F + (I - Pi_F)  (Eq. 8)

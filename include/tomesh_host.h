@@ -81,6 +81,37 @@ int  tomesh_host_get(const tomesh_host *h, tomesh_host_arrays *out);
 int  tomesh_host_filter(tomesh_host *h, double rmin);
 void tomesh_host_free(tomesh_host *h);
 
+/* Dynamic AMR mesh update (§4; readings R21-R23).
+ * tomesh_host_adapt takes per-element marks of the mesh h (+1 refine, -1
+ * derefine, 0 keep; from to_amr_mark) and the element densities x, applies
+ *   sweep 1: a derefinement survives only if all 2^dim siblings are leaves
+ *            marked -1 ("unmark ... if they have a sibling that is not marked");
+ *   sweep 2: a sibling group survives only if no leaf two or more levels finer
+ *            than the would-be parent touches it across a face/edge (3D) or an
+ *            edge (2D) in the 2:1 closure (C10) of this pass's refinements
+ *            ("level two or higher edge incompatibility");
+ * and returns the new pre-balance leaf set (ascending Morton order):
+ * refined leaves become their children with the parent's density; a
+ * derefined group becomes the parent with the children's mean density
+ * (summed in corner order).  Build the new mesh from it with
+ * tomesh_host_build (same boundary and load boxes), then
+ * tomesh_host_transfer gives every new (balanced) element the density of
+ * the pre-balance leaf containing it.  Marks beyond the level range
+ * (refine at max_level, derefine at level 0) are rejected (TO_EINVAL). */
+typedef struct tomesh_adapt tomesh_adapt;
+typedef struct {
+  int64_t n_leaf;
+  const int8_t  *leaf_level;   /* [n_leaf]                                         */
+  const int32_t *leaf_anchor;  /* [n_leaf][dim]                                    */
+  const double  *leaf_x;       /* [n_leaf] transferred densities                   */
+  const int8_t  *marks;        /* [n_elem of h] marks after the two sweeps         */
+  int64_t n_refined, n_groups, n_unmarked_sibling, n_unmarked_incompat;
+} tomesh_adapt_result;
+int  tomesh_host_adapt(const tomesh_host *h, const int8_t *marks, const double *x, tomesh_adapt **out);
+int  tomesh_adapt_get(const tomesh_adapt *a, tomesh_adapt_result *out);
+int  tomesh_host_transfer(const tomesh_host *h_new, const tomesh_adapt *a, double *x_out);
+void tomesh_adapt_free(tomesh_adapt *a);
+
 #ifdef __cplusplus
 }
 #endif

@@ -57,7 +57,19 @@ class ToOptParams(C.Structure):
     _fields_ = [("volfrac", C.c_double), ("move", C.c_double), ("eta", C.c_double), ("rho_o", C.c_double),
                 ("penal0", C.c_double), ("penal_max", C.c_double), ("penal_step", C.c_double),
                 ("stage_steps", C.c_int32), ("stop_on_converge", C.c_int32), ("change_tol", C.c_double),
-                ("rtol", C.c_double), ("max_iter", C.c_int32), ("filter", C.c_int32)]
+                ("rtol", C.c_double), ("max_iter", C.c_int32), ("filter", C.c_int32),
+                ("adapt_min_steps", C.c_int32), ("adapt_max_steps", C.c_int32)]
+
+
+class ToOptState(C.Structure):
+    _fields_ = [("penal", C.c_double), ("at_stage", C.c_int32), ("since_adapt", C.c_int32),
+                ("adapt_due", C.c_int32), ("converged", C.c_int32)]
+
+
+class AdaptResult(C.Structure):
+    _fields_ = [("n_leaf", C.c_int64), ("leaf_level", P), ("leaf_anchor", P), ("leaf_x", P), ("marks", P),
+                ("n_refined", C.c_int64), ("n_groups", C.c_int64), ("n_unmarked_sibling", C.c_int64),
+                ("n_unmarked_incompat", C.c_int64)]
 
 
 class ToOptStep(C.Structure):
@@ -100,7 +112,12 @@ EXPORTS = {
     "to_oc_update": (C.c_int, [P, P, P, C.c_double, C.c_double, C.c_double, C.c_double, P,
                                C.POINTER(ToOcStats), P]),
     "to_optimize": (C.c_int, [P, C.POINTER(ToOptParams), C.c_int32, P, P, C.POINTER(ToOptStep),
-                              C.POINTER(C.c_int32), P]),
+                              C.POINTER(C.c_int32), C.POINTER(ToOptState), P]),
+    "to_amr_mark": (C.c_int, [P, P, C.c_double, P, P]),
+    "tomesh_host_adapt": (C.c_int, [P, P, P, C.POINTER(P)]),
+    "tomesh_adapt_get": (C.c_int, [P, C.POINTER(AdaptResult)]),
+    "tomesh_host_transfer": (C.c_int, [P, P, P]),
+    "tomesh_adapt_free": (None, [P]),
     "to_apply_A": (C.c_int, [P, C.c_double, P, P, P, P]),
     "to_jacobi_diag": (C.c_int, [P, C.c_double, P, P, P]),
     "to_project_rhs": (C.c_int, [P, P, P]),

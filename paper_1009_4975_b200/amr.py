@@ -1,0 +1,70 @@
+"""Fig. 1 with dynamic AMR (PAPER.md:336-358 and §4 :360-492) on top of the
+C ABI: the design steps run in the library (`to_optimize`, every step a
+device solve, sensitivity, filter and OC update) until the adaptation
+trigger fires; then the marks are computed on the device (`to_amr_mark`),
+the mesh is updated by the C++ host code (`tomesh_host_adapt`, the
+compatibility sweeps and refine/derefine with density transfer), rebuilt
+(`tomesh_host_build`), the densities moved onto it (`tomesh_host_transfer`)
+and the new mesh uploaded.  This module only sequences those calls.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+from .api import Mesh, prepare, rebuild, tomesh_host_adapt, tomesh_host_transfer
+
+
+@dataclass
+class AmrRun:
+    host: object                       # final HostMesh
+    x: object                          # final densities (CUDA tensor, final mesh order)
+    steps: list = field(default_factory=list)         # per-step dicts (+ "n_elem", "adapted")
+    adaptations: list = field(default_factory=list)   # per adaptation: counts
+
+
+def optimize_amr(problem, volfrac, n_steps, penal0=1.0, penal_max=3.0, penal_step=0.5, stage_steps=30,
+                 rho_s=0.5, min_steps=5, max_steps=10, change_tol=0.01, rtol=1e-10, max_iter=20000,
+                 device=0, x0=None) -> AmrRun:
+    import torch
+    dev = torch.device("cuda", device)
+    host = prepare(problem, keep_handle=True)
+    mesh = Mesh(host, E0=problem.E0, Emin=problem.Emin, nu=problem.nu, rmin=problem.rmin, device=device)
+    x = torch.full((host.n_el,), float(volfrac), dtype=torch.float64, device=dev) if x0 is None else x0
+    state = L.ToOptState(penal=penal0, at_stage=0, since_adapt=0)
+    run = AmrRun(host, x)
+    done = 0
+    while done < n_steps:
+        u = torch.zeros(host.n_dof, dtype=torch.float64, device=dev)
+        _, hist = mesh.to_optimize(x, u, n_steps - done, volfrac, penal0=penal0, penal_max=penal_max,
+                                   penal_step=penal_step, stage_steps=stage_steps, change_tol=change_tol,
+                                   rtol=rtol, max_iter=max_iter, adapt_min_steps=min_steps,
+                                   adapt_max_steps=max_steps, state=state)
+        for h in hist:
+            h["n_elem"] = host.n_el
+            h["adapted"] = False
+        run.steps.extend(hist)
+        done += len(hist)
+        if not state.adapt_due:
+            break
+        marks = torch.empty(host.n_el, dtype=torch.int8, device=dev)
+        mesh.to_amr_mark(x, marks, rho_s)
+        ad = tomesh_host_adapt(host, marks.cpu().numpy(), x.cpu().numpy())
+        new_host = rebuild(problem, ad)
+        xn = tomesh_host_transfer(new_host, ad)
+        run.adaptations.append({"step": done, "n_elem_before": host.n_el, "n_elem_after": new_host.n_el,
+                                "n_refined": ad.n_refined, "n_groups": ad.n_groups,
+                                "n_unmarked_sibling": ad.n_unmarked_sibling,
+                                "n_unmarked_incompat": ad.n_unmarked_incompat})
+        run.steps[-1]["adapted"] = True
+        mesh.close()
+        host = new_host
+        mesh = Mesh(host, E0=problem.E0, Emin=problem.Emin, nu=problem.nu, rmin=problem.rmin, device=device)
+        x = torch.as_tensor(xn, device=dev)
+        state.since_adapt = 0
+        state.adapt_due = 0
+    mesh.close()
+    run.host, run.x = host, x
+    return run

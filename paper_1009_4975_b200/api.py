@@ -50,6 +50,7 @@ class HostMesh:
     filt_ptr: Optional[np.ndarray]
     filt_idx: Optional[np.ndarray]
     rmin: float
+    handle: Optional["_HostHandle"] = None   # the tomesh_host* (kept for tomesh_host_adapt)
 
     @property
     def n_el(self):
@@ -68,11 +69,27 @@ class HostMesh:
         return self.h0 / (1 << self.L)
 
 
+class _HostHandle:
+    """Owns a tomesh_host* (freed with the object)."""
+
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h and self.h.value:
+                L.lib().tomesh_host_free(self.h)
+        except Exception:
+            pass
+
+
 _KIND = {"point": L.TOH_LOAD_POINT, "line": L.TOH_LOAD_LINE, "face": L.TOH_LOAD_FACE}
 
 
-def tomesh_host_build(dim, max_level, base, h0, leaf_level, leaf_anchor, fixed, loads, rmin) -> HostMesh:
-    """fixed: [(lo, hi, mask)], loads: [(kind, lo, hi, vec)] (lattice boxes, inclusive)."""
+def tomesh_host_build(dim, max_level, base, h0, leaf_level, leaf_anchor, fixed, loads, rmin,
+                      keep_handle=False) -> HostMesh:
+    """fixed: [(lo, hi, mask)], loads: [(kind, lo, hi, vec)] (lattice boxes, inclusive).
+    keep_handle: keep the C mesh alive (needed by tomesh_host_adapt / _transfer)."""
     lib = L.lib()
     leaf_level = np.ascontiguousarray(leaf_level, dtype=np.int8)
     leaf_anchor = np.ascontiguousarray(leaf_anchor, dtype=np.int32).reshape(-1, dim)
@@ -100,35 +117,94 @@ def tomesh_host_build(dim, max_level, base, h0, leaf_level, leaf_anchor, fixed, 
     spec.rmin = float(rmin)
     h = C.c_void_p()
     L.check(lib.tomesh_host_build(C.byref(spec), C.byref(h)), "tomesh_host_build")
-    try:
-        a = L.HostArrays()
-        L.check(lib.tomesh_host_get(h, C.byref(a)), "tomesh_host_get")
-        nc = 1 << dim
-        ne, nn = a.n_elem, a.n_node
-        return HostMesh(
-            dim=dim, L=max_level, h0=h0,
-            elem_node=_copy(a.elem_node, np.int32, ne * nc, (ne, nc)),
-            elem_anchor=_copy(a.elem_anchor, np.int32, ne * dim, (ne, dim)),
-            elem_level=_copy(a.elem_level, np.int8, ne),
-            node_coord=_copy(a.node_coord, np.int32, nn * dim, (nn, dim)),
-            hang_node=_copy(a.hang_node, np.int32, a.n_hang),
-            hang_ptr=_copy(a.hang_ptr, np.int32, a.n_hang + 1),
-            hang_parent=_copy(a.hang_parent, np.int32, a.n_hang_nnz),
-            hang_weight=_copy(a.hang_weight, np.float64, a.n_hang_nnz),
-            fixed_dof=_copy(a.fixed_dof, np.int64, a.n_fixed),
-            load=_copy(a.load, np.float64, nn * dim),
-            filt_ptr=_copy(a.filt_ptr, np.int64, ne + 1) if a.filt_ptr else None,
-            filt_idx=_copy(a.filt_idx, np.int32, a.filt_nnz) if a.filt_ptr else None,
-            rmin=float(rmin),
-        )
-    finally:
-        lib.tomesh_host_free(h)
+    handle = _HostHandle(h)
+    a = L.HostArrays()
+    L.check(lib.tomesh_host_get(h, C.byref(a)), "tomesh_host_get")
+    nc = 1 << dim
+    ne, nn = a.n_elem, a.n_node
+    return HostMesh(
+        dim=dim, L=max_level, h0=h0,
+        elem_node=_copy(a.elem_node, np.int32, ne * nc, (ne, nc)),
+        elem_anchor=_copy(a.elem_anchor, np.int32, ne * dim, (ne, dim)),
+        elem_level=_copy(a.elem_level, np.int8, ne),
+        node_coord=_copy(a.node_coord, np.int32, nn * dim, (nn, dim)),
+        hang_node=_copy(a.hang_node, np.int32, a.n_hang),
+        hang_ptr=_copy(a.hang_ptr, np.int32, a.n_hang + 1),
+        hang_parent=_copy(a.hang_parent, np.int32, a.n_hang_nnz),
+        hang_weight=_copy(a.hang_weight, np.float64, a.n_hang_nnz),
+        fixed_dof=_copy(a.fixed_dof, np.int64, a.n_fixed),
+        load=_copy(a.load, np.float64, nn * dim),
+        filt_ptr=_copy(a.filt_ptr, np.int64, ne + 1) if a.filt_ptr else None,
+        filt_idx=_copy(a.filt_idx, np.int32, a.filt_nnz) if a.filt_ptr else None,
+        rmin=float(rmin),
+        handle=handle if keep_handle else None,
+    )
 
 
-def prepare(problem) -> HostMesh:
+def prepare(problem, keep_handle=False) -> HostMesh:
     """Host mesh for an ``inputs.Problem`` (its pre-balance leaves and predicates)."""
     p = problem
-    return tomesh_host_build(p.dim, p.L, p.base, p.h0, p.leaf_level, p.leaf_anchor, p.fixed, p.loads, p.rmin)
+    return tomesh_host_build(p.dim, p.L, p.base, p.h0, p.leaf_level, p.leaf_anchor, p.fixed, p.loads, p.rmin,
+                             keep_handle)
+
+
+@dataclass
+class Adaptation:
+    """Result of tomesh_host_adapt: the new pre-balance leaves (ascending Morton
+    order) with transferred densities, the marks after the two sweeps, counts."""
+    leaf_level: np.ndarray
+    leaf_anchor: np.ndarray
+    leaf_x: np.ndarray
+    marks: np.ndarray
+    n_refined: int
+    n_groups: int
+    n_unmarked_sibling: int
+    n_unmarked_incompat: int
+    handle: object = None
+
+
+class _AdaptHandle:
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h and self.h.value:
+                L.lib().tomesh_adapt_free(self.h)
+        except Exception:
+            pass
+
+
+def tomesh_host_adapt(host: HostMesh, marks, x) -> Adaptation:
+    """Sweeps + refine/derefine on the host (include/tomesh_host.h)."""
+    if host.handle is None:
+        raise ValueError("host mesh built without keep_handle=True")
+    marks = np.ascontiguousarray(marks, dtype=np.int8)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    if marks.shape[0] != host.n_el or x.shape[0] != host.n_el:
+        raise ValueError("marks and x need one value per element")
+    h = C.c_void_p()
+    L.check(L.lib().tomesh_host_adapt(host.handle.h, _ptr(marks), _ptr(x), C.byref(h)), "tomesh_host_adapt")
+    ah = _AdaptHandle(h)
+    r = L.AdaptResult()
+    L.check(L.lib().tomesh_adapt_get(h, C.byref(r)), "tomesh_adapt_get")
+    n, dim = r.n_leaf, host.dim
+    return Adaptation(_copy(r.leaf_level, np.int8, n), _copy(r.leaf_anchor, np.int32, n * dim, (n, dim)),
+                      _copy(r.leaf_x, np.float64, n), _copy(r.marks, np.int8, host.n_el),
+                      r.n_refined, r.n_groups, r.n_unmarked_sibling, r.n_unmarked_incompat, ah)
+
+
+def tomesh_host_transfer(host_new: HostMesh, ad: Adaptation) -> np.ndarray:
+    out = np.empty(host_new.n_el, dtype=np.float64)
+    L.check(L.lib().tomesh_host_transfer(host_new.handle.h, ad.handle.h, _ptr(out)), "tomesh_host_transfer")
+    return out
+
+
+def rebuild(problem, ad: Adaptation) -> HostMesh:
+    """Host mesh of the adapted leaf set with the problem's boundary boxes and loads."""
+    p = problem
+    return tomesh_host_build(p.dim, p.L, p.base, p.h0, ad.leaf_level, ad.leaf_anchor, p.fixed, p.loads, p.rmin,
+                             keep_handle=True)
 
 
 # ---------------------------------------------------------------------------
@@ -278,21 +354,32 @@ class Mesh:
 
     def to_optimize(self, x, u, n_steps, volfrac, penal0=1.0, penal_max=3.0, penal_step=0.5, stage_steps=30,
                     stop_on_converge=False, change_tol=0.01, move=0.2, eta=0.5, rho_o=1e-3, rtol=1e-10,
-                    max_iter=20000, filter=True, stream=None):
-        """Runs the Fig. 1 loop in the library; x is updated in place.  Returns
-        (status, list of per-step dicts)."""
+                    max_iter=20000, filter=True, adapt_min_steps=0, adapt_max_steps=0, state=None, stream=None):
+        """Runs the Fig. 1 loop in the library; x is updated in place.  `state`
+        (an _lib.ToOptState) carries continuation/adaptation counters across
+        calls.  Returns (status, list of per-step dicts)."""
         P = L.ToOptParams(volfrac=volfrac, move=move, eta=eta, rho_o=rho_o, penal0=penal0, penal_max=penal_max,
                           penal_step=penal_step, stage_steps=stage_steps, stop_on_converge=int(stop_on_converge),
-                          change_tol=change_tol, rtol=rtol, max_iter=max_iter, filter=int(filter))
+                          change_tol=change_tol, rtol=rtol, max_iter=max_iter, filter=int(filter),
+                          adapt_min_steps=adapt_min_steps, adapt_max_steps=adapt_max_steps)
         hist = (L.ToOptStep * max(1, n_steps))()
         done = C.c_int32(0)
         rc = L.lib().to_optimize(self._h, C.byref(P), int(n_steps), _dptr(x), _dptr(u), hist, C.byref(done),
-                                 _stream(stream))
+                                 C.byref(state) if state is not None else None, _stream(stream))
         L.check(rc, "to_optimize")
         out = [{f: getattr(hist[k], f) for f, _ in L.ToOptStep._fields_} for k in range(done.value)]
         for h in out:
             h["lam"] = h.pop("lambda_")
         return rc, out
+
+    def to_amr_mark(self, x, marks, rho_s=0.5, stream=None):
+        """marks: int8 CUDA tensor [n_el] (+1 refine, -1 derefine, 0 keep)."""
+        import torch
+        if not (marks.is_cuda and marks.dtype == torch.int8 and marks.is_contiguous()):
+            raise ValueError("marks must be a contiguous int8 CUDA tensor")
+        L.check(L.lib().to_amr_mark(self._h, _dptr(x), float(rho_s), C.c_void_p(marks.data_ptr()),
+                                    _stream(stream)), "to_amr_mark")
+        return marks
 
     # -- operator-level calls -------------------------------------------------------------
     def to_apply_A(self, penal, x, v, q, stream=None):

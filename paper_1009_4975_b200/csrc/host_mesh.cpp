@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <unordered_map>
 #include <unordered_set>
 #include <vector>
 #include <deque>
@@ -206,6 +207,48 @@ static int build_filter(tomesh_host *H, double rmin) {
   return 0;
 }
 
+// C10 2:1 balance of a leaf set in place: worklist ripple, refining the
+// coarser leaf of any face/edge (3D) or edge (2D) pair more than one level apart.
+static int balance_set(LeafSet &S, int dim, int L, const int32_t *ext) {
+  const int nc = 1 << dim;
+  auto dirs = balance_dirs(dim);
+  std::deque<uint64_t> work(S.begin(), S.end());
+  while (!work.empty()) {
+    uint64_t k = work.front();
+    work.pop_front();
+    if (!S.count(k)) continue;
+    int l = LeafKey::level(k);
+    int32_t a[3] = {0, 0, 0};
+    LeafKey::anchor(k, dim, a);
+    int32_t s = 1 << (L - l);
+    for (auto &d : dirs) {
+      int32_t q[3] = {0, 0, 0};
+      bool inside = true;
+      for (int c = 0; c < dim; ++c) {
+        q[c] = a[c] + d[c] * s;
+        if (q[c] < 0 || q[c] >= ext[c]) inside = false;
+      }
+      if (!inside) continue;
+      for (;;) {
+        int lb;
+        int32_t ab[3] = {0, 0, 0};
+        if (!locate(S, dim, L, q, &lb, ab)) { set_error("point location failed"); return TO_EINVAL; }
+        if (lb >= l - 1) break;
+        S.erase(LeafKey::make(lb, ab, dim));
+        int32_t half = 1 << (L - lb - 1);
+        for (int ch = 0; ch < nc; ++ch) {
+          int32_t ca[3] = {0, 0, 0};
+          for (int c = 0; c < dim; ++c) ca[c] = ab[c] + ((ch >> c) & 1) * half;
+          uint64_t ck = LeafKey::make(lb + 1, ca, dim);
+          S.insert(ck);
+          work.push_back(ck);
+        }
+      }
+    }
+  }
+  return 0;
+}
+
 static int build(const tomesh_host_spec *sp, tomesh_host *H) {
   const int dim = sp->dim, L = sp->max_level;
   if (dim != 2 && dim != 3) { set_error("dim must be 2 or 3"); return TO_EINVAL; }
@@ -243,41 +286,8 @@ static int build(const tomesh_host_spec *sp, tomesh_host *H) {
   for (int64_t i = 1; i < sp->n_leaf; ++i)
     if (sp->leaf_level[i] != sp->leaf_level[0]) { one_level = false; break; }
   if (!one_level) {  // a single-level tiling is trivially balanced
-    auto dirs = balance_dirs(dim);
-    std::deque<uint64_t> work(S.begin(), S.end());
-    while (!work.empty()) {
-      uint64_t k = work.front();
-      work.pop_front();
-      if (!S.count(k)) continue;
-      int l = LeafKey::level(k);
-      int32_t a[3] = {0, 0, 0};
-      LeafKey::anchor(k, dim, a);
-      int32_t s = 1 << (L - l);
-      for (auto &d : dirs) {
-        int32_t q[3] = {0, 0, 0};
-        bool inside = true;
-        for (int c = 0; c < dim; ++c) {
-          q[c] = a[c] + d[c] * s;
-          if (q[c] < 0 || q[c] >= H->ext[c]) inside = false;
-        }
-        if (!inside) continue;
-        for (;;) {
-          int lb;
-          int32_t ab[3] = {0, 0, 0};
-          if (!locate(S, dim, L, q, &lb, ab)) { set_error("point location failed"); return TO_EINVAL; }
-          if (lb >= l - 1) break;
-          S.erase(LeafKey::make(lb, ab, dim));
-          int32_t half = 1 << (L - lb - 1);
-          for (int ch = 0; ch < nc; ++ch) {
-            int32_t ca[3] = {0, 0, 0};
-            for (int c = 0; c < dim; ++c) ca[c] = ab[c] + ((ch >> c) & 1) * half;
-            uint64_t ck = LeafKey::make(lb + 1, ca, dim);
-            S.insert(ck);
-            work.push_back(ck);
-          }
-        }
-      }
-    }
+    const int rc = balance_set(S, dim, L, H->ext);
+    if (rc != 0) return rc;
   }
 
   // ---- C2: Morton order of leaves ----------------------------------------------
@@ -545,3 +555,248 @@ extern "C" int tomesh_host_filter(tomesh_host *H, double rmin) {
 }
 
 extern "C" void tomesh_host_free(tomesh_host *H) { delete H; }
+
+// ======================================================================================
+// Dynamic AMR: compatibility sweeps on the device-computed
+// marks, refine/derefine, density transfer.  Readings R21-R23.
+// ======================================================================================
+
+struct tomesh_adapt {
+  int dim = 0, L = 0;
+  std::vector<int8_t> leaf_level, marks;
+  std::vector<int32_t> leaf_anchor;
+  std::vector<double> leaf_x;
+  int64_t n_refined = 0, n_groups = 0, n_unmarked_sibling = 0, n_unmarked_incompat = 0;
+};
+
+namespace {
+
+static int adapt(const tomesh_host *H, const int8_t *marks_in, const double *x, tomesh_adapt *A) {
+  const int dim = H->dim, L = H->L, nc = 1 << dim;
+  const int64_t ne = (int64_t)H->elem_level.size();
+  A->dim = dim;
+  A->L = L;
+  std::vector<int8_t> m(marks_in, marks_in + ne);
+  for (int64_t e = 0; e < ne; ++e) {
+    const int l = H->elem_level[e];
+    if (m[e] < -1 || m[e] > 1) { set_error("marks must be -1, 0 or +1"); return TO_EINVAL; }
+    if ((m[e] == 1 && l >= L) || (m[e] == -1 && l == 0)) { set_error("mark beyond the level range"); return TO_EINVAL; }
+  }
+  std::unordered_map<uint64_t, int64_t, Splitmix> where;
+  where.reserve((size_t)ne * 2);
+  for (int64_t e = 0; e < ne; ++e) where[LeafKey::make(H->elem_level[e], &H->elem_anchor[e * dim], dim)] = e;
+  // siblings of e in corner order (-1 where the sibling is not a leaf)
+  auto group = [&](int64_t e, int32_t *pa, int64_t *sib) {
+    const int l = H->elem_level[e];
+    const int32_t s = 1 << (L - l);
+    for (int c = 0; c < dim; ++c) pa[c] = H->elem_anchor[e * dim + c] & ~(2 * s - 1);
+    for (int ch = 0; ch < nc; ++ch) {
+      int32_t a[3] = {0, 0, 0};
+      for (int c = 0; c < dim; ++c) a[c] = pa[c] + ((ch >> c) & 1) * s;
+      auto it = where.find(LeafKey::make(l, a, dim));
+      sib[ch] = it == where.end() ? -1 : it->second;
+    }
+  };
+  // sweep 1: every sibling a leaf marked for derefinement
+  {
+    std::vector<int8_t> m1(m);
+    for (int64_t e = 0; e < ne; ++e) {
+      if (m[e] != -1) continue;
+      int32_t pa[3];
+      int64_t sib[8];
+      group(e, pa, sib);
+      for (int ch = 0; ch < nc; ++ch)
+        if (sib[ch] < 0 || m[sib[ch]] != -1) {
+          m1[e] = 0;
+          A->n_unmarked_sibling++;
+          break;
+        }
+    }
+    m.swap(m1);
+  }
+  // sweep 2: no leaf two or more levels finer than the parent across a face/edge,
+  // in the 2:1 closure of this pass's refinements
+  {
+    LeafSet C;
+    C.reserve((size_t)ne * 2 + 16);
+    for (int64_t e = 0; e < ne; ++e) {
+      const int l = H->elem_level[e];
+      const int32_t *a = &H->elem_anchor[e * dim];
+      if (m[e] == 1) {
+        const int32_t half = 1 << (L - l - 1);
+        for (int ch = 0; ch < nc; ++ch) {
+          int32_t ca[3] = {0, 0, 0};
+          for (int c = 0; c < dim; ++c) ca[c] = a[c] + ((ch >> c) & 1) * half;
+          C.insert(LeafKey::make(l + 1, ca, dim));
+        }
+      } else {
+        C.insert(LeafKey::make(l, a, dim));
+      }
+    }
+    const int rc = balance_set(C, dim, L, H->ext);
+    if (rc != 0) return rc;
+    auto dirs = balance_dirs(dim);
+    std::vector<char> seen(ne, 0);
+    for (int64_t e = 0; e < ne; ++e) {
+      if (m[e] != -1 || seen[e]) continue;
+      int32_t pa[3] = {0, 0, 0};
+      int64_t sib[8];
+      group(e, pa, sib);
+      for (int ch = 0; ch < nc; ++ch) seen[sib[ch]] = 1;
+      const int l = H->elem_level[e];
+      bool bad = false;
+      if (l < L) {
+        const int32_t S2 = 2 * (1 << (L - l)), t = (1 << (L - l)) / 2;
+        for (auto &d : dirs) {
+          // probe cells of edge t along the parent's side(s) in direction d
+          int32_t lo[3] = {0, 0, 0}, cnt[3] = {1, 1, 1};
+          for (int c = 0; c < dim; ++c) {
+            if (d[c] < 0) lo[c] = pa[c] - t;
+            else if (d[c] > 0) lo[c] = pa[c] + S2;
+            else { lo[c] = pa[c]; cnt[c] = S2 / t; }
+          }
+          for (int32_t k2 = 0; k2 < cnt[2] && !bad; ++k2)
+            for (int32_t k1 = 0; k1 < cnt[1] && !bad; ++k1)
+              for (int32_t k0 = 0; k0 < cnt[0] && !bad; ++k0) {
+                int32_t q[3] = {lo[0] + k0 * t, lo[1] + k1 * t, lo[2] + k2 * t};
+                bool inside = true;
+                for (int c = 0; c < dim; ++c)
+                  if (q[c] < 0 || q[c] >= H->ext[c]) inside = false;
+                if (!inside) continue;
+                int lb;
+                int32_t ab[3];
+                if (!locate(C, dim, L, q, &lb, ab)) { set_error("point location failed"); return TO_EINVAL; }
+                if (lb >= l + 1) bad = true;
+              }
+          if (bad) break;
+        }
+      }
+      if (bad)
+        for (int ch = 0; ch < nc; ++ch)
+          if (m[sib[ch]] == -1) {
+            m[sib[ch]] = 0;
+            A->n_unmarked_incompat++;
+          }
+    }
+  }
+  // the new pre-balance leaf set with transferred densities
+  std::vector<uint64_t> key;
+  std::vector<int64_t> val;
+  std::vector<int8_t> lv;
+  std::vector<int32_t> an;
+  std::vector<double> xv;
+  auto emit = [&](int l, const int32_t *a, double xe) {
+    key.push_back(morton(dim, a));
+    val.push_back((int64_t)lv.size());
+    lv.push_back((int8_t)l);
+    for (int c = 0; c < dim; ++c) an.push_back(a[c]);
+    xv.push_back(xe);
+  };
+  for (int64_t e = 0; e < ne; ++e) {
+    const int l = H->elem_level[e];
+    const int32_t *a = &H->elem_anchor[e * dim];
+    const int32_t s = 1 << (L - l);
+    if (m[e] == 1) {
+      A->n_refined++;
+      for (int ch = 0; ch < nc; ++ch) {
+        int32_t ca[3] = {0, 0, 0};
+        for (int c = 0; c < dim; ++c) ca[c] = a[c] + ((ch >> c) & 1) * (s / 2);
+        emit(l + 1, ca, x[e]);
+      }
+    } else if (m[e] == -1) {
+      int32_t pa[3] = {0, 0, 0};
+      int64_t sib[8];
+      group(e, pa, sib);
+      bool first = true;
+      for (int c = 0; c < dim; ++c) first = first && (pa[c] == a[c]);
+      if (first) {
+        double acc = 0.0;   // mean of the children in corner order
+        for (int ch = 0; ch < nc; ++ch) acc += x[sib[ch]];
+        A->n_groups++;
+        emit(l - 1, pa, acc / nc);
+      }
+    } else {
+      emit(l, a, x[e]);
+    }
+  }
+  radix_sort_pairs(key, val);
+  const int64_t n = (int64_t)val.size();
+  A->leaf_level.resize(n);
+  A->leaf_anchor.resize(n * dim);
+  A->leaf_x.resize(n);
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t j = val[i];
+    A->leaf_level[i] = lv[j];
+    for (int c = 0; c < dim; ++c) A->leaf_anchor[i * dim + c] = an[j * dim + c];
+    A->leaf_x[i] = xv[j];
+  }
+  A->marks.swap(m);
+  return 0;
+}
+
+}  // namespace
+
+extern "C" int tomesh_host_adapt(const tomesh_host *H, const int8_t *marks, const double *x, tomesh_adapt **out) {
+  clear_error();
+  if (!H || !marks || !x || !out) { set_error("NULL argument"); return TO_EINVAL; }
+  *out = nullptr;
+  tomesh_adapt *A = new (std::nothrow) tomesh_adapt();
+  if (!A) { set_error("out of host memory"); return TO_ENOMEM; }
+  int rc;
+  try {
+    rc = adapt(H, marks, x, A);
+  } catch (const std::bad_alloc &) {
+    set_error("out of host memory");
+    rc = TO_ENOMEM;
+  } catch (...) {
+    set_error("internal error in tomesh_host_adapt");
+    rc = TO_EINVAL;
+  }
+  if (rc != 0) { delete A; return rc; }
+  *out = A;
+  return 0;
+}
+
+extern "C" int tomesh_adapt_get(const tomesh_adapt *A, tomesh_adapt_result *o) {
+  if (!A || !o) { set_error("NULL argument"); return TO_EINVAL; }
+  o->n_leaf = (int64_t)A->leaf_level.size();
+  o->leaf_level = A->leaf_level.data();
+  o->leaf_anchor = A->leaf_anchor.data();
+  o->leaf_x = A->leaf_x.data();
+  o->marks = A->marks.data();
+  o->n_refined = A->n_refined;
+  o->n_groups = A->n_groups;
+  o->n_unmarked_sibling = A->n_unmarked_sibling;
+  o->n_unmarked_incompat = A->n_unmarked_incompat;
+  return 0;
+}
+
+extern "C" int tomesh_host_transfer(const tomesh_host *H, const tomesh_adapt *A, double *x_out) {
+  clear_error();
+  if (!H || !A || !x_out) { set_error("NULL argument"); return TO_EINVAL; }
+  if (H->dim != A->dim || H->L != A->L) { set_error("mesh and adaptation differ in dim or max_level"); return TO_EINVAL; }
+  const int dim = H->dim;
+  std::unordered_map<uint64_t, double, Splitmix> xs;
+  LeafSet P;
+  const int64_t n = (int64_t)A->leaf_level.size();
+  xs.reserve((size_t)n * 2);
+  P.reserve((size_t)n * 2);
+  for (int64_t i = 0; i < n; ++i) {
+    const uint64_t k = LeafKey::make(A->leaf_level[i], &A->leaf_anchor[i * dim], dim);
+    xs[k] = A->leaf_x[i];
+    P.insert(k);
+  }
+  const int64_t ne = (int64_t)H->elem_level.size();
+  for (int64_t e = 0; e < ne; ++e) {
+    int lb;
+    int32_t ab[3];
+    if (!locate(P, dim, H->L, &H->elem_anchor[e * dim], &lb, ab) || lb > H->elem_level[e]) {
+      set_error("element %lld is not inside a leaf of the adaptation", (long long)e);
+      return TO_EINVAL;
+    }
+    x_out[e] = xs[LeafKey::make(lb, ab, dim)];
+  }
+  return 0;
+}
+
+extern "C" void tomesh_adapt_free(tomesh_adapt *A) { delete A; }

@@ -951,4 +951,23 @@ __global__ void k_filter(MeshView M, const int64_t *__restrict__ fptr, const int
   }
 }
 
+// Dynamic AMR marking (reading R21): +1 when a solid
+// element (x >= rho_s) lies in e's neighbour list (|c_d - c_e| < r_amr =
+// rmin, self included), else -1; refinement capped at level L, derefinement
+// at level 0.  Integer output, no floating-point decisions beyond x >= rho_s.
+__global__ void k_amr_mark(int64_t n_el, const int8_t *__restrict__ level, int L, const int64_t *__restrict__ fptr,
+                           const int32_t *__restrict__ fidx, const double *__restrict__ x, double rho_s,
+                           int8_t *__restrict__ marks) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_el; e += (int64_t)gridDim.x * blockDim.x) {
+    bool near = false;
+    if (fptr) {
+      for (int64_t k = fptr[e]; k < fptr[e + 1] && !near; ++k) near = x[fidx[k]] >= rho_s;
+    } else {
+      near = x[e] >= rho_s;
+    }
+    const int l = level[e];
+    marks[e] = near ? (l < L ? 1 : 0) : (l > 0 ? -1 : 0);
+  }
+}
+
 }  // namespace tomesh

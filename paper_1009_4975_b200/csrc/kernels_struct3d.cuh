@@ -522,6 +522,28 @@ __global__ void k_filter_s3(GridView G, int64_t n, const int32_t *__restrict__ p
   }
 }
 
+// Dynamic AMR marking on the uniform box (reading R21): x scattered to
+// lexicographic order in t_lex, then any solid element within the filter
+// stencil (the same exact |o|^2 h^2 < rmin^2 offsets).  lev = the mesh level.
+__global__ void k_amr_mark_s3(GridView G, int64_t n, const int32_t *__restrict__ perm_el,
+                              const S3FilterOffset *__restrict__ offs, int n_off, const double *__restrict__ t_lex,
+                              double rho_s, int lev, int L, int8_t *__restrict__ marks) {
+  GRID_STRIDE(e, n) {
+    const int64_t l = perm_el[e];
+    const int i = (int)(l % G.EX);
+    const int64_t rest = l / G.EX;
+    const int j = (int)(rest % G.EY), k = (int)(rest / G.EY);
+    bool near = false;
+    for (int o = 0; o < n_off && !near; ++o) {
+      const S3FilterOffset f = offs[o];
+      const int ii = i + f.di, jj = j + f.dj, kk = k + f.dk;
+      if (ii < 0 || ii >= G.EX || jj < 0 || jj >= G.EY || kk < 0 || kk >= G.EZ) continue;
+      near = __ldg(&t_lex[ii + (int64_t)G.EX * (jj + (int64_t)G.EY * kk)]) >= rho_s;
+    }
+    marks[e] = near ? (lev < L ? 1 : 0) : (lev > 0 ? -1 : 0);
+  }
+}
+
 // ---- setup kernels of the structured path ------------------------------------------------
 
 // s in lexicographic element order from x in canonical (Morton) element order.

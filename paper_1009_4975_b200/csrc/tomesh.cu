@@ -1035,6 +1035,34 @@ extern "C" int to_filter(to_mesh *m, int32_t mode, const double *x_dev, const do
   return check_launch();
 }
 
+extern "C" int to_amr_mark(to_mesh *m, const double *x_dev, double rho_s, int8_t *marks_dev, void *cuda_stream) {
+  clear_error();
+  if (!m || !x_dev || !marks_dev) { set_error("NULL argument"); return TO_EINVAL; }
+  if (!(rho_s > 0.0 && rho_s <= 1.0)) { set_error("rho_s must lie in (0, 1]"); return TO_EINVAL; }
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int g = grid_for(m->n_el);
+  if (m->structured) {
+    // structured meshes are one level: read it back once from the uploaded levels
+    int8_t lev = 0;
+    CK(cudaMemcpyAsync(&lev, m->elem_level, 1, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const bool filt = m->rmin > 0.0;
+    if (filt) k_filter_s3_scatter<<<g, kBlock, 0, st>>>(m->n_el, m->perm_el, 1, x_dev, x_dev, m->ftmp);
+    k_amr_mark_s3<<<g, kBlock, 0, st>>>(m->G, m->n_el, m->perm_el, m->foffs, filt ? m->n_foffs : 0,
+                                        filt ? m->ftmp : nullptr, rho_s, lev, m->L, marks_dev);
+    m->launches_total += filt ? 2 : 1;
+    if (!filt) {   // no neighbourhood: only the element itself (reading R21 with r_amr = 0)
+      k_amr_mark<<<g, kBlock, 0, st>>>(m->n_el, m->elem_level, m->L, nullptr, nullptr, x_dev, rho_s, marks_dev);
+      m->launches_total++;
+    }
+    return check_launch();
+  }
+  k_amr_mark<<<g, kBlock, 0, st>>>(m->n_el, m->elem_level, m->L, m->rmin > 0.0 ? m->filt_ptr : nullptr,
+                                   m->filt_idx, x_dev, rho_s, marks_dev);
+  m->launches_total++;
+  return check_launch();
+}
+
 extern "C" int to_oc_update(to_mesh *m, const double *x_dev, const double *dc_dev, double volfrac, double move,
                             double eta, double rho_o, double *x_new_dev, to_oc_stats *st, void *cuda_stream) {
   clear_error();
@@ -1103,21 +1131,25 @@ extern "C" int to_oc_update(to_mesh *m, const double *x_dev, const double *dc_de
 }
 
 extern "C" int to_optimize(to_mesh *m, const to_opt_params *P, int32_t n_steps, double *x_dev, double *u_dev,
-                           to_opt_step *hist, int32_t *steps_done, void *cuda_stream) {
+                           to_opt_step *hist, int32_t *steps_done, to_opt_state *state, void *cuda_stream) {
   clear_error();
   if (steps_done) *steps_done = 0;
   if (!m || !P || !x_dev || !u_dev || n_steps < 0) { set_error("bad argument"); return TO_EINVAL; }
   if (!(P->penal0 > 0.0) || !(P->penal_max >= P->penal0) || !(P->penal_step >= 0.0) || P->stage_steps < 1 ||
-      !(P->rtol > 0.0) || P->max_iter < 1) {
-    set_error("bad continuation or solver parameters");
+      !(P->rtol > 0.0) || P->max_iter < 1 || P->adapt_min_steps < 0 || P->adapt_max_steps < 0) {
+    set_error("bad continuation, solver or adaptation parameters");
     return TO_EINVAL;
   }
   if (!m->opt_dc) {
     RC(m->alloc(&m->opt_dc, (size_t)m->n_el));
     RC(m->alloc(&m->opt_dcf, (size_t)m->n_el));
   }
-  double penal = P->penal0;
-  int at_stage = 0, k = 0, result = TO_OK;
+  double penal = state ? state->penal : P->penal0;
+  int at_stage = state ? state->at_stage : 0, since = state ? state->since_adapt : 0;
+  if (!(penal > 0.0)) { set_error("state->penal must be > 0"); return TO_EINVAL; }
+  if (state) state->adapt_due = state->converged = 0;
+  const bool amr = P->adapt_max_steps > 0;
+  int k = 0, result = TO_OK;
   for (; k < n_steps; ++k) {
     to_cg_stats cs{};
     const int rc = tosolve_cg(m, penal, x_dev, u_dev, P->rtol, P->max_iter, (k > 0 ? TO_WARM : 0) | TO_NO_TRUE_RES,
@@ -1146,15 +1178,27 @@ extern "C" int to_optimize(to_mesh *m, const to_opt_params *P, int32_t n_steps, 
       h.status = rc;
     }
     ++at_stage;
+    ++since;
     const bool conv = os.change < P->change_tol;
     if (P->stop_on_converge && penal >= P->penal_max && conv) {
       ++k;
+      if (state) state->converged = 1;
       break;
     }
     if (penal < P->penal_max && (conv || at_stage >= P->stage_steps)) {
       penal = std::min(P->penal_max, penal + P->penal_step);
       at_stage = 0;
     }
+    if (amr && ((conv && since >= P->adapt_min_steps) || since >= P->adapt_max_steps)) {
+      ++k;
+      if (state) state->adapt_due = 1;
+      break;
+    }
+  }
+  if (state) {
+    state->penal = penal;
+    state->at_stage = at_stage;
+    state->since_adapt = since;
   }
   if (steps_done) *steps_done = k;
   return result;

@@ -47,7 +47,8 @@ def test_struct_layouts_match_header(tmp_path):
     structs = {"to_mesh_desc": _lib.ToMeshDesc, "to_cg_stats": _lib.ToCgStats,
                "to_mesh_info": _lib.ToMeshInfo, "tomesh_host_spec": _lib.HostSpec,
                "tomesh_host_arrays": _lib.HostArrays, "to_oc_stats": _lib.ToOcStats,
-               "to_opt_params": _lib.ToOptParams, "to_opt_step": _lib.ToOptStep}
+               "to_opt_params": _lib.ToOptParams, "to_opt_step": _lib.ToOptStep,
+               "to_opt_state": _lib.ToOptState, "tomesh_adapt_result": _lib.AdaptResult}
     lines = ['#include <cstdio>', '#include <cstddef>', '#include "tomesh.h"', '#include "tomesh_host.h"',
              "int main(){"]
     for cname, cls in structs.items():
@@ -160,3 +161,64 @@ def test_product_hadamard_factorisation(nu, rng):
                 Yh[m, i] = acc
         y = (H3 @ Yh).reshape(-1)
         assert np.max(np.abs(y - Ko @ x)) <= 1e-14 * np.max(np.abs(Ko @ x)) * 10
+
+
+# ---- dynamic AMR mesh update: C++ host code vs oracle/amr.py (bit-exact) ----------------
+
+def _amr_cases():
+    from tests.helpers import cantilever2d, cantilever3d, refine_some
+    return [
+        cantilever2d((6, 3), L=3, leaves=refine_some(2, (6, 3), 3, [(1, 1), (4, 0), (2, 2)]), rmin=0.9),
+        cantilever3d((3, 2, 2), L=2, leaves=refine_some(3, (3, 2, 2), 2, [(1, 1, 0), (0, 0, 1)]), rmin=0.7),
+    ]
+
+
+@pytest.mark.parametrize("case", [0, 1])
+def test_host_adapt_matches_oracle(case):
+    """tomesh_host_adapt + tomesh_host_build + tomesh_host_transfer reproduce the
+    oracle's sweeps, leaf set, densities and balanced mesh exactly, over a
+    sequence of adaptations driven by random density fields (oracle marks)."""
+    from oracle import amr
+    prob = _amr_cases()[case]
+    rng = np.random.default_rng(21 + case)
+    om = omesh.build_mesh(prob, density=False)
+    hm = pb.prepare(prob, keep_handle=True)
+    x = rng.uniform(1e-3, 1.0, om.n_el) ** 2
+    for it in range(4):
+        assert np.array_equal(hm.elem_level, om.elem_level) and np.array_equal(hm.elem_anchor, om.elem_anchor)
+        mk = amr.mark(om, x, 0.5, prob.rmin)
+        if it == 3:   # random marks exercise both sweeps harder
+            mk = rng.choice(np.array([-1, 0, 1], dtype=np.int8), om.n_el, p=[0.6, 0.3, 0.1])
+            mk[(mk == 1) & (om.elem_level == om.L)] = 0
+            mk[(mk == -1) & (om.elem_level == 0)] = 0
+        ro = amr.adapt(om, x, mk)
+        rh = pb.api.tomesh_host_adapt(hm, mk, x)
+        assert np.array_equal(rh.marks, ro.marks)
+        assert (rh.n_refined, rh.n_groups, rh.n_unmarked_sibling, rh.n_unmarked_incompat) == \
+            (ro.n_refined, ro.n_groups, ro.n_unmarked_sibling, ro.n_unmarked_incompat)
+        assert np.array_equal(rh.leaf_level, ro.leaf_level) and np.array_equal(rh.leaf_anchor, ro.leaf_anchor)
+        assert np.array_equal(rh.leaf_x, ro.leaf_x)                       # bit-exact means
+        om = amr.rebuild(prob, ro)
+        hm = pb.api.rebuild(prob, rh)
+        xo = amr.transfer(om, ro)
+        xh = pb.api.tomesh_host_transfer(hm, rh)
+        assert np.array_equal(xh, xo)
+        for f in ("elem_node", "hang_node", "hang_parent", "fixed_dof", "load", "filt_ptr", "filt_idx"):
+            assert np.array_equal(getattr(hm, f), getattr(om, f)), f
+        x = np.clip(xo + rng.normal(0, 0.25, om.n_el), 1e-3, 1.0)
+
+
+def test_host_adapt_rejects_bad_marks():
+    prob = _amr_cases()[0]
+    hm = pb.prepare(prob, keep_handle=True)
+    x = np.full(hm.n_el, 0.5)
+    bad = np.zeros(hm.n_el, dtype=np.int8)
+    bad[int(np.nonzero(hm.elem_level == 0)[0][0])] = -1            # derefine at level 0
+    with pytest.raises(pb.TomeshError):
+        pb.api.tomesh_host_adapt(hm, bad, x)
+    bad[:] = 0
+    bad[0] = 3
+    with pytest.raises(pb.TomeshError):
+        pb.api.tomesh_host_adapt(hm, bad, x)
+    with pytest.raises(ValueError):
+        pb.api.tomesh_host_adapt(pb.prepare(prob), np.zeros(hm.n_el, dtype=np.int8), x)   # no handle kept
