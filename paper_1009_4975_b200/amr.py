@@ -9,6 +9,7 @@ and the new mesh uploaded.  This module only sequences those calls.
 """
 from __future__ import annotations
 
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -49,20 +50,27 @@ def optimize_amr(problem, volfrac, n_steps, penal0=1.0, penal_max=3.0, penal_ste
         done += len(hist)
         if not state.adapt_due:
             break
+        t0 = time.perf_counter()
         marks = torch.empty(host.n_el, dtype=torch.int8, device=dev)
         mesh.to_amr_mark(x, marks, rho_s)
-        ad = tomesh_host_adapt(host, marks.cpu().numpy(), x.cpu().numpy())
+        mk, xh = marks.cpu().numpy(), x.cpu().numpy()
+        t1 = time.perf_counter()
+        ad = tomesh_host_adapt(host, mk, xh)
         new_host = rebuild(problem, ad)
         xn = tomesh_host_transfer(new_host, ad)
-        run.adaptations.append({"step": done, "n_elem_before": host.n_el, "n_elem_after": new_host.n_el,
-                                "n_refined": ad.n_refined, "n_groups": ad.n_groups,
-                                "n_unmarked_sibling": ad.n_unmarked_sibling,
-                                "n_unmarked_incompat": ad.n_unmarked_incompat})
-        run.steps[-1]["adapted"] = True
+        t2 = time.perf_counter()
         mesh.close()
         host = new_host
         mesh = Mesh(host, E0=problem.E0, Emin=problem.Emin, nu=problem.nu, rmin=problem.rmin, device=device)
         x = torch.as_tensor(xn, device=dev)
+        torch.cuda.synchronize(dev)
+        t3 = time.perf_counter()
+        run.adaptations.append({"step": done, "n_elem_before": len(mk), "n_elem_after": host.n_el,
+                                "n_refined": ad.n_refined, "n_groups": ad.n_groups,
+                                "n_unmarked_sibling": ad.n_unmarked_sibling,
+                                "n_unmarked_incompat": ad.n_unmarked_incompat,
+                                "mark_s": t1 - t0, "host_adapt_rebuild_s": t2 - t1, "upload_s": t3 - t2})
+        run.steps[-1]["adapted"] = True
         state.since_adapt = 0
         state.adapt_due = 0
     mesh.close()
