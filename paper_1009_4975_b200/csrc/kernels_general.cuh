@@ -564,6 +564,7 @@ __device__ __forceinline__ double g_elem_lane(const MeshView &M, int64_t e, int 
                                               const uint8_t *__restrict__ hmask, double beta, bool live) {
   constexpr int NC = 1 << DIM;
   const int n = __ldg(M.elem_node + e * NC + c);
+  const double se = __ldg(s + e);   // independent of the gather: issued first
   double v[DIM];
   g_pnode<DIM, MODE, COH>(zp, po, beta, n, v);
   if ((__ldg(hmask + e) >> c) & 1) {
@@ -578,7 +579,6 @@ __device__ __forceinline__ double g_elem_lane(const MeshView &M, int64_t e, int 
       for (int i = 0; i < DIM; ++i) v[i] = fma(w, t[i], v[i]);
     }
   }
-  const double se = __ldg(s + e);
   double en = 0.0, y[DIM];
   if constexpr (DIM == 3) {
     // forward WHT over the group: stage b pairs lanes c and c ^ b
@@ -709,17 +709,38 @@ __global__ void __launch_bounds__(256) k_node_pass_lanes(int64_t n_node, const i
        base += groups) {
     const int64_t n = base + (threadIdx.x & 31) / G;
     const bool live = n < n_node;
+    // node-side operands do not depend on q: load them before the incidence sum
+    const int64_t dpre = n * DIM + l;
+    double di_p = 0.0, r_p = 0.0, x_p = 0.0, z_p = 0.0, po_p = 0.0;
+    if (MODE == G_CG && live && l < DIM) {
+      di_p = __ldg(Dinv + dpre);
+      r_p = r[dpre];
+      x_p = x[dpre];
+      z_p = zp[n * 2 * DIM + l];
+      po_p = zp[n * 2 * DIM + DIM + l];
+    }
     double qv[DIM];
 #pragma unroll
     for (int i = 0; i < DIM; ++i) qv[i] = 0.0;
     if (live) {
       const int64_t k1 = inc_ptr[n + 1];
-      for (int64_t k = inc_ptr[n] + l; k < k1; k += G) {
+      // two incidences per lane per round: both index and value loads in flight together
+      for (int64_t k = inc_ptr[n] + l; k < k1; k += 2 * G) {
+        const bool two = k + G < k1;
         const uint32_t t = __ldg(&inc[k]);
+        const uint32_t u = two ? __ldg(&inc[k + G]) : 0u;
         const double w = (t >> 30) == 0 ? 1.0 : (t >> 30) == 1 ? 0.5 : 0.25;
+        const double wu = !two ? 0.0 : (u >> 30) == 0 ? 1.0 : (u >> 30) == 1 ? 0.5 : 0.25;
         const double *src = ye + (int64_t)(t & 0x3fffffffu) * DIM;
+        const double *srcu = ye + (int64_t)(u & 0x3fffffffu) * DIM;
+        double a[DIM], b[DIM];
 #pragma unroll
-        for (int i = 0; i < DIM; ++i) qv[i] = fma(w, __ldg(src + i), qv[i]);
+        for (int i = 0; i < DIM; ++i) {
+          a[i] = __ldg(src + i);
+          b[i] = two ? __ldg(srcu + i) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) qv[i] = fma(wu, b[i], fma(w, a[i], qv[i]));
       }
     }
 #pragma unroll
@@ -737,12 +758,12 @@ __global__ void __launch_bounds__(256) k_node_pass_lanes(int64_t n_node, const i
       continue;
     }
     double *rec = zp + n * 2 * DIM;
-    const double di = __ldg(Dinv + d);
-    const double pk = fma(beta, rec[DIM + l], rec[l]);
+    const double di = di_p;
+    const double pk = fma(beta, po_p, z_p);
     double zn = 0.0;
     if (di != 0.0) {
-      x[d] = fma(alpha, pk, x[d]);
-      const double rn = fma(-alpha, qc, r[d]);
+      x[d] = fma(alpha, pk, x_p);
+      const double rn = fma(-alpha, qc, r_p);
       r[d] = rn;
       zn = di * rn;
       acc[0] = fma(rn, zn, acc[0]);
