@@ -163,6 +163,26 @@ int  tosolve_cg(to_mesh *m, double penal, const double *x_dev, double *u_dev,
                 double rtol, int32_t max_iter, uint32_t flags, to_cg_stats *st,
                 void *cuda_stream);
 
+/* The paper's own solver (§5): MINRES (Paige-Saunders) on
+ * the explicitly rescaled system K~ = D^-1/2 A D^-1/2 (:511-523), either with
+ * the rescaling alone (TO_PC_JACOBI) or preconditioned by a zero-fill
+ * incomplete Cholesky factor of K~ (TO_PC_IC0, :524-530; shifted on
+ * breakdown, reading R24).  Krylov recycling (RMINRES) is not
+ * implemented.  Starts from u = 0; stops when the M^-1-norm of the residual,
+ * |eta|, falls to rtol times its initial value, or after max_iter steps
+ * (TO_NOT_CONVERGED).  flags: TO_NO_TRUE_RES only.  Synchronises the stream. */
+enum { TO_PC_JACOBI = 0, TO_PC_IC0 = 1 };
+typedef struct {
+  int32_t iters, status;
+  double  eta_rel;             /* |eta_final| / |eta_0|                          */
+  double  relres_true;         /* ||b - A u||_2 / ||b||_2 (-1 if skipped)         */
+  double  ms;                  /* device time of the call                        */
+  double  ic0_shift;           /* shift a of the IC(0) factor of K~ + a I (-1: none) */
+} to_minres_stats;
+int  tosolve_minres(to_mesh *m, double penal, const double *x_dev, double *u_dev, double rtol,
+                    int32_t max_iter, int32_t precond, uint32_t flags, to_minres_stats *st,
+                    void *cuda_stream);
+
 /* Residual history of the last TO_HISTORY solve: copies min(n, iters)
  * values of ||r_k||/||b|| (k = 1..iters) to host `out`; returns the count. */
 int  tosolve_history(const to_mesh *m, double *out, int32_t n);

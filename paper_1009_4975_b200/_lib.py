@@ -14,6 +14,7 @@ TO_OK, TO_NOT_CONVERGED = 0, 1
 TO_EINVAL, TO_ECUDA, TO_ENOMEM, TO_EMESH, TO_ENAN, TO_EBREAKDOWN, TO_ENONPOS_DIAG = -1, -2, -3, -4, -5, -6, -7
 TO_WARM, TO_FIXED_ITERS, TO_HISTORY, TO_NO_TRUE_RES, TO_PROFILE = 1, 2, 4, 8, 16
 TO_FILTER_SENS, TO_FILTER_DENS = 0, 1
+TO_PC_JACOBI, TO_PC_IC0 = 0, 1
 TOH_LOAD_POINT, TOH_LOAD_LINE, TOH_LOAD_FACE = 0, 1, 2
 
 STATUS_NAMES = {0: "TO_OK", 1: "TO_NOT_CONVERGED", -1: "TO_EINVAL", -2: "TO_ECUDA", -3: "TO_ENOMEM",
@@ -46,6 +47,11 @@ class ToMeshInfo(C.Structure):
                 ("n_fixed", C.c_int64), ("filt_nnz", C.c_int64), ("grid", C.c_int64 * 3),
                 ("device_bytes", C.c_int64), ("kernel_launches", C.c_int32), ("matvec_variant", C.c_int32),
                 ("launches_total", C.c_int64)]
+
+
+class ToMinresStats(C.Structure):
+    _fields_ = [("iters", C.c_int32), ("status", C.c_int32), ("eta_rel", C.c_double), ("relres_true", C.c_double),
+                ("ms", C.c_double), ("ic0_shift", C.c_double)]
 
 
 class ToOcStats(C.Structure):
@@ -105,6 +111,8 @@ EXPORTS = {
     "tomesh_free": (None, [P]),
     "tomesh_get_info": (C.c_int, [P, C.POINTER(ToMeshInfo)]),
     "tosolve_cg": (C.c_int, [P, C.c_double, P, P, C.c_double, C.c_int32, C.c_uint32, C.POINTER(ToCgStats), P]),
+    "tosolve_minres": (C.c_int, [P, C.c_double, P, P, C.c_double, C.c_int32, C.c_int32, C.c_uint32,
+                                 C.POINTER(ToMinresStats), P]),
     "tosolve_history": (C.c_int, [P, P, C.c_int32]),
     "tosolve_profile": (C.c_int, [P, P, C.c_int32]),
     "to_sensitivity": (C.c_int, [P, C.c_double, P, P, P, C.POINTER(C.c_double), P]),

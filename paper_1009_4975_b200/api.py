@@ -323,6 +323,15 @@ class Mesh:
         L.check(rc, "tosolve_cg")
         return CgStats(st.iters, st.status, st.relres, st.relres_true, st.ms, st.bnorm)
 
+    def tosolve_minres(self, penal, x, u, rtol=1e-10, max_iter=20000, precond=0, flags=0, stream=None) -> dict:
+        """The paper's solver: MINRES on the rescaled system, precond 0 = rescaling
+        only (TO_PC_JACOBI), 1 = IC(0) of the rescaled matrix (TO_PC_IC0)."""
+        st = L.ToMinresStats()
+        rc = L.lib().tosolve_minres(self._h, float(penal), _dptr(x), _dptr(u), float(rtol), int(max_iter),
+                                    int(precond), int(flags), C.byref(st), _stream(stream))
+        L.check(rc, "tosolve_minres")
+        return {f: getattr(st, f) for f, _ in L.ToMinresStats._fields_}
+
     def history(self, n):
         out = np.zeros(max(1, n))
         k = L.lib().tosolve_history(self._h, _ptr(out), int(n))

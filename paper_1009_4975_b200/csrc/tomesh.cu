@@ -19,6 +19,7 @@
 #include "kernels_general.cuh"
 #include "kernels_oc.cuh"
 #include "kernels_struct3d.cuh"
+#include "kernels_minres.cuh"
 
 using namespace tomesh;
 
@@ -68,6 +69,11 @@ struct to_mesh {
   OcState *oc_state = nullptr;
   OcState *oc_state_host = nullptr;   // pinned mirror
   double *opt_dc = nullptr, *opt_dcf = nullptr;   // to_optimize: raw and filtered sensitivities
+  // MINRES (tosolve_minres), allocated on first use, internal order with pads
+  double *mr_v[3] = {nullptr, nullptr, nullptr}, *mr_w[3] = {nullptr, nullptr, nullptr};
+  double *mr_zn[2] = {nullptr, nullptr}, *mr_z[2] = {nullptr, nullptr};
+  double *mr_xt = nullptr, *mr_msc = nullptr, *mr_az = nullptr, *mr_t = nullptr;
+  MrScalars *MS = nullptr, *MS_host = nullptr;
   int oc_blocks = 0;
   double vol_total = 0.0;             // sum_e V_e (exact dyadic sum, host)
   // workspace
@@ -141,6 +147,7 @@ struct to_mesh {
     for (auto &b : bufs) cudaFree(b.p);
     if (S_host) cudaFreeHost(S_host);
     if (oc_state_host) cudaFreeHost(oc_state_host);
+    if (MS_host) cudaFreeHost(MS_host);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     for (auto e : prof_ev) cudaEventDestroy(e);
@@ -898,6 +905,171 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   return rc;
 }
 
+int alloc_padded(to_mesh *m, double **v, cudaStream_t st) {
+  double *base = nullptr;
+  RC(m->alloc(&base, (size_t)(m->n_int + kS3PadFront + kS3PadBack)));
+  CK(cudaMemsetAsync(base, 0, sizeof(double) * (m->n_int + kS3PadFront + kS3PadBack), st));
+  *v = base + kS3PadFront;
+  return 0;
+}
+
+int read_mr(to_mesh *m, cudaStream_t st) {
+  CK(cudaMemcpyAsync(m->MS_host, m->MS, sizeof(MrScalars), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int op_ic0_solve(to_mesh *m, const double *v, double *z, cudaStream_t st);   // kernels_ic0 (below)
+int op_ic0_setup(to_mesh *m, cudaStream_t st, double *shift);
+
+// MINRES on the rescaled system (header comment of kernels_minres.cuh).
+int solve_minres(to_mesh *m, double penal, const double *x_dev, double *u_dev, double rtol, int32_t max_iter,
+                 int32_t precond, uint32_t flags, to_minres_stats *st_out, cudaStream_t st) {
+  const int64_t n = m->n_int;
+  const bool ic0 = precond == TO_PC_IC0;
+  m->last_launches = 0;
+  if (!m->MS) {
+    for (int b = 0; b < 3; ++b) {
+      RC(alloc_padded(m, &m->mr_v[b], st));
+      RC(alloc_padded(m, &m->mr_w[b], st));
+    }
+    for (int b = 0; b < 2; ++b) {
+      RC(alloc_padded(m, &m->mr_zn[b], st));
+      RC(alloc_padded(m, &m->mr_z[b], st));
+    }
+    RC(alloc_padded(m, &m->mr_xt, st));
+    RC(alloc_padded(m, &m->mr_msc, st));
+    RC(alloc_padded(m, &m->mr_az, st));
+    if (!m->structured) RC(alloc_padded(m, &m->mr_t, st));
+    RC(m->alloc(&m->MS, 1));
+    CK(cudaMallocHost(&m->MS_host, sizeof(MrScalars)));
+  }
+  double *t = m->structured ? m->rb[0] : m->mr_t;   // the apply input (TMA-mapped when structured)
+  CK(cudaEventRecord(m->ev0, st));
+  RC(reset_scalars(m, 0, false, false, st));
+  RC(op_scale_and_diag(m, penal, x_dev, nullptr, st));
+  const int gv = grid_for(n);
+  if (m->structured) {
+    k_mr_scale_s3<<<grid_for((int64_t)m->G.NX * m->G.NY * m->G.NZ), kBlock, 0, st>>>(m->G, m->dn, m->mr_msc);
+  } else {
+    k_mr_scale<<<gv, kBlock, 0, st>>>(n, m->dinv, m->mr_msc);
+  }
+  m->last_launches++;
+  RC(read_scalars(m, st));
+  if (m->S_host->status != 0) {
+    set_error(m->S_host->status == TO_EINVAL ? "density outside (0, 1]" : "non-positive diagonal on a free DOF");
+    return m->S_host->status;
+  }
+  double shift = 0.0;
+  if (ic0) RC(op_ic0_setup(m, st, &shift));
+  std::memset(m->MS_host, 0, sizeof(MrScalars));
+  m->MS_host->max_iter = max_iter;
+  CK(cudaMemcpyAsync(m->MS, m->MS_host, sizeof(MrScalars), cudaMemcpyHostToDevice, st));
+  for (int b = 0; b < 3; ++b) {
+    CK(cudaMemsetAsync(m->mr_v[b], 0, sizeof(double) * n, st));
+    CK(cudaMemsetAsync(m->mr_w[b], 0, sizeof(double) * n, st));
+  }
+  CK(cudaMemsetAsync(m->mr_xt, 0, sizeof(double) * n, st));
+  RC(op_rhs(m, m->r, st));                                   // b (internal order)
+  if (!ic0) {
+    k_mr_init<true><<<gv, kBlock, 0, st>>>(n, m->r, m->mr_msc, m->mr_v[1], m->partials, m->MS, rtol);
+    m->last_launches++;
+  } else {
+    k_mr_init<false><<<gv, kBlock, 0, st>>>(n, m->r, m->mr_msc, m->mr_v[1], m->partials, m->MS, rtol);
+    m->last_launches++;
+    RC(op_ic0_solve(m, m->mr_v[1], m->mr_z[1], st));
+    k_mr_init_gamma<<<gv, kBlock, 0, st>>>(n, m->mr_z[1], m->mr_v[1], m->partials, m->MS, rtol);
+    m->last_launches++;
+  }
+  RC(check_launch());
+  // iteration it performs Lanczos / Givens step j = it + 1 and, first, the
+  // w / x~ update of step it (buffers: v(k) in mr_v[k%3], w(k) in mr_w[k%3],
+  // zn(k) in mr_zn[k%2], z(k) in mr_z[k%2])
+  auto iteration = [&](int it) -> int {
+    const double *z_j = ic0 ? m->mr_z[(it + 1) % 2] : m->mr_v[(it + 1) % 3];
+    k_mr_wx_prep<<<gv, kBlock, 0, st>>>(n, m->mr_zn[(it + 1) % 2], m->mr_w[(it + 2) % 3], m->mr_w[it % 3],
+                                        m->mr_w[(it + 1) % 3], m->mr_xt, z_j, m->mr_msc, m->mr_zn[it % 2], t, m->MS);
+    m->last_launches++;
+    RC(op_apply(m, t, m->q, st));
+    k_mr_delta<<<gv, kBlock, 0, st>>>(n, m->q, m->mr_msc, m->mr_zn[it % 2], m->mr_az, m->partials, m->MS);
+    m->last_launches++;
+    double *v_new = m->mr_v[(it + 2) % 3];
+    if (!ic0) {
+      k_mr_lanczos<true><<<gv, kBlock, 0, st>>>(n, m->mr_az, m->mr_v[(it + 1) % 3], m->mr_v[it % 3], v_new,
+                                                m->partials, m->MS);
+      m->last_launches++;
+    } else {
+      k_mr_lanczos<false><<<gv, kBlock, 0, st>>>(n, m->mr_az, m->mr_v[(it + 1) % 3], m->mr_v[it % 3], v_new,
+                                                 m->partials, m->MS);
+      m->last_launches++;
+      RC(op_ic0_solve(m, v_new, m->mr_z[it % 2], st));
+      k_mr_gamma<<<gv, kBlock, 0, st>>>(n, m->mr_z[it % 2], v_new, m->partials, m->MS);
+      m->last_launches++;
+    }
+    return 0;
+  };
+  RC(read_mr(m, st));
+  int launched = 0, chunk = 16;
+  bool stop = m->MS_host->done != 0;
+  while (!stop && launched < max_iter) {
+    const int cnt = std::min(chunk, max_iter - launched);
+    for (int k = 0; k < cnt; ++k) RC(iteration(launched + k));
+    RC(check_launch());
+    launched += cnt;
+    RC(read_mr(m, st));
+    stop = m->MS_host->done != 0;
+    chunk = std::min(chunk * 2, 256);
+  }
+  // the w / x~ update of the last step (a no-op if an enqueued iteration did it)
+  {
+    const int it = launched;
+    k_mr_wx_prep<<<gv, kBlock, 0, st>>>(n, m->mr_zn[(it + 1) % 2], m->mr_w[(it + 2) % 3], m->mr_w[it % 3],
+                                        m->mr_w[(it + 1) % 3], m->mr_xt, m->mr_v[0], m->mr_msc, m->mr_zn[it % 2], t,
+                                        m->MS);
+    m->last_launches++;
+  }
+  k_mr_unscale<<<gv, kBlock, 0, st>>>(n, m->mr_msc, m->mr_xt, m->x);
+  m->last_launches++;
+  RC(read_mr(m, st));
+  MrScalars res = *m->MS_host;
+  double relres_true = -1.0;
+  if (!(flags & TO_NO_TRUE_RES) && res.status == 0) {
+    RC(op_rhs(m, m->r, st));
+    RC(op_apply(m, m->x, m->q, st));
+    k_resid2<<<gv, kBlock, 0, st>>>(n, m->r, m->q, free_int(m), m->partials, m->S);
+    m->last_launches++;
+    RC(read_scalars(m, st));
+    relres_true = res.bnorm2 > 0.0 ? std::sqrt(m->S_host->tmp[0] / res.bnorm2) : 0.0;
+  }
+  RC(op_recover_out(m, m->x, u_dev, st));
+  CK(cudaEventRecord(m->ev1, st));
+  CK(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
+  int rc = res.status;
+  const bool converged = res.eta0 == 0.0 || std::fabs(res.eta) <= res.thresh;
+  if (rc == 0 && !converged) rc = TO_NOT_CONVERGED;
+  if (st_out) {
+    st_out->iters = res.iter;
+    st_out->status = rc;
+    st_out->eta_rel = res.eta0 > 0.0 ? std::fabs(res.eta) / res.eta0 : 0.0;
+    st_out->relres_true = relres_true;
+    st_out->ms = ms;
+    st_out->ic0_shift = ic0 ? shift : -1.0;
+  }
+  if (rc < 0) set_error("%s", rc == TO_EBREAKDOWN ? "MINRES breakdown" : "NaN/Inf in the MINRES recurrences");
+  return rc;
+}
+
+int op_ic0_solve(to_mesh *, const double *, double *, cudaStream_t) {
+  set_error("IC(0) preconditioning is not available in this build");
+  return TO_EINVAL;
+}
+int op_ic0_setup(to_mesh *, cudaStream_t, double *) {
+  set_error("IC(0) preconditioning is not available in this build");
+  return TO_EINVAL;
+}
+
 // Adds the kernels an operator-level entry point launched (via last_launches)
 // to the handle's monotone counter, on every return path.
 struct LaunchCounter {
@@ -1033,6 +1205,20 @@ extern "C" int to_filter(to_mesh *m, int32_t mode, const double *x_dev, const do
   if (m->dim == 2) k_filter<2><<<g, kBlock, 0, st>>>(m->view(), m->filt_ptr, m->filt_idx, m->rmin, mode, x_dev, in_dev, out_dev);
   else k_filter<3><<<g, kBlock, 0, st>>>(m->view(), m->filt_ptr, m->filt_idx, m->rmin, mode, x_dev, in_dev, out_dev);
   return check_launch();
+}
+
+extern "C" int tosolve_minres(to_mesh *m, double penal, const double *x_dev, double *u_dev, double rtol,
+                              int32_t max_iter, int32_t precond, uint32_t flags, to_minres_stats *st,
+                              void *cuda_stream) {
+  LaunchCounter lc_{m, 0};
+  clear_error();
+  if (!m || !x_dev || !u_dev || !(penal > 0.0) || max_iter < 0 || !(rtol >= 0.0)) {
+    set_error("bad argument");
+    return TO_EINVAL;
+  }
+  if (precond != TO_PC_JACOBI && precond != TO_PC_IC0) { set_error("unknown preconditioner"); return TO_EINVAL; }
+  if (flags & ~(uint32_t)TO_NO_TRUE_RES) { set_error("tosolve_minres supports TO_NO_TRUE_RES only"); return TO_EINVAL; }
+  return solve_minres(m, penal, x_dev, u_dev, rtol, max_iter, precond, flags, st, (cudaStream_t)cuda_stream);
 }
 
 extern "C" int to_amr_mark(to_mesh *m, const double *x_dev, double rho_s, int8_t *marks_dev, void *cuda_stream) {

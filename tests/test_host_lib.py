@@ -48,7 +48,8 @@ def test_struct_layouts_match_header(tmp_path):
                "to_mesh_info": _lib.ToMeshInfo, "tomesh_host_spec": _lib.HostSpec,
                "tomesh_host_arrays": _lib.HostArrays, "to_oc_stats": _lib.ToOcStats,
                "to_opt_params": _lib.ToOptParams, "to_opt_step": _lib.ToOptStep,
-               "to_opt_state": _lib.ToOptState, "tomesh_adapt_result": _lib.AdaptResult}
+               "to_opt_state": _lib.ToOptState, "tomesh_adapt_result": _lib.AdaptResult,
+               "to_minres_stats": _lib.ToMinresStats}
     lines = ['#include <cstdio>', '#include <cstddef>', '#include "tomesh.h"', '#include "tomesh_host.h"',
              "int main(){"]
     for cname, cls in structs.items():
