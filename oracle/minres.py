@@ -151,7 +151,9 @@ def rescale(A, b):
         raise ArithmeticError("non-positive diagonal")
     s = 1.0 / np.sqrt(d)
     S = sp.diags(s)
-    return sp.csr_matrix(S @ A @ S), s * b, s
+    Kt = sp.csr_matrix(S @ A @ S)
+    Kt.eliminate_zeros()      # the IC(0) pattern is the nonzero structure (explicit zeros of the projection dropped)
+    return Kt, s * b, s
 
 
 def solve_paper(A, b, rtol=1e-10, max_iter=10000, precond="ic0"):

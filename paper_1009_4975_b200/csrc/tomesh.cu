@@ -20,6 +20,7 @@
 #include "kernels_oc.cuh"
 #include "kernels_struct3d.cuh"
 #include "kernels_minres.cuh"
+#include "kernels_ic0.cuh"
 
 using namespace tomesh;
 
@@ -74,6 +75,16 @@ struct to_mesh {
   double *mr_zn[2] = {nullptr, nullptr}, *mr_z[2] = {nullptr, nullptr};
   double *mr_xt = nullptr, *mr_msc = nullptr, *mr_az = nullptr, *mr_t = nullptr;
   MrScalars *MS = nullptr, *MS_host = nullptr;
+  // IC(0) of the rescaled matrix (general path), built on first use
+  bool ic_ready = false;
+  Ic0View IC{};
+  double *ic_kt = nullptr, *ic_L = nullptr, *ic_K0 = nullptr, *ic_y = nullptr;
+  int64_t *ic_lvl_ptr = nullptr, *ic_blvl_ptr = nullptr, *ic_ut_ptr = nullptr, *ic_ut_pos = nullptr;
+  int32_t *ic_lvl_rows = nullptr, *ic_blvl_rows = nullptr, *ic_ut_row = nullptr;
+  std::vector<int64_t> ic_lvl_host;   // level boundaries (host) for the per-level factor launches
+  int ic_nlvl = 0, ic_nblvl = 0;
+  int *ic_fail = nullptr;
+  double ic_setup_ms = 0.0;
   int oc_blocks = 0;
   double vol_total = 0.0;             // sum_e V_e (exact dyadic sum, host)
   // workspace
@@ -1061,13 +1072,205 @@ int solve_minres(to_mesh *m, double penal, const double *x_dev, double *u_dev, d
   return rc;
 }
 
-int op_ic0_solve(to_mesh *, const double *, double *, cudaStream_t) {
-  set_error("IC(0) preconditioning is not available in this build");
-  return TO_EINVAL;
+template <typename T>
+int download(std::vector<T> &h, const T *d, size_t n) {
+  h.resize(n);
+  if (n) CK(cudaMemcpy(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost));
+  return 0;
 }
-int op_ic0_setup(to_mesh *, cudaStream_t, double *) {
-  set_error("IC(0) preconditioning is not available in this build");
-  return TO_EINVAL;
+
+// Host symbolic phase of IC(0) (general path): the lower pattern of K~ over
+// free-free couplings (through the Eq. 6 interpolation) plus unit rows of the
+// non-free DOFs, the element contributions of every nonzero, the transposed
+// pattern and the dependency levels of both triangular solves.
+int ic0_build(to_mesh *m, cudaStream_t st) {
+  const int dim = m->dim, nc = 1 << dim, ND = dim * nc;
+  const int64_t n = m->n_dof, ne = m->n_el;
+  CK(cudaStreamSynchronize(st));
+  std::vector<int32_t> en, nh, hp, hpar;
+  std::vector<double> hw;
+  std::vector<uint8_t> fr;
+  RC(download(en, m->elem_node, (size_t)ne * nc));
+  RC(download(nh, m->node_hang, (size_t)m->n_node));
+  RC(download(fr, m->free_dof, (size_t)n));
+  if (m->n_hang > 0) {
+    RC(download(hp, m->hang_ptr, (size_t)m->n_hang + 1));
+    RC(download(hpar, m->hang_parent, (size_t)hp[m->n_hang]));
+    RC(download(hw, m->hang_weight, (size_t)hp[m->n_hang]));
+  }
+  auto wcode = [](double w) -> int { return w == 1.0 ? 0 : w == 0.5 ? 1 : w == 0.25 ? 2 : -1; };
+  // expansions of every local DOF of an element: (global free DOF, log2(1/w))
+  auto expand = [&](int64_t e, int a, std::vector<std::pair<int64_t, int>> &out) {
+    out.clear();
+    const int32_t node = en[e * nc + a / dim], c = a % dim;
+    if (nh[node] < 0) {
+      const int64_t g = (int64_t)node * dim + c;
+      if (fr[g]) out.push_back({g, 0});
+      return;
+    }
+    const int32_t h = nh[node];
+    for (int32_t k = hp[h]; k < hp[h + 1]; ++k) {
+      const int64_t g = (int64_t)hpar[k] * dim + c;
+      if (fr[g]) out.push_back({g, wcode(hw[k])});
+    }
+  };
+  std::vector<std::vector<std::pair<int64_t, int>>> ex(ND);
+  // per row: (column, packed contribution), then sorted by column
+  std::vector<std::vector<std::pair<int32_t, uint64_t>>> rows(n);
+  for (int64_t e = 0; e < ne; ++e) {
+    for (int a = 0; a < ND; ++a) expand(e, a, ex[a]);
+    for (int a = 0; a < ND; ++a)
+      for (const auto &pa : ex[a])
+        for (int b = 0; b < ND; ++b)
+          for (const auto &pb : ex[b]) {
+            if (pb.first > pa.first) continue;   // lower triangle (column <= row)
+            const uint64_t code = (uint64_t)(pa.second + pb.second);
+            rows[pa.first].push_back({(int32_t)pb.first, ((uint64_t)e << 16) | ((uint64_t)(a * ND + b) << 3) | code});
+          }
+  }
+  std::vector<int64_t> ptr(n + 1, 0), cptr(1, 0);
+  std::vector<int32_t> col, row;
+  std::vector<uint64_t> contrib;
+  for (int64_t i = 0; i < n; ++i) {
+    auto &R = rows[i];
+    std::stable_sort(R.begin(), R.end(), [](const std::pair<int32_t, uint64_t> &x, const std::pair<int32_t, uint64_t> &y) {
+      return x.first < y.first;
+    });
+    if (R.empty()) {                         // non-free DOF: unit diagonal, no contributions
+      col.push_back((int32_t)i);
+      row.push_back((int32_t)i);
+      cptr.push_back((int64_t)contrib.size());
+    } else {
+      for (size_t u = 0; u < R.size();) {
+        size_t v = u;
+        while (v < R.size() && R[v].first == R[u].first) contrib.push_back(R[v++].second);
+        col.push_back(R[u].first);
+        row.push_back((int32_t)i);
+        cptr.push_back((int64_t)contrib.size());
+        u = v;
+      }
+      if (col.back() != (int32_t)i) { set_error("IC(0): free row %lld without a diagonal", (long long)i); return TO_EMESH; }
+    }
+    ptr[i + 1] = (int64_t)col.size();
+    std::vector<std::pair<int32_t, uint64_t>>().swap(R);
+  }
+  const int64_t nnz = (int64_t)col.size();
+  // dependency levels: forward (row i after its columns k < i), backward (row k of L^T after rows i > k)
+  std::vector<int32_t> lv(n, 0), blv(n, 0);
+  int nl = 0, nbl = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int l = 0;
+    for (int64_t t = ptr[i]; t < ptr[i + 1] - 1; ++t) l = std::max(l, lv[col[t]] + 1);
+    lv[i] = l;
+    nl = std::max(nl, l + 1);
+  }
+  std::vector<int64_t> ut_ptr(n + 1, 0);
+  for (int64_t t = 0; t < nnz; ++t)
+    if (col[t] != row[t]) ut_ptr[col[t] + 1]++;
+  for (int64_t k = 0; k < n; ++k) ut_ptr[k + 1] += ut_ptr[k];
+  std::vector<int32_t> ut_row(ut_ptr[n]);
+  std::vector<int64_t> ut_pos(ut_ptr[n]), ufill(ut_ptr.begin(), ut_ptr.end() - 1);
+  for (int64_t i = 0; i < n; ++i)          // rows ascending: each column's entries ascending in i
+    for (int64_t t = ptr[i]; t < ptr[i + 1] - 1; ++t) {
+      const int64_t q = ufill[col[t]]++;
+      ut_row[q] = (int32_t)i;
+      ut_pos[q] = t;
+    }
+  for (int64_t k = n - 1; k >= 0; --k) {
+    int l = 0;
+    for (int64_t t = ut_ptr[k]; t < ut_ptr[k + 1]; ++t) l = std::max(l, blv[ut_row[t]] + 1);
+    blv[k] = l;
+    nbl = std::max(nbl, l + 1);
+  }
+  auto bucket = [&](const std::vector<int32_t> &lvl, int nlev, std::vector<int64_t> &lptr, std::vector<int32_t> &lrows) {
+    lptr.assign(nlev + 1, 0);
+    for (int64_t i = 0; i < n; ++i) lptr[lvl[i] + 1]++;
+    for (int l = 0; l < nlev; ++l) lptr[l + 1] += lptr[l];
+    lrows.resize(n);
+    std::vector<int64_t> f(lptr.begin(), lptr.end() - 1);
+    for (int64_t i = 0; i < n; ++i) lrows[f[lvl[i]]++] = (int32_t)i;
+  };
+  std::vector<int64_t> lptr, blptr;
+  std::vector<int32_t> lrows, blrows;
+  bucket(lv, nl, lptr, lrows);
+  bucket(blv, nbl, blptr, blrows);
+  // device copies
+  int64_t *d_ptr, *d_cptr;
+  int32_t *d_col, *d_row;
+  uint64_t *d_contrib;
+  RC(upload_array(m, &d_ptr, ptr.data(), ptr.size(), st));
+  RC(upload_array(m, &d_col, col.data(), col.size(), st));
+  RC(upload_array(m, &d_row, row.data(), row.size(), st));
+  RC(upload_array(m, &d_cptr, cptr.data(), cptr.size(), st));
+  RC(upload_array(m, &d_contrib, contrib.data(), std::max<size_t>(1, contrib.size()), st));
+  RC(upload_array(m, &m->ic_lvl_ptr, lptr.data(), lptr.size(), st));
+  RC(upload_array(m, &m->ic_lvl_rows, lrows.data(), lrows.size(), st));
+  RC(upload_array(m, &m->ic_blvl_ptr, blptr.data(), blptr.size(), st));
+  RC(upload_array(m, &m->ic_blvl_rows, blrows.data(), blrows.size(), st));
+  RC(upload_array(m, &m->ic_ut_ptr, ut_ptr.data(), ut_ptr.size(), st));
+  RC(upload_array(m, &m->ic_ut_row, ut_row.data(), std::max<size_t>(1, ut_row.size()), st));
+  RC(upload_array(m, &m->ic_ut_pos, ut_pos.data(), std::max<size_t>(1, ut_pos.size()), st));
+  const double *K0 = dim == 2 ? m->K2.K : m->K3.K;
+  RC(upload_array(m, &m->ic_K0, K0, (size_t)ND * ND, st));
+  RC(m->alloc(&m->ic_kt, (size_t)nnz));
+  RC(m->alloc(&m->ic_L, (size_t)nnz));
+  RC(m->alloc(&m->ic_y, (size_t)n));
+  RC(m->alloc(&m->ic_fail, 1));
+  m->IC.n = n;
+  m->IC.nnz = nnz;
+  m->IC.ptr = d_ptr;
+  m->IC.col = d_col;
+  m->IC.row = d_row;
+  m->IC.cptr = d_cptr;
+  m->IC.contrib = d_contrib;
+  m->ic_lvl_host = lptr;
+  m->ic_nlvl = nl;
+  m->ic_nblvl = nbl;
+  m->ic_ready = true;
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+// K~ (+ a I) assembled and factored; a = 0, then 1e-3 2^t until no pivot fails
+int op_ic0_setup(to_mesh *m, cudaStream_t st, double *shift) {
+  if (m->structured) {
+    set_error("IC(0) needs the general (canonical-order) operator path; upload with TOMESH_FORCE_GENERAL=1");
+    return TO_EINVAL;
+  }
+  if (!m->ic_ready) RC(ic0_build(m, st));
+  const int g = grid_for(m->IC.nnz);
+  for (int t = -1; t < 30; ++t) {
+    const double a = t < 0 ? 0.0 : 1e-3 * std::ldexp(1.0, t);
+    if (m->dim == 2) k_ic0_assemble<2><<<g, kBlock, 0, st>>>(m->IC, m->s, m->mr_msc, m->ic_K0, a, m->ic_L);
+    else k_ic0_assemble<3><<<g, kBlock, 0, st>>>(m->IC, m->s, m->mr_msc, m->ic_K0, a, m->ic_L);
+    m->last_launches++;
+    CK(cudaMemsetAsync(m->ic_fail, 0, sizeof(int), st));
+    for (int l = 0; l < m->ic_nlvl; ++l) {
+      const int64_t r0 = m->ic_lvl_host[l], r1 = m->ic_lvl_host[l + 1];
+      k_ic0_factor<<<(int)std::min<int64_t>((r1 - r0 + 127) / 128, 4 * kNumSMs), 128, 0, st>>>(
+          m->IC, m->ic_lvl_rows, r0, r1, m->ic_L, m->ic_fail);
+    }
+    m->last_launches += m->ic_nlvl;
+    RC(check_launch());
+    int fail = 0;
+    CK(cudaMemcpyAsync(&fail, m->ic_fail, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (!fail) {
+      *shift = a;
+      return 0;
+    }
+  }
+  set_error("IC(0) breaks down for every shift tried");
+  return TO_EBREAKDOWN;
+}
+
+// z = (L L^T)^-1 v
+int op_ic0_solve(to_mesh *m, const double *v, double *z, cudaStream_t st) {
+  k_ic0_fwd<<<1, 1024, 0, st>>>(m->IC, m->ic_lvl_ptr, m->ic_nlvl, m->ic_lvl_rows, m->ic_L, v, m->ic_y);
+  k_ic0_bwd<<<1, 1024, 0, st>>>(m->IC, m->ic_ut_ptr, m->ic_ut_row, m->ic_ut_pos, m->ic_blvl_ptr, m->ic_nblvl,
+                                m->ic_blvl_rows, m->ic_L, m->ic_y, z);
+  m->last_launches += 2;
+  return check_launch();
 }
 
 // Adds the kernels an operator-level entry point launched (via last_launches)

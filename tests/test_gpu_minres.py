@@ -71,3 +71,28 @@ def test_minres_edge_cases():
     xb[3] = 0.0
     with pytest.raises(pb.TomeshError):
         m.tosolve_minres(prob.penal, cuda(xb), u)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "amr2d", "amr3d"])
+def test_minres_ic0_parity(name):
+    """MINRES + IC(0) of the rescaled matrix: the same shift as the oracle's,
+    iteration counts within rounding, solution at the direct solve's."""
+    prob, om_, hm, m, x, A, b, C = _setup(name)
+    u = torch.zeros(hm.n_dof, dtype=torch.float64, device="cuda")
+    st = m.tosolve_minres(prob.penal, cuda(x), u, rtol=1e-12, max_iter=20000, precond=pb.TO_PC_IC0)
+    _, r = om.solve_paper(A, b, rtol=1e-12, precond="ic0")
+    assert st["status"] == 0 and st["ic0_shift"] == r.shift
+    assert abs(st["iters"] - r.iters) <= max(3, 0.05 * r.iters)
+    ud = fe.recover(C, spla.spsolve(A.tocsc(), b))
+    assert rel(host(u), ud) <= 1e-8
+    # fewer iterations than the rescaling alone (the point of the preconditioner)
+    st_j = m.tosolve_minres(prob.penal, cuda(x), u, rtol=1e-12, max_iter=50000, precond=pb.TO_PC_JACOBI)
+    assert st["iters"] < st_j["iters"]
+
+
+def test_minres_ic0_structured_rejected():
+    prob, om_, hm, m, x, A, b, C = _setup("c3s")
+    u = torch.zeros(hm.n_dof, dtype=torch.float64, device="cuda")
+    with pytest.raises(pb.TomeshError) as e:
+        m.tosolve_minres(prob.penal, cuda(x), u, precond=pb.TO_PC_IC0)
+    assert e.value.code == pb.TO_EINVAL
