@@ -178,6 +178,7 @@ typedef struct {
   double  relres_true;         /* ||b - A u||_2 / ||b||_2 (-1 if skipped)         */
   double  ms;                  /* device time of the call                        */
   double  ic0_shift;           /* shift a of the IC(0) factor of K~ + a I (-1: none) */
+  int32_t ic0_levels[2];       /* dependency levels of the forward / backward solves */
 } to_minres_stats;
 int  tosolve_minres(to_mesh *m, double penal, const double *x_dev, double *u_dev, double rtol,
                     int32_t max_iter, int32_t precond, uint32_t flags, to_minres_stats *st,

@@ -51,7 +51,7 @@ class ToMeshInfo(C.Structure):
 
 class ToMinresStats(C.Structure):
     _fields_ = [("iters", C.c_int32), ("status", C.c_int32), ("eta_rel", C.c_double), ("relres_true", C.c_double),
-                ("ms", C.c_double), ("ic0_shift", C.c_double)]
+                ("ms", C.c_double), ("ic0_shift", C.c_double), ("ic0_levels", C.c_int32 * 2)]
 
 
 class ToOcStats(C.Structure):

@@ -330,7 +330,9 @@ class Mesh:
         rc = L.lib().tosolve_minres(self._h, float(penal), _dptr(x), _dptr(u), float(rtol), int(max_iter),
                                     int(precond), int(flags), C.byref(st), _stream(stream))
         L.check(rc, "tosolve_minres")
-        return {f: getattr(st, f) for f, _ in L.ToMinresStats._fields_}
+        out = {f: getattr(st, f) for f, _ in L.ToMinresStats._fields_}
+        out["ic0_levels"] = list(out["ic0_levels"])
+        return out
 
     def history(self, n):
         out = np.zeros(max(1, n))

@@ -1067,6 +1067,8 @@ int solve_minres(to_mesh *m, double penal, const double *x_dev, double *u_dev, d
     st_out->relres_true = relres_true;
     st_out->ms = ms;
     st_out->ic0_shift = ic0 ? shift : -1.0;
+    st_out->ic0_levels[0] = ic0 ? m->ic_nlvl : 0;
+    st_out->ic0_levels[1] = ic0 ? m->ic_nblvl : 0;
   }
   if (rc < 0) set_error("%s", rc == TO_EBREAKDOWN ? "MINRES breakdown" : "NaN/Inf in the MINRES recurrences");
   return rc;

@@ -82,6 +82,7 @@ def test_minres_ic0_parity(name):
     st = m.tosolve_minres(prob.penal, cuda(x), u, rtol=1e-12, max_iter=20000, precond=pb.TO_PC_IC0)
     _, r = om.solve_paper(A, b, rtol=1e-12, precond="ic0")
     assert st["status"] == 0 and st["ic0_shift"] == r.shift
+    assert min(st["ic0_levels"]) >= 1
     assert abs(st["iters"] - r.iters) <= max(3, 0.05 * r.iters)
     ud = fe.recover(C, spla.spsolve(A.tocsc(), b))
     assert rel(host(u), ud) <= 1e-8
