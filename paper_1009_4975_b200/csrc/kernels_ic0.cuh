@@ -14,7 +14,7 @@
 //                    L_ii = sqrt(K~_ii - sum L_ik^2); a non-positive pivot
 //                    raises the breakdown flag (the host retries with a shift)
 //   k_ic0_fwd/bwd    L y = v and L^T z = y, level-scheduled inside ONE CTA
-//                    (__syncthreads between levels): the solves are
+//                    (a warp per row, __syncthreads between levels): the solves are
 //                    sequential chains of short rows, the dependency depth,
 //                    not bandwidth, bounds them — the reason the B200 path
 //                    keeps the plain rescaling.
@@ -83,36 +83,41 @@ __global__ void k_ic0_factor(Ic0View V, const int32_t *__restrict__ lvl_rows, in
   }
 }
 
-// L y = v, one CTA, levels in order
+// L y = v, one CTA, levels in order; a warp per row (lanes split the row's
+// entries, xor-shuffle sum)
 __global__ void __launch_bounds__(1024) k_ic0_fwd(Ic0View V, const int64_t *__restrict__ lvl_ptr, int n_lvl,
                                                   const int32_t *__restrict__ lvl_rows, const double *__restrict__ L,
                                                   const double *__restrict__ v, double *__restrict__ y) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int l = 0; l < n_lvl; ++l) {
-    for (int64_t r = lvl_ptr[l] + threadIdx.x; r < lvl_ptr[l + 1]; r += blockDim.x) {
+    for (int64_t r = lvl_ptr[l] + warp; r < lvl_ptr[l + 1]; r += nw) {
       const int i = lvl_rows[r];
       const int64_t a = V.ptr[i], b = V.ptr[i + 1];
-      double acc = v[i];
-      for (int64_t t = a; t < b - 1; ++t) acc = __dsub_rn(acc, __dmul_rn(L[t], __ldcg(&y[V.col[t]])));
-      __stcg(&y[i], __ddiv_rn(acc, L[b - 1]));
+      double acc = 0.0;
+      for (int64_t t = a + lane; t < b - 1; t += 32) acc = fma(L[t], __ldcg(&y[V.col[t]]), acc);
+      acc = warp_sum(acc);
+      if (lane == 0) __stcg(&y[i], (v[i] - acc) / L[b - 1]);
     }
     __syncthreads();
   }
 }
 
 // L^T z = y through the transposed pattern (rows of L^T: the entries below
-// the diagonal in column k of L), levels in order
+// the diagonal in column k of L), levels in order, a warp per row
 __global__ void __launch_bounds__(1024) k_ic0_bwd(Ic0View V, const int64_t *__restrict__ ut_ptr,
                                                   const int32_t *__restrict__ ut_row, const int64_t *__restrict__ ut_pos,
                                                   const int64_t *__restrict__ lvl_ptr, int n_lvl,
                                                   const int32_t *__restrict__ lvl_rows, const double *__restrict__ L,
                                                   const double *__restrict__ y, double *__restrict__ z) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int l = 0; l < n_lvl; ++l) {
-    for (int64_t r = lvl_ptr[l] + threadIdx.x; r < lvl_ptr[l + 1]; r += blockDim.x) {
+    for (int64_t r = lvl_ptr[l] + warp; r < lvl_ptr[l + 1]; r += nw) {
       const int k = lvl_rows[r];
-      double acc = y[k];
-      for (int64_t t = ut_ptr[k]; t < ut_ptr[k + 1]; ++t)
-        acc = __dsub_rn(acc, __dmul_rn(L[ut_pos[t]], __ldcg(&z[ut_row[t]])));
-      __stcg(&z[k], __ddiv_rn(acc, L[V.ptr[k + 1] - 1]));
+      double acc = 0.0;
+      for (int64_t t = ut_ptr[k] + lane; t < ut_ptr[k + 1]; t += 32)
+        acc = fma(L[ut_pos[t]], __ldcg(&z[ut_row[t]]), acc);
+      acc = warp_sum(acc);
+      if (lane == 0) __stcg(&z[k], (y[k] - acc) / L[V.ptr[k + 1] - 1]);
     }
     __syncthreads();
   }

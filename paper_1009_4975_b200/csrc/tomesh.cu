@@ -1088,6 +1088,11 @@ int download(std::vector<T> &h, const T *d, size_t n) {
 int ic0_build(to_mesh *m, cudaStream_t st) {
   const int dim = m->dim, nc = 1 << dim, ND = dim * nc;
   const int64_t n = m->n_dof, ne = m->n_el;
+  if (ne * (int64_t)(ND * (ND + 1) / 2) > (int64_t)250000000) {
+    set_error("IC(0): %lld elements give more than 2.5e8 element contributions (host symbolic phase too large)",
+              (long long)ne);
+    return TO_ENOMEM;
+  }
   CK(cudaStreamSynchronize(st));
   std::vector<int32_t> en, nh, hp, hpar;
   std::vector<double> hw;
