@@ -81,7 +81,8 @@ enum {
   TO_FIXED_ITERS = 2,     /* run exactly max_iter iterations, ignore rtol      */
   TO_HISTORY = 4,         /* record ||r_k||/||b|| into the handle's history    */
   TO_NO_TRUE_RES = 8,     /* skip the extra matvec for relres_true             */
-  TO_PROFILE = 16         /* time every iteration kernel with CUDA events      */
+  TO_PROFILE = 16,        /* time every iteration kernel with CUDA events      */
+  TO_PROFILE_LOOP = 32    /* one event pair around all iteration launches      */
 };
 
 /* to_filter modes */
@@ -191,7 +192,9 @@ int  tosolve_history(const to_mesh *m, double *out, int32_t n);
 /* Per-kernel device time of the last TO_PROFILE solve, in ms, summed over
  * its iterations: out[0] operator apply (q = A p, with p.q), out[1] the
  * alpha reduction (0 when fused into the apply), out[2] r update + (r.z,
- * r.r), out[3] x/p update, out[4] number of iterations profiled.  n >= 5. */
+ * r.r), out[3] x/p update, out[4] number of iterations profiled; with
+ * n >= 6, out[5] = the device time from the first to the last iteration
+ * launch of a TO_PROFILE_LOOP solve (one event pair, no per-launch events). */
 int  tosolve_profile(const to_mesh *m, double *out, int32_t n);
 
 /* dc_dev[n_elem] = -p x^(p-1) (E0-Emin) u_e^T K0(h_e) u_e with u_e the element

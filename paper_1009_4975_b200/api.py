@@ -341,9 +341,10 @@ class Mesh:
         return out[:k]
 
     def profile(self):
-        out = np.zeros(5)
-        L.check(L.lib().tosolve_profile(self._h, _ptr(out), 5), "tosolve_profile")
-        return {"apply_ms": out[0], "alpha_ms": out[1], "u1_ms": out[2], "u2_ms": out[3], "iters": int(out[4])}
+        out = np.zeros(6)
+        L.check(L.lib().tosolve_profile(self._h, _ptr(out), 6), "tosolve_profile")
+        return {"apply_ms": out[0], "alpha_ms": out[1], "u1_ms": out[2], "u2_ms": out[3], "iters": int(out[4]),
+                "loop_ms": out[5]}
 
     def to_sensitivity(self, penal, x, u, dc, compliance=False, stream=None):
         c = C.c_double(0.0)

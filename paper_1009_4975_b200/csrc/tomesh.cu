@@ -117,7 +117,8 @@ struct to_mesh {
   int matvec_variant = 0;
   int64_t launches_total = 0;          // every kernel launched on this handle
   std::vector<cudaEvent_t> prof_ev;   // TO_PROFILE: 5 events per iteration
-  double prof_ms[5] = {0, 0, 0, 0, 0};
+  double prof_ms[6] = {0, 0, 0, 0, 0, 0};
+  cudaEvent_t loop_ev[2] = {nullptr, nullptr};   // TO_PROFILE_LOOP: around the iteration launches
 
   MeshView view() const {
     MeshView M;
@@ -162,6 +163,8 @@ struct to_mesh {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     for (auto e : prof_ev) cudaEventDestroy(e);
+    for (auto e : loop_ev)
+      if (e) cudaEventDestroy(e);
   }
 };
 
@@ -823,6 +826,12 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
     RC(read_scalars(m, st));
     stop = m->S_host->done != 0;
   }
+  const bool loop_prof = (flags & TO_PROFILE_LOOP) != 0;
+  if (loop_prof) {
+    for (auto &e : m->loop_ev)
+      if (!e) CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(m->loop_ev[0], st));
+  }
   if (!m->structured && m->coop_blocks > 0 && !stop) {
     // the whole loop in one cooperative kernel (no host polling)
     if (prof) CK(cudaEventRecord(m->prof_ev[0], st));
@@ -862,10 +871,19 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
       chunk = std::min(chunk * 2, 256);
     }
   }
+  if (loop_prof) CK(cudaEventRecord(m->loop_ev[1], st));
   if (m->structured) RC(op_final_s3(m, max_iter, rtol, st));   // no-op if an iteration already converged
   RC(check_launch());
   RC(read_scalars(m, st));
   CgScalars res = *m->S_host;
+  if (loop_prof) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, m->loop_ev[0], m->loop_ev[1]));
+    if (!prof)
+      for (int j = 0; j < 4; ++j) m->prof_ms[j] = 0.0;
+    m->prof_ms[5] = t;
+    m->prof_ms[4] = std::min(launched, res.iter);
+  }
   if (prof) {
     for (int j = 0; j < 5; ++j) m->prof_ms[j] = 0.0;
     int nit = std::min(launched, res.iter);
@@ -1369,6 +1387,7 @@ extern "C" int tosolve_history(const to_mesh *m, double *out, int32_t n) {
 extern "C" int tosolve_profile(const to_mesh *m, double *out, int32_t n) {
   if (!m || !out || n < 5) { set_error("bad argument"); return TO_EINVAL; }
   for (int j = 0; j < 5; ++j) out[j] = m->prof_ms[j];
+  if (n >= 6) out[5] = m->prof_ms[5];
   return 0;
 }
 
