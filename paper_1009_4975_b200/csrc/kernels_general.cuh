@@ -663,7 +663,9 @@ __global__ void __launch_bounds__(256) k_elem_pass_lanes(MeshView M, const doubl
                                                          const uint8_t *__restrict__ hmask, CgScalars *S,
                                                          double *partials) {
   constexpr int NC = 1 << DIM;
-  if (MODE == G_CG && cg_stopped(S)) return;
+  // the stop flags are read without a control dependency at the top (their
+  // latency overlaps the gathers); a stopped iteration only skips the stores
+  const bool stopped = MODE == G_CG && (__ldcg(&S->done) | __ldcg(&S->done_next));
   const double beta = MODE == G_CG ? __ldcg(&S->beta) : 0.0;
   const int c = threadIdx.x & (NC - 1);
   const int64_t groups = ((int64_t)gridDim.x * blockDim.x) / NC;
@@ -673,8 +675,10 @@ __global__ void __launch_bounds__(256) k_elem_pass_lanes(MeshView M, const doubl
        base < M.n_el; base += groups) {
     const int64_t e = base + (threadIdx.x & 31) / NC;
     const bool live = e < M.n_el;
-    pq += g_elem_lane<DIM, MODE, false>(M, live ? e : M.n_el - 1, c, s, zp, po, ye, K2, H, hmask, beta, live);
+    pq += g_elem_lane<DIM, MODE, false>(M, live ? e : M.n_el - 1, c, s, zp, po, ye, K2, H, hmask, beta,
+                                        live && !stopped);
   }
+  if (stopped) return;
   if (MODE == G_CG) {
     double v[1] = {pq};
     if (grid_sum<1>(v, partials, &S->counter[CNT_PQ])) {
@@ -699,7 +703,8 @@ __global__ void __launch_bounds__(256) k_node_pass_lanes(int64_t n_node, const i
                                                          double *__restrict__ q_out, double *partials, CgScalars *S,
                                                          double *hist) {
   constexpr int G = 4;
-  if (MODE == G_CG && cg_stopped(S)) return;
+  // stop flags without a control dependency at the top (see k_elem_pass_lanes)
+  const bool stopped = MODE == G_CG && (__ldcg(&S->done) | __ldcg(&S->done_next));
   const double beta = MODE == G_CG ? __ldcg(&S->beta) : 0.0;
   const double alpha = MODE == G_CG ? __ldcg(&S->alpha) : 0.0;
   const int l = threadIdx.x & (G - 1);
@@ -747,7 +752,7 @@ __global__ void __launch_bounds__(256) k_node_pass_lanes(int64_t n_node, const i
     for (int b = 1; b < G; b <<= 1)
 #pragma unroll
       for (int i = 0; i < DIM; ++i) qv[i] += __shfl_xor_sync(0xffffffffu, qv[i], b);
-    if (!live || l >= DIM) continue;
+    if (!live || l >= DIM || stopped) continue;
     // lane l < DIM: component l
     double qc = qv[0];
 #pragma unroll
@@ -772,6 +777,7 @@ __global__ void __launch_bounds__(256) k_node_pass_lanes(int64_t n_node, const i
     rec[l] = zn;
     rec[DIM + l] = pk;
   }
+  if (stopped) return;
   if (MODE == G_CG) {
     if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) {
       cg_after_rupdate(S, acc[0], acc[1], hist);
