@@ -336,6 +336,15 @@ __device__ __forceinline__ double g_ld(const double *p) {
   return v;
 }
 
+// L1-cached 16-byte load for data written earlier in the same (persistent)
+// kernel by other blocks: coherent because every grid barrier executes a
+// gpu-scope fence, which invalidates the SM's L1 (B300_MICROARCH.md, L1D).
+__device__ __forceinline__ double2 g_ld2_ca(const double2 *p) {
+  double2 v;
+  asm volatile("ld.global.ca.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+  return v;
+}
+
 // Node record of the general-path CG: zp[n] = {z_k = Dinv r_k (DIM), p_{k-1}
 // (DIM)}, written by the node pass, so that a corner gather is one contiguous
 // 16*DIM-byte record instead of separate r, Dinv and p loads.
@@ -353,7 +362,7 @@ __device__ __forceinline__ void g_pnode(const double *__restrict__ zp, const dou
   double t[2 * DIM];
 #pragma unroll
   for (int h = 0; h < DIM; ++h) {
-    const double2 w = COH ? __ldcg(rec + h) : __ldg(rec + h);
+    const double2 w = COH ? g_ld2_ca(rec + h) : __ldg(rec + h);
     t[2 * h] = w.x;
     t[2 * h + 1] = w.y;
   }
@@ -695,6 +704,84 @@ __global__ void __launch_bounds__(256) k_elem_pass_lanes(MeshView M, const doubl
 // Node pass with a group of 4 lanes per node: lane l sums incidences l, l+4,
 // ... of the node, an xor-shuffle tree completes q_n in every lane of the
 // group, and lane i < DIM updates component i of the node (record, x, r).
+// One node of the 4-lane node pass (lane l of the group): q_n over the node's
+// incidences, then on lane l < DIM the CG update of component l.  COH: ye is
+// read through L2 (it was written in the same kernel by other blocks).
+template <int DIM, int MODE, bool COH>
+__device__ __forceinline__ void g_node_group(int64_t n, bool live, int l, const int64_t *__restrict__ inc_ptr,
+                                             const uint32_t *__restrict__ inc, const double *__restrict__ ye,
+                                             double *__restrict__ r, const double *__restrict__ Dinv,
+                                             double *__restrict__ zp, double *__restrict__ x,
+                                             double *__restrict__ q_out, double alpha, double beta, bool stopped,
+                                             double (&acc)[2]) {
+  constexpr int G = 4;
+  // node-side operands do not depend on q: load them before the incidence sum
+  const int64_t dpre = n * DIM + l;
+  double di_p = 0.0, r_p = 0.0, x_p = 0.0, z_p = 0.0, po_p = 0.0;
+  if (MODE == G_CG && live && l < DIM) {
+    di_p = __ldg(Dinv + dpre);
+    r_p = r[dpre];
+    x_p = x[dpre];
+    z_p = zp[n * 2 * DIM + l];
+    po_p = zp[n * 2 * DIM + DIM + l];
+  }
+  double qv[DIM];
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) qv[i] = 0.0;
+  if (live) {
+    const int64_t k1 = inc_ptr[n + 1];
+    // two incidences per lane per round: both index and value loads in flight together
+    for (int64_t k = inc_ptr[n] + l; k < k1; k += 2 * G) {
+      const bool two = k + G < k1;
+      const uint32_t t = __ldg(&inc[k]);
+      const uint32_t u = two ? __ldg(&inc[k + G]) : 0u;
+      const double w = (t >> 30) == 0 ? 1.0 : (t >> 30) == 1 ? 0.5 : 0.25;
+      const double wu = !two ? 0.0 : (u >> 30) == 0 ? 1.0 : (u >> 30) == 1 ? 0.5 : 0.25;
+      const double *src = ye + (int64_t)(t & 0x3fffffffu) * DIM;
+      const double *srcu = ye + (int64_t)(u & 0x3fffffffu) * DIM;
+      double a[DIM], b[DIM];
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        a[i] = COH ? g_ld<true>(src + i) : __ldg(src + i);
+        b[i] = two ? (COH ? g_ld<true>(srcu + i) : __ldg(srcu + i)) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) qv[i] = fma(wu, b[i], fma(w, a[i], qv[i]));
+    }
+  }
+#pragma unroll
+  for (int b = 1; b < G; b <<= 1)
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) qv[i] += __shfl_xor_sync(0xffffffffu, qv[i], b);
+  if (!live || l >= DIM || stopped) return;
+  // lane l < DIM: component l
+  double qc = qv[0];
+#pragma unroll
+  for (int i = 1; i < DIM; ++i) qc = (l == i) ? qv[i] : qc;
+  const int64_t d = n * DIM + l;
+  if (MODE == G_PLAIN) {
+    q_out[d] = qc;
+    return;
+  }
+  double *rec = zp + n * 2 * DIM;
+  const double di = di_p;
+  const double pk = fma(beta, po_p, z_p);
+  double zn = 0.0;
+  if (di != 0.0) {
+    x[d] = fma(alpha, pk, x_p);
+    const double rn = fma(-alpha, qc, r_p);
+    r[d] = rn;
+    zn = di * rn;
+    acc[0] = fma(rn, zn, acc[0]);
+    acc[1] = fma(rn, rn, acc[1]);
+  }
+  rec[l] = zn;
+  rec[DIM + l] = pk;
+}
+
+// Node pass with a group of 4 lanes per node: lane l sums incidences l, l+4,
+// ... of the node, an xor-shuffle tree completes q_n in every lane of the
+// group, and lane i < DIM updates component i of the node (record, x, r).
 template <int DIM, int MODE>
 __global__ void __launch_bounds__(256) k_node_pass_lanes(int64_t n_node, const int64_t *__restrict__ inc_ptr,
                                                          const uint32_t *__restrict__ inc, const double *__restrict__ ye,
@@ -713,69 +800,8 @@ __global__ void __launch_bounds__(256) k_node_pass_lanes(int64_t n_node, const i
   for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G - (threadIdx.x & 31) / G; base < n_node;
        base += groups) {
     const int64_t n = base + (threadIdx.x & 31) / G;
-    const bool live = n < n_node;
-    // node-side operands do not depend on q: load them before the incidence sum
-    const int64_t dpre = n * DIM + l;
-    double di_p = 0.0, r_p = 0.0, x_p = 0.0, z_p = 0.0, po_p = 0.0;
-    if (MODE == G_CG && live && l < DIM) {
-      di_p = __ldg(Dinv + dpre);
-      r_p = r[dpre];
-      x_p = x[dpre];
-      z_p = zp[n * 2 * DIM + l];
-      po_p = zp[n * 2 * DIM + DIM + l];
-    }
-    double qv[DIM];
-#pragma unroll
-    for (int i = 0; i < DIM; ++i) qv[i] = 0.0;
-    if (live) {
-      const int64_t k1 = inc_ptr[n + 1];
-      // two incidences per lane per round: both index and value loads in flight together
-      for (int64_t k = inc_ptr[n] + l; k < k1; k += 2 * G) {
-        const bool two = k + G < k1;
-        const uint32_t t = __ldg(&inc[k]);
-        const uint32_t u = two ? __ldg(&inc[k + G]) : 0u;
-        const double w = (t >> 30) == 0 ? 1.0 : (t >> 30) == 1 ? 0.5 : 0.25;
-        const double wu = !two ? 0.0 : (u >> 30) == 0 ? 1.0 : (u >> 30) == 1 ? 0.5 : 0.25;
-        const double *src = ye + (int64_t)(t & 0x3fffffffu) * DIM;
-        const double *srcu = ye + (int64_t)(u & 0x3fffffffu) * DIM;
-        double a[DIM], b[DIM];
-#pragma unroll
-        for (int i = 0; i < DIM; ++i) {
-          a[i] = __ldg(src + i);
-          b[i] = two ? __ldg(srcu + i) : 0.0;
-        }
-#pragma unroll
-        for (int i = 0; i < DIM; ++i) qv[i] = fma(wu, b[i], fma(w, a[i], qv[i]));
-      }
-    }
-#pragma unroll
-    for (int b = 1; b < G; b <<= 1)
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) qv[i] += __shfl_xor_sync(0xffffffffu, qv[i], b);
-    if (!live || l >= DIM || stopped) continue;
-    // lane l < DIM: component l
-    double qc = qv[0];
-#pragma unroll
-    for (int i = 1; i < DIM; ++i) qc = (l == i) ? qv[i] : qc;
-    const int64_t d = n * DIM + l;
-    if (MODE == G_PLAIN) {
-      q_out[d] = qc;
-      continue;
-    }
-    double *rec = zp + n * 2 * DIM;
-    const double di = di_p;
-    const double pk = fma(beta, po_p, z_p);
-    double zn = 0.0;
-    if (di != 0.0) {
-      x[d] = fma(alpha, pk, x_p);
-      const double rn = fma(-alpha, qc, r_p);
-      r[d] = rn;
-      zn = di * rn;
-      acc[0] = fma(rn, zn, acc[0]);
-      acc[1] = fma(rn, rn, acc[1]);
-    }
-    rec[l] = zn;
-    rec[DIM + l] = pk;
+    g_node_group<DIM, MODE, false>(n, n < n_node, l, inc_ptr, inc, ye, r, Dinv, zp, x, q_out, alpha, beta, stopped,
+                                   acc);
   }
   if (stopped) return;
   if (MODE == G_CG) {

@@ -554,13 +554,14 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
     int coop = 0;
     CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
     // (latency-bound small meshes only: on large ones the separate element and
-    // node kernels run at higher occupancy)
-    // 2D only: on 3D meshes the launched lane passes measured faster at every size
-    // (7.6k elements: 22.5 vs 39 us per iteration; 66k: 44 vs 60 us)
+    // node kernels run at higher occupancy).  2D only: on 3D meshes the
+    // launched lane passes measured faster at every size (7.6k elements: 22.6
+    // vs 39 us per iteration; 66k: 44 vs 60 us; a persistent variant built from
+    // the lane passes was also slower, 26.6 / 68.6 us: its grid barriers cost
+    // more than the two launches)
     if (coop && !std::getenv("TOMESH_NO_PERSISTENT") && d->dim == 2 && d->n_elem <= 100000) {
       int per_sm = 0;
-      if (d->dim == 2) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_general_persistent<2>, kBlock, 0));
-      else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_general_persistent<3>, kBlock, 0));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_general_persistent<2>, kBlock, 0));
       const int64_t need = (std::max<int64_t>(d->n_elem, d->n_node) + kBlock - 1) / kBlock;
       m->coop_blocks = (int)std::min<int64_t>(need, (int64_t)per_sm * kNumSMs);
       if (m->coop_blocks * 3 > kMaxPartialBlocks * 4) m->coop_blocks = kMaxPartialBlocks * 4 / 3;
@@ -857,7 +858,7 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
     MeshView V = m->view();
     void *args3[] = {&V, &m->s, &m->r, &m->dinv, &m->zp, &m->x, &m->ye, &m->inc_ptr, &m->inc, &m->K2, &m->KS,
                      &m->hmask, &m->S, &pa, &pb_, &m->hist};
-    const void *fn = m->dim == 2 ? (const void *)k_cg_general_persistent<2> : (const void *)k_cg_general_persistent<3>;
+    const void *fn = (const void *)k_cg_general_persistent<2>;   // 2D only (upload)
     CK(cudaLaunchCooperativeKernel(fn, dim3(m->coop_blocks), dim3(kBlock), args3, 0, st));
     m->last_launches++;
     if (prof) CK(cudaEventRecord(m->prof_ev[1], st));
