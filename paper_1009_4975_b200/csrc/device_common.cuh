@@ -31,6 +31,15 @@ struct CgScalars {
 
 enum { CNT_PQ = 0, CNT_U1 = 1, CNT_INIT = 2, CNT_MISC = 3, CNT_MISC2 = 4 };
 
+// Programmatic dependent launch (PDL): a kernel launched with the
+// programmatic-serialization attribute may be scheduled while its predecessor
+// in the stream is still draining; pdl_wait() blocks until the predecessor
+// has completed and its memory is visible (a no-op for a normal launch), and
+// pdl_release() lets the successor be scheduled as blocks of this kernel free
+// their SM resources.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -672,6 +672,8 @@ __global__ void __launch_bounds__(256) k_elem_pass_lanes(MeshView M, const doubl
                                                          const uint8_t *__restrict__ hmask, CgScalars *S,
                                                          double *partials) {
   constexpr int NC = 1 << DIM;
+  pdl_wait();
+  pdl_release();
   // the stop flags are read without a control dependency at the top (their
   // latency overlaps the gathers); a stopped iteration only skips the stores
   const bool stopped = MODE == G_CG && (__ldcg(&S->done) | __ldcg(&S->done_next));
@@ -790,6 +792,8 @@ __global__ void __launch_bounds__(256) k_node_pass_lanes(int64_t n_node, const i
                                                          double *__restrict__ q_out, double *partials, CgScalars *S,
                                                          double *hist) {
   constexpr int G = 4;
+  pdl_wait();
+  pdl_release();
   // stop flags without a control dependency at the top (see k_elem_pass_lanes)
   const bool stopped = MODE == G_CG && (__ldcg(&S->done) | __ldcg(&S->done_next));
   const double beta = MODE == G_CG ? __ldcg(&S->beta) : 0.0;

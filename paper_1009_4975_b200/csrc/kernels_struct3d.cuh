@@ -208,6 +208,8 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
            double *__restrict__ pnew, double *__restrict__ x, double *__restrict__ q,
            const __grid_constant__ K0HadSym H, CgScalars *S, double *partials, int kit, double rtol, double *hist) {
   constexpr bool CG = MODE == S3_CG;
+  pdl_wait();
+  pdl_release();
   if (CG && cg_stopped(S)) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   S3Smem<TYW> &sm = *reinterpret_cast<S3Smem<TYW> *>(smem_raw);

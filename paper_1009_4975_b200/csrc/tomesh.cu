@@ -699,6 +699,25 @@ int op_rhs(to_mesh *m, double *b_int, cudaStream_t st) {
 
 int s3_grid(const to_mesh *m) { return m->G.ntx * m->G.nty * m->G.nzs; }
 
+// Launch with programmatic stream serialization (PDL, see pdl_wait in
+// device_common.cuh) unless TOMESH_NO_PDL is set.
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  static const bool off = std::getenv("TOMESH_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+  return 0;
+}
+
 // out = C^T K C in (in vanishing on non-free DOFs), plain apply.  Structured:
 // `in` must be one of the handle's TMA-mapped vectors (x, pb[0], rb[*]).
 int op_apply(to_mesh *m, const double *in, double *out, cudaStream_t st) {
@@ -727,14 +746,18 @@ int op_cg_general(to_mesh *m, cudaStream_t st) {
   const int ge8 = std::min(grid_for(m->n_el * 8, kBlock, 8), m->ge_blocks);
   const int gn4 = std::min(grid_for(m->n_node * 4, kBlock, 8), m->gn_blocks);
   double *p = m->pb[0];
+  const double *no_po = nullptr;
+  double *no_q = nullptr;
   if (m->dim == 2) {
-    k_elem_pass_lanes<2, G_CG><<<ge4, kBlock, 0, st>>>(m->view(), m->s, m->zp, nullptr, m->ye, m->K2, m->KS, m->hmask, m->S, m->partials);
-    k_node_pass_lanes<2, G_CG><<<gn4, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, m->r, m->dinv, m->zp, m->x, nullptr,
-                                                m->partials, m->S, m->hist);
+    RC(launch_pdl(k_elem_pass_lanes<2, G_CG>, dim3(ge4), dim3(kBlock), 0, st, m->view(), m->s, m->zp, no_po, m->ye,
+                  m->K2, m->KS, m->hmask, m->S, m->partials));
+    RC(launch_pdl(k_node_pass_lanes<2, G_CG>, dim3(gn4), dim3(kBlock), 0, st, m->n_node, m->inc_ptr, m->inc, m->ye,
+                  m->r, m->dinv, m->zp, m->x, no_q, m->partials, m->S, m->hist));
   } else {
-    k_elem_pass_lanes<3, G_CG><<<ge8, kBlock, 0, st>>>(m->view(), m->s, m->zp, nullptr, m->ye, m->K2, m->KS, m->hmask, m->S, m->partials);
-    k_node_pass_lanes<3, G_CG><<<gn4, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, m->r, m->dinv, m->zp, m->x, nullptr,
-                                                m->partials, m->S, m->hist);
+    RC(launch_pdl(k_elem_pass_lanes<3, G_CG>, dim3(ge8), dim3(kBlock), 0, st, m->view(), m->s, m->zp, no_po, m->ye,
+                  m->K2, m->KS, m->hmask, m->S, m->partials));
+    RC(launch_pdl(k_node_pass_lanes<3, G_CG>, dim3(gn4), dim3(kBlock), 0, st, m->n_node, m->inc_ptr, m->inc, m->ye,
+                  m->r, m->dinv, m->zp, m->x, no_q, m->partials, m->S, m->hist));
   }
   m->last_launches += 2;
   return 0;
@@ -749,8 +772,9 @@ int op_cg_s3(to_mesh *m, int k, double rtol, cudaStream_t st) {
   M.p = m->tm_pb[o];
   M.d = m->tm_dn;
   dim3 block(32, kS3TYW);
-  k_apply_s3<kS3TYW, S3_CG><<<s3_grid(m), block, sizeof(S3Smem<kS3TYW>), st>>>(
-      m->G, m->s, M, m->rb[w], m->pb[w], m->x, m->qb[w], m->KS, m->S, m->partials, k, rtol, m->hist);
+  RC(launch_pdl(k_apply_s3<kS3TYW, S3_CG>, dim3(s3_grid(m)), block, sizeof(S3Smem<kS3TYW>), st, m->G,
+                (const double *)m->s, M, m->rb[w], m->pb[w], m->x, m->qb[w], m->KS, m->S, m->partials, k, rtol,
+                m->hist));
   m->last_launches++;
   return 0;
 }
