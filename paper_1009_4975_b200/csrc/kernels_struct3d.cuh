@@ -61,6 +61,7 @@ struct GridView {
   int RS;                // doubles per node row in the internal layout (3 NXP)
   int ntx, nty, nzs;     // CTA tiles in x, y and z segments
   int zlen;              // node planes per z segment
+  const int4 *plan;      // nullptr, or per CTA {x tile, y tile, k_lo, k_hi} (host-planned waves)
 };
 
 constexpr int kS3PadFront = 16;    // doubles (or nodes) before an internal vector
@@ -218,14 +219,23 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
   // x tiles fastest: the CTAs resident together cover whole node rows of the
   // same z range, so their TMA boxes (and stores) of a plane are adjacent in
   // memory (DRAM page locality)
-  int bid = blockIdx.x;
-  const int tx_t = bid % G.ntx;
-  bid /= G.ntx;
-  const int ty_t = bid % G.nty;
-  const int zs = bid / G.nty;
+  int tx_t, ty_t, k_lo, k_hi;
+  if (G.plan) {
+    const int4 pl = G.plan[blockIdx.x];
+    tx_t = pl.x;
+    ty_t = pl.y;
+    k_lo = pl.z;
+    k_hi = pl.w;
+  } else {
+    int bid = blockIdx.x;
+    tx_t = bid % G.ntx;
+    bid /= G.ntx;
+    ty_t = bid % G.nty;
+    const int zs = bid / G.nty;
+    k_lo = zs * G.zlen;
+    k_hi = min(G.NZ, k_lo + G.zlen);
+  }
   const int i0 = tx_t * 31, j0 = ty_t * (TYW - 1);
-  const int k_lo = zs * G.zlen;
-  const int k_hi = min(G.NZ, k_lo + G.zlen);
   const int off = (i0 - 1) & 1;                         // DOF window starts on an even double
   const int noff = (i0 - 1) & 1;                        // node window starts on an even node
   const int ei = i0 - 1 + tx, ej = j0 - 1 + ty;        // this thread's element column / node column

@@ -110,6 +110,7 @@ struct to_mesh {
   uint8_t *free_lex = nullptr;         // per DOF, internal order
   uint8_t *free_node_lex = nullptr;    // per node, internal order
   int64_t n_int_nodes = 0;
+  int s3_ncta = 0;                     // > 0: CTAs of the host-planned K1 grid (G.plan)
   double k0d = 0.0, h_struct = 1.0;
   // TMA tensor maps of the internal vectors (structured path): [NZ][NY][RS] doubles
   // (boxes of TYW+1 rows x 100 doubles) and the node array Dinv [NZ][NY][NXP].
@@ -301,6 +302,63 @@ int make_tensor_map(CUtensorMap *map, const double *base, uint64_t d0, uint64_t 
 
 // Uniform 3D meshes (one level, leaves tiling a box, no hanging nodes) use the
 // structured fast path: lexicographic internal vectors, implicit connectivity.
+// Host-planned K1 grid: z segments of two lengths by x tile column so that
+// the CTA count fills whole waves of resident slots; long CTAs are dispatched
+// first, so each slot pairs a long with a short one.  Chosen only if the
+// simulated in-order list schedule beats the uniform segmentation.
+int plan_s3(to_mesh *m, cudaStream_t st) {
+  const GridView &G = m->G;
+  const int slots = kNumSMs * kS3CtasPerSM, over = 3;   // ~3 planes of start-up per CTA
+  auto makespan = [&](const std::vector<int> &len) {
+    std::vector<int64_t> fin(slots, 0);
+    int64_t t_max = 0;
+    for (size_t c = 0; c < len.size(); ++c) {
+      auto it = std::min_element(fin.begin(), fin.end());
+      *it += len[c] + over;
+      t_max = std::max(t_max, *it);
+    }
+    return t_max;
+  };
+  std::vector<int> uni;
+  for (int z = 0; z < G.nzs; ++z)
+    for (int t = 0; t < G.ntx * G.nty; ++t) uni.push_back(std::min(G.NZ, (z + 1) * G.zlen) - z * G.zlen);
+  int64_t best = makespan(uni);
+  std::vector<int4> best_plan;
+  const int tiles = G.ntx * G.nty;
+  for (int W = 1; W <= 6; ++W) {
+    const int T = W * slots, n_lo = T / tiles;
+    if (n_lo < 1) continue;
+    int a = (T - tiles * n_lo) / G.nty;          // columns with n_lo + 1 segments
+    a = std::min(a, G.ntx);
+    std::vector<int4> plan;
+    std::vector<int> len;
+    for (int pass = 0; pass < 2; ++pass) {         // long CTAs (n_lo segments) first
+      for (int seg = 0; seg < n_lo + 1; ++seg)
+        for (int ty = 0; ty < G.nty; ++ty)
+          for (int tx = 0; tx < G.ntx; ++tx) {
+            const int ns = tx < a ? n_lo + 1 : n_lo;
+            if ((pass == 0) != (ns == n_lo) || seg >= ns) continue;
+            const int zl = (G.NZ + ns - 1) / ns;
+            const int lo = seg * zl, hi = std::min(G.NZ, lo + zl);
+            if (lo >= hi) continue;
+            plan.push_back(make_int4(tx, ty, lo, hi));
+            len.push_back(hi - lo);
+          }
+    }
+    const int64_t ms = makespan(len);
+    if (ms < best) {
+      best = ms;
+      best_plan = plan;
+    }
+  }
+  if (best_plan.empty()) return 0;
+  int4 *d = nullptr;
+  RC(upload_array(m, &d, best_plan.data(), best_plan.size(), st));
+  m->G.plan = d;
+  m->s3_ncta = (int)best_plan.size();
+  return 0;
+}
+
 int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof, cudaStream_t st, to_mesh *m) {
   m->structured = false;
   if (d->dim != 3 || d->n_hang != 0 || m->force_general) return 0;
@@ -314,7 +372,7 @@ int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof
   if (ext[0] * ext[1] * ext[2] != d->n_elem) return 0;
   if ((ext[0] + 1) * (ext[1] + 1) * (ext[2] + 1) != d->n_node) return 0;
   if (ext[0] + 1 >= (1 << 30) / 4) return 0;
-  GridView G;
+  GridView G{};
   G.EX = (int)ext[0]; G.EY = (int)ext[1]; G.EZ = (int)ext[2];
   G.NX = G.EX + 1; G.NY = G.EY + 1; G.NZ = G.EZ + 1;
   G.NXP = G.NX + (G.NX & 1);              // even node count per row: node pairs never straddle rows
@@ -375,6 +433,7 @@ int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof
   const int64_t grid = (int64_t)G.ntx * G.nty * G.nzs;
   if (grid > kMaxPartialBlocks) RC(m->alloc(&m->partials, (size_t)grid * 4));
   m->G = G;
+  if (!std::getenv("TOMESH_S3_NO_PLAN")) RC(plan_s3(m, st));
   m->k0d = m->K3.K[0];
   m->h_struct = m->hL * (double)sz;
   m->structured = true;
@@ -697,7 +756,7 @@ int op_rhs(to_mesh *m, double *b_int, cudaStream_t st) {
   return check_launch();
 }
 
-int s3_grid(const to_mesh *m) { return m->G.ntx * m->G.nty * m->G.nzs; }
+int s3_grid(const to_mesh *m) { return m->s3_ncta > 0 ? m->s3_ncta : m->G.ntx * m->G.nty * m->G.nzs; }
 
 // Launch with programmatic stream serialization (PDL, see pdl_wait in
 // device_common.cuh) unless TOMESH_NO_PDL is set.
