@@ -26,7 +26,7 @@ using namespace tomesh;
 
 namespace tomesh {
 #ifndef TOMESH_S3_TYW
-#define TOMESH_S3_TYW 8   // the validated value (8 and 16 pass the parity tests; 4 does not)
+#define TOMESH_S3_TYW 8   // the value the tests validate (16 ran but slower; 4 fails on c5)
 #endif
 constexpr int kS3TYW = TOMESH_S3_TYW;   // warps per CTA (node rows + 1) of the structured H8 kernel
 constexpr int kS3CtasPerSM = kS3TYW <= 8 ? 2 : 1;
