@@ -28,7 +28,17 @@ class AmrRun:
 
 def optimize_amr(problem, volfrac, n_steps, penal0=1.0, penal_max=3.0, penal_step=0.5, stage_steps=30,
                  rho_s=0.5, min_steps=5, max_steps=10, change_tol=0.01, rtol=1e-10, max_iter=20000,
-                 device=0, x0=None) -> AmrRun:
+                 device=0, x0=None, mode="dynamic", stop_on_converge=False, level_steps=150) -> AmrRun:
+    """mode "dynamic": the paper's strategy (§4).  mode "static": the
+    refine-only baseline the paper argues against (Costa/Stainko, PAPER.md:
+    754-790): optimise to convergence at p_max, refine the marked elements
+    (no derefinement; after at most level_steps steps on a level if it does not
+    converge), repeat until nothing is refined.  stop_on_converge:
+    end when the design change is < change_tol at p_max and the adaptation
+    that follows would not change the mesh."""
+    static = mode == "static"
+    if mode not in ("dynamic", "static"):
+        raise ValueError("mode must be 'dynamic' or 'static'")
     import torch
     dev = torch.device("cuda", device)
     host = prepare(problem, keep_handle=True)
@@ -39,23 +49,34 @@ def optimize_amr(problem, volfrac, n_steps, penal0=1.0, penal_max=3.0, penal_ste
     done = 0
     while done < n_steps:
         u = torch.zeros(host.n_dof, dtype=torch.float64, device=dev)
-        _, hist = mesh.to_optimize(x, u, n_steps - done, volfrac, penal0=penal0, penal_max=penal_max,
+        n_call = min(n_steps - done, level_steps) if static else n_steps - done
+        _, hist = mesh.to_optimize(x, u, n_call, volfrac, penal0=penal0, penal_max=penal_max,
                                    penal_step=penal_step, stage_steps=stage_steps, change_tol=change_tol,
-                                   rtol=rtol, max_iter=max_iter, adapt_min_steps=min_steps,
-                                   adapt_max_steps=max_steps, state=state)
+                                   rtol=rtol, max_iter=max_iter, adapt_min_steps=0 if static else min_steps,
+                                   adapt_max_steps=0 if static else max_steps,
+                                   stop_on_converge=stop_on_converge or static, state=state)
         for h in hist:
             h["n_elem"] = host.n_el
+            h["n_dof"] = host.n_dof
             h["adapted"] = False
         run.steps.extend(hist)
         done += len(hist)
-        if not state.adapt_due:
-            break
+        converged = bool(state.converged)
+        if done >= n_steps or (not static and not state.adapt_due and not converged):
+            break                                        # step budget used up
         t0 = time.perf_counter()
         marks = torch.empty(host.n_el, dtype=torch.int8, device=dev)
         mesh.to_amr_mark(x, marks, rho_s)
         mk, xh = marks.cpu().numpy(), x.cpu().numpy()
+        if static:
+            mk[mk < 0] = 0                               # refinement only
         t1 = time.perf_counter()
         ad = tomesh_host_adapt(host, mk, xh)
+        if ad.n_refined == 0 and ad.n_groups == 0:
+            if converged:
+                break                                    # converged on a mesh the strategy keeps
+            if static:
+                continue                                 # finest level reached: keep optimising
         new_host = rebuild(problem, ad)
         xn = tomesh_host_transfer(new_host, ad)
         t2 = time.perf_counter()
