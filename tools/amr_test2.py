@@ -11,7 +11,7 @@ Prints one JSON line: total device-side wall time, CG iterations, element /
 DOF counts of both runs, the compliance of each, and the design difference D
 of Eq. 10 between the final designs on the fine lattice.
 
-    python tools/amr_test2.py [steps]
+    python tools/amr_test2.py [steps] [rmin] [change_tol]   (change_tol > 0: run to convergence at p = 3)
 """
 import json
 import os
@@ -29,14 +29,14 @@ from inputs import DensitySpec, make_problem, uniform_leaves
 NX, NY, NZ = 128, 32, 32
 
 
-def problem(amr):
+def problem(amr, rmin=1.5):
     base = (NX // 2, NY // 2, NZ // 2) if amr else (NX, NY, NZ)
     L = 1 if amr else 0
     return make_problem("test2_cantilever3d_" + ("amr" if amr else "uniform"), 3, base, L=L,
                         h0=2.0 if amr else 1.0, leaves=uniform_leaves(3, base, L, 0),
                         density=DensitySpec("const", value=0.25),
                         fixed=[((0, 0, 0), (0, NY, NZ), 0b111)],
-                        loads=[("line", (NX, 0, 0), (NX, 0, NZ), (0.0, -1.0, 0.0))], rmin=1.5, rtol=1e-8)
+                        loads=[("line", (NX, 0, 0), (NX, 0, NZ), (0.0, -1.0, 0.0))], rmin=rmin, rtol=1e-8)
 
 
 def raster(host, x):
@@ -51,34 +51,41 @@ def raster(host, x):
 
 def main():
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 60
+    rmin = float(sys.argv[2]) if len(sys.argv) > 2 else 1.5
+    tol = float(sys.argv[3]) if len(sys.argv) > 3 else 0.0
+    conv = tol > 0
     volfrac, stage = 0.25, 12
     # uniform fine mesh
-    pu = problem(False)
+    pu = problem(False, rmin)
     hu = pb.prepare(pu)
     mu = pb.Mesh(hu, E0=pu.E0, Emin=pu.Emin, nu=pu.nu, rmin=pu.rmin)
     xu = torch.full((hu.n_el,), volfrac, dtype=torch.float64, device="cuda")
     uu = torch.zeros(hu.n_dof, dtype=torch.float64, device="cuda")
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    _, hist_u = mu.to_optimize(xu, uu, steps, volfrac, stage_steps=stage, rtol=1e-8)
+    _, hist_u = mu.to_optimize(xu, uu, steps, volfrac, stage_steps=stage, rtol=1e-8, stop_on_converge=conv,
+                               change_tol=tol if conv else 0.01)
     torch.cuda.synchronize()
     wall_u = time.perf_counter() - t0
     # dynamic AMR
-    pa = problem(True)
+    pa = problem(True, rmin)
     t0 = time.perf_counter()
-    run = pb.amr.optimize_amr(pa, volfrac, steps, stage_steps=stage, rtol=1e-8)
+    run = pb.amr.optimize_amr(pa, volfrac, steps, stage_steps=stage, rtol=1e-8, stop_on_converge=conv,
+                              change_tol=tol if conv else 0.01)
     torch.cuda.synchronize()
     wall_a = time.perf_counter() - t0
     ru = raster(hu, xu.cpu().numpy())
     ra = raster(run.host, run.x.cpu().numpy())
     D = float(np.abs(ru - ra).sum() / ru.sum())
     line = {
-        "workload": "test2_cantilever3d_128x32x32", "steps": steps, "volfrac": volfrac,
-        "uniform": {"n_elem": hu.n_el, "n_dof": hu.n_dof, "wall_s": wall_u,
+        "workload": "test2_cantilever3d_128x32x32", "step_cap": steps, "rmin": rmin, "change_tol": tol,
+        "volfrac": volfrac,
+        "uniform": {"steps": len(hist_u), "n_elem": hu.n_el, "n_dof": hu.n_dof, "wall_s": wall_u,
                     "solve_ms": float(sum(h["solve_ms"] for h in hist_u)),
                     "cg_iters": int(sum(h["cg_iters"] for h in hist_u)),
                     "compliance_last": hist_u[-1]["compliance"], "structured": mu.info()["structured"]},
-        "amr": {"n_elem_first_last": [run.steps[0]["n_elem"], run.host.n_el], "n_dof_last": run.host.n_dof,
+        "amr": {"steps": len(run.steps), "n_elem_first_last": [run.steps[0]["n_elem"], run.host.n_el],
+                "n_dof_last": run.host.n_dof,
                 "wall_s": wall_a, "solve_ms": float(sum(h["solve_ms"] for h in run.steps)),
                 "cg_iters": int(sum(h["cg_iters"] for h in run.steps)),
                 "compliance_last": run.steps[-1]["compliance"], "adaptations": len(run.adaptations),
