@@ -68,3 +68,19 @@ def test_dynamic_amr_loop_parity(dim):
     assert np.array_equal(run.host.elem_level, om.elem_level) and np.array_equal(run.host.elem_anchor,
                                                                                   om.elem_anchor)
     np.testing.assert_allclose(host(run.x), xo, rtol=1e-8, atol=1e-12)
+
+
+def test_static_refine_only_and_stop_on_converge():
+    """The refine-only baseline never derefines and only adds levels; with
+    stop_on_converge the dynamic run ends converged at p_max (or at the cap)."""
+    prob = cantilever2d((8, 4), L=2, leaves=uniform_leaves(2, (8, 4), 2, 0), rmin=1.2)
+    run = pb.amr.optimize_amr(prob, 0.5, 120, mode="static", level_steps=30, rtol=1e-10)
+    assert run.adaptations and all(a["n_groups"] == 0 for a in run.adaptations)
+    counts = [a["n_elem_after"] for a in run.adaptations]
+    assert all(b >= a for a, b in zip(counts, counts[1:]))
+    assert all(abs(s["volume"] - 0.5) <= 1e-10 for s in run.steps)
+    run = pb.amr.optimize_amr(prob, 0.5, 300, stop_on_converge=True, change_tol=0.02, rtol=1e-10)
+    last = run.steps[-1]
+    assert len(run.steps) == 300 or (last["penal"] == 3.0 and last["change"] < 0.02)
+    with pytest.raises(ValueError):
+        pb.amr.optimize_amr(prob, 0.5, 5, mode="bogus")
