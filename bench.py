@@ -288,6 +288,13 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     loop = m.profile()
 
+    # ---- the full solve time of the metric: one solve to the config's
+    # tolerance from zero, device time of the call (setup + iterations + recovery)
+    u_full = torch.zeros_like(u)
+    st_full = m.tosolve_cg(prob.penal, x, u_full, rtol=prob.rtol, max_iter=200000, stream=stream)
+    full_line = {"rtol": prob.rtol, "iters": st_full.iters, "ms": st_full.ms, "relres_true": st_full.relres_true,
+                 "status": st_full.status}
+
     # ---- §8(f) row 1: the OC design update on this step's filtered sensitivities ------
     # (untimed for the headline; the library's own CUDA events per call)
     xo = torch.empty_like(dc)
@@ -354,6 +361,7 @@ def run_ours(args):
                 "iteration": {"ms": k1_ms + k2_ms, "bytes": kb["k1"] + kb["k2"],
                               "gbs": (kb["k1"] + kb["k2"]) / ((k1_ms + k2_ms) / 1000.0) / 1e9},
             },
+            "solve_to_rtol": full_line,
             "oc_update": oc_line,
             "cpu_baseline": cpu,
             "clocks": clk,
