@@ -31,6 +31,9 @@ struct CgScalars {
 
 enum { CNT_PQ = 0, CNT_U1 = 1, CNT_INIT = 2, CNT_MISC = 3, CNT_MISC2 = 4 };
 
+#define GRID_STRIDE(i, n) \
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
 // Programmatic dependent launch (PDL): a kernel launched with the
 // programmatic-serialization attribute may be scheduled while its predecessor
 // in the stream is still draining; pdl_wait() blocks until the predecessor

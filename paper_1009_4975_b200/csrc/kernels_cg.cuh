@@ -10,8 +10,6 @@
 
 namespace tomesh {
 
-#define GRID_STRIDE(i, n) \
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
 // Scalars after the initial residual: rho0 = r0.z0, rr0, thresholds.
 __device__ __forceinline__ void cg_init_scalars(CgScalars *S, double rho, double rr, double rtol) {

@@ -14,23 +14,10 @@
 #include "device_common.cuh"
 #include "element.h"
 #include "kernels_cg.cuh"
+#include "tomesh_types.cuh"
 
 namespace tomesh {
 
-struct MeshView {
-  int64_t n_el, n_node;
-  const int32_t *elem_node;     // [n_el][NC]
-  const int8_t *elem_level;
-  const int32_t *elem_anchor;   // [n_el][DIM]
-  const int32_t *node_hang;     // [n_node] index into hang rows or -1
-  const int32_t *hang_ptr, *hang_parent;
-  const double *hang_weight;
-  const int32_t *child_ptr, *child_hang;  // transpose: parent node -> hanging children
-  const double *child_weight;
-  const uint8_t *free_dof;      // [n_dof] 1 = neither hanging nor fixed
-  int L;
-  double hL;
-};
 
 template <int DIM>
 __global__ void k_simp(int64_t n, const double *__restrict__ x, const int8_t *__restrict__ lev,

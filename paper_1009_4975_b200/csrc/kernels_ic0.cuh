@@ -20,17 +20,10 @@
 //                    keeps the plain rescaling.
 #pragma once
 #include "device_common.cuh"
+#include "tomesh_types.cuh"
 
 namespace tomesh {
 
-struct Ic0View {
-  int64_t n, nnz;
-  const int64_t *ptr;      // [n+1] lower CSR, columns ascending, diagonal last
-  const int32_t *col;      // [nnz]
-  const int32_t *row;      // [nnz]
-  const int64_t *cptr;     // [nnz+1] contributions of each nonzero
-  const uint64_t *contrib; // element << 16 | (a * ND + b) << 3 | log2(1/w)
-};
 
 template <int DIM>
 __global__ void k_ic0_assemble(Ic0View V, const double *__restrict__ s, const double *__restrict__ msc,

@@ -16,17 +16,10 @@
 // (mr_givens).  Deterministic: last-block-done reductions in block order.
 #pragma once
 #include "device_common.cuh"
+#include "tomesh_types.cuh"
 
 namespace tomesh {
 
-struct MrScalars {
-  double gamma, gamma_old, delta, c, c_old, s, s_old, eta, eta0, thresh;
-  double a1, a2, a3, cn, eta_prev;      // w / x~ update coefficients of the last completed step
-  double bnorm2, tmp;
-  int32_t iter, wx_done, max_iter, done, status, pad;
-  uint32_t counter[6];
-};
-enum { MRC_GAMMA = 0, MRC_DELTA = 1, MRC_WX = 2, MRC_MISC = 3 };
 
 // Givens step after gamma_{j+1}^2 is known (last block only).
 __device__ __forceinline__ void mr_givens(MrScalars *S, double g2) {

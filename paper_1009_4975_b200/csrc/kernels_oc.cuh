@@ -20,18 +20,10 @@
 // lies within rounding of the target.
 #pragma once
 #include "device_common.cuh"
+#include "tomesh_types.cuh"
 
 namespace tomesh {
 
-struct OcState {
-  double lam, volume_abs, change;
-  int32_t steps, state;   // state: 0 active, 1 inactive, 2 infeasible, -5 NaN
-  int32_t passes;         // passes over the elements (grid-wide reductions)
-  // grid-wide reduction words; zeroed by the host before every launch
-  uint32_t arrive, flag;
-  unsigned long long change_bits;   // max |x_new - x| as the bits of a non-negative double
-  double tot[2][8];
-};
 
 struct OcArgs {
   int64_t n;

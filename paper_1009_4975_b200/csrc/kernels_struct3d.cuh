@@ -51,24 +51,11 @@
 #include "element.h"
 #include "kernels_cg.cuh"
 #include "kernels_general.cuh"
+#include "tomesh_types.cuh"
 
 namespace tomesh {
 
-struct GridView {
-  int EX, EY, EZ;        // elements per axis
-  int NX, NY, NZ;        // nodes per axis
-  int NXP;               // nodes per internal row (NX rounded up to even)
-  int RS;                // doubles per node row in the internal layout (3 NXP)
-  int ntx, nty, nzs;     // CTA tiles in x, y and z segments
-  int zlen;              // node planes per z segment
-  const int4 *plan;      // nullptr, or per CTA {x tile, y tile, k_lo, k_hi} (host-planned waves)
-};
 
-constexpr int kS3PadFront = 16;    // doubles (or nodes) before an internal vector
-constexpr int kS3PadBack = 128;    // doubles (or nodes) after it
-constexpr int kS3RowD = 100;       // doubles staged per node row: 33 nodes + alignment (800 B)
-constexpr int kS3RowN = 34;        // node values staged per row: 33 + alignment (272 B)
-constexpr int kS3NBuf = 2;         // staging depth: plane P is issued ~1.5 layers before it is formed
 
 __device__ __forceinline__ int64_t s3_row(const GridView &G, int j, int k) {
   return ((int64_t)j + (int64_t)G.NY * k) * G.RS;
@@ -503,10 +490,6 @@ __global__ void __launch_bounds__(512) k_final_s3(int n, const double *__restric
 // box boundary; V_d = h^3 for every element.  Two passes: the filtered
 // quantity (x in for SENS, in for DENS) is scattered to lexicographic order,
 // then each element (canonical order) sums its stencil.
-struct S3FilterOffset {
-  int di, dj, dk;
-  double w;          // H * V
-};
 
 __global__ void k_filter_s3_scatter(int64_t n, const int32_t *__restrict__ perm_el, int mode,
                                     const double *__restrict__ x, const double *__restrict__ in,

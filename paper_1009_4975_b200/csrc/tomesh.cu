@@ -1,208 +1,13 @@
 // libtomesh — C ABI entry points (include/tomesh.h) and the host side of the
-// device path: validation, upload, the PCG driver loop, sensitivities, filter.
-#include <cuda.h>
-#include <cudaTypedefs.h>
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <cmath>
-#include <cstdlib>
-#include <cstring>
-#include <memory>
-#include <vector>
-
-#include "../../include/tomesh.h"
-#include "common.h"
-#include "device_common.cuh"
-#include "element.h"
+// device path: validation, upload, the PCG driver loop, sensitivities, filter,
+// AMR marks and the operator-level calls.  MINRES / IC(0): tomesh_minres.cu;
+// OC update and the Fig. 1 loop: tomesh_opt.cu.
+#include "tomesh_impl.cuh"
 #include "kernels_cg.cuh"
 #include "kernels_general.cuh"
-#include "kernels_oc.cuh"
 #include "kernels_struct3d.cuh"
-#include "kernels_minres.cuh"
-#include "kernels_ic0.cuh"
 
 using namespace tomesh;
-
-namespace tomesh {
-#ifndef TOMESH_S3_TYW
-#define TOMESH_S3_TYW 8   // the value the tests validate (16 ran but slower; 4 fails on c5)
-#endif
-constexpr int kS3TYW = TOMESH_S3_TYW;   // warps per CTA (node rows + 1) of the structured H8 kernel
-constexpr int kS3CtasPerSM = kS3TYW <= 8 ? 2 : 1;
-}
-
-namespace {
-
-struct DevBuf {
-  void *p = nullptr;
-  size_t bytes = 0;
-};
-
-}  // namespace
-
-struct to_mesh {
-  int dim = 0, L = 0, device = 0;
-  double h0 = 1.0, hL = 1.0, E0 = 1.0, Emin = 1e-9, nu = 0.3, rmin = 0.0;
-  int64_t n_el = 0, n_node = 0, n_dof = 0, n_hang = 0, n_fixed = 0, filt_nnz = 0;
-  int64_t n_int = 0;   // length of the internal CG vectors (n_dof, or padded rows when structured)
-  std::vector<DevBuf> bufs;
-  int64_t dev_bytes = 0;
-  // mesh
-  int32_t *elem_node = nullptr, *elem_anchor = nullptr, *node_hang = nullptr;
-  int8_t *elem_level = nullptr;
-  int32_t *hang_ptr = nullptr, *hang_parent = nullptr, *child_ptr = nullptr, *child_hang = nullptr;
-  double *hang_weight = nullptr, *child_weight = nullptr, *load = nullptr;
-  uint8_t *free_dof = nullptr;
-  int64_t *filt_ptr = nullptr;
-  S3FilterOffset *foffs = nullptr;     // structured filter stencil
-  int n_foffs = 0;
-  double *ftmp = nullptr;              // structured filter: lexicographic temporary
-  int64_t *inc_ptr = nullptr;          // general path: node -> (element, corner, weight) incidences
-  uint32_t *inc = nullptr;
-  double *ye = nullptr;                // general path: element vectors s_e K0 C_e p
-  uint8_t *hmask = nullptr;            // general path: bit c = corner c of the element is hanging
-  double *zp = nullptr;                // general path: node records {Dinv r, p}
-  int coop_blocks = 0;                 // general path: grid of the persistent cooperative solver (0 = off)
-  int ge_blocks = 0, gn_blocks = 0;    // general path: one resident wave of the element / node pass
-  int32_t *filt_idx = nullptr;
-  // OC update (allocated on first use)
-  double *oc_a = nullptr, *oc_part = nullptr;
-  OcState *oc_state = nullptr;
-  OcState *oc_state_host = nullptr;   // pinned mirror
-  double *opt_dc = nullptr, *opt_dcf = nullptr;   // to_optimize: raw and filtered sensitivities
-  // MINRES (tosolve_minres), allocated on first use, internal order with pads
-  double *mr_v[3] = {nullptr, nullptr, nullptr}, *mr_w[3] = {nullptr, nullptr, nullptr};
-  double *mr_zn[2] = {nullptr, nullptr}, *mr_z[2] = {nullptr, nullptr};
-  double *mr_xt = nullptr, *mr_msc = nullptr, *mr_az = nullptr, *mr_t = nullptr;
-  MrScalars *MS = nullptr, *MS_host = nullptr;
-  // IC(0) of the rescaled matrix (general path), built on first use
-  bool ic_ready = false;
-  Ic0View IC{};
-  double *ic_kt = nullptr, *ic_L = nullptr, *ic_K0 = nullptr, *ic_y = nullptr;
-  int64_t *ic_lvl_ptr = nullptr, *ic_blvl_ptr = nullptr, *ic_ut_ptr = nullptr, *ic_ut_pos = nullptr;
-  int32_t *ic_lvl_rows = nullptr, *ic_blvl_rows = nullptr, *ic_ut_row = nullptr;
-  std::vector<int64_t> ic_lvl_host;   // level boundaries (host) for the per-level factor launches
-  int ic_nlvl = 0, ic_nblvl = 0;
-  int *ic_fail = nullptr;
-  double ic_setup_ms = 0.0;
-  int oc_blocks = 0;
-  double vol_total = 0.0;             // sum_e V_e (exact dyadic sum, host)
-  // workspace
-  double *s = nullptr, *x = nullptr, *r = nullptr, *q = nullptr, *dinv = nullptr, *D = nullptr;
-  double *pb[2] = {nullptr, nullptr};   // p ping-pong: iteration k writes pb[k & 1]
-  double *rb[2] = {nullptr, nullptr};   // structured: r ping-pong (rb[0] = r)
-  double *qb[2] = {nullptr, nullptr};   // structured: q ping-pong (qb[0] = q)
-  double *dn = nullptr;                 // structured: Dinv per node (internal node order)
-  double *partials = nullptr, *hist = nullptr;
-  int32_t hist_len = 0, hist_cap = 0;
-  CgScalars *S = nullptr;
-  CgScalars *S_host = nullptr;   // pinned mirror
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  K0Dense2 K2{};
-  K0Dense3 K3{};
-  K0Had3 KH{};
-  K0HadSym KS{};
-  // structured fast path (uniform H8 box)
-  bool structured = false, force_general = false;
-  GridView G{};
-  int32_t *perm_el = nullptr, *perm_node = nullptr;
-  uint8_t *free_lex = nullptr;         // per DOF, internal order
-  uint8_t *free_node_lex = nullptr;    // per node, internal order
-  int64_t n_int_nodes = 0;
-  int s3_ncta = 0;                     // > 0: CTAs of the host-planned K1 grid (G.plan)
-  double k0d = 0.0, h_struct = 1.0;
-  // TMA tensor maps of the internal vectors (structured path): [NZ][NY][RS] doubles
-  // (boxes of TYW+1 rows x 100 doubles) and the node array Dinv [NZ][NY][NXP].
-  CUtensorMap tm_x, tm_rb[2], tm_qb[2], tm_pb[2], tm_dn;
-  int last_launches = 0;
-  int matvec_variant = 0;
-  int64_t launches_total = 0;          // every kernel launched on this handle
-  std::vector<cudaEvent_t> prof_ev;   // TO_PROFILE: 5 events per iteration
-  double prof_ms[6] = {0, 0, 0, 0, 0, 0};
-  cudaEvent_t loop_ev[2] = {nullptr, nullptr};   // TO_PROFILE_LOOP: around the iteration launches
-
-  MeshView view() const {
-    MeshView M;
-    M.n_el = n_el;
-    M.n_node = n_node;
-    M.elem_node = elem_node;
-    M.elem_level = elem_level;
-    M.elem_anchor = elem_anchor;
-    M.node_hang = node_hang;
-    M.hang_ptr = hang_ptr;
-    M.hang_parent = hang_parent;
-    M.hang_weight = hang_weight;
-    M.child_ptr = child_ptr;
-    M.child_hang = child_hang;
-    M.child_weight = child_weight;
-    M.free_dof = free_dof;
-    M.L = L;
-    M.hL = hL;
-    return M;
-  }
-
-  template <typename T>
-  int alloc(T **ptr, size_t count) {
-    *ptr = nullptr;
-    if (count == 0) count = 1;
-    void *d = nullptr;
-    if (cudaMalloc(&d, count * sizeof(T)) != cudaSuccess) {
-      cudaGetLastError();
-      set_error("cudaMalloc of %zu bytes failed", count * sizeof(T));
-      return TO_ENOMEM;
-    }
-    bufs.push_back({d, count * sizeof(T)});
-    dev_bytes += (int64_t)(count * sizeof(T));
-    *ptr = (T *)d;
-    return 0;
-  }
-  ~to_mesh() {
-    for (auto &b : bufs) cudaFree(b.p);
-    if (S_host) cudaFreeHost(S_host);
-    if (oc_state_host) cudaFreeHost(oc_state_host);
-    if (MS_host) cudaFreeHost(MS_host);
-    if (ev0) cudaEventDestroy(ev0);
-    if (ev1) cudaEventDestroy(ev1);
-    for (auto e : prof_ev) cudaEventDestroy(e);
-    for (auto e : loop_ev)
-      if (e) cudaEventDestroy(e);
-  }
-};
-
-namespace {
-
-#define CK(call)                                                                 \
-  do {                                                                           \
-    cudaError_t _e = (call);                                                     \
-    if (_e != cudaSuccess) {                                                     \
-      set_error("%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, __LINE__); \
-      return TO_ECUDA;                                                           \
-    }                                                                            \
-  } while (0)
-
-#define RC(call)                 \
-  do {                           \
-    int _rc = (call);            \
-    if (_rc != 0) return _rc;    \
-  } while (0)
-
-inline int grid_for(int64_t n, int per_block = kBlock, int max_waves = 8) {
-  int64_t g = (n + per_block - 1) / per_block;
-  g = std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)kNumSMs * max_waves));
-  return (int)g;
-}
-
-constexpr int kMaxPartialBlocks = kNumSMs * 8;
-
-int check_launch() {
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    set_error("kernel launch failed: %s", cudaGetErrorString(e));
-    return TO_ECUDA;
-  }
-  return 0;
-}
 
 int validate(const to_mesh_desc *d) {
   if (d->dim != 2 && d->dim != 3) { set_error("dim must be 2 or 3"); return TO_EINVAL; }
@@ -260,13 +65,6 @@ int validate(const to_mesh_desc *d) {
     for (int64_t k = 0; k < d->filt_nnz; ++k)
       if (d->filt_idx[k] < 0 || d->filt_idx[k] >= d->n_elem) { set_error("filt_idx out of range"); return TO_EMESH; }
   }
-  return 0;
-}
-
-template <typename T>
-int upload_array(to_mesh *m, T **dst, const T *src, size_t count, cudaStream_t st) {
-  RC(m->alloc(dst, count));
-  if (count) CK(cudaMemcpyAsync(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice, st));
   return 0;
 }
 
@@ -758,27 +556,6 @@ int op_rhs(to_mesh *m, double *b_int, cudaStream_t st) {
 
 int s3_grid(const to_mesh *m) { return m->s3_ncta > 0 ? m->s3_ncta : m->G.ntx * m->G.nty * m->G.nzs; }
 
-// Launch with programmatic stream serialization (PDL, see pdl_wait in
-// device_common.cuh) unless TOMESH_NO_PDL is set.
-template <typename... KArgs, typename... Args>
-int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
-  static const bool off = std::getenv("TOMESH_NO_PDL") != nullptr;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
-  return 0;
-}
-
-// out = C^T K C in (in vanishing on non-free DOFs), plain apply.  Structured:
-// `in` must be one of the handle's TMA-mapped vectors (x, pb[0], rb[*]).
 int op_apply(to_mesh *m, const double *in, double *out, cudaStream_t st) {
   if (!m->structured) return launch_matvec(m, in, out, st);
   const CUtensorMap *tin = in == m->x        ? &m->tm_x
@@ -873,6 +650,17 @@ int op_recover_out(to_mesh *m, const double *v_int, double *u_canon, cudaStream_
   k_from_int<<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->perm_node, v_int, u_canon);
   m->last_launches++;
   return check_launch();
+}
+
+// ||b - A x||^2 over free DOFs for the internal x in m->x (true residual)
+int op_resid2_x(to_mesh *m, double *r2, cudaStream_t st) {
+  RC(op_rhs(m, m->r, st));                      // r := b
+  RC(op_apply(m, m->x, m->q, st));              // q := C^T K C x
+  k_resid2<<<grid_for(m->n_int), kBlock, 0, st>>>(m->n_int, m->r, m->q, free_int(m), m->partials, m->S);
+  m->last_launches++;
+  RC(read_scalars(m, st));
+  *r2 = m->S_host->tmp[0];
+  return 0;
 }
 
 int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double rtol, int32_t max_iter,
@@ -1001,12 +789,9 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   }
   double relres_true = -1.0;
   if (!(flags & TO_NO_TRUE_RES) && res.status == 0) {
-    RC(op_rhs(m, m->r, st));                      // r := b
-    RC(op_apply(m, m->x, m->q, st));              // q := C^T K C x
-    k_resid2<<<gv, kBlock, 0, st>>>(n, m->r, m->q, free_int(m), m->partials, m->S);
-    m->last_launches++;
-    RC(read_scalars(m, st));
-    relres_true = res.bnorm2 > 0.0 ? std::sqrt(m->S_host->tmp[0] / res.bnorm2) : 0.0;
+    double r2 = 0.0;
+    RC(op_resid2_x(m, &r2, st));
+    relres_true = res.bnorm2 > 0.0 ? std::sqrt(r2 / res.bnorm2) : 0.0;
   }
   RC(op_recover_out(m, m->x, u_dev, st));
   CK(cudaEventRecord(m->ev1, st));
@@ -1034,382 +819,6 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   }
   return rc;
 }
-
-int alloc_padded(to_mesh *m, double **v, cudaStream_t st) {
-  double *base = nullptr;
-  RC(m->alloc(&base, (size_t)(m->n_int + kS3PadFront + kS3PadBack)));
-  CK(cudaMemsetAsync(base, 0, sizeof(double) * (m->n_int + kS3PadFront + kS3PadBack), st));
-  *v = base + kS3PadFront;
-  return 0;
-}
-
-int read_mr(to_mesh *m, cudaStream_t st) {
-  CK(cudaMemcpyAsync(m->MS_host, m->MS, sizeof(MrScalars), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  return 0;
-}
-
-int op_ic0_solve(to_mesh *m, const double *v, double *z, cudaStream_t st);   // kernels_ic0 (below)
-int op_ic0_setup(to_mesh *m, cudaStream_t st, double *shift);
-
-// MINRES on the rescaled system (header comment of kernels_minres.cuh).
-int solve_minres(to_mesh *m, double penal, const double *x_dev, double *u_dev, double rtol, int32_t max_iter,
-                 int32_t precond, uint32_t flags, to_minres_stats *st_out, cudaStream_t st) {
-  const int64_t n = m->n_int;
-  const bool ic0 = precond == TO_PC_IC0;
-  m->last_launches = 0;
-  if (!m->MS) {
-    for (int b = 0; b < 3; ++b) {
-      RC(alloc_padded(m, &m->mr_v[b], st));
-      RC(alloc_padded(m, &m->mr_w[b], st));
-    }
-    for (int b = 0; b < 2; ++b) {
-      RC(alloc_padded(m, &m->mr_zn[b], st));
-      RC(alloc_padded(m, &m->mr_z[b], st));
-    }
-    RC(alloc_padded(m, &m->mr_xt, st));
-    RC(alloc_padded(m, &m->mr_msc, st));
-    RC(alloc_padded(m, &m->mr_az, st));
-    if (!m->structured) RC(alloc_padded(m, &m->mr_t, st));
-    RC(m->alloc(&m->MS, 1));
-    CK(cudaMallocHost(&m->MS_host, sizeof(MrScalars)));
-  }
-  double *t = m->structured ? m->rb[0] : m->mr_t;   // the apply input (TMA-mapped when structured)
-  CK(cudaEventRecord(m->ev0, st));
-  RC(reset_scalars(m, 0, false, false, st));
-  RC(op_scale_and_diag(m, penal, x_dev, nullptr, st));
-  const int gv = grid_for(n);
-  if (m->structured) {
-    k_mr_scale_s3<<<grid_for((int64_t)m->G.NX * m->G.NY * m->G.NZ), kBlock, 0, st>>>(m->G, m->dn, m->mr_msc);
-  } else {
-    k_mr_scale<<<gv, kBlock, 0, st>>>(n, m->dinv, m->mr_msc);
-  }
-  m->last_launches++;
-  RC(read_scalars(m, st));
-  if (m->S_host->status != 0) {
-    set_error(m->S_host->status == TO_EINVAL ? "density outside (0, 1]" : "non-positive diagonal on a free DOF");
-    return m->S_host->status;
-  }
-  double shift = 0.0;
-  if (ic0) RC(op_ic0_setup(m, st, &shift));
-  std::memset(m->MS_host, 0, sizeof(MrScalars));
-  m->MS_host->max_iter = max_iter;
-  CK(cudaMemcpyAsync(m->MS, m->MS_host, sizeof(MrScalars), cudaMemcpyHostToDevice, st));
-  for (int b = 0; b < 3; ++b) {
-    CK(cudaMemsetAsync(m->mr_v[b], 0, sizeof(double) * n, st));
-    CK(cudaMemsetAsync(m->mr_w[b], 0, sizeof(double) * n, st));
-  }
-  CK(cudaMemsetAsync(m->mr_xt, 0, sizeof(double) * n, st));
-  RC(op_rhs(m, m->r, st));                                   // b (internal order)
-  if (!ic0) {
-    k_mr_init<true><<<gv, kBlock, 0, st>>>(n, m->r, m->mr_msc, m->mr_v[1], m->partials, m->MS, rtol);
-    m->last_launches++;
-  } else {
-    k_mr_init<false><<<gv, kBlock, 0, st>>>(n, m->r, m->mr_msc, m->mr_v[1], m->partials, m->MS, rtol);
-    m->last_launches++;
-    RC(op_ic0_solve(m, m->mr_v[1], m->mr_z[1], st));
-    k_mr_init_gamma<<<gv, kBlock, 0, st>>>(n, m->mr_z[1], m->mr_v[1], m->partials, m->MS, rtol);
-    m->last_launches++;
-  }
-  RC(check_launch());
-  // iteration it performs Lanczos / Givens step j = it + 1 and, first, the
-  // w / x~ update of step it (buffers: v(k) in mr_v[k%3], w(k) in mr_w[k%3],
-  // zn(k) in mr_zn[k%2], z(k) in mr_z[k%2])
-  auto iteration = [&](int it) -> int {
-    const double *z_j = ic0 ? m->mr_z[(it + 1) % 2] : m->mr_v[(it + 1) % 3];
-    k_mr_wx_prep<<<gv, kBlock, 0, st>>>(n, m->mr_zn[(it + 1) % 2], m->mr_w[(it + 2) % 3], m->mr_w[it % 3],
-                                        m->mr_w[(it + 1) % 3], m->mr_xt, z_j, m->mr_msc, m->mr_zn[it % 2], t, m->MS);
-    m->last_launches++;
-    RC(op_apply(m, t, m->q, st));
-    k_mr_delta<<<gv, kBlock, 0, st>>>(n, m->q, m->mr_msc, m->mr_zn[it % 2], m->mr_az, m->partials, m->MS);
-    m->last_launches++;
-    double *v_new = m->mr_v[(it + 2) % 3];
-    if (!ic0) {
-      k_mr_lanczos<true><<<gv, kBlock, 0, st>>>(n, m->mr_az, m->mr_v[(it + 1) % 3], m->mr_v[it % 3], v_new,
-                                                m->partials, m->MS);
-      m->last_launches++;
-    } else {
-      k_mr_lanczos<false><<<gv, kBlock, 0, st>>>(n, m->mr_az, m->mr_v[(it + 1) % 3], m->mr_v[it % 3], v_new,
-                                                 m->partials, m->MS);
-      m->last_launches++;
-      RC(op_ic0_solve(m, v_new, m->mr_z[it % 2], st));
-      k_mr_gamma<<<gv, kBlock, 0, st>>>(n, m->mr_z[it % 2], v_new, m->partials, m->MS);
-      m->last_launches++;
-    }
-    return 0;
-  };
-  RC(read_mr(m, st));
-  int launched = 0, chunk = 16;
-  bool stop = m->MS_host->done != 0;
-  while (!stop && launched < max_iter) {
-    const int cnt = std::min(chunk, max_iter - launched);
-    for (int k = 0; k < cnt; ++k) RC(iteration(launched + k));
-    RC(check_launch());
-    launched += cnt;
-    RC(read_mr(m, st));
-    stop = m->MS_host->done != 0;
-    chunk = std::min(chunk * 2, 256);
-  }
-  // the w / x~ update of the last step (a no-op if an enqueued iteration did it)
-  {
-    const int it = launched;
-    k_mr_wx_prep<<<gv, kBlock, 0, st>>>(n, m->mr_zn[(it + 1) % 2], m->mr_w[(it + 2) % 3], m->mr_w[it % 3],
-                                        m->mr_w[(it + 1) % 3], m->mr_xt, m->mr_v[0], m->mr_msc, m->mr_zn[it % 2], t,
-                                        m->MS);
-    m->last_launches++;
-  }
-  k_mr_unscale<<<gv, kBlock, 0, st>>>(n, m->mr_msc, m->mr_xt, m->x);
-  m->last_launches++;
-  RC(read_mr(m, st));
-  MrScalars res = *m->MS_host;
-  double relres_true = -1.0;
-  if (!(flags & TO_NO_TRUE_RES) && res.status == 0) {
-    RC(op_rhs(m, m->r, st));
-    RC(op_apply(m, m->x, m->q, st));
-    k_resid2<<<gv, kBlock, 0, st>>>(n, m->r, m->q, free_int(m), m->partials, m->S);
-    m->last_launches++;
-    RC(read_scalars(m, st));
-    relres_true = res.bnorm2 > 0.0 ? std::sqrt(m->S_host->tmp[0] / res.bnorm2) : 0.0;
-  }
-  RC(op_recover_out(m, m->x, u_dev, st));
-  CK(cudaEventRecord(m->ev1, st));
-  CK(cudaStreamSynchronize(st));
-  float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
-  int rc = res.status;
-  const bool converged = res.eta0 == 0.0 || std::fabs(res.eta) <= res.thresh;
-  if (rc == 0 && !converged) rc = TO_NOT_CONVERGED;
-  if (st_out) {
-    st_out->iters = res.iter;
-    st_out->status = rc;
-    st_out->eta_rel = res.eta0 > 0.0 ? std::fabs(res.eta) / res.eta0 : 0.0;
-    st_out->relres_true = relres_true;
-    st_out->ms = ms;
-    st_out->ic0_shift = ic0 ? shift : -1.0;
-    st_out->ic0_levels[0] = ic0 ? m->ic_nlvl : 0;
-    st_out->ic0_levels[1] = ic0 ? m->ic_nblvl : 0;
-  }
-  if (rc < 0) set_error("%s", rc == TO_EBREAKDOWN ? "MINRES breakdown" : "NaN/Inf in the MINRES recurrences");
-  return rc;
-}
-
-template <typename T>
-int download(std::vector<T> &h, const T *d, size_t n) {
-  h.resize(n);
-  if (n) CK(cudaMemcpy(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost));
-  return 0;
-}
-
-// Host symbolic phase of IC(0) (general path): the lower pattern of K~ over
-// free-free couplings (through the Eq. 6 interpolation) plus unit rows of the
-// non-free DOFs, the element contributions of every nonzero, the transposed
-// pattern and the dependency levels of both triangular solves.
-int ic0_build(to_mesh *m, cudaStream_t st) {
-  const int dim = m->dim, nc = 1 << dim, ND = dim * nc;
-  const int64_t n = m->n_dof, ne = m->n_el;
-  if (ne * (int64_t)(ND * (ND + 1) / 2) > (int64_t)250000000) {
-    set_error("IC(0): %lld elements give more than 2.5e8 element contributions (host symbolic phase too large)",
-              (long long)ne);
-    return TO_ENOMEM;
-  }
-  CK(cudaStreamSynchronize(st));
-  std::vector<int32_t> en, nh, hp, hpar;
-  std::vector<double> hw;
-  std::vector<uint8_t> fr;
-  RC(download(en, m->elem_node, (size_t)ne * nc));
-  RC(download(nh, m->node_hang, (size_t)m->n_node));
-  RC(download(fr, m->free_dof, (size_t)n));
-  if (m->n_hang > 0) {
-    RC(download(hp, m->hang_ptr, (size_t)m->n_hang + 1));
-    RC(download(hpar, m->hang_parent, (size_t)hp[m->n_hang]));
-    RC(download(hw, m->hang_weight, (size_t)hp[m->n_hang]));
-  }
-  auto wcode = [](double w) -> int { return w == 1.0 ? 0 : w == 0.5 ? 1 : w == 0.25 ? 2 : -1; };
-  // expansions of every local DOF of an element: (global free DOF, log2(1/w))
-  auto expand = [&](int64_t e, int a, std::vector<std::pair<int64_t, int>> &out) {
-    out.clear();
-    const int32_t node = en[e * nc + a / dim], c = a % dim;
-    if (nh[node] < 0) {
-      const int64_t g = (int64_t)node * dim + c;
-      if (fr[g]) out.push_back({g, 0});
-      return;
-    }
-    const int32_t h = nh[node];
-    for (int32_t k = hp[h]; k < hp[h + 1]; ++k) {
-      const int64_t g = (int64_t)hpar[k] * dim + c;
-      if (fr[g]) out.push_back({g, wcode(hw[k])});
-    }
-  };
-  std::vector<std::vector<std::pair<int64_t, int>>> ex(ND);
-  // per row: (column, packed contribution), then sorted by column
-  std::vector<std::vector<std::pair<int32_t, uint64_t>>> rows(n);
-  for (int64_t e = 0; e < ne; ++e) {
-    for (int a = 0; a < ND; ++a) expand(e, a, ex[a]);
-    for (int a = 0; a < ND; ++a)
-      for (const auto &pa : ex[a])
-        for (int b = 0; b < ND; ++b)
-          for (const auto &pb : ex[b]) {
-            if (pb.first > pa.first) continue;   // lower triangle (column <= row)
-            const uint64_t code = (uint64_t)(pa.second + pb.second);
-            rows[pa.first].push_back({(int32_t)pb.first, ((uint64_t)e << 16) | ((uint64_t)(a * ND + b) << 3) | code});
-          }
-  }
-  std::vector<int64_t> ptr(n + 1, 0), cptr(1, 0);
-  std::vector<int32_t> col, row;
-  std::vector<uint64_t> contrib;
-  for (int64_t i = 0; i < n; ++i) {
-    auto &R = rows[i];
-    std::stable_sort(R.begin(), R.end(), [](const std::pair<int32_t, uint64_t> &x, const std::pair<int32_t, uint64_t> &y) {
-      return x.first < y.first;
-    });
-    if (R.empty()) {                         // non-free DOF: unit diagonal, no contributions
-      col.push_back((int32_t)i);
-      row.push_back((int32_t)i);
-      cptr.push_back((int64_t)contrib.size());
-    } else {
-      for (size_t u = 0; u < R.size();) {
-        size_t v = u;
-        while (v < R.size() && R[v].first == R[u].first) contrib.push_back(R[v++].second);
-        col.push_back(R[u].first);
-        row.push_back((int32_t)i);
-        cptr.push_back((int64_t)contrib.size());
-        u = v;
-      }
-      if (col.back() != (int32_t)i) { set_error("IC(0): free row %lld without a diagonal", (long long)i); return TO_EMESH; }
-    }
-    ptr[i + 1] = (int64_t)col.size();
-    std::vector<std::pair<int32_t, uint64_t>>().swap(R);
-  }
-  const int64_t nnz = (int64_t)col.size();
-  // dependency levels: forward (row i after its columns k < i), backward (row k of L^T after rows i > k)
-  std::vector<int32_t> lv(n, 0), blv(n, 0);
-  int nl = 0, nbl = 0;
-  for (int64_t i = 0; i < n; ++i) {
-    int l = 0;
-    for (int64_t t = ptr[i]; t < ptr[i + 1] - 1; ++t) l = std::max(l, lv[col[t]] + 1);
-    lv[i] = l;
-    nl = std::max(nl, l + 1);
-  }
-  std::vector<int64_t> ut_ptr(n + 1, 0);
-  for (int64_t t = 0; t < nnz; ++t)
-    if (col[t] != row[t]) ut_ptr[col[t] + 1]++;
-  for (int64_t k = 0; k < n; ++k) ut_ptr[k + 1] += ut_ptr[k];
-  std::vector<int32_t> ut_row(ut_ptr[n]);
-  std::vector<int64_t> ut_pos(ut_ptr[n]), ufill(ut_ptr.begin(), ut_ptr.end() - 1);
-  for (int64_t i = 0; i < n; ++i)          // rows ascending: each column's entries ascending in i
-    for (int64_t t = ptr[i]; t < ptr[i + 1] - 1; ++t) {
-      const int64_t q = ufill[col[t]]++;
-      ut_row[q] = (int32_t)i;
-      ut_pos[q] = t;
-    }
-  for (int64_t k = n - 1; k >= 0; --k) {
-    int l = 0;
-    for (int64_t t = ut_ptr[k]; t < ut_ptr[k + 1]; ++t) l = std::max(l, blv[ut_row[t]] + 1);
-    blv[k] = l;
-    nbl = std::max(nbl, l + 1);
-  }
-  auto bucket = [&](const std::vector<int32_t> &lvl, int nlev, std::vector<int64_t> &lptr, std::vector<int32_t> &lrows) {
-    lptr.assign(nlev + 1, 0);
-    for (int64_t i = 0; i < n; ++i) lptr[lvl[i] + 1]++;
-    for (int l = 0; l < nlev; ++l) lptr[l + 1] += lptr[l];
-    lrows.resize(n);
-    std::vector<int64_t> f(lptr.begin(), lptr.end() - 1);
-    for (int64_t i = 0; i < n; ++i) lrows[f[lvl[i]]++] = (int32_t)i;
-  };
-  std::vector<int64_t> lptr, blptr;
-  std::vector<int32_t> lrows, blrows;
-  bucket(lv, nl, lptr, lrows);
-  bucket(blv, nbl, blptr, blrows);
-  // device copies
-  int64_t *d_ptr, *d_cptr;
-  int32_t *d_col, *d_row;
-  uint64_t *d_contrib;
-  RC(upload_array(m, &d_ptr, ptr.data(), ptr.size(), st));
-  RC(upload_array(m, &d_col, col.data(), col.size(), st));
-  RC(upload_array(m, &d_row, row.data(), row.size(), st));
-  RC(upload_array(m, &d_cptr, cptr.data(), cptr.size(), st));
-  RC(upload_array(m, &d_contrib, contrib.data(), std::max<size_t>(1, contrib.size()), st));
-  RC(upload_array(m, &m->ic_lvl_ptr, lptr.data(), lptr.size(), st));
-  RC(upload_array(m, &m->ic_lvl_rows, lrows.data(), lrows.size(), st));
-  RC(upload_array(m, &m->ic_blvl_ptr, blptr.data(), blptr.size(), st));
-  RC(upload_array(m, &m->ic_blvl_rows, blrows.data(), blrows.size(), st));
-  RC(upload_array(m, &m->ic_ut_ptr, ut_ptr.data(), ut_ptr.size(), st));
-  RC(upload_array(m, &m->ic_ut_row, ut_row.data(), std::max<size_t>(1, ut_row.size()), st));
-  RC(upload_array(m, &m->ic_ut_pos, ut_pos.data(), std::max<size_t>(1, ut_pos.size()), st));
-  const double *K0 = dim == 2 ? m->K2.K : m->K3.K;
-  RC(upload_array(m, &m->ic_K0, K0, (size_t)ND * ND, st));
-  RC(m->alloc(&m->ic_kt, (size_t)nnz));
-  RC(m->alloc(&m->ic_L, (size_t)nnz));
-  RC(m->alloc(&m->ic_y, (size_t)n));
-  RC(m->alloc(&m->ic_fail, 1));
-  m->IC.n = n;
-  m->IC.nnz = nnz;
-  m->IC.ptr = d_ptr;
-  m->IC.col = d_col;
-  m->IC.row = d_row;
-  m->IC.cptr = d_cptr;
-  m->IC.contrib = d_contrib;
-  m->ic_lvl_host = lptr;
-  m->ic_nlvl = nl;
-  m->ic_nblvl = nbl;
-  m->ic_ready = true;
-  CK(cudaStreamSynchronize(st));
-  return 0;
-}
-
-// K~ (+ a I) assembled and factored; a = 0, then 1e-3 2^t until no pivot fails
-int op_ic0_setup(to_mesh *m, cudaStream_t st, double *shift) {
-  if (m->structured) {
-    set_error("IC(0) needs the general (canonical-order) operator path; upload with TOMESH_FORCE_GENERAL=1");
-    return TO_EINVAL;
-  }
-  if (!m->ic_ready) RC(ic0_build(m, st));
-  const int g = grid_for(m->IC.nnz);
-  for (int t = -1; t < 30; ++t) {
-    const double a = t < 0 ? 0.0 : 1e-3 * std::ldexp(1.0, t);
-    if (m->dim == 2) k_ic0_assemble<2><<<g, kBlock, 0, st>>>(m->IC, m->s, m->mr_msc, m->ic_K0, a, m->ic_L);
-    else k_ic0_assemble<3><<<g, kBlock, 0, st>>>(m->IC, m->s, m->mr_msc, m->ic_K0, a, m->ic_L);
-    m->last_launches++;
-    CK(cudaMemsetAsync(m->ic_fail, 0, sizeof(int), st));
-    for (int l = 0; l < m->ic_nlvl; ++l) {
-      const int64_t r0 = m->ic_lvl_host[l], r1 = m->ic_lvl_host[l + 1];
-      k_ic0_factor<<<(int)std::min<int64_t>((r1 - r0 + 127) / 128, 4 * kNumSMs), 128, 0, st>>>(
-          m->IC, m->ic_lvl_rows, r0, r1, m->ic_L, m->ic_fail);
-    }
-    m->last_launches += m->ic_nlvl;
-    RC(check_launch());
-    int fail = 0;
-    CK(cudaMemcpyAsync(&fail, m->ic_fail, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (!fail) {
-      *shift = a;
-      return 0;
-    }
-  }
-  set_error("IC(0) breaks down for every shift tried");
-  return TO_EBREAKDOWN;
-}
-
-// z = (L L^T)^-1 v
-int op_ic0_solve(to_mesh *m, const double *v, double *z, cudaStream_t st) {
-  k_ic0_fwd<<<1, 1024, 0, st>>>(m->IC, m->ic_lvl_ptr, m->ic_nlvl, m->ic_lvl_rows, m->ic_L, v, m->ic_y);
-  k_ic0_bwd<<<1, 1024, 0, st>>>(m->IC, m->ic_ut_ptr, m->ic_ut_row, m->ic_ut_pos, m->ic_blvl_ptr, m->ic_nblvl,
-                                m->ic_blvl_rows, m->ic_L, m->ic_y, z);
-  m->last_launches += 2;
-  return check_launch();
-}
-
-// Adds the kernels an operator-level entry point launched (via last_launches)
-// to the handle's monotone counter, on every return path.
-struct LaunchCounter {
-  to_mesh *m;
-  int l0;
-  ~LaunchCounter() {
-    if (m) m->launches_total += m->last_launches - l0;
-  }
-};
-
-}  // namespace
 
 // ======================================================================================
 // C ABI
@@ -1537,20 +946,6 @@ extern "C" int to_filter(to_mesh *m, int32_t mode, const double *x_dev, const do
   return check_launch();
 }
 
-extern "C" int tosolve_minres(to_mesh *m, double penal, const double *x_dev, double *u_dev, double rtol,
-                              int32_t max_iter, int32_t precond, uint32_t flags, to_minres_stats *st,
-                              void *cuda_stream) {
-  LaunchCounter lc_{m, 0};
-  clear_error();
-  if (!m || !x_dev || !u_dev || !(penal > 0.0) || max_iter < 0 || !(rtol >= 0.0)) {
-    set_error("bad argument");
-    return TO_EINVAL;
-  }
-  if (precond != TO_PC_JACOBI && precond != TO_PC_IC0) { set_error("unknown preconditioner"); return TO_EINVAL; }
-  if (flags & ~(uint32_t)TO_NO_TRUE_RES) { set_error("tosolve_minres supports TO_NO_TRUE_RES only"); return TO_EINVAL; }
-  return solve_minres(m, penal, x_dev, u_dev, rtol, max_iter, precond, flags, st, (cudaStream_t)cuda_stream);
-}
-
 extern "C" int to_amr_mark(to_mesh *m, const double *x_dev, double rho_s, int8_t *marks_dev, void *cuda_stream) {
   clear_error();
   if (!m || !x_dev || !marks_dev) { set_error("NULL argument"); return TO_EINVAL; }
@@ -1577,147 +972,6 @@ extern "C" int to_amr_mark(to_mesh *m, const double *x_dev, double rho_s, int8_t
                                    m->filt_idx, x_dev, rho_s, marks_dev);
   m->launches_total++;
   return check_launch();
-}
-
-extern "C" int to_oc_update(to_mesh *m, const double *x_dev, const double *dc_dev, double volfrac, double move,
-                            double eta, double rho_o, double *x_new_dev, to_oc_stats *st, void *cuda_stream) {
-  clear_error();
-  if (!m || !x_dev || !dc_dev || !x_new_dev) { set_error("NULL argument"); return TO_EINVAL; }
-  if (x_new_dev == dc_dev) { set_error("x_new_dev aliases dc_dev"); return TO_EINVAL; }
-  if (!(volfrac > 0.0 && volfrac <= 1.0) || !(move >= 0.0 && move <= 1.0) || !(eta > 0.0 && eta <= 4.0) ||
-      !(rho_o > 0.0 && rho_o < 1.0)) {
-    set_error("OC parameters out of range (volfrac in (0,1], move in [0,1], eta in (0,4], rho_o in (0,1))");
-    return TO_EINVAL;
-  }
-  if (m->L > 23) { set_error("max_level too large for the OC volume table"); return TO_EINVAL; }
-  cudaStream_t st_ = (cudaStream_t)cuda_stream;
-  if (!m->oc_a) {
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_oc_update, kOcBlock, 0));
-    if (per_sm < 1) { set_error("OC kernel cannot be resident"); return TO_ECUDA; }
-    const int64_t need = (m->n_el + kOcBlock - 1) / kOcBlock;
-    m->oc_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)per_sm * kNumSMs));
-    if (m->n_el <= 16 * kOcBlock) m->oc_blocks = 1;   // latency-bound: one block, block-level sums only
-    RC(m->alloc(&m->oc_a, (size_t)m->n_el));
-    RC(m->alloc(&m->oc_part, (size_t)kOcCand * m->oc_blocks));
-    RC(m->alloc(&m->oc_state, 1));
-    if (!m->oc_state_host) CK(cudaMallocHost(&m->oc_state_host, sizeof(OcState)));
-  }
-  OcArgs A{};
-  A.n = m->n_el;
-  A.x = x_dev;
-  A.dc = dc_dev;
-  A.level = m->structured ? nullptr : m->elem_level;
-  A.a = m->oc_a;
-  A.xn = x_new_dev;
-  A.target = volfrac * m->vol_total;
-  A.move = move;
-  A.eta = eta;
-  A.rho_o = rho_o;
-  A.lam_hi = 1e9;
-  A.tol = 1e-12;
-  A.max_steps = 200;
-  for (int l = 0; l < 24; ++l) {
-    const double hs = l <= m->L ? std::ldexp(m->hL, m->L - l) : 0.0;   // (2^(L-l) h_L)
-    A.vtab[l] = m->dim == 2 ? hs * hs : hs * hs * hs;
-  }
-  if (m->structured) A.vtab[0] = m->dim == 2 ? m->h_struct * m->h_struct : m->h_struct * m->h_struct * m->h_struct;
-  CK(cudaEventRecord(m->ev0, st_));
-  CK(cudaMemsetAsync(m->oc_state, 0, sizeof(OcState), st_));   // reduction counters, flag, max
-  void *args[] = {(void *)&A, (void *)&m->oc_part, (void *)&m->oc_state};
-  CK(cudaLaunchCooperativeKernel((const void *)k_oc_update, dim3(m->oc_blocks), dim3(kOcBlock), args, 0, st_));
-  m->launches_total++;
-  CK(cudaEventRecord(m->ev1, st_));
-  RC(check_launch());
-  if (!st) return 0;
-  CK(cudaMemcpyAsync(m->oc_state_host, m->oc_state, sizeof(OcState), cudaMemcpyDeviceToHost, st_));
-  CK(cudaStreamSynchronize(st_));
-  const OcState &S = *m->oc_state_host;
-  float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
-  st->lambda = S.lam;
-  st->volume = S.volume_abs / m->vol_total;
-  st->change = S.change;
-  st->ms = ms;
-  st->steps = S.steps;
-  st->state = S.state;
-  st->passes = S.passes;
-  if (S.state < 0) { set_error("NaN/Inf in x or dc"); return TO_ENAN; }
-  return 0;
-}
-
-extern "C" int to_optimize(to_mesh *m, const to_opt_params *P, int32_t n_steps, double *x_dev, double *u_dev,
-                           to_opt_step *hist, int32_t *steps_done, to_opt_state *state, void *cuda_stream) {
-  clear_error();
-  if (steps_done) *steps_done = 0;
-  if (!m || !P || !x_dev || !u_dev || n_steps < 0) { set_error("bad argument"); return TO_EINVAL; }
-  if (!(P->penal0 > 0.0) || !(P->penal_max >= P->penal0) || !(P->penal_step >= 0.0) || P->stage_steps < 1 ||
-      !(P->rtol > 0.0) || P->max_iter < 1 || P->adapt_min_steps < 0 || P->adapt_max_steps < 0) {
-    set_error("bad continuation, solver or adaptation parameters");
-    return TO_EINVAL;
-  }
-  if (!m->opt_dc) {
-    RC(m->alloc(&m->opt_dc, (size_t)m->n_el));
-    RC(m->alloc(&m->opt_dcf, (size_t)m->n_el));
-  }
-  double penal = state ? state->penal : P->penal0;
-  int at_stage = state ? state->at_stage : 0, since = state ? state->since_adapt : 0;
-  if (!(penal > 0.0)) { set_error("state->penal must be > 0"); return TO_EINVAL; }
-  if (state) state->adapt_due = state->converged = 0;
-  const bool amr = P->adapt_max_steps > 0;
-  int k = 0, result = TO_OK;
-  for (; k < n_steps; ++k) {
-    to_cg_stats cs{};
-    const int rc = tosolve_cg(m, penal, x_dev, u_dev, P->rtol, P->max_iter, (k > 0 ? TO_WARM : 0) | TO_NO_TRUE_RES,
-                              &cs, cuda_stream);
-    if (rc < 0) return rc;
-    if (rc > 0) result = TO_NOT_CONVERGED;
-    double c = 0.0;
-    RC(to_sensitivity(m, penal, x_dev, u_dev, m->opt_dc, &c, cuda_stream));
-    const double *dcf = m->opt_dc;
-    if (P->filter && m->rmin > 0.0) {
-      RC(to_filter(m, TO_FILTER_SENS, x_dev, m->opt_dc, m->opt_dcf, cuda_stream));
-      dcf = m->opt_dcf;
-    }
-    to_oc_stats os{};
-    RC(to_oc_update(m, x_dev, dcf, P->volfrac, P->move, P->eta, P->rho_o, x_dev, &os, cuda_stream));
-    if (hist) {
-      to_opt_step &h = hist[k];
-      h.compliance = c;
-      h.penal = penal;
-      h.volume = os.volume;
-      h.change = os.change;
-      h.lambda = os.lambda;
-      h.solve_ms = cs.ms;
-      h.oc_ms = os.ms;
-      h.cg_iters = cs.iters;
-      h.status = rc;
-    }
-    ++at_stage;
-    ++since;
-    const bool conv = os.change < P->change_tol;
-    if (P->stop_on_converge && penal >= P->penal_max && conv) {
-      ++k;
-      if (state) state->converged = 1;
-      break;
-    }
-    if (penal < P->penal_max && (conv || at_stage >= P->stage_steps)) {
-      penal = std::min(P->penal_max, penal + P->penal_step);
-      at_stage = 0;
-    }
-    if (amr && ((conv && since >= P->adapt_min_steps) || since >= P->adapt_max_steps)) {
-      ++k;
-      if (state) state->adapt_due = 1;
-      break;
-    }
-  }
-  if (state) {
-    state->penal = penal;
-    state->at_stage = at_stage;
-    state->since_adapt = since;
-  }
-  if (steps_done) *steps_done = k;
-  return result;
 }
 
 extern "C" int to_apply_A(to_mesh *m, double penal, const double *x_dev, const double *v_dev, double *q_dev,

@@ -1,0 +1,246 @@
+#pragma once
+// libtomesh internals shared by its translation units: the handle (struct
+// to_mesh), error macros, launch helpers and the internal-order operations
+// that tomesh.cu defines and tomesh_minres.cu / tomesh_opt.cu call.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "../../include/tomesh.h"
+#include "common.h"
+#include "device_common.cuh"
+#include "element.h"
+#include "tomesh_types.cuh"
+
+using namespace tomesh;
+
+namespace tomesh {
+#ifndef TOMESH_S3_TYW
+#define TOMESH_S3_TYW 8   // the value the tests validate (16 ran but slower; 4 fails on c5)
+#endif
+constexpr int kS3TYW = TOMESH_S3_TYW;   // warps per CTA (node rows + 1) of the structured H8 kernel
+constexpr int kS3CtasPerSM = kS3TYW <= 8 ? 2 : 1;
+}
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+};
+
+struct to_mesh {
+  int dim = 0, L = 0, device = 0;
+  double h0 = 1.0, hL = 1.0, E0 = 1.0, Emin = 1e-9, nu = 0.3, rmin = 0.0;
+  int64_t n_el = 0, n_node = 0, n_dof = 0, n_hang = 0, n_fixed = 0, filt_nnz = 0;
+  int64_t n_int = 0;   // length of the internal CG vectors (n_dof, or padded rows when structured)
+  std::vector<DevBuf> bufs;
+  int64_t dev_bytes = 0;
+  // mesh
+  int32_t *elem_node = nullptr, *elem_anchor = nullptr, *node_hang = nullptr;
+  int8_t *elem_level = nullptr;
+  int32_t *hang_ptr = nullptr, *hang_parent = nullptr, *child_ptr = nullptr, *child_hang = nullptr;
+  double *hang_weight = nullptr, *child_weight = nullptr, *load = nullptr;
+  uint8_t *free_dof = nullptr;
+  int64_t *filt_ptr = nullptr;
+  S3FilterOffset *foffs = nullptr;     // structured filter stencil
+  int n_foffs = 0;
+  double *ftmp = nullptr;              // structured filter: lexicographic temporary
+  int64_t *inc_ptr = nullptr;          // general path: node -> (element, corner, weight) incidences
+  uint32_t *inc = nullptr;
+  double *ye = nullptr;                // general path: element vectors s_e K0 C_e p
+  uint8_t *hmask = nullptr;            // general path: bit c = corner c of the element is hanging
+  double *zp = nullptr;                // general path: node records {Dinv r, p}
+  int coop_blocks = 0;                 // general path: grid of the persistent cooperative solver (0 = off)
+  int ge_blocks = 0, gn_blocks = 0;    // general path: one resident wave of the element / node pass
+  int32_t *filt_idx = nullptr;
+  // OC update (allocated on first use)
+  double *oc_a = nullptr, *oc_part = nullptr;
+  OcState *oc_state = nullptr;
+  OcState *oc_state_host = nullptr;   // pinned mirror
+  double *opt_dc = nullptr, *opt_dcf = nullptr;   // to_optimize: raw and filtered sensitivities
+  // MINRES (tosolve_minres), allocated on first use, internal order with pads
+  double *mr_v[3] = {nullptr, nullptr, nullptr}, *mr_w[3] = {nullptr, nullptr, nullptr};
+  double *mr_zn[2] = {nullptr, nullptr}, *mr_z[2] = {nullptr, nullptr};
+  double *mr_xt = nullptr, *mr_msc = nullptr, *mr_az = nullptr, *mr_t = nullptr;
+  MrScalars *MS = nullptr, *MS_host = nullptr;
+  // IC(0) of the rescaled matrix (general path), built on first use
+  bool ic_ready = false;
+  Ic0View IC{};
+  double *ic_kt = nullptr, *ic_L = nullptr, *ic_K0 = nullptr, *ic_y = nullptr;
+  int64_t *ic_lvl_ptr = nullptr, *ic_blvl_ptr = nullptr, *ic_ut_ptr = nullptr, *ic_ut_pos = nullptr;
+  int32_t *ic_lvl_rows = nullptr, *ic_blvl_rows = nullptr, *ic_ut_row = nullptr;
+  std::vector<int64_t> ic_lvl_host;   // level boundaries (host) for the per-level factor launches
+  int ic_nlvl = 0, ic_nblvl = 0;
+  int *ic_fail = nullptr;
+  double ic_setup_ms = 0.0;
+  int oc_blocks = 0;
+  double vol_total = 0.0;             // sum_e V_e (exact dyadic sum, host)
+  // workspace
+  double *s = nullptr, *x = nullptr, *r = nullptr, *q = nullptr, *dinv = nullptr, *D = nullptr;
+  double *pb[2] = {nullptr, nullptr};   // p ping-pong: iteration k writes pb[k & 1]
+  double *rb[2] = {nullptr, nullptr};   // structured: r ping-pong (rb[0] = r)
+  double *qb[2] = {nullptr, nullptr};   // structured: q ping-pong (qb[0] = q)
+  double *dn = nullptr;                 // structured: Dinv per node (internal node order)
+  double *partials = nullptr, *hist = nullptr;
+  int32_t hist_len = 0, hist_cap = 0;
+  CgScalars *S = nullptr;
+  CgScalars *S_host = nullptr;   // pinned mirror
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  K0Dense2 K2{};
+  K0Dense3 K3{};
+  K0Had3 KH{};
+  K0HadSym KS{};
+  // structured fast path (uniform H8 box)
+  bool structured = false, force_general = false;
+  GridView G{};
+  int32_t *perm_el = nullptr, *perm_node = nullptr;
+  uint8_t *free_lex = nullptr;         // per DOF, internal order
+  uint8_t *free_node_lex = nullptr;    // per node, internal order
+  int64_t n_int_nodes = 0;
+  int s3_ncta = 0;                     // > 0: CTAs of the host-planned K1 grid (G.plan)
+  double k0d = 0.0, h_struct = 1.0;
+  // TMA tensor maps of the internal vectors (structured path): [NZ][NY][RS] doubles
+  // (boxes of TYW+1 rows x 100 doubles) and the node array Dinv [NZ][NY][NXP].
+  CUtensorMap tm_x, tm_rb[2], tm_qb[2], tm_pb[2], tm_dn;
+  int last_launches = 0;
+  int matvec_variant = 0;
+  int64_t launches_total = 0;          // every kernel launched on this handle
+  std::vector<cudaEvent_t> prof_ev;   // TO_PROFILE: 5 events per iteration
+  double prof_ms[6] = {0, 0, 0, 0, 0, 0};
+  cudaEvent_t loop_ev[2] = {nullptr, nullptr};   // TO_PROFILE_LOOP: around the iteration launches
+
+  MeshView view() const {
+    MeshView M;
+    M.n_el = n_el;
+    M.n_node = n_node;
+    M.elem_node = elem_node;
+    M.elem_level = elem_level;
+    M.elem_anchor = elem_anchor;
+    M.node_hang = node_hang;
+    M.hang_ptr = hang_ptr;
+    M.hang_parent = hang_parent;
+    M.hang_weight = hang_weight;
+    M.child_ptr = child_ptr;
+    M.child_hang = child_hang;
+    M.child_weight = child_weight;
+    M.free_dof = free_dof;
+    M.L = L;
+    M.hL = hL;
+    return M;
+  }
+
+  template <typename T>
+  int alloc(T **ptr, size_t count) {
+    *ptr = nullptr;
+    if (count == 0) count = 1;
+    void *d = nullptr;
+    if (cudaMalloc(&d, count * sizeof(T)) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("cudaMalloc of %zu bytes failed", count * sizeof(T));
+      return TO_ENOMEM;
+    }
+    bufs.push_back({d, count * sizeof(T)});
+    dev_bytes += (int64_t)(count * sizeof(T));
+    *ptr = (T *)d;
+    return 0;
+  }
+  ~to_mesh() {
+    for (auto &b : bufs) cudaFree(b.p);
+    if (S_host) cudaFreeHost(S_host);
+    if (oc_state_host) cudaFreeHost(oc_state_host);
+    if (MS_host) cudaFreeHost(MS_host);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    for (auto e : prof_ev) cudaEventDestroy(e);
+    for (auto e : loop_ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+#define CK(call)                                                                 \
+  do {                                                                           \
+    cudaError_t _e = (call);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      set_error("%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, __LINE__); \
+      return TO_ECUDA;                                                           \
+    }                                                                            \
+  } while (0)
+
+#define RC(call)                 \
+  do {                           \
+    int _rc = (call);            \
+    if (_rc != 0) return _rc;    \
+  } while (0)
+
+inline int grid_for(int64_t n, int per_block = kBlock, int max_waves = 8) {
+  int64_t g = (n + per_block - 1) / per_block;
+  g = std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)kNumSMs * max_waves));
+  return (int)g;
+}
+
+constexpr int kMaxPartialBlocks = kNumSMs * 8;
+
+inline int check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("kernel launch failed: %s", cudaGetErrorString(e));
+    return TO_ECUDA;
+  }
+  return 0;
+}
+
+template <typename T>
+int upload_array(to_mesh *m, T **dst, const T *src, size_t count, cudaStream_t st) {
+  RC(m->alloc(dst, count));
+  if (count) CK(cudaMemcpyAsync(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice, st));
+  return 0;
+}
+
+// Launch with programmatic stream serialization (PDL, see pdl_wait in
+// device_common.cuh) unless TOMESH_NO_PDL is set.
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  static const bool off = std::getenv("TOMESH_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+  return 0;
+}
+
+// out = C^T K C in (in vanishing on non-free DOFs), plain apply.  Structured:
+// `in` must be one of the handle's TMA-mapped vectors (x, pb[0], rb[*]).
+
+// Adds the kernels an operator-level entry point launched (via last_launches)
+// to the handle's monotone counter, on every return path.
+struct LaunchCounter {
+  to_mesh *m;
+  int l0;
+  ~LaunchCounter() {
+    if (m) m->launches_total += m->last_launches - l0;
+  }
+};
+
+// internal-order operations (tomesh.cu)
+const uint8_t *free_int(const to_mesh *m);
+int s3_grid(const to_mesh *m);
+int reset_scalars(to_mesh *m, int max_iter, bool fixed, bool history, cudaStream_t st);
+int read_scalars(to_mesh *m, cudaStream_t st);
+int op_scale_and_diag(to_mesh *m, double penal, const double *x, double *d_int, cudaStream_t st);
+int op_rhs(to_mesh *m, double *b_int, cudaStream_t st);
+int op_apply(to_mesh *m, const double *in, double *out, cudaStream_t st);
+int op_recover_out(to_mesh *m, const double *v_int, double *u_canon, cudaStream_t st);
+int op_resid2_x(to_mesh *m, double *r2, cudaStream_t st);

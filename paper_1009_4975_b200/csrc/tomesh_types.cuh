@@ -1,0 +1,83 @@
+// Data types shared by the kernels and the host side of libtomesh (the
+// handle in tomesh_impl.cuh holds them), kept apart from the kernel
+// definitions so that each translation unit includes only the kernels it
+// launches.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "device_common.cuh"
+
+namespace tomesh {
+
+// General (AMR) path: the mesh arrays a kernel reads (kernels_general.cuh).
+struct MeshView {
+  int64_t n_el, n_node;
+  const int32_t *elem_node;     // [n_el][NC]
+  const int8_t *elem_level;
+  const int32_t *elem_anchor;   // [n_el][DIM]
+  const int32_t *node_hang;     // [n_node] index into hang rows or -1
+  const int32_t *hang_ptr, *hang_parent;
+  const double *hang_weight;
+  const int32_t *child_ptr, *child_hang;  // transpose: parent node -> hanging children
+  const double *child_weight;
+  const uint8_t *free_dof;      // [n_dof] 1 = neither hanging nor fixed
+  int L;
+  double hL;
+};
+
+// Structured path (kernels_struct3d.cuh): the uniform H8 box and its CTA grid.
+struct GridView {
+  int EX, EY, EZ;        // elements per axis
+  int NX, NY, NZ;        // nodes per axis
+  int NXP;               // nodes per internal row (NX rounded up to even)
+  int RS;                // doubles per node row in the internal layout (3 NXP)
+  int ntx, nty, nzs;     // CTA tiles in x, y and z segments
+  int zlen;              // node planes per z segment
+  const int4 *plan;      // nullptr, or per CTA {x tile, y tile, k_lo, k_hi} (host-planned waves)
+};
+
+constexpr int kS3PadFront = 16;    // doubles (or nodes) before an internal vector
+constexpr int kS3PadBack = 128;    // doubles (or nodes) after it
+constexpr int kS3RowD = 100;       // doubles staged per node row: 33 nodes + alignment (800 B)
+constexpr int kS3RowN = 34;        // node values staged per row: 33 + alignment (272 B)
+constexpr int kS3NBuf = 2;         // staging depth: plane P is issued ~1.5 layers before it is formed
+
+// One offset of the uniform-box filter stencil (k_filter_s3).
+struct S3FilterOffset {
+  int di, dj, dk;
+  double w;          // H * V
+};
+
+// OC update (kernels_oc.cuh): results and the grid-reduction words.
+struct OcState {
+  double lam, volume_abs, change;
+  int32_t steps, state;   // state: 0 active, 1 inactive, 2 infeasible, -5 NaN
+  int32_t passes;         // passes over the elements (grid-wide reductions)
+  // grid-wide reduction words; zeroed by the host before every launch
+  uint32_t arrive, flag;
+  unsigned long long change_bits;   // max |x_new - x| as the bits of a non-negative double
+  double tot[2][8];
+};
+
+// MINRES (kernels_minres.cuh): device scalars.
+struct MrScalars {
+  double gamma, gamma_old, delta, c, c_old, s, s_old, eta, eta0, thresh;
+  double a1, a2, a3, cn, eta_prev;      // w / x~ update coefficients of the last completed step
+  double bnorm2, tmp;
+  int32_t iter, wx_done, max_iter, done, status, pad;
+  uint32_t counter[6];
+};
+enum { MRC_GAMMA = 0, MRC_DELTA = 1, MRC_WX = 2, MRC_MISC = 3 };
+
+// IC(0) of the rescaled matrix (kernels_ic0.cuh).
+struct Ic0View {
+  int64_t n, nnz;
+  const int64_t *ptr;      // [n+1] lower CSR, columns ascending, diagonal last
+  const int32_t *col;      // [nnz]
+  const int32_t *row;      // [nnz]
+  const int64_t *cptr;     // [nnz+1] contributions of each nonzero
+  const uint64_t *contrib; // element << 16 | (a * ND + b) << 3 | log2(1/w)
+};
+
+}  // namespace tomesh
