@@ -83,7 +83,6 @@ struct S3Smem {
   double own[3][4][TYW * 32];                                 // owned node of plane k mod 3: z_k (3), Dinv
   double xch[2][TYW - 1][3][32];                              // y-exchange (layer parity); row TYW-1 sends to nobody
   unsigned long long mbar[kS3NBuf];
-  int fcnt[kS3NBuf];                                          // warps done forming from each staging buffer
 };
 
 __device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
@@ -238,13 +237,12 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
   if (tid == 0) {
     for (int bb = 0; bb < kS3NBuf; ++bb) {
       mbar_init(&sm.mbar[bb], 1);
-      sm.fcnt[bb] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   // initial staging: planes k_lo-1 .. k_lo-2+NBUF; afterwards plane P is
-  // issued by the last warp to finish forming plane P-NBUF (same buffer)
+  // issued after the CTA barrier that follows the form of plane P-NBUF
   if (tid == 0)
     for (int k = k_lo - 1; k < k_lo - 1 + kS3NBuf; ++k)
       if (staged(k)) s3_issue_plane<TYW, MODE>(sm, buf_of(k), M, i0, j0, k, off, noff);
@@ -313,20 +311,22 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
 #pragma unroll
       for (int d = 0; d < 3; ++d) dst[xe_row][off + 3 * xe_col + d] = pv[d];
     }
-    // staging buffer bb: the last warp done with plane k refills it with
-    // plane k+NBUF (monotone count: round r completes at TYW (r+1))
-    if (tx == 0) {
-      const int round = (k - (k_lo - 1)) / kS3NBuf;
-      int old;
-      asm volatile("atom.acq_rel.cta.shared.add.u32 %0, [%1], 1;\n" : "=r"(old) : "r"(smem_u32(&sm.fcnt[bb])) : "memory");
-      if (old == TYW * (round + 1) - 1 && staged(k + kS3NBuf))
-        s3_issue_plane<TYW, MODE>(sm, bb, M, i0, j0, k + kS3NBuf, off, noff);
-    }
-    __syncwarp();
+  };
+  // staging buffer of plane k is free once every warp has formed plane k,
+  // i.e. after the CTA barrier that follows the form: thread 0 then refills it
+  // with plane k+NBUF (no per-warp completion count on the critical path)
+  auto refill = [&](int k) {
+    if (tid == 0 && staged(k + kS3NBuf)) s3_issue_plane<TYW, MODE>(sm, buf_of(k), M, i0, j0, k + kS3NBuf, off, noff);
   };
   // prologue: planes k_lo-1 .. k_lo+1 (no element has read a ring slot yet)
-  for (int k = k_lo - 1; k <= min(k_lo + 1, k_hi); ++k) form_plane(k, k == k_lo + 1 ? xb : xa);
+  form_plane(k_lo - 1, xa);
+  if (k_lo <= k_hi) form_plane(k_lo, xa);
   __syncthreads();
+  refill(k_lo - 1);
+  refill(k_lo);
+  if (k_lo + 1 <= k_hi) form_plane(k_lo + 1, xb);
+  __syncthreads();
+  refill(k_lo + 1);
 
   // z carry at the face level: the top-face half of layer ek-1's inverse
   // transform (still in the x-y Hadamard basis of the 4 face nodes), added to
@@ -423,6 +423,7 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
     // barrier and overlaps the other warps' element work
     if (ek + 3 <= k_hi) form_plane(ek + 3, x_slot);
     __syncthreads();                                    // the one CTA barrier of the layer
+    refill(ek + 3);
     // node plane ek is complete: (cz=0) parts of layer ek + (cz=1) parts of layer ek-1
     if (qmine) {
       const int64_t dof = s3_row(G, ej, ek) + 3 * ei;
