@@ -263,11 +263,11 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
   double dots[5] = {0.0, 0.0, 0.0, 0.0, 0.0};           // rho, rr, p.q, q.z, q.Dinv q
 
   // form plane k into ring slot k%3.  Every thread forms its own node
-  // (tx, ty), which is the node it owns (if it owns one); the 41 halo nodes of
-  // column 32 and row TYW are spread over lanes 0-5 of all warps so that every
-  // warp does at most two rounds.
-  const int xe = tx * TYW + ty;                         // this thread's extra halo node, if < 33 + TYW
-  const int xe_row = xe < 33 ? TYW : xe - 33, xe_col = xe < 33 ? xe : 32;
+  // (tx, ty), which is the node it owns (if it owns one).  The 41 halo nodes
+  // of row TYW and column 32 go to warp 0, which owns no node (no stores, no
+  // x update): two extra rounds there instead of one divergent round in
+  // every warp.
+  const int xe_row = tx == 0 ? TYW : tx - 1;            // warp 0, round 2 (lanes 0..TYW): column 32
   auto form_plane = [&](int k, double(&xs)[3]) {
     const bool pin = k >= 0 && k < G.NZ;
     const int bb = buf_of(k);
@@ -306,10 +306,15 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
         }
       }
     }
-    if (xe < 33 + TYW) {
-      s3_form_node<TYW, MODE>(sm, bb, xe_row, xe_col, off, noff, alpha_old, beta, pin, rv, pv, dv);
+    if (ty == 0) {
+      s3_form_node<TYW, MODE>(sm, bb, TYW, tx, off, noff, alpha_old, beta, pin, rv, pv, dv);
 #pragma unroll
-      for (int d = 0; d < 3; ++d) dst[xe_row][off + 3 * xe_col + d] = pv[d];
+      for (int d = 0; d < 3; ++d) dst[TYW][off + 3 * tx + d] = pv[d];
+      if (tx <= TYW) {
+        s3_form_node<TYW, MODE>(sm, bb, xe_row, 32, off, noff, alpha_old, beta, pin, rv, pv, dv);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) dst[xe_row][off + 3 * 32 + d] = pv[d];
+      }
     }
   };
   // staging buffer of plane k is free once every warp has formed plane k,
