@@ -297,6 +297,73 @@ int  to_optimize(to_mesh *m, const to_opt_params *params, int32_t n_steps, doubl
                  double *u_dev, to_opt_step *hist, int32_t *steps_done, to_opt_state *state,
                  void *cuda_stream);
 
+/* ---- z-slab sharding of the structured path (one handle per
+ * slab and per GPU) -----------------------------------------------
+ * The path shards with "one exchange step per matvec plus scalar reductions":
+ * the mesh is cut into slabs of node planes along z; rank r OWNS the global
+ * node planes [a_r, b_r) and its handle is uploaded (tomesh_upload) with the
+ * uniform sub-box of element layers [a_r - 2, b_r + 1) (clipped to the mesh),
+ * i.e. two ghost node planes on each interior side, its loads and Dirichlet
+ * DOFs sliced from the global problem.  The exchange is fused into the
+ * iteration kernel (the owners of the boundary planes store r, p and q into
+ * the neighbour's ghost plane: NVLink peer stores when the neighbour is
+ * another GPU) and every scalar reduction is a device-side all-reduce (each
+ * rank pushes its partials into every rank's slots, flags with release
+ * semantics, the ranks sum the slots in rank order), so every rank takes the
+ * same alpha, beta and stop decision and no host sync is added.
+ *
+ * to_shard_buffers  fills this handle's exchange buffers (device addresses on
+ *                   its device; allocates the slots on first use).  Share them
+ *                   with the other ranks: directly within one process, through
+ *                   to_ipc_export / to_ipc_open across processes.
+ * to_shard_attach   makes the handle rank `rank` of `nranks` (<= TO_SHARD_MAX):
+ *                   gz_lo[r] = global node plane of rank r's local plane 0,
+ *                   [own_lo, own_hi) = this rank's owned LOCAL planes (>= 2;
+ *                   rank 0 starts at 0, the last rank ends at its last plane,
+ *                   interior sides need two ghost planes), peers[r] = rank r's
+ *                   buffers as addressable from this handle's device (peers[rank]
+ *                   = its own).  TO_EINVAL on any inconsistency.  Synchronises.
+ * tosolve_cg_group  tosolve_cg on n attached handles of one group in
+ *                   lockstep (n = nranks in one process: several GPUs, or all
+ *                   slabs on one GPU; n = 1 per process when each rank runs in
+ *                   its own process).  Every rank of the group must make the
+ *                   same sequence of group calls.  x_dev[i] are the local
+ *                   element densities, u_dev[i] receives the local u: owned
+ *                   planes and the ghost planes the sensitivities and filter of
+ *                   the owned elements need (a-1, b, b+1).  flags: TO_FIXED_ITERS,
+ *                   TO_HISTORY, TO_PROFILE_LOOP, TO_NO_TRUE_RES (the true residual is
+ *                   not computed: relres_true = -1).  A rank that waits ~20 s
+ *                   for a peer fails with TO_ECUDA instead of hanging.
+ *                   Synchronises every stream.  st[i] per handle (identical
+ *                   iteration counts and residuals on every rank).
+ * After a group solve, to_sensitivity and to_filter on each handle are exact on
+ * its owned elements (the element layers [a_r, b_r)), and to_sensitivity's
+ * compliance_host is this rank's partial sum of f.u over its owned DOFs (the
+ * compliance is the sum over ranks). */
+#define TO_SHARD_MAX 16
+typedef struct {
+  double *rb[2], *pb[2], *qb[2];   /* internal CG vectors (ping-pong)                  */
+  double *x;                       /* internal iterate                                 */
+  double *slots;                   /* [2][TO_SHARD_MAX][8] all-reduce slots            */
+  unsigned long long *flags;       /* [2][TO_SHARD_MAX] sequence flags                 */
+  int32_t nx, ny, nz;              /* node box of the handle                            */
+  int32_t pad;
+  int64_t plane_doubles;           /* doubles per internal node plane                  */
+} to_shard_bufs;
+int  to_shard_buffers(to_mesh *m, to_shard_bufs *out, void *cuda_stream);
+int  to_shard_attach(to_mesh *m, int32_t rank, int32_t nranks, const int32_t *gz_lo, int32_t own_lo,
+                     int32_t own_hi, const to_shard_bufs *peers, void *cuda_stream);
+int  tosolve_cg_group(to_mesh *const *ms, int32_t n, double penal, const double *const *x_dev,
+                      double *const *u_dev, double rtol, int32_t max_iter, uint32_t flags,
+                      to_cg_stats *st, void *const *cuda_streams);
+/* CUDA IPC of a device buffer of the handle (any address inside one of its
+ * allocations): 64-byte handle + byte offset; to_ipc_open maps it on `device`
+ * (peer access enabled lazily) and returns the address of the same byte;
+ * to_ipc_close unmaps (pass the opened address minus the offset). */
+int  to_ipc_export(to_mesh *m, const void *dev_ptr, void *handle64, uint64_t *offset);
+int  to_ipc_open(int device, const void *handle64, uint64_t offset, void **dev_ptr);
+int  to_ipc_close(int device, void *base_ptr);
+
 /* Operator-level entry points (parity and diagnostics; asynchronous).
  * to_apply_A:      q = A v,  A = Pi_F C^T K(x) C Pi_F + (I - Pi_F)  (Eq. 8)
  * to_jacobi_diag:  d = diag(A)  (1 on hanging and fixed DOFs)

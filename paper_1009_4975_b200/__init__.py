@@ -4,7 +4,7 @@ Jacobi-PCG, sensitivities and the volume-weighted filter, as a C-ABI CUDA
 library (libtomesh.so, include/tomesh.h) with a thin Python binding.
 """
 from . import _lib  # noqa: F401
-from . import api, amr  # noqa: F401
+from . import api, amr, shard  # noqa: F401
 from .api import HostMesh, Mesh, CgStats, prepare, tomesh_host_build  # noqa: F401
 from ._lib import (TO_WARM, TO_FIXED_ITERS, TO_HISTORY, TO_NO_TRUE_RES, TO_PROFILE, TO_PROFILE_LOOP,  # noqa: F401
                    TO_FILTER_SENS, TO_FILTER_DENS, TomeshError, TO_PC_JACOBI, TO_PC_IC0,

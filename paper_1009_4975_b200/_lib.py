@@ -105,6 +105,15 @@ class HostArrays(C.Structure):
     ]
 
 
+TO_SHARD_MAX = 16
+
+
+class ToShardBufs(C.Structure):
+    _fields_ = [("rb", P * 2), ("pb", P * 2), ("qb", P * 2), ("x", P), ("slots", P), ("flags", P),
+                ("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("pad", C.c_int32),
+                ("plane_doubles", C.c_int64)]
+
+
 EXPORTS = {
     # name: (restype, argtypes)
     "tomesh_upload": (C.c_int, [C.POINTER(ToMeshDesc), C.c_int, P, C.POINTER(P)]),
@@ -133,6 +142,13 @@ EXPORTS = {
     "to_element_matrix": (C.c_int, [C.c_int32, C.c_double, P]),
     "to_element_hadamard": (C.c_int, [C.c_double, P, P]),
     "to_last_error": (C.c_char_p, []),
+    "to_shard_buffers": (C.c_int, [P, C.POINTER(ToShardBufs), P]),
+    "to_shard_attach": (C.c_int, [P, C.c_int32, C.c_int32, P, C.c_int32, C.c_int32, C.POINTER(ToShardBufs), P]),
+    "tosolve_cg_group": (C.c_int, [P, C.c_int32, C.c_double, P, P, C.c_double, C.c_int32, C.c_uint32,
+                                   C.POINTER(ToCgStats), P]),
+    "to_ipc_export": (C.c_int, [P, P, P, C.POINTER(C.c_uint64)]),
+    "to_ipc_open": (C.c_int, [C.c_int, P, C.c_uint64, C.POINTER(P)]),
+    "to_ipc_close": (C.c_int, [C.c_int, P]),
     "tomesh_host_build": (C.c_int, [C.POINTER(HostSpec), C.POINTER(P)]),
     "tomesh_host_get": (C.c_int, [P, C.POINTER(HostArrays)]),
     "tomesh_host_filter": (C.c_int, [P, C.c_double]),

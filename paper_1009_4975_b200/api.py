@@ -323,6 +323,24 @@ class Mesh:
         L.check(rc, "tosolve_cg")
         return CgStats(st.iters, st.status, st.relres, st.relres_true, st.ms, st.bnorm)
 
+    # -- z-slab sharding (include/tomesh.h to_shard_*; paper_1009_4975_b200.shard) -------
+    def shard_buffers(self, stream=None) -> "L.ToShardBufs":
+        b = L.ToShardBufs()
+        L.check(L.lib().to_shard_buffers(self._h, C.byref(b), _stream(stream)), "to_shard_buffers")
+        return b
+
+    def shard_attach(self, rank, nranks, gz_lo, own_lo, own_hi, peers, stream=None):
+        gz = np.ascontiguousarray(gz_lo, dtype=np.int32)
+        arr = (L.ToShardBufs * nranks)(*peers)
+        L.check(L.lib().to_shard_attach(self._h, int(rank), int(nranks), _ptr(gz), int(own_lo), int(own_hi), arr,
+                                        _stream(stream)), "to_shard_attach")
+
+    def ipc_export(self, dev_ptr):
+        h = (C.c_byte * 64)()
+        off = C.c_uint64()
+        L.check(L.lib().to_ipc_export(self._h, C.c_void_p(dev_ptr), h, C.byref(off)), "to_ipc_export")
+        return bytes(h), int(off.value)
+
     def tosolve_minres(self, penal, x, u, rtol=1e-10, max_iter=20000, precond=0, flags=0, stream=None) -> dict:
         """The paper's solver: MINRES on the rescaled system, precond 0 = rescaling
         only (TO_PC_JACOBI), 1 = IC(0) of the rescaled matrix (TO_PC_IC0)."""
@@ -409,3 +427,27 @@ class Mesh:
     def to_recover(self, v, u, stream=None):
         L.check(L.lib().to_recover(self._h, _dptr(v), _dptr(u), _stream(stream)), "to_recover")
         return u
+
+
+def tosolve_cg_group(meshes, penal, xs, us, rtol=1e-10, max_iter=20000, flags=0, streams=None):
+    """tosolve_cg on attached shard handles in lockstep (include/tomesh.h)."""
+    n = len(meshes)
+    hs = (C.c_void_p * n)(*[m._h for m in meshes])
+    xp = (C.c_void_p * n)(*[_dptr(x) for x in xs])
+    up = (C.c_void_p * n)(*[_dptr(u) for u in us])
+    sp = (C.c_void_p * n)(*[_stream(None if streams is None else streams[i]) for i in range(n)])
+    st = (L.ToCgStats * n)()
+    rc = L.lib().tosolve_cg_group(hs, n, float(penal), xp, up, float(rtol), int(max_iter), int(flags), st, sp)
+    L.check(rc, "tosolve_cg_group")
+    return [CgStats(s.iters, s.status, s.relres, s.relres_true, s.ms, s.bnorm) for s in st]
+
+
+def ipc_open(device, handle: bytes, offset: int) -> int:
+    h = (C.c_byte * 64).from_buffer_copy(handle)
+    p = C.c_void_p()
+    L.check(L.lib().to_ipc_open(int(device), h, C.c_uint64(offset), C.byref(p)), "to_ipc_open")
+    return int(p.value)
+
+
+def ipc_close(device, base_ptr: int):
+    L.check(L.lib().to_ipc_close(int(device), C.c_void_p(base_ptr)), "to_ipc_close")

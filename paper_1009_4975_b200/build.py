@@ -14,9 +14,10 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtomesh.so")
 
-SOURCES = ["tomesh.cu", "tomesh_minres.cu", "tomesh_opt.cu", "host_mesh.cpp", "element.cpp", "errors.cpp"]
+SOURCES = ["tomesh.cu", "tomesh_minres.cu", "tomesh_opt.cu", "tomesh_shard.cu", "host_mesh.cpp", "element.cpp", "errors.cpp"]
 HEADERS = ["common.h", "device_common.cuh", "element.h", "tomesh_types.cuh", "tomesh_impl.cuh", "kernels_cg.cuh",
-           "kernels_general.cuh", "kernels_struct3d.cuh", "kernels_oc.cuh", "kernels_minres.cuh", "kernels_ic0.cuh"]
+           "kernels_general.cuh", "kernels_struct3d.cuh", "kernels_oc.cuh", "kernels_minres.cuh", "kernels_ic0.cuh",
+           "kernels_shard.cuh"]
 
 NVCC_FLAGS = [
     *([f"-DTOMESH_S3_TYW={os.environ['TOMESH_S3_TYW']}"] if os.environ.get("TOMESH_S3_TYW") else []),

@@ -101,14 +101,14 @@ __device__ __forceinline__ void cg_final_step(CgScalars *S, int n_iter, double r
 }
 
 // ||v||^2 -> S->bnorm2 (used for b).
-__global__ void k_norm2_b(int64_t n, const double *__restrict__ v, double *partials, CgScalars *S) {
+static __global__ void k_norm2_b(int64_t n, const double *__restrict__ v, double *partials, CgScalars *S) {
   double acc[1] = {0.0};
   GRID_STRIDE(i, n) { double t = v[i]; acc[0] = fma(t, t, acc[0]); }
   if (grid_sum<1>(acc, partials, &S->counter[CNT_MISC])) S->bnorm2 = acc[0];
 }
 
 // r = r - q on free DOFs (warm start: r = b - A x0); `free` per DOF.
-__global__ void k_sub_masked(int64_t n, const double *__restrict__ q, const uint8_t *__restrict__ free_dof,
+static __global__ void k_sub_masked(int64_t n, const double *__restrict__ q, const uint8_t *__restrict__ free_dof,
                              double *__restrict__ r) {
   GRID_STRIDE(i, n) { r[i] = free_dof[i] ? r[i] - q[i] : 0.0; }
 }
@@ -138,7 +138,7 @@ __global__ void k_rupd(int64_t n, const double *__restrict__ q, const double *__
 }
 
 // sum over free DOFs of (b - t)^2 -> S->tmp[0]
-__global__ void k_resid2(int64_t n, const double *__restrict__ b, const double *__restrict__ t,
+static __global__ void k_resid2(int64_t n, const double *__restrict__ b, const double *__restrict__ t,
                          const uint8_t *__restrict__ free_dof, double *partials, CgScalars *S) {
   double acc[1] = {0.0};
   GRID_STRIDE(i, n) {
@@ -148,7 +148,7 @@ __global__ void k_resid2(int64_t n, const double *__restrict__ b, const double *
 }
 
 // a . b -> S->tmp[slot]
-__global__ void k_dot(int64_t n, const double *__restrict__ a, const double *__restrict__ b, double *partials,
+static __global__ void k_dot(int64_t n, const double *__restrict__ a, const double *__restrict__ b, double *partials,
                       CgScalars *S, int slot) {
   double acc[1] = {0.0};
   GRID_STRIDE(i, n) { acc[0] = fma(a[i], b[i], acc[0]); }
@@ -156,12 +156,12 @@ __global__ void k_dot(int64_t n, const double *__restrict__ a, const double *__r
 }
 
 // q_i = free ? q_i : v_i   (completes A v = Pi_F C^T K C Pi_F v + (I - Pi_F) v)
-__global__ void k_fix_nonfree(int64_t n, const uint8_t *__restrict__ free_dof, const double *__restrict__ v,
+static __global__ void k_fix_nonfree(int64_t n, const uint8_t *__restrict__ free_dof, const double *__restrict__ v,
                               double *__restrict__ q) {
   GRID_STRIDE(i, n) { if (!free_dof[i]) q[i] = v[i]; }
 }
 
-__global__ void k_mask_free(int64_t n, const uint8_t *__restrict__ free_dof, const double *__restrict__ v,
+static __global__ void k_mask_free(int64_t n, const uint8_t *__restrict__ free_dof, const double *__restrict__ v,
                             double *__restrict__ w) {
   GRID_STRIDE(i, n) { w[i] = free_dof[i] ? v[i] : 0.0; }
 }

@@ -79,7 +79,7 @@ __global__ void k_diag_node(int64_t n_node, const int64_t *__restrict__ inc_ptr,
 
 // Dinv = 1/D on free DOFs, 0 elsewhere (the zero doubles as the free mask of the
 // CG loop); d_out (optional) = diag(A) with 1 on non-free DOFs.
-__global__ void k_dinv(int64_t ndof, const uint8_t *__restrict__ free_dof, const double *__restrict__ D,
+static __global__ void k_dinv(int64_t ndof, const uint8_t *__restrict__ free_dof, const double *__restrict__ D,
                        double *__restrict__ Dinv, double *__restrict__ d_out, CgScalars *S) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ndof; i += (int64_t)gridDim.x * blockDim.x) {
     double d = D[i];
@@ -921,7 +921,7 @@ __global__ void k_zp_init(int64_t n_node, const double *__restrict__ r, const do
 
 // ---- sensitivities (a10) ----------------------------------------------------------------
 // 3D: u_e^T K0 u_e from the Hadamard middle product (sum xhat . yhat).
-__global__ void __launch_bounds__(256) k_sens_had3(MeshView M, const double *__restrict__ x,
+static __global__ void __launch_bounds__(256) k_sens_had3(MeshView M, const double *__restrict__ x,
                                                    const double *__restrict__ u, double penal, double E0, double Emin,
                                                    double *__restrict__ dc, const __grid_constant__ K0HadSym H) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M.n_el; e += (int64_t)gridDim.x * blockDim.x) {
@@ -999,7 +999,7 @@ __global__ void k_filter(MeshView M, const int64_t *__restrict__ fptr, const int
 // element (x >= rho_s) lies in e's neighbour list (|c_d - c_e| < r_amr =
 // rmin, self included), else -1; refinement capped at level L, derefinement
 // at level 0.  Integer output, no floating-point decisions beyond x >= rho_s.
-__global__ void k_amr_mark(int64_t n_el, const int8_t *__restrict__ level, int L, const int64_t *__restrict__ fptr,
+static __global__ void k_amr_mark(int64_t n_el, const int8_t *__restrict__ level, int L, const int64_t *__restrict__ fptr,
                            const int32_t *__restrict__ fidx, const double *__restrict__ x, double rho_s,
                            int8_t *__restrict__ marks) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_el; e += (int64_t)gridDim.x * blockDim.x) {

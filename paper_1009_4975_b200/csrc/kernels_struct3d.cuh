@@ -51,6 +51,7 @@
 #include "element.h"
 #include "kernels_cg.cuh"
 #include "kernels_general.cuh"
+#include "kernels_shard.cuh"
 #include "tomesh_types.cuh"
 
 namespace tomesh {
@@ -189,11 +190,17 @@ __device__ __forceinline__ void s3_form_node(const S3Smem<TYW> &sm, int b, int r
 //   4. y-exchange read: q and the dots of the owned node of plane ek
 // (A variant with neighbour-only progress counters instead of the barrier was
 // measured 18% slower: the counter handshakes cost more than the barrier.)
-template <int TYW, int MODE>
+//
+// SHARD (z-slab sharding, kernels_shard.cuh): the owners of planes own_lo and
+// own_hi-1 also store r_k, p_k and q_k into the neighbours' ghost planes, and
+// the last block pushes the 5 partial dots to every rank instead of forming
+// the step (k_shard_step does that once all ranks have arrived).
+template <int TYW, int MODE, bool SHARD = false>
 __global__ void __launch_bounds__(32 * TYW, TYW <= 8 ? 2 : 1)
 k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3Maps M, double *__restrict__ rnew,
            double *__restrict__ pnew, double *__restrict__ x, double *__restrict__ q,
-           const __grid_constant__ K0HadSym H, CgScalars *S, double *partials, int kit, double rtol, double *hist) {
+           const __grid_constant__ K0HadSym H, CgScalars *S, double *partials, int kit, double rtol, double *hist,
+           const __grid_constant__ ShardComm C, unsigned long long seq) {
   constexpr bool CG = MODE == S3_CG;
   pdl_wait();
   pdl_release();
@@ -294,6 +301,19 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
           __stcs(&pnew[dof + d], pv[d]);
           dots[0] = fma(dv * rv[d], rv[d], dots[0]);
           dots[1] = fma(rv[d], rv[d], dots[1]);
+        }
+        if (SHARD) {   // boundary planes also go to the neighbour's ghost plane
+          const int w = kit & 1;
+          double *gr = nullptr, *gp = nullptr;
+          if (k == C.own_lo && C.lo_r[0]) { gr = C.lo_r[w]; gp = C.lo_p[w]; }
+          if (k == C.own_hi - 1 && C.hi_r[0]) { gr = C.hi_r[w]; gp = C.hi_p[w]; }
+          if (gr) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              gr[dof + d] = rv[d];
+              gp[dof + d] = pv[d];
+            }
+          }
         }
         if (xupd) {
           const double *pp = &sm.pa[bb][ty * kS3RowD + off + 3 * tx];
@@ -436,6 +456,10 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
       for (int d = 0; d < 3; ++d) {
         const double qv = a_row[0][d] + sm.xch[ek & 1][ty - 1][d][tx];
         __stcs(&q[dof + d], qv);
+        if (SHARD) {
+          if (ek == C.own_lo && C.lo_q[0]) C.lo_q[kit & 1][dof + d] = qv;
+          if (ek == C.own_hi - 1 && C.hi_q[0]) C.hi_q[kit & 1][dof + d] = qv;
+        }
         if (CG) {
           dots[2] = fma(sm.pn[slo][ty][off + 3 * tx + d], qv, dots[2]);   // p_k of the own node (this thread formed it)
           dots[3] = fma(zown[d], qv, dots[3]);
@@ -450,7 +474,12 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
     if (ek + 1 < k_hi) layer(ek + 1, s_b, xb);
   }
   if (CG) {
-    if (grid_sum<5>(dots, partials, &S->counter[CNT_PQ])) cg_single_step(S, kit, dots, rtol, hist);
+    if (SHARD && ((k_lo <= C.own_lo && C.own_lo < k_hi) || (k_lo <= C.own_hi - 1 && C.own_hi - 1 < k_hi)))
+      __threadfence_system();   // ghost-plane stores before the arrival (header of kernels_shard.cuh)
+    if (grid_sum<5>(dots, partials, &S->counter[CNT_PQ])) {
+      if (SHARD) shard_push(C, seq, dots, 5);
+      else cg_single_step(S, kit, dots, rtol, hist);
+    }
   }
 }
 
@@ -458,10 +487,14 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
 // r_N = r_{N-1} - alpha q_{N-1} (free nodes), x_N = x_{N-1} + alpha p_{N-1},
 // rho_N, rr_N -> cg_final_step.  Coalesced double2 streams; Dinv gathered
 // per node (node = DOF / 3, an L1 hit).  r_N itself is not stored.
+// SHARD: over the owned planes only (the caller offsets the pointers), and
+// the partial rho_N, rr_N are pushed for k_shard_final.
+template <bool SHARD = false>
 __global__ void __launch_bounds__(512) k_final_s3(int n, const double *__restrict__ ro, const double *__restrict__ qo,
                                                   const double *__restrict__ po, const double *__restrict__ dn,
                                                   double *__restrict__ x, double *partials, CgScalars *S, int n_iter,
-                                                  double rtol, double *hist) {
+                                                  double rtol, double *hist, const __grid_constant__ ShardComm C,
+                                                  unsigned long long seq) {
   if (cg_stopped(S)) return;
   const double alpha = __ldcg(&S->alpha);
   double acc[2] = {0.0, 0.0};
@@ -486,7 +519,10 @@ __global__ void __launch_bounds__(512) k_final_s3(int n, const double *__restric
     acc[0] = fma(rv.x, d0 * rv.x, fma(rv.y, d1 * rv.y, acc[0]));
     acc[1] = fma(rv.x, rv.x, fma(rv.y, rv.y, acc[1]));
   }
-  if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) cg_final_step(S, n_iter, acc[0], acc[1], rtol, hist);
+  if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) {
+    if (SHARD) shard_push(C, seq, acc, 2);
+    else cg_final_step(S, n_iter, acc[0], acc[1], rtol, hist);
+  }
 }
 
 // ---- filter on the uniform lattice (a11; Eqs. 3-5) --------------------
@@ -497,13 +533,13 @@ __global__ void __launch_bounds__(512) k_final_s3(int n, const double *__restric
 // quantity (x in for SENS, in for DENS) is scattered to lexicographic order,
 // then each element (canonical order) sums its stencil.
 
-__global__ void k_filter_s3_scatter(int64_t n, const int32_t *__restrict__ perm_el, int mode,
+static __global__ void k_filter_s3_scatter(int64_t n, const int32_t *__restrict__ perm_el, int mode,
                                     const double *__restrict__ x, const double *__restrict__ in,
                                     double *__restrict__ t_lex) {
   GRID_STRIDE(e, n) { t_lex[perm_el[e]] = mode == 0 ? x[e] * in[e] : in[e]; }
 }
 
-__global__ void k_filter_s3(GridView G, int64_t n, const int32_t *__restrict__ perm_el,
+static __global__ void k_filter_s3(GridView G, int64_t n, const int32_t *__restrict__ perm_el,
                             const S3FilterOffset *__restrict__ offs, int n_off, int mode,
                             const double *__restrict__ x, const double *__restrict__ t_lex, double *__restrict__ out) {
   GRID_STRIDE(e, n) {
@@ -526,7 +562,7 @@ __global__ void k_filter_s3(GridView G, int64_t n, const int32_t *__restrict__ p
 // Dynamic AMR marking on the uniform box (reading R21): x scattered to
 // lexicographic order in t_lex, then any solid element within the filter
 // stencil (the same exact |o|^2 h^2 < rmin^2 offsets).  lev = the mesh level.
-__global__ void k_amr_mark_s3(GridView G, int64_t n, const int32_t *__restrict__ perm_el,
+static __global__ void k_amr_mark_s3(GridView G, int64_t n, const int32_t *__restrict__ perm_el,
                               const S3FilterOffset *__restrict__ offs, int n_off, const double *__restrict__ t_lex,
                               double rho_s, int lev, int L, int8_t *__restrict__ marks) {
   GRID_STRIDE(e, n) {
@@ -548,7 +584,7 @@ __global__ void k_amr_mark_s3(GridView G, int64_t n, const int32_t *__restrict__
 // ---- setup kernels of the structured path ------------------------------------------------
 
 // s in lexicographic element order from x in canonical (Morton) element order.
-__global__ void k_simp_s3(int64_t n, const double *__restrict__ x, const int32_t *__restrict__ perm_el,
+static __global__ void k_simp_s3(int64_t n, const double *__restrict__ x, const int32_t *__restrict__ perm_el,
                           double penal, double E0, double Emin, double h, double *__restrict__ s_lex,
                           CgScalars *S) {
   GRID_STRIDE(e, n) {
@@ -561,7 +597,7 @@ __global__ void k_simp_s3(int64_t n, const double *__restrict__ x, const int32_t
 // D = K0_diag * sum of s over the <= 8 elements around each node (all 24
 // diagonal entries of the cube's K0 are equal); Dinv = free ? 1/D : 0 per
 // node; d_out (optional, per DOF) = diag(A) with 1 on non-free DOFs.
-__global__ void k_diag_s3(GridView G, const double *__restrict__ s_lex, const uint8_t *__restrict__ free_node,
+static __global__ void k_diag_s3(GridView G, const double *__restrict__ s_lex, const uint8_t *__restrict__ free_node,
                           double k0d, double *__restrict__ dn, double *__restrict__ d_out, CgScalars *S) {
   const int64_t nn = (int64_t)G.NX * G.NY * G.NZ;
   GRID_STRIDE(n, nn) {
@@ -590,7 +626,7 @@ __global__ void k_diag_s3(GridView G, const double *__restrict__ s_lex, const ui
 }
 
 // out_int[base(n)+c] = mask ? in[n*3+c] : 0   (canonical -> internal)
-__global__ void k_to_int(int64_t n_node, const int32_t *__restrict__ base_of, const double *__restrict__ in,
+static __global__ void k_to_int(int64_t n_node, const int32_t *__restrict__ base_of, const double *__restrict__ in,
                          const uint8_t *__restrict__ free_canon, double *__restrict__ out_int) {
   GRID_STRIDE(n, n_node) {
     const int64_t l = base_of[n];
@@ -603,7 +639,7 @@ __global__ void k_to_int(int64_t n_node, const int32_t *__restrict__ base_of, co
 }
 
 // out[n*3+c] = in_int[base(n)+c]   (internal -> canonical)
-__global__ void k_from_int(int64_t n_node, const int32_t *__restrict__ base_of, const double *__restrict__ in_int,
+static __global__ void k_from_int(int64_t n_node, const int32_t *__restrict__ base_of, const double *__restrict__ in_int,
                            double *__restrict__ out) {
   GRID_STRIDE(n, n_node) {
     const int64_t l = base_of[n];

@@ -104,8 +104,11 @@ int make_tensor_map(CUtensorMap *map, const double *base, uint64_t d0, uint64_t 
 // the CTA count fills whole waves of resident slots; long CTAs are dispatched
 // first, so each slot pairs a long with a short one.  Chosen only if the
 // simulated in-order list schedule beats the uniform segmentation.
-int plan_s3(to_mesh *m, cudaStream_t st) {
+// [z0, z1): the node planes to own (a shard's owned range); force: always
+// install a plan (uniform segments if nothing beats them).
+int plan_s3(to_mesh *m, cudaStream_t st, int z0, int z1, bool force, const int4 **plan_out, int *ncta_out) {
   const GridView &G = m->G;
+  const int NZo = z1 - z0;
   const int slots = kNumSMs * kS3CtasPerSM, over = 3;   // ~3 planes of start-up per CTA
   auto makespan = [&](const std::vector<int> &len) {
     std::vector<int64_t> fin(slots, 0);
@@ -118,10 +121,20 @@ int plan_s3(to_mesh *m, cudaStream_t st) {
     return t_max;
   };
   std::vector<int> uni;
-  for (int z = 0; z < G.nzs; ++z)
-    for (int t = 0; t < G.ntx * G.nty; ++t) uni.push_back(std::min(G.NZ, (z + 1) * G.zlen) - z * G.zlen);
+  std::vector<int4> uni_plan;
+  {
+    const int zl = std::min(G.zlen, NZo), nzs = (NZo + zl - 1) / zl;
+    for (int z = 0; z < nzs; ++z)
+      for (int ty = 0; ty < G.nty; ++ty)
+        for (int tx = 0; tx < G.ntx; ++tx) {
+          const int lo = z0 + z * zl, hi = std::min(z1, lo + zl);
+          uni.push_back(hi - lo);
+          uni_plan.push_back(make_int4(tx, ty, lo, hi));
+        }
+  }
   int64_t best = makespan(uni);
   std::vector<int4> best_plan;
+  if (force) best_plan = uni_plan;
   const int tiles = G.ntx * G.nty;
   for (int W = 1; W <= 6; ++W) {
     const int T = W * slots, n_lo = T / tiles;
@@ -136,8 +149,8 @@ int plan_s3(to_mesh *m, cudaStream_t st) {
           for (int tx = 0; tx < G.ntx; ++tx) {
             const int ns = tx < a ? n_lo + 1 : n_lo;
             if ((pass == 0) != (ns == n_lo) || seg >= ns) continue;
-            const int zl = (G.NZ + ns - 1) / ns;
-            const int lo = seg * zl, hi = std::min(G.NZ, lo + zl);
+            const int zl = (NZo + ns - 1) / ns;
+            const int lo = z0 + seg * zl, hi = std::min(z1, lo + zl);
             if (lo >= hi) continue;
             plan.push_back(make_int4(tx, ty, lo, hi));
             len.push_back(hi - lo);
@@ -152,8 +165,9 @@ int plan_s3(to_mesh *m, cudaStream_t st) {
   if (best_plan.empty()) return 0;
   int4 *d = nullptr;
   RC(upload_array(m, &d, best_plan.data(), best_plan.size(), st));
-  m->G.plan = d;
-  m->s3_ncta = (int)best_plan.size();
+  *plan_out = d;
+  *ncta_out = (int)best_plan.size();
+  if (best_plan.size() * 5 > (size_t)kMaxPartialBlocks * 4) RC(m->alloc(&m->partials, best_plan.size() * 5));
   return 0;
 }
 
@@ -231,7 +245,7 @@ int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof
   const int64_t grid = (int64_t)G.ntx * G.nty * G.nzs;
   if (grid > kMaxPartialBlocks) RC(m->alloc(&m->partials, (size_t)grid * 4));
   m->G = G;
-  if (!std::getenv("TOMESH_S3_NO_PLAN")) RC(plan_s3(m, st));
+  if (!std::getenv("TOMESH_S3_NO_PLAN")) RC(plan_s3(m, st, 0, G.NZ, false, &m->G.plan, &m->s3_ncta));
   m->k0d = m->K3.K[0];
   m->h_struct = m->hL * (double)sz;
   m->structured = true;
@@ -568,7 +582,7 @@ int op_apply(to_mesh *m, const double *in, double *out, cudaStream_t st) {
   M.a = M.q = M.p = M.d = *tin;
   dim3 block(32, kS3TYW);
   k_apply_s3<kS3TYW, S3_PLAIN><<<s3_grid(m), block, sizeof(S3Smem<kS3TYW>), st>>>(
-      m->G, m->s, M, nullptr, nullptr, nullptr, out, m->KS, nullptr, nullptr, 0, 0.0, nullptr);
+      m->G, m->s, M, nullptr, nullptr, nullptr, out, m->KS, nullptr, nullptr, 0, 0.0, nullptr, ShardComm{}, 0ull);
   m->last_launches++;
   return check_launch();
 }
@@ -610,7 +624,7 @@ int op_cg_s3(to_mesh *m, int k, double rtol, cudaStream_t st) {
   dim3 block(32, kS3TYW);
   RC(launch_pdl(k_apply_s3<kS3TYW, S3_CG>, dim3(s3_grid(m)), block, sizeof(S3Smem<kS3TYW>), st, m->G,
                 (const double *)m->s, M, m->rb[w], m->pb[w], m->x, m->qb[w], m->KS, m->S, m->partials, k, rtol,
-                m->hist));
+                m->hist, ShardComm{}, 0ull));
   m->last_launches++;
   return 0;
 }
@@ -618,8 +632,8 @@ int op_cg_s3(to_mesh *m, int k, double rtol, cudaStream_t st) {
 // Structured path, x_N and the final residual after N iterations.
 int op_final_s3(to_mesh *m, int n_iter, double rtol, cudaStream_t st) {
   const int o = (n_iter + 1) & 1;
-  k_final_s3<<<kNumSMs * 4, 512, 0, st>>>((int)m->n_int, m->rb[o], m->qb[o], m->pb[o], m->dn, m->x, m->partials,
-                                          m->S, n_iter, rtol, m->hist);
+  k_final_s3<false><<<kNumSMs * 4, 512, 0, st>>>((int)m->n_int, m->rb[o], m->qb[o], m->pb[o], m->dn, m->x,
+                                                 m->partials, m->S, n_iter, rtol, m->hist, ShardComm{}, 0ull);
   m->last_launches++;
   return check_launch();
 }
@@ -911,6 +925,7 @@ extern "C" int to_sensitivity(to_mesh *m, double penal, const double *x_dev, con
   else k_sens_had3<<<g, kBlock, 0, st>>>(m->view(), x_dev, u_dev, penal, m->E0, m->Emin, dc_dev, m->KS);
   m->launches_total++;
   RC(check_launch());
+  if (compliance_host && m->sharded) return shard_compliance_partial(m, u_dev, compliance_host, st);
   if (compliance_host) {
     m->launches_total++;
     k_dot<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->load, u_dev, m->partials, m->S, 1);

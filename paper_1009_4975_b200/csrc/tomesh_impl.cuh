@@ -108,6 +108,15 @@ struct to_mesh {
   // TMA tensor maps of the internal vectors (structured path): [NZ][NY][RS] doubles
   // (boxes of TYW+1 rows x 100 doubles) and the node array Dinv [NZ][NY][NXP].
   CUtensorMap tm_x, tm_rb[2], tm_qb[2], tm_pb[2], tm_dn;
+  // z-slab sharding (tomesh_shard.cu, kernels_shard.cuh)
+  bool sharded = false;
+  ShardComm SC{};
+  unsigned long long shard_seq = 1;    // sequence number of the next collective (equal on every rank)
+  double *shard_slots = nullptr;       // [2][kShardMax][kShardVals]
+  unsigned long long *shard_flags = nullptr;   // [2][kShardMax]
+  const int4 *shard_plan = nullptr;    // K1 grid over the owned planes
+  int shard_ncta = 0;
+  uint8_t *own_dof = nullptr;          // canonical DOF on an owned plane (compliance partial)
   int last_launches = 0;
   int matvec_variant = 0;
   int64_t launches_total = 0;          // every kernel launched on this handle
@@ -244,3 +253,6 @@ int op_rhs(to_mesh *m, double *b_int, cudaStream_t st);
 int op_apply(to_mesh *m, const double *in, double *out, cudaStream_t st);
 int op_recover_out(to_mesh *m, const double *v_int, double *u_canon, cudaStream_t st);
 int op_resid2_x(to_mesh *m, double *r2, cudaStream_t st);
+int plan_s3(to_mesh *m, cudaStream_t st, int z0, int z1, bool force, const int4 **plan_out, int *ncta_out);
+// sharded handles (tomesh_shard.cu)
+int shard_compliance_partial(to_mesh *m, const double *u_dev, double *out, cudaStream_t st);

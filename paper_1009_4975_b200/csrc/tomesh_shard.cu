@@ -1,0 +1,389 @@
+// libtomesh — z-slab sharding of the structured path: one
+// handle per slab (per GPU), a per-iteration exchange fused into K1 plus
+// device-side scalar all-reduces (kernels_shard.cuh), and the group solve
+// tosolve_cg_group that drives one or several handles in lockstep.
+//
+// Slab layout (the caller's partition, paper_1009_4975_b200/shard.py): rank r
+// owns the global node planes [a_r, b_r); its local box holds the element
+// layers [a_r - 2, b_r + 1) and node planes [a_r - 2, b_r + 2), clipped to the
+// mesh.  With these two ghost layers the Jacobi diagonal of the ghost planes
+// a_r - 1 and b_r (which K1 stages) is complete locally, and after the solve
+// the filter of every owned element finds its neighbours (reach 1 layer,
+// rmin <= 2 element edges) in the local box.
+#include "tomesh_impl.cuh"
+#include "kernels_cg.cuh"
+#include "kernels_shard.cuh"
+#include "kernels_struct3d.cuh"
+
+using namespace tomesh;
+
+namespace {
+
+__global__ void k_own_dof(int64_t n_node, const int32_t *__restrict__ perm_node, int64_t plane_d, int own_lo,
+                          int own_hi, uint8_t *__restrict__ own) {
+  GRID_STRIDE(n, n_node) {
+    const int64_t kp = (int64_t)perm_node[n] / plane_d;
+    const uint8_t o = (kp >= own_lo && kp < own_hi) ? 1 : 0;
+    own[3 * n] = own[3 * n + 1] = own[3 * n + 2] = o;
+  }
+}
+
+__global__ void k_dot_masked(int64_t n, const double *__restrict__ a, const double *__restrict__ b,
+                             const uint8_t *__restrict__ mask, double *partials, CgScalars *S, int slot) {
+  double acc[1] = {0.0};
+  GRID_STRIDE(i, n) {
+    if (mask[i]) acc[0] = fma(a[i], b[i], acc[0]);
+  }
+  if (grid_sum<1>(acc, partials, &S->counter[CNT_MISC2])) S->tmp[slot] = acc[0];
+}
+
+int64_t plane_doubles(const to_mesh *m) { return (int64_t)m->G.NY * m->G.RS; }
+
+int ensure_shard_mem(to_mesh *m, cudaStream_t st) {
+  if (m->shard_slots) return 0;
+  RC(m->alloc(&m->shard_slots, (size_t)2 * kShardMax * kShardVals));
+  RC(m->alloc(&m->shard_flags, (size_t)2 * kShardMax));
+  CK(cudaMemsetAsync(m->shard_slots, 0, sizeof(double) * 2 * kShardMax * kShardVals, st));
+  CK(cudaMemsetAsync(m->shard_flags, 0, sizeof(unsigned long long) * 2 * kShardMax, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+// Iteration k of a sharded solve: K1 (SHARD) then the step.
+int op_cg_s3_shard(to_mesh *m, int k, double rtol, cudaStream_t st) {
+  const int o = (k + 1) & 1, w = k & 1;
+  S3Maps M;
+  M.a = m->tm_rb[o];
+  M.q = m->tm_qb[o];
+  M.p = m->tm_pb[o];
+  M.d = m->tm_dn;
+  GridView G = m->G;
+  G.plan = m->shard_plan;
+  dim3 block(32, kS3TYW);
+  RC(launch_pdl(k_apply_s3<kS3TYW, S3_CG, true>, dim3(m->shard_ncta), block, sizeof(S3Smem<kS3TYW>), st, G,
+                (const double *)m->s, M, m->rb[w], m->pb[w], m->x, m->qb[w], m->KS, m->S, m->partials, k, rtol,
+                m->hist, m->SC, m->shard_seq));
+  m->last_launches++;
+  return 0;
+}
+
+int op_step_shard(to_mesh *m, int k, double rtol, cudaStream_t st) {
+  RC(launch_pdl(k_shard_step, dim3(1), dim3(32), 0, st, m->SC, m->shard_seq, m->S, k, rtol, m->hist));
+  m->shard_seq++;
+  m->last_launches++;
+  return 0;
+}
+
+int check_group(to_mesh *const *ms, int n) {
+  if (!ms || n <= 0) { set_error("empty group"); return TO_EINVAL; }
+  for (int i = 0; i < n; ++i) {
+    if (!ms[i]) { set_error("NULL handle in group"); return TO_EINVAL; }
+    if (!ms[i]->sharded) { set_error("handle %d of the group is not attached (to_shard_attach)", i); return TO_EINVAL; }
+    if (ms[i]->shard_seq != ms[0]->shard_seq) { set_error("group handles out of step (sequence numbers differ)"); return TO_EINVAL; }
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" int to_shard_buffers(to_mesh *m, to_shard_bufs *out, void *cuda_stream) {
+  clear_error();
+  if (!m || !out) { set_error("NULL argument"); return TO_EINVAL; }
+  if (!m->structured) { set_error("sharding needs the structured path (uniform H8 box)"); return TO_EINVAL; }
+  CK(cudaSetDevice(m->device));
+  RC(ensure_shard_mem(m, (cudaStream_t)cuda_stream));
+  std::memset(out, 0, sizeof(*out));
+  for (int w = 0; w < 2; ++w) {
+    out->rb[w] = m->rb[w];
+    out->pb[w] = m->pb[w];
+    out->qb[w] = m->qb[w];
+  }
+  out->x = m->x;
+  out->slots = m->shard_slots;
+  out->flags = m->shard_flags;
+  out->nx = m->G.NX;
+  out->ny = m->G.NY;
+  out->nz = m->G.NZ;
+  out->plane_doubles = plane_doubles(m);
+  return 0;
+}
+
+extern "C" int to_shard_attach(to_mesh *m, int32_t rank, int32_t nranks, const int32_t *gz_lo, int32_t own_lo,
+                               int32_t own_hi, const to_shard_bufs *peers, void *cuda_stream) {
+  clear_error();
+  if (!m || !gz_lo || !peers) { set_error("NULL argument"); return TO_EINVAL; }
+  if (!m->structured) { set_error("sharding needs the structured path (uniform H8 box)"); return TO_EINVAL; }
+  if (nranks < 1 || nranks > kShardMax || rank < 0 || rank >= nranks) {
+    set_error("rank %d of %d outside [0, %d)", rank, nranks, kShardMax);
+    return TO_EINVAL;
+  }
+  const GridView &G = m->G;
+  const int64_t pd = plane_doubles(m);
+  if (own_hi - own_lo < 2 || own_lo < 0 || own_hi > G.NZ) { set_error("owned planes [%d, %d) invalid (>= 2 planes inside the box)", own_lo, own_hi); return TO_EINVAL; }
+  if ((rank > 0) != (own_lo >= 1) || (rank > 0 && own_lo < 2)) { set_error("rank %d needs two ghost planes below its owned range", rank); return TO_EINVAL; }
+  if ((rank < nranks - 1) && own_hi > G.NZ - 2) { set_error("rank %d needs two ghost planes above its owned range", rank); return TO_EINVAL; }
+  if (rank == 0 && own_lo != 0) { set_error("rank 0 must own its first plane"); return TO_EINVAL; }
+  if (rank == nranks - 1 && own_hi != G.NZ) { set_error("the last rank must own its last plane"); return TO_EINVAL; }
+  for (int r = 0; r < nranks; ++r) {
+    const to_shard_bufs &p = peers[r];
+    const bool nb = r == rank - 1 || r == rank + 1;   // neighbours: their vectors are written too
+    if (!p.slots || !p.flags || p.nx != G.NX || p.ny != G.NY || p.plane_doubles != pd ||
+        (nb && (!p.x || !p.rb[0] || !p.rb[1] || !p.pb[0] || !p.pb[1] || !p.qb[0] || !p.qb[1]))) {
+      set_error("peer %d: missing buffers or a different x-y box", r);
+      return TO_EINVAL;
+    }
+  }
+  CK(cudaSetDevice(m->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  RC(ensure_shard_mem(m, st));
+  if (peers[rank].x != m->x || peers[rank].slots != m->shard_slots) { set_error("peers[rank] is not this handle"); return TO_EINVAL; }
+  ShardComm C{};
+  C.rank = rank;
+  C.nranks = nranks;
+  C.own_lo = own_lo;
+  C.own_hi = own_hi;
+  // neighbour r' sees this rank's local plane kp at its own plane kp + gz_lo[rank] - gz_lo[r']
+  auto shifted = [&](double *base, int rp) { return base + (int64_t)(gz_lo[rank] - gz_lo[rp]) * pd; };
+  if (rank > 0) {
+    const to_shard_bufs &p = peers[rank - 1];
+    const int g0 = gz_lo[rank] + own_lo;   // pushed planes g0, g0 + 1 must lie in the lower box's ghost region
+    if (g0 + 1 - gz_lo[rank - 1] >= p.nz) { set_error("lower neighbour box too small"); return TO_EINVAL; }
+    for (int w = 0; w < 2; ++w) {
+      C.lo_r[w] = shifted(p.rb[w], rank - 1);
+      C.lo_p[w] = shifted(p.pb[w], rank - 1);
+      C.lo_q[w] = shifted(p.qb[w], rank - 1);
+    }
+    C.lo_x = shifted(p.x, rank - 1);
+  }
+  if (rank < nranks - 1) {
+    const to_shard_bufs &p = peers[rank + 1];
+    const int g1 = gz_lo[rank] + own_hi - 1;
+    if (g1 - gz_lo[rank + 1] < 0) { set_error("upper neighbour box does not reach below its owned range"); return TO_EINVAL; }
+    for (int w = 0; w < 2; ++w) {
+      C.hi_r[w] = shifted(p.rb[w], rank + 1);
+      C.hi_p[w] = shifted(p.pb[w], rank + 1);
+      C.hi_q[w] = shifted(p.qb[w], rank + 1);
+    }
+    C.hi_x = shifted(p.x, rank + 1);
+  }
+  for (int r = 0; r < nranks; ++r) {
+    C.slots[r] = peers[r].slots;
+    C.flags[r] = peers[r].flags;
+  }
+  C.my_slots = m->shard_slots;
+  C.my_flags = m->shard_flags;
+  RC(plan_s3(m, st, own_lo, own_hi, true, &m->shard_plan, &m->shard_ncta));
+  CK(cudaFuncSetAttribute(k_apply_s3<kS3TYW, S3_CG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)sizeof(S3Smem<kS3TYW>)));
+  if (!m->own_dof) RC(m->alloc(&m->own_dof, (size_t)m->n_dof));
+  k_own_dof<<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->perm_node, pd, own_lo, own_hi, m->own_dof);
+  RC(check_launch());
+  CK(cudaStreamSynchronize(st));
+  m->SC = C;
+  m->sharded = true;
+  m->shard_seq = 1;
+  return 0;
+}
+
+// Compliance partial of a sharded handle: sum of f.u over the owned DOFs.
+int shard_compliance_partial(to_mesh *m, const double *u_dev, double *out, cudaStream_t st) {
+  k_dot_masked<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->load, u_dev, m->own_dof, m->partials, m->S, 1);
+  m->launches_total++;
+  RC(check_launch());
+  CK(cudaMemcpyAsync(m->S_host, m->S, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  *out = m->S_host->tmp[1];
+  return 0;
+}
+
+extern "C" int tosolve_cg_group(to_mesh *const *ms, int32_t n, double penal, const double *const *x_dev,
+                                double *const *u_dev, double rtol, int32_t max_iter, uint32_t flags,
+                                to_cg_stats *st_out, void *const *streams) {
+  clear_error();
+  RC(check_group(ms, n));
+  if (!x_dev || !u_dev || !streams) { set_error("NULL argument"); return TO_EINVAL; }
+  for (int i = 0; i < n; ++i)
+    if (!x_dev[i] || !u_dev[i]) { set_error("NULL density or output of handle %d", i); return TO_EINVAL; }
+  if (!(penal > 0.0)) { set_error("penal must be > 0"); return TO_EINVAL; }
+  if (max_iter < 0) { set_error("max_iter < 0"); return TO_EINVAL; }
+  if (flags & (TO_WARM | TO_PROFILE)) { set_error("TO_WARM / TO_PROFILE are not supported on sharded handles"); return TO_EINVAL; }
+  const bool fixed = (flags & TO_FIXED_ITERS) != 0;
+  const bool hist = (flags & TO_HISTORY) != 0;
+  auto S_ = [&](int i) { return (cudaStream_t)streams[i]; };
+  for (int i = 0; i < n; ++i) {
+    to_mesh *m = ms[i];
+    CK(cudaSetDevice(m->device));
+    m->last_launches = 0;
+    if (hist && max_iter > m->hist_cap) {
+      RC(m->alloc(&m->hist, (size_t)max_iter));
+      m->hist_cap = max_iter;
+    }
+    CK(cudaEventRecord(m->ev0, S_(i)));
+    RC(reset_scalars(m, max_iter, fixed, hist, S_(i)));
+    RC(op_scale_and_diag(m, penal, x_dev[i], nullptr, S_(i)));
+    RC(op_rhs(m, m->rb[1], S_(i)));   // r0 = b (iteration 0 reads rb[1]), ghost planes included
+    CK(cudaMemsetAsync(m->x, 0, sizeof(double) * m->n_int, S_(i)));
+    const int64_t pd = plane_doubles(m), n_own = (int64_t)(m->SC.own_hi - m->SC.own_lo) * pd;
+    k_shard_norm2_push<<<grid_for(n_own), kBlock, 0, S_(i)>>>(n_own, m->rb[1] + m->SC.own_lo * pd, m->partials,
+                                                               m->S, m->SC, m->shard_seq);
+    m->last_launches++;
+    RC(check_launch());
+  }
+  for (int i = 0; i < n; ++i) {
+    to_mesh *m = ms[i];
+    CK(cudaSetDevice(m->device));
+    k_shard_set_bnorm<<<1, 32, 0, S_(i)>>>(m->SC, m->shard_seq, m->S);
+    m->shard_seq++;
+    m->last_launches++;
+    RC(check_launch());
+  }
+  const bool loop_prof = (flags & TO_PROFILE_LOOP) != 0;
+  if (loop_prof)
+    for (int i = 0; i < n; ++i) {
+      CK(cudaSetDevice(ms[i]->device));
+      for (auto &e : ms[i]->loop_ev)
+        if (!e) CK(cudaEventCreate(&e));
+      CK(cudaEventRecord(ms[i]->loop_ev[0], S_(i)));
+    }
+  int launched = 0, chunk = fixed ? std::max(1, max_iter) : 16;
+  bool stop = false;
+  while (!stop && launched < max_iter) {
+    const int cnt = std::min(chunk, max_iter - launched);
+    for (int k = 0; k < cnt; ++k) {
+      for (int i = 0; i < n; ++i) {
+        CK(cudaSetDevice(ms[i]->device));
+        RC(op_cg_s3_shard(ms[i], launched + k, rtol, S_(i)));
+      }
+      for (int i = 0; i < n; ++i) {
+        CK(cudaSetDevice(ms[i]->device));
+        RC(op_step_shard(ms[i], launched + k, rtol, S_(i)));
+      }
+    }
+    RC(check_launch());
+    launched += cnt;
+    if (!fixed) {
+      int done = -1;
+      for (int i = 0; i < n; ++i) {
+        CK(cudaSetDevice(ms[i]->device));
+        RC(read_scalars(ms[i], S_(i)));
+        const int d = (ms[i]->S_host->done || ms[i]->S_host->done_next) ? 1 : 0;
+        if (done >= 0 && d != done) { set_error("sharded solve: ranks disagree on the stop test"); return TO_ECUDA; }
+        done = d;
+      }
+      stop = done == 1;
+      chunk = std::min(chunk * 2, 256);
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    to_mesh *m = ms[i];
+    CK(cudaSetDevice(m->device));
+    if (loop_prof) CK(cudaEventRecord(m->loop_ev[1], S_(i)));
+    const int o = (max_iter + 1) & 1;
+    const int64_t pd = plane_doubles(m), off = m->SC.own_lo * pd, nodes_off = off / 3;
+    const int n_own = (int)((m->SC.own_hi - m->SC.own_lo) * pd);
+    k_final_s3<true><<<kNumSMs * 4, 512, 0, S_(i)>>>(n_own, m->rb[o] + off, m->qb[o] + off, m->pb[o] + off,
+                                                     m->dn + nodes_off, m->x + off, m->partials, m->S, max_iter, rtol,
+                                                     m->hist, m->SC, m->shard_seq);
+    m->last_launches++;
+    RC(check_launch());
+  }
+  for (int i = 0; i < n; ++i) {
+    to_mesh *m = ms[i];
+    CK(cudaSetDevice(m->device));
+    k_shard_final<<<1, 32, 0, S_(i)>>>(m->SC, m->shard_seq, m->S, max_iter, rtol, m->hist);
+    m->shard_seq++;
+    m->last_launches++;
+    RC(check_launch());
+  }
+  // the neighbours' ghost planes of x (sensitivities and filter of their owned elements)
+  for (int i = 0; i < n; ++i) {
+    to_mesh *m = ms[i];
+    CK(cudaSetDevice(m->device));
+    const int64_t pd = plane_doubles(m);
+    k_shard_push_x<<<grid_for(3 * pd), kBlock, 0, S_(i)>>>(m->x, pd, m->partials, m->S, m->SC, m->shard_seq);
+    m->last_launches++;
+    RC(check_launch());
+  }
+  for (int i = 0; i < n; ++i) {
+    to_mesh *m = ms[i];
+    CK(cudaSetDevice(m->device));
+    k_shard_wait<<<1, 32, 0, S_(i)>>>(m->SC, m->shard_seq, m->S);
+    m->shard_seq++;
+    m->last_launches++;
+    RC(check_launch());
+    RC(op_recover_out(m, m->x, u_dev[i], S_(i)));
+    CK(cudaEventRecord(m->ev1, S_(i)));
+  }
+  int rc_all = 0;
+  for (int i = 0; i < n; ++i) {
+    to_mesh *m = ms[i];
+    CK(cudaSetDevice(m->device));
+    CK(cudaStreamSynchronize(S_(i)));
+    RC(read_scalars(m, S_(i)));
+    const CgScalars res = *m->S_host;
+    float ms_ = 0.f;
+    CK(cudaEventElapsedTime(&ms_, m->ev0, m->ev1));
+    if (loop_prof) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, m->loop_ev[0], m->loop_ev[1]));
+      for (int j = 0; j < 4; ++j) m->prof_ms[j] = 0.0;
+      m->prof_ms[4] = std::min(launched, res.iter);
+      m->prof_ms[5] = t;
+    }
+    m->hist_len = hist ? res.iter : 0;
+    m->launches_total += m->last_launches;
+    int rc = res.status;
+    if (rc == 0 && !fixed && !(res.rr <= res.thresh2) && res.bnorm2 > 0.0) rc = TO_NOT_CONVERGED;
+    if (st_out) {
+      st_out[i].iters = res.iter;
+      st_out[i].status = rc;
+      st_out[i].relres = res.bnorm2 > 0.0 ? std::sqrt(res.rr / res.bnorm2) : 0.0;
+      st_out[i].relres_true = -1.0;
+      st_out[i].ms = ms_;
+      st_out[i].bnorm = std::sqrt(res.bnorm2);
+    }
+    if (rc < 0 && rc_all >= 0) rc_all = rc;
+    else if (rc > 0 && rc_all == 0) rc_all = rc;
+  }
+  if (rc_all < 0) set_error("sharded solve failed (status %d)", rc_all);
+  return rc_all;
+}
+
+// ---- CUDA IPC of the exchange buffers (one process per GPU) ---------------------------
+
+extern "C" int to_ipc_export(to_mesh *m, const void *dev_ptr, void *handle64, uint64_t *offset) {
+  clear_error();
+  if (!m || !dev_ptr || !handle64 || !offset) { set_error("NULL argument"); return TO_EINVAL; }
+  for (const DevBuf &b : m->bufs) {
+    const char *base = (const char *)b.p;
+    if ((const char *)dev_ptr >= base && (const char *)dev_ptr < base + b.bytes) {
+      CK(cudaSetDevice(m->device));
+      cudaIpcMemHandle_t h;
+      CK(cudaIpcGetMemHandle(&h, b.p));
+      std::memcpy(handle64, &h, sizeof(h));
+      *offset = (uint64_t)((const char *)dev_ptr - base);
+      return 0;
+    }
+  }
+  set_error("pointer is not inside a buffer of this handle");
+  return TO_EINVAL;
+}
+
+extern "C" int to_ipc_open(int device, const void *handle64, uint64_t offset, void **dev_ptr) {
+  clear_error();
+  if (!handle64 || !dev_ptr) { set_error("NULL argument"); return TO_EINVAL; }
+  CK(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  void *p = nullptr;
+  CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  *dev_ptr = (char *)p + offset;
+  return 0;
+}
+
+extern "C" int to_ipc_close(int device, void *base_ptr) {
+  clear_error();
+  CK(cudaSetDevice(device));
+  CK(cudaIpcCloseMemHandle(base_ptr));
+  return 0;
+}

@@ -43,6 +43,28 @@ constexpr int kS3RowD = 100;       // doubles staged per node row: 33 nodes + al
 constexpr int kS3RowN = 34;        // node values staged per row: 33 + alignment (272 B)
 constexpr int kS3NBuf = 2;         // staging depth: plane P is issued ~1.5 layers before it is formed
 
+// z-slab sharding of the structured path (kernels_shard.cuh).
+// Rank r owns the node planes [own_lo, own_hi) of its local box; the box adds
+// up to two ghost node planes (and element layers) on each side.  Every
+// collective is a push into every rank's slots plus a flag store
+// (release, system scope) and a wait on the local flags (acquire): deterministic
+// (the gather sums the ranks in rank order on every rank).
+constexpr int kShardMax = 16;          // ranks per group
+constexpr int kShardVals = 8;          // doubles per slot
+struct ShardComm {
+  int rank, nranks;
+  int own_lo, own_hi;                  // owned local node planes
+  // neighbours' vectors as seen from this device, pre-offset so that this
+  // rank's internal index i addresses the same global node there (nullptr at
+  // the ends of the stack); [w] = ping-pong buffer w
+  double *lo_r[2], *lo_p[2], *lo_q[2], *lo_x;
+  double *hi_r[2], *hi_p[2], *hi_q[2], *hi_x;
+  double *slots[kShardMax];            // rank r's slots [2][kShardMax][kShardVals]
+  unsigned long long *flags[kShardMax];   // rank r's flags [2][kShardMax]
+  double *my_slots;
+  unsigned long long *my_flags;
+};
+
 // One offset of the uniform-box filter stencil (k_filter_s3).
 struct S3FilterOffset {
   int di, dj, dk;
