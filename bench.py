@@ -9,6 +9,8 @@ recovery, sensitivities + compliance, Eq. 5 filter (rmin = 2).
 
 N > 1 (torchrun): every rank solves its own replica of the workload, no
 collective on the data path ("scaling": "weak"); value = total iterations/s.
+--shard: ONE c5 solve split into z-slabs over the N ranks ("scaling":
+"strong", paper_1009_4975_b200/shard.py).
 --impl reference times the oracle (plain numpy/scipy CPU program) on a
 bounded sample of the same workload, rank 0 only.
 """
@@ -380,6 +382,121 @@ def run_ours(args):
     return 0
 
 
+def run_shard(args):
+    """--shard: ONE c5 solve split into z-slabs over the N ranks (SURVEY §8(e);
+    paper_1009_4975_b200/shard.py): every rank uploads its slab, the ghost
+    planes travel by peer stores fused into K1 (CUDA IPC mappings of the
+    neighbours' buffers) and the dots by the device-side all-reduce.  Strong
+    scaling: value = iterations/s of the one global solve."""
+    import torch
+    import paper_1009_4975_b200 as pb
+    from paper_1009_4975_b200 import shard
+    from inputs import config, density_at
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")          # plumbing only: IPC handles, barriers, the max over ranks
+    dev = torch.device("cuda", local)
+    prob = config("c5")
+    iters = prob.fixed_iters or 500
+    hm = pb.prepare(prob)
+    sr = shard.ShardRank(hm, E0=prob.E0, Emin=prob.Emin, nu=prob.nu, rmin=prob.rmin, device=local)
+    sl, m = sr.slab, sr.mesh
+    stream = torch.cuda.Stream(device=dev)
+    x_glob = density_at(prob, hm.elem_level, hm.elem_anchor)
+    x_host = torch.from_numpy(np.ascontiguousarray(x_glob[sl.elem_global])).pin_memory()
+    x = x_host.to(dev)
+    u = torch.zeros(m.n_dof, dtype=torch.float64, device=dev)
+    dc = torch.empty(m.n_el, dtype=torch.float64, device=dev)
+    dcf = torch.empty_like(dc)
+    flags = pb.TO_FIXED_ITERS
+
+    def step(extra=0):
+        st = sr.solve(prob.penal, x, u, rtol=0.0, max_iter=iters, flags=flags | extra, stream=stream)
+        m.to_sensitivity(prob.penal, x, u, dc, stream=stream)
+        m.to_filter(pb.TO_FILTER_SENS, x, dc, dcf, stream=stream)
+        return st
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    l0 = m.info()["launches_total"]
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    launches = m.info()["launches_total"] - l0
+    barrier()
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1), ws)
+    # end to end: the slab's densities in from pinned host memory, its filtered
+    # sensitivities out, every step
+    dcf_host = torch.empty(m.n_el, dtype=torch.float64).pin_memory()
+    barrier()
+    torch.cuda.synchronize(dev)
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            x.copy_(x_host, non_blocking=True)
+        step()
+        with torch.cuda.stream(stream):
+            dcf_host.copy_(dcf, non_blocking=True)
+    e3.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = max_over_ranks(e2.elapsed_time(e3), ws)
+    # per-rank iteration time (K1 + step kernel), one event pair around the loop
+    step(pb.TO_PROFILE_LOOP)
+    torch.cuda.synchronize(dev)
+    p = m.profile()
+    it_ms = max_over_ranks(p["loop_ms"] / max(1, p["iters"]), ws)
+    own_nodes = int(sl.node_owned.sum())
+    own_el = int(sl.elem_owned.sum())
+    kb = 8 * own_el + 8 * own_nodes + 64 * 3 * own_nodes
+    hbm, peak_kind = _peaks()
+    if rank == 0:
+        line = {
+            "metric": "pcg_iterations_per_sec", "value": iters * args.steps / (ms / 1000.0), "unit": "iterations/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": prob.name, "n_elem": hm.n_el, "n_dof": hm.n_dof, "iters_per_solve": iters,
+                       "step": "simp+diag+rhs+500 PCG its+recover+sens+filter, z-slab sharded",
+                       "parallelism": f"zslab{ws}", "slab_planes": [sl.a, sl.b],
+                       "l2": "inputs larger than L2 at N <= 8 (slab working set >= 160 MB)"},
+            "dof_matvecs_per_sec": iters * args.steps / (ms / 1000.0) * hm.n_dof,
+            "e2e": {"value": iters * args.steps / (e2e_ms / 1000.0), "unit": "iterations/s",
+                    "h2d_bytes_per_step": m.n_el * 8, "d2h_bytes_per_step": m.n_el * 8},
+            "roofline": {"bound": "hbm", "achieved": kb / (it_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": kb / (it_ms / 1000.0) / 1e9 / hbm, "traffic": None,
+                         "kernel": "k_apply_s3<CG, SHARD> + k_shard_step per iteration (rank 0's slab)",
+                         "algorithmic_bytes_per_launch": kb, "avg_launch_ms": it_ms, "peak_source": peak_kind},
+            "cpu_baseline": None, "clocks": clk, "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    sr.close()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -389,9 +506,13 @@ def main():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="split ONE c5 solve into z-slabs over the ranks (strong scaling) instead of replicas")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.shard:
+        return run_shard(args)
     return run_ours(args)
 
 

@@ -86,6 +86,70 @@ __device__ __forceinline__ void cg_single_step(CgScalars *S, int k, const double
   S->beta = rho_next / rho;
 }
 
+// cg_single_step split for the sharded K1, where EVERY CTA of iteration k+1
+// forms the step of iteration k from the same gathered dots (no separate step
+// kernel): cg_step_eval is the pure decision (reads only fields that are
+// constant during the solve, or that every CTA writes with the same value),
+// cg_step_commit writes it to S (one CTA).  Same arithmetic as cg_single_step.
+struct CgStepOut {
+  double alpha, beta, rho, rr, thresh2;
+  int done, fail, early;   // early: k == 0 with a failed status (nothing else is written)
+};
+__device__ __forceinline__ void cg_step_eval(const CgScalars *S, int k, const double (&d)[5], double rtol,
+                                             CgStepOut &o) {
+  const double rho = d[0], rr = d[1], pq = d[2], qz = d[3], qdq = d[4];
+  const double bnorm2 = __ldcg(&S->bnorm2);
+  o.alpha = o.beta = 0.0;
+  o.rho = rho;
+  o.rr = rr;
+  o.done = o.fail = o.early = 0;
+  o.thresh2 = k == 0 ? rtol * rtol * bnorm2 : __ldcg(&S->thresh2);
+  if (k == 0 && __ldcg(&S->status) != 0) {
+    o.done = o.early = 1;
+    return;
+  }
+  if (!(rho == rho) || !(rr == rr) || !(pq == pq) || !(qz == qz) || !(qdq == qdq)) {
+    o.fail = -5;
+    o.done = 1;
+    return;
+  }
+  if ((!S->fixed && rr <= o.thresh2) || bnorm2 == 0.0) {
+    o.done = 1;
+    return;
+  }
+  if (!(pq > 0.0)) {
+    o.fail = -6;
+    o.done = 1;
+    return;
+  }
+  const double alpha = rho / pq;
+  const double rho_next = fma(alpha * alpha, qdq, fma(-2.0 * alpha, qz, rho));
+  o.alpha = alpha;
+  o.beta = rho_next / rho;
+}
+__device__ __forceinline__ void cg_step_commit(CgScalars *S, int k, const CgStepOut &o, double *hist) {
+  if (k == 0) S->thresh2 = o.thresh2;
+  if (o.early) {
+    S->done = 1;
+    return;
+  }
+  S->iter = k;
+  S->rho = o.rho;
+  S->rr = o.rr;
+  if (o.fail) cg_fail(S, o.fail);
+  if (o.fail == -5) {
+    S->done = 1;
+    return;
+  }
+  if (S->history && hist && k >= 1) hist[k - 1] = sqrt(o.rr / S->bnorm2);
+  if (o.done) {
+    S->done = 1;
+    return;
+  }
+  S->alpha = o.alpha;
+  S->beta = o.beta;
+}
+
 // Structured path, final step after N = max_iter iterations (or 0): r_N =
 // r_{N-1} - alpha q_{N-1}, x_N = x_{N-1} + alpha p_{N-1}, rho_N, rr_N.
 // Elementwise over node pairs (no operator needed).

@@ -3,9 +3,10 @@
 // owners of the first and last owned plane also store r_k, p_k and q_k into
 // the neighbour's ghost plane, over NVLink when the neighbour is another GPU),
 // and the scalar all-reduce is a push of each rank's partial dots into every
-// rank's slot array followed by a flag store; the per-iteration step kernel
-// waits for all flags of this sequence number and sums the slots in rank
-// order, so every rank forms the same alpha, beta and stop decision.
+// rank's slot array followed by a flag store; the next K1 waits (one thread
+// per CTA) for all flags of that sequence number and sums the slots in rank
+// order, so every CTA of every rank forms the same alpha, beta and stop
+// decision and an iteration stays one kernel.
 //
 // Ordering: the writer stores its data, fence.sc.sys, then stores the flag
 // with release semantics at system scope; the reader loads the flag with
@@ -68,8 +69,8 @@ __device__ __forceinline__ bool shard_gather(const ShardComm &C, unsigned long l
   return true;
 }
 
-// Iteration k, after K1 pushed its 5 partial dots: the global dots, then the
-// single-kernel CG step (cg_single_step) on every rank alike.
+// The step of the LAST launched iteration k (every earlier step is formed at
+// the start of the next K1): the global dots, then cg_single_step.
 static __global__ void k_shard_step(const __grid_constant__ ShardComm C, unsigned long long seq, CgScalars *S, int k,
                              double rtol, double *hist) {
   pdl_wait();

@@ -194,7 +194,10 @@ __device__ __forceinline__ void s3_form_node(const S3Smem<TYW> &sm, int b, int r
 // SHARD (z-slab sharding, kernels_shard.cuh): the owners of planes own_lo and
 // own_hi-1 also store r_k, p_k and q_k into the neighbours' ghost planes, and
 // the last block pushes the 5 partial dots to every rank instead of forming
-// the step (k_shard_step does that once all ranks have arrived).
+// the step.  Iteration k+1 starts with the step of iteration k: thread 0 of
+// every CTA waits for the flags of sequence seq-1, sums the ranks' dots in
+// rank order and evaluates the step (cg_step_eval, the same on every CTA and
+// rank); CTA 0 also commits it to S.  One kernel per iteration, as unsharded.
 template <int TYW, int MODE, bool SHARD = false>
 __global__ void __launch_bounds__(32 * TYW, TYW <= 8 ? 2 : 1)
 k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3Maps M, double *__restrict__ rnew,
@@ -234,8 +237,30 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
   const int ei = i0 - 1 + tx, ej = j0 - 1 + ty;        // this thread's element column / node column
   const bool col_el = (ei >= 0 && ei < G.EX && ej >= 0 && ej < G.EY);
   const bool owner = (tx >= 1 && ty >= 1 && ei < G.NX && ej < G.NY);
-  const double beta = CG ? __ldcg(&S->beta) : 0.0;
-  const double alpha_old = CG ? __ldcg(&S->alpha) : 0.0;
+  double beta = CG ? __ldcg(&S->beta) : 0.0;
+  double alpha_old = CG ? __ldcg(&S->alpha) : 0.0;
+  if (SHARD && kit > 0) {
+    __shared__ double s_ab[2];
+    __shared__ int s_go;
+    if (tid == 0) {
+      double d[5];
+      CgStepOut o;
+      if (shard_gather(C, seq - 1, d, 5)) {
+        cg_step_eval(S, kit - 1, d, rtol, o);
+      } else {
+        o = CgStepOut{0.0, 0.0, 0.0, 0.0, 0.0, 1, -2, 0};
+        o.thresh2 = __ldcg(&S->thresh2);
+      }
+      if (blockIdx.x == 0) cg_step_commit(S, kit - 1, o, hist);
+      s_ab[0] = o.alpha;
+      s_ab[1] = o.beta;
+      s_go = !o.done;
+    }
+    __syncthreads();
+    if (!s_go) return;
+    alpha_old = s_ab[0];
+    beta = s_ab[1];
+  }
   const bool xupd = CG && owner && alpha_old != 0.0;
   const int64_t plane_d = (int64_t)G.NY * G.RS;        // doubles per node plane
 
@@ -301,19 +326,6 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
           __stcs(&pnew[dof + d], pv[d]);
           dots[0] = fma(dv * rv[d], rv[d], dots[0]);
           dots[1] = fma(rv[d], rv[d], dots[1]);
-        }
-        if (SHARD) {   // boundary planes also go to the neighbour's ghost plane
-          const int w = kit & 1;
-          double *gr = nullptr, *gp = nullptr;
-          if (k == C.own_lo && C.lo_r[0]) { gr = C.lo_r[w]; gp = C.lo_p[w]; }
-          if (k == C.own_hi - 1 && C.hi_r[0]) { gr = C.hi_r[w]; gp = C.hi_p[w]; }
-          if (gr) {
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              gr[dof + d] = rv[d];
-              gp[dof + d] = pv[d];
-            }
-          }
         }
         if (xupd) {
           const double *pp = &sm.pa[bb][ty * kS3RowD + off + 3 * tx];
@@ -456,10 +468,6 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
       for (int d = 0; d < 3; ++d) {
         const double qv = a_row[0][d] + sm.xch[ek & 1][ty - 1][d][tx];
         __stcs(&q[dof + d], qv);
-        if (SHARD) {
-          if (ek == C.own_lo && C.lo_q[0]) C.lo_q[kit & 1][dof + d] = qv;
-          if (ek == C.own_hi - 1 && C.hi_q[0]) C.hi_q[kit & 1][dof + d] = qv;
-        }
         if (CG) {
           dots[2] = fma(sm.pn[slo][ty][off + 3 * tx + d], qv, dots[2]);   // p_k of the own node (this thread formed it)
           dots[3] = fma(zown[d], qv, dots[3]);
@@ -473,9 +481,36 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
     layer(ek, s_a, xa);
     if (ek + 1 < k_hi) layer(ek + 1, s_b, xb);
   }
+  if (SHARD) {
+    // a CTA owning a boundary plane copies its tile of r_k, p_k, q_k there to
+    // the neighbour's ghost plane (row segments, coalesced; the values were
+    // stored by this CTA, so after the barrier they are read back from L2),
+    // then fences at system scope before its arrival (kernels_shard.cuh)
+    const bool lo_b = C.lo_r[0] && k_lo <= C.own_lo && C.own_lo < k_hi;
+    const bool hi_b = C.hi_r[0] && k_lo <= C.own_hi - 1 && C.own_hi - 1 < k_hi;
+    if (lo_b || hi_b) {
+      __syncthreads();
+      const int w = kit & 1;
+      for (int side = 0; side < 2; ++side) {
+        if (!(side ? hi_b : lo_b)) continue;
+        const int kb = side ? C.own_hi - 1 : C.own_lo;
+        double *tr = side ? C.hi_r[w] : C.lo_r[w], *tp = side ? C.hi_p[w] : C.lo_p[w];
+        double *tq = side ? C.hi_q[w] : C.lo_q[w];
+        for (int t = tid; t < (TYW - 1) * 93; t += 32 * TYW) {
+          const int row = t / 93, e = t - 93 * row;
+          const int j = j0 + row, i = i0 + e / 3;
+          if (i < G.NX && j < G.NY) {
+            const int64_t idx = s3_row(G, j, kb) + 3 * i0 + e;
+            tr[idx] = __ldcg(&rnew[idx]);
+            tp[idx] = __ldcg(&pnew[idx]);
+            tq[idx] = __ldcg(&q[idx]);
+          }
+        }
+      }
+      __threadfence_system();
+    }
+  }
   if (CG) {
-    if (SHARD && ((k_lo <= C.own_lo && C.own_lo < k_hi) || (k_lo <= C.own_hi - 1 && C.own_hi - 1 < k_hi)))
-      __threadfence_system();   // ghost-plane stores before the arrival (header of kernels_shard.cuh)
     if (grid_sum<5>(dots, partials, &S->counter[CNT_PQ])) {
       if (SHARD) shard_push(C, seq, dots, 5);
       else cg_single_step(S, kit, dots, rtol, hist);

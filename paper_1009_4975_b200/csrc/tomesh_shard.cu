@@ -63,13 +63,14 @@ int op_cg_s3_shard(to_mesh *m, int k, double rtol, cudaStream_t st) {
   RC(launch_pdl(k_apply_s3<kS3TYW, S3_CG, true>, dim3(m->shard_ncta), block, sizeof(S3Smem<kS3TYW>), st, G,
                 (const double *)m->s, M, m->rb[w], m->pb[w], m->x, m->qb[w], m->KS, m->S, m->partials, k, rtol,
                 m->hist, m->SC, m->shard_seq));
+  m->shard_seq++;   // K1 k pushes this sequence; K1 k+1 gathers it and forms the step of iteration k
   m->last_launches++;
   return 0;
 }
 
+// The step of the last launched iteration k (no K1 follows to form it).
 int op_step_shard(to_mesh *m, int k, double rtol, cudaStream_t st) {
-  RC(launch_pdl(k_shard_step, dim3(1), dim3(32), 0, st, m->SC, m->shard_seq, m->S, k, rtol, m->hist));
-  m->shard_seq++;
+  RC(launch_pdl(k_shard_step, dim3(1), dim3(32), 0, st, m->SC, m->shard_seq - 1, m->S, k, rtol, m->hist));
   m->last_launches++;
   return 0;
 }
@@ -249,16 +250,11 @@ extern "C" int tosolve_cg_group(to_mesh *const *ms, int32_t n, double penal, con
   bool stop = false;
   while (!stop && launched < max_iter) {
     const int cnt = std::min(chunk, max_iter - launched);
-    for (int k = 0; k < cnt; ++k) {
+    for (int k = 0; k < cnt; ++k)
       for (int i = 0; i < n; ++i) {
         CK(cudaSetDevice(ms[i]->device));
         RC(op_cg_s3_shard(ms[i], launched + k, rtol, S_(i)));
       }
-      for (int i = 0; i < n; ++i) {
-        CK(cudaSetDevice(ms[i]->device));
-        RC(op_step_shard(ms[i], launched + k, rtol, S_(i)));
-      }
-    }
     RC(check_launch());
     launched += cnt;
     if (!fixed) {
@@ -274,6 +270,11 @@ extern "C" int tosolve_cg_group(to_mesh *const *ms, int32_t n, double penal, con
       chunk = std::min(chunk * 2, 256);
     }
   }
+  if (launched > 0)
+    for (int i = 0; i < n; ++i) {
+      CK(cudaSetDevice(ms[i]->device));
+      RC(op_step_shard(ms[i], launched - 1, rtol, S_(i)));
+    }
   for (int i = 0; i < n; ++i) {
     to_mesh *m = ms[i];
     CK(cudaSetDevice(m->device));

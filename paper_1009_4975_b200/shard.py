@@ -172,7 +172,8 @@ class ShardRank:
     def __init__(self, host: HostMesh, E0=1.0, Emin=1e-9, nu=0.3, rmin=None, device=0, group=None):
         import torch.distributed as dist
         check_filter_reach(host)
-        rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+        single = not (dist.is_available() and dist.is_initialized())
+        rank, nranks = (0, 1) if single else (dist.get_rank(group), dist.get_world_size(group))
         self.slab = slice_host(host, nranks, rank)
         self.mesh = Mesh(self.slab.host, E0=E0, Emin=Emin, nu=nu, rmin=rmin, device=device)
         self.device = device
@@ -188,7 +189,10 @@ class ShardRank:
                     "plane": mine.plane_doubles,
                     "ipc": [self.mesh.ipc_export(ptr(mine, f, i)) for f, i in fields]}
         allx = [None] * nranks
-        dist.all_gather_object(allx, exported, group=group)
+        if single:
+            allx[0] = exported
+        else:
+            dist.all_gather_object(allx, exported, group=group)
         self._opened = []
         peers = []
         for r, ex in enumerate(allx):
@@ -213,7 +217,8 @@ class ShardRank:
             peers.append(b)
         gz = [ex["gz_lo"] for ex in allx]
         self.mesh.shard_attach(rank, nranks, gz, self.slab.own_lo, self.slab.own_hi, peers)
-        dist.barrier(group=group)
+        if not single:
+            dist.barrier(group=group)
 
     def solve(self, penal, x, u, rtol=1e-10, max_iter=20000, flags=0, stream=None):
         return tosolve_cg_group([self.mesh], penal, [x], [u], rtol, max_iter, flags | L.TO_NO_TRUE_RES,
