@@ -21,6 +21,7 @@ HEADERS = ["common.h", "device_common.cuh", "element.h", "tomesh_types.cuh", "to
 
 NVCC_FLAGS = [
     *([f"-DTOMESH_S3_TYW={os.environ['TOMESH_S3_TYW']}"] if os.environ.get("TOMESH_S3_TYW") else []),
+    *os.environ.get("TOMESH_NVCC_EXTRA", "").split(),   # experiments (e.g. -DTOMESH_LANES_MINB=5)
     "-O3", "-std=c++17", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-Xcompiler", "-fPIC,-fopenmp,-O3",

@@ -9,6 +9,9 @@
 //   k_sens        a10 dc_e = -p x^(p-1)(E0-Emin) h^(d-2) u_e^T K0 u_e    (:343-346)
 //   k_filter      a11 Eq. 5 / density variant                             (:613-616)
 #pragma once
+#ifndef TOMESH_LANES_MINB
+#define TOMESH_LANES_MINB 1   // min resident blocks of the general-path lane passes (register cap)
+#endif
 #include <cooperative_groups.h>
 
 #include "device_common.cuh"
@@ -651,7 +654,7 @@ __device__ __forceinline__ double g_elem_lane(const MeshView &M, int64_t e, int 
 }
 
 template <int DIM, int MODE>
-__global__ void __launch_bounds__(256) k_elem_pass_lanes(MeshView M, const double *__restrict__ s,
+__global__ void __launch_bounds__(256, TOMESH_LANES_MINB) k_elem_pass_lanes(MeshView M, const double *__restrict__ s,
                                                          const double *__restrict__ zp, const double *__restrict__ po,
                                                          double *__restrict__ ye,
                                                          const __grid_constant__ K0Dense2 K2,
@@ -772,7 +775,7 @@ __device__ __forceinline__ void g_node_group(int64_t n, bool live, int l, const 
 // ... of the node, an xor-shuffle tree completes q_n in every lane of the
 // group, and lane i < DIM updates component i of the node (record, x, r).
 template <int DIM, int MODE>
-__global__ void __launch_bounds__(256) k_node_pass_lanes(int64_t n_node, const int64_t *__restrict__ inc_ptr,
+__global__ void __launch_bounds__(256, TOMESH_LANES_MINB) k_node_pass_lanes(int64_t n_node, const int64_t *__restrict__ inc_ptr,
                                                          const uint32_t *__restrict__ inc, const double *__restrict__ ye,
                                                          double *__restrict__ r, const double *__restrict__ Dinv,
                                                          double *__restrict__ zp, double *__restrict__ x,

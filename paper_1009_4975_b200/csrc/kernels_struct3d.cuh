@@ -246,6 +246,9 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
       double d[5];
       CgStepOut o;
       if (shard_gather(C, seq - 1, d, 5)) {
+        // the neighbours' ghost planes (generic stores, ordered before their
+        // flags) are read below by TMA (async proxy): cross-proxy fence
+        asm volatile("fence.proxy.async;\n" ::: "memory");
         cg_step_eval(S, kit - 1, d, rtol, o);
       } else {
         o = CgStepOut{0.0, 0.0, 0.0, 0.0, 0.0, 1, -2, 0};
