@@ -179,6 +179,10 @@ extern "C" int to_shard_attach(to_mesh *m, int32_t rank, int32_t nranks, const i
   if (!m->own_dof) RC(m->alloc(&m->own_dof, (size_t)m->n_dof));
   k_own_dof<<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->perm_node, pd, own_lo, own_hi, m->own_dof);
   RC(check_launch());
+  // a (re)attached group restarts its sequence numbers at 1: clear this
+  // handle's flags so that no flag of an earlier attachment can match
+  // (every rank attaches before any rank solves; ShardRank barriers on it)
+  CK(cudaMemsetAsync(m->shard_flags, 0, sizeof(unsigned long long) * 2 * kShardMax, st));
   CK(cudaStreamSynchronize(st));
   m->SC = C;
   m->sharded = true;
