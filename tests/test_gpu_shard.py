@@ -91,6 +91,13 @@ def test_sharded_fixed_iterations_and_repeat():
         assert all(s.iters == 40 and s.status == 0 for s in sts)
         runs.append(g.gather_nodes(us))
     assert np.array_equal(runs[0], runs[1])
+    # re-attaching the whole group restarts the sequence numbers (flags cleared)
+    bufs = [m.shard_buffers() for m in g.meshes]
+    for sl, m in zip(g.slabs, g.meshes):
+        m.shard_attach(sl.rank, 3, [t.gz_lo for t in g.slabs], sl.own_lo, sl.own_hi, bufs)
+    us = [torch.zeros(m.n_dof, dtype=torch.float64, device="cuda") for m in g.meshes]
+    g.solve(prob.penal, xs, us, max_iter=40, flags=pb.TO_FIXED_ITERS)
+    assert np.array_equal(g.gather_nodes(us), runs[0])
     m1 = pb.Mesh(hm, E0=prob.E0, Emin=prob.Emin, nu=prob.nu, rmin=prob.rmin)
     u1 = torch.zeros(hm.n_dof, dtype=torch.float64, device="cuda")
     m1.tosolve_cg(prob.penal, cuda(x), u1, max_iter=40, flags=pb.TO_FIXED_ITERS)
