@@ -356,22 +356,42 @@ extern "C" int tosolve_cg_group(to_mesh *const *ms, int32_t n, double penal, con
 
 // ---- CUDA IPC of the exchange buffers (one process per GPU) ---------------------------
 
+// The driver may place several small cudaMalloc allocations in one IPC-able
+// block, and an IPC handle maps the whole block: the offset is taken from the
+// block's base as the driver reports it (cuMemGetAddressRange).
+using PFN_memrange = CUresult (*)(CUdeviceptr *, size_t *, CUdeviceptr);
+static PFN_memrange mem_range_fn() {
+  static PFN_memrange fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_memrange)p;
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
 extern "C" int to_ipc_export(to_mesh *m, const void *dev_ptr, void *handle64, uint64_t *offset) {
   clear_error();
   if (!m || !dev_ptr || !handle64 || !offset) { set_error("NULL argument"); return TO_EINVAL; }
-  for (const DevBuf &b : m->bufs) {
-    const char *base = (const char *)b.p;
-    if ((const char *)dev_ptr >= base && (const char *)dev_ptr < base + b.bytes) {
-      CK(cudaSetDevice(m->device));
-      cudaIpcMemHandle_t h;
-      CK(cudaIpcGetMemHandle(&h, b.p));
-      std::memcpy(handle64, &h, sizeof(h));
-      *offset = (uint64_t)((const char *)dev_ptr - base);
-      return 0;
-    }
-  }
-  set_error("pointer is not inside a buffer of this handle");
-  return TO_EINVAL;
+  bool mine = false;
+  for (const DevBuf &b : m->bufs)
+    if ((const char *)dev_ptr >= (const char *)b.p && (const char *)dev_ptr < (const char *)b.p + b.bytes) mine = true;
+  if (!mine) { set_error("pointer is not inside a buffer of this handle"); return TO_EINVAL; }
+  CK(cudaSetDevice(m->device));
+  auto range = mem_range_fn();
+  if (!range) { set_error("cuMemGetAddressRange unavailable"); return TO_ECUDA; }
+  CUdeviceptr base = 0;
+  size_t bytes = 0;
+  if (range(&base, &bytes, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS) { set_error("cuMemGetAddressRange failed"); return TO_ECUDA; }
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, (void *)base));
+  std::memcpy(handle64, &h, sizeof(h));
+  *offset = (uint64_t)((CUdeviceptr)dev_ptr - base);
+  return 0;
 }
 
 extern "C" int to_ipc_open(int device, const void *handle64, uint64_t offset, void **dev_ptr) {

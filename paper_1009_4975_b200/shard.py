@@ -194,6 +194,14 @@ class ShardRank:
         else:
             dist.all_gather_object(allx, exported, group=group)
         self._opened = []
+        opened = {}   # one mapping per IPC handle (small buffers may share an allocation block)
+
+        def open_ptr(h, off):
+            if h not in opened:
+                opened[h] = ipc_open(device, h, 0)
+                self._opened.append(opened[h])
+            return opened[h] + off
+
         peers = []
         for r, ex in enumerate(allx):
             b = L.ToShardBufs()
@@ -205,9 +213,7 @@ class ShardRank:
             vals = {}
             for k in need:
                 h, off = ex["ipc"][k]
-                p = ipc_open(device, h, off)
-                self._opened.append(p - off)
-                vals[k] = p
+                vals[k] = open_ptr(h, off)
             for k, (f, i) in enumerate(fields):
                 p = vals.get(k, 0)
                 if f in ("rb", "pb", "qb"):

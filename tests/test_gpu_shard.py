@@ -138,3 +138,30 @@ def test_sharded_errors():
     # the group recovers: a valid solve right after
     sts = g.solve(prob.penal, xs, us, rtol=1e-10, max_iter=50000)
     assert sts[0].status == 0 and rel(g.gather_nodes(us), ref.u) <= 1e-8
+
+
+def test_ipc_export_open_in_another_process():
+    """CUDA IPC of the exchange buffers (the one-process-per-GPU form): the
+    handle + offset of two addresses inside one buffer reopen in another
+    process at the same distance (no kernel runs; nobody waits)."""
+    import subprocess
+    import sys
+    prob, om, x, ref, hm = _ref("c5s")
+    m = pb.Mesh(hm, E0=prob.E0, Emin=prob.Emin, nu=prob.nu, rmin=prob.rmin)
+    b = m.shard_buffers()
+    h1, o1 = m.ipc_export(b.x)
+    h2, o2 = m.ipc_export(b.x + 64)
+    assert o2 - o1 == 64
+    hs, os_ = m.ipc_export(b.slots)
+    assert h1 == h2                                                       # one allocation, one handle
+    code = ("import sys; import paper_1009_4975_b200 as pb; import torch; torch.cuda.init();"
+            "a = pb.api.ipc_open(0, bytes.fromhex(sys.argv[1]), int(sys.argv[2]));"
+            "pb.api.ipc_close(0, a - int(sys.argv[2])); print(a % 8)")
+    r = subprocess.run([sys.executable, "-c", code, h1.hex(), str(o1)], capture_output=True,
+                       text=True, timeout=300, cwd=__import__("os").path.dirname(__import__("os").path.dirname(
+                           __import__("os").path.abspath(__file__))))
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert int(r.stdout.strip().splitlines()[-1]) == 0                     # an aligned double address
+    with pytest.raises(pb.TomeshError):                                   # not a buffer of this handle
+        m.ipc_export(xs_ptr := torch.zeros(8, dtype=torch.float64, device="cuda").data_ptr())
+    assert hs and os_ >= 0 and xs_ptr
