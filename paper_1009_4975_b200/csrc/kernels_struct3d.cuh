@@ -35,15 +35,18 @@
 //    every node is written by exactly one thread, so the result is
 //    deterministic.  The halo element row/column of each patch is recomputed
 //    instead of exchanged.
-//  * The r, p_{k-1} and Dinv plane tiles (33 x (TYW+1) nodes) arrive by TMA
-//    1D bulk copies (cp.async.bulk, one row each, issued by one thread,
-//    completion on an mbarrier), NBUF planes ahead of the compute.  p_k is
-//    formed from them in shared memory (two planes live), so the gather of
-//    the element corners never touches global memory.
+//  * The r_{k-1}, q_{k-1}, p_{k-1} and Dinv plane tiles (33 x (TYW+1) nodes)
+//    arrive as TMA boxes (cp.async.bulk.tensor.3d over tensor maps encoded at
+//    upload, out-of-range rows and columns zero-filled), issued by one thread
+//    with completion on an mbarrier, NBUF planes ahead of the compute; a
+//    buffer is refilled right after the layer barrier that follows its form.
+//    p_k is formed from them into a 4-plane shared-memory ring, so the gather
+//    of the element corners never touches global memory.
 //  * The element product uses the Hadamard factorisation of K0 (element.h):
 //    ~215 fp64 operations instead of 576 FMAs.
-//  * p.q of the owned nodes is reduced in the same kernel (last-block-done),
-//    and the last block forms alpha = rho / p.q (CG scalars stay on device).
+//  * The 5 dots of the owned nodes are reduced in the same kernel
+//    (last-block-done), and the last block forms the step (CG scalars stay on
+//    device; sharded: the partials go to every rank, kernels_shard.cuh).
 #pragma once
 #include <cuda.h>
 
