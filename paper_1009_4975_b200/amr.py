@@ -28,17 +28,25 @@ class AmrRun:
 
 def optimize_amr(problem, volfrac, n_steps, penal0=1.0, penal_max=3.0, penal_step=0.5, stage_steps=30,
                  rho_s=0.5, min_steps=5, max_steps=10, change_tol=0.01, rtol=1e-10, max_iter=20000,
-                 device=0, x0=None, mode="dynamic", stop_on_converge=False, level_steps=150) -> AmrRun:
+                 device=0, x0=None, mode="dynamic", stop_on_converge=False, level_steps=150,
+                 stop_rule="mesh") -> AmrRun:
     """mode "dynamic": the paper's strategy (§4).  mode "static": the
     refine-only baseline the paper argues against (Costa/Stainko, PAPER.md:
     754-790): optimise to convergence at p_max, refine the marked elements
     (no derefinement; after at most level_steps steps on a level if it does not
     converge), repeat until nothing is refined.  stop_on_converge:
     end when the design change is < change_tol at p_max and the adaptation
-    that follows would not change the mesh."""
+    that follows would not change the mesh (stop_rule "mesh"),
+    or (stop_rule "design", reading R25) when the design converges
+    again within min_steps steps of an adaptation that was itself made at a
+    converged design: "if the local minimum is not an artifact of the mesh,
+    the design will remain the same after mesh adaptation"."""
     static = mode == "static"
     if mode not in ("dynamic", "static"):
         raise ValueError("mode must be 'dynamic' or 'static'")
+    if stop_rule not in ("mesh", "design"):
+        raise ValueError("stop_rule must be 'mesh' or 'design'")
+    last_adapt_at_conv = False
     import torch
     dev = torch.device("cuda", device)
     host = prepare(problem, keep_handle=True)
@@ -64,6 +72,9 @@ def optimize_amr(problem, volfrac, n_steps, penal0=1.0, penal_max=3.0, penal_ste
         converged = bool(state.converged)
         if done >= n_steps or (not static and not state.adapt_due and not converged):
             break                                        # step budget used up
+        if (converged and not static and stop_rule == "design" and last_adapt_at_conv
+                and state.since_adapt <= min_steps):
+            break                                        # re-converged right after a converged adaptation
         t0 = time.perf_counter()
         marks = torch.empty(host.n_el, dtype=torch.int8, device=dev)
         mesh.to_amr_mark(x, marks, rho_s)
@@ -92,6 +103,7 @@ def optimize_amr(problem, volfrac, n_steps, penal0=1.0, penal_max=3.0, penal_ste
                                 "n_unmarked_incompat": ad.n_unmarked_incompat,
                                 "mark_s": t1 - t0, "host_adapt_rebuild_s": t2 - t1, "upload_s": t3 - t2})
         run.steps[-1]["adapted"] = True
+        last_adapt_at_conv = converged
         state.since_adapt = 0
         state.adapt_due = 0
     mesh.close()

@@ -84,3 +84,14 @@ def test_static_refine_only_and_stop_on_converge():
     assert len(run.steps) == 300 or (last["penal"] == 3.0 and last["change"] < 0.02)
     with pytest.raises(ValueError):
         pb.amr.optimize_amr(prob, 0.5, 5, mode="bogus")
+    with pytest.raises(ValueError):
+        pb.amr.optimize_amr(prob, 0.5, 5, stop_rule="bogus")
+    # reading R25: stop once the design re-converges within min_steps of a
+    # converged adaptation (never later than the mesh rule on the same run)
+    run2 = pb.amr.optimize_amr(prob, 0.5, 300, stop_on_converge=True, change_tol=0.02, rtol=1e-10,
+                               stop_rule="design")
+    last = run2.steps[-1]
+    assert len(run2.steps) == 300 or (last["penal"] == 3.0 and last["change"] < 0.02)
+    assert len(run2.steps) <= len(run.steps)
+    # the two rules see the same (deterministic) trajectory until the design rule stops
+    assert [t["compliance"] for t in run2.steps] == [t["compliance"] for t in run.steps[:len(run2.steps)]]

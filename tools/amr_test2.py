@@ -11,7 +11,8 @@ Prints one JSON line: total device-side wall time, CG iterations, element /
 DOF counts of both runs, the compliance of each, and the design difference D
 of Eq. 10 between the final designs on the fine lattice.
 
-    python tools/amr_test2.py [steps] [rmin] [change_tol]   (change_tol > 0: run to convergence at p = 3)
+    python tools/amr_test2.py [steps] [rmin] [change_tol] [stop_rule]
+    (change_tol > 0: run to convergence at p = 3; stop_rule "mesh" (default) or "design")
 """
 import json
 import os
@@ -53,6 +54,7 @@ def main():
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 60
     rmin = float(sys.argv[2]) if len(sys.argv) > 2 else 1.5
     tol = float(sys.argv[3]) if len(sys.argv) > 3 else 0.0
+    stop_rule = sys.argv[4] if len(sys.argv) > 4 else "mesh"
     conv = tol > 0
     volfrac, stage = 0.25, 12
     # uniform fine mesh
@@ -71,7 +73,7 @@ def main():
     pa = problem(True, rmin)
     t0 = time.perf_counter()
     run = pb.amr.optimize_amr(pa, volfrac, steps, stage_steps=stage, rtol=1e-8, stop_on_converge=conv,
-                              change_tol=tol if conv else 0.01)
+                              change_tol=tol if conv else 0.01, stop_rule=stop_rule)
     torch.cuda.synchronize()
     wall_a = time.perf_counter() - t0
     ru = raster(hu, xu.cpu().numpy())
@@ -79,6 +81,7 @@ def main():
     D = float(np.abs(ru - ra).sum() / ru.sum())
     line = {
         "workload": "test2_cantilever3d_128x32x32", "step_cap": steps, "rmin": rmin, "change_tol": tol,
+        "stop_rule": stop_rule,
         "volfrac": volfrac,
         "uniform": {"steps": len(hist_u), "n_elem": hu.n_el, "n_dof": hu.n_dof, "wall_s": wall_u,
                     "solve_ms": float(sum(h["solve_ms"] for h in hist_u)),

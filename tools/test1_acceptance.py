@@ -19,7 +19,7 @@ the mesh would not change) or after `steps` design steps.
 
 D is Eq. 10 on the fine lattice.  Prints one JSON line.
 
-    python tools/test1_acceptance.py [steps] [rmin] [change_tol]
+    python tools/test1_acceptance.py [steps] [rmin] [change_tol] [stop_rule]
 """
 import json
 import os
@@ -68,6 +68,7 @@ def main():
     cap = int(sys.argv[1]) if len(sys.argv) > 1 else 400
     rmin = float(sys.argv[2]) if len(sys.argv) > 2 else 1.5
     tol = float(sys.argv[3]) if len(sys.argv) > 3 else 0.01
+    stop_rule = sys.argv[4] if len(sys.argv) > 4 else "mesh"
     volfrac = 0.5
     pu = problem(False, rmin)
     hu = pb.prepare(pu)
@@ -81,11 +82,13 @@ def main():
         h["n_dof"] = hu.n_dof
     ru = raster(hu, xu.cpu().numpy())
     out = {"workload": "test1_cantilever2d_128x64", "step_cap": cap, "rmin": rmin, "change_tol": tol,
+           "stop_rule": stop_rule,
            "uniform": summary(hist_u, hu, wall_u)}
     pa = problem(True, rmin)
     for mode in ("dynamic", "static"):
         t0 = time.perf_counter()
-        run = pb.amr.optimize_amr(pa, volfrac, cap, mode=mode, stop_on_converge=True, change_tol=tol, rtol=1e-8)
+        run = pb.amr.optimize_amr(pa, volfrac, cap, mode=mode, stop_on_converge=True, change_tol=tol, rtol=1e-8,
+                                  stop_rule=stop_rule)
         wall = time.perf_counter() - t0
         ra = raster(run.host, run.x.cpu().numpy())
         out[mode] = summary(run.steps, run.host, wall)
