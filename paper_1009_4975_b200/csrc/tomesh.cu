@@ -408,6 +408,10 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
   }
   if (!m->structured) {
     RC(setup_incidence(d, node_hang, st, m));
+    if (std::getenv("TOMESH_GENERAL_ATOMIC")) {   // experiment: see k_node_pass_atom
+      RC(m->alloc(&m->qacc, (size_t)m->n_dof));
+      CK(cudaMemsetAsync(m->qacc, 0, sizeof(double) * m->n_dof, st));
+    }
     // launched passes: one resident wave (the end-of-pass reduction then runs once per block slot)
     {
       int pe = 0, pn = 0;
@@ -598,6 +602,23 @@ int op_cg_general(to_mesh *m, cudaStream_t st) {
   double *p = m->pb[0];
   const double *no_po = nullptr;
   double *no_q = nullptr;
+  if (m->qacc) {   // TOMESH_GENERAL_ATOMIC experiment: atomic scatter into q, streaming node pass
+    const int gd = std::min(grid_for(m->n_dof, kBlock, 8), m->gn_blocks);
+    if (m->dim == 2)
+      RC(launch_pdl(k_elem_pass_lanes<2, G_CG, true>, dim3(ge4), dim3(kBlock), 0, st, m->view(), m->s, m->zp, no_po,
+                    m->qacc, m->K2, m->KS, m->hmask, m->S, m->partials));
+    else
+      RC(launch_pdl(k_elem_pass_lanes<3, G_CG, true>, dim3(ge8), dim3(kBlock), 0, st, m->view(), m->s, m->zp, no_po,
+                    m->qacc, m->K2, m->KS, m->hmask, m->S, m->partials));
+    if (m->dim == 2)
+      RC(launch_pdl(k_node_pass_atom<2>, dim3(gd), dim3(kBlock), 0, st, m->n_dof, m->qacc, m->r, m->dinv, m->zp,
+                    m->x, m->partials, m->S, m->hist));
+    else
+      RC(launch_pdl(k_node_pass_atom<3>, dim3(gd), dim3(kBlock), 0, st, m->n_dof, m->qacc, m->r, m->dinv, m->zp,
+                    m->x, m->partials, m->S, m->hist));
+    m->last_launches += 2;
+    return 0;
+  }
   if (m->dim == 2) {
     RC(launch_pdl(k_elem_pass_lanes<2, G_CG>, dim3(ge4), dim3(kBlock), 0, st, m->view(), m->s, m->zp, no_po, m->ye,
                   m->K2, m->KS, m->hmask, m->S, m->partials));

@@ -56,6 +56,7 @@ struct to_mesh {
   double *ye = nullptr;                // general path: element vectors s_e K0 C_e p
   uint8_t *hmask = nullptr;            // general path: bit c = corner c of the element is hanging
   double *zp = nullptr;                // general path: node records {Dinv r, p}
+  double *qacc = nullptr;              // general path, TOMESH_GENERAL_ATOMIC: atomic q accumulator
   int coop_blocks = 0;                 // general path: grid of the persistent cooperative solver (0 = off)
   int ge_blocks = 0, gn_blocks = 0;    // general path: one resident wave of the element / node pass
   int32_t *filt_idx = nullptr;
