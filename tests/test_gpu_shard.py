@@ -165,3 +165,40 @@ def test_ipc_export_open_in_another_process():
     with pytest.raises(pb.TomeshError):                                   # not a buffer of this handle
         m.ipc_export(xs_ptr := torch.zeros(8, dtype=torch.float64, device="cuda").data_ptr())
     assert hs and os_ >= 0 and xs_ptr
+
+
+def test_sharded_full_size_c5_matches_unsharded():
+    """BASELINE.json's full c5 (4.19M elements) as 2 z-slabs against the
+    unsharded handle, same 30 fixed PCG iterations, then sensitivities and the
+    SENS filter: only the summation order of the dots differs, so u, dc and
+    the filtered dc agree to 1e-8 relative (the unsharded c5 path itself is
+    checked against the oracle in tests/test_gpu_fullsize.py)."""
+    from inputs import density_at
+    prob = config("c5")
+    hm = pb.prepare(prob)
+    x = torch.as_tensor(density_at(prob, hm.elem_level, hm.elem_anchor), device="cuda")
+    m = pb.Mesh(hm, E0=prob.E0, Emin=prob.Emin, nu=prob.nu, rmin=prob.rmin)
+    u1 = torch.zeros(hm.n_dof, dtype=torch.float64, device="cuda")
+    st1 = m.tosolve_cg(prob.penal, x, u1, max_iter=30, flags=pb.TO_FIXED_ITERS | pb.TO_NO_TRUE_RES)
+    dc1 = torch.empty(hm.n_el, dtype=torch.float64, device="cuda")
+    m.to_sensitivity(prob.penal, x, u1, dc1)
+    df1 = torch.empty_like(dc1)
+    m.to_filter(pb.TO_FILTER_SENS, x, dc1, df1)
+    u1h, df1h = host(u1), host(df1)
+    m.close()
+    del u1, dc1, df1
+    torch.cuda.empty_cache()
+    g = shard.ShardGroup(hm, 2, E0=prob.E0, Emin=prob.Emin, nu=prob.nu, rmin=prob.rmin)
+    xs = g.scatter_elems(x)
+    us = [torch.zeros(mm.n_dof, dtype=torch.float64, device="cuda") for mm in g.meshes]
+    sts = g.solve(prob.penal, xs, us, max_iter=30, flags=pb.TO_FIXED_ITERS)
+    assert all(s.iters == 30 for s in sts) and abs(sts[0].relres - st1.relres) <= 1e-8 * st1.relres
+    assert rel(g.gather_nodes(us), u1h) <= 1e-8
+    dfs = []
+    for mm, xl, ul in zip(g.meshes, xs, us):
+        dc = torch.empty(mm.n_el, dtype=torch.float64, device="cuda")
+        mm.to_sensitivity(prob.penal, xl, ul, dc)
+        out = torch.empty_like(dc)
+        mm.to_filter(pb.TO_FILTER_SENS, xl, dc, out)
+        dfs.append(out)
+    assert rel(g.gather_elems(dfs), df1h) <= 1e-8
