@@ -49,7 +49,7 @@ def test_struct_layouts_match_header(tmp_path):
                "tomesh_host_arrays": _lib.HostArrays, "to_oc_stats": _lib.ToOcStats,
                "to_opt_params": _lib.ToOptParams, "to_opt_step": _lib.ToOptStep,
                "to_opt_state": _lib.ToOptState, "tomesh_adapt_result": _lib.AdaptResult,
-               "to_minres_stats": _lib.ToMinresStats}
+               "to_minres_stats": _lib.ToMinresStats, "to_shard_bufs": _lib.ToShardBufs}
     lines = ['#include <cstdio>', '#include <cstddef>', '#include "tomesh.h"', '#include "tomesh_host.h"',
              "int main(){"]
     for cname, cls in structs.items():
