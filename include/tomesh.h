@@ -136,7 +136,10 @@ typedef struct {
   int64_t device_bytes;        /* device memory held by the handle               */
   int32_t kernel_launches;     /* kernels launched by the last tosolve_cg        */
   int32_t matvec_variant;      /* operator path: 1 structured H8, 2 general
-                                  (launched passes), 3 general persistent       */
+                                  (launched passes), 3 general persistent;
+                                  + 10 * (1 + e + 2 n) when the 3D launched
+                                  passes use the 64-register variant of the
+                                  element (e) / node (n) pass (upload timing) */
   int64_t launches_total;      /* kernels launched by every call on this handle
                                   since upload (monotone counter)               */
 } to_mesh_info;

@@ -672,8 +672,8 @@ __device__ __forceinline__ double g_elem_lane(const MeshView &M, int64_t e, int 
   return live ? se * en : 0.0;
 }
 
-template <int DIM, int MODE, bool ATOM = false>
-__global__ void __launch_bounds__(256, TOMESH_LANES_MINB) k_elem_pass_lanes(MeshView M, const double *__restrict__ s,
+template <int DIM, int MODE, bool ATOM = false, int MINB = TOMESH_LANES_MINB>
+__global__ void __launch_bounds__(256, MINB) k_elem_pass_lanes(MeshView M, const double *__restrict__ s,
                                                          const double *__restrict__ zp, const double *__restrict__ po,
                                                          double *__restrict__ ye,
                                                          const __grid_constant__ K0Dense2 K2,
@@ -793,8 +793,8 @@ __device__ __forceinline__ void g_node_group(int64_t n, bool live, int l, const 
 // Node pass with a group of 4 lanes per node: lane l sums incidences l, l+4,
 // ... of the node, an xor-shuffle tree completes q_n in every lane of the
 // group, and lane i < DIM updates component i of the node (record, x, r).
-template <int DIM, int MODE>
-__global__ void __launch_bounds__(256, TOMESH_LANES_MINB) k_node_pass_lanes(int64_t n_node, const int64_t *__restrict__ inc_ptr,
+template <int DIM, int MODE, int MINB = TOMESH_LANES_MINB>
+__global__ void __launch_bounds__(256, MINB) k_node_pass_lanes(int64_t n_node, const int64_t *__restrict__ inc_ptr,
                                                          const uint32_t *__restrict__ inc, const double *__restrict__ ye,
                                                          double *__restrict__ r, const double *__restrict__ Dinv,
                                                          double *__restrict__ zp, double *__restrict__ x,

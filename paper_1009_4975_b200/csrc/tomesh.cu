@@ -303,6 +303,66 @@ int setup_incidence(const to_mesh_desc *d, const std::vector<int32_t> &node_hang
   return 0;
 }
 
+// 3D general path: the lane passes exist at the default register budget
+// (3 blocks per SM) and capped at 64 registers (4 blocks per SM); which one
+// is faster depends on the mesh (profiles/r1/general_minblocks_ab.txt), so
+// both are timed here on the zeroed workspace (same memory traffic as a real
+// iteration; the scalars are reset by every solve) and the faster one kept.
+int tune_lanes(to_mesh *m, cudaStream_t st) {
+  int pe4 = 0, pn4 = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pe4, k_elem_pass_lanes<3, G_CG, false, 4>, kBlock, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pn4, k_node_pass_lanes<3, G_CG, 4>, kBlock, 0));
+  const int ge_def = m->ge_blocks, gn_def = m->gn_blocks;
+  const int ge_4 = std::max(1, pe4) * kNumSMs, gn_4 = std::max(1, pn4) * kNumSMs;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  const double *no_po = nullptr;
+  double *no_q = nullptr;
+  auto time_it = [&](auto launch) -> float {
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+      cudaEventRecord(e0, st);
+      launch();
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      float t = 0.f;
+      cudaEventElapsedTime(&t, e0, e1);
+      if (rep > 0) best = std::min(best, t);
+    }
+    return best;
+  };
+  auto elem = [&](bool v4) {
+    const int g = std::min(grid_for(m->n_el * 8, kBlock, 8), v4 ? ge_4 : ge_def);
+    if (v4)
+      k_elem_pass_lanes<3, G_CG, false, 4><<<g, kBlock, 0, st>>>(m->view(), m->s, m->zp, no_po, m->ye, m->K2, m->KS,
+                                                                 m->hmask, m->S, m->partials);
+    else
+      k_elem_pass_lanes<3, G_CG><<<g, kBlock, 0, st>>>(m->view(), m->s, m->zp, no_po, m->ye, m->K2, m->KS, m->hmask,
+                                                       m->S, m->partials);
+  };
+  auto node = [&](bool v4) {
+    const int g = std::min(grid_for(m->n_node * 4, kBlock, 8), v4 ? gn_4 : gn_def);
+    if (v4)
+      k_node_pass_lanes<3, G_CG, 4><<<g, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, m->r, m->dinv, m->zp,
+                                                          m->x, no_q, m->partials, m->S, m->hist);
+    else
+      k_node_pass_lanes<3, G_CG><<<g, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, m->r, m->dinv, m->zp,
+                                                       m->x, no_q, m->partials, m->S, m->hist);
+  };
+  const float te_def = time_it([&] { elem(false); }), te_4 = time_it([&] { elem(true); });
+  const float tn_def = time_it([&] { node(false); }), tn_4 = time_it([&] { node(true); });
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  RC(check_launch());
+  m->lanes_e4 = te_4 < 0.97f * te_def ? 1 : 0;
+  m->lanes_n4 = tn_4 < 0.97f * tn_def ? 1 : 0;
+  if (m->lanes_e4) m->ge_blocks = ge_4;
+  if (m->lanes_n4) m->gn_blocks = gn_4;
+  CK(cudaMemsetAsync(m->S, 0, sizeof(CgScalars), st));   // the timing runs touched the scalars
+  return 0;
+}
+
 int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
   CK(cudaSetDevice(device));
   m->device = device;
@@ -469,6 +529,7 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
     }
     RC(make_tensor_map(&m->tm_dn, m->dn, G.NXP, G.NY, G.NZ, kS3RowN, PY));
   }
+  if (!m->structured && d->dim == 3 && !std::getenv("TOMESH_NO_LANES_TUNE")) RC(tune_lanes(m, st));
   CK(cudaStreamSynchronize(st));
   return 0;
 }
@@ -625,10 +686,18 @@ int op_cg_general(to_mesh *m, cudaStream_t st) {
     RC(launch_pdl(k_node_pass_lanes<2, G_CG>, dim3(gn4), dim3(kBlock), 0, st, m->n_node, m->inc_ptr, m->inc, m->ye,
                   m->r, m->dinv, m->zp, m->x, no_q, m->partials, m->S, m->hist));
   } else {
-    RC(launch_pdl(k_elem_pass_lanes<3, G_CG>, dim3(ge8), dim3(kBlock), 0, st, m->view(), m->s, m->zp, no_po, m->ye,
-                  m->K2, m->KS, m->hmask, m->S, m->partials));
-    RC(launch_pdl(k_node_pass_lanes<3, G_CG>, dim3(gn4), dim3(kBlock), 0, st, m->n_node, m->inc_ptr, m->inc, m->ye,
-                  m->r, m->dinv, m->zp, m->x, no_q, m->partials, m->S, m->hist));
+    if (m->lanes_e4)
+      RC(launch_pdl(k_elem_pass_lanes<3, G_CG, false, 4>, dim3(ge8), dim3(kBlock), 0, st, m->view(), m->s, m->zp,
+                    no_po, m->ye, m->K2, m->KS, m->hmask, m->S, m->partials));
+    else
+      RC(launch_pdl(k_elem_pass_lanes<3, G_CG>, dim3(ge8), dim3(kBlock), 0, st, m->view(), m->s, m->zp, no_po,
+                    m->ye, m->K2, m->KS, m->hmask, m->S, m->partials));
+    if (m->lanes_n4)
+      RC(launch_pdl(k_node_pass_lanes<3, G_CG, 4>, dim3(gn4), dim3(kBlock), 0, st, m->n_node, m->inc_ptr, m->inc,
+                    m->ye, m->r, m->dinv, m->zp, m->x, no_q, m->partials, m->S, m->hist));
+    else
+      RC(launch_pdl(k_node_pass_lanes<3, G_CG>, dim3(gn4), dim3(kBlock), 0, st, m->n_node, m->inc_ptr, m->inc,
+                    m->ye, m->r, m->dinv, m->zp, m->x, no_q, m->partials, m->S, m->hist));
   }
   m->last_launches += 2;
   return 0;
@@ -901,6 +970,7 @@ extern "C" int tomesh_get_info(const to_mesh *m, to_mesh_info *info) {
   info->device_bytes = m->dev_bytes;
   info->kernel_launches = m->last_launches;
   info->matvec_variant = m->structured ? 1 : (m->coop_blocks > 0 ? 3 : 2);
+  if (info->matvec_variant == 2 && (m->lanes_e4 || m->lanes_n4)) info->matvec_variant += 10 * (1 + m->lanes_e4 + 2 * m->lanes_n4);
   info->launches_total = m->launches_total;
   return 0;
 }

@@ -59,6 +59,8 @@ struct to_mesh {
   double *qacc = nullptr;              // general path, TOMESH_GENERAL_ATOMIC: atomic q accumulator
   int coop_blocks = 0;                 // general path: grid of the persistent cooperative solver (0 = off)
   int ge_blocks = 0, gn_blocks = 0;    // general path: one resident wave of the element / node pass
+  int lanes_e4 = 0, lanes_n4 = 0;      // 3D general path: 1 = the 4-blocks-per-SM (64-register) variant of the
+                                       // element / node pass, chosen at upload by timing both
   int32_t *filt_idx = nullptr;
   // OC update (allocated on first use)
   double *oc_a = nullptr, *oc_part = nullptr;
