@@ -325,7 +325,9 @@ int  to_optimize(to_mesh *m, const to_opt_params *params, int32_t n_steps, doubl
  *                   rank 0 starts at 0, the last rank ends at its last plane,
  *                   interior sides need two ghost planes), peers[r] = rank r's
  *                   buffers as addressable from this handle's device (peers[rank]
- *                   = its own).  TO_EINVAL on any inconsistency.  Synchronises.
+ *                   = its own).  Peer access is enabled to every other device a
+ *                   peer buffer lives on (one process, several GPUs).  TO_EINVAL
+ *                   on any inconsistency.  Synchronises.
  * tosolve_cg_group  tosolve_cg on n attached handles of one group in
  *                   lockstep (n = nranks in one process: several GPUs, or all
  *                   slabs on one GPU; n = 1 per process when each rank runs in

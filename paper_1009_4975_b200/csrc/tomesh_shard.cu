@@ -171,6 +171,24 @@ extern "C" int to_shard_attach(to_mesh *m, int32_t rank, int32_t nranks, const i
     C.slots[r] = peers[r].slots;
     C.flags[r] = peers[r].flags;
   }
+  // a group spread over several GPUs of one process: this device stores into
+  // the others' memory, so enable peer access to every device a peer buffer
+  // lives on (buffers mapped by CUDA IPC already belong to this context)
+  for (int r = 0; r < nranks; ++r) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, peers[r].slots) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (at.type == cudaMemoryTypeDevice && at.device != m->device) {
+      int can = 0;
+      CK(cudaDeviceCanAccessPeer(&can, m->device, at.device));
+      if (!can) { set_error("device %d cannot access peer device %d", m->device, at.device); return TO_ECUDA; }
+      const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+      cudaGetLastError();
+    }
+  }
   C.my_slots = m->shard_slots;
   C.my_flags = m->shard_flags;
   RC(plan_s3(m, st, own_lo, own_hi, true, &m->shard_plan, &m->shard_ncta));
