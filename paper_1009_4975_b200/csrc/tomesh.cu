@@ -363,48 +363,6 @@ int tune_lanes(to_mesh *m, cudaStream_t st) {
   return 0;
 }
 
-int op_cg_s3(to_mesh *m, int k, double rtol, cudaStream_t st);
-
-// Structured path: the whole-wave K1 grid plan was chosen by a scheduling
-// simulation; confirm it against the uniform segmentation by timing one
-// iteration kernel of each on the zeroed workspace (the scalars are reset by
-// every solve) and keep the faster.
-int tune_s3_plan(to_mesh *m, cudaStream_t st) {
-  cudaEvent_t e0, e1;
-  CK(cudaEventCreate(&e0));
-  CK(cudaEventCreate(&e1));
-  const int4 *plan = m->G.plan;
-  const int ncta = m->s3_ncta;
-  auto time_it = [&]() -> float {
-    float best = 1e30f;
-    for (int rep = 0; rep < 4; ++rep) {
-      cudaMemsetAsync(m->S, 0, sizeof(CgScalars), st);
-      cudaEventRecord(e0, st);
-      op_cg_s3(m, 0, 0.0, st);
-      cudaEventRecord(e1, st);
-      cudaEventSynchronize(e1);
-      float t = 0.f;
-      cudaEventElapsedTime(&t, e0, e1);
-      if (rep > 0) best = std::min(best, t);
-    }
-    return best;
-  };
-  const float t_plan = time_it();
-  m->G.plan = nullptr;
-  m->s3_ncta = 0;
-  const float t_uni = time_it();
-  if (!(t_uni < 0.97f * t_plan)) {
-    m->G.plan = plan;
-    m->s3_ncta = ncta;
-  }
-  m->last_launches = 0;
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  RC(check_launch());
-  CK(cudaMemsetAsync(m->S, 0, sizeof(CgScalars), st));
-  return 0;
-}
-
 int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
   CK(cudaSetDevice(device));
   m->device = device;
@@ -572,7 +530,6 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
     RC(make_tensor_map(&m->tm_dn, m->dn, G.NXP, G.NY, G.NZ, kS3RowN, PY));
   }
   if (!m->structured && d->dim == 3 && !std::getenv("TOMESH_NO_LANES_TUNE")) RC(tune_lanes(m, st));
-  if (m->structured && m->G.plan && !std::getenv("TOMESH_NO_LANES_TUNE")) RC(tune_s3_plan(m, st));
   CK(cudaStreamSynchronize(st));
   return 0;
 }
