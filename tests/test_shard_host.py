@@ -1,8 +1,10 @@
 """Host logic of the z-slab sharding (paper_1009_4975_b200/shard.py; SURVEY
 §8(e)), on CPU: the slab plan, the local meshes sliced from the global host
-mesh, and the per-rank slicing under torch.distributed (gloo, world size 2).
-The device side (the fused exchange and the all-reduce) is covered by
-tests/test_gpu_shard.py."""
+mesh, the per-rank slicing under torch.distributed (gloo, world size 2), and
+the one-process-per-GPU plumbing of ShardRank (IPC handle exchange, which peer
+buffers are mapped, the attach arguments) with fake device calls (gloo, world
+size 3).  The device side (the fused exchange and the all-reduce) is covered
+by tests/test_gpu_shard.py."""
 import os
 import socket
 import sys
@@ -126,3 +128,85 @@ def test_slices_gloo_world2():
         p.join(180)
         assert p.exitcode == 0
     assert q.get(timeout=10) is True
+
+
+def _rank_worker(rank, ws, port, out):
+    """ShardRank's host plumbing with the device calls replaced by fakes: the
+    IPC exchange through all_gather_object, which peer buffers each rank maps
+    (neighbours' vectors, everyone's slots and flags), one mapping per handle,
+    and the arguments it hands to to_shard_attach."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(ws))
+    sys.path.insert(0, ROOT)
+    import paper_1009_4975_b200 as pb_
+    from paper_1009_4975_b200 import _lib as L
+    from paper_1009_4975_b200 import shard as sh
+    from inputs import config as cfg
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    try:
+        base = 1 << 40 | rank << 32            # fake device addresses of this rank
+        opened = []
+        seen = {}
+
+        class FakeMesh:
+            def __init__(self, host, **kw):
+                self.host = host
+
+            def shard_buffers(self):
+                b = L.ToShardBufs()
+                for i in range(2):
+                    b.rb[i], b.pb[i], b.qb[i] = base + 0x100 * (1 + i), base + 0x100 * (3 + i), base + 0x100 * (5 + i)
+                b.x, b.slots, b.flags = base + 0x700, base + 0x10000, base + 0x10100   # slots+flags: one block
+                b.nx, b.ny, b.nz, b.plane_doubles = 13, 7, int(self.host.node_coord[:, 2].max()) + 1, 3 * 14 * 7
+                return b
+
+            def ipc_export(self, ptr):
+                blk = ptr & ~0xFFFF
+                return (f"r{rank}-{blk:x}".encode().ljust(64, b"\0"), ptr - blk)
+
+            def shard_attach(self, r, n, gz, lo, hi, peers):
+                seen.update(rank=r, n=n, gz=list(gz), own=(lo, hi),
+                            peers=[(p.x or 0, p.rb[0] or 0, p.slots or 0, p.flags or 0) for p in peers])
+
+            def close(self):
+                pass
+
+        def fake_open(device, h, off):
+            opened.append(h)
+            owner = int(h.split(b"-")[0][1:])
+            blk = int(h.rstrip(b"\0").split(b"-")[1], 16)
+            assert blk >> 32 == (1 << 8 | owner)
+            return blk + off
+
+        sh.Mesh, sh.ipc_open, sh.ipc_close = FakeMesh, fake_open, lambda d, p: None
+        hm = pb_.prepare(cfg("c5", nx=12, ny=6, nz=11))
+        sr = sh.ShardRank(hm)
+        ok = seen["rank"] == rank and seen["n"] == ws and seen["own"] == (sr.slab.own_lo, sr.slab.own_hi)
+        ok &= len(set(opened)) == len(opened)                   # one mapping per handle
+        for r, (x, rb0, slots, flags) in enumerate(seen["peers"]):
+            owner = (1 << 40 | r << 32)
+            ok &= slots == owner + 0x10000 and flags == owner + 0x10100
+            if abs(r - rank) <= 1:
+                ok &= x == owner + 0x700 and rb0 == owner + 0x100
+            else:
+                ok &= x == 0 and rb0 == 0                        # non-neighbours' vectors are never mapped
+        allseen = [None] * ws
+        dist.all_gather_object(allseen, seen["gz"])
+        ok &= all(g == allseen[0] for g in allseen)
+        out.put((rank, bool(ok)))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_rank_plumbing_gloo_world3():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(240)
+        assert p.exitcode == 0
+    res = dict(q.get(timeout=10) for _ in range(3))
+    assert res == {0: True, 1: True, 2: True}
