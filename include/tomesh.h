@@ -118,7 +118,18 @@ typedef struct {
   const int64_t *filt_ptr;     /* [n_elem+1] or NULL when rmin == 0              */
   const int32_t *filt_idx;     /* [filt_nnz] neighbours with |c_d-c_e| < rmin,
                                   ascending, self included (C9)                  */
+  uint32_t options;            /* TO_UPLOAD_* bits below (0 = defaults)          */
+  uint32_t reserved;           /* must be 0                                      */
 } to_mesh_desc;
+
+/* to_mesh_desc.options.  The operator, and therefore u, is the same on every
+ * path; these only choose the device code that applies it.
+ *   TO_UPLOAD_GENERAL        keep a uniform H8 box on the general (canonical
+ *                            Morton order) path instead of the structured
+ *                            one; tosolve_minres with TO_PC_IC0 needs it.
+ *   TO_UPLOAD_NO_PERSISTENT  2D meshes: launch one kernel per PCG iteration
+ *                            instead of the persistent cooperative solver. */
+enum { TO_UPLOAD_GENERAL = 1, TO_UPLOAD_NO_PERSISTENT = 2 };
 
 typedef struct {
   int32_t iters;               /* CG iterations performed                        */

@@ -247,7 +247,7 @@ def _stream(stream):
     return C.c_void_p(s.cuda_stream)
 
 
-def make_desc(host: HostMesh, E0, Emin, nu, rmin):
+def make_desc(host: HostMesh, E0, Emin, nu, rmin, options=0):
     """to_mesh_desc of a host mesh (argument marshalling only); returns the
     struct and the numpy arrays it points into (keep them alive)."""
     keep = []
@@ -280,13 +280,16 @@ def make_desc(host: HostMesh, E0, Emin, nu, rmin):
         d.filt_nnz = host.filt_idx.shape[0]
         d.filt_ptr = arr(host.filt_ptr, np.int64)
         d.filt_idx = arr(host.filt_idx, np.int32)
+    d.options = int(options)
     return d, keep
 
 
 class Mesh:
     """Device copy of a mesh + CG workspace (tomesh_upload / tomesh_free)."""
 
-    def __init__(self, host: HostMesh, E0=1.0, Emin=1e-9, nu=0.3, rmin=None, device=0, stream=None):
+    def __init__(self, host: HostMesh, E0=1.0, Emin=1e-9, nu=0.3, rmin=None, device=0, stream=None, options=0):
+        """options: TO_UPLOAD_* bits of include/tomesh.h (which device code
+        applies the operator; the operator itself does not change)."""
         import torch
         self.host = host
         self.device = torch.device("cuda", device)
@@ -294,7 +297,7 @@ class Mesh:
         self.n_el, self.n_node, self.n_dof = host.n_el, host.n_node, host.n_dof
         self.E0, self.Emin, self.nu = E0, Emin, nu
         rmin = host.rmin if rmin is None else rmin
-        d, self._keep = make_desc(host, E0, Emin, nu, rmin)
+        d, self._keep = make_desc(host, E0, Emin, nu, rmin, options)
         self._h = C.c_void_p()
         with torch.cuda.device(self.device):
             L.check(L.lib().tomesh_upload(C.byref(d), device, _stream(stream), C.byref(self._h)), "tomesh_upload")

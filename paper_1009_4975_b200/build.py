@@ -1,6 +1,11 @@
 """Build libtomesh.so in-tree with nvcc for sm_100a (no torch extension machinery).
 
     python -m paper_1009_4975_b200.build          # or __graft_entry__.build()
+
+A/B experiments build a variant library elsewhere (the shipped build never
+reads the environment):
+
+    python -m paper_1009_4975_b200.build --out ab/lib_new.so -DTOMESH_NO_PDL
 """
 from __future__ import annotations
 
@@ -20,8 +25,6 @@ HEADERS = ["common.h", "device_common.cuh", "element.h", "tomesh_types.cuh", "to
            "kernels_shard.cuh"]
 
 NVCC_FLAGS = [
-    *([f"-DTOMESH_S3_TYW={os.environ['TOMESH_S3_TYW']}"] if os.environ.get("TOMESH_S3_TYW") else []),
-    *os.environ.get("TOMESH_NVCC_EXTRA", "").split(),   # experiments (e.g. -DTOMESH_LANES_MINB=5)
     "-O3", "-std=c++17", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-Xcompiler", "-fPIC,-fopenmp,-O3",
@@ -47,15 +50,19 @@ def _stale() -> bool:
     return any(os.path.exists(d) and os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra=(), out: str = None) -> str:
+    """Compile every source for sm_100a and link libtomesh.so.  `extra`
+    (nvcc flags) and `out` (another path) are for A/B variant builds only."""
+    lib = LIB if out is None else os.path.abspath(out)
+    if out is None and not extra and not force and not _stale():
         return LIB
     nvcc = _nvcc()
     objs = []
-    os.makedirs(os.path.join(PKG, "build"), exist_ok=True)
+    bdir = os.path.join(PKG, "build" if out is None and not extra else "build_variant")
+    os.makedirs(bdir, exist_ok=True)
     for src in SOURCES:
-        obj = os.path.join(PKG, "build", os.path.splitext(src)[0] + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c",
+        obj = os.path.join(bdir, os.path.splitext(src)[0] + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c",
                os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cpp"):
             cmd = [shutil.which("g++") or "g++", "-O3", "-std=c++17", "-fPIC", "-fopenmp", "-g",
@@ -67,16 +74,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stderr.write(res.stderr)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
            "-Xcompiler", "-fopenmp", "-o", tmp, *objs, "-lgomp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("link failed")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    args = sys.argv[1:]
+    out = None
+    if "--out" in args:
+        i = args.index("--out")
+        out = args[i + 1]
+        del args[i:i + 2]
+    print(build(force="--force" in args, verbose=True, extra=[a for a in args if a != "--force"], out=out))

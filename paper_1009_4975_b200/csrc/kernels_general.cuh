@@ -9,9 +9,6 @@
 //   k_sens        a10 dc_e = -p x^(p-1)(E0-Emin) h^(d-2) u_e^T K0 u_e    (:343-346)
 //   k_filter      a11 Eq. 5 / density variant                             (:613-616)
 #pragma once
-#ifndef TOMESH_LANES_MINB
-#define TOMESH_LANES_MINB 1   // min resident blocks of the general-path lane passes (register cap)
-#endif
 #include <cooperative_groups.h>
 
 #include "device_common.cuh"
@@ -555,11 +552,7 @@ __global__ void __launch_bounds__(256) k_node_pass(int64_t n_node, const int64_t
 // the Eq. 6 interpolation if it is hanging), the element product runs across
 // the group with warp shuffles, lane c stores y_e[corner c].  In 3D the
 // Walsh-Hadamard stages are xor-shuffles and lane c holds Hadamard mode c.
-// ATOM (experiment, TOMESH_GENERAL_ATOMIC): lane c adds s_e y_e[c] straight
-// into q at its node (C^T: a hanging corner's share goes to its parents with
-// the Eq. 6 weights) with fp64 atomics instead of storing y_e; the node pass
-// then streams q.  Summation order, hence the last bits, vary run to run.
-template <int DIM, int MODE, bool COH, bool ATOM = false>
+template <int DIM, int MODE, bool COH>
 __device__ __forceinline__ double g_elem_lane(const MeshView &M, int64_t e, int c, const double *__restrict__ s,
                                               const double *__restrict__ zp, const double *__restrict__ po,
                                               double *__restrict__ ye,
@@ -651,29 +644,14 @@ __device__ __forceinline__ double g_elem_lane(const MeshView &M, int64_t e, int 
     for (int i = 0; i < 2; ++i) en = fma(v[i], y[i], en);
   }
   if (live) {
-    if (ATOM) {
-      if (!((__ldg(hmask + e) >> c) & 1)) {
 #pragma unroll
-        for (int i = 0; i < DIM; ++i) atomicAdd(ye + (int64_t)n * DIM + i, se * y[i]);
-      } else {
-        const int h = M.node_hang[n];
-        for (int k = M.hang_ptr[h]; k < M.hang_ptr[h + 1]; ++k) {
-          const double w = M.hang_weight[k] * se;
-          const int64_t pd = (int64_t)M.hang_parent[k] * DIM;
-#pragma unroll
-          for (int i = 0; i < DIM; ++i) atomicAdd(ye + pd + i, w * y[i]);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) ye[(e * NC + c) * DIM + i] = se * y[i];
-    }
+    for (int i = 0; i < DIM; ++i) ye[(e * NC + c) * DIM + i] = se * y[i];
   }
   return live ? se * en : 0.0;
 }
 
-template <int DIM, int MODE, bool ATOM = false, int MINB = TOMESH_LANES_MINB>
-__global__ void __launch_bounds__(256, MINB) k_elem_pass_lanes(MeshView M, const double *__restrict__ s,
+template <int DIM, int MODE>
+__global__ void __launch_bounds__(256) k_elem_pass_lanes(MeshView M, const double *__restrict__ s,
                                                          const double *__restrict__ zp, const double *__restrict__ po,
                                                          double *__restrict__ ye,
                                                          const __grid_constant__ K0Dense2 K2,
@@ -695,7 +673,7 @@ __global__ void __launch_bounds__(256, MINB) k_elem_pass_lanes(MeshView M, const
        base < M.n_el; base += groups) {
     const int64_t e = base + (threadIdx.x & 31) / NC;
     const bool live = e < M.n_el;
-    pq += g_elem_lane<DIM, MODE, false, ATOM>(M, live ? e : M.n_el - 1, c, s, zp, po, ye, K2, H, hmask, beta,
+    pq += g_elem_lane<DIM, MODE, false>(M, live ? e : M.n_el - 1, c, s, zp, po, ye, K2, H, hmask, beta,
                                         live && !stopped);
   }
   if (stopped) return;
@@ -793,8 +771,8 @@ __device__ __forceinline__ void g_node_group(int64_t n, bool live, int l, const 
 // Node pass with a group of 4 lanes per node: lane l sums incidences l, l+4,
 // ... of the node, an xor-shuffle tree completes q_n in every lane of the
 // group, and lane i < DIM updates component i of the node (record, x, r).
-template <int DIM, int MODE, int MINB = TOMESH_LANES_MINB>
-__global__ void __launch_bounds__(256, MINB) k_node_pass_lanes(int64_t n_node, const int64_t *__restrict__ inc_ptr,
+template <int DIM, int MODE>
+__global__ void __launch_bounds__(256) k_node_pass_lanes(int64_t n_node, const int64_t *__restrict__ inc_ptr,
                                                          const uint32_t *__restrict__ inc, const double *__restrict__ ye,
                                                          double *__restrict__ r, const double *__restrict__ Dinv,
                                                          double *__restrict__ zp, double *__restrict__ x,
@@ -822,47 +800,6 @@ __global__ void __launch_bounds__(256, MINB) k_node_pass_lanes(int64_t n_node, c
       cg_after_rupdate(S, acc[0], acc[1], hist);
       if (S->done_next) S->done = 1;                 // x is already complete
     }
-  }
-}
-
-// Node pass of the ATOM variant: one thread per DOF, q streamed from the
-// atomic accumulator (and reset to 0 for the next iteration), the same CG
-// update and reductions as g_node_group.
-template <int DIM>
-__global__ void __launch_bounds__(256) k_node_pass_atom(int64_t n_dof, double *__restrict__ qacc,
-                                                        double *__restrict__ r, const double *__restrict__ Dinv,
-                                                        double *__restrict__ zp, double *__restrict__ x,
-                                                        double *partials, CgScalars *S, double *hist) {
-  pdl_wait();
-  pdl_release();
-  const bool stopped = __ldcg(&S->done) | __ldcg(&S->done_next);
-  const double beta = __ldcg(&S->beta), alpha = __ldcg(&S->alpha);
-  double acc[2] = {0.0, 0.0};
-  GRID_STRIDE(d, n_dof) {
-    const int64_t n = d / DIM;
-    const int l = (int)(d - n * DIM);
-    const double qc = __ldcg(qacc + d);
-    qacc[d] = 0.0;
-    if (stopped) continue;
-    double *rec = zp + n * 2 * DIM;
-    const double di = __ldg(Dinv + d);
-    const double pk = fma(beta, rec[DIM + l], rec[l]);
-    double zn = 0.0;
-    if (di != 0.0) {
-      x[d] = fma(alpha, pk, x[d]);
-      const double rn = fma(-alpha, qc, r[d]);
-      r[d] = rn;
-      zn = di * rn;
-      acc[0] = fma(rn, zn, acc[0]);
-      acc[1] = fma(rn, rn, acc[1]);
-    }
-    rec[l] = zn;
-    rec[DIM + l] = pk;
-  }
-  if (stopped) return;
-  if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) {
-    cg_after_rupdate(S, acc[0], acc[1], hist);
-    if (S->done_next) S->done = 1;
   }
 }
 

@@ -15,7 +15,13 @@
 // so the ghost data is ordered before the flag the last block publishes.
 // Slots and flags are double-buffered by sequence parity: a rank can push
 // sequence s+1 only after its own gather of s, so the slot of s is not
-// overwritten before every rank has read it.
+// overwritten before every rank has read it.  That argument needs every rank
+// to push every sequence number of a bank.  K1 stops pushing once the solve
+// has stopped (the same iteration on every rank), so the collectives around
+// the iteration loop (||b||, the final step, the x ghost planes) use a bank
+// pair of their own (sequence numbers tagged kShardTail), which every rank
+// pushes on every solve, stopped or not: a rank that runs ahead into them
+// can never overwrite a flag a lagging peer's K1 still waits for.
 #pragma once
 #include "device_common.cuh"
 #include "kernels_cg.cuh"
@@ -37,9 +43,14 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
+// Bank of a sequence number: 0/1 = K1 (parity), 2/3 = tail collectives.
+__device__ __forceinline__ int shard_bank(unsigned long long seq) {
+  return (int)(seq & 1ull) + ((seq & kShardTail) ? 2 : 0);
+}
+
 // One thread: push n values of sequence `seq` into every rank's slot.
 __device__ __forceinline__ void shard_push(const ShardComm &C, unsigned long long seq, const double *v, int n) {
-  const int par = (int)(seq & 1ull);
+  const int par = shard_bank(seq);
   for (int r = 0; r < C.nranks; ++r) {
     double *dst = C.slots[r] + ((size_t)par * kShardMax + C.rank) * kShardVals;
     for (int k = 0; k < n; ++k) dst[k] = v[k];
@@ -52,7 +63,7 @@ __device__ __forceinline__ void shard_push(const ShardComm &C, unsigned long lon
 // values in rank order.  Returns false after ~20 s without all flags (a peer
 // that never arrives): the caller records a failure instead of hanging.
 __device__ __forceinline__ bool shard_gather(const ShardComm &C, unsigned long long seq, double *out, int n) {
-  const int par = (int)(seq & 1ull);
+  const int par = shard_bank(seq);
   const unsigned long long t0 = global_ns();
   for (int r = 0; r < C.nranks; ++r) {
     const unsigned long long *f = C.my_flags + par * kShardMax + r;
@@ -113,17 +124,19 @@ static __global__ void k_shard_set_bnorm(const __grid_constant__ ShardComm C, un
   if (b2[1] > 0.0) cg_fail(S, -1);   // a density outside (0, 1] on some rank
 }
 
-// After N iterations: the global rho_N, rr_N (k_final_s3<true> pushed them).
+// After N iterations: the global rho_N, rr_N (k_final_s3<true> pushed them;
+// a stopped solve pushed zeros, which are gathered and dropped).
 static __global__ void k_shard_final(const __grid_constant__ ShardComm C, unsigned long long seq, CgScalars *S, int n_iter,
                               double rtol, double *hist) {
-  if (threadIdx.x != 0 || cg_stopped(S)) return;
+  if (threadIdx.x != 0) return;
+  const bool stopped = cg_stopped(S);
   double d[2];
   if (!shard_gather(C, seq, d, 2)) {
     cg_fail(S, -2);
     S->done = 1;
     return;
   }
-  cg_final_step(S, n_iter, d[0], d[1], rtol, hist);
+  if (!stopped) cg_final_step(S, n_iter, d[0], d[1], rtol, hist);
 }
 
 // After the solve: the owned planes the neighbours need for sensitivities and

@@ -536,7 +536,14 @@ __global__ void __launch_bounds__(512) k_final_s3(int n, const double *__restric
                                                   double *__restrict__ x, double *partials, CgScalars *S, int n_iter,
                                                   double rtol, double *hist, const __grid_constant__ ShardComm C,
                                                   unsigned long long seq) {
-  if (cg_stopped(S)) return;
+  if (cg_stopped(S)) {
+    // sharded: every rank pushes every tail sequence (kernels_shard.cuh)
+    if (SHARD && blockIdx.x == 0 && threadIdx.x == 0) {
+      const double zero[2] = {0.0, 0.0};
+      shard_push(C, seq, zero, 2);
+    }
+    return;
+  }
   const double alpha = __ldcg(&S->alpha);
   double acc[2] = {0.0, 0.0};
   const int n2 = n >> 1;

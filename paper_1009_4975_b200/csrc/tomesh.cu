@@ -57,6 +57,10 @@ int validate(const to_mesh_desc *d) {
     if (f < 0 || f >= d->n_node * d->dim || (i > 0 && f <= d->fixed_dof[i - 1])) { set_error("fixed_dof not ascending / out of range"); return TO_EMESH; }
     if (hang[f / d->dim]) { set_error("fixed DOF %lld is on a hanging node", (long long)f); return TO_EMESH; }
   }
+  if ((d->options & ~(uint32_t)(TO_UPLOAD_GENERAL | TO_UPLOAD_NO_PERSISTENT)) != 0 || d->reserved != 0) {
+    set_error("unknown upload option bits 0x%x", d->options);
+    return TO_EINVAL;
+  }
   if (d->rmin > 0.0) {
     if (!d->filt_ptr || !d->filt_idx) { set_error("rmin > 0 but no filter lists"); return TO_EINVAL; }
     if (d->filt_ptr[0] != 0 || d->filt_ptr[d->n_elem] != d->filt_nnz) { set_error("bad filt_ptr"); return TO_EMESH; }
@@ -167,7 +171,7 @@ int plan_s3(to_mesh *m, cudaStream_t st, int z0, int z1, bool force, const int4 
   RC(upload_array(m, &d, best_plan.data(), best_plan.size(), st));
   *plan_out = d;
   *ncta_out = (int)best_plan.size();
-  if (best_plan.size() * 5 > (size_t)kMaxPartialBlocks * 4) RC(m->alloc(&m->partials, best_plan.size() * 5));
+  RC(ensure_partials(m, best_plan.size() * 5));
   return 0;
 }
 
@@ -242,10 +246,11 @@ int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof
     CK(cudaMemsetAsync(base, 0, sizeof(double) * cnt, st));
     m->dn = base + kS3PadFront;
   }
+  // K1 reduces 5 values per CTA (grid_sum<5>), on the uniform grid or the plan
   const int64_t grid = (int64_t)G.ntx * G.nty * G.nzs;
-  if (grid > kMaxPartialBlocks) RC(m->alloc(&m->partials, (size_t)grid * 4));
+  RC(ensure_partials(m, (size_t)grid * 5));
   m->G = G;
-  if (!std::getenv("TOMESH_S3_NO_PLAN")) RC(plan_s3(m, st, 0, G.NZ, false, &m->G.plan, &m->s3_ncta));
+  RC(plan_s3(m, st, 0, G.NZ, false, &m->G.plan, &m->s3_ncta));
   m->k0d = m->K3.K[0];
   m->h_struct = m->hL * (double)sz;
   m->structured = true;
@@ -300,66 +305,6 @@ int setup_incidence(const to_mesh_desc *d, const std::vector<int32_t> &node_hang
   RC(m->alloc(&m->ye, (size_t)d->n_elem * nc * d->dim));
   RC(m->alloc(&m->zp, (size_t)d->n_node * 2 * d->dim));
   CK(cudaMemsetAsync(m->ye, 0, sizeof(double) * (size_t)d->n_elem * nc * d->dim, st));
-  return 0;
-}
-
-// 3D general path: the lane passes exist at the default register budget
-// (3 blocks per SM) and capped at 64 registers (4 blocks per SM); which one
-// is faster depends on the mesh (profiles/r1/general_minblocks_ab.txt), so
-// both are timed here on the zeroed workspace (same memory traffic as a real
-// iteration; the scalars are reset by every solve) and the faster one kept.
-int tune_lanes(to_mesh *m, cudaStream_t st) {
-  int pe4 = 0, pn4 = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pe4, k_elem_pass_lanes<3, G_CG, false, 4>, kBlock, 0));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pn4, k_node_pass_lanes<3, G_CG, 4>, kBlock, 0));
-  const int ge_def = m->ge_blocks, gn_def = m->gn_blocks;
-  const int ge_4 = std::max(1, pe4) * kNumSMs, gn_4 = std::max(1, pn4) * kNumSMs;
-  cudaEvent_t e0, e1;
-  CK(cudaEventCreate(&e0));
-  CK(cudaEventCreate(&e1));
-  const double *no_po = nullptr;
-  double *no_q = nullptr;
-  auto time_it = [&](auto launch) -> float {
-    float best = 1e30f;
-    for (int rep = 0; rep < 4; ++rep) {
-      cudaEventRecord(e0, st);
-      launch();
-      cudaEventRecord(e1, st);
-      cudaEventSynchronize(e1);
-      float t = 0.f;
-      cudaEventElapsedTime(&t, e0, e1);
-      if (rep > 0) best = std::min(best, t);
-    }
-    return best;
-  };
-  auto elem = [&](bool v4) {
-    const int g = std::min(grid_for(m->n_el * 8, kBlock, 8), v4 ? ge_4 : ge_def);
-    if (v4)
-      k_elem_pass_lanes<3, G_CG, false, 4><<<g, kBlock, 0, st>>>(m->view(), m->s, m->zp, no_po, m->ye, m->K2, m->KS,
-                                                                 m->hmask, m->S, m->partials);
-    else
-      k_elem_pass_lanes<3, G_CG><<<g, kBlock, 0, st>>>(m->view(), m->s, m->zp, no_po, m->ye, m->K2, m->KS, m->hmask,
-                                                       m->S, m->partials);
-  };
-  auto node = [&](bool v4) {
-    const int g = std::min(grid_for(m->n_node * 4, kBlock, 8), v4 ? gn_4 : gn_def);
-    if (v4)
-      k_node_pass_lanes<3, G_CG, 4><<<g, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, m->r, m->dinv, m->zp,
-                                                          m->x, no_q, m->partials, m->S, m->hist);
-    else
-      k_node_pass_lanes<3, G_CG><<<g, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, m->r, m->dinv, m->zp,
-                                                       m->x, no_q, m->partials, m->S, m->hist);
-  };
-  const float te_def = time_it([&] { elem(false); }), te_4 = time_it([&] { elem(true); });
-  const float tn_def = time_it([&] { node(false); }), tn_4 = time_it([&] { node(true); });
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  RC(check_launch());
-  m->lanes_e4 = te_4 < 0.97f * te_def ? 1 : 0;
-  m->lanes_n4 = tn_4 < 0.97f * tn_def ? 1 : 0;
-  if (m->lanes_e4) m->ge_blocks = ge_4;
-  if (m->lanes_n4) m->gn_blocks = gn_4;
-  CK(cudaMemsetAsync(m->S, 0, sizeof(CgScalars), st));   // the timing runs touched the scalars
   return 0;
 }
 
@@ -432,7 +377,7 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
     RC(upload_array(m, &m->child_weight, cw.data(), cw.size(), st));
   }
 
-  RC(m->alloc(&m->partials, (size_t)kMaxPartialBlocks * 4));
+  RC(ensure_partials(m, (size_t)kMaxPartialBlocks * 4));
   RC(m->alloc(&m->S, 1));
   CK(cudaMemsetAsync(m->S, 0, sizeof(CgScalars), st));
   CK(cudaMallocHost(&m->S_host, sizeof(CgScalars)));
@@ -444,8 +389,8 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
   if (build_K0_hadamard(d->nu, &m->KH) != 0) { set_error("Hadamard factorisation check failed"); return TO_EINVAL; }
   if (build_K0_hadamard_sym(m->KH, &m->KS) != 0) { set_error("Hadamard coefficient classes check failed"); return TO_EINVAL; }
   m->n_int = m->n_dof;
-  // diagnostics: TOMESH_FORCE_GENERAL=1 keeps uniform H8 meshes on the general path
-  m->force_general = std::getenv("TOMESH_FORCE_GENERAL") != nullptr;
+  // TO_UPLOAD_GENERAL keeps uniform H8 meshes on the general path
+  m->force_general = (d->options & TO_UPLOAD_GENERAL) != 0;
   RC(setup_structured(d, free_dof, st, m));
   // (the structured path filters with a lattice stencil and needs no lists)
   if ((m->filt_nnz > 0 || d->rmin > 0.0) && !m->structured) {
@@ -468,10 +413,6 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
   }
   if (!m->structured) {
     RC(setup_incidence(d, node_hang, st, m));
-    if (std::getenv("TOMESH_GENERAL_ATOMIC")) {   // experiment: see k_node_pass_atom
-      RC(m->alloc(&m->qacc, (size_t)m->n_dof));
-      CK(cudaMemsetAsync(m->qacc, 0, sizeof(double) * m->n_dof, st));
-    }
     // launched passes: one resident wave (the end-of-pass reduction then runs once per block slot)
     {
       int pe = 0, pn = 0;
@@ -494,12 +435,12 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
     // vs 39 us per iteration; 66k: 44 vs 60 us; a persistent variant built from
     // the lane passes was also slower, 26.6 / 68.6 us: its grid barriers cost
     // more than the two launches)
-    if (coop && !std::getenv("TOMESH_NO_PERSISTENT") && d->dim == 2 && d->n_elem <= 100000) {
+    if (coop && !(d->options & TO_UPLOAD_NO_PERSISTENT) && d->dim == 2 && d->n_elem <= 100000) {
       int per_sm = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_general_persistent<2>, kBlock, 0));
       const int64_t need = (std::max<int64_t>(d->n_elem, d->n_node) + kBlock - 1) / kBlock;
       m->coop_blocks = (int)std::min<int64_t>(need, (int64_t)per_sm * kNumSMs);
-      if (m->coop_blocks * 3 > kMaxPartialBlocks * 4) m->coop_blocks = kMaxPartialBlocks * 4 / 3;
+      RC(ensure_partials(m, (size_t)m->coop_blocks * 3));   // part_a [coop] + part_b [2 coop]
     }
   }
   // workspace: internal-order vectors with zero pads on both sides (the
@@ -529,7 +470,6 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
     }
     RC(make_tensor_map(&m->tm_dn, m->dn, G.NXP, G.NY, G.NZ, kS3RowN, PY));
   }
-  if (!m->structured && d->dim == 3 && !std::getenv("TOMESH_NO_LANES_TUNE")) RC(tune_lanes(m, st));
   CK(cudaStreamSynchronize(st));
   return 0;
 }
@@ -660,43 +600,17 @@ int op_cg_general(to_mesh *m, cudaStream_t st) {
   const int ge4 = std::min(grid_for(m->n_el * 4, kBlock, 8), m->ge_blocks);
   const int ge8 = std::min(grid_for(m->n_el * 8, kBlock, 8), m->ge_blocks);
   const int gn4 = std::min(grid_for(m->n_node * 4, kBlock, 8), m->gn_blocks);
-  double *p = m->pb[0];
   const double *no_po = nullptr;
   double *no_q = nullptr;
-  if (m->qacc) {   // TOMESH_GENERAL_ATOMIC experiment: atomic scatter into q, streaming node pass
-    const int gd = std::min(grid_for(m->n_dof, kBlock, 8), m->gn_blocks);
-    if (m->dim == 2)
-      RC(launch_pdl(k_elem_pass_lanes<2, G_CG, true>, dim3(ge4), dim3(kBlock), 0, st, m->view(), m->s, m->zp, no_po,
-                    m->qacc, m->K2, m->KS, m->hmask, m->S, m->partials));
-    else
-      RC(launch_pdl(k_elem_pass_lanes<3, G_CG, true>, dim3(ge8), dim3(kBlock), 0, st, m->view(), m->s, m->zp, no_po,
-                    m->qacc, m->K2, m->KS, m->hmask, m->S, m->partials));
-    if (m->dim == 2)
-      RC(launch_pdl(k_node_pass_atom<2>, dim3(gd), dim3(kBlock), 0, st, m->n_dof, m->qacc, m->r, m->dinv, m->zp,
-                    m->x, m->partials, m->S, m->hist));
-    else
-      RC(launch_pdl(k_node_pass_atom<3>, dim3(gd), dim3(kBlock), 0, st, m->n_dof, m->qacc, m->r, m->dinv, m->zp,
-                    m->x, m->partials, m->S, m->hist));
-    m->last_launches += 2;
-    return 0;
-  }
   if (m->dim == 2) {
     RC(launch_pdl(k_elem_pass_lanes<2, G_CG>, dim3(ge4), dim3(kBlock), 0, st, m->view(), m->s, m->zp, no_po, m->ye,
                   m->K2, m->KS, m->hmask, m->S, m->partials));
     RC(launch_pdl(k_node_pass_lanes<2, G_CG>, dim3(gn4), dim3(kBlock), 0, st, m->n_node, m->inc_ptr, m->inc, m->ye,
                   m->r, m->dinv, m->zp, m->x, no_q, m->partials, m->S, m->hist));
   } else {
-    if (m->lanes_e4)
-      RC(launch_pdl(k_elem_pass_lanes<3, G_CG, false, 4>, dim3(ge8), dim3(kBlock), 0, st, m->view(), m->s, m->zp,
-                    no_po, m->ye, m->K2, m->KS, m->hmask, m->S, m->partials));
-    else
-      RC(launch_pdl(k_elem_pass_lanes<3, G_CG>, dim3(ge8), dim3(kBlock), 0, st, m->view(), m->s, m->zp, no_po,
+    RC(launch_pdl(k_elem_pass_lanes<3, G_CG>, dim3(ge8), dim3(kBlock), 0, st, m->view(), m->s, m->zp, no_po,
                     m->ye, m->K2, m->KS, m->hmask, m->S, m->partials));
-    if (m->lanes_n4)
-      RC(launch_pdl(k_node_pass_lanes<3, G_CG, 4>, dim3(gn4), dim3(kBlock), 0, st, m->n_node, m->inc_ptr, m->inc,
-                    m->ye, m->r, m->dinv, m->zp, m->x, no_q, m->partials, m->S, m->hist));
-    else
-      RC(launch_pdl(k_node_pass_lanes<3, G_CG>, dim3(gn4), dim3(kBlock), 0, st, m->n_node, m->inc_ptr, m->inc,
+    RC(launch_pdl(k_node_pass_lanes<3, G_CG>, dim3(gn4), dim3(kBlock), 0, st, m->n_node, m->inc_ptr, m->inc,
                     m->ye, m->r, m->dinv, m->zp, m->x, no_q, m->partials, m->S, m->hist));
   }
   m->last_launches += 2;
@@ -828,8 +742,7 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   if (!m->structured && m->coop_blocks > 0 && !stop) {
     // the whole loop in one cooperative kernel (no host polling)
     if (prof) CK(cudaEventRecord(m->prof_ev[0], st));
-    double *pa = m->partials, *pb_ = m->partials + kMaxPartialBlocks;
-    double *p = m->pb[0];
+    double *pa = m->partials, *pb_ = m->partials + m->coop_blocks;
     MeshView V = m->view();
     void *args3[] = {&V, &m->s, &m->r, &m->dinv, &m->zp, &m->x, &m->ye, &m->inc_ptr, &m->inc, &m->K2, &m->KS,
                      &m->hmask, &m->S, &pa, &pb_, &m->hist};
@@ -970,7 +883,6 @@ extern "C" int tomesh_get_info(const to_mesh *m, to_mesh_info *info) {
   info->device_bytes = m->dev_bytes;
   info->kernel_launches = m->last_launches;
   info->matvec_variant = m->structured ? 1 : (m->coop_blocks > 0 ? 3 : 2);
-  if (info->matvec_variant == 2 && (m->lanes_e4 || m->lanes_n4)) info->matvec_variant += 10 * (1 + m->lanes_e4 + 2 * m->lanes_n4);
   info->launches_total = m->launches_total;
   return 0;
 }

@@ -56,11 +56,8 @@ struct to_mesh {
   double *ye = nullptr;                // general path: element vectors s_e K0 C_e p
   uint8_t *hmask = nullptr;            // general path: bit c = corner c of the element is hanging
   double *zp = nullptr;                // general path: node records {Dinv r, p}
-  double *qacc = nullptr;              // general path, TOMESH_GENERAL_ATOMIC: atomic q accumulator
   int coop_blocks = 0;                 // general path: grid of the persistent cooperative solver (0 = off)
   int ge_blocks = 0, gn_blocks = 0;    // general path: one resident wave of the element / node pass
-  int lanes_e4 = 0, lanes_n4 = 0;      // 3D general path: 1 = the 4-blocks-per-SM (64-register) variant of the
-                                       // element / node pass, chosen at upload by timing both
   int32_t *filt_idx = nullptr;
   // OC update (allocated on first use)
   double *oc_a = nullptr, *oc_part = nullptr;
@@ -91,6 +88,7 @@ struct to_mesh {
   double *qb[2] = {nullptr, nullptr};   // structured: q ping-pong (qb[0] = q)
   double *dn = nullptr;                 // structured: Dinv per node (internal node order)
   double *partials = nullptr, *hist = nullptr;
+  size_t partials_cap = 0;              // doubles in `partials` (only ever grows)
   int32_t hist_len = 0, hist_cap = 0;
   CgScalars *S = nullptr;
   CgScalars *S_host = nullptr;   // pinned mirror
@@ -114,9 +112,10 @@ struct to_mesh {
   // z-slab sharding (tomesh_shard.cu, kernels_shard.cuh)
   bool sharded = false;
   ShardComm SC{};
-  unsigned long long shard_seq = 1;    // sequence number of the next collective (equal on every rank)
-  double *shard_slots = nullptr;       // [2][kShardMax][kShardVals]
-  unsigned long long *shard_flags = nullptr;   // [2][kShardMax]
+  unsigned long long shard_seq = 1;    // sequence number of the next K1 collective (equal on every rank)
+  unsigned long long tail_seq = 1;     // ... of the next tail collective (tagged kShardTail)
+  double *shard_slots = nullptr;       // [kShardBanks][kShardMax][kShardVals]
+  unsigned long long *shard_flags = nullptr;   // [kShardBanks][kShardMax]
   const int4 *shard_plan = nullptr;    // K1 grid over the owned planes
   int shard_ncta = 0;
   uint8_t *own_dof = nullptr;          // canonical DOF on an owned plane (compliance partial)
@@ -161,6 +160,17 @@ struct to_mesh {
     dev_bytes += (int64_t)(count * sizeof(T));
     *ptr = (T *)d;
     return 0;
+  }
+  // Frees one buffer of this handle (the caller has synchronised every
+  // stream that may still use it).
+  void release(const void *ptr) {
+    for (size_t i = 0; i < bufs.size(); ++i)
+      if (bufs[i].p == ptr) {
+        cudaFree(bufs[i].p);
+        dev_bytes -= (int64_t)bufs[i].bytes;
+        bufs.erase(bufs.begin() + (long)i);
+        return;
+      }
   }
   ~to_mesh() {
     for (auto &b : bufs) cudaFree(b.p);
@@ -214,11 +224,26 @@ int upload_array(to_mesh *m, T **dst, const T *src, size_t count, cudaStream_t s
   return 0;
 }
 
+// The grid-reduction partials: at least n doubles.  Grows only, so a handle
+// never holds a buffer smaller than any grid it launched before (the old
+// buffer stays allocated until tomesh_free; kernels already queued on it
+// finish against it).
+inline int ensure_partials(to_mesh *m, size_t n) {
+  if (n <= m->partials_cap) return 0;
+  RC(m->alloc(&m->partials, n));
+  m->partials_cap = n;
+  return 0;
+}
+
 // Launch with programmatic stream serialization (PDL, see pdl_wait in
-// device_common.cuh) unless TOMESH_NO_PDL is set.
+// device_common.cuh); the A/B build without it defines TOMESH_NO_PDL.
 template <typename... KArgs, typename... Args>
 int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
-  static const bool off = std::getenv("TOMESH_NO_PDL") != nullptr;
+#ifdef TOMESH_NO_PDL
+  constexpr bool off = true;
+#else
+  constexpr bool off = false;
+#endif
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;

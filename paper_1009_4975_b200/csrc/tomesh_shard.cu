@@ -41,10 +41,10 @@ int64_t plane_doubles(const to_mesh *m) { return (int64_t)m->G.NY * m->G.RS; }
 
 int ensure_shard_mem(to_mesh *m, cudaStream_t st) {
   if (m->shard_slots) return 0;
-  RC(m->alloc(&m->shard_slots, (size_t)2 * kShardMax * kShardVals));
-  RC(m->alloc(&m->shard_flags, (size_t)2 * kShardMax));
-  CK(cudaMemsetAsync(m->shard_slots, 0, sizeof(double) * 2 * kShardMax * kShardVals, st));
-  CK(cudaMemsetAsync(m->shard_flags, 0, sizeof(unsigned long long) * 2 * kShardMax, st));
+  RC(m->alloc(&m->shard_slots, (size_t)kShardBanks * kShardMax * kShardVals));
+  RC(m->alloc(&m->shard_flags, (size_t)kShardBanks * kShardMax));
+  CK(cudaMemsetAsync(m->shard_slots, 0, sizeof(double) * kShardBanks * kShardMax * kShardVals, st));
+  CK(cudaMemsetAsync(m->shard_flags, 0, sizeof(unsigned long long) * kShardBanks * kShardMax, st));
   CK(cudaStreamSynchronize(st));
   return 0;
 }
@@ -80,7 +80,10 @@ int check_group(to_mesh *const *ms, int n) {
   for (int i = 0; i < n; ++i) {
     if (!ms[i]) { set_error("NULL handle in group"); return TO_EINVAL; }
     if (!ms[i]->sharded) { set_error("handle %d of the group is not attached (to_shard_attach)", i); return TO_EINVAL; }
-    if (ms[i]->shard_seq != ms[0]->shard_seq) { set_error("group handles out of step (sequence numbers differ)"); return TO_EINVAL; }
+    if (ms[i]->shard_seq != ms[0]->shard_seq || ms[i]->tail_seq != ms[0]->tail_seq) {
+      set_error("group handles out of step (sequence numbers differ)");
+      return TO_EINVAL;
+    }
   }
   return 0;
 }
@@ -191,6 +194,11 @@ extern "C" int to_shard_attach(to_mesh *m, int32_t rank, int32_t nranks, const i
   }
   C.my_slots = m->shard_slots;
   C.my_flags = m->shard_flags;
+  if (m->shard_plan) {   // re-attach: the previous plan is no longer referenced
+    CK(cudaStreamSynchronize(st));
+    m->release(m->shard_plan);
+    m->shard_plan = nullptr;
+  }
   RC(plan_s3(m, st, own_lo, own_hi, true, &m->shard_plan, &m->shard_ncta));
   CK(cudaFuncSetAttribute(k_apply_s3<kS3TYW, S3_CG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)sizeof(S3Smem<kS3TYW>)));
@@ -200,11 +208,12 @@ extern "C" int to_shard_attach(to_mesh *m, int32_t rank, int32_t nranks, const i
   // a (re)attached group restarts its sequence numbers at 1: clear this
   // handle's flags so that no flag of an earlier attachment can match
   // (every rank attaches before any rank solves; ShardRank barriers on it)
-  CK(cudaMemsetAsync(m->shard_flags, 0, sizeof(unsigned long long) * 2 * kShardMax, st));
+  CK(cudaMemsetAsync(m->shard_flags, 0, sizeof(unsigned long long) * kShardBanks * kShardMax, st));
   CK(cudaStreamSynchronize(st));
   m->SC = C;
   m->sharded = true;
   m->shard_seq = 1;
+  m->tail_seq = 1;
   return 0;
 }
 
@@ -248,15 +257,15 @@ extern "C" int tosolve_cg_group(to_mesh *const *ms, int32_t n, double penal, con
     CK(cudaMemsetAsync(m->x, 0, sizeof(double) * m->n_int, S_(i)));
     const int64_t pd = plane_doubles(m), n_own = (int64_t)(m->SC.own_hi - m->SC.own_lo) * pd;
     k_shard_norm2_push<<<grid_for(n_own), kBlock, 0, S_(i)>>>(n_own, m->rb[1] + m->SC.own_lo * pd, m->partials,
-                                                               m->S, m->SC, m->shard_seq);
+                                                               m->S, m->SC, kShardTail | m->tail_seq);
     m->last_launches++;
     RC(check_launch());
   }
   for (int i = 0; i < n; ++i) {
     to_mesh *m = ms[i];
     CK(cudaSetDevice(m->device));
-    k_shard_set_bnorm<<<1, 32, 0, S_(i)>>>(m->SC, m->shard_seq, m->S);
-    m->shard_seq++;
+    k_shard_set_bnorm<<<1, 32, 0, S_(i)>>>(m->SC, kShardTail | m->tail_seq, m->S);
+    m->tail_seq++;
     m->last_launches++;
     RC(check_launch());
   }
@@ -306,15 +315,15 @@ extern "C" int tosolve_cg_group(to_mesh *const *ms, int32_t n, double penal, con
     const int n_own = (int)((m->SC.own_hi - m->SC.own_lo) * pd);
     k_final_s3<true><<<kNumSMs * 4, 512, 0, S_(i)>>>(n_own, m->rb[o] + off, m->qb[o] + off, m->pb[o] + off,
                                                      m->dn + nodes_off, m->x + off, m->partials, m->S, max_iter, rtol,
-                                                     m->hist, m->SC, m->shard_seq);
+                                                     m->hist, m->SC, kShardTail | m->tail_seq);
     m->last_launches++;
     RC(check_launch());
   }
   for (int i = 0; i < n; ++i) {
     to_mesh *m = ms[i];
     CK(cudaSetDevice(m->device));
-    k_shard_final<<<1, 32, 0, S_(i)>>>(m->SC, m->shard_seq, m->S, max_iter, rtol, m->hist);
-    m->shard_seq++;
+    k_shard_final<<<1, 32, 0, S_(i)>>>(m->SC, kShardTail | m->tail_seq, m->S, max_iter, rtol, m->hist);
+    m->tail_seq++;
     m->last_launches++;
     RC(check_launch());
   }
@@ -323,15 +332,16 @@ extern "C" int tosolve_cg_group(to_mesh *const *ms, int32_t n, double penal, con
     to_mesh *m = ms[i];
     CK(cudaSetDevice(m->device));
     const int64_t pd = plane_doubles(m);
-    k_shard_push_x<<<grid_for(3 * pd), kBlock, 0, S_(i)>>>(m->x, pd, m->partials, m->S, m->SC, m->shard_seq);
+    k_shard_push_x<<<grid_for(3 * pd), kBlock, 0, S_(i)>>>(m->x, pd, m->partials, m->S, m->SC,
+                                                           kShardTail | m->tail_seq);
     m->last_launches++;
     RC(check_launch());
   }
   for (int i = 0; i < n; ++i) {
     to_mesh *m = ms[i];
     CK(cudaSetDevice(m->device));
-    k_shard_wait<<<1, 32, 0, S_(i)>>>(m->SC, m->shard_seq, m->S);
-    m->shard_seq++;
+    k_shard_wait<<<1, 32, 0, S_(i)>>>(m->SC, kShardTail | m->tail_seq, m->S);
+    m->tail_seq++;
     m->last_launches++;
     RC(check_launch());
     RC(op_recover_out(m, m->x, u_dev[i], S_(i)));

@@ -51,6 +51,8 @@ constexpr int kS3NBuf = 2;         // staging depth: plane P is issued ~1.5 laye
 // (the gather sums the ranks in rank order on every rank).
 constexpr int kShardMax = 16;          // ranks per group
 constexpr int kShardVals = 8;          // doubles per slot
+constexpr int kShardBanks = 4;         // slot / flag banks: K1 parity 0/1, tail collectives 2/3
+constexpr unsigned long long kShardTail = 1ull << 62;   // sequence tag of the tail collectives
 struct ShardComm {
   int rank, nranks;
   int own_lo, own_hi;                  // owned local node planes
@@ -59,8 +61,8 @@ struct ShardComm {
   // the ends of the stack); [w] = ping-pong buffer w
   double *lo_r[2], *lo_p[2], *lo_q[2], *lo_x;
   double *hi_r[2], *hi_p[2], *hi_q[2], *hi_x;
-  double *slots[kShardMax];            // rank r's slots [2][kShardMax][kShardVals]
-  unsigned long long *flags[kShardMax];   // rank r's flags [2][kShardMax]
+  double *slots[kShardMax];            // rank r's slots [kShardBanks][kShardMax][kShardVals]
+  unsigned long long *flags[kShardMax];   // rank r's flags [kShardBanks][kShardMax]
   double *my_slots;
   unsigned long long *my_flags;
 };

@@ -12,10 +12,10 @@ def rel(a, b):
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
-def product_mesh(prob):
+def product_mesh(prob, options=0):
     import paper_1009_4975_b200 as pb
     hm = pb.prepare(prob)
-    m = pb.Mesh(hm, E0=prob.E0, Emin=prob.Emin, nu=prob.nu, rmin=prob.rmin)
+    m = pb.Mesh(hm, E0=prob.E0, Emin=prob.Emin, nu=prob.nu, rmin=prob.rmin, options=options)
     return hm, m
 
 

@@ -12,7 +12,7 @@ torch = pytest.importorskip("torch")
 from inputs import config
 from oracle import fe, mesh as omesh, pipeline, topopt
 from tests.gpu_helpers import cuda, host, product_input_density, product_mesh, rel
-from tests.helpers import cantilever2d, cantilever3d, refine_some
+from tests.helpers import cantilever2d, cantilever3d, hanging_load2d, hanging_load3d, refine_some
 
 pytestmark = pytest.mark.gpu
 
@@ -27,6 +27,8 @@ CASES = {
     "c2_launches": lambda: config("c2"),     # general path with per-iteration launches (no persistent kernel)
     "amr2d": lambda: cantilever2d((5, 3), L=3, leaves=refine_some(2, (5, 3), 3, [(1, 1), (3, 0)]), rmin=0.3),
     "amr3d": lambda: cantilever3d((3, 2, 2), L=2, leaves=refine_some(3, (3, 2, 2), 2, [(1, 1, 0)]), rmin=0.4),
+    "hload2d": hanging_load2d,       # loads on hanging nodes (C8): b = Pi_F C^T f, c = f^T u with them
+    "hload3d": hanging_load3d,
 }
 
 _cache = {}
@@ -36,15 +38,10 @@ def _setup(name):
     if name not in _cache:
         prob = CASES[name]()
         om = omesh.build_mesh(prob)
-        if name.endswith("_general"):
-            os.environ["TOMESH_FORCE_GENERAL"] = "1"
-        if name.endswith("_launches"):
-            os.environ["TOMESH_NO_PERSISTENT"] = "1"
-        try:
-            hm, m = product_mesh(prob)
-        finally:
-            os.environ.pop("TOMESH_FORCE_GENERAL", None)
-            os.environ.pop("TOMESH_NO_PERSISTENT", None)
+        import paper_1009_4975_b200 as pb
+        opts = (pb.TO_UPLOAD_GENERAL if name.endswith("_general") else 0) | \
+               (pb.TO_UPLOAD_NO_PERSISTENT if name.endswith("_launches") else 0)
+        hm, m = product_mesh(prob, options=opts)
         if name.startswith(("c3s", "c5s")):
             assert m.info()["structured"] == (0 if name.endswith("_general") else 1)
         x_dev = product_input_density(prob, hm, m)
@@ -169,3 +166,21 @@ def test_solver_edge_cases(name):
     assert st.iters == 7 and st.status == pb.TO_NOT_CONVERGED
     assert np.isfinite(host(u)).all()
     assert abs(st.relres_true - st.relres) <= 1e-6 * st.relres
+
+
+@pytest.mark.parametrize("name", ["c4s", "amr3d", "c2_launches"])
+def test_upload_is_deterministic(name):
+    """Two uploads of the same mesh solve to bit-identical u: nothing at upload
+    depends on timing (no timing-based kernel or grid choice), and every
+    reduction sums in a fixed order."""
+    prob, om, hm, m, x_dev = _setup(name)
+    import paper_1009_4975_b200 as pb
+    opts = pb.TO_UPLOAD_NO_PERSISTENT if name.endswith("_launches") else 0
+    us = []
+    for _ in range(2):
+        _, m2 = product_mesh(prob, options=opts)
+        u = torch.zeros(om.n_dof, dtype=torch.float64, device="cuda")
+        m2.tosolve_cg(prob.penal, x_dev, u, rtol=1e-10, max_iter=50000)
+        us.append(u)
+        m2.close()
+    assert torch.equal(us[0], us[1])

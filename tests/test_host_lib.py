@@ -12,7 +12,7 @@ from inputs import config
 from oracle import mesh as omesh, fe
 import paper_1009_4975_b200 as pb
 from paper_1009_4975_b200 import _lib
-from tests.helpers import cantilever2d, cantilever3d, refine_some
+from tests.helpers import cantilever2d, cantilever3d, refine_some, hanging_load2d, hanging_load3d
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -93,7 +93,7 @@ def _compare(prob):
 
 @pytest.mark.parametrize("case", [
     "c1", "c2", "c3", "c4", "c3s", "c5s", "c4s",
-    "amr2d", "amr3d", "ripple2d"])
+    "amr2d", "amr3d", "ripple2d", "hload2d", "hload3d"])
 def test_host_builder_bit_exact_vs_oracle(case):
     if case == "c1":
         prob = config("c1")
@@ -111,9 +111,18 @@ def test_host_builder_bit_exact_vs_oracle(case):
         prob = cantilever2d((5, 3), L=3, leaves=refine_some(2, (5, 3), 3, [(1, 1), (3, 0)]), rmin=0.3)
     elif case == "amr3d":
         prob = cantilever3d((3, 2, 2), L=2, leaves=refine_some(3, (3, 2, 2), 2, [(1, 1, 0)]), rmin=0.4)
+    elif case == "hload2d":
+        prob = hanging_load2d()
+    elif case == "hload3d":
+        prob = hanging_load3d()
     else:
         prob = cantilever2d((4, 4), L=4, leaves=refine_some(2, (4, 4), 4, [(1, 1)]), rmin=0.2)
     hm, om = _compare(prob)
+    if case.startswith("hload"):
+        # C8: loads on hanging nodes stay in f (both sides); two loaded nodes are hanging
+        d = om.dim
+        loaded = {n for n in range(om.n_node) if np.any(om.load[d * n:d * n + d] != 0.0)}
+        assert len(loaded & set(om.hang_node.tolist())) == 2
     if case in ("c2", "c4", "c4s", "amr2d", "amr3d", "ripple2d"):
         assert hm.hang_node.size > 0
 
@@ -167,7 +176,7 @@ def test_product_hadamard_factorisation(nu, rng):
 # ---- dynamic AMR mesh update: C++ host code vs oracle/amr.py (bit-exact) ----------------
 
 def _amr_cases():
-    from tests.helpers import cantilever2d, cantilever3d, refine_some
+    from tests.helpers import cantilever2d, cantilever3d, refine_some, hanging_load2d, hanging_load3d
     return [
         cantilever2d((6, 3), L=3, leaves=refine_some(2, (6, 3), 3, [(1, 1), (4, 0), (2, 2)]), rmin=0.9),
         cantilever3d((3, 2, 2), L=2, leaves=refine_some(3, (3, 2, 2), 2, [(1, 1, 0), (0, 0, 1)]), rmin=0.7),
