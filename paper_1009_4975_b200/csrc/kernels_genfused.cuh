@@ -1,0 +1,372 @@
+// General (AMR) path, one PCG iteration = ONE kernel (k_gen_fused).  Same
+// operator as every other path (Eq. 8 with Dirichlet rows, PAPER.md:678-682:
+// A = Pi_F C^T K C Pi_F + (I - Pi_F), the hanging-node interpolation C of
+// Eq. 6, :653-663, applied at the element gather and transposed at the
+// scatter), same Hestenes-Stiefel recurrences on the rescaled system
+// (reading R3) in the single-kernel form of the structured
+// path (kernels_struct3d.cuh, kernels_cg.cuh cg_single_step).
+//
+// Decomposition ("owner computes", built on the host at upload, tomesh.cu
+// build_gen_blocks): the canonical node order (Morton, C3) is cut into
+// contiguous ranges; CTA b OWNS the nodes [node0[b], node0[b+1]).  It stages
+//   * every element that contributes to an owned node (directly, or through a
+//     hanging corner whose parent is owned) -- the halo elements are
+//     recomputed by each CTA that needs them, so no element result ever
+//     leaves the CTA and no atomics or element buffers are needed;
+//   * the "local nodes": owned nodes (slots [0, nOwn), contiguous in global
+//     memory), halo nodes (the other non-hanging corners and parents,
+//     ascending global id) and one virtual slot per hanging corner node
+//     (ascending id) holding the Eq. 6 interpolation of its parents.
+// Per iteration k (alpha_{k-1}, beta_{k-1} from the previous kernel's last
+// block; buffers ping-pong as in K1: read (k+1)&1, write k&1):
+//   1. every local node: r_k = r_{k-1} - alpha q_{k-1}, z_k = Dinv r_k,
+//      p_k = z_k + beta p_{k-1} into shared memory; owners also store r_k,
+//      p_k, x += alpha p_{k-1} and reduce rho_k = r_k.z_k, rr_k;
+//   2. virtual slots: p of a hanging node = sum_parents w p_parent (Eq. 6);
+//   3. elements in chunks of kGfChunk: lane c of an element group gathers
+//      corner c from shared memory, the element product (Hadamard form of K0
+//      in 3D, dense in 2D, across the group by warp shuffles) times s_e goes
+//      to a shared chunk buffer; then every owned node sums its block-local
+//      incidences (element, corner, weight 1 or the Eq. 6 weight: C^T) of that
+//      chunk in ascending order -- a fixed summation order, so the result is
+//      bit-reproducible;
+//   4. owners store q_k (0 on non-free DOFs) and reduce p.q, q.z, q.Dinv q;
+//      one grid reduction; the last block forms alpha_k and beta_k
+//      (cg_single_step, one-step rho expansion) and tests rr_k.
+// PLAIN mode (operator-level calls, warm start, true residual, MINRES):
+// step 1 loads v, step 4 stores q = C^T K C v on the owned nodes, no dots.
+#pragma once
+#include "device_common.cuh"
+#include "element.h"
+#include "kernels_cg.cuh"
+#include "kernels_general.cuh"
+#include "tomesh_types.cuh"
+
+namespace tomesh {
+
+constexpr int kGfThreads = 256;
+constexpr int kGfOwnPerThread = 2;                       // owned nodes per thread (max_own <= 512)
+constexpr int kGfMaxOwn = kGfThreads * kGfOwnPerThread;
+constexpr int kGfMaxLoc = 1536;                          // local node slots per block (uint16 slots)
+#ifndef TOMESH_GF_OWN3
+#define TOMESH_GF_OWN3 320
+#endif
+#ifndef TOMESH_GF_OWN2
+#define TOMESH_GF_OWN2 448
+#endif
+constexpr int kGfOwnTarget3 = TOMESH_GF_OWN3;           // owned nodes per block before splitting (3D)
+constexpr int kGfOwnTarget2 = TOMESH_GF_OWN2;           // (2D)
+
+template <int DIM>
+struct GfChunk {
+  static constexpr int NC = 1 << DIM;
+  static constexpr int CH = kGfThreads * (DIM == 3 ? 4 : 8) / NC;   // elements per chunk (1024 lane tasks)
+};
+
+__host__ __device__ constexpr int gf_pad16(int bytes) { return (bytes + 15) & ~15; }
+
+// Byte offsets of the sections of a block record (tomesh_types.cuh GfMeta).
+struct GfSections {
+  int halo, virt, corner, iptr, inc, total;
+};
+template <int DIM>
+__host__ __device__ inline GfSections gf_sections(int n_own, int n_halo, int n_virt, int n_el, int n_inc) {
+  GfSections s;
+  s.halo = 0;
+  s.virt = s.halo + gf_pad16(4 * n_halo);
+  s.corner = s.virt + gf_pad16(8 * n_virt);
+  s.iptr = s.corner + gf_pad16(2 * (1 << DIM) * n_el);
+  s.inc = s.iptr + gf_pad16(2 * (n_own + 1));
+  s.total = s.inc + gf_pad16(2 * n_inc);
+  return s;
+}
+
+// Dynamic shared memory of k_gen_fused in bytes: the block record, s_e of
+// the block's elements, local node values P, the owners' z and Dinv, one
+// chunk of element results, the mbarrier.
+template <int DIM>
+__host__ __device__ constexpr size_t gf_smem_bytes(int max_rec16, int max_el, int max_loc, int max_own) {
+  return (size_t)16 * max_rec16 + 8 * (size_t)((max_el + 1) & ~1) +
+         8 * ((size_t)max_loc * DIM + 2 * (size_t)max_own * DIM + (size_t)GfChunk<DIM>::CH * (1 << DIM) * DIM) + 16;
+}
+
+// Lane c of an 2^DIM-lane group holds v = the element's corner c values;
+// returns y = (K0 v)[corner c] (unit modulus, h = 1).  3D: Walsh-Hadamard
+// stages as xor-shuffles, lane c = Hadamard mode c (element.h); 2D: dense.
+template <int DIM>
+__device__ __forceinline__ void gf_elem_lane(const double (&v_in)[DIM], int c, const K0Dense2 &K2, const K0HadSym &H,
+                                             double (&y)[DIM]) {
+  double v[DIM];
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) v[i] = v_in[i];
+  if constexpr (DIM == 3) {
+#pragma unroll
+    for (int b = 1; b < 8; b <<= 1)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double o = __shfl_xor_sync(0xffffffffu, v[i], b);
+        v[i] = (c & b) ? o - v[i] : v[i] + o;
+      }
+    const int m = c;
+    const int bit[3] = {m & 1, (m >> 1) & 1, (m >> 2) & 1};
+    const int pop = bit[0] + bit[1] + bit[2];
+    double xo[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = i + 1; j < 3; ++j) {
+        const int mask = (1 << i) | (1 << j);
+        xo[i][j] = __shfl_xor_sync(0xffffffffu, v[j], mask);
+        xo[j][i] = __shfl_xor_sync(0xffffffffu, v[i], mask);
+      }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int b = bit[i], nn = pop - b;
+      const double dco = b ? (nn == 0 ? H.d[1][0] : nn == 1 ? H.d[1][1] : H.d[1][2])
+                           : (nn == 0 ? 0.0 : nn == 1 ? H.d[0][1] : H.d[0][2]);
+      double acc = dco * v[i];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        if (j == i) continue;
+        const int t = 3 - i - j;
+        const double oco = b ? (bit[t] ? H.o[1][1] : H.o[1][0]) : (bit[t] ? H.o[0][1] : H.o[0][0]);
+        acc = (bit[j] != b) ? fma(oco, xo[i][j], acc) : acc;
+      }
+      y[i] = acc;
+    }
+#pragma unroll
+    for (int b = 1; b < 8; b <<= 1)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double o = __shfl_xor_sync(0xffffffffu, y[i], b);
+        y[i] = (c & b) ? o - y[i] : y[i] + o;
+      }
+  } else {
+    const int base = (threadIdx.x & 31) & ~3;
+    double vv[4][2];
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) vv[cc][j] = __shfl_sync(0xffffffffu, v[j], base + cc);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc = fma(K2.K[(2 * c + i) * 8 + 2 * cc + j], vv[cc][j], acc);
+      y[i] = acc;
+    }
+  }
+}
+
+__device__ __forceinline__ double gf_weight(unsigned code) { return code == 0 ? 1.0 : code == 1 ? 0.5 : 0.25; }
+
+template <int DIM, int MODE>
+__global__ void __launch_bounds__(kGfThreads, 2)
+k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_loc, const double *__restrict__ ro,
+            const double *__restrict__ qo, const double *__restrict__ po, const double *__restrict__ Dinv,
+            double *__restrict__ rw, double *__restrict__ pw, double *__restrict__ qw, double *__restrict__ x,
+            const __grid_constant__ K0Dense2 K2, const __grid_constant__ K0HadSym H, CgScalars *S,
+            double *partials, int kit, double rtol, double *hist) {
+  constexpr bool CG = MODE == G_CG;
+  constexpr int NC = 1 << DIM, CH = GfChunk<DIM>::CH;
+  extern __shared__ __align__(16) unsigned char gsm_raw[];
+  const int tid = threadIdx.x;
+  const GfMeta mt = B.meta[blockIdx.x];
+  const int nOwn = mt.n_own, nHalo = mt.n_halo, nVirt = mt.n_virt, nE = mt.n_el;
+  const GfSections sec = gf_sections<DIM>(nOwn, nHalo, nVirt, nE, mt.n_inc);
+  unsigned char *rec = gsm_raw;                                     // the block record
+  double *sl = reinterpret_cast<double *>(gsm_raw + 16 * (size_t)B.max_rec16);   // s_e of the elements
+  double *P = sl + ((B.max_el + 1) & ~1);                            // [max_loc][DIM]
+  double *Zs = P + (size_t)B.max_loc * DIM;                          // [max_own][DIM] z_k of owned DOFs
+  double *Ds = Zs + (size_t)B.max_own * DIM;                         // [max_own][DIM] Dinv of owned DOFs
+  double *Y = Ds + (size_t)B.max_own * DIM;                          // [CH][NC][DIM] element results
+  unsigned long long *bar = reinterpret_cast<unsigned long long *>(Y + (size_t)CH * NC * DIM);
+  const int32_t *halo = reinterpret_cast<const int32_t *>(rec + sec.halo);
+  const ushort4 *virt = reinterpret_cast<const ushort4 *>(rec + sec.virt);
+  const uint16_t *corner = reinterpret_cast<const uint16_t *>(rec + sec.corner);
+  const uint16_t *iptr = reinterpret_cast<const uint16_t *>(rec + sec.iptr);
+  const uint16_t *inc = reinterpret_cast<const uint16_t *>(rec + sec.inc);
+  // static block data and s_e (written before the first iteration's launch):
+  // one bulk copy each, issued before the wait on the previous iteration
+  const unsigned s_bytes = 8u * (unsigned)((nE + 1) & ~1);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_proxy_async();
+    mbar_arrive_expect_tx(bar, (unsigned)sec.total + s_bytes);
+    bulk_load_1d(rec, B.rec + mt.rec_off16, (unsigned)sec.total, bar);
+    if (s_bytes) bulk_load_1d(sl, s_loc + mt.el_off, s_bytes, bar);
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_release();
+  if (CG && cg_stopped(S)) {
+    mbar_wait(bar, 0);   // no bulk copy may still be writing when the CTA exits
+    return;
+  }
+  const double alpha = CG ? __ldcg(&S->alpha) : 0.0;
+  const double beta = CG ? __ldcg(&S->beta) : 0.0;
+  const int64_t g0 = (int64_t)mt.node0 * DIM;
+  double rho = 0.0, rr = 0.0;
+  // 1. owned nodes (contiguous DOFs)
+#pragma unroll 4
+  for (int j = tid; j < nOwn * DIM; j += kGfThreads) {
+    const int64_t g = g0 + j;
+    if (CG) {
+      const double r_o = __ldg(ro + g), q_o = __ldg(qo + g), p_o = __ldg(po + g), d = __ldg(Dinv + g);
+      const double rn = fma(-alpha, q_o, r_o);          // q is 0 on non-free DOFs, so r stays 0 there
+      const double z = d * rn;
+      const double pn = fma(beta, p_o, z);
+      rw[g] = rn;
+      pw[g] = pn;
+      if (alpha != 0.0) x[g] = fma(alpha, p_o, x[g]);
+      rho = fma(rn, z, rho);
+      rr = fma(rn, rn, rr);
+      P[j] = pn;
+      Zs[j] = z;
+      Ds[j] = d;
+    } else {
+      P[j] = __ldg(po + g);
+    }
+  }
+  mbar_wait(bar, 0);
+  // ... and halo nodes
+#pragma unroll 4
+  for (int j = tid; j < nHalo * DIM; j += kGfThreads) {
+    const int node = halo[j / DIM];
+    const int64_t g = (int64_t)node * DIM + (j % DIM);
+    double pn;
+    if (CG) {
+      const double r_o = __ldg(ro + g), q_o = __ldg(qo + g), p_o = __ldg(po + g), d = __ldg(Dinv + g);
+      pn = fma(beta, p_o, d * fma(-alpha, q_o, r_o));
+    } else {
+      pn = __ldg(po + g);
+    }
+    P[nOwn * DIM + j] = pn;
+  }
+  __syncthreads();
+  // 2. hanging corners: Eq. 6 interpolation of the parents (ascending parent order)
+  {
+    const int vb = (nOwn + nHalo) * DIM;
+    for (int v = tid; v < nVirt; v += kGfThreads) {
+      const ushort4 pv = virt[v];
+      const int np = pv.z == 0xffff ? 2 : 4;
+      const double w = np == 2 ? 0.5 : 0.25;
+      const int par[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        double acc = 0.0;
+        for (int k = 0; k < np; ++k) acc = fma(w, P[par[k] * DIM + i], acc);
+        P[vb + v * DIM + i] = acc;
+      }
+    }
+  }
+  __syncthreads();
+  // 3. elements by chunks; owned nodes sum their incidences of each chunk
+  int cur[kGfOwnPerThread], cend[kGfOwnPerThread];
+  double qa[kGfOwnPerThread][DIM];
+#pragma unroll
+  for (int u = 0; u < kGfOwnPerThread; ++u) {
+    const int o = tid + u * kGfThreads;
+    cur[u] = cend[u] = 0;
+    if (o < nOwn) {
+      cur[u] = iptr[o];
+      cend[u] = iptr[o + 1];
+    }
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) qa[u][i] = 0.0;
+  }
+  for (int c0 = 0; c0 < nE; c0 += CH) {
+    // lane tasks: CH * NC = a multiple of the block, so every warp stays converged
+#pragma unroll 2
+    for (int t = tid; t < CH * NC; t += kGfThreads) {
+      const int lc = t / NC, c = t % NC;
+      const int le = c0 + lc;
+      const bool live = le < nE;
+      const int lq = live ? le : nE - 1;
+      const int slot = corner[lq * NC + c];
+      const double se = sl[lq];
+      double v[DIM], y[DIM];
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) v[i] = P[slot * DIM + i];
+      gf_elem_lane<DIM>(v, c, K2, H, y);
+      if (live) {
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) Y[(lc * NC + c) * DIM + i] = se * y[i];
+      }
+    }
+    __syncthreads();
+    const int lim = (c0 + CH) * NC;
+#pragma unroll
+    for (int u = 0; u < kGfOwnPerThread; ++u) {
+      while (cur[u] < cend[u]) {
+        const unsigned ent = inc[cur[u]];
+        const int lec = (int)(ent & 0x3fffu);
+        if (lec >= lim) break;
+        const double w = gf_weight(ent >> 14);
+        const double *src = Y + (size_t)(lec - c0 * NC) * DIM;
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) qa[u][i] = fma(w, src[i], qa[u][i]);
+        ++cur[u];
+      }
+    }
+    __syncthreads();
+  }
+  // 4. owners: q (masked), dots
+  double pq = 0.0, qz = 0.0, qdq = 0.0;
+#pragma unroll
+  for (int u = 0; u < kGfOwnPerThread; ++u) {
+    const int o = tid + u * kGfThreads;
+    if (o >= nOwn) continue;
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) {
+      const int j = o * DIM + i;
+      if (CG) {
+        const double d = Ds[j];
+        const double q = d != 0.0 ? qa[u][i] : 0.0;
+        qw[g0 + j] = q;
+        pq = fma(P[j], q, pq);
+        qz = fma(Zs[j], q, qz);
+        qdq = fma(d * q, q, qdq);
+      } else {
+        qw[g0 + j] = qa[u][i];
+      }
+    }
+  }
+  if (CG) {
+    double dots[5] = {rho, rr, pq, qz, qdq};
+    if (grid_sum<5>(dots, partials, &S->counter[CNT_PQ])) cg_single_step(S, kit, dots, rtol, hist);
+  }
+}
+
+// After exactly N iterations (general path): r_N = r_{N-1} - alpha q_{N-1},
+// x_N = x_{N-1} + alpha p_{N-1}, rho_N, rr_N (per-DOF Dinv).
+static __global__ void k_final_gen(int64_t n, const double *__restrict__ ro, const double *__restrict__ qo,
+                                   const double *__restrict__ po, const double *__restrict__ Dinv,
+                                   double *__restrict__ x, double *partials, CgScalars *S, int n_iter, double rtol,
+                                   double *hist) {
+  if (cg_stopped(S)) return;
+  const double alpha = __ldcg(&S->alpha);
+  double acc[2] = {0.0, 0.0};
+  GRID_STRIDE(i, n) {
+    const double d = __ldg(Dinv + i);
+    const double rn = fma(-alpha, __ldg(qo + i), __ldg(ro + i));
+    if (alpha != 0.0) x[i] = fma(alpha, __ldg(po + i), x[i]);
+    acc[0] = fma(rn, d * rn, acc[0]);
+    acc[1] = fma(rn, rn, acc[1]);
+  }
+  if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) cg_final_step(S, n_iter, acc[0], acc[1], rtol, hist);
+}
+
+// s_loc[j] = s[el_id[j]]: the SIMP factors in block-local element order (once
+// per solve; el_id = -1 on the padding slots, which get 0).
+static __global__ void k_gather_s(int64_t n, const int32_t *__restrict__ el_id, const double *__restrict__ s,
+                                  double *__restrict__ s_loc) {
+  GRID_STRIDE(j, n) {
+    const int32_t e = el_id[j];
+    s_loc[j] = e >= 0 ? __ldg(s + e) : 0.0;
+  }
+}
+
+}  // namespace tomesh

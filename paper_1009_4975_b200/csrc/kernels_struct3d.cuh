@@ -70,7 +70,6 @@ __device__ __forceinline__ int64_t s3_nrow(const GridView &G, int j, int k) {
 
 constexpr int s3_pad128(int doubles) { return (doubles + 15) / 16 * 16; }   // 128-byte multiple
 
-__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 enum { S3_PLAIN = 0, S3_CG = 1 };
 
@@ -89,24 +88,6 @@ struct S3Smem {
   unsigned long long mbar[kS3NBuf];
 };
 
-__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
 // 3D tiled TMA load of one box (OOB elements zero-filled; the transaction
 // count is always the full box).
 __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2,
@@ -117,7 +98,6 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 struct S3Maps {           // TMA maps of the arrays one K1 launch stages
   CUtensorMap a, q, p, d;   // r_{k-1} (or v), q_{k-1}, p_{k-1}, Dinv

@@ -5,6 +5,7 @@
 #include "tomesh_impl.cuh"
 #include "kernels_cg.cuh"
 #include "kernels_general.cuh"
+#include "kernels_genfused.cuh"
 #include "kernels_struct3d.cuh"
 
 using namespace tomesh;
@@ -266,10 +267,11 @@ int setup_structured(const to_mesh_desc *d, const std::vector<uint8_t> &free_dof
 // of the gather C_e P_e: a non-hanging corner contributes to its node with
 // weight 1, a hanging corner to each parent with the Eq. 6 weight.  Entries
 // per node in ascending (element, corner) order (deterministic sums).
-int setup_incidence(const to_mesh_desc *d, const std::vector<int32_t> &node_hang, cudaStream_t st, to_mesh *m) {
+int setup_incidence(const to_mesh_desc *d, const std::vector<int32_t> &node_hang, cudaStream_t st, to_mesh *m,
+                    std::vector<int64_t> &ptr, std::vector<uint32_t> &inc) {
   const int nc = 1 << d->dim;
   if ((int64_t)d->n_elem * nc >= (1LL << 30)) { set_error("mesh too large for the packed incidence list"); return TO_EINVAL; }
-  std::vector<int64_t> ptr(d->n_node + 1, 0);
+  ptr.assign(d->n_node + 1, 0);
   for (int64_t e = 0; e < d->n_elem; ++e)
     for (int c = 0; c < nc; ++c) {
       const int32_t n = d->elem_node[e * nc + c];
@@ -279,7 +281,7 @@ int setup_incidence(const to_mesh_desc *d, const std::vector<int32_t> &node_hang
         for (int32_t k = d->hang_ptr[h]; k < d->hang_ptr[h + 1]; ++k) ptr[d->hang_parent[k] + 1]++;
     }
   for (int64_t n = 0; n < d->n_node; ++n) ptr[n + 1] += ptr[n];
-  std::vector<uint32_t> inc(ptr[d->n_node]);
+  inc.assign(ptr[d->n_node], 0u);
   std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
   auto code = [](double w) -> uint32_t { return w == 1.0 ? 0u : w == 0.5 ? 1u : 2u; };
   for (int64_t e = 0; e < d->n_elem; ++e)
@@ -302,9 +304,221 @@ int setup_incidence(const to_mesh_desc *d, const std::vector<int32_t> &node_hang
   RC(upload_array(m, &m->hmask, hmask.data(), hmask.size(), st));
   RC(upload_array(m, &m->inc_ptr, ptr.data(), ptr.size(), st));
   RC(upload_array(m, &m->inc, inc.data(), inc.size(), st));
+  return 0;
+}
+
+// Element-vector buffer and node records of the two-pass general operator
+// (only the 2D persistent cooperative solver uses them).
+int setup_two_pass(const to_mesh_desc *d, cudaStream_t st, to_mesh *m) {
+  const int nc = 1 << d->dim;
   RC(m->alloc(&m->ye, (size_t)d->n_elem * nc * d->dim));
   RC(m->alloc(&m->zp, (size_t)d->n_node * 2 * d->dim));
   CK(cudaMemsetAsync(m->ye, 0, sizeof(double) * (size_t)d->n_elem * nc * d->dim, st));
+  return 0;
+}
+
+// Owner-computes decomposition of the single-kernel general iteration
+// (kernels_genfused.cuh).  Canonical nodes are cut into contiguous ranges of
+// about `own_target` nodes (Morton order keeps a range compact in space);
+// a range whose staged elements or local slots exceed the kernel's limits
+// is split in halves until it fits.  Every array is ordered deterministically
+// (elements and halo / hanging nodes ascending), so the decomposition, and
+// with it every summation order, depends on the mesh only.
+int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_hang, const std::vector<int64_t> &iptr,
+                     const std::vector<uint32_t> &inc, cudaStream_t st, to_mesh *m) {
+  const int nc = 1 << d->dim;
+  const int64_t N = d->n_node;
+  const int own_target = d->dim == 3 ? kGfOwnTarget3 : kGfOwnTarget2;
+  const int el_max = (1 << 14) / nc - 1, loc_max = kGfMaxLoc;
+  std::vector<int32_t> el_mark(d->n_elem, -1), nd_mark(N, -1), el_le(d->n_elem, 0), nd_slot(N, 0);
+  int stamp = 0;
+  auto elem_of = [&](uint32_t t) { return (int64_t)((t & 0x3fffffffu) / (uint32_t)nc); };
+  auto fits = [&](int64_t a, int64_t b) {
+    if (b - a > kGfMaxOwn) return false;
+    const int sp = ++stamp;
+    int64_t nE = 0, nOut = 0;
+    for (int64_t n = a; n < b; ++n)
+      for (int64_t k = iptr[n]; k < iptr[n + 1]; ++k) {
+        const int64_t e = elem_of(inc[k]);
+        if (el_mark[e] == sp) continue;
+        el_mark[e] = sp;
+        ++nE;
+        for (int c = 0; c < nc; ++c) {
+          const int32_t g = d->elem_node[e * nc + c];
+          const int32_t h = node_hang[g];
+          if (h < 0) {
+            if ((g < a || g >= b) && nd_mark[g] != sp) { nd_mark[g] = sp; ++nOut; }
+          } else {
+            if (nd_mark[g] != sp) { nd_mark[g] = sp; ++nOut; }
+            for (int32_t q = d->hang_ptr[h]; q < d->hang_ptr[h + 1]; ++q) {
+              const int32_t pn = d->hang_parent[q];
+              if ((pn < a || pn >= b) && nd_mark[pn] != sp) { nd_mark[pn] = sp; ++nOut; }
+            }
+          }
+        }
+      }
+    return nE <= el_max && (b - a) + nOut <= loc_max;
+  };
+  std::vector<int32_t> node0;
+  {
+    std::vector<std::pair<int64_t, int64_t>> todo;
+    for (int64_t a = 0; a < N; a += own_target) todo.push_back({a, std::min<int64_t>(N, a + own_target)});
+    std::reverse(todo.begin(), todo.end());
+    while (!todo.empty()) {
+      auto [a, b] = todo.back();
+      todo.pop_back();
+      if (fits(a, b)) {
+        node0.push_back((int32_t)a);
+        continue;
+      }
+      if (b - a <= 1) { set_error("general-path block of node %lld exceeds the kernel limits", (long long)a); return TO_EINVAL; }
+      const int64_t mid = a + (b - a) / 2;
+      todo.push_back({mid, b});
+      todo.push_back({a, mid});
+    }
+    node0.push_back((int32_t)N);
+  }
+  const int nb = (int)node0.size() - 1;
+  std::vector<GfMeta> meta(nb);
+  std::vector<uint8_t> rec;
+  std::vector<int32_t> el_id;
+  int max_loc = 0, max_own = 0, max_rec16 = 0, max_el = 0;
+  std::vector<int64_t> elems;
+  std::vector<int32_t> hl, vt;
+  std::vector<uint16_t> iptr_l, inc_l;
+  auto put = [&](const void *src, size_t bytes) {
+    const size_t at = rec.size();
+    rec.resize(at + ((bytes + 15) & ~(size_t)15), 0);
+    if (bytes) std::memcpy(rec.data() + at, src, bytes);
+  };
+  for (int bk = 0; bk < nb; ++bk) {
+    const int64_t a = node0[bk], b = node0[bk + 1];
+    const int sp = ++stamp;
+    elems.clear();
+    hl.clear();
+    vt.clear();
+    for (int64_t n = a; n < b; ++n)
+      for (int64_t k = iptr[n]; k < iptr[n + 1]; ++k) {
+        const int64_t e = elem_of(inc[k]);
+        if (el_mark[e] != sp) { el_mark[e] = sp; elems.push_back(e); }
+      }
+    std::sort(elems.begin(), elems.end());
+    for (size_t i = 0; i < elems.size(); ++i) el_le[elems[i]] = (int32_t)i;
+    for (int64_t e : elems)
+      for (int c = 0; c < nc; ++c) {
+        const int32_t g = d->elem_node[e * nc + c];
+        const int32_t h = node_hang[g];
+        if (h < 0) {
+          if ((g < a || g >= b) && nd_mark[g] != sp) { nd_mark[g] = sp; hl.push_back(g); }
+        } else {
+          if (nd_mark[g] != sp) { nd_mark[g] = sp; vt.push_back(g); }
+          for (int32_t q = d->hang_ptr[h]; q < d->hang_ptr[h + 1]; ++q) {
+            const int32_t pn = d->hang_parent[q];
+            if ((pn < a || pn >= b) && nd_mark[pn] != sp) { nd_mark[pn] = sp; hl.push_back(pn); }
+          }
+        }
+      }
+    std::sort(hl.begin(), hl.end());
+    std::sort(vt.begin(), vt.end());
+    const int nOwn = (int)(b - a), nHalo = (int)hl.size(), nVirt = (int)vt.size(), nE = (int)elems.size();
+    for (int i = 0; i < nHalo; ++i) nd_slot[hl[i]] = nOwn + i;
+    for (int i = 0; i < nVirt; ++i) nd_slot[vt[i]] = nOwn + nHalo + i;
+    auto slot = [&](int32_t g) { return (g >= a && g < b && node_hang[g] < 0) ? (int)(g - a) : nd_slot[g]; };
+    std::vector<ushort4> vrec(nVirt);
+    for (int i = 0; i < nVirt; ++i) {
+      const int32_t g = vt[i], h = node_hang[g];
+      const int np = d->hang_ptr[h + 1] - d->hang_ptr[h];
+      if (np != 2 && np != 4) { set_error("hanging node %d has %d parents (2 or 4 expected)", g, np); return TO_EMESH; }
+      uint16_t ps[4] = {0xffff, 0xffff, 0xffff, 0xffff};
+      for (int q = 0; q < np; ++q) {
+        const double w = d->hang_weight[d->hang_ptr[h] + q];
+        if (w != 1.0 / np) { set_error("hanging node %d: weight %g with %d parents", g, w, np); return TO_EMESH; }
+        ps[q] = (uint16_t)slot(d->hang_parent[d->hang_ptr[h] + q]);
+      }
+      vrec[i] = make_ushort4(ps[0], ps[1], ps[2], ps[3]);
+    }
+    std::vector<uint16_t> crec((size_t)nE * nc);
+    for (int i = 0; i < nE; ++i)
+      for (int c = 0; c < nc; ++c) crec[(size_t)i * nc + c] = (uint16_t)slot(d->elem_node[elems[i] * nc + c]);
+    iptr_l.assign(1, 0);
+    inc_l.clear();
+    for (int64_t n = a; n < b; ++n) {
+      for (int64_t k = iptr[n]; k < iptr[n + 1]; ++k) {
+        const uint32_t t = inc[k];
+        const int64_t e = elem_of(t);
+        const uint32_t c = (t & 0x3fffffffu) % (uint32_t)nc, code = t >> 30;
+        inc_l.push_back((uint16_t)(((uint32_t)el_le[e] * nc + c) | (code << 14)));
+      }
+      if (inc_l.size() > 0xffff) { set_error("general-path block with more than 65535 incidences"); return TO_EINVAL; }
+      iptr_l.push_back((uint16_t)inc_l.size());
+    }
+    GfMeta &mt = meta[bk];
+    mt.node0 = (int32_t)a;
+    mt.n_own = nOwn;
+    mt.n_halo = nHalo;
+    mt.n_virt = nVirt;
+    mt.n_el = nE;
+    mt.n_inc = (int32_t)inc_l.size();
+    mt.el_off = (int32_t)el_id.size();
+    mt.rec_off16 = (int32_t)(rec.size() / 16);
+    const size_t r0 = rec.size();
+    put(hl.data(), 4 * hl.size());
+    put(vrec.data(), 8 * vrec.size());
+    put(crec.data(), 2 * crec.size());
+    put(iptr_l.data(), 2 * iptr_l.size());
+    put(inc_l.data(), 2 * inc_l.size());
+    const GfSections sec = d->dim == 3 ? gf_sections<3>(nOwn, nHalo, nVirt, nE, mt.n_inc)
+                                       : gf_sections<2>(nOwn, nHalo, nVirt, nE, mt.n_inc);
+    if ((size_t)sec.total != rec.size() - r0) { set_error("internal: block record layout"); return TO_EINVAL; }
+    for (int64_t e : elems) el_id.push_back((int32_t)e);
+    if (nE & 1) el_id.push_back(-1);   // every block's s_e starts 16-byte aligned
+    max_loc = std::max(max_loc, nOwn + nHalo + nVirt);
+    max_own = std::max(max_own, nOwn);
+    max_rec16 = std::max(max_rec16, sec.total / 16);
+    max_el = std::max(max_el, nE);
+  }
+  if (rec.size() / 16 >= (size_t)INT32_MAX || el_id.size() >= (size_t)INT32_MAX) { set_error("mesh too large for the general-path records"); return TO_EINVAL; }
+  GenBlocks &B = m->GB;
+  B.n_blk = nb;
+  B.max_loc = max_loc;
+  B.max_own = max_own;
+  B.max_rec16 = max_rec16;
+  B.max_el = max_el;
+  GfMeta *dmeta;
+  uint4 *drec;
+  int32_t *deid;
+  RC(upload_array(m, &dmeta, meta.data(), meta.size(), st));
+  RC(upload_array(m, &drec, reinterpret_cast<const uint4 *>(rec.data()), rec.size() / 16, st));
+  RC(upload_array(m, &deid, el_id.data(), el_id.size(), st));
+  B.meta = dmeta;
+  B.rec = drec;
+  m->gb_el_id = deid;
+  m->gb_n_loc_el = (int64_t)el_id.size();
+  RC(m->alloc(&m->s_loc, (size_t)std::max<int64_t>(2, m->gb_n_loc_el)));
+  m->gb_smem = d->dim == 3 ? gf_smem_bytes<3>(max_rec16, max_el, max_loc, max_own)
+                           : gf_smem_bytes<2>(max_rec16, max_el, max_loc, max_own);
+  // the attribute is per function, not per handle: allow the device's opt-in
+  // maximum (less the kernel's static shared memory) so that a later upload
+  // of a smaller mesh cannot lower it below what an earlier handle launches with
+  int optin = 0;
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
+  auto allow = [&](const void *fn) -> int {
+    cudaFuncAttributes fa{};
+    CK(cudaFuncGetAttributes(&fa, fn));
+    const int dyn = optin - (int)fa.sharedSizeBytes;
+    if (m->gb_smem > (size_t)dyn) { set_error("general-path blocks need %zu bytes of shared memory", m->gb_smem); return TO_EINVAL; }
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    return 0;
+  };
+  if (d->dim == 3) {
+    RC(allow((const void *)k_gen_fused<3, G_CG>));
+    RC(allow((const void *)k_gen_fused<3, G_PLAIN>));
+  } else {
+    RC(allow((const void *)k_gen_fused<2, G_CG>));
+    RC(allow((const void *)k_gen_fused<2, G_PLAIN>));
+  }
+  RC(ensure_partials(m, (size_t)nb * 5));
+  m->gen_fused = true;
   return 0;
 }
 
@@ -412,42 +626,28 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
     RC(m->alloc(&m->ftmp, (size_t)m->n_el));
   }
   if (!m->structured) {
-    RC(setup_incidence(d, node_hang, st, m));
-    // launched passes: one resident wave (the end-of-pass reduction then runs once per block slot)
-    {
-      int pe = 0, pn = 0;
-      if (d->dim == 2) {
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pe, k_elem_pass_lanes<2, G_CG>, kBlock, 0));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pn, k_node_pass_lanes<2, G_CG>, kBlock, 0));
-      } else {
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pe, k_elem_pass_lanes<3, G_CG>, kBlock, 0));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pn, k_node_pass_lanes<3, G_CG>, kBlock, 0));
-      }
-      m->ge_blocks = std::max(1, pe) * kNumSMs;
-      m->gn_blocks = std::max(1, pn) * kNumSMs;
-    }
-    // persistent cooperative solver: as many co-resident blocks as the work needs
+    std::vector<int64_t> iptr;
+    std::vector<uint32_t> incv;
+    RC(setup_incidence(d, node_hang, st, m, iptr, incv));
+    RC(build_gen_blocks(d, node_hang, iptr, incv, st, m));
+    // persistent cooperative solver for small 2D meshes (latency-bound: one
+    // kernel for the whole loop, no launches)
     int coop = 0;
     CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
-    // (latency-bound small meshes only: on large ones the separate element and
-    // node kernels run at higher occupancy).  2D only: on 3D meshes the
-    // launched lane passes measured faster at every size (7.6k elements: 22.6
-    // vs 39 us per iteration; 66k: 44 vs 60 us; a persistent variant built from
-    // the lane passes was also slower, 26.6 / 68.6 us: its grid barriers cost
-    // more than the two launches)
     if (coop && !(d->options & TO_UPLOAD_NO_PERSISTENT) && d->dim == 2 && d->n_elem <= 100000) {
       int per_sm = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_general_persistent<2>, kBlock, 0));
       const int64_t need = (std::max<int64_t>(d->n_elem, d->n_node) + kBlock - 1) / kBlock;
       m->coop_blocks = (int)std::min<int64_t>(need, (int64_t)per_sm * kNumSMs);
       RC(ensure_partials(m, (size_t)m->coop_blocks * 3));   // part_a [coop] + part_b [2 coop]
+      RC(setup_two_pass(d, st, m));
     }
   }
   // workspace: internal-order vectors with zero pads on both sides (the
   // structured kernels read whole aligned row windows)
   RC(m->alloc(&m->s, m->n_el));
   std::vector<double **> vecs = {&m->x, &m->r, &m->pb[0], &m->pb[1], &m->q, &m->dinv, &m->D};
-  if (m->structured) {
+  if (m->structured || m->gen_fused) {
     vecs.push_back(&m->rb[1]);
     vecs.push_back(&m->qb[1]);
   }
@@ -504,20 +704,21 @@ int launch_rhs(to_mesh *m, double *b, cudaStream_t st) {
   return check_launch();
 }
 
-// q = C^T K C p for p vanishing on non-free DOFs (values on non-free DOFs of q
-// are not meaningful; callers mask).  Plain apply: element pass + node pass.
+// q = C^T K C p for p vanishing on non-free DOFs (values on non-free DOFs of
+// q are not meaningful; callers mask): the single-kernel general operator in
+// its plain mode.
 int launch_matvec(to_mesh *m, const double *p, double *q, cudaStream_t st) {
-  const int ge = grid_for(m->n_el, kBlock, 16), gn = grid_for(m->n_node, kBlock, 16);
-  if (m->dim == 2) {
-    k_elem_pass<2, G_PLAIN><<<ge, kBlock, 0, st>>>(m->view(), m->s, nullptr, p, m->ye, m->K2, m->KS, m->hmask, nullptr, nullptr);
-    k_node_pass<2, G_PLAIN><<<gn, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, nullptr, nullptr, nullptr,
-                                                   nullptr, q, nullptr, nullptr, nullptr);
-  } else {
-    k_elem_pass<3, G_PLAIN><<<ge, kBlock, 0, st>>>(m->view(), m->s, nullptr, p, m->ye, m->K2, m->KS, m->hmask, nullptr, nullptr);
-    k_node_pass<3, G_PLAIN><<<gn, kBlock, 0, st>>>(m->n_node, m->inc_ptr, m->inc, m->ye, nullptr, nullptr, nullptr,
-                                                   nullptr, q, nullptr, nullptr, nullptr);
-  }
-  m->last_launches += 2;
+  if (m->dim == 2)
+    RC(launch_pdl(k_gen_fused<2, G_PLAIN>, dim3(m->GB.n_blk), dim3(kGfThreads), m->gb_smem, st, m->GB,
+                  (const double *)m->s_loc, (const double *)nullptr, (const double *)nullptr, p,
+                  (const double *)nullptr, (double *)nullptr, (double *)nullptr, q, (double *)nullptr, m->K2, m->KS,
+                  (CgScalars *)nullptr, (double *)nullptr, 0, 0.0, (double *)nullptr));
+  else
+    RC(launch_pdl(k_gen_fused<3, G_PLAIN>, dim3(m->GB.n_blk), dim3(kGfThreads), m->gb_smem, st, m->GB,
+                  (const double *)m->s_loc, (const double *)nullptr, (const double *)nullptr, p,
+                  (const double *)nullptr, (double *)nullptr, (double *)nullptr, q, (double *)nullptr, m->K2, m->KS,
+                  (CgScalars *)nullptr, (double *)nullptr, 0, 0.0, (double *)nullptr));
+  m->last_launches++;
   return check_launch();
 }
 
@@ -556,7 +757,10 @@ const uint8_t *free_int(const to_mesh *m) { return m->structured ? m->free_lex :
 int op_scale_and_diag(to_mesh *m, double penal, const double *x, double *d_int, cudaStream_t st) {
   if (!m->structured) {
     RC(launch_simp(m, penal, x, st));
-    return launch_diag(m, d_int, st);
+    RC(launch_diag(m, d_int, st));
+    k_gather_s<<<grid_for(m->gb_n_loc_el), kBlock, 0, st>>>(m->gb_n_loc_el, m->gb_el_id, m->s, m->s_loc);
+    m->last_launches++;
+    return check_launch();
   }
   k_simp_s3<<<grid_for(m->n_el), kBlock, 0, st>>>(m->n_el, x, m->perm_el, penal, m->E0, m->Emin, m->h_struct,
                                                    m->s, m->S);
@@ -592,29 +796,30 @@ int op_apply(to_mesh *m, const double *in, double *out, cudaStream_t st) {
   return check_launch();
 }
 
-// General path, iteration k: element pass (p_k formed on the fly, y_e,
-// p^T A p -> alpha_k) + node pass (q, r, x, p_k in place, rho, rr -> beta_k).
-int op_cg_general(to_mesh *m, cudaStream_t st) {
-  // one resident wave (3 blocks of 256 per SM): several elements / nodes per
-  // thread, so the end-of-kernel reduction barrier is amortised
-  const int ge4 = std::min(grid_for(m->n_el * 4, kBlock, 8), m->ge_blocks);
-  const int ge8 = std::min(grid_for(m->n_el * 8, kBlock, 8), m->ge_blocks);
-  const int gn4 = std::min(grid_for(m->n_node * 4, kBlock, 8), m->gn_blocks);
-  const double *no_po = nullptr;
-  double *no_q = nullptr;
-  if (m->dim == 2) {
-    RC(launch_pdl(k_elem_pass_lanes<2, G_CG>, dim3(ge4), dim3(kBlock), 0, st, m->view(), m->s, m->zp, no_po, m->ye,
-                  m->K2, m->KS, m->hmask, m->S, m->partials));
-    RC(launch_pdl(k_node_pass_lanes<2, G_CG>, dim3(gn4), dim3(kBlock), 0, st, m->n_node, m->inc_ptr, m->inc, m->ye,
-                  m->r, m->dinv, m->zp, m->x, no_q, m->partials, m->S, m->hist));
-  } else {
-    RC(launch_pdl(k_elem_pass_lanes<3, G_CG>, dim3(ge8), dim3(kBlock), 0, st, m->view(), m->s, m->zp, no_po,
-                    m->ye, m->K2, m->KS, m->hmask, m->S, m->partials));
-    RC(launch_pdl(k_node_pass_lanes<3, G_CG>, dim3(gn4), dim3(kBlock), 0, st, m->n_node, m->inc_ptr, m->inc,
-                    m->ye, m->r, m->dinv, m->zp, m->x, no_q, m->partials, m->S, m->hist));
-  }
-  m->last_launches += 2;
+// General path, the whole iteration k in one kernel (kernels_genfused.cuh).
+int op_cg_gen(to_mesh *m, int k, double rtol, cudaStream_t st) {
+  const int o = (k + 1) & 1, w = k & 1;
+  if (m->dim == 2)
+    RC(launch_pdl(k_gen_fused<2, G_CG>, dim3(m->GB.n_blk), dim3(kGfThreads), m->gb_smem, st, m->GB,
+                  (const double *)m->s_loc, (const double *)m->rb[o], (const double *)m->qb[o],
+                  (const double *)m->pb[o], (const double *)m->dinv, m->rb[w], m->pb[w], m->qb[w], m->x, m->K2,
+                  m->KS, m->S, m->partials, k, rtol, m->hist));
+  else
+    RC(launch_pdl(k_gen_fused<3, G_CG>, dim3(m->GB.n_blk), dim3(kGfThreads), m->gb_smem, st, m->GB,
+                  (const double *)m->s_loc, (const double *)m->rb[o], (const double *)m->qb[o],
+                  (const double *)m->pb[o], (const double *)m->dinv, m->rb[w], m->pb[w], m->qb[w], m->x, m->K2,
+                  m->KS, m->S, m->partials, k, rtol, m->hist));
+  m->last_launches++;
   return 0;
+}
+
+// General path, x_N and the final residual after N iterations.
+int op_final_gen(to_mesh *m, int n_iter, double rtol, cudaStream_t st) {
+  const int o = (n_iter + 1) & 1;
+  k_final_gen<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->rb[o], m->qb[o], m->pb[o], m->dinv, m->x,
+                                                    m->partials, m->S, n_iter, rtol, m->hist);
+  m->last_launches++;
+  return check_launch();
 }
 
 // Structured path, the whole iteration k in one kernel (kernels_struct3d.cuh).
@@ -695,8 +900,14 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   CK(cudaEventRecord(m->ev0, st));
   RC(reset_scalars(m, max_iter, fixed, hist, st));
   RC(op_scale_and_diag(m, penal, x_dev, nullptr, st));
-  // r0 = b: the structured kernel of iteration 0 reads r from rb[1]
-  double *r0 = m->structured ? m->rb[1] : m->r;
+  // single-kernel iterations (structured, and the general path unless the 2D
+  // persistent solver runs the loop): iteration 0 reads r0 = b from rb[1]
+  const bool persistent = !m->structured && m->coop_blocks > 0;
+  double *r0 = persistent ? m->r : m->rb[1];
+  if (!m->structured && !persistent) {   // q_{-1} = p_{-1} = 0 (finite whatever an earlier solve left)
+    CK(cudaMemsetAsync(m->qb[1], 0, sizeof(double) * n, st));
+    CK(cudaMemsetAsync(m->pb[1], 0, sizeof(double) * n, st));
+  }
   RC(op_rhs(m, r0, st));
   const int gv = grid_for(n);
   k_norm2_b<<<gv, kBlock, 0, st>>>(n, r0, m->partials, m->S);
@@ -709,10 +920,9 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   } else {
     CK(cudaMemsetAsync(m->x, 0, sizeof(double) * n, st));
   }
-  if (!m->structured) {
+  if (persistent) {
     RC(op_cg_k2<true>(m, rtol, st));
-    if (m->dim == 2) k_zp_init<2><<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->r, m->dinv, m->zp);
-    else k_zp_init<3><<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->r, m->dinv, m->zp);
+    k_zp_init<2><<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->r, m->dinv, m->zp);
     m->last_launches++;
   }
   RC(check_launch());
@@ -729,7 +939,7 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   int launched = 0;
   int chunk = fixed ? std::max(1, max_iter) : 16;
   bool stop = false;
-  if (!m->structured) {
+  if (persistent) {
     RC(read_scalars(m, st));
     stop = m->S_host->done != 0;
   }
@@ -739,7 +949,7 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
       if (!e) CK(cudaEventCreate(&e));
     CK(cudaEventRecord(m->loop_ev[0], st));
   }
-  if (!m->structured && m->coop_blocks > 0 && !stop) {
+  if (persistent && !stop) {
     // the whole loop in one cooperative kernel (no host polling)
     if (prof) CK(cudaEventRecord(m->prof_ev[0], st));
     double *pa = m->partials, *pb_ = m->partials + m->coop_blocks;
@@ -764,7 +974,7 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
         if (prof) CK(cudaEventRecord(E[1], st));
         if (prof) CK(cudaEventRecord(E[2], st));
       } else {
-        RC(op_cg_general(m, st));
+        RC(op_cg_gen(m, launched + k, rtol, st));
         if (prof) CK(cudaEventRecord(E[1], st));
         if (prof) CK(cudaEventRecord(E[2], st));
       }
@@ -778,7 +988,9 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
     }
   }
   if (loop_prof) CK(cudaEventRecord(m->loop_ev[1], st));
-  if (m->structured) RC(op_final_s3(m, max_iter, rtol, st));   // no-op if an iteration already converged
+  // x_N after exactly N iterations (a no-op if an iteration already converged)
+  if (m->structured) RC(op_final_s3(m, max_iter, rtol, st));
+  else if (!persistent) RC(op_final_gen(m, max_iter, rtol, st));
   RC(check_launch());
   RC(read_scalars(m, st));
   CgScalars res = *m->S_host;
@@ -793,7 +1005,6 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   if (prof) {
     for (int j = 0; j < 5; ++j) m->prof_ms[j] = 0.0;
     int nit = std::min(launched, res.iter);
-    const bool persistent = !m->structured && m->coop_blocks > 0;
     for (int it = 0; it < (persistent ? std::min(nit, 1) : nit); ++it) {
       const int slot[2] = {0, 2};   // K1 (p/x update + apply + alpha), K2 (r update + reductions)
       for (int j = 0; j < 2; ++j) {
@@ -882,7 +1093,7 @@ extern "C" int tomesh_get_info(const to_mesh *m, to_mesh_info *info) {
   info->filt_nnz = m->filt_nnz;
   info->device_bytes = m->dev_bytes;
   info->kernel_launches = m->last_launches;
-  info->matvec_variant = m->structured ? 1 : (m->coop_blocks > 0 ? 3 : 2);
+  info->matvec_variant = m->structured ? 1 : (m->coop_blocks > 0 ? 3 : 4);
   info->launches_total = m->launches_total;
   return 0;
 }

@@ -57,7 +57,13 @@ struct to_mesh {
   uint8_t *hmask = nullptr;            // general path: bit c = corner c of the element is hanging
   double *zp = nullptr;                // general path: node records {Dinv r, p}
   int coop_blocks = 0;                 // general path: grid of the persistent cooperative solver (0 = off)
-  int ge_blocks = 0, gn_blocks = 0;    // general path: one resident wave of the element / node pass
+  // general path, single-kernel iteration (kernels_genfused.cuh)
+  bool gen_fused = false;
+  GenBlocks GB{};
+  int32_t *gb_el_id = nullptr;         // block-local element -> element
+  int64_t gb_n_loc_el = 0;
+  double *s_loc = nullptr;             // s_e in block-local element order
+  size_t gb_smem = 0;                  // dynamic shared memory of k_gen_fused
   int32_t *filt_idx = nullptr;
   // OC update (allocated on first use)
   double *oc_a = nullptr, *oc_part = nullptr;

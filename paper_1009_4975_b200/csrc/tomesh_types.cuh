@@ -26,6 +26,33 @@ struct MeshView {
   double hL;
 };
 
+// General path, single-kernel iteration (kernels_genfused.cuh): the
+// owner-computes decomposition built at upload (tomesh.cu build_gen_blocks).
+// CTA b owns the canonical nodes [node0, node0 + n_own).  Its local node
+// slots are [0, n_own) owned, then n_halo halo nodes, then n_virt virtual
+// slots (hanging corner nodes).  Everything static about the block is one
+// contiguous 16-byte-aligned record (one bulk copy into shared memory), with
+// sections, each padded to 16 bytes, in this order:
+//   halo    int32  [n_halo]       global node ids, ascending
+//   virt    ushort4[n_virt]       the parents' local slots of a hanging corner
+//                                 node (.z = 0xffff: two parents), ascending
+//                                 hanging node id
+//   corner  uint16 [n_el][2^dim]  local slot of every corner of the block's
+//                                 elements (ascending element id)
+//   iptr    uint16 [n_own + 1]    owned node o's incidences are inc[iptr[o]
+//                                 .. iptr[o+1])
+//   inc     uint16 [n_inc]        (local element * 2^dim + corner) | weight
+//                                 code << 14 (0: 1, 1: 1/2, 2: 1/4), ascending
+// s_e of the block's elements: s_loc[el_off .. el_off + n_el) (el_off even).
+struct GfMeta {
+  int32_t node0, n_own, n_halo, n_virt, n_el, n_inc, el_off, rec_off16;
+};
+struct GenBlocks {
+  int n_blk, max_loc, max_own, max_rec16, max_el;   // shared-memory sizing: maxima over the blocks
+  const GfMeta *meta;
+  const uint4 *rec;
+};
+
 // Structured path (kernels_struct3d.cuh): the uniform H8 box and its CTA grid.
 struct GridView {
   int EX, EY, EZ;        // elements per axis
