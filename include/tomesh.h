@@ -146,11 +146,10 @@ typedef struct {
   int64_t grid[3];             /* element grid when structured                   */
   int64_t device_bytes;        /* device memory held by the handle               */
   int32_t kernel_launches;     /* kernels launched by the last tosolve_cg        */
-  int32_t matvec_variant;      /* operator path: 1 structured H8, 2 general
-                                  (launched passes), 3 general persistent;
-                                  + 10 * (1 + e + 2 n) when the 3D launched
-                                  passes use the 64-register variant of the
-                                  element (e) / node (n) pass (upload timing) */
+  int32_t matvec_variant;      /* CG iteration path: 1 structured H8 (one
+                                  kernel per iteration), 3 general, 2D
+                                  persistent cooperative solver, 4 general
+                                  one kernel per iteration                  */
   int64_t launches_total;      /* kernels launched by every call on this handle
                                   since upload (monotone counter)               */
 } to_mesh_info;

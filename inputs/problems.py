@@ -277,6 +277,14 @@ def _c5(nx=256, ny=128, nz=128, seed=5):
         rmin=2.0, rtol=1e-8, fixed_iters=500)
 
 
+def config_c4L():
+    """c4 recipe with one more refinement level (L = 5, finest-equivalent
+    768x384x384): 1,486,742 active elements, the "~1-2M active elements" that
+    BASELINE.json's config 4 names (the L = 4 recipe gives 225,090;
+    DESIGN.md §3, reading R26)."""
+    return _c4(L=5)
+
+
 _CONFIGS = {
     "c1": _c1, "c2": _c2, "c3": _c3, "c4": _c4, "c5": _c5,
 }

@@ -58,7 +58,8 @@ def build(force: bool = False, verbose: bool = False, extra=(), out: str = None)
         return LIB
     nvcc = _nvcc()
     objs = []
-    bdir = os.path.join(PKG, "build" if out is None and not extra else "build_variant")
+    bdir = os.path.join(PKG, "build") if out is None and not extra else \
+        os.path.join(PKG, "build_variant", os.path.splitext(os.path.basename(lib))[0])
     os.makedirs(bdir, exist_ok=True)
     for src in SOURCES:
         obj = os.path.join(bdir, os.path.splitext(src)[0] + ".o")

@@ -73,6 +73,29 @@ __device__ __forceinline__ void bulk_load_1d(void *dst, const void *src, unsigne
                : "memory");
 }
 
+// 8-byte asynchronous copy global -> shared (LDGSTS), and an mbarrier arrival
+// triggered when all of this thread's prior cp.async copies have completed
+// (.noinc: the arrival is part of the barrier's initial count).
+__device__ __forceinline__ void cp_async_8(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(unsigned long long *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+// Named barrier over the first `nthreads` threads (warp-aligned), id 1..15.
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -117,8 +140,10 @@ __device__ __forceinline__ bool grid_sum(double (&v)[NV], double *partials, uint
   if (tid == 0) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) partials[(size_t)blockIdx.x * NV + k] = v[k];
-    __threadfence();
-    uint32_t t = atomicAdd(counter, 1u);
+    // release: this block's partials (and everything its threads wrote before
+    // the barrier in block_sum) are visible before the arrival is counted
+    uint32_t t;
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(counter) : "memory");
     s_last = (t == gridDim.x - 1);
   }
   __syncthreads();

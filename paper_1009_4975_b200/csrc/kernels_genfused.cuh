@@ -49,21 +49,30 @@ constexpr int kGfOwnPerThread = 2;                       // owned nodes per thre
 constexpr int kGfMaxOwn = kGfThreads * kGfOwnPerThread;
 constexpr int kGfMaxLoc = 1536;                          // local node slots per block (uint16 slots)
 #ifndef TOMESH_GF_OWN3
-#define TOMESH_GF_OWN3 320
+#define TOMESH_GF_OWN3 224      // A/B on c4 / c4L: 224 < 320 < 448 < 512 (us per iteration)
 #endif
 #ifndef TOMESH_GF_OWN2
-#define TOMESH_GF_OWN2 448
+#define TOMESH_GF_OWN2 224
 #endif
 constexpr int kGfOwnTarget3 = TOMESH_GF_OWN3;           // owned nodes per block before splitting (3D)
 constexpr int kGfOwnTarget2 = TOMESH_GF_OWN2;           // (2D)
+#ifndef TOMESH_GF_CH
+#define TOMESH_GF_CH 256
+#endif
+#ifndef TOMESH_GF_MINB
+#define TOMESH_GF_MINB 2
+#endif
+#ifndef TOMESH_GF_ELMAX
+#define TOMESH_GF_ELMAX 2047    // capping blocks at one chunk (256) split them too finely: c4 62 -> 92 us
+#endif
+constexpr int kGfElMax = TOMESH_GF_ELMAX;               // elements per block (chunks of TOMESH_GF_CH)
 
 template <int DIM>
 struct GfChunk {
   static constexpr int NC = 1 << DIM;
-  static constexpr int CH = kGfThreads * (DIM == 3 ? 4 : 8) / NC;   // elements per chunk (1024 lane tasks)
+  static constexpr int CH = TOMESH_GF_CH;               // elements per chunk: one per thread (threads < CH)
+  static constexpr int YS = NC * DIM + 1;               // doubles per element result (odd: no bank conflicts)
 };
-
-__host__ __device__ constexpr int gf_pad16(int bytes) { return (bytes + 15) & ~15; }
 
 // Byte offsets of the sections of a block record (tomesh_types.cuh GfMeta).
 struct GfSections {
@@ -82,12 +91,12 @@ __host__ __device__ inline GfSections gf_sections(int n_own, int n_halo, int n_v
 }
 
 // Dynamic shared memory of k_gen_fused in bytes: the block record, s_e of
-// the block's elements, local node values P, the owners' z and Dinv, one
-// chunk of element results, the mbarrier.
+// the block's elements, local node values P, one chunk of element results,
+// the mbarrier.
 template <int DIM>
 __host__ __device__ constexpr size_t gf_smem_bytes(int max_rec16, int max_el, int max_loc, int max_own) {
   return (size_t)16 * max_rec16 + 8 * (size_t)((max_el + 1) & ~1) +
-         8 * ((size_t)max_loc * DIM + 2 * (size_t)max_own * DIM + (size_t)GfChunk<DIM>::CH * (1 << DIM) * DIM) + 16;
+         8 * ((size_t)max_loc * DIM + 2 * (size_t)max_own * DIM + (size_t)GfChunk<DIM>::CH * GfChunk<DIM>::YS) + 16;
 }
 
 // Lane c of an 2^DIM-lane group holds v = the element's corner c values;
@@ -160,29 +169,44 @@ __device__ __forceinline__ void gf_elem_lane(const double (&v_in)[DIM], int c, c
   }
 }
 
+#ifdef TOMESH_GF_TRACE
+// A/B instrumentation build only: per-block phase timestamps of the last launch.
+__device__ unsigned long long g_gf_trace[16384][8];
+#define GF_MARK(k)                                                                     \
+  do {                                                                                 \
+    if (threadIdx.x == 0 && blockIdx.x < 16384) g_gf_trace[blockIdx.x][k] = global_ns(); \
+  } while (0)
+#else
+#define GF_MARK(k) \
+  do {             \
+  } while (0)
+#endif
+
 __device__ __forceinline__ double gf_weight(unsigned code) { return code == 0 ? 1.0 : code == 1 ? 0.5 : 0.25; }
 
 template <int DIM, int MODE>
-__global__ void __launch_bounds__(kGfThreads, 2)
+__global__ void __launch_bounds__(kGfThreads, TOMESH_GF_MINB)
 k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_loc, const double *__restrict__ ro,
             const double *__restrict__ qo, const double *__restrict__ po, const double *__restrict__ Dinv,
             double *__restrict__ rw, double *__restrict__ pw, double *__restrict__ qw, double *__restrict__ x,
             const __grid_constant__ K0Dense2 K2, const __grid_constant__ K0HadSym H, CgScalars *S,
             double *partials, int kit, double rtol, double *hist) {
   constexpr bool CG = MODE == G_CG;
-  constexpr int NC = 1 << DIM, CH = GfChunk<DIM>::CH;
+  constexpr int NC = 1 << DIM, ND = NC * DIM, CH = GfChunk<DIM>::CH, YS = GfChunk<DIM>::YS;
+  constexpr int OPT = kGfOwnPerThread;
   extern __shared__ __align__(16) unsigned char gsm_raw[];
   const int tid = threadIdx.x;
+  GF_MARK(0);
   const GfMeta mt = B.meta[blockIdx.x];
   const int nOwn = mt.n_own, nHalo = mt.n_halo, nVirt = mt.n_virt, nE = mt.n_el;
   const GfSections sec = gf_sections<DIM>(nOwn, nHalo, nVirt, nE, mt.n_inc);
   unsigned char *rec = gsm_raw;                                     // the block record
   double *sl = reinterpret_cast<double *>(gsm_raw + 16 * (size_t)B.max_rec16);   // s_e of the elements
-  double *P = sl + ((B.max_el + 1) & ~1);                            // [max_loc][DIM]
-  double *Zs = P + (size_t)B.max_loc * DIM;                          // [max_own][DIM] z_k of owned DOFs
-  double *Ds = Zs + (size_t)B.max_own * DIM;                         // [max_own][DIM] Dinv of owned DOFs
-  double *Y = Ds + (size_t)B.max_own * DIM;                          // [CH][NC][DIM] element results
-  unsigned long long *bar = reinterpret_cast<unsigned long long *>(Y + (size_t)CH * NC * DIM);
+  double *P = sl + ((B.max_el + 1) & ~1);                            // [max_loc][DIM] local node values
+  double *Zs = P + (size_t)B.max_loc * DIM;                          // [max_own][DIM] z_k of the owned DOFs
+  double *Ds = Zs + (size_t)B.max_own * DIM;                         // [max_own][DIM] Dinv of the owned DOFs
+  double *Y = Ds + (size_t)B.max_own * DIM;                          // [CH][YS] element results of a chunk
+  unsigned long long *bar = reinterpret_cast<unsigned long long *>(Y + (size_t)CH * YS);
   const int32_t *halo = reinterpret_cast<const int32_t *>(rec + sec.halo);
   const ushort4 *virt = reinterpret_cast<const ushort4 *>(rec + sec.virt);
   const uint16_t *corner = reinterpret_cast<const uint16_t *>(rec + sec.corner);
@@ -205,33 +229,48 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
     mbar_wait(bar, 0);   // no bulk copy may still be writing when the CTA exits
     return;
   }
+  GF_MARK(1);
   const double alpha = CG ? __ldcg(&S->alpha) : 0.0;
   const double beta = CG ? __ldcg(&S->beta) : 0.0;
   const int64_t g0 = (int64_t)mt.node0 * DIM;
   double rho = 0.0, rr = 0.0;
-  // 1. owned nodes (contiguous DOFs)
-#pragma unroll 4
-  for (int j = tid; j < nOwn * DIM; j += kGfThreads) {
-    const int64_t g = g0 + j;
+  // 1. owned nodes o = tid + u * kGfThreads (the same nodes as in step 4)
+#pragma unroll
+  for (int u = 0; u < OPT; ++u) {
+    const int o = tid + u * kGfThreads;
+    if (o >= nOwn) continue;
+    const int64_t g = g0 + (int64_t)o * DIM;
     if (CG) {
-      const double r_o = __ldg(ro + g), q_o = __ldg(qo + g), p_o = __ldg(po + g), d = __ldg(Dinv + g);
-      const double rn = fma(-alpha, q_o, r_o);          // q is 0 on non-free DOFs, so r stays 0 there
-      const double z = d * rn;
-      const double pn = fma(beta, p_o, z);
-      rw[g] = rn;
-      pw[g] = pn;
-      if (alpha != 0.0) x[g] = fma(alpha, p_o, x[g]);
-      rho = fma(rn, z, rho);
-      rr = fma(rn, rn, rr);
-      P[j] = pn;
-      Zs[j] = z;
-      Ds[j] = d;
+      double r_o[DIM], q_o[DIM], p_o[DIM], d_o[DIM];
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        r_o[i] = __ldg(ro + g + i);
+        q_o[i] = __ldg(qo + g + i);
+        p_o[i] = __ldg(po + g + i);
+        d_o[i] = __ldg(Dinv + g + i);
+      }
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        const double rn = fma(-alpha, q_o[i], r_o[i]);   // q is 0 on non-free DOFs, so r stays 0 there
+        const double z = d_o[i] * rn;
+        const double pn = fma(beta, p_o[i], z);
+        rw[g + i] = rn;
+        pw[g + i] = pn;
+        if (alpha != 0.0) x[g + i] = fma(alpha, p_o[i], x[g + i]);
+        rho = fma(rn, z, rho);
+        rr = fma(rn, rn, rr);
+        P[o * DIM + i] = pn;
+        Zs[o * DIM + i] = z;
+        Ds[o * DIM + i] = d_o[i];
+      }
     } else {
-      P[j] = __ldg(po + g);
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) P[o * DIM + i] = __ldg(po + g + i);
     }
   }
+  GF_MARK(2);
   mbar_wait(bar, 0);
-  // ... and halo nodes
+  // ... and the halo nodes
 #pragma unroll 4
   for (int j = tid; j < nHalo * DIM; j += kGfThreads) {
     const int node = halo[j / DIM];
@@ -246,6 +285,7 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
     P[nOwn * DIM + j] = pn;
   }
   __syncthreads();
+  GF_MARK(3);
   // 2. hanging corners: Eq. 6 interpolation of the parents (ascending parent order)
   {
     const int vb = (nOwn + nHalo) * DIM;
@@ -263,11 +303,12 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
     }
   }
   __syncthreads();
-  // 3. elements by chunks; owned nodes sum their incidences of each chunk
-  int cur[kGfOwnPerThread], cend[kGfOwnPerThread];
-  double qa[kGfOwnPerThread][DIM];
+  // 3. elements by chunks of CH (one per thread); then owned nodes sum their
+  //    incidences of the chunk in ascending order
+  int cur[OPT], cend[OPT];
+  double qa[OPT][DIM];
 #pragma unroll
-  for (int u = 0; u < kGfOwnPerThread; ++u) {
+  for (int u = 0; u < OPT; ++u) {
     const int o = tid + u * kGfThreads;
     cur[u] = cend[u] = 0;
     if (o < nOwn) {
@@ -278,34 +319,47 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
     for (int i = 0; i < DIM; ++i) qa[u][i] = 0.0;
   }
   for (int c0 = 0; c0 < nE; c0 += CH) {
-    // lane tasks: CH * NC = a multiple of the block, so every warp stays converged
-#pragma unroll 2
-    for (int t = tid; t < CH * NC; t += kGfThreads) {
-      const int lc = t / NC, c = t % NC;
-      const int le = c0 + lc;
-      const bool live = le < nE;
-      const int lq = live ? le : nE - 1;
-      const int slot = corner[lq * NC + c];
-      const double se = sl[lq];
-      double v[DIM], y[DIM];
+    const int le = c0 + tid;
+    if (tid < CH && le < nE) {
+      double y[ND];
+      if constexpr (DIM == 3) {
+        const uint4 cs = *reinterpret_cast<const uint4 *>(corner + (size_t)le * NC);
+        const unsigned sw[4] = {cs.x, cs.y, cs.z, cs.w};
 #pragma unroll
-      for (int i = 0; i < DIM; ++i) v[i] = P[slot * DIM + i];
-      gf_elem_lane<DIM>(v, c, K2, H, y);
-      if (live) {
+        for (int c = 0; c < NC; ++c) {
+          const int slot = (int)((sw[c >> 1] >> (16 * (c & 1))) & 0xffffu);
 #pragma unroll
-        for (int i = 0; i < DIM; ++i) Y[(lc * NC + c) * DIM + i] = se * y[i];
+          for (int i = 0; i < DIM; ++i) y[DIM * c + i] = P[slot * DIM + i];
+        }
+        had_apply_inplace(H, y);
+      } else {
+        const uint2 cs = *reinterpret_cast<const uint2 *>(corner + (size_t)le * NC);
+        const unsigned sw[2] = {cs.x, cs.y};
+        double v[ND];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const int slot = (int)((sw[c >> 1] >> (16 * (c & 1))) & 0xffffu);
+#pragma unroll
+          for (int i = 0; i < DIM; ++i) v[DIM * c + i] = P[slot * DIM + i];
+        }
+        dense_apply<ND>(K2.K, v, y);
       }
+      const double se = sl[le];
+      double *dst = Y + (size_t)tid * YS;
+#pragma unroll
+      for (int a = 0; a < ND; ++a) dst[a] = se * y[a];
     }
     __syncthreads();
     const int lim = (c0 + CH) * NC;
 #pragma unroll
-    for (int u = 0; u < kGfOwnPerThread; ++u) {
+    for (int u = 0; u < OPT; ++u) {
       while (cur[u] < cend[u]) {
         const unsigned ent = inc[cur[u]];
         const int lec = (int)(ent & 0x3fffu);
         if (lec >= lim) break;
         const double w = gf_weight(ent >> 14);
-        const double *src = Y + (size_t)(lec - c0 * NC) * DIM;
+        const int lr = lec - c0 * NC;
+        const double *src = Y + (size_t)(lr / NC) * YS + (lr % NC) * DIM;
 #pragma unroll
         for (int i = 0; i < DIM; ++i) qa[u][i] = fma(w, src[i], qa[u][i]);
         ++cur[u];
@@ -313,31 +367,64 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
     }
     __syncthreads();
   }
+  GF_MARK(4);
   // 4. owners: q (masked), dots
   double pq = 0.0, qz = 0.0, qdq = 0.0;
 #pragma unroll
-  for (int u = 0; u < kGfOwnPerThread; ++u) {
+  for (int u = 0; u < OPT; ++u) {
     const int o = tid + u * kGfThreads;
     if (o >= nOwn) continue;
 #pragma unroll
     for (int i = 0; i < DIM; ++i) {
-      const int j = o * DIM + i;
+      const int64_t g = g0 + (int64_t)o * DIM + i;
       if (CG) {
-        const double d = Ds[j];
+        const double d = Ds[o * DIM + i];
         const double q = d != 0.0 ? qa[u][i] : 0.0;
-        qw[g0 + j] = q;
-        pq = fma(P[j], q, pq);
-        qz = fma(Zs[j], q, qz);
+        qw[g] = q;
+        pq = fma(P[o * DIM + i], q, pq);
+        qz = fma(Zs[o * DIM + i], q, qz);
         qdq = fma(d * q, q, qdq);
       } else {
-        qw[g0 + j] = qa[u][i];
+        qw[g] = qa[u][i];
       }
     }
   }
+  GF_MARK(5);
+#ifdef TOMESH_GF_GRIDSUM
   if (CG) {
     double dots[5] = {rho, rr, pq, qz, qdq};
     if (grid_sum<5>(dots, partials, &S->counter[CNT_PQ])) cg_single_step(S, kit, dots, rtol, hist);
   }
+#else
+  if (CG) {   // this block's dots; k_gen_step sums the blocks in a fixed order
+    double dots[5] = {rho, rr, pq, qz, qdq};
+    block_sum<5>(dots);
+    if (tid == 0)
+#pragma unroll
+      for (int k = 0; k < 5; ++k) partials[(size_t)5 * blockIdx.x + k] = dots[k];
+  }
+#endif
+  GF_MARK(6);
+}
+
+// The step of general-path iteration k: the blocks' dots summed in block
+// order (thread t adds blocks t, t + 512, ... then a fixed tree), then
+// cg_single_step (alpha_k, beta_k, stop test).  One CTA.
+static __global__ void __launch_bounds__(512) k_gen_step(int nb, const double *__restrict__ partials, CgScalars *S,
+                                                          int kit, double rtol, double *hist) {
+  pdl_wait();
+  if (cg_stopped(S)) {
+    pdl_release();
+    return;
+  }
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) acc[k] += __ldcg(&partials[(size_t)5 * b + k]);
+  block_sum<5>(acc);
+  if (threadIdx.x == 0) cg_single_step(S, kit, acc, rtol, hist);
+  __syncthreads();
+  pdl_release();
 }
 
 // After exactly N iterations (general path): r_N = r_{N-1} - alpha q_{N-1},

@@ -37,11 +37,6 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ unsigned long long global_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
-  return t;
-}
 
 // Bank of a sequence number: 0/1 = K1 (parity), 2/3 = tail collectives.
 __device__ __forceinline__ int shard_bank(unsigned long long seq) {

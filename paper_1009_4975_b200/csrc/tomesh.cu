@@ -329,7 +329,7 @@ int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_han
   const int nc = 1 << d->dim;
   const int64_t N = d->n_node;
   const int own_target = d->dim == 3 ? kGfOwnTarget3 : kGfOwnTarget2;
-  const int el_max = (1 << 14) / nc - 1, loc_max = kGfMaxLoc;
+  const int el_max = std::min(kGfElMax, (1 << 14) / nc - 1), loc_max = kGfMaxLoc;   // (incidence encoding: le * 2^dim < 2^14)
   std::vector<int32_t> el_mark(d->n_elem, -1), nd_mark(N, -1), el_le(d->n_elem, 0), nd_slot(N, 0);
   int stamp = 0;
   auto elem_of = [&](uint32_t t) { return (int64_t)((t & 0x3fffffffu) / (uint32_t)nc); };
@@ -362,7 +362,9 @@ int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_han
   std::vector<int32_t> node0;
   {
     std::vector<std::pair<int64_t, int64_t>> todo;
-    for (int64_t a = 0; a < N; a += own_target) todo.push_back({a, std::min<int64_t>(N, a + own_target)});
+    // block starts are even node ids (3D: 16-byte aligned bulk copies of the owned DOFs)
+    const int64_t tgt = (own_target + 1) & ~1;
+    for (int64_t a = 0; a < N; a += tgt) todo.push_back({a, std::min<int64_t>(N, a + tgt)});
     std::reverse(todo.begin(), todo.end());
     while (!todo.empty()) {
       auto [a, b] = todo.back();
@@ -371,8 +373,8 @@ int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_han
         node0.push_back((int32_t)a);
         continue;
       }
-      if (b - a <= 1) { set_error("general-path block of node %lld exceeds the kernel limits", (long long)a); return TO_EINVAL; }
-      const int64_t mid = a + (b - a) / 2;
+      if (b - a <= 2) { set_error("general-path block of node %lld exceeds the kernel limits", (long long)a); return TO_EINVAL; }
+      const int64_t mid = a + ((b - a) / 2 & ~(int64_t)1);
       todo.push_back({mid, b});
       todo.push_back({a, mid});
     }
@@ -809,6 +811,11 @@ int op_cg_gen(to_mesh *m, int k, double rtol, cudaStream_t st) {
                   (const double *)m->s_loc, (const double *)m->rb[o], (const double *)m->qb[o],
                   (const double *)m->pb[o], (const double *)m->dinv, m->rb[w], m->pb[w], m->qb[w], m->x, m->K2,
                   m->KS, m->S, m->partials, k, rtol, m->hist));
+#ifndef TOMESH_GF_GRIDSUM
+  RC(launch_pdl(k_gen_step, dim3(1), dim3(512), 0, st, m->GB.n_blk, (const double *)m->partials, m->S, k, rtol,
+                m->hist));
+  m->last_launches++;
+#endif
   m->last_launches++;
   return 0;
 }
@@ -1093,7 +1100,7 @@ extern "C" int tomesh_get_info(const to_mesh *m, to_mesh_info *info) {
   info->filt_nnz = m->filt_nnz;
   info->device_bytes = m->dev_bytes;
   info->kernel_launches = m->last_launches;
-  info->matvec_variant = m->structured ? 1 : (m->coop_blocks > 0 ? 3 : 4);
+  info->matvec_variant = m->structured ? 1 : m->coop_blocks > 0 ? 3 : 4;
   info->launches_total = m->launches_total;
   return 0;
 }
@@ -1265,3 +1272,12 @@ extern "C" int to_element_hadamard(double nu, double *diag_host, double *off_hos
   std::memcpy(off_host, h.off, sizeof(h.off));
   return bad;
 }
+
+#ifdef TOMESH_GF_TRACE
+// A/B instrumentation build only: the per-block phase timestamps of the last
+// k_gen_fused launch (16384 x 8 u64).
+extern "C" int to_debug_gf_trace(unsigned long long *out) {
+  return cudaMemcpyFromSymbol(out, g_gf_trace, sizeof(g_gf_trace)) == cudaSuccess ? 0 : TO_ECUDA;
+}
+
+#endif

@@ -53,6 +53,8 @@ struct GenBlocks {
   const uint4 *rec;
 };
 
+__host__ __device__ constexpr int gf_pad16(int bytes) { return (bytes + 15) & ~15; }
+
 // Structured path (kernels_struct3d.cuh): the uniform H8 box and its CTA grid.
 struct GridView {
   int EX, EY, EZ;        // elements per axis
