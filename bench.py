@@ -7,14 +7,26 @@ recovery, sensitivities + compliance, Eq. 5 filter (rmin = 2).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): every rank solves its own replica of the workload, no
-collective on the data path ("scaling": "weak"); value = total iterations/s.
---shard: ONE c5 solve split into z-slabs over the N ranks ("scaling":
-"strong", paper_1009_4975_b200/shard.py).
+N > 1 (torchrun): weak scaling of ONE sharded solve: the c5
+box stacked N times along z (256 x 128 x 128N elements), rank r owning one
+c5-sized z-slab; every PCG iteration is one kernel per rank with the ghost
+planes stored into the neighbours' buffers (NVLink peer stores, CUDA IPC) and
+the dots all-reduced on the device ("scaling": "weak", "comm":
+"device_peer_stores").  value = c5-box iterations/s (N boxes per global
+iteration).  --replicas: N independent c5 solves instead (no data-path
+collective).  --shard: ONE c5 solve split into z-slabs over the N ranks
+("scaling": "strong"; paper_1009_4975_b200/shard.py).
 --impl reference times the oracle (plain numpy/scipy CPU program) on a
 bounded sample of the same workload, rank 0 only.
 """
 from __future__ import annotations
+
+import os as _os
+
+# the oracle legs (cpu_baseline, --impl reference) run on ONE host thread:
+# pinned before numpy / scipy load their BLAS
+for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+    _os.environ.setdefault(_v, "1")
 
 import argparse
 import json
@@ -99,13 +111,82 @@ def kernel_bytes(dim, n_el, n_node, n_dof, structured):
     Structured path, one kernel per iteration (k1): s (8/elem) + Dinv
     (8/node) + read r_{k-1}, q_{k-1}, p_{k-1}, x and write r_k, p_k, q_k, x
     (8 x 8/DOF); k2 = 0.
-    General path: k1 = the elementwise pre-pass (read r, Dinv, p, x; write p,
-    x, q: 7 x 8/DOF) + the operator (s + connectivity per element, gather of
-    p, scatter of q: 2 x 8/DOF); k2 = read r, q, Dinv, write r (4 x 8/DOF)."""
+    General path (k_gen_fused, one kernel per iteration + a one-CTA step):
+    read r, q, p, Dinv, x and write r, p, q, x (9 x 8/DOF) + s and
+    connectivity per element (8 + 4 * 2^dim); k2 = 0."""
     nc = 1 << dim
     if structured:
         return {"k1": 8 * n_el + 8 * n_node + 64 * n_dof, "k2": 0}
-    return {"k1": 56 * n_dof + n_el * (8 + 4 * nc) + 16 * n_dof, "k2": 32 * n_dof}
+    return {"k1": 72 * n_dof + n_el * (8 + 4 * nc), "k2": 0}
+
+
+def general_bytes(hm):
+    """SURVEY §8(d) algorithmic bytes of one general-path PCG iteration with
+    the minimal V = 7 vector passes: 8 n_dof V + n_el (8 + 4 * 2^d) + the fixed
+    bitmask n_dof / 8 + n_hang * 4 + (hanging parent entries) * 12."""
+    nc = 1 << hm.dim
+    return (8 * hm.n_dof * 7 + hm.n_el * (8 + 4 * nc) + hm.n_dof // 8 + 4 * hm.hang_node.shape[0]
+            + 12 * hm.hang_parent.shape[0])
+
+
+def general_path_record(dev, hbm, peak_kind, its=200):
+    """The general (AMR) path on c4L, BASELINE.json's config 4 at its "~1-2M
+    active elements" (the c4 recipe at L = 5, reading R26), measured
+    in the same run: iteration time (the block kernel k_gen_fused + the step
+    kernel, launched back to back, one event pair around 200 iterations,
+    median of three), the block kernel alone (events around every launch),
+    §8(d) bytes and roofline fraction, and the solve to the config's rtol."""
+    import torch
+    import paper_1009_4975_b200 as pb
+    from inputs import density_at
+    from inputs.problems import config_c4L
+    prob = config_c4L()
+    t0 = time.perf_counter()
+    hm = pb.prepare(prob)
+    t_prep = time.perf_counter() - t0
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        m = pb.Mesh(hm, E0=prob.E0, Emin=prob.Emin, nu=prob.nu, rmin=prob.rmin, device=dev.index, stream=stream)
+        x = torch.as_tensor(density_at(prob, hm.elem_level, hm.elem_anchor), device=dev)
+        u = torch.zeros(hm.n_dof, dtype=torch.float64, device=dev)
+    flags = pb.TO_FIXED_ITERS | pb.TO_NO_TRUE_RES
+    m.tosolve_cg(prob.penal, x, u, rtol=0.0, max_iter=its, flags=flags, stream=stream)
+    loops = []
+    for _ in range(3):
+        m.tosolve_cg(prob.penal, x, u, rtol=0.0, max_iter=its, flags=flags | pb.TO_PROFILE_LOOP, stream=stream)
+        loops.append(m.profile())
+    loop = sorted(loops, key=lambda p: p["loop_ms"])[1]
+    it_ms = loop["loop_ms"] / max(1, loop["iters"])
+    m.tosolve_cg(prob.penal, x, u, rtol=0.0, max_iter=its, flags=flags | pb.TO_PROFILE, stream=stream)
+    pr = m.profile()
+    k_ms = pr["apply_ms"] / max(1, pr["iters"])
+    step_ms = pr["u1_ms"] / max(1, pr["iters"])
+    u.zero_()
+    st = m.tosolve_cg(prob.penal, x, u, rtol=prob.rtol, max_iter=200000, stream=stream)
+    B = general_bytes(hm)
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(prob.name, {}).get("k1_dram_bytes")
+        except Exception:
+            traffic = None
+    info = m.info()
+    m.close()
+    return {
+        "workload": prob.name, "n_elem": hm.n_el, "n_dof": hm.n_dof, "n_hang": int(hm.hang_node.shape[0]),
+        "matvec_variant": info["matvec_variant"], "iters_per_sec": 1000.0 / it_ms, "us_per_iter": 1000.0 * it_ms,
+        "roofline": {"bound": "hbm", "achieved": B / (k_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
+                     "frac": B / (k_ms / 1000.0) / 1e9 / hbm, "traffic": traffic,
+                     "kernel": "k_gen_fused<3, CG>: the whole general-path PCG iteration but the step",
+                     "algorithmic_bytes_per_launch": B, "avg_launch_ms": k_ms,
+                     "avg_launch_ms_method": "events around every launch of an untimed 200-iteration solve",
+                     "peak_source": peak_kind},
+        "iteration_frac": B / (it_ms / 1000.0) / 1e9 / hbm, "step_kernel_ms": step_ms,
+        "solve_to_rtol": {"rtol": prob.rtol, "iters": st.iters, "ms": st.ms, "relres_true": st.relres_true,
+                          "status": st.status},
+        "host_prepare_s": t_prep,
+    }
 
 
 def max_over_ranks(value, ws, device=None):
@@ -124,6 +205,32 @@ def _dist():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def _host_facts():
+    """The host the oracle legs ran on (CPU model, cores, affinity, RAM)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    ram_gb = None
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                ram_gb = round(int(line.split()[1]) / 1024 ** 2, 1)
+                break
+    except OSError:
+        pass
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except AttributeError:
+        aff = None
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "affinity": aff, "ram_gb": ram_gb,
+            "threads": {v: os.environ.get(v) for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}}
 
 
 def _cpu_baseline(budget_s=15.0, sample_dims=(48, 24, 24)):
@@ -156,6 +263,7 @@ def _cpu_baseline(budget_s=15.0, sample_dims=(48, 24, 24)):
         "sample": (f"oracle Jacobi-PCG ({its} iterations, {dt:.1f} s) on a c5-recipe "
                    f"{sample_dims[0]}x{sample_dims[1]}x{sample_dims[2]} sub-box ({om.n_dof} DOFs); "
                    f"{it_s_sample:.2f} it/s there, scaled by DOF count to c5"),
+        "host": _host_facts(),
     }
 
 
@@ -174,7 +282,10 @@ def run_reference(args):
     val = cb["value"]
     line = {
         "impl": "reference", "metric": "pcg_iterations_per_sec", "value": val, "unit": "iterations/s",
-        "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": 1000.0 * float(np.mean(times)),
+        "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+        # a c5 step (500 iterations) at the measured rate; the wall time of one
+        # bounded sample is reported beside it
+        "ms_per_step": 1000.0 * 500 / val, "ms_per_sample": 1000.0 * float(np.mean(times)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "c5_uniform3d_256x128x128", "iters_per_solve": 500},
         "cpu_baseline": cb,
@@ -334,6 +445,9 @@ def run_ours(args):
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = _cpu_baseline(budget_s=args.ref_budget)
+    gen = None
+    if rank == 0 and ws == 1 and not args.no_general:
+        gen = general_path_record(dev, hbm, peak_kind)
 
     if rank == 0:
         line = {
@@ -351,7 +465,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "kernel": ("k_apply_s3<CG>: the whole PCG iteration (r, p, x updates, q = A p, 5 dots)"
-                                    if info["structured"] else "k_elem_pass_lanes + k_node_pass_lanes"),
+                                    if info["structured"] else "k_gen_fused<CG> (+ the one-CTA step kernel)"),
                          "algorithmic_bytes_per_launch": kb["k1"], "avg_launch_ms": k1_ms,
                          "avg_launch_ms_method": ("one event pair around the 500 back-to-back K1 launches of an "
                                                   "untimed step, median of three" if info["structured"] else
@@ -368,6 +482,7 @@ def run_ours(args):
             },
             "solve_to_rtol": full_line,
             "oc_update": oc_line,
+            "general_path": gen,
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": launches,
@@ -379,6 +494,147 @@ def run_ours(args):
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+    return 0
+
+
+def weak_slab(nranks, rank, nx=256, ny=128, nz=128, seed=5):
+    """Rank `rank`'s z-slab of the weak-scaling workload: the c5 recipe on a
+    box of nx x ny x (nz * nranks) elements (x = 0 clamped, unit traction on
+    x = nx, x ~ U(0.001, 1) i.i.d. in lexicographic element order, seed 5),
+    built locally -- the global mesh is never formed.  The local box holds the
+    owned node planes plus two ghost planes per interior side (shard.slice_host's
+    layout); its face loads are the GLOBAL consistent nodal loads (1 inside,
+    1/2 on an edge, 1/4 at a corner of the loaded face), so a slab cut is never
+    a boundary.  Returns (Slab, local densities, local problem); elem_global
+    and node_global hold GLOBAL lexicographic ids."""
+    import paper_1009_4975_b200 as pb
+    from paper_1009_4975_b200 import shard
+    from inputs import config
+    nzg = nz * nranks
+    a, b = shard.slab_plan(nzg + 1, nranks)[rank]
+    gz_lo, gz_hi = max(a - shard.GHOST, 0), min(b + shard.GHOST, nzg + 1)
+    prob = config("c5", nx=nx, ny=ny, nz=gz_hi - 1 - gz_lo)
+    host = pb.prepare(prob)
+    nc = host.node_coord.astype(np.int64)
+    gzn = nc[:, 2] + gz_lo
+    face = nc[:, 0] == nx
+    wy = np.where((nc[:, 1] == 0) | (nc[:, 1] == ny), 0.5, 1.0)
+    wz = np.where((gzn == 0) | (gzn == nzg), 0.5, 1.0)
+    load = np.zeros(host.n_dof)
+    load[3 * np.nonzero(face)[0] + 1] = -(wy * wz)[face]
+    host.load = load
+    ea = host.elem_anchor.astype(np.int64)
+    elem_global = ea[:, 0] + nx * (ea[:, 1] + ny * (ea[:, 2] + gz_lo))
+    node_global = nc[:, 0] + (nx + 1) * (nc[:, 1] + (ny + 1) * gzn)
+    field = np.random.default_rng(seed).uniform(0.001, 1.0, nx * ny * nzg)
+    layer = ea[:, 2] + gz_lo
+    sl = shard.Slab(rank=rank, a=a, b=b, gz_lo=gz_lo, own_lo=a - gz_lo, own_hi=b - gz_lo, host=host,
+                    elem_global=elem_global, node_global=node_global,
+                    elem_owned=(layer >= a) & (layer < min(b, nzg)), node_owned=(gzn >= a) & (gzn < b))
+    return sl, np.ascontiguousarray(field[elem_global]), prob
+
+
+def run_weak(args):
+    """N > 1 default: weak scaling of one sharded solve (module docstring)."""
+    import torch
+    import paper_1009_4975_b200 as pb
+    from paper_1009_4975_b200 import shard
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    import torch.distributed as dist
+    dist.init_process_group("gloo")              # plumbing only: IPC handles, barriers, the max over ranks
+    dev = torch.device("cuda", local)
+    t_prep = time.perf_counter()
+    sl, x_np, prob = weak_slab(ws, rank)
+    t_prep = time.perf_counter() - t_prep
+    iters = 500
+    sr = shard.ShardRank(slab=sl, E0=prob.E0, Emin=prob.Emin, nu=prob.nu, rmin=prob.rmin, device=local)
+    m = sr.mesh
+    stream = torch.cuda.Stream(device=dev)
+    x_host = torch.from_numpy(x_np).pin_memory()
+    x = x_host.to(dev)
+    u = torch.zeros(m.n_dof, dtype=torch.float64, device=dev)
+    dc = torch.empty(m.n_el, dtype=torch.float64, device=dev)
+    dcf = torch.empty_like(dc)
+    flags = pb.TO_FIXED_ITERS
+
+    def step(extra=0):
+        st = sr.solve(prob.penal, x, u, rtol=0.0, max_iter=iters, flags=flags | extra, stream=stream)
+        m.to_sensitivity(prob.penal, x, u, dc, stream=stream)
+        m.to_filter(pb.TO_FILTER_SENS, x, dc, dcf, stream=stream)
+        return st
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    l0 = m.info()["launches_total"]
+    e0.record(stream)
+    for _ in range(args.steps):
+        st = step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    launches = m.info()["launches_total"] - l0
+    dist.barrier()
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1), ws)
+    dcf_host = torch.empty(m.n_el, dtype=torch.float64).pin_memory()
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            x.copy_(x_host, non_blocking=True)
+        step()
+        with torch.cuda.stream(stream):
+            dcf_host.copy_(dcf, non_blocking=True)
+    e3.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = max_over_ranks(e2.elapsed_time(e3), ws)
+    step(pb.TO_PROFILE_LOOP)
+    torch.cuda.synchronize(dev)
+    p = m.profile()
+    it_ms = max_over_ranks(p["loop_ms"] / max(1, p["iters"]), ws)
+    own_nodes = int(sl.node_owned.sum())
+    own_el = int(sl.elem_owned.sum())
+    kb = 8 * own_el + 8 * own_nodes + 64 * 3 * own_nodes
+    hbm, peak_kind = _peaks()
+    n_dof_g = 3 * 257 * 129 * (128 * ws + 1)
+    if rank == 0:
+        line = {
+            "metric": "pcg_iterations_per_sec", "value": ws * iters * args.steps / (ms / 1000.0),
+            "unit": "iterations/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"c5x{ws}_weak_256x128x{128 * ws}", "n_elem": 256 * 128 * 128 * ws,
+                       "n_dof": n_dof_g, "iters_per_solve": iters,
+                       "step": "simp+diag+rhs+500 PCG its+recover+sens+filter, one z-slab sharded solve",
+                       "value_counts": "c5-box iterations: N boxes per global PCG iteration",
+                       "parallelism": f"zslab{ws}", "slab_planes": [sl.a, sl.b],
+                       "l2": "inputs larger than L2 (slab working set ~1.3 GB per GPU)"},
+            "comm": "device_peer_stores", "gpus_active": ws,
+            "global_iterations_per_sec": iters * args.steps / (ms / 1000.0),
+            "dof_matvecs_per_sec": iters * args.steps / (ms / 1000.0) * n_dof_g,
+            "e2e": {"value": ws * iters * args.steps / (e2e_ms / 1000.0), "unit": "iterations/s",
+                    "h2d_bytes_per_step": m.n_el * 8, "d2h_bytes_per_step": m.n_el * 8},
+            "roofline": {"bound": "hbm", "achieved": kb / (it_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": kb / (it_ms / 1000.0) / 1e9 / hbm, "traffic": None,
+                         "kernel": "k_apply_s3<CG, SHARD> + k_shard_step per iteration (rank 0's slab)",
+                         "algorithmic_bytes_per_launch": kb, "avg_launch_ms": it_ms, "peak_source": peak_kind},
+            "cpu_baseline": None, "clocks": clk, "gpu_launches": launches, "host_prepare_s": t_prep,
+        }
+        print(json.dumps(line), flush=True)
+    sr.close()
+    dist.destroy_process_group()
     return 0
 
 
@@ -506,13 +762,19 @@ def main():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-general", action="store_true", help="skip the c4L general-path sub-record")
     ap.add_argument("--shard", action="store_true",
-                    help="split ONE c5 solve into z-slabs over the ranks (strong scaling) instead of replicas")
+                    help="split ONE c5 solve into z-slabs over the ranks (strong scaling)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: N independent c5 solves (no data-path collective) instead of the weak-scaled "
+                         "sharded solve")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
     if args.shard:
         return run_shard(args)
+    if _dist()[0] > 1 and not args.replicas:
+        return run_weak(args)
     return run_ours(args)
 
 

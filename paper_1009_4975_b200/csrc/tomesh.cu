@@ -798,7 +798,8 @@ int op_apply(to_mesh *m, const double *in, double *out, cudaStream_t st) {
   return check_launch();
 }
 
-// General path, the whole iteration k in one kernel (kernels_genfused.cuh).
+// General path, iteration k (kernels_genfused.cuh): the block kernel, then
+// the one-CTA step kernel (alpha_k, beta_k, stop test).
 int op_cg_gen(to_mesh *m, int k, double rtol, cudaStream_t st) {
   const int o = (k + 1) & 1, w = k & 1;
   if (m->dim == 2)
@@ -811,12 +812,15 @@ int op_cg_gen(to_mesh *m, int k, double rtol, cudaStream_t st) {
                   (const double *)m->s_loc, (const double *)m->rb[o], (const double *)m->qb[o],
                   (const double *)m->pb[o], (const double *)m->dinv, m->rb[w], m->pb[w], m->qb[w], m->x, m->K2,
                   m->KS, m->S, m->partials, k, rtol, m->hist));
+  m->last_launches++;
+  return 0;
+}
+int op_cg_gen_step(to_mesh *m, int k, double rtol, cudaStream_t st) {
 #ifndef TOMESH_GF_GRIDSUM
   RC(launch_pdl(k_gen_step, dim3(1), dim3(512), 0, st, m->GB.n_blk, (const double *)m->partials, m->S, k, rtol,
                 m->hist));
   m->last_launches++;
 #endif
-  m->last_launches++;
   return 0;
 }
 
@@ -983,6 +987,7 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
       } else {
         RC(op_cg_gen(m, launched + k, rtol, st));
         if (prof) CK(cudaEventRecord(E[1], st));
+        RC(op_cg_gen_step(m, launched + k, rtol, st));
         if (prof) CK(cudaEventRecord(E[2], st));
       }
     }

@@ -169,12 +169,22 @@ class ShardRank:
     neighbours and every rank's all-reduce slots are mapped with CUDA IPC;
     the handles travel through ``dist.all_gather_object`` (plumbing)."""
 
-    def __init__(self, host: HostMesh, E0=1.0, Emin=1e-9, nu=0.3, rmin=None, device=0, group=None):
+    def __init__(self, host: HostMesh = None, E0=1.0, Emin=1e-9, nu=0.3, rmin=None, device=0, group=None,
+                 slab: Slab = None):
+        """host: the global mesh (this rank's slab is sliced from it), or
+        slab: this rank's slab built by the caller (e.g. a weak-scaling box
+        whose global mesh is never formed)."""
         import torch.distributed as dist
-        check_filter_reach(host)
         single = not (dist.is_available() and dist.is_initialized())
         rank, nranks = (0, 1) if single else (dist.get_rank(group), dist.get_world_size(group))
-        self.slab = slice_host(host, nranks, rank)
+        if slab is None:
+            check_filter_reach(host)
+            slab = slice_host(host, nranks, rank)
+        else:
+            check_filter_reach(slab.host)
+            if slab.rank != rank:
+                raise ValueError(f"slab of rank {slab.rank} given to rank {rank}")
+        self.slab = slab
         self.mesh = Mesh(self.slab.host, E0=E0, Emin=Emin, nu=nu, rmin=rmin, device=device)
         self.device = device
         mine = self.mesh.shard_buffers()

@@ -25,18 +25,20 @@ torch = pytest.importorskip("torch")
 from inputs import config
 from oracle import fe, mesh as omesh, oc, pipeline, sample, topopt
 from tests.gpu_helpers import cuda, host, product_mesh, rel
-from tests.oracle_cache import cache_path, input_key
+from tests.oracle_cache import cache_path, input_key, variant
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
-@pytest.fixture(scope="module", params=["c3", "c4", "c5"])
+@pytest.fixture(scope="module", params=["c3", "c4", "c4L", "c5"])
 def setup(request):
     """One config at a time (module scope groups the tests by config, so each
-    full-size mesh is built once)."""
+    full-size mesh is built once).  c4L: the c4 recipe at L = 5 (1.49M
+    elements, reading R26)."""
     name = request.param
-    prob = config(name)
-    om = omesh.build_mesh(prob, with_filter=(name != "c5"))
+    prob = variant(name)
+    big = name in ("c4L", "c5")
+    om = omesh.build_mesh(prob, with_filter=not big)
     hm, m = product_mesh(prob)
     x = pipeline.input_density(prob, om) if name != "c5" else om.density
     yield name, (prob, om, hm, m, x)
@@ -48,7 +50,7 @@ def test_fullsize_host_arrays_bit_exact(setup):
     for f in ("elem_level", "elem_anchor", "elem_node", "hang_node", "hang_ptr", "hang_parent", "hang_weight",
               "fixed_dof", "load"):
         assert np.array_equal(getattr(hm, f), getattr(om, f)), f
-    if name != "c5":
+    if name not in ("c4L", "c5"):
         assert np.array_equal(hm.filt_ptr, om.filt_ptr) and np.array_equal(hm.filt_idx, om.filt_idx)
     info = m.info()
     assert info["structured"] == (1 if name in ("c3", "c5") else 0)

@@ -210,3 +210,32 @@ def test_shard_rank_plumbing_gloo_world3():
         assert p.exitcode == 0
     res = dict(q.get(timeout=10) for _ in range(3))
     assert res == {0: True, 1: True, 2: True}
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 3])
+def test_weak_slab_matches_slice_of_global_mesh(nranks):
+    """bench.py's weak-scaling slabs, built without the global mesh, equal the
+    slabs shard.slice_host cuts from the global c5-recipe box: loads and
+    Dirichlet DOFs bit-exact by global node, element and node ownership, and
+    densities from the one global lexicographic field."""
+    import bench
+    from inputs import config
+    from paper_1009_4975_b200 import shard
+    nx, ny, nz = 8, 4, 4
+    glob = pb.prepare(config("c5", nx=nx, ny=ny, nz=nz * nranks))
+    gc = glob.node_coord.astype(np.int64)
+    gid = gc[:, 0] + (nx + 1) * (gc[:, 1] + (ny + 1) * gc[:, 2])
+    gload = dict(zip(gid.tolist(), map(tuple, glob.load.reshape(-1, 3).tolist())))
+    gfix = {(int(gid[f // 3]), int(f % 3)) for f in glob.fixed_dof}
+    field = np.random.default_rng(5).uniform(0.001, 1.0, nx * ny * nz * nranks)
+    for r in range(nranks):
+        sl, x, _ = bench.weak_slab(nranks, r, nx=nx, ny=ny, nz=nz)
+        ref = shard.slice_host(glob, nranks, r)
+        assert (sl.a, sl.b, sl.gz_lo, sl.own_lo, sl.own_hi) == (ref.a, ref.b, ref.gz_lo, ref.own_lo, ref.own_hi)
+        assert sl.host.n_el == ref.host.n_el and sl.host.n_node == ref.host.n_node
+        loads = sl.host.load.reshape(-1, 3)
+        assert all(tuple(loads[i]) == gload[int(g)] for i, g in enumerate(sl.node_global))
+        fix = {(int(sl.node_global[f // 3]), int(f % 3)) for f in sl.host.fixed_dof}
+        assert fix == {fg for fg in gfix if fg[0] in set(sl.node_global.tolist())}
+        assert sl.elem_owned.sum() == ref.elem_owned.sum() and sl.node_owned.sum() == ref.node_owned.sum()
+        assert np.array_equal(x, field[sl.elem_global])

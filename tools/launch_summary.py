@@ -9,6 +9,7 @@ import sys
 
 def main(path):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    rows = rows[next(i for i, r in enumerate(rows) if "Kernel Name" in r):]   # skip the program's own output
     hdr = rows[0]
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
     mi = hdr.index("Metric Name")
