@@ -182,6 +182,21 @@ __device__ unsigned long long g_gf_trace[16384][8];
   } while (0)
 #endif
 
+#ifdef TOMESH_DEBUG_CHECKS
+// checking build (sanitizer substitute): trap on an index outside its array
+#define GF_CHECK(cond)                                                                            \
+  do {                                                                                            \
+    if (!(cond)) {                                                                                \
+      printf("k_gen_fused check failed: %s (block %d thread %d)\n", #cond, blockIdx.x, threadIdx.x); \
+      __trap();                                                                                   \
+    }                                                                                             \
+  } while (0)
+#else
+#define GF_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
 __device__ __forceinline__ double gf_weight(unsigned code) { return code == 0 ? 1.0 : code == 1 ? 0.5 : 0.25; }
 
 template <int DIM, int MODE>
@@ -200,6 +215,8 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
   const GfMeta mt = B.meta[blockIdx.x];
   const int nOwn = mt.n_own, nHalo = mt.n_halo, nVirt = mt.n_virt, nE = mt.n_el;
   const GfSections sec = gf_sections<DIM>(nOwn, nHalo, nVirt, nE, mt.n_inc);
+  GF_CHECK(sec.total <= 16 * B.max_rec16 && nE <= B.max_el && nOwn <= B.max_own && nOwn <= kGfMaxOwn);
+  GF_CHECK(nOwn + nHalo + nVirt <= B.max_loc && (mt.el_off & 1) == 0);
   unsigned char *rec = gsm_raw;                                     // the block record
   double *sl = reinterpret_cast<double *>(gsm_raw + 16 * (size_t)B.max_rec16);   // s_e of the elements
   double *P = sl + ((B.max_el + 1) & ~1);                            // [max_loc][DIM] local node values
@@ -274,6 +291,7 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
 #pragma unroll 4
   for (int j = tid; j < nHalo * DIM; j += kGfThreads) {
     const int node = halo[j / DIM];
+    GF_CHECK(node >= 0 && (node < mt.node0 || node >= mt.node0 + nOwn));
     const int64_t g = (int64_t)node * DIM + (j % DIM);
     double pn;
     if (CG) {
@@ -294,6 +312,7 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
       const int np = pv.z == 0xffff ? 2 : 4;
       const double w = np == 2 ? 0.5 : 0.25;
       const int par[4] = {pv.x, pv.y, pv.z, pv.w};
+      for (int k = 0; k < np; ++k) GF_CHECK(par[k] < nOwn + nHalo);
 #pragma unroll
       for (int i = 0; i < DIM; ++i) {
         double acc = 0.0;
@@ -328,6 +347,7 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           const int slot = (int)((sw[c >> 1] >> (16 * (c & 1))) & 0xffffu);
+          GF_CHECK(slot < nOwn + nHalo + nVirt);
 #pragma unroll
           for (int i = 0; i < DIM; ++i) y[DIM * c + i] = P[slot * DIM + i];
         }
@@ -357,6 +377,7 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
         const unsigned ent = inc[cur[u]];
         const int lec = (int)(ent & 0x3fffu);
         if (lec >= lim) break;
+        GF_CHECK(lec >= c0 * NC && lec < nE * NC && (ent >> 14) <= 2);
         const double w = gf_weight(ent >> 14);
         const int lr = lec - c0 * NC;
         const double *src = Y + (size_t)(lr / NC) * YS + (lr % NC) * DIM;

@@ -162,6 +162,12 @@ struct to_mesh {
       set_error("cudaMalloc of %zu bytes failed", count * sizeof(T));
       return TO_ENOMEM;
     }
+#ifdef TOMESH_DEBUG_POISON
+    // checking build (sanitizer substitute): every allocation starts as 0xff
+    // bytes (NaN doubles, -1 indices), so a read of memory no kernel or memset
+    // wrote poisons the results that parity tests compare
+    cudaMemset(d, 0xff, count * sizeof(T));
+#endif
     bufs.push_back({d, count * sizeof(T)});
     dev_bytes += (int64_t)(count * sizeof(T));
     *ptr = (T *)d;
