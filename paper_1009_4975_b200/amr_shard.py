@@ -1,0 +1,173 @@
+"""Morton-range partition of the general (AMR) path over ranks (SURVEY §8(e):
+"contiguous C2 (Morton) element ranges ... each node is owned by ... ;
+hanging-node parents on another rank join the halo"), host side.
+
+The device decomposition of the general path is already "owner computes"
+over contiguous ranges of the canonical (Morton, C3) node order
+(kernels_genfused.cuh).  The multi-GPU partition is the same cut one level
+up: rank r owns the nodes [n_r, n_{r+1}) (a union of whole blocks' worth of
+nodes, balanced by incidence count).  Its local mesh holds
+
+* every element that contributes to an owned node -- directly, or through a
+  hanging corner whose Eq. 6 parent is owned;
+* the local nodes: owned nodes first (in canonical order), then the ghosts
+  (every other non-hanging corner of a local element and every parent of a
+  local hanging corner: "hanging-node parents on another rank join the
+  halo"), then the hanging corner nodes that are not owned;
+* the hanging constraints of its hanging nodes (parents remapped, all local),
+  the fixed DOFs and loads of its nodes (a hanging node's load reaches its
+  owned parents through C^T, so b = Pi_F C^T f is exact on owned DOFs).
+
+Per PCG iteration a rank needs, for its ghosts, the previous iterate's r, q
+and p from their owners (send/recv lists below), the same data the
+structured z-slab path pushes into its ghost planes; the dots are all-reduced
+exactly as there.  Everything here is index bookkeeping (no method
+arithmetic); tests/test_amr_shard_host.py checks that the owned part of the
+operator computed from a rank's local mesh alone equals the global operator.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .api import HostMesh
+
+
+def node_incidence(host: HostMesh):
+    """Node -> contributing elements (direct corner, or hanging corner whose
+    parent is the node), as CSR (ptr, elems), elements ascending per node."""
+    d = host.dim
+    nc = 1 << d
+    en = host.elem_node.reshape(-1, nc).astype(np.int64)
+    hang_row = np.full(host.n_node, -1, dtype=np.int64)
+    hang_row[host.hang_node] = np.arange(host.hang_node.shape[0])
+    rows, cols = [], []
+    h = hang_row[en]                                          # [n_el, nc]
+    direct = h < 0
+    rows.append(en[direct])
+    cols.append(np.nonzero(direct)[0])
+    e_h, c_h = np.nonzero(~direct)
+    for e, row in zip(e_h, h[e_h, c_h]):
+        ps = host.hang_parent[host.hang_ptr[row]:host.hang_ptr[row + 1]].astype(np.int64)
+        rows.append(ps)
+        cols.append(np.full(ps.shape[0], e, dtype=np.int64))
+    rows = np.concatenate(rows)
+    cols = np.concatenate(cols)
+    o = np.lexsort((cols, rows))
+    rows, cols = rows[o], cols[o]
+    keep = np.ones(rows.shape[0], dtype=bool)
+    keep[1:] = (rows[1:] != rows[:-1]) | (cols[1:] != cols[:-1])
+    rows, cols = rows[keep], cols[keep]
+    ptr = np.searchsorted(rows, np.arange(host.n_node + 1))
+    return ptr, cols
+
+
+def partition(host: HostMesh, nranks: int, ptr=None):
+    """Contiguous node ranges [(n_r, n_{r+1})] of about equal incidence count
+    (the per-node work of the owner-computes operator)."""
+    if nranks < 1 or nranks > host.n_node:
+        raise ValueError("bad rank count")
+    if ptr is None:
+        ptr, _ = node_incidence(host)
+    cost = np.diff(ptr).astype(np.float64) + 1.0
+    cum = np.concatenate([[0.0], np.cumsum(cost)])
+    cuts = [0]
+    for r in range(1, nranks):
+        c = int(np.searchsorted(cum, cum[-1] * r / nranks))
+        cuts.append(max(cuts[-1] + 1, min(c, host.n_node - (nranks - r))))
+    cuts.append(host.n_node)
+    return list(zip(cuts[:-1], cuts[1:]))
+
+
+@dataclass
+class AmrSlab:
+    rank: int
+    n0: int                          # owned global nodes [n0, n1)
+    n1: int
+    host: HostMesh                   # local mesh: owned nodes are local [0, n_own)
+    n_own: int
+    n_ghost: int                     # ghosts: local [n_own, n_own + n_ghost)
+    node_global: np.ndarray          # local node -> global node
+    elem_global: np.ndarray          # local element -> global element
+    ghost_owner: np.ndarray          # [n_ghost] owning rank of each ghost
+    recv: dict = field(default_factory=dict)   # rank s -> local ghost indices whose values come from s
+    send: dict = field(default_factory=dict)   # rank s -> local owned indices that s needs
+
+
+def slice_host(host: HostMesh, nranks: int, rank: int, ranges=None, inc=None) -> AmrSlab:
+    """Rank `rank`'s local mesh and exchange lists (module docstring)."""
+    d = host.dim
+    nc = 1 << d
+    if inc is None:
+        inc = node_incidence(host)
+    ptr, els_of = inc
+    if ranges is None:
+        ranges = partition(host, nranks, ptr)
+    n0, n1 = ranges[rank]
+    elems = np.unique(els_of[ptr[n0]:ptr[n1]])
+    en = host.elem_node.reshape(-1, nc)[elems].astype(np.int64)
+    is_hang = np.zeros(host.n_node, dtype=bool)
+    is_hang[host.hang_node] = True
+    hang_row = np.full(host.n_node, -1, dtype=np.int64)
+    hang_row[host.hang_node] = np.arange(host.hang_node.shape[0])
+    corners = np.unique(en)
+    hang_c = corners[is_hang[corners]]
+    parents = [host.hang_parent[host.hang_ptr[hang_row[g]]:host.hang_ptr[hang_row[g] + 1]] for g in hang_c]
+    parents = np.unique(np.concatenate(parents).astype(np.int64)) if parents else np.zeros(0, np.int64)
+    nonhang = np.union1d(corners[~is_hang[corners]], parents)
+    owned = np.arange(n0, n1, dtype=np.int64)
+    ghosts = np.setdiff1d(nonhang, owned)
+    extra_hang = np.setdiff1d(hang_c, owned)                  # hanging corners outside the owned range
+    node_global = np.concatenate([owned, ghosts, extra_hang])
+    loc = np.full(host.n_node, -1, dtype=np.int64)
+    loc[node_global] = np.arange(node_global.shape[0])
+    # hanging constraints of the local hanging nodes (owned ones included), parents remapped
+    lh = node_global[is_hang[node_global]]
+    lh_local = loc[lh]
+    order = np.argsort(lh_local, kind="stable")
+    hptr, hpar, hw = [0], [], []
+    for g in lh[order]:
+        row = hang_row[g]
+        ps = host.hang_parent[host.hang_ptr[row]:host.hang_ptr[row + 1]]
+        ws = host.hang_weight[host.hang_ptr[row]:host.hang_ptr[row + 1]]
+        lp = loc[ps]
+        if np.any(lp < 0):
+            raise AssertionError("a parent of a local hanging node is not local")
+        o = np.argsort(lp)
+        hpar.extend(lp[o].tolist())
+        hw.extend(ws[o].tolist())
+        hptr.append(len(hpar))
+    fixed_g = host.fixed_dof
+    fnode = fixed_g // d
+    lf = loc[fnode]
+    sel = lf >= 0
+    fixed = np.sort(lf[sel] * d + fixed_g[sel] % d).astype(np.int64)
+    load = host.load.reshape(-1, d)[node_global].reshape(-1).copy()
+    local = HostMesh(
+        dim=d, L=host.L, h0=host.h0,
+        elem_node=loc[en].astype(np.int32), elem_anchor=host.elem_anchor[elems].copy(),
+        elem_level=host.elem_level[elems].copy(), node_coord=host.node_coord[node_global].copy(),
+        hang_node=np.sort(lh_local).astype(np.int32), hang_ptr=np.array(hptr, dtype=np.int32),
+        hang_parent=np.array(hpar, dtype=np.int32), hang_weight=np.array(hw, dtype=np.float64),
+        fixed_dof=fixed, load=load, filt_ptr=None, filt_idx=None, rmin=0.0)
+    starts = np.array([a for a, _ in ranges])
+    ghost_owner = np.searchsorted(starts, ghosts, side="right") - 1
+    slab = AmrSlab(rank=rank, n0=n0, n1=n1, host=local, n_own=int(n1 - n0), n_ghost=int(ghosts.shape[0]),
+                   node_global=node_global, elem_global=elems, ghost_owner=ghost_owner)
+    for s in np.unique(ghost_owner).tolist():
+        slab.recv[int(s)] = (n1 - n0) + np.nonzero(ghost_owner == s)[0]
+    return slab
+
+
+def exchange_lists(slabs):
+    """send[s] of every slab from the recv lists of the others (the global
+    node ids a rank receives are the ones its owner sends, same order)."""
+    for sl in slabs:
+        sl.send = {}
+    for sl in slabs:
+        for s, idx in sl.recv.items():
+            g = sl.node_global[idx]
+            owner = slabs[s]
+            owner.send[sl.rank] = g - owner.n0
+    return slabs
