@@ -127,9 +127,12 @@ typedef struct {
  *   TO_UPLOAD_GENERAL        keep a uniform H8 box on the general (canonical
  *                            Morton order) path instead of the structured
  *                            one; tosolve_minres with TO_PC_IC0 needs it.
- *   TO_UPLOAD_NO_PERSISTENT  2D meshes: launch one kernel per PCG iteration
- *                            instead of the persistent cooperative solver. */
-enum { TO_UPLOAD_GENERAL = 1, TO_UPLOAD_NO_PERSISTENT = 2 };
+ *   TO_UPLOAD_PERSISTENT     2D meshes up to 100k elements: run the whole PCG
+ *                            loop in one cooperative kernel (round 1's path
+ *                            for small meshes; the default one kernel per
+ *                            iteration is faster: c1 6.9 vs 8.0, c2 9.0 vs
+ *                            16.2 us per iteration). */
+enum { TO_UPLOAD_GENERAL = 1, TO_UPLOAD_PERSISTENT = 2 };
 
 typedef struct {
   int32_t iters;               /* CG iterations performed                        */

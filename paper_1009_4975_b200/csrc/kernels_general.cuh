@@ -4,7 +4,10 @@
 //   k_simp        a1  s_e = (E_min + x_e^p (E0 - E_min)) h_e^(d-2)       (Eq. 2)
 //   k_diag_*      a2  D = diag(Pi_F C^T K C Pi_F) (cross terms included)  (:515-521)
 //   k_rhs         a3  b = Pi_F C^T f                                      (Eq. 7 rhs)
-//   k_elem_pass + k_node_pass  a4-a6  one PCG iteration (or q = C^T K C p)  (Eq. 8)
+//   k_cg_general_persistent  a4-a7  the whole PCG loop in one cooperative
+//                                    kernel (opt-in for small 2D meshes; the
+//                                    default iteration is k_gen_fused,
+//                                    kernels_genfused.cuh)                  (Eq. 8)
 //   k_recover     a8  u = C u_hat                                         (Eq. 9)
 //   k_sens        a10 dc_e = -p x^(p-1)(E0-Emin) h^(d-2) u_e^T K0 u_e    (:343-346)
 //   k_filter      a11 Eq. 5 / density variant                             (:613-616)
@@ -303,7 +306,7 @@ __device__ __forceinline__ void had_apply(const K0Had3 &H, double (&x)[24], doub
   for (int a = 0; a < 24; ++a) y[a] = x[a];
 }
 
-// ---- general path, one PCG iteration = element pass + node pass --------------------------
+// ---- the persistent solver's iteration = element pass + node pass ------------------------
 // Deterministic and atomic-free (the paper's operator, Eq. 8, assembled on
 // the fly): the element pass stores y_e = s_e K0 (C_e p)_e per element; the
 // node pass sums, for each node, the (element, corner, weight) incidences of
@@ -499,308 +502,6 @@ __device__ __forceinline__ void g_node_one(int64_t n, const int64_t *__restrict_
   }
 #pragma unroll
   for (int h = 0; h < DIM; ++h) rec[h] = make_double2(t[2 * h], t[2 * h + 1]);
-}
-
-template <int DIM, int MODE>
-__global__ void __launch_bounds__(256, 3) k_elem_pass(MeshView M, const double *__restrict__ s,
-                                                      const double *__restrict__ zp, const double *__restrict__ po,
-                                                      double *__restrict__ ye,
-                                                      const __grid_constant__ K0Dense2 K2,
-                                                      const __grid_constant__ K0HadSym H, const uint8_t *__restrict__ hmask,
-                                                      CgScalars *S, double *partials) {
-  if (MODE == G_CG && cg_stopped(S)) return;
-  const double beta = MODE == G_CG ? __ldcg(&S->beta) : 0.0;
-  double pq = 0.0;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M.n_el; e += (int64_t)gridDim.x * blockDim.x)
-    pq += g_elem_one<DIM, MODE, false>(M, e, s, zp, po, ye, K2, H, hmask, beta);
-  if (MODE == G_CG) {
-    double v[1] = {pq};
-    if (grid_sum<1>(v, partials, &S->counter[CNT_PQ])) {
-      if (!(v[0] > 0.0)) {
-        cg_fail(S, (v[0] != v[0]) ? -5 : -6);
-        S->done = 1;
-      } else {
-        S->alpha = S->rho / v[0];
-      }
-    }
-  }
-}
-
-template <int DIM, int MODE>
-__global__ void __launch_bounds__(256) k_node_pass(int64_t n_node, const int64_t *__restrict__ inc_ptr,
-                                                   const uint32_t *__restrict__ inc, const double *__restrict__ ye,
-                                                   double *__restrict__ r, const double *__restrict__ Dinv,
-                                                   double *__restrict__ zp, double *__restrict__ x,
-                                                   double *__restrict__ q_out, double *partials, CgScalars *S,
-                                                   double *hist) {
-  if (MODE == G_CG && cg_stopped(S)) return;
-  const double beta = MODE == G_CG ? __ldcg(&S->beta) : 0.0;
-  const double alpha = MODE == G_CG ? __ldcg(&S->alpha) : 0.0;
-  double acc[2] = {0.0, 0.0};
-  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_node; n += (int64_t)gridDim.x * blockDim.x)
-    g_node_one<DIM, MODE, false>(n, inc_ptr, inc, ye, r, Dinv, zp, x, q_out, alpha, beta, acc);
-  if (MODE == G_CG) {
-    if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) {
-      cg_after_rupdate(S, acc[0], acc[1], hist);
-      if (S->done_next) S->done = 1;                 // x is already complete
-    }
-  }
-}
-
-// ---- lane-per-corner variants (latency-bound AMR meshes) --------------------------------
-// A group of 2^DIM lanes handles one element: lane c gathers corner c (with
-// the Eq. 6 interpolation if it is hanging), the element product runs across
-// the group with warp shuffles, lane c stores y_e[corner c].  In 3D the
-// Walsh-Hadamard stages are xor-shuffles and lane c holds Hadamard mode c.
-template <int DIM, int MODE, bool COH>
-__device__ __forceinline__ double g_elem_lane(const MeshView &M, int64_t e, int c, const double *__restrict__ s,
-                                              const double *__restrict__ zp, const double *__restrict__ po,
-                                              double *__restrict__ ye,
-                                              const K0Dense2 &K2, const K0HadSym &H,
-                                              const uint8_t *__restrict__ hmask, double beta, bool live) {
-  constexpr int NC = 1 << DIM;
-  const int n = __ldg(M.elem_node + e * NC + c);
-  const double se = __ldg(s + e);   // independent of the gather: issued first
-  double v[DIM];
-  g_pnode<DIM, MODE, COH>(zp, po, beta, n, v);
-  if ((__ldg(hmask + e) >> c) & 1) {
-    const int h = M.node_hang[n];
-#pragma unroll
-    for (int i = 0; i < DIM; ++i) v[i] = 0.0;
-    for (int k = M.hang_ptr[h]; k < M.hang_ptr[h + 1]; ++k) {
-      const double w = M.hang_weight[k];
-      double t[DIM];
-      g_pnode<DIM, MODE, COH>(zp, po, beta, M.hang_parent[k], t);
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) v[i] = fma(w, t[i], v[i]);
-    }
-  }
-  double en = 0.0, y[DIM];
-  if constexpr (DIM == 3) {
-    // forward WHT over the group: stage b pairs lanes c and c ^ b
-#pragma unroll
-    for (int b = 1; b < 8; b <<= 1)
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const double o = __shfl_xor_sync(0xffffffffu, v[i], b);
-        v[i] = (c & b) ? o - v[i] : v[i] + o;
-      }
-    // middle: mode m = c; coupling to lane m ^ e_i ^ e_j, component j
-    const int m = c;
-    const int bit[3] = {m & 1, (m >> 1) & 1, (m >> 2) & 1};
-    const int pop = bit[0] + bit[1] + bit[2];
-    double xo[3][3];                                    // xo[i][j] = xhat(m ^ e_i ^ e_j, j)
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = i + 1; j < 3; ++j) {
-        const int mask = (1 << i) | (1 << j);
-        xo[i][j] = __shfl_xor_sync(0xffffffffu, v[j], mask);
-        xo[j][i] = __shfl_xor_sync(0xffffffffu, v[i], mask);
-      }
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const int b = bit[i], nn = pop - b;
-      const double dco = b ? (nn == 0 ? H.d[1][0] : nn == 1 ? H.d[1][1] : H.d[1][2])
-                           : (nn == 0 ? 0.0 : nn == 1 ? H.d[0][1] : H.d[0][2]);
-      double acc = dco * v[i];
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        if (j == i) continue;
-        const int t = 3 - i - j;
-        const double oco = b ? (bit[t] ? H.o[1][1] : H.o[1][0]) : (bit[t] ? H.o[0][1] : H.o[0][0]);
-        acc = (bit[j] != b) ? fma(oco, xo[i][j], acc) : acc;
-      }
-      y[i] = acc;
-    }
-#pragma unroll
-    for (int i = 0; i < 3; ++i) en = fma(v[i], y[i], en);
-    // inverse WHT over the group
-#pragma unroll
-    for (int b = 1; b < 8; b <<= 1)
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const double o = __shfl_xor_sync(0xffffffffu, y[i], b);
-        y[i] = (c & b) ? o - y[i] : y[i] + o;
-      }
-  } else {
-    // 2D: y(c,i) = sum_{c',j} K0[(c,i),(c',j)] v(c',j), the other corners by shuffles
-    const int base = (threadIdx.x & 31) & ~(NC - 1);
-    double vv[NC][2];
-#pragma unroll
-    for (int cc = 0; cc < NC; ++cc)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) vv[cc][j] = __shfl_sync(0xffffffffu, v[j], base + cc);
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      double acc = 0.0;
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) acc = fma(K2.K[(2 * c + i) * 8 + 2 * cc + j], vv[cc][j], acc);
-      y[i] = acc;
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i) en = fma(v[i], y[i], en);
-  }
-  if (live) {
-#pragma unroll
-    for (int i = 0; i < DIM; ++i) ye[(e * NC + c) * DIM + i] = se * y[i];
-  }
-  return live ? se * en : 0.0;
-}
-
-template <int DIM, int MODE>
-__global__ void __launch_bounds__(256) k_elem_pass_lanes(MeshView M, const double *__restrict__ s,
-                                                         const double *__restrict__ zp, const double *__restrict__ po,
-                                                         double *__restrict__ ye,
-                                                         const __grid_constant__ K0Dense2 K2,
-                                                         const __grid_constant__ K0HadSym H,
-                                                         const uint8_t *__restrict__ hmask, CgScalars *S,
-                                                         double *partials) {
-  constexpr int NC = 1 << DIM;
-  pdl_wait();
-  pdl_release();
-  // the stop flags are read without a control dependency at the top (their
-  // latency overlaps the gathers); a stopped iteration only skips the stores
-  const bool stopped = MODE == G_CG && (__ldcg(&S->done) | __ldcg(&S->done_next));
-  const double beta = MODE == G_CG ? __ldcg(&S->beta) : 0.0;
-  const int c = threadIdx.x & (NC - 1);
-  const int64_t groups = ((int64_t)gridDim.x * blockDim.x) / NC;
-  double pq = 0.0;
-  // the loop bound is uniform per warp (whole groups), so the shuffles stay converged
-  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / NC - (threadIdx.x & 31) / NC;
-       base < M.n_el; base += groups) {
-    const int64_t e = base + (threadIdx.x & 31) / NC;
-    const bool live = e < M.n_el;
-    pq += g_elem_lane<DIM, MODE, false>(M, live ? e : M.n_el - 1, c, s, zp, po, ye, K2, H, hmask, beta,
-                                        live && !stopped);
-  }
-  if (stopped) return;
-  if (MODE == G_CG) {
-    double v[1] = {pq};
-    if (grid_sum<1>(v, partials, &S->counter[CNT_PQ])) {
-      if (!(v[0] > 0.0)) {
-        cg_fail(S, (v[0] != v[0]) ? -5 : -6);
-        S->done = 1;
-      } else {
-        S->alpha = S->rho / v[0];
-      }
-    }
-  }
-}
-
-// Node pass with a group of 4 lanes per node: lane l sums incidences l, l+4,
-// ... of the node, an xor-shuffle tree completes q_n in every lane of the
-// group, and lane i < DIM updates component i of the node (record, x, r).
-// One node of the 4-lane node pass (lane l of the group): q_n over the node's
-// incidences, then on lane l < DIM the CG update of component l.  COH: ye is
-// read through L2 (it was written in the same kernel by other blocks).
-template <int DIM, int MODE, bool COH>
-__device__ __forceinline__ void g_node_group(int64_t n, bool live, int l, const int64_t *__restrict__ inc_ptr,
-                                             const uint32_t *__restrict__ inc, const double *__restrict__ ye,
-                                             double *__restrict__ r, const double *__restrict__ Dinv,
-                                             double *__restrict__ zp, double *__restrict__ x,
-                                             double *__restrict__ q_out, double alpha, double beta, bool stopped,
-                                             double (&acc)[2]) {
-  constexpr int G = 4;
-  // node-side operands do not depend on q: load them before the incidence sum
-  const int64_t dpre = n * DIM + l;
-  double di_p = 0.0, r_p = 0.0, x_p = 0.0, z_p = 0.0, po_p = 0.0;
-  if (MODE == G_CG && live && l < DIM) {
-    di_p = __ldg(Dinv + dpre);
-    r_p = r[dpre];
-    x_p = x[dpre];
-    z_p = zp[n * 2 * DIM + l];
-    po_p = zp[n * 2 * DIM + DIM + l];
-  }
-  double qv[DIM];
-#pragma unroll
-  for (int i = 0; i < DIM; ++i) qv[i] = 0.0;
-  if (live) {
-    const int64_t k1 = inc_ptr[n + 1];
-    // two incidences per lane per round: both index and value loads in flight together
-    for (int64_t k = inc_ptr[n] + l; k < k1; k += 2 * G) {
-      const bool two = k + G < k1;
-      const uint32_t t = __ldg(&inc[k]);
-      const uint32_t u = two ? __ldg(&inc[k + G]) : 0u;
-      const double w = (t >> 30) == 0 ? 1.0 : (t >> 30) == 1 ? 0.5 : 0.25;
-      const double wu = !two ? 0.0 : (u >> 30) == 0 ? 1.0 : (u >> 30) == 1 ? 0.5 : 0.25;
-      const double *src = ye + (int64_t)(t & 0x3fffffffu) * DIM;
-      const double *srcu = ye + (int64_t)(u & 0x3fffffffu) * DIM;
-      double a[DIM], b[DIM];
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) {
-        a[i] = COH ? g_ld<true>(src + i) : __ldg(src + i);
-        b[i] = two ? (COH ? g_ld<true>(srcu + i) : __ldg(srcu + i)) : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) qv[i] = fma(wu, b[i], fma(w, a[i], qv[i]));
-    }
-  }
-#pragma unroll
-  for (int b = 1; b < G; b <<= 1)
-#pragma unroll
-    for (int i = 0; i < DIM; ++i) qv[i] += __shfl_xor_sync(0xffffffffu, qv[i], b);
-  if (!live || l >= DIM || stopped) return;
-  // lane l < DIM: component l
-  double qc = qv[0];
-#pragma unroll
-  for (int i = 1; i < DIM; ++i) qc = (l == i) ? qv[i] : qc;
-  const int64_t d = n * DIM + l;
-  if (MODE == G_PLAIN) {
-    q_out[d] = qc;
-    return;
-  }
-  double *rec = zp + n * 2 * DIM;
-  const double di = di_p;
-  const double pk = fma(beta, po_p, z_p);
-  double zn = 0.0;
-  if (di != 0.0) {
-    x[d] = fma(alpha, pk, x_p);
-    const double rn = fma(-alpha, qc, r_p);
-    r[d] = rn;
-    zn = di * rn;
-    acc[0] = fma(rn, zn, acc[0]);
-    acc[1] = fma(rn, rn, acc[1]);
-  }
-  rec[l] = zn;
-  rec[DIM + l] = pk;
-}
-
-// Node pass with a group of 4 lanes per node: lane l sums incidences l, l+4,
-// ... of the node, an xor-shuffle tree completes q_n in every lane of the
-// group, and lane i < DIM updates component i of the node (record, x, r).
-template <int DIM, int MODE>
-__global__ void __launch_bounds__(256) k_node_pass_lanes(int64_t n_node, const int64_t *__restrict__ inc_ptr,
-                                                         const uint32_t *__restrict__ inc, const double *__restrict__ ye,
-                                                         double *__restrict__ r, const double *__restrict__ Dinv,
-                                                         double *__restrict__ zp, double *__restrict__ x,
-                                                         double *__restrict__ q_out, double *partials, CgScalars *S,
-                                                         double *hist) {
-  constexpr int G = 4;
-  pdl_wait();
-  pdl_release();
-  // stop flags without a control dependency at the top (see k_elem_pass_lanes)
-  const bool stopped = MODE == G_CG && (__ldcg(&S->done) | __ldcg(&S->done_next));
-  const double beta = MODE == G_CG ? __ldcg(&S->beta) : 0.0;
-  const double alpha = MODE == G_CG ? __ldcg(&S->alpha) : 0.0;
-  const int l = threadIdx.x & (G - 1);
-  const int64_t groups = ((int64_t)gridDim.x * blockDim.x) / G;
-  double acc[2] = {0.0, 0.0};
-  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G - (threadIdx.x & 31) / G; base < n_node;
-       base += groups) {
-    const int64_t n = base + (threadIdx.x & 31) / G;
-    g_node_group<DIM, MODE, false>(n, n < n_node, l, inc_ptr, inc, ye, r, Dinv, zp, x, q_out, alpha, beta, stopped,
-                                   acc);
-  }
-  if (stopped) return;
-  if (MODE == G_CG) {
-    if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) {
-      cg_after_rupdate(S, acc[0], acc[1], hist);
-      if (S->done_next) S->done = 1;                 // x is already complete
-    }
-  }
 }
 
 // The whole general-path PCG loop in one cooperative (persistent) kernel:

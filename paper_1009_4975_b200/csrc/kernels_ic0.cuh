@@ -28,7 +28,6 @@ namespace tomesh {
 template <int DIM>
 __global__ void k_ic0_assemble(Ic0View V, const double *__restrict__ s, const double *__restrict__ msc,
                                const double *__restrict__ K0, double shift, double *__restrict__ kt) {
-  constexpr int ND = DIM << DIM;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < V.nnz; t += (int64_t)gridDim.x * blockDim.x) {
     const int i = V.row[t], j = V.col[t];
     double a = 0.0;

@@ -58,7 +58,7 @@ int validate(const to_mesh_desc *d) {
     if (f < 0 || f >= d->n_node * d->dim || (i > 0 && f <= d->fixed_dof[i - 1])) { set_error("fixed_dof not ascending / out of range"); return TO_EMESH; }
     if (hang[f / d->dim]) { set_error("fixed DOF %lld is on a hanging node", (long long)f); return TO_EMESH; }
   }
-  if ((d->options & ~(uint32_t)(TO_UPLOAD_GENERAL | TO_UPLOAD_NO_PERSISTENT)) != 0 || d->reserved != 0) {
+  if ((d->options & ~(uint32_t)(TO_UPLOAD_GENERAL | TO_UPLOAD_PERSISTENT)) != 0 || d->reserved != 0) {
     set_error("unknown upload option bits 0x%x", d->options);
     return TO_EINVAL;
   }
@@ -632,11 +632,11 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
     std::vector<uint32_t> incv;
     RC(setup_incidence(d, node_hang, st, m, iptr, incv));
     RC(build_gen_blocks(d, node_hang, iptr, incv, st, m));
-    // persistent cooperative solver for small 2D meshes (latency-bound: one
-    // kernel for the whole loop, no launches)
+    // opt-in: the persistent cooperative solver for small 2D meshes (the whole
+    // loop in one kernel; slower than one kernel per iteration since round 2)
     int coop = 0;
     CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
-    if (coop && !(d->options & TO_UPLOAD_NO_PERSISTENT) && d->dim == 2 && d->n_elem <= 100000) {
+    if (coop && (d->options & TO_UPLOAD_PERSISTENT) && d->dim == 2 && d->n_elem <= 100000) {
       int per_sm = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_general_persistent<2>, kBlock, 0));
       const int64_t need = (std::max<int64_t>(d->n_elem, d->n_node) + kBlock - 1) / kBlock;

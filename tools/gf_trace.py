@@ -26,7 +26,7 @@ u = torch.zeros(hm.n_dof, dtype=torch.float64, device="cuda:0")
 st = m.tosolve_cg(prob.penal, x, u, rtol=0.0, max_iter=iters, flags=pb.TO_FIXED_ITERS | pb.TO_NO_TRUE_RES)
 buf = np.zeros((16384, 8), dtype=np.uint64)
 L.lib().to_debug_gf_trace(buf.ctypes.data_as(C.c_void_p))
-t = buf[np.any(buf != 0, axis=1)].astype(np.int64)
+t = buf[np.any(buf[:, :7] != 0, axis=1)].astype(np.int64)
 nb = t.shape[0]
 t0 = t[:, 0].min()
 names = ["meta+issue+pdl", "S+owned", "mbar+halo", "virt+elem+acc", "q+dots", "grid_sum"]
@@ -34,6 +34,8 @@ print(name, "blocks", nb, "us/it", round(st.ms * 1e3 / iters, 2), "kernel span u
 for k in range(6):
     d = (t[:, k + 1] - t[:, k]) / 1e3
     print(f"  {names[k]:16s} mean {d.mean():7.2f} us  p50 {np.median(d):7.2f}  p90 {np.percentile(d, 90):7.2f}")
+el = t[:, 7] / 1e3
+print(f"  (elements+barrier mean {el.mean():7.2f} us  p50 {np.median(el):7.2f})")
 life = (t[:, 6] - t[:, 0]) / 1e3
 print(f"  block lifetime   mean {life.mean():7.2f} us  p50 {np.median(life):7.2f}  max {life.max():7.2f}")
 start = (t[:, 0] - t0) / 1e3
