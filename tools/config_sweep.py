@@ -16,11 +16,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_1009_4975_b200 as pb  # noqa: E402
-from inputs import config, density_at  # noqa: E402
+from inputs import density_at  # noqa: E402
+from tests.oracle_cache import variant  # noqa: E402
 
 
 def run(name):
-    prob = config(name)
+    prob = variant(name)
     t0 = time.perf_counter()
     hm = pb.prepare(prob)
     t1 = time.perf_counter()
@@ -55,10 +56,10 @@ def run(name):
             "it_per_s_to_tol": round(st.iters / (st.ms / 1e3), 1) if st.ms else None,
             "it_per_s_fixed200": round(200 / (fx.ms / 1e3), 1),
             "us_per_iter_fixed200": round(fx.ms * 1e3 / 200, 2),
-            "sens_plus_filter_ms": round(e0.elapsed_time(e1) / 5, 3)}
+            "sens_plus_filter_ms": round(e0.elapsed_time(e1) / 5, 3), "variant": info["matvec_variant"]}
 
 
 if __name__ == "__main__":
-    names = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"]
+    names = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c4L", "c5"]
     for n in names:
         print(json.dumps(run(n)), flush=True)
