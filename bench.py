@@ -543,7 +543,9 @@ def run_weak(args):
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
     import torch.distributed as dist
-    dist.init_process_group("gloo")              # plumbing only: IPC handles, barriers, the max over ranks
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")   # (a single process: --weak at N = 1)
+    os.environ.setdefault("MASTER_PORT", "29517")
+    dist.init_process_group("gloo", rank=rank, world_size=ws)   # plumbing only: IPC handles, barriers, the max
     dev = torch.device("cuda", local)
     t_prep = time.perf_counter()
     sl, x_np, prob = weak_slab(ws, rank)
@@ -765,6 +767,7 @@ def main():
     ap.add_argument("--no-general", action="store_true", help="skip the c4L general-path sub-record")
     ap.add_argument("--shard", action="store_true",
                     help="split ONE c5 solve into z-slabs over the ranks (strong scaling)")
+    ap.add_argument("--weak", action="store_true", help="the weak-scaled sharded solve even at N = 1")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: N independent c5 solves (no data-path collective) instead of the weak-scaled "
                          "sharded solve")
@@ -773,7 +776,7 @@ def main():
         return run_reference(args)
     if args.shard:
         return run_shard(args)
-    if _dist()[0] > 1 and not args.replicas:
+    if args.weak or (_dist()[0] > 1 and not args.replicas):
         return run_weak(args)
     return run_ours(args)
 
