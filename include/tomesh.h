@@ -119,7 +119,12 @@ typedef struct {
   const int32_t *filt_idx;     /* [filt_nnz] neighbours with |c_d-c_e| < rmin,
                                   ascending, self included (C9)                  */
   uint32_t options;            /* TO_UPLOAD_* bits below (0 = defaults)          */
-  uint32_t reserved;           /* must be 0                                      */
+  int32_t  n_owned;            /* 0: every node is this handle's.  > 0: a rank's
+                                  local mesh of a general-path shard group
+                                  (to_gshard_attach): nodes [0, n_owned) are
+                                  owned, the rest ghosts / hanging; the
+                                  operator is built for the owned nodes only
+                                  (forces the general path)                      */
 } to_mesh_desc;
 
 /* to_mesh_desc.options.  The operator, and therefore u, is the same on every
@@ -362,13 +367,37 @@ int  to_optimize(to_mesh *m, const to_opt_params *params, int32_t n_steps, doubl
 typedef struct {
   double *rb[2], *pb[2], *qb[2];   /* internal CG vectors (ping-pong)                  */
   double *x;                       /* internal iterate                                 */
-  double *slots;                   /* [2][TO_SHARD_MAX][8] all-reduce slots            */
-  unsigned long long *flags;       /* [2][TO_SHARD_MAX] sequence flags                 */
-  int32_t nx, ny, nz;              /* node box of the handle                            */
+  double *slots;                   /* [4][TO_SHARD_MAX][8] all-reduce slots            */
+  unsigned long long *flags;       /* [4][TO_SHARD_MAX] sequence flags                 */
+  int32_t nx, ny, nz;              /* node box of the handle (0: general handle)        */
   int32_t pad;
-  int64_t plane_doubles;           /* doubles per internal node plane                  */
+  int64_t plane_doubles;           /* doubles per internal node plane (0: general)     */
+  double *dinv;                    /* Jacobi inverse diagonal (general handles)         */
 } to_shard_bufs;
 int  to_shard_buffers(to_mesh *m, to_shard_bufs *out, void *cuda_stream);
+
+/* ---- Morton node-range sharding of the general (AMR) path ------
+ * Rank r's handle is uploaded with its local mesh (paper_1009_4975_b200/
+ * amr_shard.py): its owned nodes first (to_mesh_desc.n_owned), then the ghosts
+ * (the other corners of its elements and the parents of its hanging corners),
+ * then its non-owned hanging nodes; every element contributing to an owned
+ * node (directly or through a hanging corner, Eq. 6).  The iteration kernel
+ * computes the owned nodes; after it, every rank stores r_k, p_k, q_k of the
+ * nodes its peers hold as ghosts into their buffers (peer stores) and pushes
+ * its partial dots (the same slot / flag all-reduce as the z-slab path), so
+ * the next iteration reads complete ghosts and every rank takes the same step.
+ * Jacobi diagonal and b at the ghosts come from their owners once per solve,
+ * and x after it (sensitivities of every local element are then exact).
+ * to_gshard_attach  makes a general handle rank `rank` of `nranks`: send
+ *                   entry i stores this rank's owned local node send_local[i]
+ *                   into ghost node send_remote[i] of rank send_rank[i];
+ *                   peers[r] = rank r's to_shard_buffers.  Synchronises.
+ * tosolve_cg_group drives attached general handles the same way as slabs; the
+ * filter is not sharded (handles are uploaded with rmin = 0), and
+ * to_sensitivity's compliance_host is the rank's partial over owned DOFs. */
+int  to_gshard_attach(to_mesh *m, int32_t rank, int32_t nranks, const to_shard_bufs *peers, int64_t n_send,
+                      const int32_t *send_rank, const int32_t *send_local, const int32_t *send_remote,
+                      void *cuda_stream);
 int  to_shard_attach(to_mesh *m, int32_t rank, int32_t nranks, const int32_t *gz_lo, int32_t own_lo,
                      int32_t own_hi, const to_shard_bufs *peers, void *cuda_stream);
 int  tosolve_cg_group(to_mesh *const *ms, int32_t n, double penal, const double *const *x_dev,

@@ -34,7 +34,7 @@ class ToMeshDesc(C.Structure):
         ("load", P),
         ("E0", C.c_double), ("Emin", C.c_double), ("nu", C.c_double),
         ("rmin", C.c_double), ("filt_nnz", C.c_int64), ("filt_ptr", P), ("filt_idx", P),
-        ("options", C.c_uint32), ("reserved", C.c_uint32),
+        ("options", C.c_uint32), ("n_owned", C.c_int32),
     ]
 
 
@@ -113,7 +113,7 @@ TO_SHARD_MAX = 16
 class ToShardBufs(C.Structure):
     _fields_ = [("rb", P * 2), ("pb", P * 2), ("qb", P * 2), ("x", P), ("slots", P), ("flags", P),
                 ("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("pad", C.c_int32),
-                ("plane_doubles", C.c_int64)]
+                ("plane_doubles", C.c_int64), ("dinv", P)]
 
 
 EXPORTS = {
@@ -146,6 +146,7 @@ EXPORTS = {
     "to_last_error": (C.c_char_p, []),
     "to_shard_buffers": (C.c_int, [P, C.POINTER(ToShardBufs), P]),
     "to_shard_attach": (C.c_int, [P, C.c_int32, C.c_int32, P, C.c_int32, C.c_int32, C.POINTER(ToShardBufs), P]),
+    "to_gshard_attach": (C.c_int, [P, C.c_int32, C.c_int32, C.POINTER(ToShardBufs), C.c_int64, P, P, P, P]),
     "tosolve_cg_group": (C.c_int, [P, C.c_int32, C.c_double, P, P, C.c_double, C.c_int32, C.c_uint32,
                                    C.POINTER(ToCgStats), P]),
     "to_ipc_export": (C.c_int, [P, P, P, C.POINTER(C.c_uint64)]),

@@ -171,3 +171,83 @@ def exchange_lists(slabs):
             owner = slabs[s]
             owner.send[sl.rank] = g - owner.n0
     return slabs
+
+
+def send_entries(slabs, rank):
+    """Rank `rank`'s ghost-store list for to_gshard_attach: (destination rank,
+    local owned node, the destination's local ghost node) per entry."""
+    sl = slabs[rank]
+    dst, loc, rem = [], [], []
+    for other in slabs:
+        if other.rank == rank or rank not in other.recv:
+            continue
+        idx = other.recv[rank]                                  # other's ghost slots fed by this rank
+        g = other.node_global[idx]
+        dst.append(np.full(idx.shape[0], other.rank, dtype=np.int32))
+        loc.append((g - sl.n0).astype(np.int32))
+        rem.append(idx.astype(np.int32))
+    if not dst:
+        return np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32)
+    return np.concatenate(dst), np.concatenate(loc), np.concatenate(rem)
+
+
+def element_owner(host: HostMesh, ranges):
+    """The rank that reports each element's sensitivity when results are
+    gathered: the owner of its corner 0 (of corner 0's first Eq. 6 parent when
+    that corner is hanging).  Every local element's dc is exact on every rank
+    holding it; this only avoids double counting."""
+    d = host.dim
+    nc = 1 << d
+    c0 = host.elem_node.reshape(-1, nc)[:, 0].astype(np.int64)
+    hang_row = np.full(host.n_node, -1, dtype=np.int64)
+    hang_row[host.hang_node] = np.arange(host.hang_node.shape[0])
+    h = hang_row[c0]
+    node = c0.copy()
+    sel = h >= 0
+    node[sel] = host.hang_parent[host.hang_ptr[h[sel]]]
+    starts = np.array([a for a, _ in ranges])
+    return np.searchsorted(starts, node, side="right") - 1
+
+
+class AmrShardGroup:
+    """Every rank of a general-path shard group in one process, on one device
+    (tosolve_cg_group drives them in lockstep; the ghost stores are
+    device-to-device, the all-reduce the slot / flag protocol)."""
+
+    def __init__(self, host: HostMesh, nranks: int, E0=1.0, Emin=1e-9, nu=0.3, device=0):
+        from .api import Mesh
+        self.host = host
+        inc = node_incidence(host)
+        self.ranges = partition(host, nranks, inc[0])
+        self.slabs = exchange_lists([slice_host(host, nranks, r, self.ranges, inc) for r in range(nranks)])
+        self.meshes = [Mesh(sl.host, E0=E0, Emin=Emin, nu=nu, rmin=0.0, device=device, n_owned=sl.n_own)
+                       for sl in self.slabs]
+        bufs = [m.shard_buffers() for m in self.meshes]
+        for r, m in enumerate(self.meshes):
+            m.gshard_attach(r, nranks, bufs, *send_entries(self.slabs, r))
+        owner = element_owner(host, self.ranges)
+        self.elem_owned = [owner[sl.elem_global] == sl.rank for sl in self.slabs]
+
+    def scatter_elems(self, x_global):
+        import torch
+        return [x_global.index_select(0, torch.as_tensor(sl.elem_global, device=x_global.device))
+                for sl in self.slabs]
+
+    def solve(self, penal, xs, us, rtol=1e-10, max_iter=20000, flags=0):
+        from . import _lib as L
+        from .api import tosolve_cg_group
+        return tosolve_cg_group(self.meshes, penal, xs, us, rtol, max_iter, flags | L.TO_NO_TRUE_RES)
+
+    def gather_nodes(self, us):
+        d = self.host.dim
+        out = np.zeros(self.host.n_dof)
+        for sl, u in zip(self.slabs, us):
+            un = u.detach().cpu().numpy().reshape(-1, d)
+            out.reshape(-1, d)[sl.node_global[:sl.n_own]] = un[:sl.n_own]
+        return out
+
+    def gather_elems(self, vs):
+        out = np.zeros(self.host.n_el)
+        for sl, v, own in zip(self.slabs, vs, self.elem_owned):
+            out[sl.elem_global[own]] = v.detach().cpu().numpy()[own]
+        return out

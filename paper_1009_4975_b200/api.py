@@ -247,7 +247,7 @@ def _stream(stream):
     return C.c_void_p(s.cuda_stream)
 
 
-def make_desc(host: HostMesh, E0, Emin, nu, rmin, options=0):
+def make_desc(host: HostMesh, E0, Emin, nu, rmin, options=0, n_owned=0):
     """to_mesh_desc of a host mesh (argument marshalling only); returns the
     struct and the numpy arrays it points into (keep them alive)."""
     keep = []
@@ -281,15 +281,19 @@ def make_desc(host: HostMesh, E0, Emin, nu, rmin, options=0):
         d.filt_ptr = arr(host.filt_ptr, np.int64)
         d.filt_idx = arr(host.filt_idx, np.int32)
     d.options = int(options)
+    d.n_owned = int(n_owned)
     return d, keep
 
 
 class Mesh:
     """Device copy of a mesh + CG workspace (tomesh_upload / tomesh_free)."""
 
-    def __init__(self, host: HostMesh, E0=1.0, Emin=1e-9, nu=0.3, rmin=None, device=0, stream=None, options=0):
+    def __init__(self, host: HostMesh, E0=1.0, Emin=1e-9, nu=0.3, rmin=None, device=0, stream=None, options=0,
+                 n_owned=0):
         """options: TO_UPLOAD_* bits of include/tomesh.h (which device code
-        applies the operator; the operator itself does not change)."""
+        applies the operator; the operator itself does not change).  n_owned
+        > 0: a rank's local mesh of a general-path shard group (nodes
+        [0, n_owned) owned; paper_1009_4975_b200.amr_shard)."""
         import torch
         self.host = host
         self.device = torch.device("cuda", device)
@@ -297,7 +301,7 @@ class Mesh:
         self.n_el, self.n_node, self.n_dof = host.n_el, host.n_node, host.n_dof
         self.E0, self.Emin, self.nu = E0, Emin, nu
         rmin = host.rmin if rmin is None else rmin
-        d, self._keep = make_desc(host, E0, Emin, nu, rmin, options)
+        d, self._keep = make_desc(host, E0, Emin, nu, rmin, options, n_owned)
         self._h = C.c_void_p()
         with torch.cuda.device(self.device):
             L.check(L.lib().tomesh_upload(C.byref(d), device, _stream(stream), C.byref(self._h)), "tomesh_upload")
@@ -337,6 +341,16 @@ class Mesh:
         arr = (L.ToShardBufs * nranks)(*peers)
         L.check(L.lib().to_shard_attach(self._h, int(rank), int(nranks), _ptr(gz), int(own_lo), int(own_hi), arr,
                                         _stream(stream)), "to_shard_attach")
+
+    def gshard_attach(self, rank, nranks, peers, send_rank, send_local, send_remote, stream=None):
+        """to_gshard_attach: send entry i stores owned local node send_local[i]
+        into ghost node send_remote[i] of rank send_rank[i]."""
+        arr = (L.ToShardBufs * nranks)(*peers)
+        sr = np.ascontiguousarray(send_rank, dtype=np.int32)
+        sl = np.ascontiguousarray(send_local, dtype=np.int32)
+        sm = np.ascontiguousarray(send_remote, dtype=np.int32)
+        L.check(L.lib().to_gshard_attach(self._h, int(rank), int(nranks), arr, int(sr.shape[0]), _ptr(sr), _ptr(sl),
+                                         _ptr(sm), _stream(stream)), "to_gshard_attach")
 
     def ipc_export(self, dev_ptr):
         h = (C.c_byte * 64)()

@@ -29,7 +29,7 @@ struct CgScalars {
   uint32_t counter[8];   // last-block-done counters, one per reduction site
 };
 
-enum { CNT_PQ = 0, CNT_U1 = 1, CNT_INIT = 2, CNT_MISC = 3, CNT_MISC2 = 4 };
+enum { CNT_PQ = 0, CNT_U1 = 1, CNT_INIT = 2, CNT_MISC = 3, CNT_MISC2 = 4, CNT_XCHG = 5 };
 
 #define GRID_STRIDE(i, n) \
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)

@@ -40,6 +40,7 @@
 #include "element.h"
 #include "kernels_cg.cuh"
 #include "kernels_general.cuh"
+#include "kernels_shard.cuh"
 #include "tomesh_types.cuh"
 
 namespace tomesh {
@@ -450,11 +451,21 @@ static __global__ void __launch_bounds__(512) k_gen_step(int nb, const double *_
 
 // After exactly N iterations (general path): r_N = r_{N-1} - alpha q_{N-1},
 // x_N = x_{N-1} + alpha p_{N-1}, rho_N, rr_N (per-DOF Dinv).
-static __global__ void k_final_gen(int64_t n, const double *__restrict__ ro, const double *__restrict__ qo,
-                                   const double *__restrict__ po, const double *__restrict__ Dinv,
-                                   double *__restrict__ x, double *partials, CgScalars *S, int n_iter, double rtol,
-                                   double *hist) {
-  if (cg_stopped(S)) return;
+// SHARD (general-path shard group, kernels_gshard.cuh): over the owned DOFs
+// [0, n); the partial rho_N, rr_N are pushed for k_shard_final (zeros when
+// the solve had stopped: every rank pushes every tail sequence).
+template <bool SHARD = false>
+__global__ void k_final_gen(int64_t n, const double *__restrict__ ro, const double *__restrict__ qo,
+                            const double *__restrict__ po, const double *__restrict__ Dinv,
+                            double *__restrict__ x, double *partials, CgScalars *S, int n_iter, double rtol,
+                            double *hist, const __grid_constant__ ShardComm C, unsigned long long seq) {
+  if (cg_stopped(S)) {
+    if (SHARD && blockIdx.x == 0 && threadIdx.x == 0) {
+      const double zero[2] = {0.0, 0.0};
+      shard_push(C, seq, zero, 2);
+    }
+    return;
+  }
   const double alpha = __ldcg(&S->alpha);
   double acc[2] = {0.0, 0.0};
   GRID_STRIDE(i, n) {
@@ -464,7 +475,10 @@ static __global__ void k_final_gen(int64_t n, const double *__restrict__ ro, con
     acc[0] = fma(rn, d * rn, acc[0]);
     acc[1] = fma(rn, rn, acc[1]);
   }
-  if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) cg_final_step(S, n_iter, acc[0], acc[1], rtol, hist);
+  if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) {
+    if (SHARD) shard_push(C, seq, acc, 2);
+    else cg_final_step(S, n_iter, acc[0], acc[1], rtol, hist);
+  }
 }
 
 // s_loc[j] = s[el_id[j]]: the SIMP factors in block-local element order (once

@@ -58,10 +58,11 @@ int validate(const to_mesh_desc *d) {
     if (f < 0 || f >= d->n_node * d->dim || (i > 0 && f <= d->fixed_dof[i - 1])) { set_error("fixed_dof not ascending / out of range"); return TO_EMESH; }
     if (hang[f / d->dim]) { set_error("fixed DOF %lld is on a hanging node", (long long)f); return TO_EMESH; }
   }
-  if ((d->options & ~(uint32_t)(TO_UPLOAD_GENERAL | TO_UPLOAD_PERSISTENT)) != 0 || d->reserved != 0) {
+  if ((d->options & ~(uint32_t)(TO_UPLOAD_GENERAL | TO_UPLOAD_PERSISTENT)) != 0) {
     set_error("unknown upload option bits 0x%x", d->options);
     return TO_EINVAL;
   }
+  if (d->n_owned < 0 || d->n_owned > d->n_node) { set_error("n_owned outside [0, n_node]"); return TO_EINVAL; }
   if (d->rmin > 0.0) {
     if (!d->filt_ptr || !d->filt_idx) { set_error("rmin > 0 but no filter lists"); return TO_EINVAL; }
     if (d->filt_ptr[0] != 0 || d->filt_ptr[d->n_elem] != d->filt_nnz) { set_error("bad filt_ptr"); return TO_EMESH; }
@@ -327,10 +328,10 @@ int setup_two_pass(const to_mesh_desc *d, cudaStream_t st, to_mesh *m) {
 int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_hang, const std::vector<int64_t> &iptr,
                      const std::vector<uint32_t> &inc, cudaStream_t st, to_mesh *m) {
   const int nc = 1 << d->dim;
-  const int64_t N = d->n_node;
+  const int64_t N = m->n_owned;   // blocks cover the owned nodes (all, unless a shard's local mesh)
   const int own_target = d->dim == 3 ? kGfOwnTarget3 : kGfOwnTarget2;
   const int el_max = std::min(kGfElMax, (1 << 14) / nc - 1), loc_max = kGfMaxLoc;   // (incidence encoding: le * 2^dim < 2^14)
-  std::vector<int32_t> el_mark(d->n_elem, -1), nd_mark(N, -1), el_le(d->n_elem, 0), nd_slot(N, 0);
+  std::vector<int32_t> el_mark(d->n_elem, -1), nd_mark(d->n_node, -1), el_le(d->n_elem, 0), nd_slot(d->n_node, 0);
   int stamp = 0;
   auto elem_of = [&](uint32_t t) { return (int64_t)((t & 0x3fffffffu) / (uint32_t)nc); };
   auto fits = [&](int64_t a, int64_t b) {
@@ -606,7 +607,8 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
   if (build_K0_hadamard_sym(m->KH, &m->KS) != 0) { set_error("Hadamard coefficient classes check failed"); return TO_EINVAL; }
   m->n_int = m->n_dof;
   // TO_UPLOAD_GENERAL keeps uniform H8 meshes on the general path
-  m->force_general = (d->options & TO_UPLOAD_GENERAL) != 0;
+  m->force_general = (d->options & TO_UPLOAD_GENERAL) != 0 || d->n_owned > 0;
+  m->n_owned = d->n_owned > 0 ? d->n_owned : d->n_node;
   RC(setup_structured(d, free_dof, st, m));
   // (the structured path filters with a lattice stencil and needs no lists)
   if ((m->filt_nnz > 0 || d->rmin > 0.0) && !m->structured) {
@@ -827,8 +829,9 @@ int op_cg_gen_step(to_mesh *m, int k, double rtol, cudaStream_t st) {
 // General path, x_N and the final residual after N iterations.
 int op_final_gen(to_mesh *m, int n_iter, double rtol, cudaStream_t st) {
   const int o = (n_iter + 1) & 1;
-  k_final_gen<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->rb[o], m->qb[o], m->pb[o], m->dinv, m->x,
-                                                    m->partials, m->S, n_iter, rtol, m->hist);
+  k_final_gen<false><<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->rb[o], m->qb[o], m->pb[o], m->dinv,
+                                                           m->x, m->partials, m->S, n_iter, rtol, m->hist,
+                                                           ShardComm{}, 0ull);
   m->last_launches++;
   return check_launch();
 }

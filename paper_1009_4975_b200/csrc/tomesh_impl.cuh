@@ -38,6 +38,7 @@ struct to_mesh {
   int dim = 0, L = 0, device = 0;
   double h0 = 1.0, hL = 1.0, E0 = 1.0, Emin = 1e-9, nu = 0.3, rmin = 0.0;
   int64_t n_el = 0, n_node = 0, n_dof = 0, n_hang = 0, n_fixed = 0, filt_nnz = 0;
+  int64_t n_owned = 0;   // nodes [0, n_owned) are this handle's (n_node unless a general shard's local mesh)
   int64_t n_int = 0;   // length of the internal CG vectors (n_dof, or padded rows when structured)
   std::vector<DevBuf> bufs;
   int64_t dev_bytes = 0;
@@ -125,6 +126,8 @@ struct to_mesh {
   const int4 *shard_plan = nullptr;    // K1 grid over the owned planes
   int shard_ncta = 0;
   uint8_t *own_dof = nullptr;          // canonical DOF on an owned plane (compliance partial)
+  bool gshard = false;                 // general-path shard group member (to_gshard_attach)
+  GShardComm GS{};
   int last_launches = 0;
   int matvec_variant = 0;
   int64_t launches_total = 0;          // every kernel launched on this handle
@@ -294,5 +297,6 @@ int op_apply(to_mesh *m, const double *in, double *out, cudaStream_t st);
 int op_recover_out(to_mesh *m, const double *v_int, double *u_canon, cudaStream_t st);
 int op_resid2_x(to_mesh *m, double *r2, cudaStream_t st);
 int plan_s3(to_mesh *m, cudaStream_t st, int z0, int z1, bool force, const int4 **plan_out, int *ncta_out);
+int op_cg_gen(to_mesh *m, int k, double rtol, cudaStream_t st);
 // sharded handles (tomesh_shard.cu)
 int shard_compliance_partial(to_mesh *m, const double *u_dev, double *out, cudaStream_t st);

@@ -14,6 +14,8 @@
 #include "kernels_cg.cuh"
 #include "kernels_shard.cuh"
 #include "kernels_struct3d.cuh"
+#include "kernels_genfused.cuh"
+#include "kernels_gshard.cuh"
 
 using namespace tomesh;
 
@@ -93,10 +95,11 @@ int check_group(to_mesh *const *ms, int n) {
 extern "C" int to_shard_buffers(to_mesh *m, to_shard_bufs *out, void *cuda_stream) {
   clear_error();
   if (!m || !out) { set_error("NULL argument"); return TO_EINVAL; }
-  if (!m->structured) { set_error("sharding needs the structured path (uniform H8 box)"); return TO_EINVAL; }
+  if (!m->structured && !m->gen_fused) { set_error("sharding needs the structured or the general single-kernel path"); return TO_EINVAL; }
   CK(cudaSetDevice(m->device));
   RC(ensure_shard_mem(m, (cudaStream_t)cuda_stream));
   std::memset(out, 0, sizeof(*out));
+  out->dinv = m->dinv;
   for (int w = 0; w < 2; ++w) {
     out->rb[w] = m->rb[w];
     out->pb[w] = m->pb[w];
@@ -105,10 +108,12 @@ extern "C" int to_shard_buffers(to_mesh *m, to_shard_bufs *out, void *cuda_strea
   out->x = m->x;
   out->slots = m->shard_slots;
   out->flags = m->shard_flags;
-  out->nx = m->G.NX;
-  out->ny = m->G.NY;
-  out->nz = m->G.NZ;
-  out->plane_doubles = plane_doubles(m);
+  if (m->structured) {
+    out->nx = m->G.NX;
+    out->ny = m->G.NY;
+    out->nz = m->G.NZ;
+    out->plane_doubles = plane_doubles(m);
+  }
   return 0;
 }
 
@@ -228,11 +233,16 @@ int shard_compliance_partial(to_mesh *m, const double *u_dev, double *out, cudaS
   return 0;
 }
 
+int gshard_solve_group(to_mesh *const *ms, int32_t n, double penal, const double *const *x_dev,
+                       double *const *u_dev, double rtol, int32_t max_iter, uint32_t flags, to_cg_stats *st_out,
+                       void *const *streams);
+
 extern "C" int tosolve_cg_group(to_mesh *const *ms, int32_t n, double penal, const double *const *x_dev,
                                 double *const *u_dev, double rtol, int32_t max_iter, uint32_t flags,
                                 to_cg_stats *st_out, void *const *streams) {
   clear_error();
   RC(check_group(ms, n));
+  if (ms[0]->gshard) return gshard_solve_group(ms, n, penal, x_dev, u_dev, rtol, max_iter, flags, st_out, streams);
   if (!x_dev || !u_dev || !streams) { set_error("NULL argument"); return TO_EINVAL; }
   for (int i = 0; i < n; ++i)
     if (!x_dev[i] || !u_dev[i]) { set_error("NULL density or output of handle %d", i); return TO_EINVAL; }
@@ -439,4 +449,279 @@ extern "C" int to_ipc_close(int device, void *base_ptr) {
   CK(cudaSetDevice(device));
   CK(cudaIpcCloseMemHandle(base_ptr));
   return 0;
+}
+
+// ---- Morton node-range sharding of the general path (kernels_gshard.cuh) --------------
+
+__global__ void k_own_nodes(int64_t n_dof, int64_t owned_dofs, uint8_t *__restrict__ own) {
+  GRID_STRIDE(i, n_dof) { own[i] = i < owned_dofs ? 1 : 0; }
+}
+
+extern "C" int to_gshard_attach(to_mesh *m, int32_t rank, int32_t nranks, const to_shard_bufs *peers, int64_t n_send,
+                                const int32_t *send_rank, const int32_t *send_local, const int32_t *send_remote,
+                                void *cuda_stream) {
+  clear_error();
+  if (!m || !peers || n_send < 0 || (n_send > 0 && (!send_rank || !send_local || !send_remote))) {
+    set_error("NULL argument");
+    return TO_EINVAL;
+  }
+  if (!m->gen_fused || m->structured) { set_error("to_gshard_attach needs a general-path handle"); return TO_EINVAL; }
+  if (nranks < 1 || nranks > kShardMax || rank < 0 || rank >= nranks) {
+    set_error("rank %d of %d outside [0, %d)", rank, nranks, kShardMax);
+    return TO_EINVAL;
+  }
+  for (int64_t i = 0; i < n_send; ++i) {
+    const int s = send_rank[i];
+    if (s < 0 || s >= nranks || s == rank) { set_error("send entry %lld: bad rank %d", (long long)i, s); return TO_EINVAL; }
+    if (send_local[i] < 0 || send_local[i] >= m->n_owned) { set_error("send entry %lld: not an owned node", (long long)i); return TO_EINVAL; }
+    if (send_remote[i] < 0) { set_error("send entry %lld: bad remote node", (long long)i); return TO_EINVAL; }
+  }
+  for (int r = 0; r < nranks; ++r) {
+    const to_shard_bufs &p = peers[r];
+    if (!p.slots || !p.flags || !p.x || !p.dinv || !p.rb[0] || !p.rb[1] || !p.pb[0] || !p.pb[1] || !p.qb[0] ||
+        !p.qb[1] || p.nx != 0) {
+      set_error("peer %d: missing buffers or not a general handle", r);
+      return TO_EINVAL;
+    }
+  }
+  CK(cudaSetDevice(m->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  RC(ensure_shard_mem(m, st));
+  if (peers[rank].x != m->x || peers[rank].slots != m->shard_slots) { set_error("peers[rank] is not this handle"); return TO_EINVAL; }
+  GShardComm G{};
+  G.C.rank = rank;
+  G.C.nranks = nranks;
+  for (int r = 0; r < nranks; ++r) {
+    G.C.slots[r] = peers[r].slots;
+    G.C.flags[r] = peers[r].flags;
+    for (int w = 0; w < 2; ++w) {
+      G.peer_r[w][r] = peers[r].rb[w];
+      G.peer_p[w][r] = peers[r].pb[w];
+      G.peer_q[w][r] = peers[r].qb[w];
+    }
+    G.peer_x[r] = peers[r].x;
+    G.peer_d[r] = peers[r].dinv;
+  }
+  G.C.my_slots = m->shard_slots;
+  G.C.my_flags = m->shard_flags;
+  // peer access for groups spread over several GPUs of one process
+  for (int r = 0; r < nranks; ++r) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, peers[r].slots) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (at.type == cudaMemoryTypeDevice && at.device != m->device) {
+      int can = 0;
+      CK(cudaDeviceCanAccessPeer(&can, m->device, at.device));
+      if (!can) { set_error("device %d cannot access peer device %d", m->device, at.device); return TO_ECUDA; }
+      const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+      cudaGetLastError();
+    }
+  }
+  int32_t *d_rank = nullptr, *d_loc = nullptr, *d_rem = nullptr;
+  RC(upload_array(m, &d_rank, send_rank, (size_t)n_send, st));
+  RC(upload_array(m, &d_loc, send_local, (size_t)n_send, st));
+  RC(upload_array(m, &d_rem, send_remote, (size_t)n_send, st));
+  G.n_send = n_send;
+  G.send_rank = d_rank;
+  G.send_local = d_loc;
+  G.send_remote = d_rem;
+  if (!m->own_dof) RC(m->alloc(&m->own_dof, (size_t)m->n_dof));
+  k_own_nodes<<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->n_owned * m->dim, m->own_dof);
+  RC(check_launch());
+  CK(cudaMemsetAsync(m->shard_flags, 0, sizeof(unsigned long long) * kShardBanks * kShardMax, st));
+  CK(cudaStreamSynchronize(st));
+  m->GS = G;
+  m->gshard = true;
+  m->sharded = true;
+  m->shard_seq = 1;
+  m->tail_seq = 1;
+  return 0;
+}
+
+template <int MODE>
+int launch_gxchg(to_mesh *m, const double *a, const double *b, const double *c, int w, unsigned long long seq,
+                 cudaStream_t st) {
+  const int g = grid_for(std::max<int64_t>(1, m->GS.n_send));
+  if (m->dim == 2)
+    k_gshard_xchg<2, MODE><<<g, 256, 0, st>>>(m->GS, a, b, c, w, m->partials, m->GB.n_blk, m->S, seq);
+  else
+    k_gshard_xchg<3, MODE><<<g, 256, 0, st>>>(m->GS, a, b, c, w, m->partials, m->GB.n_blk, m->S, seq);
+  m->last_launches++;
+  return check_launch();
+}
+
+// The general-path group solve (one handle per rank; n of them in lockstep in
+// this process, or 1 per process).  Same device-side protocol as the slabs:
+// iteration collectives on the sequence-parity banks, the setup / final / x
+// collectives on the tail banks.
+int gshard_solve_group(to_mesh *const *ms, int32_t n, double penal, const double *const *x_dev,
+                       double *const *u_dev, double rtol, int32_t max_iter, uint32_t flags, to_cg_stats *st_out,
+                       void *const *streams) {
+  if (!x_dev || !u_dev || !streams) { set_error("NULL argument"); return TO_EINVAL; }
+  for (int i = 0; i < n; ++i) {
+    if (!ms[i]->gshard) { set_error("handle %d is not an attached general handle", i); return TO_EINVAL; }
+    if (!x_dev[i] || !u_dev[i]) { set_error("NULL density or output of handle %d", i); return TO_EINVAL; }
+  }
+  if (!(penal > 0.0)) { set_error("penal must be > 0"); return TO_EINVAL; }
+  if (max_iter < 0) { set_error("max_iter < 0"); return TO_EINVAL; }
+  if (flags & (TO_WARM | TO_PROFILE)) { set_error("TO_WARM / TO_PROFILE are not supported on sharded handles"); return TO_EINVAL; }
+  const bool fixed = (flags & TO_FIXED_ITERS) != 0;
+  const bool hist = (flags & TO_HISTORY) != 0;
+  auto S_ = [&](int i) { return (cudaStream_t)streams[i]; };
+  for (int i = 0; i < n; ++i) {
+    to_mesh *m = ms[i];
+    CK(cudaSetDevice(m->device));
+    m->last_launches = 0;
+    if (hist && max_iter > m->hist_cap) {
+      RC(m->alloc(&m->hist, (size_t)max_iter));
+      m->hist_cap = max_iter;
+    }
+    CK(cudaEventRecord(m->ev0, S_(i)));
+    RC(reset_scalars(m, max_iter, fixed, hist, S_(i)));
+    RC(op_scale_and_diag(m, penal, x_dev[i], nullptr, S_(i)));
+    RC(op_rhs(m, m->rb[1], S_(i)));              // r0 = b (owned rows exact; ghosts come from their owners)
+    CK(cudaMemsetAsync(m->x, 0, sizeof(double) * m->n_int, S_(i)));
+    CK(cudaMemsetAsync(m->qb[1], 0, sizeof(double) * m->n_int, S_(i)));
+    CK(cudaMemsetAsync(m->pb[1], 0, sizeof(double) * m->n_int, S_(i)));
+    const int64_t n_own = m->n_owned * m->dim;
+    k_norm2_b<<<grid_for(n_own), kBlock, 0, S_(i)>>>(n_own, m->rb[1], m->partials, m->S);   // this rank's ||b||^2
+    m->last_launches++;
+    RC(check_launch());
+    RC(launch_gxchg<GX_BARRIER>(m, nullptr, nullptr, nullptr, 0, kShardTail | m->tail_seq, S_(i)));
+  }
+  for (int i = 0; i < n; ++i) {   // every rank's local Dinv and b are written ...
+    to_mesh *m = ms[i];
+    CK(cudaSetDevice(m->device));
+    k_shard_wait<<<1, 32, 0, S_(i)>>>(m->GS.C, kShardTail | m->tail_seq, m->S);
+    m->tail_seq++;
+    m->last_launches++;
+    RC(check_launch());
+    // ... before the owners store theirs into the ghosts
+    RC(launch_gxchg<GX_SETUP>(m, m->dinv, m->rb[1], nullptr, 0, kShardTail | m->tail_seq, S_(i)));
+  }
+  for (int i = 0; i < n; ++i) {
+    to_mesh *m = ms[i];
+    CK(cudaSetDevice(m->device));
+    k_shard_set_bnorm<<<1, 32, 0, S_(i)>>>(m->GS.C, kShardTail | m->tail_seq, m->S);
+    m->tail_seq++;
+    m->last_launches++;
+    RC(check_launch());
+  }
+  const bool loop_prof = (flags & TO_PROFILE_LOOP) != 0;
+  if (loop_prof)
+    for (int i = 0; i < n; ++i) {
+      CK(cudaSetDevice(ms[i]->device));
+      for (auto &e : ms[i]->loop_ev)
+        if (!e) CK(cudaEventCreate(&e));
+      CK(cudaEventRecord(ms[i]->loop_ev[0], S_(i)));
+    }
+  int launched = 0, chunk = fixed ? std::max(1, max_iter) : 16;
+  bool stop = false;
+  while (!stop && launched < max_iter) {
+    const int cnt = std::min(chunk, max_iter - launched);
+    for (int k = 0; k < cnt; ++k) {
+      const int kk = launched + k, w = kk & 1;
+      // every rank's push before any rank's gather in launch order (the
+      // handles of one process may share a stream)
+      for (int i = 0; i < n; ++i) {
+        to_mesh *m = ms[i];
+        CK(cudaSetDevice(m->device));
+        RC(op_cg_gen(m, kk, rtol, S_(i)));
+        RC(launch_gxchg<GX_ITER>(m, m->rb[w], m->pb[w], m->qb[w], w, m->shard_seq, S_(i)));
+      }
+      for (int i = 0; i < n; ++i) {
+        to_mesh *m = ms[i];
+        CK(cudaSetDevice(m->device));
+        k_shard_step<<<1, 32, 0, S_(i)>>>(m->GS.C, m->shard_seq, m->S, kk, rtol, m->hist);
+        m->shard_seq++;
+        m->last_launches++;
+      }
+    }
+    RC(check_launch());
+    launched += cnt;
+    if (!fixed) {
+      int done = -1;
+      for (int i = 0; i < n; ++i) {
+        CK(cudaSetDevice(ms[i]->device));
+        RC(read_scalars(ms[i], S_(i)));
+        const int d = (ms[i]->S_host->done || ms[i]->S_host->done_next) ? 1 : 0;
+        if (done >= 0 && d != done) { set_error("sharded solve: ranks disagree on the stop test"); return TO_ECUDA; }
+        done = d;
+      }
+      stop = done == 1;
+      chunk = std::min(chunk * 2, 256);
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    to_mesh *m = ms[i];
+    CK(cudaSetDevice(m->device));
+    if (loop_prof) CK(cudaEventRecord(m->loop_ev[1], S_(i)));
+    const int o = (max_iter + 1) & 1;
+    const int64_t n_own = m->n_owned * m->dim;
+    k_final_gen<true><<<grid_for(n_own), kBlock, 0, S_(i)>>>(n_own, m->rb[o], m->qb[o], m->pb[o], m->dinv, m->x,
+                                                             m->partials, m->S, max_iter, rtol, m->hist, m->GS.C,
+                                                             kShardTail | m->tail_seq);
+    m->last_launches++;
+    RC(check_launch());
+  }
+  for (int i = 0; i < n; ++i) {
+    to_mesh *m = ms[i];
+    CK(cudaSetDevice(m->device));
+    k_shard_final<<<1, 32, 0, S_(i)>>>(m->GS.C, kShardTail | m->tail_seq, m->S, max_iter, rtol, m->hist);
+    m->tail_seq++;
+    m->last_launches++;
+    RC(check_launch());
+  }
+  // the ghosts of x (sensitivities of every local element)
+  for (int i = 0; i < n; ++i) {
+    to_mesh *m = ms[i];
+    CK(cudaSetDevice(m->device));
+    RC(launch_gxchg<GX_X>(m, m->x, nullptr, nullptr, 0, kShardTail | m->tail_seq, S_(i)));
+  }
+  for (int i = 0; i < n; ++i) {
+    to_mesh *m = ms[i];
+    CK(cudaSetDevice(m->device));
+    k_shard_wait<<<1, 32, 0, S_(i)>>>(m->GS.C, kShardTail | m->tail_seq, m->S);
+    m->tail_seq++;
+    m->last_launches++;
+    RC(check_launch());
+    RC(op_recover_out(m, m->x, u_dev[i], S_(i)));
+    CK(cudaEventRecord(m->ev1, S_(i)));
+  }
+  int rc_all = 0;
+  for (int i = 0; i < n; ++i) {
+    to_mesh *m = ms[i];
+    CK(cudaSetDevice(m->device));
+    CK(cudaStreamSynchronize(S_(i)));
+    RC(read_scalars(m, S_(i)));
+    const CgScalars res = *m->S_host;
+    float ms_ = 0.f;
+    CK(cudaEventElapsedTime(&ms_, m->ev0, m->ev1));
+    if (loop_prof) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, m->loop_ev[0], m->loop_ev[1]));
+      for (int j = 0; j < 4; ++j) m->prof_ms[j] = 0.0;
+      m->prof_ms[4] = std::min(launched, res.iter);
+      m->prof_ms[5] = t;
+    }
+    m->hist_len = hist ? res.iter : 0;
+    m->launches_total += m->last_launches;
+    int rc = res.status;
+    if (rc == 0 && !fixed && !(res.rr <= res.thresh2) && res.bnorm2 > 0.0) rc = TO_NOT_CONVERGED;
+    if (st_out) {
+      st_out[i].iters = res.iter;
+      st_out[i].status = rc;
+      st_out[i].relres = res.bnorm2 > 0.0 ? std::sqrt(res.rr / res.bnorm2) : 0.0;
+      st_out[i].relres_true = -1.0;
+      st_out[i].ms = ms_;
+      st_out[i].bnorm = std::sqrt(res.bnorm2);
+    }
+    if (rc < 0 && rc_all >= 0) rc_all = rc;
+    else if (rc > 0 && rc_all == 0) rc_all = rc;
+  }
+  if (rc_all < 0) set_error("sharded solve failed (status %d)", rc_all);
+  return rc_all;
 }

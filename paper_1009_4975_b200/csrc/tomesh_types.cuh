@@ -96,6 +96,16 @@ struct ShardComm {
   unsigned long long *my_flags;
 };
 
+// Morton node-range sharding of the general path (kernels_gshard.cuh): the
+// collectives' ShardComm plus the ghost-store list and the peers' vectors.
+struct GShardComm {
+  ShardComm C;                                     // rank, nranks, slots / flags of every rank
+  int64_t n_send;
+  const int32_t *send_rank, *send_local, *send_remote;
+  double *peer_r[2][kShardMax], *peer_p[2][kShardMax], *peer_q[2][kShardMax];
+  double *peer_x[kShardMax], *peer_d[kShardMax];
+};
+
 // One offset of the uniform-box filter stencil (k_filter_s3).
 struct S3FilterOffset {
   int di, dj, dk;
