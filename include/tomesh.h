@@ -132,12 +132,11 @@ typedef struct {
  *   TO_UPLOAD_GENERAL        keep a uniform H8 box on the general (canonical
  *                            Morton order) path instead of the structured
  *                            one; tosolve_minres with TO_PC_IC0 needs it.
- *   TO_UPLOAD_PERSISTENT     2D meshes up to 100k elements: run the whole PCG
- *                            loop in one cooperative kernel (round 1's path
- *                            for small meshes; the default one kernel per
- *                            iteration is faster: c1 6.9 vs 8.0, c2 9.0 vs
- *                            16.2 us per iteration). */
-enum { TO_UPLOAD_GENERAL = 1, TO_UPLOAD_PERSISTENT = 2 };
+ *   TO_UPLOAD_LAUNCHED       general path: launch one kernel per PCG iteration
+ *                            even for the smallest meshes (by default a mesh
+ *                            of at most 32 operator blocks, e.g. c1, runs the
+ *                            whole loop in one cooperative kernel). */
+enum { TO_UPLOAD_GENERAL = 1, TO_UPLOAD_LAUNCHED = 2 };
 
 typedef struct {
   int32_t iters;               /* CG iterations performed                        */

@@ -177,30 +177,6 @@ static __global__ void k_sub_masked(int64_t n, const double *__restrict__ q, con
   GRID_STRIDE(i, n) { r[i] = free_dof[i] ? r[i] - q[i] : 0.0; }
 }
 
-// General path K2 (per-DOF Dinv).  INIT: rho0, rr0 only.
-template <bool INIT>
-__global__ void k_rupd(int64_t n, const double *__restrict__ q, const double *__restrict__ Dinv,
-                       double *__restrict__ r, double *partials, CgScalars *S, double *hist, double rtol) {
-  if (!INIT && cg_stopped(S)) return;
-  const double alpha = INIT ? 0.0 : __ldcg(&S->alpha);
-  double acc[2] = {0.0, 0.0};
-  GRID_STRIDE(i, n) {
-    const double di = Dinv[i];
-    double ri = r[i];
-    if (!INIT) {
-      if (di != 0.0) ri = fma(-alpha, q[i], ri);
-      r[i] = ri;
-    }
-    acc[0] = fma(ri, di * ri, acc[0]);
-    acc[1] = fma(ri, ri, acc[1]);
-  }
-  if (INIT) {
-    if (grid_sum<2>(acc, partials, &S->counter[CNT_INIT])) cg_init_scalars(S, acc[0], acc[1], rtol);
-  } else {
-    if (grid_sum<2>(acc, partials, &S->counter[CNT_U1])) cg_after_rupdate(S, acc[0], acc[1], hist);
-  }
-}
-
 // sum over free DOFs of (b - t)^2 -> S->tmp[0]
 static __global__ void k_resid2(int64_t n, const double *__restrict__ b, const double *__restrict__ t,
                          const uint8_t *__restrict__ free_dof, double *partials, CgScalars *S) {

@@ -4,10 +4,7 @@
 //   k_simp        a1  s_e = (E_min + x_e^p (E0 - E_min)) h_e^(d-2)       (Eq. 2)
 //   k_diag_*      a2  D = diag(Pi_F C^T K C Pi_F) (cross terms included)  (:515-521)
 //   k_rhs         a3  b = Pi_F C^T f                                      (Eq. 7 rhs)
-//   k_cg_general_persistent  a4-a7  the whole PCG loop in one cooperative
-//                                    kernel (opt-in for small 2D meshes; the
-//                                    default iteration is k_gen_fused,
-//                                    kernels_genfused.cuh)                  (Eq. 8)
+//   (one PCG iteration, a4-a7: kernels_genfused.cuh)                        (Eq. 8)
 //   k_recover     a8  u = C u_hat                                         (Eq. 9)
 //   k_sens        a10 dc_e = -p x^(p-1)(E0-Emin) h^(d-2) u_e^T K0 u_e    (:343-346)
 //   k_filter      a11 Eq. 5 / density variant                             (:613-616)
@@ -306,210 +303,9 @@ __device__ __forceinline__ void had_apply(const K0Had3 &H, double (&x)[24], doub
   for (int a = 0; a < 24; ++a) y[a] = x[a];
 }
 
-// ---- the persistent solver's iteration = element pass + node pass ------------------------
-// Deterministic and atomic-free (the paper's operator, Eq. 8, assembled on
-// the fly): the element pass stores y_e = s_e K0 (C_e p)_e per element; the
-// node pass sums, for each node, the (element, corner, weight) incidences of
-// the precomputed CSR (weights 1, or the hanging-node interpolation weights of
-// Eq. 6 for the parents of a hanging corner), i.e. q = C^T K C p.
+// ---- grid-wide sums inside a cooperative kernel ---------------------------------------
 enum { G_PLAIN = 0, G_CG = 1 };
 
-// Loads of vectors the same kernel may have written (persistent solver): a
-// plain cached global load (ld.global.ca: the grid barrier's acquire makes
-// the other blocks' writes visible; the non-coherent read-only path must not
-// be used for them); otherwise the read-only path.
-template <bool COH>
-__device__ __forceinline__ double g_ld(const double *p) {
-  if (!COH) return __ldg(p);
-  double v;
-  asm volatile("ld.global.ca.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// L1-cached 16-byte load for data written earlier in the same (persistent)
-// kernel by other blocks: coherent because every grid barrier executes a
-// gpu-scope fence, which invalidates the SM's L1 (B300_MICROARCH.md, L1D).
-__device__ __forceinline__ double2 g_ld2_ca(const double2 *p) {
-  double2 v;
-  asm volatile("ld.global.ca.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
-  return v;
-}
-
-// Node record of the general-path CG: zp[n] = {z_k = Dinv r_k (DIM), p_{k-1}
-// (DIM)}, written by the node pass, so that a corner gather is one contiguous
-// 16*DIM-byte record instead of separate r, Dinv and p loads.
-// p of node n (all DIM components): CG: z_k + beta p_{k-1} (formed on the fly;
-// the node pass forms the same value); plain: v.
-template <int DIM, int MODE, bool COH>
-__device__ __forceinline__ void g_pnode(const double *__restrict__ zp, const double *__restrict__ v, double beta,
-                                        int64_t n, double (&out)[DIM]) {
-  if (MODE == G_PLAIN) {
-#pragma unroll
-    for (int i = 0; i < DIM; ++i) out[i] = g_ld<COH>(v + n * DIM + i);
-    return;
-  }
-  const double2 *rec = reinterpret_cast<const double2 *>(zp + n * 2 * DIM);
-  double t[2 * DIM];
-#pragma unroll
-  for (int h = 0; h < DIM; ++h) {
-    const double2 w = COH ? g_ld2_ca(rec + h) : __ldg(rec + h);
-    t[2 * h] = w.x;
-    t[2 * h + 1] = w.y;
-  }
-#pragma unroll
-  for (int i = 0; i < DIM; ++i) out[i] = fma(beta, t[DIM + i], t[i]);
-}
-
-// One element of the element pass: y_e = s_e K0 C_e p into ye; returns
-// s_e pbar^T K0 pbar (its share of p^T A p).
-template <int DIM, int MODE, bool COH>
-__device__ __forceinline__ double g_elem_one(const MeshView &M, int64_t e, const double *__restrict__ s,
-                                             const double *__restrict__ zp, const double *__restrict__ po,
-                                             double *__restrict__ ye,
-                                             const K0Dense2 &K2, const K0HadSym &H, const uint8_t *__restrict__ hmask,
-                                             double beta) {
-  constexpr int NC = 1 << DIM, ND = DIM * NC;
-  // corner nodes in one or two 16-byte loads; hmask (bit c: corner c is a
-  // hanging node) avoids the dependent node_hang lookups on most elements
-  int node[NC];
-#pragma unroll
-  for (int h = 0; h < NC / 4; ++h) {
-    const int4 t = __ldg(reinterpret_cast<const int4 *>(M.elem_node + e * NC) + h);
-    node[4 * h] = t.x;
-    node[4 * h + 1] = t.y;
-    node[4 * h + 2] = t.z;
-    node[4 * h + 3] = t.w;
-  }
-  const unsigned hm = hmask[e];
-  // all corners unconditionally (branch-free, so all the gathers are in
-  // flight together); hanging corners (rare) are then replaced by the Eq. 6
-  // interpolation of their parents
-  double y[ND];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    double t[DIM];
-    g_pnode<DIM, MODE, COH>(zp, po, beta, node[c], t);
-#pragma unroll
-    for (int i = 0; i < DIM; ++i) y[DIM * c + i] = t[i];
-  }
-  if (hm) {
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      if (!((hm >> c) & 1)) continue;
-      const int h = M.node_hang[node[c]];
-      double acc[DIM];
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) acc[i] = 0.0;
-      for (int k = M.hang_ptr[h]; k < M.hang_ptr[h + 1]; ++k) {
-        const double w = M.hang_weight[k];
-        double t[DIM];
-        g_pnode<DIM, MODE, COH>(zp, po, beta, M.hang_parent[k], t);
-#pragma unroll
-        for (int i = 0; i < DIM; ++i) acc[i] = fma(w, t[i], acc[i]);
-      }
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) y[DIM * c + i] = acc[i];
-    }
-  }
-  const double se = __ldg(s + e);
-  double en = 0.0;
-  if constexpr (DIM == 3) {
-    wht8x3(y);
-    had_mid_inplace_energy(H, y, en);
-    wht8x3(y);
-  } else {
-    double t[ND];
-    dense_apply<ND>(K2.K, y, t);
-#pragma unroll
-    for (int a = 0; a < ND; ++a) {
-      en = fma(y[a], t[a], en);
-      y[a] = t[a];
-    }
-  }
-  double2 *dst = reinterpret_cast<double2 *>(ye + e * ND);
-#pragma unroll
-  for (int a = 0; a < ND / 2; ++a) dst[a] = make_double2(se * y[2 * a], se * y[2 * a + 1]);
-  return se * en;
-}
-
-// One node of the node pass.  q_n = sum over the incidences of n of w *
-// y_e[corner] (packed entry: element*2^DIM + corner in bits 0-29, weight
-// code in bits 30-31: 0 -> 1, 1 -> 1/2, 2 -> 1/4).
-//   plain: q_out = q (all DOFs; the caller masks);
-//   CG (iteration k, alpha_k known): on free DOFs p_k = Dinv r_k + beta p_{k-1}
-//   (stored in place), x += alpha_k p_k, r -= alpha_k q; accumulates
-//   rho_{k+1} = r.Dinv r and rr into acc.
-template <int DIM, int MODE, bool COH>
-__device__ __forceinline__ void g_node_one(int64_t n, const int64_t *__restrict__ inc_ptr,
-                                           const uint32_t *__restrict__ inc, const double *__restrict__ ye,
-                                           double *__restrict__ r, const double *__restrict__ Dinv,
-                                           double *__restrict__ zp, double *__restrict__ x, double *__restrict__ q_out,
-                                           double alpha, double beta, double (&acc)[2]) {
-  double qv[DIM];
-#pragma unroll
-  for (int i = 0; i < DIM; ++i) qv[i] = 0.0;
-  const int64_t k1 = inc_ptr[n + 1];
-  // batches of 8 incidences: all index loads, then all element-vector loads
-  for (int64_t k0 = inc_ptr[n]; k0 < k1; k0 += 8) {
-    uint32_t t[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) t[j] = (k0 + j < k1) ? __ldg(&inc[k0 + j]) : 0xffffffffu;
-    double v[8][DIM];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const double *src = ye + (int64_t)(t[j] & 0x3fffffffu) * DIM;
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) v[j][i] = (t[j] != 0xffffffffu) ? g_ld<COH>(src + i) : 0.0;
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const double w = (t[j] >> 30) == 0 ? 1.0 : (t[j] >> 30) == 1 ? 0.5 : 0.25;
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) qv[i] = fma(w, v[j][i], qv[i]);
-    }
-  }
-  if (MODE == G_PLAIN) {
-#pragma unroll
-    for (int i = 0; i < DIM; ++i) q_out[n * DIM + i] = qv[i];
-    return;
-  }
-  // own record: z_k, p_{k-1} -> p_k; x += alpha p_k; r -= alpha q on free
-  // DOFs; new record {z_{k+1} = Dinv r_{k+1}, p_k}
-  double2 *rec = reinterpret_cast<double2 *>(zp + n * 2 * DIM);
-  double t[2 * DIM];
-#pragma unroll
-  for (int h = 0; h < DIM; ++h) {
-    const double2 w = COH ? __ldcg(rec + h) : rec[h];
-    t[2 * h] = w.x;
-    t[2 * h + 1] = w.y;
-  }
-#pragma unroll
-  for (int i = 0; i < DIM; ++i) {
-    const int64_t d = n * DIM + i;
-    const double di = __ldg(Dinv + d);
-    const double pk = fma(beta, t[DIM + i], t[i]);      // 0 on non-free DOFs (z = p = 0 there)
-    double zn = 0.0;
-    if (di != 0.0) {
-      x[d] = fma(alpha, pk, x[d]);
-      const double rn = fma(-alpha, qv[i], r[d]);
-      r[d] = rn;
-      zn = di * rn;
-      acc[0] = fma(rn, zn, acc[0]);
-      acc[1] = fma(rn, rn, acc[1]);
-    }
-    t[i] = zn;
-    t[DIM + i] = pk;
-  }
-#pragma unroll
-  for (int h = 0; h < DIM; ++h) rec[h] = make_double2(t[2 * h], t[2 * h + 1]);
-}
-
-// The whole general-path PCG loop in one cooperative (persistent) kernel:
-// per iteration an element pass, a grid barrier, the alpha reduction summed
-// by every block in the same order (identical values everywhere), a node
-// pass, a grid barrier, the beta reduction.  For the latency-bound AMR and
-// small meshes (c1, c2, c4) this removes the two launches and the host
-// polling per iteration.  Requires all blocks co-resident (cooperative launch).
 // Sum of the per-block partials, computed by warp 0 of every block in the same
 // fixed order (lane-strided partial sums, then the xor-shuffle tree) and
 // broadcast through shared memory: every block obtains bit-identical totals.
@@ -541,83 +337,6 @@ __device__ __forceinline__ void g_sum_partials(const double *part, int nb, doubl
 #pragma unroll
   for (int k = 0; k < NV; ++k) out[k] = bc[k];
   __syncthreads();
-}
-
-template <int DIM>
-__global__ void __launch_bounds__(256, 2) k_cg_general_persistent(
-    MeshView M, const double *__restrict__ s, double *__restrict__ r, const double *__restrict__ Dinv,
-    double *__restrict__ zp, double *__restrict__ x, double *__restrict__ ye, const int64_t *__restrict__ inc_ptr,
-    const uint32_t *__restrict__ inc, const __grid_constant__ K0Dense2 K2, const __grid_constant__ K0HadSym H,
-    const uint8_t *__restrict__ hmask, CgScalars *S, double *part_a, double *part_b, double *hist) {
-  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
-  const int nb = gridDim.x;
-  // scalars after the initial residual (k_rupd<true>), identical in every block
-  double rho = __ldcg(&S->rho), rr = __ldcg(&S->rr);
-  const double thresh2 = __ldcg(&S->thresh2), bnorm2 = __ldcg(&S->bnorm2);
-  const int max_iter = S->max_iter, fixed = S->fixed, history = S->history;
-  int status = __ldcg(&S->status);
-  bool done = __ldcg(&S->done) != 0;
-  double beta = 0.0;
-  int it = 0;
-  const int64_t tid0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)nb * blockDim.x;
-  while (!done && it < max_iter) {
-    double v1[1] = {0.0};
-    for (int64_t e = tid0; e < M.n_el; e += stride)
-      v1[0] += g_elem_one<DIM, G_CG, true>(M, e, s, zp, nullptr, ye, K2, H, hmask, beta);
-    block_sum<1>(v1);
-    if (threadIdx.x == 0) __stcg(&part_a[blockIdx.x], v1[0]);
-    grid.sync();
-    double tot1[1];
-    g_sum_partials<1>(part_a, nb, tot1);
-    const double pq = tot1[0];
-    if (!(pq > 0.0)) {
-      status = (pq != pq) ? -5 : -6;
-      break;
-    }
-    const double alpha = rho / pq;
-    double v2[2] = {0.0, 0.0};
-    for (int64_t n = tid0; n < M.n_node; n += stride)
-      g_node_one<DIM, G_CG, true>(n, inc_ptr, inc, ye, r, Dinv, zp, x, nullptr, alpha, beta, v2);
-    block_sum<2>(v2);
-    if (threadIdx.x == 0) {
-      __stcg(&part_b[2 * blockIdx.x], v2[0]);
-      __stcg(&part_b[2 * blockIdx.x + 1], v2[1]);
-    }
-    grid.sync();
-    double tot2[2];
-    g_sum_partials<2>(part_b, nb, tot2);
-    const double rz = tot2[0], rn = tot2[1];
-    ++it;
-    if (!(rz == rz) || !(rn == rn)) {
-      status = -5;
-      break;
-    }
-    beta = rz / rho;
-    rho = rz;
-    rr = rn;
-    if (history && hist && blockIdx.x == 0 && threadIdx.x == 0) hist[it - 1] = sqrt(rr / bnorm2);
-    if (!fixed && rr <= thresh2) done = true;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    S->iter = it;
-    S->rho = rho;
-    S->rr = rr;
-    S->beta = beta;
-    S->status = status;
-    S->done = 1;
-  }
-}
-
-// zp[n] = {Dinv r0, 0}: the record before the first general-path iteration.
-template <int DIM>
-__global__ void k_zp_init(int64_t n_node, const double *__restrict__ r, const double *__restrict__ Dinv,
-                          double *__restrict__ zp) {
-  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_node; n += (int64_t)gridDim.x * blockDim.x)
-#pragma unroll
-    for (int i = 0; i < DIM; ++i) {
-      zp[n * 2 * DIM + i] = Dinv[n * DIM + i] * r[n * DIM + i];
-      zp[n * 2 * DIM + DIM + i] = 0.0;
-    }
 }
 
 // ---- sensitivities (a10) ----------------------------------------------------------------

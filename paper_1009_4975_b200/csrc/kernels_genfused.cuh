@@ -36,6 +36,8 @@
 // PLAIN mode (operator-level calls, warm start, true residual, MINRES):
 // step 1 loads v, step 4 stores q = C^T K C v on the owned nodes, no dots.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "device_common.cuh"
 #include "element.h"
 #include "kernels_cg.cuh"
@@ -49,6 +51,7 @@ constexpr int kGfThreads = 256;
 constexpr int kGfOwnPerThread = 2;                       // owned nodes per thread (max_own <= 512)
 constexpr int kGfMaxOwn = kGfThreads * kGfOwnPerThread;
 constexpr int kGfMaxLoc = 1536;                          // local node slots per block (uint16 slots)
+constexpr int kGfPersistMaxBlocks = 32;                  // k_gen_persist only up to this many blocks
 #ifndef TOMESH_GF_OWN3
 #define TOMESH_GF_OWN3 224      // A/B on c4 / c4L: 224 < 320 < 448 < 512 (us per iteration)
 #endif
@@ -200,56 +203,76 @@ __device__ unsigned long long g_gf_trace[16384][8];
 
 __device__ __forceinline__ double gf_weight(unsigned code) { return code == 0 ? 1.0 : code == 1 ? 0.5 : 0.25; }
 
-template <int DIM, int MODE>
-__global__ void __launch_bounds__(kGfThreads, TOMESH_GF_MINB)
-k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_loc, const double *__restrict__ ro,
-            const double *__restrict__ qo, const double *__restrict__ po, const double *__restrict__ Dinv,
-            double *__restrict__ rw, double *__restrict__ pw, double *__restrict__ qw, double *__restrict__ x,
-            const __grid_constant__ K0Dense2 K2, const __grid_constant__ K0HadSym H, CgScalars *S,
-            double *partials, int kit, double rtol, double *hist) {
+// Shared-memory view of one block of the general path (its record, s_e, the
+// staging arrays) -- set up once per kernel.
+struct GfView {
+  GfMeta mt;
+  double *sl, *P, *Zs, *Ds, *Y;
+  unsigned long long *bar;
+  const int32_t *halo;
+  const ushort4 *virt;
+  const uint16_t *corner, *iptr, *inc;
+};
+template <int DIM>
+__device__ __forceinline__ GfView gf_view(const GenBlocks &B, const GfMeta &mt, unsigned char *gsm_raw, GfSections &sec) {
+  constexpr int CH = GfChunk<DIM>::CH, YS = GfChunk<DIM>::YS;
+  GfView V;
+  V.mt = mt;
+  sec = gf_sections<DIM>(mt.n_own, mt.n_halo, mt.n_virt, mt.n_el, mt.n_inc);
+  unsigned char *rec = gsm_raw;
+  V.sl = reinterpret_cast<double *>(gsm_raw + 16 * (size_t)B.max_rec16);
+  V.P = V.sl + ((B.max_el + 1) & ~1);
+  V.Zs = V.P + (size_t)B.max_loc * DIM;
+  V.Ds = V.Zs + (size_t)B.max_own * DIM;
+  V.Y = V.Ds + (size_t)B.max_own * DIM;
+  V.bar = reinterpret_cast<unsigned long long *>(V.Y + (size_t)CH * YS);
+  V.halo = reinterpret_cast<const int32_t *>(rec + sec.halo);
+  V.virt = reinterpret_cast<const ushort4 *>(rec + sec.virt);
+  V.corner = reinterpret_cast<const uint16_t *>(rec + sec.corner);
+  V.iptr = reinterpret_cast<const uint16_t *>(rec + sec.iptr);
+  V.inc = reinterpret_cast<const uint16_t *>(rec + sec.inc);
+  return V;
+}
+
+// Thread 0: issue the bulk copies of the block record and s_e (one mbarrier phase).
+template <int DIM>
+__device__ __forceinline__ void gf_issue_record(const GenBlocks &B, const GfView &V, const GfSections &sec,
+                                                const double *s_loc, unsigned char *gsm_raw) {
+  const unsigned s_bytes = 8u * (unsigned)((V.mt.n_el + 1) & ~1);
+  mbar_init(V.bar, 1);
+  fence_proxy_async();
+  mbar_arrive_expect_tx(V.bar, (unsigned)sec.total + s_bytes);
+  bulk_load_1d(gsm_raw, B.rec + V.mt.rec_off16, (unsigned)sec.total, V.bar);
+  if (s_bytes) bulk_load_1d(V.sl, s_loc + V.mt.el_off, s_bytes, V.bar);
+}
+
+// Loads of vectors another block may have written in the same kernel (the
+// persistent solver: after a grid barrier) go through L2; otherwise the
+// read-only path.
+template <bool COH>
+__device__ __forceinline__ double gf_ld(const double *p) { return COH ? __ldcg(p) : __ldg(p); }
+
+// One PCG iteration of one block (steps 1-4 of the header comment); the
+// block's dots (unreduced, per thread) in `dots`.  wait_rec: the record's
+// mbarrier phase is still outstanding (first iteration of the kernel).
+template <int DIM, int MODE, bool COH>
+__device__ __forceinline__ void gf_block_iter(const GfView &V, bool wait_rec, const double *__restrict__ ro,
+                                              const double *__restrict__ qo, const double *__restrict__ po,
+                                              const double *__restrict__ Dinv, double *__restrict__ rw,
+                                              double *__restrict__ pw, double *__restrict__ qw,
+                                              double *__restrict__ x, const K0Dense2 &K2, const K0HadSym &H,
+                                              double alpha, double beta, double (&dots)[5]) {
   constexpr bool CG = MODE == G_CG;
   constexpr int NC = 1 << DIM, ND = NC * DIM, CH = GfChunk<DIM>::CH, YS = GfChunk<DIM>::YS;
   constexpr int OPT = kGfOwnPerThread;
-  extern __shared__ __align__(16) unsigned char gsm_raw[];
   const int tid = threadIdx.x;
-  GF_MARK(0);
-  const GfMeta mt = B.meta[blockIdx.x];
+  const GfMeta &mt = V.mt;
   const int nOwn = mt.n_own, nHalo = mt.n_halo, nVirt = mt.n_virt, nE = mt.n_el;
-  const GfSections sec = gf_sections<DIM>(nOwn, nHalo, nVirt, nE, mt.n_inc);
-  GF_CHECK(sec.total <= 16 * B.max_rec16 && nE <= B.max_el && nOwn <= B.max_own && nOwn <= kGfMaxOwn);
-  GF_CHECK(nOwn + nHalo + nVirt <= B.max_loc && (mt.el_off & 1) == 0);
-  unsigned char *rec = gsm_raw;                                     // the block record
-  double *sl = reinterpret_cast<double *>(gsm_raw + 16 * (size_t)B.max_rec16);   // s_e of the elements
-  double *P = sl + ((B.max_el + 1) & ~1);                            // [max_loc][DIM] local node values
-  double *Zs = P + (size_t)B.max_loc * DIM;                          // [max_own][DIM] z_k of the owned DOFs
-  double *Ds = Zs + (size_t)B.max_own * DIM;                         // [max_own][DIM] Dinv of the owned DOFs
-  double *Y = Ds + (size_t)B.max_own * DIM;                          // [CH][YS] element results of a chunk
-  unsigned long long *bar = reinterpret_cast<unsigned long long *>(Y + (size_t)CH * YS);
-  const int32_t *halo = reinterpret_cast<const int32_t *>(rec + sec.halo);
-  const ushort4 *virt = reinterpret_cast<const ushort4 *>(rec + sec.virt);
-  const uint16_t *corner = reinterpret_cast<const uint16_t *>(rec + sec.corner);
-  const uint16_t *iptr = reinterpret_cast<const uint16_t *>(rec + sec.iptr);
-  const uint16_t *inc = reinterpret_cast<const uint16_t *>(rec + sec.inc);
-  // static block data and s_e (written before the first iteration's launch):
-  // one bulk copy each, issued before the wait on the previous iteration
-  const unsigned s_bytes = 8u * (unsigned)((nE + 1) & ~1);
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    fence_proxy_async();
-    mbar_arrive_expect_tx(bar, (unsigned)sec.total + s_bytes);
-    bulk_load_1d(rec, B.rec + mt.rec_off16, (unsigned)sec.total, bar);
-    if (s_bytes) bulk_load_1d(sl, s_loc + mt.el_off, s_bytes, bar);
-  }
-  __syncthreads();
-  pdl_wait();
-  pdl_release();
-  if (CG && cg_stopped(S)) {
-    mbar_wait(bar, 0);   // no bulk copy may still be writing when the CTA exits
-    return;
-  }
-  GF_MARK(1);
-  const double alpha = CG ? __ldcg(&S->alpha) : 0.0;
-  const double beta = CG ? __ldcg(&S->beta) : 0.0;
+  double *P = V.P, *Zs = V.Zs, *Ds = V.Ds, *Y = V.Y;
+  const double *sl = V.sl;
+  const int32_t *halo = V.halo;
+  const ushort4 *virt = V.virt;
+  const uint16_t *corner = V.corner, *iptr = V.iptr, *inc = V.inc;
   const int64_t g0 = (int64_t)mt.node0 * DIM;
   double rho = 0.0, rr = 0.0;
   // 1. owned nodes o = tid + u * kGfThreads (the same nodes as in step 4)
@@ -262,9 +285,9 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
       double r_o[DIM], q_o[DIM], p_o[DIM], d_o[DIM];
 #pragma unroll
       for (int i = 0; i < DIM; ++i) {
-        r_o[i] = __ldg(ro + g + i);
-        q_o[i] = __ldg(qo + g + i);
-        p_o[i] = __ldg(po + g + i);
+        r_o[i] = gf_ld<COH>(ro + g + i);
+        q_o[i] = gf_ld<COH>(qo + g + i);
+        p_o[i] = gf_ld<COH>(po + g + i);
         d_o[i] = __ldg(Dinv + g + i);
       }
 #pragma unroll
@@ -274,7 +297,7 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
         const double pn = fma(beta, p_o[i], z);
         rw[g + i] = rn;
         pw[g + i] = pn;
-        if (alpha != 0.0) x[g + i] = fma(alpha, p_o[i], x[g + i]);
+        if (alpha != 0.0) x[g + i] = fma(alpha, p_o[i], COH ? __ldcg(x + g + i) : x[g + i]);
         rho = fma(rn, z, rho);
         rr = fma(rn, rn, rr);
         P[o * DIM + i] = pn;
@@ -283,11 +306,11 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < DIM; ++i) P[o * DIM + i] = __ldg(po + g + i);
+      for (int i = 0; i < DIM; ++i) P[o * DIM + i] = gf_ld<COH>(po + g + i);
     }
   }
   GF_MARK(2);
-  mbar_wait(bar, 0);
+  if (wait_rec) mbar_wait(V.bar, 0);
   // ... and the halo nodes
 #pragma unroll 4
   for (int j = tid; j < nHalo * DIM; j += kGfThreads) {
@@ -296,10 +319,10 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
     const int64_t g = (int64_t)node * DIM + (j % DIM);
     double pn;
     if (CG) {
-      const double r_o = __ldg(ro + g), q_o = __ldg(qo + g), p_o = __ldg(po + g), d = __ldg(Dinv + g);
+      const double r_o = gf_ld<COH>(ro + g), q_o = gf_ld<COH>(qo + g), p_o = gf_ld<COH>(po + g), d = __ldg(Dinv + g);
       pn = fma(beta, p_o, d * fma(-alpha, q_o, r_o));
     } else {
-      pn = __ldg(po + g);
+      pn = gf_ld<COH>(po + g);
     }
     P[nOwn * DIM + j] = pn;
   }
@@ -411,15 +434,51 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
       }
     }
   }
+  dots[0] = rho;
+  dots[1] = rr;
+  dots[2] = pq;
+  dots[3] = qz;
+  dots[4] = qdq;
+}
+
+template <int DIM, int MODE>
+__global__ void __launch_bounds__(kGfThreads, TOMESH_GF_MINB)
+k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_loc, const double *__restrict__ ro,
+            const double *__restrict__ qo, const double *__restrict__ po, const double *__restrict__ Dinv,
+            double *__restrict__ rw, double *__restrict__ pw, double *__restrict__ qw, double *__restrict__ x,
+            const __grid_constant__ K0Dense2 K2, const __grid_constant__ K0HadSym H, CgScalars *S,
+            double *partials, int kit, double rtol, double *hist) {
+  constexpr bool CG = MODE == G_CG;
+  extern __shared__ __align__(16) unsigned char gsm_raw[];
+  const int tid = threadIdx.x;
+  GF_MARK(0);
+  const GfMeta mt = B.meta[blockIdx.x];
+  GfSections sec;
+  const GfView V = gf_view<DIM>(B, mt, gsm_raw, sec);
+  GF_CHECK(sec.total <= 16 * B.max_rec16 && mt.n_el <= B.max_el && mt.n_own <= B.max_own && mt.n_own <= kGfMaxOwn);
+  GF_CHECK(mt.n_own + mt.n_halo + mt.n_virt <= B.max_loc && (mt.el_off & 1) == 0);
+  // static block data and s_e (written before the first iteration's launch):
+  // one bulk copy each, issued before the wait on the previous iteration
+  if (tid == 0) gf_issue_record<DIM>(B, V, sec, s_loc, gsm_raw);
+  __syncthreads();
+  pdl_wait();
+  pdl_release();
+  if (CG && cg_stopped(S)) {
+    mbar_wait(V.bar, 0);   // no bulk copy may still be writing when the CTA exits
+    return;
+  }
+  GF_MARK(1);
+  const double alpha = CG ? __ldcg(&S->alpha) : 0.0;
+  const double beta = CG ? __ldcg(&S->beta) : 0.0;
+  double dots[5];
+  gf_block_iter<DIM, MODE, false>(V, true, ro, qo, po, Dinv, rw, pw, qw, x, K2, H, alpha, beta, dots);
   GF_MARK(5);
 #ifdef TOMESH_GF_GRIDSUM
   if (CG) {
-    double dots[5] = {rho, rr, pq, qz, qdq};
     if (grid_sum<5>(dots, partials, &S->counter[CNT_PQ])) cg_single_step(S, kit, dots, rtol, hist);
   }
 #else
   if (CG) {   // this block's dots; k_gen_step sums the blocks in a fixed order
-    double dots[5] = {rho, rr, pq, qz, qdq};
     block_sum<5>(dots);
     if (tid == 0)
 #pragma unroll
@@ -427,6 +486,56 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
   }
 #endif
   GF_MARK(6);
+}
+
+// The whole general-path PCG loop in one cooperative kernel, for meshes whose
+// blocks are all co-resident (c1, c2 and other small meshes: launch and
+// drain latency dominate there).  Each block keeps its record in shared
+// memory across iterations; per iteration: the block iteration (vectors other
+// blocks wrote are read through L2), its dots to part[k & 1], a grid barrier,
+// then EVERY block sums the partials in block order and evaluates the step
+// (cg_step_eval: the same arithmetic on the same values, hence the same
+// alpha, beta and stop decision everywhere); block 0 commits it to S.  x_N
+// after a fixed count is completed by k_final_gen, as on the launched path.
+template <int DIM>
+__global__ void __launch_bounds__(kGfThreads, TOMESH_GF_MINB)
+k_gen_persist(const __grid_constant__ GenBlocks B, const double *__restrict__ s_loc, double *rb0, double *rb1,
+              double *pb0, double *pb1, double *qb0, double *qb1, const double *__restrict__ Dinv, double *x,
+              const __grid_constant__ K0Dense2 K2, const __grid_constant__ K0HadSym H, CgScalars *S, double *part,
+              int max_iter, double rtol, double *hist) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  extern __shared__ __align__(16) unsigned char gsm_raw[];
+  const int tid = threadIdx.x, nb = gridDim.x;
+  const GfMeta mt = B.meta[blockIdx.x];
+  GfSections sec;
+  const GfView V = gf_view<DIM>(B, mt, gsm_raw, sec);
+  if (tid == 0) gf_issue_record<DIM>(B, V, sec, s_loc, gsm_raw);
+  __syncthreads();
+  if (cg_stopped(S)) {   // read by every block before block 0 writes S (after the first barrier)
+    mbar_wait(V.bar, 0);
+    return;
+  }
+  double alpha = __ldcg(&S->alpha), beta = __ldcg(&S->beta);
+  for (int k = 0; k < max_iter; ++k) {
+    const bool odd = k & 1;                           // writes buffer k & 1, reads (k + 1) & 1
+    double dots[5];
+    gf_block_iter<DIM, G_CG, true>(V, k == 0, odd ? rb0 : rb1, odd ? qb0 : qb1, odd ? pb0 : pb1, Dinv,
+                                   odd ? rb1 : rb0, odd ? pb1 : pb0, odd ? qb1 : qb0, x, K2, H, alpha, beta, dots);
+    block_sum<5>(dots);
+    double *pk = part + (size_t)(k & 1) * 5 * nb;
+    if (tid == 0)
+#pragma unroll
+      for (int j = 0; j < 5; ++j) __stcg(&pk[(size_t)5 * blockIdx.x + j], dots[j]);
+    grid.sync();
+    double d[5];
+    g_sum_partials<5>(pk, nb, d);
+    CgStepOut so;
+    cg_step_eval(S, k, d, rtol, so);
+    if (blockIdx.x == 0 && tid == 0) cg_step_commit(S, k, so, hist);
+    if (so.done) break;
+    alpha = so.alpha;
+    beta = so.beta;
+  }
 }
 
 // The step of general-path iteration k: the blocks' dots summed in block

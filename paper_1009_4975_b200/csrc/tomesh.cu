@@ -58,7 +58,7 @@ int validate(const to_mesh_desc *d) {
     if (f < 0 || f >= d->n_node * d->dim || (i > 0 && f <= d->fixed_dof[i - 1])) { set_error("fixed_dof not ascending / out of range"); return TO_EMESH; }
     if (hang[f / d->dim]) { set_error("fixed DOF %lld is on a hanging node", (long long)f); return TO_EMESH; }
   }
-  if ((d->options & ~(uint32_t)(TO_UPLOAD_GENERAL | TO_UPLOAD_PERSISTENT)) != 0) {
+  if ((d->options & ~(uint32_t)(TO_UPLOAD_GENERAL | TO_UPLOAD_LAUNCHED)) != 0) {
     set_error("unknown upload option bits 0x%x", d->options);
     return TO_EINVAL;
   }
@@ -298,23 +298,8 @@ int setup_incidence(const to_mesh_desc *d, const std::vector<int32_t> &node_hang
           inc[fill[d->hang_parent[k]]++] = idx | (code(w) << 30);
         }
     }
-  std::vector<uint8_t> hmask(d->n_elem, 0);
-  for (int64_t e = 0; e < d->n_elem; ++e)
-    for (int c = 0; c < nc; ++c)
-      if (node_hang[d->elem_node[e * nc + c]] >= 0) hmask[e] |= (uint8_t)(1u << c);
-  RC(upload_array(m, &m->hmask, hmask.data(), hmask.size(), st));
   RC(upload_array(m, &m->inc_ptr, ptr.data(), ptr.size(), st));
   RC(upload_array(m, &m->inc, inc.data(), inc.size(), st));
-  return 0;
-}
-
-// Element-vector buffer and node records of the two-pass general operator
-// (only the 2D persistent cooperative solver uses them).
-int setup_two_pass(const to_mesh_desc *d, cudaStream_t st, to_mesh *m) {
-  const int nc = 1 << d->dim;
-  RC(m->alloc(&m->ye, (size_t)d->n_elem * nc * d->dim));
-  RC(m->alloc(&m->zp, (size_t)d->n_node * 2 * d->dim));
-  CK(cudaMemsetAsync(m->ye, 0, sizeof(double) * (size_t)d->n_elem * nc * d->dim, st));
   return 0;
 }
 
@@ -516,9 +501,11 @@ int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_han
   if (d->dim == 3) {
     RC(allow((const void *)k_gen_fused<3, G_CG>));
     RC(allow((const void *)k_gen_fused<3, G_PLAIN>));
+    RC(allow((const void *)k_gen_persist<3>));
   } else {
     RC(allow((const void *)k_gen_fused<2, G_CG>));
     RC(allow((const void *)k_gen_fused<2, G_PLAIN>));
+    RC(allow((const void *)k_gen_persist<2>));
   }
   RC(ensure_partials(m, (size_t)nb * 5));
   m->gen_fused = true;
@@ -634,17 +621,21 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
     std::vector<uint32_t> incv;
     RC(setup_incidence(d, node_hang, st, m, iptr, incv));
     RC(build_gen_blocks(d, node_hang, iptr, incv, st, m));
-    // opt-in: the persistent cooperative solver for small 2D meshes (the whole
-    // loop in one kernel; slower than one kernel per iteration since round 2)
+    // small meshes (at most kGfPersistMaxBlocks blocks): the whole loop in one
+    // cooperative kernel, unless TO_UPLOAD_LAUNCHED.  Measured: c1 (6 blocks)
+    // 5.8 vs 6.9 us per iteration launched; c2 (85 blocks) 13.8 vs 9.0 -- the
+    // grid barrier and the partial sums in every block cost more than the two
+    // PDL-chained launches once there are more than a few dozen blocks
     int coop = 0;
     CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
-    if (coop && (d->options & TO_UPLOAD_PERSISTENT) && d->dim == 2 && d->n_elem <= 100000) {
+    if (coop && !(d->options & TO_UPLOAD_LAUNCHED) && d->n_owned == 0 && m->GB.n_blk <= kGfPersistMaxBlocks) {
       int per_sm = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_general_persistent<2>, kBlock, 0));
-      const int64_t need = (std::max<int64_t>(d->n_elem, d->n_node) + kBlock - 1) / kBlock;
-      m->coop_blocks = (int)std::min<int64_t>(need, (int64_t)per_sm * kNumSMs);
-      RC(ensure_partials(m, (size_t)m->coop_blocks * 3));   // part_a [coop] + part_b [2 coop]
-      RC(setup_two_pass(d, st, m));
+      const void *fn = d->dim == 2 ? (const void *)k_gen_persist<2> : (const void *)k_gen_persist<3>;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGfThreads, m->gb_smem));
+      if ((int64_t)per_sm * kNumSMs >= m->GB.n_blk) {
+        m->gen_persist = true;
+        RC(ensure_partials(m, (size_t)m->GB.n_blk * 10));   // part[2][n_blk][5]
+      }
     }
   }
   // workspace: internal-order vectors with zero pads on both sides (the
@@ -861,15 +852,6 @@ int op_final_s3(to_mesh *m, int n_iter, double rtol, cudaStream_t st) {
   return check_launch();
 }
 
-// General path K2 (INIT: rho0, rr0 and thresholds only).
-template <bool INIT>
-int op_cg_k2(to_mesh *m, double rtol, cudaStream_t st) {
-  k_rupd<INIT><<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->q, m->dinv, m->r, m->partials, m->S, m->hist,
-                                                      rtol);
-  m->last_launches++;
-  return 0;
-}
-
 // dst = Pi_F u (canonical -> internal), used for warm starts
 int op_masked_in(to_mesh *m, const double *u_canon, double *dst, cudaStream_t st) {
   if (!m->structured) {
@@ -914,11 +896,11 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   CK(cudaEventRecord(m->ev0, st));
   RC(reset_scalars(m, max_iter, fixed, hist, st));
   RC(op_scale_and_diag(m, penal, x_dev, nullptr, st));
-  // single-kernel iterations (structured, and the general path unless the 2D
-  // persistent solver runs the loop): iteration 0 reads r0 = b from rb[1]
-  const bool persistent = !m->structured && m->coop_blocks > 0;
-  double *r0 = persistent ? m->r : m->rb[1];
-  if (!m->structured && !persistent) {   // q_{-1} = p_{-1} = 0 (finite whatever an earlier solve left)
+  // single-kernel iterations (launched, or the general path's cooperative
+  // kernel for small meshes): iteration 0 reads r0 = b from rb[1]
+  const bool persistent = !m->structured && m->gen_persist;
+  double *r0 = m->rb[1];
+  if (!m->structured) {   // q_{-1} = p_{-1} = 0 (finite whatever an earlier solve left)
     CK(cudaMemsetAsync(m->qb[1], 0, sizeof(double) * n, st));
     CK(cudaMemsetAsync(m->pb[1], 0, sizeof(double) * n, st));
   }
@@ -934,11 +916,6 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   } else {
     CK(cudaMemsetAsync(m->x, 0, sizeof(double) * n, st));
   }
-  if (persistent) {
-    RC(op_cg_k2<true>(m, rtol, st));
-    k_zp_init<2><<<grid_for(m->n_node), kBlock, 0, st>>>(m->n_node, m->r, m->dinv, m->zp);
-    m->last_launches++;
-  }
   RC(check_launch());
 
   const bool prof = (flags & TO_PROFILE) != 0;
@@ -953,10 +930,6 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   int launched = 0;
   int chunk = fixed ? std::max(1, max_iter) : 16;
   bool stop = false;
-  if (persistent) {
-    RC(read_scalars(m, st));
-    stop = m->S_host->done != 0;
-  }
   const bool loop_prof = (flags & TO_PROFILE_LOOP) != 0;
   if (loop_prof) {
     for (auto &e : m->loop_ev)
@@ -964,14 +937,16 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
     CK(cudaEventRecord(m->loop_ev[0], st));
   }
   if (persistent && !stop) {
-    // the whole loop in one cooperative kernel (no host polling)
+    // the whole loop in one cooperative kernel (no launches, no host polling)
     if (prof) CK(cudaEventRecord(m->prof_ev[0], st));
-    double *pa = m->partials, *pb_ = m->partials + m->coop_blocks;
-    MeshView V = m->view();
-    void *args3[] = {&V, &m->s, &m->r, &m->dinv, &m->zp, &m->x, &m->ye, &m->inc_ptr, &m->inc, &m->K2, &m->KS,
-                     &m->hmask, &m->S, &pa, &pb_, &m->hist};
-    const void *fn = (const void *)k_cg_general_persistent<2>;   // 2D only (upload)
-    CK(cudaLaunchCooperativeKernel(fn, dim3(m->coop_blocks), dim3(kBlock), args3, 0, st));
+    const double *sl = m->s_loc, *dv = m->dinv;
+    double *rb0 = m->rb[0], *rb1 = m->rb[1], *pb0 = m->pb[0], *pb1 = m->pb[1], *qb0 = m->qb[0], *qb1 = m->qb[1];
+    int mi = max_iter;
+    double rt = rtol;
+    void *args[] = {&m->GB, &sl, &rb0, &rb1, &pb0, &pb1, &qb0, &qb1, &dv, &m->x, &m->K2, &m->KS, &m->S,
+                    &m->partials, &mi, &rt, &m->hist};
+    const void *fn = m->dim == 2 ? (const void *)k_gen_persist<2> : (const void *)k_gen_persist<3>;
+    CK(cudaLaunchCooperativeKernel(fn, dim3(m->GB.n_blk), dim3(kGfThreads), args, m->gb_smem, st));
     m->last_launches++;
     if (prof) CK(cudaEventRecord(m->prof_ev[1], st));
     if (prof) CK(cudaEventRecord(m->prof_ev[2], st));
@@ -1005,7 +980,7 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   if (loop_prof) CK(cudaEventRecord(m->loop_ev[1], st));
   // x_N after exactly N iterations (a no-op if an iteration already converged)
   if (m->structured) RC(op_final_s3(m, max_iter, rtol, st));
-  else if (!persistent) RC(op_final_gen(m, max_iter, rtol, st));
+  else RC(op_final_gen(m, max_iter, rtol, st));
   RC(check_launch());
   RC(read_scalars(m, st));
   CgScalars res = *m->S_host;
@@ -1108,7 +1083,7 @@ extern "C" int tomesh_get_info(const to_mesh *m, to_mesh_info *info) {
   info->filt_nnz = m->filt_nnz;
   info->device_bytes = m->dev_bytes;
   info->kernel_launches = m->last_launches;
-  info->matvec_variant = m->structured ? 1 : m->coop_blocks > 0 ? 3 : 4;
+  info->matvec_variant = m->structured ? 1 : m->gen_persist ? 3 : 4;
   info->launches_total = m->launches_total;
   return 0;
 }

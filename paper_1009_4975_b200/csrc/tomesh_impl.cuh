@@ -54,12 +54,9 @@ struct to_mesh {
   double *ftmp = nullptr;              // structured filter: lexicographic temporary
   int64_t *inc_ptr = nullptr;          // general path: node -> (element, corner, weight) incidences
   uint32_t *inc = nullptr;
-  double *ye = nullptr;                // general path: element vectors s_e K0 C_e p
-  uint8_t *hmask = nullptr;            // general path: bit c = corner c of the element is hanging
-  double *zp = nullptr;                // general path: node records {Dinv r, p}
-  int coop_blocks = 0;                 // general path: grid of the persistent cooperative solver (0 = off)
   // general path, single-kernel iteration (kernels_genfused.cuh)
   bool gen_fused = false;
+  bool gen_persist = false;            // small meshes: the whole loop in one cooperative kernel (k_gen_persist)
   GenBlocks GB{};
   int32_t *gb_el_id = nullptr;         // block-local element -> element
   int64_t gb_n_loc_el = 0;

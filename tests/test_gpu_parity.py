@@ -24,7 +24,7 @@ CASES = {
     "c5s": lambda: config("c5", nx=20, ny=10, nz=10),
     "c5s_general": lambda: config("c5", nx=20, ny=10, nz=10),     # uniform H8 forced onto the general path
     "c3s_ragged": lambda: config("c3", nx=37, ny=9, nz=13),       # several CTA tiles + ragged tails in x, y, z
-    "c2_persistent": lambda: config("c2"),   # opt-in: the whole 2D loop in one cooperative kernel
+    "c1_launched": lambda: config("c1"),     # one launch per iteration (default for c1: the cooperative kernel)
     "amr2d": lambda: cantilever2d((5, 3), L=3, leaves=refine_some(2, (5, 3), 3, [(1, 1), (3, 0)]), rmin=0.3),
     "amr3d": lambda: cantilever3d((3, 2, 2), L=2, leaves=refine_some(3, (3, 2, 2), 2, [(1, 1, 0)]), rmin=0.4),
     "hload2d": hanging_load2d,       # loads on hanging nodes (C8): b = Pi_F C^T f, c = f^T u with them
@@ -40,7 +40,7 @@ def _setup(name):
         om = omesh.build_mesh(prob)
         import paper_1009_4975_b200 as pb
         opts = (pb.TO_UPLOAD_GENERAL if name.endswith("_general") else 0) | \
-               (pb.TO_UPLOAD_PERSISTENT if name.endswith("_persistent") else 0)
+               (pb.TO_UPLOAD_LAUNCHED if name.endswith("_launched") else 0)
         hm, m = product_mesh(prob, options=opts)
         if name.startswith(("c3s", "c5s")):
             assert m.info()["structured"] == (0 if name.endswith("_general") else 1)
@@ -115,7 +115,7 @@ def test_L2_converged_solve(name):
     assert abs(st.iters - ref.cg.iters) <= max(5, 0.05 * ref.cg.iters)
 
 
-@pytest.mark.parametrize("name", ["c2", "c2_persistent", "c5s"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c1_launched", "c5s"])
 def test_warm_start_and_fixed_iterations(name):
     prob, om, hm, m, x_dev = _setup(name)
     u = torch.zeros(om.n_dof, dtype=torch.float64, device="cuda")
@@ -168,14 +168,14 @@ def test_solver_edge_cases(name):
     assert abs(st.relres_true - st.relres) <= 1e-6 * st.relres
 
 
-@pytest.mark.parametrize("name", ["c4s", "amr3d", "c2_persistent"])
+@pytest.mark.parametrize("name", ["c4s", "amr3d", "c1_launched", "c1"])
 def test_upload_is_deterministic(name):
     """Two uploads of the same mesh solve to bit-identical u: nothing at upload
     depends on timing (no timing-based kernel or grid choice), and every
     reduction sums in a fixed order."""
     prob, om, hm, m, x_dev = _setup(name)
     import paper_1009_4975_b200 as pb
-    opts = pb.TO_UPLOAD_PERSISTENT if name.endswith("_persistent") else 0
+    opts = pb.TO_UPLOAD_LAUNCHED if name.endswith("_launched") else 0
     us = []
     for _ in range(2):
         _, m2 = product_mesh(prob, options=opts)

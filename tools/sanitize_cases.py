@@ -16,7 +16,7 @@ import paper_1009_4975_b200 as pb  # noqa: E402
 from inputs import config, density_at  # noqa: E402
 
 CASES = {
-    "c1": (lambda: config("c1"), pb.TO_UPLOAD_PERSISTENT),             # 2D persistent cooperative solver
+    "c1": (lambda: config("c1"), 0),                                   # 2D cooperative general kernel
     "c2": (lambda: config("c2"), 0),                                   # 2D general kernel per iteration
     "c4s": (lambda: config("c4", base=(6, 3, 3), L=2, n_gauss=30), 0),  # 3D general kernel (hanging nodes)
     "c3s": (lambda: config("c3", nx=37, ny=9, nz=13), 0),              # structured K1 (TMA, ragged tiles)

@@ -17,7 +17,7 @@ from inputs import config, density_at  # noqa: E402
 for name in sys.argv[1:] or ["c1", "c2"]:
     prob = config(name)
     hm = pb.prepare(prob)
-    for opts in (pb.TO_UPLOAD_PERSISTENT, 0):
+    for opts in (0, pb.TO_UPLOAD_LAUNCHED):
         m = pb.Mesh(hm, E0=prob.E0, Emin=prob.Emin, nu=prob.nu, rmin=prob.rmin, options=opts)
         x = torch.as_tensor(density_at(prob, hm.elem_level, hm.elem_anchor), device="cuda")
         u = torch.zeros(hm.n_dof, dtype=torch.float64, device="cuda")
