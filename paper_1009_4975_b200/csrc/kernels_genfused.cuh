@@ -60,6 +60,10 @@ constexpr int kGfPersistMaxBlocks = 32;                  // k_gen_persist only u
 #endif
 constexpr int kGfOwnTarget3 = TOMESH_GF_OWN3;           // owned nodes per block before splitting (3D)
 constexpr int kGfOwnTarget2 = TOMESH_GF_OWN2;           // (2D)
+#ifndef TOMESH_GF_OWN_MIN
+#define TOMESH_GF_OWN_MIN 64
+#endif
+constexpr int kGfOwnMin = TOMESH_GF_OWN_MIN;             // smallest block target (mid-size meshes)
 #ifndef TOMESH_GF_CH
 #define TOMESH_GF_CH 256
 #endif
