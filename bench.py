@@ -105,18 +105,30 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def kernel_bytes(dim, n_el, n_node, n_dof, structured):
+def x_touch_fraction(iters):
+    """Share of the structured kernel's launches that read and write x: with
+    the deferred x update (kernels_cg.cuh cg_x_coef) kernel 0 and every odd
+    kernel leave x alone and the even kernels k >= 2 apply two steps' terms,
+    so floor((iters - 1) / 2) of `iters` launches touch x."""
+    if not iters:
+        return 1.0
+    return max(0, (iters - 1) // 2) / iters
+
+
+def kernel_bytes(dim, n_el, n_node, n_dof, structured, iters=None):
     """Algorithmic bytes per launch of the PCG kernels.
 
     Structured path, one kernel per iteration (k1): s (8/elem) + Dinv
-    (8/node) + read r_{k-1}, q_{k-1}, p_{k-1}, x and write r_k, p_k, q_k, x
-    (8 x 8/DOF); k2 = 0.
+    (8/node) + read r_{k-1}, q_{k-1}, p_{k-1} and write r_k, p_k, q_k (6 x
+    8/DOF) + read and write x (2 x 8/DOF) in the launches that touch x
+    (x_touch_fraction of `iters` launches; all of them when iters is None),
+    averaged per launch; k2 = 0.
     General path (k_gen_fused, one kernel per iteration + a one-CTA step):
     read r, q, p, Dinv, x and write r, p, q, x (9 x 8/DOF) + s and
     connectivity per element (8 + 4 * 2^dim); k2 = 0."""
     nc = 1 << dim
     if structured:
-        return {"k1": 8 * n_el + 8 * n_node + 64 * n_dof, "k2": 0}
+        return {"k1": 8 * n_el + 8 * n_node + 48 * n_dof + round(16 * n_dof * x_touch_fraction(iters)), "k2": 0}
     return {"k1": 72 * n_dof + n_el * (8 + 4 * nc), "k2": 0}
 
 
@@ -427,7 +439,7 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (K1: p update + operator + x update) ---------
     hbm, peak_kind = _peaks()
     info = m.info()
-    kb = kernel_bytes(hm.dim, hm.n_el, hm.n_node, hm.n_dof, bool(info["structured"]))
+    kb = kernel_bytes(hm.dim, hm.n_el, hm.n_node, hm.n_dof, bool(info["structured"]), iters)
     k1_ms_events = prof["apply_ms"] / max(1, prof["iters"])
     k2_ms = prof["u1_ms"] / max(1, prof["iters"])
     # structured path: the loop holds K1 launches only, so its mean is K1's average launch duration
@@ -608,7 +620,7 @@ def run_weak(args):
     it_ms = max_over_ranks(p["loop_ms"] / max(1, p["iters"]), ws)
     own_nodes = int(sl.node_owned.sum())
     own_el = int(sl.elem_owned.sum())
-    kb = 8 * own_el + 8 * own_nodes + 64 * 3 * own_nodes
+    kb = 8 * own_el + 8 * own_nodes + round((48 + 16 * x_touch_fraction(iters)) * 3 * own_nodes)
     hbm, peak_kind = _peaks()
     n_dof_g = 3 * 257 * 129 * (128 * ws + 1)
     if rank == 0:
@@ -726,7 +738,7 @@ def run_shard(args):
     it_ms = max_over_ranks(p["loop_ms"] / max(1, p["iters"]), ws)
     own_nodes = int(sl.node_owned.sum())
     own_el = int(sl.elem_owned.sum())
-    kb = 8 * own_el + 8 * own_nodes + 64 * 3 * own_nodes
+    kb = 8 * own_el + 8 * own_nodes + round((48 + 16 * x_touch_fraction(iters)) * 3 * own_nodes)
     hbm, peak_kind = _peaks()
     if rank == 0:
         line = {

@@ -27,6 +27,7 @@ struct CgScalars {
   int32_t history;   // record ||r||/||b|| per iteration
   int32_t pad;
   uint32_t counter[8];   // last-block-done counters, one per reduction site
+  double ab[2][2];       // {alpha_k, beta_k} of step k in slot k & 1 (the structured kernel's deferred x update)
 };
 
 enum { CNT_PQ = 0, CNT_U1 = 1, CNT_INIT = 2, CNT_MISC = 3, CNT_MISC2 = 4, CNT_XCHG = 5 };

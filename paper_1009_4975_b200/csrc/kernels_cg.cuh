@@ -84,6 +84,8 @@ __device__ __forceinline__ void cg_single_step(CgScalars *S, int k, const double
   const double rho_next = fma(alpha * alpha, qdq, fma(-2.0 * alpha, qz, rho));
   S->alpha = alpha;
   S->beta = rho_next / rho;
+  S->ab[k & 1][0] = S->alpha;
+  S->ab[k & 1][1] = S->beta;
 }
 
 // cg_single_step split for the sharded K1, where EVERY CTA of iteration k+1
@@ -148,6 +150,43 @@ __device__ __forceinline__ void cg_step_commit(CgScalars *S, int k, const CgStep
   }
   S->alpha = o.alpha;
   S->beta = o.beta;
+  S->ab[k & 1][0] = o.alpha;
+  S->ab[k & 1][1] = o.beta;
+}
+
+// Deferred x update of the structured kernel (kernels_struct3d.cuh).  Kernel
+// k stages p_{k-1} and r_{k-1} (z_{k-1} = Dinv r_{k-1}); the textbook update
+// there is x_k = x_{k-1} + alpha_{k-1} p_{k-1}.  An odd kernel k skips x (one
+// read and one write of x saved) and the next kernel applies both terms:
+//   alpha_{k-1} p_{k-1} = (alpha_{k-1} / beta_{k-1}) (p_k - z_k)
+// since p_k = z_k + beta_{k-1} p_{k-1}.  Only when |beta_{k-1}| is not tiny
+// (a deterministic test on the step's own scalars, so every CTA, rank and the
+// final kernel take the same decision); x's rounding differs from the
+// textbook order by the reconstruction only (it never feeds back into r, p).
+constexpr double kXDeferMinBeta = 1e-6;
+__device__ __forceinline__ bool cg_x_deferred(int k, double alpha_km1, double beta_km1) {
+  return (k & 1) && alpha_km1 != 0.0 && fabs(beta_km1) >= kXDeferMinBeta;
+}
+// x += cp p_{k-1} + cz z_{k-1} in kernel k (touch = false: x untouched).
+// a1 = alpha_{k-1}; (a2, b2) = (alpha_{k-2}, beta_{k-2}); defer = false
+// forces the update (the final kernel).
+struct XCoef {
+  double cp, cz;
+  bool touch;
+};
+__device__ __forceinline__ XCoef cg_x_coef(int k, double a1, double b1, double a2, double b2, bool defer) {
+  XCoef c{a1, 0.0, a1 != 0.0};
+  if (defer && cg_x_deferred(k, a1, b1)) {
+    c.touch = false;
+    return c;
+  }
+  if (k >= 2 && cg_x_deferred(k - 1, a2, b2)) {   // kernel k-1 left alpha_{k-2} p_{k-2} pending
+    const double t = a2 / b2;
+    c.cp = a1 + t;
+    c.cz = -t;
+    c.touch = true;
+  }
+  return c;
 }
 
 // Structured path, final step after N = max_iter iterations (or 0): r_N =

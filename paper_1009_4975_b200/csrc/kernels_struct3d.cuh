@@ -247,7 +247,12 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
     alpha_old = s_ab[0];
     beta = s_ab[1];
   }
-  const bool xupd = CG && owner && alpha_old != 0.0;
+  // x += cp p_{k-1} + cz z_{k-1}, or x untouched in a deferring (odd) kernel
+  // (cg_x_coef, kernels_cg.cuh).  (alpha, beta)_{k-2} sit in slot k & 1 of S,
+  // which neither this kernel nor a sharded CTA 0 committing step k-1 writes.
+  XCoef xc{0.0, 0.0, false};
+  if (CG) xc = cg_x_coef(kit, alpha_old, beta, __ldcg(&S->ab[kit & 1][0]), __ldcg(&S->ab[kit & 1][1]), true);
+  const bool xupd = CG && owner && xc.touch;
   const int64_t plane_d = (int64_t)G.NY * G.RS;        // doubles per node plane
 
   auto buf_of = [&](int k) { return (k - (k_lo - 1)) % kS3NBuf; };
@@ -315,8 +320,9 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
         }
         if (xupd) {
           const double *pp = &sm.pa[bb][ty * kS3RowD + off + 3 * tx];
+          const double *rp = &sm.ra[bb][ty * kS3RowD + off + 3 * tx];
 #pragma unroll
-          for (int d = 0; d < 3; ++d) __stcs(&x[dof + d], fma(alpha_old, pp[d], xs[d]));
+          for (int d = 0; d < 3; ++d) __stcs(&x[dof + d], fma(xc.cp, pp[d], fma(xc.cz * dv, rp[d], xs[d])));
           if (k + 2 < k_hi) {
 #pragma unroll
             for (int d = 0; d < 3; ++d) xs[d] = __ldcs(&x[dof + 2 * plane_d + d]);
@@ -510,13 +516,35 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
 // per node (node = DOF / 3, an L1 hit).  r_N itself is not stored.
 // SHARD: over the owned planes only (the caller offsets the pointers), and
 // the partial rho_N, rr_N are pushed for k_shard_final.
+// The deferred x update (cg_x_coef): x_N also takes the term kernel N-1 left
+// pending.  A solve that stopped at an odd iteration k whose kernel deferred
+// gets that term here too (x += (alpha_{k-1}/beta_{k-1}) (p_k - z_k), from
+// r_k, p_k in buffer 1 = rk, pk); nothing else happens then.
 template <bool SHARD = false>
 __global__ void __launch_bounds__(512) k_final_s3(int n, const double *__restrict__ ro, const double *__restrict__ qo,
                                                   const double *__restrict__ po, const double *__restrict__ dn,
                                                   double *__restrict__ x, double *partials, CgScalars *S, int n_iter,
                                                   double rtol, double *hist, const __grid_constant__ ShardComm C,
-                                                  unsigned long long seq) {
+                                                  unsigned long long seq, const double *__restrict__ rk,
+                                                  const double *__restrict__ pk) {
+  const int n2 = n >> 1;
+  double2 *x2 = reinterpret_cast<double2 *>(x);
   if (cg_stopped(S)) {
+    const int k = __ldcg(&S->iter);
+    if (__ldcg(&S->status) == 0 && cg_x_deferred(k, __ldcg(&S->alpha), __ldcg(&S->beta))) {
+      const double t = __ldcg(&S->alpha) / __ldcg(&S->beta);
+      const double2 *r2 = reinterpret_cast<const double2 *>(rk);
+      const double2 *p2 = reinterpret_cast<const double2 *>(pk);
+      for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n2; j += gridDim.x * blockDim.x) {
+        const unsigned e = 2u * (unsigned)j;
+        const double d0 = __ldg(&dn[e / 3u]), d1 = __ldg(&dn[(e + 1u) / 3u]);
+        const double2 rv = __ldcs(&r2[j]), pv = __ldcs(&p2[j]);
+        double2 xv = x2[j];
+        xv.x = fma(t, pv.x, fma(-t * d0, rv.x, xv.x));
+        xv.y = fma(t, pv.y, fma(-t * d1, rv.y, xv.y));
+        x2[j] = xv;
+      }
+    }
     // sharded: every rank pushes every tail sequence (kernels_shard.cuh)
     if (SHARD && blockIdx.x == 0 && threadIdx.x == 0) {
       const double zero[2] = {0.0, 0.0};
@@ -525,24 +553,27 @@ __global__ void __launch_bounds__(512) k_final_s3(int n, const double *__restric
     return;
   }
   const double alpha = __ldcg(&S->alpha);
+  const XCoef xc = cg_x_coef(n_iter, alpha, __ldcg(&S->beta), __ldcg(&S->ab[n_iter & 1][0]),
+                             __ldcg(&S->ab[n_iter & 1][1]), false);
   double acc[2] = {0.0, 0.0};
-  const int n2 = n >> 1;
   const double2 *r2 = reinterpret_cast<const double2 *>(ro);
   const double2 *q2 = reinterpret_cast<const double2 *>(qo);
   const double2 *p2 = reinterpret_cast<const double2 *>(po);
-  double2 *x2 = reinterpret_cast<double2 *>(x);
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n2; j += gridDim.x * blockDim.x) {
     double2 rv = __ldcs(&r2[j]);
     const unsigned e = 2u * (unsigned)j;
     const double d0 = __ldg(&dn[e / 3u]), d1 = __ldg(&dn[(e + 1u) / 3u]);
-    if (alpha != 0.0) {
-      const double2 qv = __ldcs(&q2[j]), pv = __ldcs(&p2[j]);
+    if (xc.touch) {
+      const double2 pv = __ldcs(&p2[j]);
       double2 xv = x2[j];
+      xv.x = fma(xc.cp, pv.x, fma(xc.cz * d0, rv.x, xv.x));
+      xv.y = fma(xc.cp, pv.y, fma(xc.cz * d1, rv.y, xv.y));
+      x2[j] = xv;
+    }
+    if (alpha != 0.0) {
+      const double2 qv = __ldcs(&q2[j]);
       if (d0 != 0.0) rv.x = fma(-alpha, qv.x, rv.x);
       if (d1 != 0.0) rv.y = fma(-alpha, qv.y, rv.y);
-      xv.x = fma(alpha, pv.x, xv.x);
-      xv.y = fma(alpha, pv.y, xv.y);
-      x2[j] = xv;
     }
     acc[0] = fma(rv.x, d0 * rv.x, fma(rv.y, d1 * rv.y, acc[0]));
     acc[1] = fma(rv.x, rv.x, fma(rv.y, rv.y, acc[1]));

@@ -854,7 +854,8 @@ int op_cg_s3(to_mesh *m, int k, double rtol, cudaStream_t st) {
 int op_final_s3(to_mesh *m, int n_iter, double rtol, cudaStream_t st) {
   const int o = (n_iter + 1) & 1;
   k_final_s3<false><<<kNumSMs * 4, 512, 0, st>>>((int)m->n_int, m->rb[o], m->qb[o], m->pb[o], m->dn, m->x,
-                                                 m->partials, m->S, n_iter, rtol, m->hist, ShardComm{}, 0ull);
+                                                 m->partials, m->S, n_iter, rtol, m->hist, ShardComm{}, 0ull,
+                                                 m->rb[1], m->pb[1]);
   m->last_launches++;
   return check_launch();
 }

@@ -325,7 +325,8 @@ extern "C" int tosolve_cg_group(to_mesh *const *ms, int32_t n, double penal, con
     const int n_own = (int)((m->SC.own_hi - m->SC.own_lo) * pd);
     k_final_s3<true><<<kNumSMs * 4, 512, 0, S_(i)>>>(n_own, m->rb[o] + off, m->qb[o] + off, m->pb[o] + off,
                                                      m->dn + nodes_off, m->x + off, m->partials, m->S, max_iter, rtol,
-                                                     m->hist, m->SC, kShardTail | m->tail_seq);
+                                                     m->hist, m->SC, kShardTail | m->tail_seq, m->rb[1] + off,
+                                                     m->pb[1] + off);
     m->last_launches++;
     RC(check_launch());
   }

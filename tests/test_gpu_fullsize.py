@@ -133,15 +133,18 @@ def test_fullsize_L2_converged_vs_cached_oracle(setup):
     u = torch.zeros(om.n_dof, dtype=torch.float64, device="cuda")
     st = m.tosolve_cg(prob.penal, xd, u, rtol=1e-10, max_iter=400000)
     assert st.status == 0 and st.relres <= 1e-10
-    assert rel(host(u), ref["u"]) <= 1e-8
+    eu = rel(host(u), ref["u"])
     dc = torch.empty(om.n_el, dtype=torch.float64, device="cuda")
     c = m.to_sensitivity(prob.penal, xd, u, dc, compliance=True)
     c_ref = float(ref["compliance"])
-    assert abs(c - c_ref) <= 1e-8 * abs(c_ref)
-    assert rel(host(dc), ref["dc"]) <= 1e-8
+    ec = abs(c - c_ref) / abs(c_ref)
+    edc = rel(host(dc), ref["dc"])
     out = torch.empty_like(dc)
     m.to_filter(0, xd, dc, out)
-    assert rel(host(out), ref["dcf"]) <= 1e-8
+    edcf = rel(host(out), ref["dcf"])
+    print(f"L2 {name}: iters={st.iters} (oracle {json_meta(ref)['iters']}) relres={st.relres:.3e} "
+          f"|du|={eu:.2e} |dc|={ec:.2e} |ddc|={edc:.2e} |ddc~|={edcf:.2e}")
+    assert eu <= 1e-8 and ec <= 1e-8 and edc <= 1e-8 and edcf <= 1e-8
 
 
 def json_meta(ref):

@@ -184,3 +184,71 @@ def test_upload_is_deterministic(name):
         us.append(u)
         m2.close()
     assert torch.equal(us[0], us[1])
+
+
+def _stop_targets(h, lo=8):
+    """An odd and an even iteration k >= lo at which a solve with rtol just
+    above h[k-1] stops (every earlier residual, and ||r_0|| = ||b||, clearly
+    above it)."""
+    out = {}
+    for k in range(lo, len(h) + 1):
+        if h[k - 1] < 0.99 * min(h[:k - 1].min(), 1.0) and (k & 1) not in out:
+            out[k & 1] = k
+    assert set(out) == {0, 1}, h
+    return [out[1], out[0]]
+
+
+def test_structured_deferred_x_update():
+    """The structured kernel defers x (kernels_cg.cuh cg_x_coef): an odd kernel
+    k leaves x alone and kernel k+1 adds alpha_{k-1} p_{k-1} = (alpha_{k-1} /
+    beta_{k-1}) (p_k - z_k) to its own term; k_final_s3 adds what is pending
+    after N iterations or at a stop.  Against the general path's textbook
+    update (x += alpha p in every iteration) on the same mesh: u after every
+    fixed count N = 0..12 (both parities) to rounding (1e-11; two fp64 CG runs
+    in different summation orders drift apart exponentially on this problem,
+    ~1e-13 at 40 iterations and ~1e-4 at 97, whatever the parity).  Solves that
+    stop at an odd and at an even iteration k, unsharded and as a 2-slab
+    group: ||b - A u|| / ||b|| of the returned u (the operator applied by the
+    library to u) equals the recurrence residual the solve reports (a missing
+    alpha p term changes it at O(1e-1))."""
+    import paper_1009_4975_b200 as pb
+    from paper_1009_4975_b200 import shard
+    prob, om, hm, m, x_dev = _setup("c5s")
+    _, _, _, mg, _ = _setup("c5s_general")
+    n = om.n_dof
+    fixed = pb.TO_FIXED_ITERS | pb.TO_NO_TRUE_RES
+    for N in range(13):
+        us = torch.zeros(n, dtype=torch.float64, device="cuda")
+        ug = torch.zeros_like(us)
+        m.tosolve_cg(prob.penal, x_dev, us, rtol=0.0, max_iter=N, flags=fixed)
+        mg.tosolve_cg(prob.penal, x_dev, ug, rtol=0.0, max_iter=N, flags=fixed)
+        if N == 0:
+            assert torch.count_nonzero(us) == 0 and torch.count_nonzero(ug) == 0
+        else:
+            assert rel(host(us), host(ug)) <= 1e-11, N
+    b = torch.empty(n, dtype=torch.float64, device="cuda")
+    m.to_project_rhs(b)
+    q = torch.empty_like(b)
+
+    def true_res(u):
+        m.to_apply_A(prob.penal, x_dev, u, q)
+        return float(torch.linalg.norm(b - q) / torch.linalg.norm(b))
+
+    u = torch.zeros(n, dtype=torch.float64, device="cuda")
+    m.tosolve_cg(prob.penal, x_dev, u, rtol=0.0, max_iter=400, flags=pb.TO_FIXED_ITERS | pb.TO_HISTORY)
+    h = m.history(400)     # ||r_k|| / ||b|| is not monotone: the first new minima below 1 come late
+    ks = _stop_targets(h)
+    g = shard.ShardGroup(hm, 2, E0=prob.E0, Emin=prob.Emin, nu=prob.nu, rmin=prob.rmin)
+    xs = g.scatter_elems(x_dev)
+    for k in ks:
+        rtol = float(h[k - 1]) * (1 + 1e-6)   # stops at k: h[j-1] > rtol for every j < k
+        us = torch.zeros(n, dtype=torch.float64, device="cuda")
+        st = m.tosolve_cg(prob.penal, x_dev, us, rtol=rtol, max_iter=1000)
+        assert st.iters == k and st.status == 0
+        assert abs(st.relres_true - st.relres) <= 1e-8 * st.relres
+        assert abs(true_res(us) - st.relres) <= 1e-8 * st.relres
+        uss = [torch.zeros(mm.n_dof, dtype=torch.float64, device="cuda") for mm in g.meshes]
+        sts = g.solve(prob.penal, xs, uss, rtol=rtol, max_iter=1000)
+        assert all(s.iters == k and s.status == 0 for s in sts), (k, [s.iters for s in sts])
+        ug = cuda(g.gather_nodes(uss))
+        assert abs(true_res(ug) - sts[0].relres) <= 1e-8 * sts[0].relres, k

@@ -60,6 +60,11 @@ def test_kernel_bytes_formula():
     assert kb["k1"] == 8 * 4194304 + 8 * 4276737 + 64 * 12830211
     assert abs(kb["k1"] / 1e6 - 888.9) < 0.1
     assert kb["k2"] == 0
+    # the deferred x update: 249 of 500 launches read and write x (kernels 2, 4, ..., 498)
+    assert bench.x_touch_fraction(500) == 249 / 500 and bench.x_touch_fraction(1) == 0.0
+    kb = bench.kernel_bytes(3, 4194304, 4276737, 12830211, True, 500)
+    assert kb["k1"] == 8 * 4194304 + 8 * 4276737 + 48 * 12830211 + round(16 * 12830211 * 249 / 500)
+    assert abs(kb["k1"] / 1e6 - 785.85) < 0.01
 
 
 def test_reference_arm_json_contract():
