@@ -134,9 +134,16 @@ typedef struct {
  *                            one; tosolve_minres with TO_PC_IC0 needs it.
  *   TO_UPLOAD_LAUNCHED       general path: launch one kernel per PCG iteration
  *                            even for the smallest meshes (by default a mesh
- *                            of at most 32 operator blocks, e.g. c1, runs the
- *                            whole loop in one cooperative kernel). */
-enum { TO_UPLOAD_GENERAL = 1, TO_UPLOAD_LAUNCHED = 2 };
+ *                            that one thread-block cluster of at most 16
+ *                            CTAs holds, e.g. c1 and c2, runs the whole loop
+ *                            in that cluster with the CG state in shared
+ *                            memory; failing that, a mesh of at most 32
+ *                            operator blocks runs it in one cooperative
+ *                            kernel).
+ *   TO_UPLOAD_NO_CLUSTER     general path: do not use the cluster-resident
+ *                            solver (the cooperative kernel, or one kernel
+ *                            per iteration, instead). */
+enum { TO_UPLOAD_GENERAL = 1, TO_UPLOAD_LAUNCHED = 2, TO_UPLOAD_NO_CLUSTER = 4 };
 
 typedef struct {
   int32_t iters;               /* CG iterations performed                        */
@@ -154,9 +161,10 @@ typedef struct {
   int64_t device_bytes;        /* device memory held by the handle               */
   int32_t kernel_launches;     /* kernels launched by the last tosolve_cg        */
   int32_t matvec_variant;      /* CG iteration path: 1 structured H8 (one
-                                  kernel per iteration), 3 general, 2D
-                                  persistent cooperative solver, 4 general
-                                  one kernel per iteration                  */
+                                  kernel per iteration), 3 general, whole
+                                  loop in one cooperative kernel, 4 general
+                                  one kernel per iteration, 5 general, whole
+                                  loop in one thread-block cluster          */
   int64_t launches_total;      /* kernels launched by every call on this handle
                                   since upload (monotone counter)               */
 } to_mesh_info;

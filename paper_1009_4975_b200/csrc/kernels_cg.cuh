@@ -129,6 +129,51 @@ __device__ __forceinline__ void cg_step_eval(const CgScalars *S, int k, const do
   o.alpha = alpha;
   o.beta = rho_next / rho;
 }
+// cg_step_eval with the fields it reads from S loaded once per solve (a
+// kernel that runs the whole loop): bnorm2, fixed, the status before the
+// loop, thresh2 = rtol^2 bnorm2 (what step 0 computes).  Same arithmetic.
+struct CgConst {
+  double bnorm2, thresh2;
+  int fixed, status;
+};
+__device__ __forceinline__ CgConst cg_const(const CgScalars *S, double rtol) {
+  CgConst c;
+  c.bnorm2 = __ldcg(&S->bnorm2);
+  c.thresh2 = rtol * rtol * c.bnorm2;
+  c.fixed = __ldcg(&S->fixed);
+  c.status = __ldcg(&S->status);
+  return c;
+}
+__device__ __forceinline__ void cg_step_eval_c(const CgConst &c, int k, const double (&d)[5], CgStepOut &o) {
+  const double rho = d[0], rr = d[1], pq = d[2], qz = d[3], qdq = d[4];
+  o.alpha = o.beta = 0.0;
+  o.rho = rho;
+  o.rr = rr;
+  o.done = o.fail = o.early = 0;
+  o.thresh2 = c.thresh2;
+  if (k == 0 && c.status != 0) {
+    o.done = o.early = 1;
+    return;
+  }
+  if (!(rho == rho) || !(rr == rr) || !(pq == pq) || !(qz == qz) || !(qdq == qdq)) {
+    o.fail = -5;
+    o.done = 1;
+    return;
+  }
+  if ((!c.fixed && rr <= o.thresh2) || c.bnorm2 == 0.0) {
+    o.done = 1;
+    return;
+  }
+  if (!(pq > 0.0)) {
+    o.fail = -6;
+    o.done = 1;
+    return;
+  }
+  const double alpha = rho / pq;
+  const double rho_next = fma(alpha * alpha, qdq, fma(-2.0 * alpha, qz, rho));
+  o.alpha = alpha;
+  o.beta = rho_next / rho;
+}
 __device__ __forceinline__ void cg_step_commit(CgScalars *S, int k, const CgStepOut &o, double *hist) {
   if (k == 0) S->thresh2 = o.thresh2;
   if (o.early) {

@@ -392,11 +392,19 @@ k_apply_s3(GridView G, const double *__restrict__ s, const __grid_constant__ S3M
         for (int d = 0; d < 3; ++d) y[3 * c + d] = row[d];
       }
     }
-    // element product in the Hadamard basis (mode m = mx + 2 my + 4 mz), scaled
-    wht8x3(y);
-    had_mid_inplace(H, y);
+    // element product in the Hadamard basis (mode m = mx + 2 my + 4 mz), with
+    // s_e folded into the 10 class coefficients (se = 0 for elements outside
+    // the mesh / segment)
+    K0HadSym Hs;
 #pragma unroll
-    for (int a = 0; a < 24; ++a) y[a] *= se;            // se = 0 for elements outside the mesh / segment
+    for (int b = 0; b < 2; ++b) {
+#pragma unroll
+      for (int t = 0; t < 3; ++t) Hs.d[b][t] = H.d[b][t] * se;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) Hs.o[b][t] = H.o[b][t] * se;
+    }
+    wht8x3(y);
+    had_mid_inplace(Hs, y);
     // inverse transform, z stage: bottom face (plane ek) and top face (plane ek+1)
     double face[12];
 #pragma unroll

@@ -6,6 +6,7 @@
 #include "kernels_cg.cuh"
 #include "kernels_general.cuh"
 #include "kernels_genfused.cuh"
+#include "kernels_gencluster.cuh"
 #include "kernels_struct3d.cuh"
 
 using namespace tomesh;
@@ -58,7 +59,7 @@ int validate(const to_mesh_desc *d) {
     if (f < 0 || f >= d->n_node * d->dim || (i > 0 && f <= d->fixed_dof[i - 1])) { set_error("fixed_dof not ascending / out of range"); return TO_EMESH; }
     if (hang[f / d->dim]) { set_error("fixed DOF %lld is on a hanging node", (long long)f); return TO_EMESH; }
   }
-  if ((d->options & ~(uint32_t)(TO_UPLOAD_GENERAL | TO_UPLOAD_LAUNCHED)) != 0) {
+  if ((d->options & ~(uint32_t)(TO_UPLOAD_GENERAL | TO_UPLOAD_LAUNCHED | TO_UPLOAD_NO_CLUSTER)) != 0) {
     set_error("unknown upload option bits 0x%x", d->options);
     return TO_EINVAL;
   }
@@ -310,24 +311,22 @@ int setup_incidence(const to_mesh_desc *d, const std::vector<int32_t> &node_hang
 // is split in halves until it fits.  Every array is ordered deterministically
 // (elements and halo / hanging nodes ascending), so the decomposition, and
 // with it every summation order, depends on the mesh only.
-int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_hang, const std::vector<int64_t> &iptr,
-                     const std::vector<uint32_t> &inc, cudaStream_t st, to_mesh *m) {
+struct HostBlocks {
+  std::vector<GfMeta> meta;
+  std::vector<uint8_t> rec;
+  std::vector<int32_t> el_id;
+  int max_loc = 0, max_own = 0, max_rec16 = 0, max_el = 0;
+};
+// max_blocks > 0: stop (return 1) as soon as the cut has more ranges.
+int make_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_hang, const std::vector<int64_t> &iptr,
+                    const std::vector<uint32_t> &inc, int64_t N, int own_target, int el_max, int loc_max, int own_max,
+                    int max_blocks, HostBlocks &hb) {
   const int nc = 1 << d->dim;
-  const int64_t N = m->n_owned;   // blocks cover the owned nodes (all, unless a shard's local mesh)
-  // mid-size 3D meshes get smaller blocks, about two per SM slot pair (a
-  // grid that fills the GPU beats the lower halo overhead of big blocks:
-  // 6k / 12k-element octree meshes 16.8 / 17.2 -> 12.1 / 13.9 us per
-  // iteration; c4 unchanged; in 2D it lost, c2 9.0 -> 10.0, so 2D keeps its
-  // target; profiles/r2/general_midsize_ab.txt)
-  const int own_target = d->dim == 3 ? (int)std::max<int64_t>(kGfOwnMin, std::min<int64_t>(kGfOwnTarget3,
-                                                                                           N / (2 * kNumSMs)))
-                                     : kGfOwnTarget2;
-  const int el_max = std::min(kGfElMax, (1 << 14) / nc - 1), loc_max = kGfMaxLoc;   // (incidence encoding: le * 2^dim < 2^14)
   std::vector<int32_t> el_mark(d->n_elem, -1), nd_mark(d->n_node, -1), el_le(d->n_elem, 0), nd_slot(d->n_node, 0);
   int stamp = 0;
   auto elem_of = [&](uint32_t t) { return (int64_t)((t & 0x3fffffffu) / (uint32_t)nc); };
   auto fits = [&](int64_t a, int64_t b) {
-    if (b - a > kGfMaxOwn) return false;
+    if (b - a > own_max) return false;
     const int sp = ++stamp;
     int64_t nE = 0, nOut = 0;
     for (int64_t n = a; n < b; ++n)
@@ -364,6 +363,7 @@ int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_han
       todo.pop_back();
       if (fits(a, b)) {
         node0.push_back((int32_t)a);
+        if (max_blocks > 0 && (int)node0.size() > max_blocks) return 1;
         continue;
       }
       if (b - a <= 2) { set_error("general-path block of node %lld exceeds the kernel limits", (long long)a); return TO_EINVAL; }
@@ -374,10 +374,14 @@ int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_han
     node0.push_back((int32_t)N);
   }
   const int nb = (int)node0.size() - 1;
-  std::vector<GfMeta> meta(nb);
-  std::vector<uint8_t> rec;
-  std::vector<int32_t> el_id;
-  int max_loc = 0, max_own = 0, max_rec16 = 0, max_el = 0;
+  std::vector<GfMeta> &meta = hb.meta;
+  std::vector<uint8_t> &rec = hb.rec;
+  std::vector<int32_t> &el_id = hb.el_id;
+  meta.assign(nb, GfMeta{});
+  rec.clear();
+  el_id.clear();
+  int &max_loc = hb.max_loc, &max_own = hb.max_own, &max_rec16 = hb.max_rec16, &max_el = hb.max_el;
+  max_loc = max_own = max_rec16 = max_el = 0;
   std::vector<int64_t> elems;
   std::vector<int32_t> hl, vt;
   std::vector<uint16_t> iptr_l, inc_l;
@@ -473,49 +477,181 @@ int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_han
     max_el = std::max(max_el, nE);
   }
   if (rec.size() / 16 >= (size_t)INT32_MAX || el_id.size() >= (size_t)INT32_MAX) { set_error("mesh too large for the general-path records"); return TO_EINVAL; }
-  GenBlocks &B = m->GB;
-  B.n_blk = nb;
-  B.max_loc = max_loc;
-  B.max_own = max_own;
-  B.max_rec16 = max_rec16;
-  B.max_el = max_el;
+  return 0;
+}
+
+// Device copies of a decomposition; s_loc (s_e in block-local order, filled
+// per solve by k_gather_s) allocated to match.
+int upload_gen_blocks(to_mesh *m, const HostBlocks &hb, GenBlocks &B, int32_t **el_id, int64_t *n_loc_el,
+                      double **s_loc, cudaStream_t st) {
+  B.n_blk = (int)hb.meta.size();
+  B.max_loc = hb.max_loc;
+  B.max_own = hb.max_own;
+  B.max_rec16 = hb.max_rec16;
+  B.max_el = hb.max_el;
   GfMeta *dmeta;
   uint4 *drec;
-  int32_t *deid;
-  RC(upload_array(m, &dmeta, meta.data(), meta.size(), st));
-  RC(upload_array(m, &drec, reinterpret_cast<const uint4 *>(rec.data()), rec.size() / 16, st));
-  RC(upload_array(m, &deid, el_id.data(), el_id.size(), st));
+  RC(upload_array(m, &dmeta, hb.meta.data(), hb.meta.size(), st));
+  RC(upload_array(m, &drec, reinterpret_cast<const uint4 *>(hb.rec.data()), hb.rec.size() / 16, st));
+  RC(upload_array(m, el_id, hb.el_id.data(), hb.el_id.size(), st));
   B.meta = dmeta;
   B.rec = drec;
-  m->gb_el_id = deid;
-  m->gb_n_loc_el = (int64_t)el_id.size();
-  RC(m->alloc(&m->s_loc, (size_t)std::max<int64_t>(2, m->gb_n_loc_el)));
-  m->gb_smem = d->dim == 3 ? gf_smem_bytes<3>(max_rec16, max_el, max_loc, max_own)
-                           : gf_smem_bytes<2>(max_rec16, max_el, max_loc, max_own);
-  // the attribute is per function, not per handle: allow the device's opt-in
-  // maximum (less the kernel's static shared memory) so that a later upload
-  // of a smaller mesh cannot lower it below what an earlier handle launches with
+  *n_loc_el = (int64_t)hb.el_id.size();
+  RC(m->alloc(s_loc, (size_t)std::max<int64_t>(2, *n_loc_el)));
+  return 0;
+}
+
+// the attribute is per function, not per handle: allow the device's opt-in
+// maximum (less the kernel's static shared memory) so that a later upload of
+// a smaller mesh cannot lower it below what an earlier handle launches with
+int allow_smem(to_mesh *m, const void *fn, size_t need) {
   int optin = 0;
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
-  auto allow = [&](const void *fn) -> int {
-    cudaFuncAttributes fa{};
-    CK(cudaFuncGetAttributes(&fa, fn));
-    const int dyn = optin - (int)fa.sharedSizeBytes;
-    if (m->gb_smem > (size_t)dyn) { set_error("general-path blocks need %zu bytes of shared memory", m->gb_smem); return TO_EINVAL; }
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
-    return 0;
-  };
+  cudaFuncAttributes fa{};
+  CK(cudaFuncGetAttributes(&fa, fn));
+  const int dyn = optin - (int)fa.sharedSizeBytes;
+  if (need > (size_t)dyn) { set_error("general-path blocks need %zu bytes of shared memory", need); return TO_EINVAL; }
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+  return 0;
+}
+
+int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_hang, const std::vector<int64_t> &iptr,
+                     const std::vector<uint32_t> &inc, cudaStream_t st, to_mesh *m) {
+  const int nc = 1 << d->dim;
+  const int64_t N = m->n_owned;   // blocks cover the owned nodes (all, unless a shard's local mesh)
+  // mid-size 3D meshes get smaller blocks, about two per SM slot pair (a
+  // grid that fills the GPU beats the lower halo overhead of big blocks:
+  // 6k / 12k-element octree meshes 16.8 / 17.2 -> 12.1 / 13.9 us per
+  // iteration; c4 unchanged; in 2D it lost, c2 9.0 -> 10.0, so 2D keeps its
+  // target; profiles/r2/general_midsize_ab.txt)
+  const int own_target = d->dim == 3 ? (int)std::max<int64_t>(kGfOwnMin, std::min<int64_t>(kGfOwnTarget3,
+                                                                                           N / (2 * kNumSMs)))
+                                     : kGfOwnTarget2;
+  // (incidence encoding: le * 2^dim < 2^14)
+  HostBlocks hb;
+  RC(make_gen_blocks(d, node_hang, iptr, inc, N, own_target, std::min(kGfElMax, (1 << 14) / nc - 1), kGfMaxLoc,
+                     kGfMaxOwn, 0, hb));
+  GenBlocks &B = m->GB;
+  RC(upload_gen_blocks(m, hb, B, &m->gb_el_id, &m->gb_n_loc_el, &m->s_loc, st));
+  const int nb = B.n_blk;
+  m->gb_smem = d->dim == 3 ? gf_smem_bytes<3>(B.max_rec16, B.max_el, B.max_loc, B.max_own)
+                           : gf_smem_bytes<2>(B.max_rec16, B.max_el, B.max_loc, B.max_own);
   if (d->dim == 3) {
-    RC(allow((const void *)k_gen_fused<3, G_CG>));
-    RC(allow((const void *)k_gen_fused<3, G_PLAIN>));
-    RC(allow((const void *)k_gen_persist<3>));
+    RC(allow_smem(m, (const void *)k_gen_fused<3, G_CG>, m->gb_smem));
+    RC(allow_smem(m, (const void *)k_gen_fused<3, G_PLAIN>, m->gb_smem));
+    RC(allow_smem(m, (const void *)k_gen_persist<3>, m->gb_smem));
   } else {
-    RC(allow((const void *)k_gen_fused<2, G_CG>));
-    RC(allow((const void *)k_gen_fused<2, G_PLAIN>));
-    RC(allow((const void *)k_gen_persist<2>));
+    RC(allow_smem(m, (const void *)k_gen_fused<2, G_CG>, m->gb_smem));
+    RC(allow_smem(m, (const void *)k_gen_fused<2, G_PLAIN>, m->gb_smem));
+    RC(allow_smem(m, (const void *)k_gen_persist<2>, m->gb_smem));
   }
   RC(ensure_partials(m, (size_t)nb * 5));
   m->gen_fused = true;
+  return 0;
+}
+
+const void *gc_kernel(int dim, int T) {
+  if (dim == 2) return T == 128 ? (const void *)k_gen_cluster<2, 128> : T == 256 ? (const void *)k_gen_cluster<2, 256>
+                                                                              : (const void *)k_gen_cluster<2, 512>;
+  return T == 128 ? (const void *)k_gen_cluster<3, 128> : T == 256 ? (const void *)k_gen_cluster<3, 256>
+                                                                   : (const void *)k_gen_cluster<3, 512>;
+}
+size_t gc_smem(int dim, int T, const HostBlocks &hb, int max_halo, int max_send) {
+  auto f = [&](auto lay) { return lay(hb.max_rec16, hb.max_el, hb.max_loc, hb.max_own, max_halo, max_send).total; };
+  if (dim == 2) return T == 128 ? f(gc_layout<2, 128>) : T == 256 ? f(gc_layout<2, 256>) : f(gc_layout<2, 512>);
+  return T == 128 ? f(gc_layout<3, 128>) : T == 256 ? f(gc_layout<3, 256>) : f(gc_layout<3, 512>);
+}
+
+// Small meshes: a second decomposition into at most kGcMaxBlocks blocks for
+// the cluster-resident solver (kernels_gencluster.cuh), if one cluster of
+// that many CTAs with the state of its owned nodes in shared memory fits
+// (shared memory, and a cluster placement the device reports possible).
+// Leaves m->gen_cluster false otherwise.
+int build_gen_cluster(const to_mesh_desc *d, const std::vector<int32_t> &node_hang, const std::vector<int64_t> &iptr,
+                      const std::vector<uint32_t> &inc, cudaStream_t st, to_mesh *m) {
+  const int nc = 1 << d->dim;
+  const int64_t N = m->n_owned;
+  if (N > (int64_t)kGcMaxBlocks * kGcMaxOwn) return 0;
+  const int64_t nb_t = std::min<int64_t>(kGcMaxBlocks, std::max<int64_t>(1, (N + kGcOwnMin - 1) / kGcOwnMin));
+  const int own_target = (int)((N + nb_t - 1) / nb_t);
+  // 2 T >= the target; beyond 512 owned nodes per CTA (T = 512) one kernel
+  // per iteration over the whole GPU is faster (c2: 1,184 nodes per CTA,
+  // 10.7 us per iteration in the cluster against 8.6 launched)
+  if (own_target > kGcOwnMaxTarget) return 0;
+  const int T = own_target <= 256 ? 128 : own_target <= 512 ? 256 : 512;
+  HostBlocks hb;
+  const int rc = make_gen_blocks(d, node_hang, iptr, inc, N, own_target, (1 << 14) / nc - 1, 0xfffe,
+                                 kGcOwnPerThread * T, kGcMaxBlocks, hb);
+  if (rc == 1) return 0;     // the limits split it into more blocks than one cluster holds
+  RC(rc);
+  // send lists: for every halo node of block b (index i in b's halo list), an
+  // entry in its owner's list; each list sorted by (destination, index)
+  const int nbk = (int)hb.meta.size();
+  std::vector<std::vector<uint32_t>> lists(nbk);
+  int max_halo = 0;
+  for (int b = 0; b < nbk; ++b) {
+    const GfMeta &mb = hb.meta[b];
+    max_halo = std::max(max_halo, mb.n_halo);
+    const int32_t *hl = reinterpret_cast<const int32_t *>(hb.rec.data() + (size_t)16 * mb.rec_off16);   // section 0
+    for (int i = 0; i < mb.n_halo; ++i) {
+      const int32_t g = hl[i];
+      int o = 0;
+      while (o + 1 < nbk && hb.meta[o + 1].node0 <= g) ++o;
+      const int src = g - hb.meta[o].node0;
+      if (o == b || src < 0 || src >= hb.meta[o].n_own || src > 0xfff || i > 0x7fff) {
+        set_error("internal: cluster send list (block %d, halo %d)", b, i);
+        return TO_EINVAL;
+      }
+      lists[o].push_back((uint32_t)src | ((uint32_t)i << 12) | ((uint32_t)b << 27));
+    }
+  }
+  std::vector<uint32_t> ent;
+  std::vector<int32_t> off(1, 0);
+  int max_send = 0;
+  for (int o = 0; o < nbk; ++o) {
+    std::sort(lists[o].begin(), lists[o].end(), [](uint32_t a, uint32_t b) {
+      return (a >> 27) != (b >> 27) ? (a >> 27) < (b >> 27) : ((a >> 12) & 0x7fff) < ((b >> 12) & 0x7fff);
+    });
+    ent.insert(ent.end(), lists[o].begin(), lists[o].end());
+    off.push_back((int32_t)ent.size());
+    max_send = std::max(max_send, (int)lists[o].size());
+  }
+  const size_t smem = gc_smem(d->dim, T, hb, max_halo, max_send);
+  const void *fn = gc_kernel(d->dim, T);
+  int optin = 0;
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
+  cudaFuncAttributes fa{};
+  CK(cudaFuncGetAttributes(&fa, fn));
+  if (smem > (size_t)(optin - (int)fa.sharedSizeBytes)) return 0;
+  RC(allow_smem(m, fn, smem));
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  const int nb = (int)hb.meta.size();
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)nb;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(nb);
+  cfg.blockDim = dim3(T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nclu = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclu, fn, &cfg) != cudaSuccess || nclu < 1) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  RC(upload_gen_blocks(m, hb, m->GC, &m->gc_el_id, &m->gc_n_loc_el, &m->gc_s_loc, st));
+  uint32_t *dent;
+  int32_t *doff;
+  if (ent.empty()) ent.push_back(0u);   // (a single-block cluster sends nothing)
+  RC(upload_array(m, &dent, ent.data(), ent.size(), st));
+  RC(upload_array(m, &doff, off.data(), off.size(), st));
+  m->GCS = GcSend{dent, doff, max_halo, max_send};
+  m->gc_smem = smem;
+  m->gc_threads = T;
+  m->gen_cluster = true;
   return 0;
 }
 
@@ -628,6 +764,10 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
     std::vector<uint32_t> incv;
     RC(setup_incidence(d, node_hang, st, m, iptr, incv));
     RC(build_gen_blocks(d, node_hang, iptr, incv, st, m));
+    // the smallest meshes: one thread-block cluster holds the whole solve
+    // (k_gen_cluster), unless TO_UPLOAD_LAUNCHED / NO_CLUSTER or a shard's local mesh
+    if (!(d->options & (TO_UPLOAD_LAUNCHED | TO_UPLOAD_NO_CLUSTER)) && d->n_owned == 0)
+      RC(build_gen_cluster(d, node_hang, iptr, incv, st, m));
     // small meshes (at most kGfPersistMaxBlocks blocks): the whole loop in one
     // cooperative kernel, unless TO_UPLOAD_LAUNCHED.  Measured: c1 (6 blocks)
     // 5.8 vs 6.9 us per iteration launched; c2 (85 blocks) 13.8 vs 9.0 -- the
@@ -635,7 +775,8 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
     // PDL-chained launches once there are more than a few dozen blocks
     int coop = 0;
     CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
-    if (coop && !(d->options & TO_UPLOAD_LAUNCHED) && d->n_owned == 0 && m->GB.n_blk <= kGfPersistMaxBlocks) {
+    if (coop && !m->gen_cluster && !(d->options & TO_UPLOAD_LAUNCHED) && d->n_owned == 0 &&
+        m->GB.n_blk <= kGfPersistMaxBlocks) {
       int per_sm = 0;
       const void *fn = d->dim == 2 ? (const void *)k_gen_persist<2> : (const void *)k_gen_persist<3>;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGfThreads, m->gb_smem));
@@ -762,6 +903,10 @@ int op_scale_and_diag(to_mesh *m, double penal, const double *x, double *d_int, 
     RC(launch_diag(m, d_int, st));
     k_gather_s<<<grid_for(m->gb_n_loc_el), kBlock, 0, st>>>(m->gb_n_loc_el, m->gb_el_id, m->s, m->s_loc);
     m->last_launches++;
+    if (m->gen_cluster) {
+      k_gather_s<<<grid_for(m->gc_n_loc_el), kBlock, 0, st>>>(m->gc_n_loc_el, m->gc_el_id, m->s, m->gc_s_loc);
+      m->last_launches++;
+    }
     return check_launch();
   }
   k_simp_s3<<<grid_for(m->n_el), kBlock, 0, st>>>(m->n_el, x, m->perm_el, penal, m->E0, m->Emin, m->h_struct,
@@ -906,7 +1051,8 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   RC(op_scale_and_diag(m, penal, x_dev, nullptr, st));
   // single-kernel iterations (launched, or the general path's cooperative
   // kernel for small meshes): iteration 0 reads r0 = b from rb[1]
-  const bool persistent = !m->structured && m->gen_persist;
+  const bool cluster = !m->structured && m->gen_cluster;
+  const bool persistent = !m->structured && !cluster && m->gen_persist;
   double *r0 = m->rb[1];
   if (!m->structured) {   // q_{-1} = p_{-1} = 0 (finite whatever an earlier solve left)
     CK(cudaMemsetAsync(m->qb[1], 0, sizeof(double) * n, st));
@@ -961,6 +1107,33 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
     stop = true;
     launched = max_iter;
   }
+  if (cluster && !stop) {
+    // the whole loop in one thread-block cluster (kernels_gencluster.cuh)
+    if (prof) CK(cudaEventRecord(m->prof_ev[0], st));
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)m->GC.n_blk;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(m->GC.n_blk);
+    cfg.blockDim = dim3(m->gc_threads);
+    cfg.dynamicSmemBytes = m->gc_smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const double *sl = m->gc_s_loc, *dv = m->dinv;
+    int mi = max_iter;
+    double rt = rtol;
+    void *args[] = {&m->GC, &m->GCS, &sl, &m->rb[0], &m->rb[1], &m->pb[0], &m->pb[1], &m->qb[0], &m->qb[1], &dv,
+                    &m->x, &m->K2, &m->KS, &m->S, &mi, &rt, &m->hist};
+    CK(cudaLaunchKernelExC(&cfg, gc_kernel(m->dim, m->gc_threads), args));
+    m->last_launches++;
+    if (prof) CK(cudaEventRecord(m->prof_ev[1], st));
+    if (prof) CK(cudaEventRecord(m->prof_ev[2], st));
+    stop = true;
+    launched = max_iter;
+  }
   while (!stop && launched < max_iter) {
     int cnt = std::min(chunk, max_iter - launched);
     for (int k = 0; k < cnt; ++k) {
@@ -1003,7 +1176,7 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   if (prof) {
     for (int j = 0; j < 5; ++j) m->prof_ms[j] = 0.0;
     int nit = std::min(launched, res.iter);
-    for (int it = 0; it < (persistent ? std::min(nit, 1) : nit); ++it) {
+    for (int it = 0; it < (persistent || cluster ? std::min(nit, 1) : nit); ++it) {
       const int slot[2] = {0, 2};   // K1 (p/x update + apply + alpha), K2 (r update + reductions)
       for (int j = 0; j < 2; ++j) {
         float t = 0.f;
@@ -1091,7 +1264,7 @@ extern "C" int tomesh_get_info(const to_mesh *m, to_mesh_info *info) {
   info->filt_nnz = m->filt_nnz;
   info->device_bytes = m->dev_bytes;
   info->kernel_launches = m->last_launches;
-  info->matvec_variant = m->structured ? 1 : m->gen_persist ? 3 : 4;
+  info->matvec_variant = m->structured ? 1 : m->gen_cluster ? 5 : m->gen_persist ? 3 : 4;
   info->launches_total = m->launches_total;
   return 0;
 }

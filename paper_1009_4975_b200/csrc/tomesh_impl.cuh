@@ -62,6 +62,15 @@ struct to_mesh {
   int64_t gb_n_loc_el = 0;
   double *s_loc = nullptr;             // s_e in block-local element order
   size_t gb_smem = 0;                  // dynamic shared memory of k_gen_fused
+  // small meshes: the whole loop in one thread-block cluster (kernels_gencluster.cuh)
+  bool gen_cluster = false;
+  GenBlocks GC{};                      // its decomposition (at most kGcMaxBlocks blocks)
+  GcSend GCS{};                        // and the send lists of its halo exchange
+  int32_t *gc_el_id = nullptr;
+  int64_t gc_n_loc_el = 0;
+  double *gc_s_loc = nullptr;
+  size_t gc_smem = 0;
+  int gc_threads = 0;                  // its CTA size
   int32_t *filt_idx = nullptr;
   // OC update (allocated on first use)
   double *oc_a = nullptr, *oc_part = nullptr;

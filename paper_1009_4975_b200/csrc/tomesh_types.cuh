@@ -53,6 +53,15 @@ struct GenBlocks {
   const uint4 *rec;
 };
 
+// Send lists of the cluster solver's halo exchange (kernels_gencluster.cuh),
+// built at upload: entry = src owned node (12 bits) | index in the
+// destination's halo list (15 bits) << 12 | destination rank (4 bits) << 27.
+struct GcSend {
+  const uint32_t *ent;
+  const int32_t *off;   // [n_blk + 1]
+  int max_halo, max_send;
+};
+
 __host__ __device__ constexpr int gf_pad16(int bytes) { return (bytes + 15) & ~15; }
 
 // Structured path (kernels_struct3d.cuh): the uniform H8 box and its CTA grid.

@@ -24,7 +24,9 @@ CASES = {
     "c5s": lambda: config("c5", nx=20, ny=10, nz=10),
     "c5s_general": lambda: config("c5", nx=20, ny=10, nz=10),     # uniform H8 forced onto the general path
     "c3s_ragged": lambda: config("c3", nx=37, ny=9, nz=13),       # several CTA tiles + ragged tails in x, y, z
-    "c1_launched": lambda: config("c1"),     # one launch per iteration (default for c1: the cooperative kernel)
+    "c1_launched": lambda: config("c1"),     # one launch per iteration (default for c1: the cluster solver)
+    "c1_coop": lambda: config("c1"),         # the whole loop in one cooperative kernel (k_gen_persist)
+    "c2_launched": lambda: config("c2"),
     "amr2d": lambda: cantilever2d((5, 3), L=3, leaves=refine_some(2, (5, 3), 3, [(1, 1), (3, 0)]), rmin=0.3),
     "amr3d": lambda: cantilever3d((3, 2, 2), L=2, leaves=refine_some(3, (3, 2, 2), 2, [(1, 1, 0)]), rmin=0.4),
     "hload2d": hanging_load2d,       # loads on hanging nodes (C8): b = Pi_F C^T f, c = f^T u with them
@@ -40,10 +42,15 @@ def _setup(name):
         om = omesh.build_mesh(prob)
         import paper_1009_4975_b200 as pb
         opts = (pb.TO_UPLOAD_GENERAL if name.endswith("_general") else 0) | \
-               (pb.TO_UPLOAD_LAUNCHED if name.endswith("_launched") else 0)
+               (pb.TO_UPLOAD_LAUNCHED if name.endswith("_launched") else 0) | \
+               (pb.TO_UPLOAD_NO_CLUSTER if name.endswith("_coop") else 0)
         hm, m = product_mesh(prob, options=opts)
         if name.startswith(("c3s", "c5s")):
             assert m.info()["structured"] == (0 if name.endswith("_general") else 1)
+        # which device path runs the loop (include/tomesh.h matvec_variant)
+        want = {"c1": 5, "c2": 4, "c1_launched": 4, "c2_launched": 4, "c1_coop": 3, "amr2d": 5, "hload2d": 5}
+        if name in want:
+            assert m.info()["matvec_variant"] == want[name], (name, m.info())
         x_dev = product_input_density(prob, hm, m)
         _cache[name] = (prob, om, hm, m, x_dev)
     return _cache[name]
@@ -115,7 +122,7 @@ def test_L2_converged_solve(name):
     assert abs(st.iters - ref.cg.iters) <= max(5, 0.05 * ref.cg.iters)
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c1_launched", "c5s"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c1_launched", "c1_coop", "c5s"])
 def test_warm_start_and_fixed_iterations(name):
     prob, om, hm, m, x_dev = _setup(name)
     u = torch.zeros(om.n_dof, dtype=torch.float64, device="cuda")
@@ -168,7 +175,7 @@ def test_solver_edge_cases(name):
     assert abs(st.relres_true - st.relres) <= 1e-6 * st.relres
 
 
-@pytest.mark.parametrize("name", ["c4s", "amr3d", "c1_launched", "c1"])
+@pytest.mark.parametrize("name", ["c4s", "amr3d", "c1_launched", "c1", "c2"])
 def test_upload_is_deterministic(name):
     """Two uploads of the same mesh solve to bit-identical u: nothing at upload
     depends on timing (no timing-based kernel or grid choice), and every

@@ -1,6 +1,6 @@
-"""us per PCG iteration of the small 2D configs on both 2D paths (the
-persistent cooperative solver and the one-kernel-per-iteration general
-kernel), fixed iterations.
+"""us per PCG iteration of the small configs on the general-path variants
+(the cluster-resident solver, the persistent cooperative kernel and one
+kernel per iteration), fixed iterations.
 
     python tools/small_cfg.py [c1 c2]
 """
@@ -17,7 +17,7 @@ from inputs import config, density_at  # noqa: E402
 for name in sys.argv[1:] or ["c1", "c2"]:
     prob = config(name)
     hm = pb.prepare(prob)
-    for opts in (0, pb.TO_UPLOAD_LAUNCHED):
+    for opts in (0, pb.TO_UPLOAD_NO_CLUSTER, pb.TO_UPLOAD_LAUNCHED):
         m = pb.Mesh(hm, E0=prob.E0, Emin=prob.Emin, nu=prob.nu, rmin=prob.rmin, options=opts)
         x = torch.as_tensor(density_at(prob, hm.elem_level, hm.elem_anchor), device="cuda")
         u = torch.zeros(hm.n_dof, dtype=torch.float64, device="cuda")
