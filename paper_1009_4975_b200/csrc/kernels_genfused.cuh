@@ -52,6 +52,11 @@ constexpr int kGfOwnPerThread = 2;                       // owned nodes per thre
 constexpr int kGfMaxOwn = kGfThreads * kGfOwnPerThread;
 constexpr int kGfMaxLoc = 1536;                          // local node slots per block (uint16 slots)
 constexpr int kGfPersistMaxBlocks = 32;                  // k_gen_persist only up to this many blocks
+// Launched path: every block evaluates the previous step itself (no step
+// kernel) up to this many blocks; beyond, the O(blocks^2) partial reads cost
+// more than the step launch (c2, 85 blocks: 8.98 -> 8.07 us per iteration;
+// c4, 1,131 blocks: 62.4 -> 78.2; c4L, 7,099 blocks: 320 -> 772)
+constexpr int kGfStepInMaxBlocks = 256;
 #ifndef TOMESH_GF_OWN3
 #define TOMESH_GF_OWN3 224      // A/B on c4 / c4L: 224 < 320 < 448 < 512 (us per iteration)
 #endif
@@ -256,16 +261,47 @@ __device__ __forceinline__ void gf_issue_record(const GenBlocks &B, const GfView
 template <bool COH>
 __device__ __forceinline__ double gf_ld(const double *p) { return COH ? __ldcg(p) : __ldg(p); }
 
+// The owned nodes' r, q, p, Dinv of one block (o = tid + u * kGfThreads),
+// loaded ahead of the step evaluation in k_gen_fused (they do not depend on
+// alpha, beta): gf_block_iter<..., PRE = true> takes them from here.
+template <int DIM>
+struct GfOwned {
+  double r[kGfOwnPerThread][DIM], q[kGfOwnPerThread][DIM], p[kGfOwnPerThread][DIM], d[kGfOwnPerThread][DIM];
+};
+template <int DIM, bool COH>
+__device__ __forceinline__ void gf_load_owned(const GfMeta &mt, const double *__restrict__ ro,
+                                              const double *__restrict__ qo, const double *__restrict__ po,
+                                              const double *__restrict__ Dinv, GfOwned<DIM> &w) {
+  const int64_t g0 = (int64_t)mt.node0 * DIM;
+#pragma unroll
+  for (int u = 0; u < kGfOwnPerThread; ++u) {
+    const int o = threadIdx.x + u * kGfThreads;
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) {
+      w.r[u][i] = w.q[u][i] = w.p[u][i] = w.d[u][i] = 0.0;
+      if (o < mt.n_own) {
+        const int64_t g = g0 + (int64_t)o * DIM + i;
+        w.r[u][i] = gf_ld<COH>(ro + g);
+        w.q[u][i] = gf_ld<COH>(qo + g);
+        w.p[u][i] = gf_ld<COH>(po + g);
+        w.d[u][i] = __ldg(Dinv + g);
+      }
+    }
+  }
+}
+
 // One PCG iteration of one block (steps 1-4 of the header comment); the
 // block's dots (unreduced, per thread) in `dots`.  wait_rec: the record's
 // mbarrier phase is still outstanding (first iteration of the kernel).
-template <int DIM, int MODE, bool COH>
+// PRE: the owned r, q, p, Dinv come preloaded in `pre` (CG mode).
+template <int DIM, int MODE, bool COH, bool PRE = false>
 __device__ __forceinline__ void gf_block_iter(const GfView &V, bool wait_rec, const double *__restrict__ ro,
                                               const double *__restrict__ qo, const double *__restrict__ po,
                                               const double *__restrict__ Dinv, double *__restrict__ rw,
                                               double *__restrict__ pw, double *__restrict__ qw,
                                               double *__restrict__ x, const K0Dense2 &K2, const K0HadSym &H,
-                                              double alpha, double beta, double (&dots)[5]) {
+                                              double alpha, double beta, double (&dots)[5],
+                                              const GfOwned<DIM> *pre = nullptr) {
   constexpr bool CG = MODE == G_CG;
   constexpr int NC = 1 << DIM, ND = NC * DIM, CH = GfChunk<DIM>::CH, YS = GfChunk<DIM>::YS;
   constexpr int OPT = kGfOwnPerThread;
@@ -289,10 +325,17 @@ __device__ __forceinline__ void gf_block_iter(const GfView &V, bool wait_rec, co
       double r_o[DIM], q_o[DIM], p_o[DIM], d_o[DIM];
 #pragma unroll
       for (int i = 0; i < DIM; ++i) {
-        r_o[i] = gf_ld<COH>(ro + g + i);
-        q_o[i] = gf_ld<COH>(qo + g + i);
-        p_o[i] = gf_ld<COH>(po + g + i);
-        d_o[i] = __ldg(Dinv + g + i);
+        if (PRE) {
+          r_o[i] = pre->r[u][i];
+          q_o[i] = pre->q[u][i];
+          p_o[i] = pre->p[u][i];
+          d_o[i] = pre->d[u][i];
+        } else {
+          r_o[i] = gf_ld<COH>(ro + g + i);
+          q_o[i] = gf_ld<COH>(qo + g + i);
+          p_o[i] = gf_ld<COH>(po + g + i);
+          d_o[i] = __ldg(Dinv + g + i);
+        }
       }
 #pragma unroll
       for (int i = 0; i < DIM; ++i) {
@@ -445,13 +488,42 @@ __device__ __forceinline__ void gf_block_iter(const GfView &V, bool wait_rec, co
   dots[4] = qdq;
 }
 
+// The blocks' dots of one launch summed in a fixed order (thread t takes
+// blocks t, t + blockDim, ...; then block_sum): every caller with the same
+// blockDim gets the same bits.  Block-wide (barriers); the sums in warp 0.
+__device__ __forceinline__ void gf_step_sum(const double *part, int nb, double (&d)[5]) {
+#pragma unroll
+  for (int k = 0; k < 5; ++k) d[k] = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) d[k] += __ldcg(&part[(size_t)5 * b + k]);
+  block_sum<5>(d);
+}
+
+// This block's dots (summed in a fixed order by the next launch / k_gen_step).
+__device__ __forceinline__ void gf_block_dots(double (&dots)[5], double *partials, int nbk, int kit, int step_in) {
+  block_sum<5>(dots);
+  double *pk = partials + (step_in ? (size_t)5 * nbk * (kit & 1) : 0);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) pk[(size_t)5 * blockIdx.x + k] = dots[k];
+}
+
+// step_in = 1 (the unsharded solve): the step of iteration kit-1 is evaluated
+// at the start of this launch by EVERY block from the previous launch's
+// block dots (partials[(kit-1) & 1], the same sum and the same cg_step_eval
+// everywhere, so every block takes the same alpha, beta and stop decision);
+// block 0 commits it to S.  This launch's dots go to partials[kit & 1].  One
+// launch per iteration; k_gen_step evaluates the last step after the loop.
+// step_in = 0 (the shard group, kernels_gshard.cuh): alpha, beta from S,
+// dots to partials[0..nb).
 template <int DIM, int MODE>
 __global__ void __launch_bounds__(kGfThreads, TOMESH_GF_MINB)
 k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_loc, const double *__restrict__ ro,
             const double *__restrict__ qo, const double *__restrict__ po, const double *__restrict__ Dinv,
             double *__restrict__ rw, double *__restrict__ pw, double *__restrict__ qw, double *__restrict__ x,
             const __grid_constant__ K0Dense2 K2, const __grid_constant__ K0HadSym H, CgScalars *S,
-            double *partials, int kit, double rtol, double *hist) {
+            double *partials, int kit, double rtol, double *hist, int step_in) {
   constexpr bool CG = MODE == G_CG;
   extern __shared__ __align__(16) unsigned char gsm_raw[];
   const int tid = threadIdx.x;
@@ -472,23 +544,41 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
     return;
   }
   GF_MARK(1);
-  const double alpha = CG ? __ldcg(&S->alpha) : 0.0;
-  const double beta = CG ? __ldcg(&S->beta) : 0.0;
+  double alpha = CG ? __ldcg(&S->alpha) : 0.0;
+  double beta = CG ? __ldcg(&S->beta) : 0.0;
+  const int nbk = (int)gridDim.x;
+  if (CG && step_in && kit > 0) {
+    // the owned vectors do not depend on the step: their loads are in flight
+    // while the step is evaluated
+    GfOwned<DIM> pre;
+    gf_load_owned<DIM, false>(mt, ro, qo, po, Dinv, pre);
+    __shared__ double s_st[3];
+    double d[5];
+    gf_step_sum(partials + (size_t)5 * nbk * ((kit - 1) & 1), nbk, d);
+    if (tid == 0) {
+      CgStepOut so;
+      cg_step_eval(S, kit - 1, d, rtol, so);
+      if (blockIdx.x == 0) cg_step_commit(S, kit - 1, so, hist);
+      s_st[0] = so.alpha;
+      s_st[1] = so.beta;
+      s_st[2] = so.done ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (s_st[2] != 0.0) {
+      mbar_wait(V.bar, 0);
+      return;
+    }
+    alpha = s_st[0];
+    beta = s_st[1];
+    double dots[5];
+    gf_block_iter<DIM, MODE, false, true>(V, true, ro, qo, po, Dinv, rw, pw, qw, x, K2, H, alpha, beta, dots, &pre);
+    gf_block_dots(dots, partials, nbk, kit, step_in);
+    return;
+  }
   double dots[5];
   gf_block_iter<DIM, MODE, false>(V, true, ro, qo, po, Dinv, rw, pw, qw, x, K2, H, alpha, beta, dots);
   GF_MARK(5);
-#ifdef TOMESH_GF_GRIDSUM
-  if (CG) {
-    if (grid_sum<5>(dots, partials, &S->counter[CNT_PQ])) cg_single_step(S, kit, dots, rtol, hist);
-  }
-#else
-  if (CG) {   // this block's dots; k_gen_step sums the blocks in a fixed order
-    block_sum<5>(dots);
-    if (tid == 0)
-#pragma unroll
-      for (int k = 0; k < 5; ++k) partials[(size_t)5 * blockIdx.x + k] = dots[k];
-  }
-#endif
+  if (CG) gf_block_dots(dots, partials, nbk, kit, step_in);
   GF_MARK(6);
 }
 
@@ -545,18 +635,17 @@ k_gen_persist(const __grid_constant__ GenBlocks B, const double *__restrict__ s_
 // The step of general-path iteration k: the blocks' dots summed in block
 // order (thread t adds blocks t, t + 512, ... then a fixed tree), then
 // cg_single_step (alpha_k, beta_k, stop test).  One CTA.
-static __global__ void __launch_bounds__(512) k_gen_step(int nb, const double *__restrict__ partials, CgScalars *S,
-                                                          int kit, double rtol, double *hist) {
+// The step of iteration kit from the block dots at `partials` (every
+// iteration on large grids; after the last launch of a solve on small ones).
+static __global__ void __launch_bounds__(512) k_gen_step(int nb, const double *__restrict__ partials,
+                                                                CgScalars *S, int kit, double rtol, double *hist) {
   pdl_wait();
   if (cg_stopped(S)) {
     pdl_release();
     return;
   }
-  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  for (int b = threadIdx.x; b < nb; b += blockDim.x)
-#pragma unroll
-    for (int k = 0; k < 5; ++k) acc[k] += __ldcg(&partials[(size_t)5 * b + k]);
-  block_sum<5>(acc);
+  double acc[5];
+  gf_step_sum(partials, nb, acc);
   if (threadIdx.x == 0) cg_single_step(S, kit, acc, rtol, hist);
   __syncthreads();
   pdl_release();

@@ -545,7 +545,7 @@ int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_han
     RC(allow_smem(m, (const void *)k_gen_fused<2, G_PLAIN>, m->gb_smem));
     RC(allow_smem(m, (const void *)k_gen_persist<2>, m->gb_smem));
   }
-  RC(ensure_partials(m, (size_t)nb * 5));
+  RC(ensure_partials(m, (size_t)nb * 10));   // dots of two launches (parity)
   m->gen_fused = true;
   return 0;
 }
@@ -855,12 +855,12 @@ int launch_matvec(to_mesh *m, const double *p, double *q, cudaStream_t st) {
     RC(launch_pdl(k_gen_fused<2, G_PLAIN>, dim3(m->GB.n_blk), dim3(kGfThreads), m->gb_smem, st, m->GB,
                   (const double *)m->s_loc, (const double *)nullptr, (const double *)nullptr, p,
                   (const double *)nullptr, (double *)nullptr, (double *)nullptr, q, (double *)nullptr, m->K2, m->KS,
-                  (CgScalars *)nullptr, (double *)nullptr, 0, 0.0, (double *)nullptr));
+                  (CgScalars *)nullptr, (double *)nullptr, 0, 0.0, (double *)nullptr, 0));
   else
     RC(launch_pdl(k_gen_fused<3, G_PLAIN>, dim3(m->GB.n_blk), dim3(kGfThreads), m->gb_smem, st, m->GB,
                   (const double *)m->s_loc, (const double *)nullptr, (const double *)nullptr, p,
                   (const double *)nullptr, (double *)nullptr, (double *)nullptr, q, (double *)nullptr, m->K2, m->KS,
-                  (CgScalars *)nullptr, (double *)nullptr, 0, 0.0, (double *)nullptr));
+                  (CgScalars *)nullptr, (double *)nullptr, 0, 0.0, (double *)nullptr, 0));
   m->last_launches++;
   return check_launch();
 }
@@ -943,29 +943,32 @@ int op_apply(to_mesh *m, const double *in, double *out, cudaStream_t st) {
   return check_launch();
 }
 
-// General path, iteration k (kernels_genfused.cuh): the block kernel, then
-// the one-CTA step kernel (alpha_k, beta_k, stop test).
-int op_cg_gen(to_mesh *m, int k, double rtol, cudaStream_t st) {
+// General path, iteration k (kernels_genfused.cuh): the block kernel.
+// step_in: it evaluates the step of iteration k-1 itself (the unsharded
+// solve; op_cg_gen_step after the loop evaluates the last one); otherwise the
+// shard group's exchange and step kernels follow it.
+int op_cg_gen(to_mesh *m, int k, double rtol, cudaStream_t st, bool step_in) {
   const int o = (k + 1) & 1, w = k & 1;
   if (m->dim == 2)
     RC(launch_pdl(k_gen_fused<2, G_CG>, dim3(m->GB.n_blk), dim3(kGfThreads), m->gb_smem, st, m->GB,
                   (const double *)m->s_loc, (const double *)m->rb[o], (const double *)m->qb[o],
                   (const double *)m->pb[o], (const double *)m->dinv, m->rb[w], m->pb[w], m->qb[w], m->x, m->K2,
-                  m->KS, m->S, m->partials, k, rtol, m->hist));
+                  m->KS, m->S, m->partials, k, rtol, m->hist, step_in ? 1 : 0));
   else
     RC(launch_pdl(k_gen_fused<3, G_CG>, dim3(m->GB.n_blk), dim3(kGfThreads), m->gb_smem, st, m->GB,
                   (const double *)m->s_loc, (const double *)m->rb[o], (const double *)m->qb[o],
                   (const double *)m->pb[o], (const double *)m->dinv, m->rb[w], m->pb[w], m->qb[w], m->x, m->K2,
-                  m->KS, m->S, m->partials, k, rtol, m->hist));
+                  m->KS, m->S, m->partials, k, rtol, m->hist, step_in ? 1 : 0));
   m->last_launches++;
   return 0;
 }
-int op_cg_gen_step(to_mesh *m, int k, double rtol, cudaStream_t st) {
-#ifndef TOMESH_GF_GRIDSUM
-  RC(launch_pdl(k_gen_step, dim3(1), dim3(512), 0, st, m->GB.n_blk, (const double *)m->partials, m->S, k, rtol,
+// The step of iteration k from the dots of launch k (partials[k & 1] when
+// the launches evaluate the steps themselves, else partials[0]).
+int op_cg_gen_step(to_mesh *m, int k, double rtol, cudaStream_t st, bool step_in) {
+  RC(launch_pdl(k_gen_step, dim3(1), dim3(512), 0, st, m->GB.n_blk,
+                (const double *)(m->partials + (step_in ? (size_t)5 * m->GB.n_blk * (k & 1) : 0)), m->S, k, rtol,
                 m->hist));
   m->last_launches++;
-#endif
   return 0;
 }
 
@@ -1053,6 +1056,8 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   // kernel for small meshes): iteration 0 reads r0 = b from rb[1]
   const bool cluster = !m->structured && m->gen_cluster;
   const bool persistent = !m->structured && !cluster && m->gen_persist;
+  // launched general path: the step inside the block kernel for small grids
+  const bool step_in = !m->structured && m->GB.n_blk <= kGfStepInMaxBlocks;
   double *r0 = m->rb[1];
   if (!m->structured) {   // q_{-1} = p_{-1} = 0 (finite whatever an earlier solve left)
     CK(cudaMemsetAsync(m->qb[1], 0, sizeof(double) * n, st));
@@ -1143,10 +1148,14 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
         RC(op_cg_s3(m, launched + k, rtol, st));
         if (prof) CK(cudaEventRecord(E[1], st));
         if (prof) CK(cudaEventRecord(E[2], st));
-      } else {
-        RC(op_cg_gen(m, launched + k, rtol, st));
+      } else if (step_in) {
+        RC(op_cg_gen(m, launched + k, rtol, st, true));
         if (prof) CK(cudaEventRecord(E[1], st));
-        RC(op_cg_gen_step(m, launched + k, rtol, st));
+        if (prof) CK(cudaEventRecord(E[2], st));
+      } else {
+        RC(op_cg_gen(m, launched + k, rtol, st, false));
+        if (prof) CK(cudaEventRecord(E[1], st));
+        RC(op_cg_gen_step(m, launched + k, rtol, st, false));
         if (prof) CK(cudaEventRecord(E[2], st));
       }
     }
@@ -1158,6 +1167,9 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
       chunk = std::min(chunk * 2, 256);
     }
   }
+  // general path, one launch per iteration: the step of the last launch (a
+  // no-op if the solve has stopped)
+  if (step_in && !persistent && !cluster && launched > 0) RC(op_cg_gen_step(m, launched - 1, rtol, st, true));
   if (loop_prof) CK(cudaEventRecord(m->loop_ev[1], st));
   // x_N after exactly N iterations (a no-op if an iteration already converged)
   if (m->structured) RC(op_final_s3(m, max_iter, rtol, st));

@@ -303,6 +303,6 @@ int op_apply(to_mesh *m, const double *in, double *out, cudaStream_t st);
 int op_recover_out(to_mesh *m, const double *v_int, double *u_canon, cudaStream_t st);
 int op_resid2_x(to_mesh *m, double *r2, cudaStream_t st);
 int plan_s3(to_mesh *m, cudaStream_t st, int z0, int z1, bool force, const int4 **plan_out, int *ncta_out);
-int op_cg_gen(to_mesh *m, int k, double rtol, cudaStream_t st);
+int op_cg_gen(to_mesh *m, int k, double rtol, cudaStream_t st, bool step_in);
 // sharded handles (tomesh_shard.cu)
 int shard_compliance_partial(to_mesh *m, const double *u_dev, double *out, cudaStream_t st);

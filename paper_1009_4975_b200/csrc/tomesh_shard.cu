@@ -630,7 +630,7 @@ int gshard_solve_group(to_mesh *const *ms, int32_t n, double penal, const double
       for (int i = 0; i < n; ++i) {
         to_mesh *m = ms[i];
         CK(cudaSetDevice(m->device));
-        RC(op_cg_gen(m, kk, rtol, S_(i)));
+        RC(op_cg_gen(m, kk, rtol, S_(i), false));
         RC(launch_gxchg<GX_ITER>(m, m->rb[w], m->pb[w], m->qb[w], w, m->shard_seq, S_(i)));
       }
       for (int i = 0; i < n; ++i) {
