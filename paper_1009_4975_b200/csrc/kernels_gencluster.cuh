@@ -247,6 +247,7 @@ k_gen_cluster(const __grid_constant__ GenBlocks B, const __grid_constant__ GcSen
       for (int e = tid; e < nSend; e += T) {
         const uint32_t ent = send[e];
         const int src = (int)(ent & 0xfffu), dst = (int)((ent >> 12) & 0x7fffu), r = (int)(ent >> 27);
+        GF_CHECK(src < nOwn && r < nb && r != rank && dst < SL.max_halo);
         const uint32_t ra = gc_mapa(phb + (size_t)dst * DIM, r), rb = gc_mapa(&bar[1 + par], r);
         if (DIM == 2) {
           gc_st_async2(ra, P[src * DIM], P[src * DIM + 1], rb);

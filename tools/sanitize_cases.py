@@ -16,9 +16,13 @@ import paper_1009_4975_b200 as pb  # noqa: E402
 from inputs import config, density_at  # noqa: E402
 
 CASES = {
-    "c1": (lambda: config("c1"), 0),                                   # 2D cooperative general kernel
-    "c2": (lambda: config("c2"), 0),                                   # 2D general kernel per iteration
-    "c4s": (lambda: config("c4", base=(6, 3, 3), L=2, n_gauss=30), 0),  # 3D general kernel (hanging nodes)
+    "c1": (lambda: config("c1"), 0),                                   # 2D cluster-resident solver
+    "c1_coop": (lambda: config("c1"), pb.TO_UPLOAD_NO_CLUSTER),        # 2D cooperative general kernel
+    "c1_launched": (lambda: config("c1"), pb.TO_UPLOAD_LAUNCHED),      # 2D kernel per iteration, step inside
+    "c2L2": (lambda: config("c2", L=2), 0),                            # 2D cluster solver with hanging nodes
+    "c2": (lambda: config("c2"), 0),                                   # 2D general kernel per iteration, step inside
+    "c4s": (lambda: config("c4", base=(6, 3, 3), L=2, n_gauss=30), 0),  # 3D cluster solver (hanging nodes)
+    "c4s_launched": (lambda: config("c4", base=(6, 3, 3), L=2, n_gauss=30), pb.TO_UPLOAD_LAUNCHED),
     "c3s": (lambda: config("c3", nx=37, ny=9, nz=13), 0),              # structured K1 (TMA, ragged tiles)
     "c5s": (lambda: config("c5", nx=20, ny=10, nz=10), 0),
 }
