@@ -167,6 +167,15 @@ typedef struct {
                                   loop in one thread-block cluster          */
   int64_t launches_total;      /* kernels launched by every call on this handle
                                   since upload (monotone counter)               */
+  int32_t gen_blocks;          /* general path: owner-computes blocks (CTAs per
+                                  iteration launch; 0 when structured)         */
+  int32_t gen_smem_bytes;      /* general path: dynamic shared memory per CTA  */
+  int32_t gen_max_loc, gen_max_el;   /* largest local node / element count of
+                                  a block (they size the shared memory)       */
+  int64_t gen_local_el;        /* sum over blocks of the staged elements (the
+                                  element recompute is gen_local_el / n_elem) */
+  int64_t gen_local_nodes;     /* sum over blocks of owned + halo + virtual
+                                  node slots                                    */
 } to_mesh_info;
 
 /* Validate, copy to `device`, derive device encodings, allocate the CG

@@ -48,7 +48,9 @@ class ToMeshInfo(C.Structure):
                 ("n_elem", C.c_int64), ("n_node", C.c_int64), ("n_dof", C.c_int64), ("n_hang", C.c_int64),
                 ("n_fixed", C.c_int64), ("filt_nnz", C.c_int64), ("grid", C.c_int64 * 3),
                 ("device_bytes", C.c_int64), ("kernel_launches", C.c_int32), ("matvec_variant", C.c_int32),
-                ("launches_total", C.c_int64)]
+                ("launches_total", C.c_int64), ("gen_blocks", C.c_int32), ("gen_smem_bytes", C.c_int32),
+                ("gen_max_loc", C.c_int32), ("gen_max_el", C.c_int32), ("gen_local_el", C.c_int64),
+                ("gen_local_nodes", C.c_int64)]
 
 
 class ToMinresStats(C.Structure):

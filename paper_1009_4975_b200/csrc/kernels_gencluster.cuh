@@ -144,7 +144,7 @@ k_gen_cluster(const __grid_constant__ GenBlocks B, const __grid_constant__ GcSen
   extern __shared__ __align__(16) unsigned char gsm_raw[];
   const int tid = threadIdx.x, nb = (int)cl.num_blocks(), rank = (int)cl.block_rank();
   const GfMeta mt = B.meta[rank];
-  const GfSections sec = gf_sections<DIM>(mt.n_own, mt.n_halo, mt.n_virt, mt.n_el, mt.n_inc);
+  const GfSections sec = gf_sections<DIM>(mt.n_own, mt.n_halo, mt.n_virt, mt.n_el, mt.n_inc, CH);
   const GcLayout L = gc_layout<DIM, T>(B.max_rec16, B.max_el, B.max_loc, B.max_own, SL.max_halo, SL.max_send);
   unsigned char *rec = gsm_raw;
   double *sl = reinterpret_cast<double *>(gsm_raw + L.sl);
@@ -280,19 +280,11 @@ k_gen_cluster(const __grid_constant__ GenBlocks B, const __grid_constant__ GcSen
       __syncthreads();
       // 3. elements by chunks of CH; owned nodes sum their incidences of the
       //    chunk in ascending order (C^T, weights 1, 1/2, 1/4)
-      int cur[OPT], cend[OPT];
       double qa[OPT][DIM];
 #pragma unroll
-      for (int u = 0; u < OPT; ++u) {
-        const int o = tid + u * T;
-        cur[u] = cend[u] = 0;
-        if (o < nOwn) {
-          cur[u] = iptr[o];
-          cend[u] = iptr[o + 1];
-        }
+      for (int u = 0; u < OPT; ++u)
 #pragma unroll
         for (int i = 0; i < DIM; ++i) qa[u][i] = 0.0;
-      }
       for (int c0 = 0; c0 < nE; c0 += CH) {
         const int le = c0 + tid;
         if (tid < CH && le < nE) {
@@ -325,21 +317,7 @@ k_gen_cluster(const __grid_constant__ GenBlocks B, const __grid_constant__ GcSen
           for (int a = 0; a < ND; ++a) dst[a] = se * y[a];
         }
         __syncthreads();
-        const int lim = (c0 + CH) * NC;
-#pragma unroll
-        for (int u = 0; u < OPT; ++u) {
-          while (cur[u] < cend[u]) {
-            const unsigned ent = inc[cur[u]];
-            const int lec = (int)(ent & 0x3fffu);
-            if (lec >= lim) break;
-            const double w = gf_weight(ent >> 14);
-            const int lr = lec - c0 * NC;
-            const double *src = Y + (size_t)(lr / NC) * YS + (lr % NC) * DIM;
-#pragma unroll
-            for (int i = 0; i < DIM; ++i) qa[u][i] = fma(w, src[i], qa[u][i]);
-            ++cur[u];
-          }
-        }
+        gf_ct_chunk<DIM, OPT, T>(iptr, inc, Y, nOwn, c0 / CH, qa);
         __syncthreads();
       }
       GC_MARK(4);

@@ -48,8 +48,8 @@
 namespace tomesh {
 
 constexpr int kGfThreads = 256;
-constexpr int kGfOwnPerThread = 2;                       // owned nodes per thread (max_own <= 512)
-constexpr int kGfMaxOwn = kGfThreads * kGfOwnPerThread;
+constexpr int kGfOwnPerThread = 1;                       // owned nodes per thread in the C^T sums
+constexpr int kGfMaxOwn = kGfThreads * kGfOwnPerThread;  // (block targets are <= 224 nodes)
 constexpr int kGfMaxLoc = 1536;                          // local node slots per block (uint16 slots)
 constexpr int kGfPersistMaxBlocks = 32;                  // k_gen_persist only up to this many blocks
 // Launched path: every block evaluates the previous step itself (no step
@@ -91,14 +91,17 @@ struct GfChunk {
 struct GfSections {
   int halo, virt, corner, iptr, inc, total;
 };
+// ch: elements per chunk of the kernel that reads the record (the incidence
+// lists are chunk-major, tomesh_types.cuh GfMeta).
+__host__ __device__ inline int gf_nchunks(int n_el, int ch) { return (n_el + ch - 1) / ch; }
 template <int DIM>
-__host__ __device__ inline GfSections gf_sections(int n_own, int n_halo, int n_virt, int n_el, int n_inc) {
+__host__ __device__ inline GfSections gf_sections(int n_own, int n_halo, int n_virt, int n_el, int n_inc, int ch) {
   GfSections s;
   s.halo = 0;
   s.virt = s.halo + gf_pad16(4 * n_halo);
   s.corner = s.virt + gf_pad16(8 * n_virt);
   s.iptr = s.corner + gf_pad16(2 * (1 << DIM) * n_el);
-  s.inc = s.iptr + gf_pad16(2 * (n_own + 1));
+  s.inc = s.iptr + gf_pad16(2 * gf_nchunks(n_el, ch) * (n_own + 1));
   s.total = s.inc + gf_pad16(2 * n_inc);
   return s;
 }
@@ -210,7 +213,35 @@ __device__ unsigned long long g_gf_trace[16384][8];
   } while (0)
 #endif
 
-__device__ __forceinline__ double gf_weight(unsigned code) { return code == 0 ? 1.0 : code == 1 ? 0.5 : 0.25; }
+// weight code 0, 1, 2 -> 1, 1/2, 1/4 (2^-code: the exponent field alone)
+__device__ __forceinline__ double gf_weight(unsigned code) {
+  return __longlong_as_double((long long)(0x3ffu - code) << 52);
+}
+
+// C^T of one chunk: owned node o = tid + u * T adds its incidences of chunk
+// `ch` (chunk-major CSR: cp = iptr + ch (n_own + 1); entry = double offset of
+// the corner's result row in Y | weight code << 14), in ascending element
+// order -- the same order across chunks as one ascending list, so the sum
+// is fixed by the mesh.
+template <int DIM, int OPT, int T>
+__device__ __forceinline__ void gf_ct_chunk(const uint16_t *__restrict__ iptr, const uint16_t *__restrict__ inc,
+                                            const double *__restrict__ Y, int nOwn, int ch, double (&qa)[OPT][DIM]) {
+  const uint16_t *cp = iptr + (size_t)ch * (nOwn + 1);
+#pragma unroll
+  for (int u = 0; u < OPT; ++u) {
+    const int o = threadIdx.x + u * T;
+    if (o >= nOwn) continue;
+    const int kb = cp[o], ke = cp[o + 1];
+#pragma unroll 2
+    for (int k = kb; k < ke; ++k) {
+      const unsigned ent = inc[k];
+      const double w = gf_weight(ent >> 14);
+      const double *src = Y + (ent & 0x3fffu);
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) qa[u][i] = fma(w, src[i], qa[u][i]);
+    }
+  }
+}
 
 // Shared-memory view of one block of the general path (its record, s_e, the
 // staging arrays) -- set up once per kernel.
@@ -227,7 +258,7 @@ __device__ __forceinline__ GfView gf_view(const GenBlocks &B, const GfMeta &mt, 
   constexpr int CH = GfChunk<DIM>::CH, YS = GfChunk<DIM>::YS;
   GfView V;
   V.mt = mt;
-  sec = gf_sections<DIM>(mt.n_own, mt.n_halo, mt.n_virt, mt.n_el, mt.n_inc);
+  sec = gf_sections<DIM>(mt.n_own, mt.n_halo, mt.n_virt, mt.n_el, mt.n_inc, CH);
   unsigned char *rec = gsm_raw;
   V.sl = reinterpret_cast<double *>(gsm_raw + 16 * (size_t)B.max_rec16);
   V.P = V.sl + ((B.max_el + 1) & ~1);
@@ -261,41 +292,39 @@ __device__ __forceinline__ void gf_issue_record(const GenBlocks &B, const GfView
 template <bool COH>
 __device__ __forceinline__ double gf_ld(const double *p) { return COH ? __ldcg(p) : __ldg(p); }
 
-// The owned nodes' r, q, p, Dinv of one block (o = tid + u * kGfThreads),
-// loaded ahead of the step evaluation in k_gen_fused (they do not depend on
-// alpha, beta): gf_block_iter<..., PRE = true> takes them from here.
+// The owned DOFs' r, q, p, Dinv of one block, DOF-linear (owned DOF j = tid +
+// v * kGfThreads: coalesced), loaded before the stop test and the step are
+// known (they do not depend on alpha, beta): gf_block_iter takes them from here.
 template <int DIM>
 struct GfOwned {
-  double r[kGfOwnPerThread][DIM], q[kGfOwnPerThread][DIM], p[kGfOwnPerThread][DIM], d[kGfOwnPerThread][DIM];
+  static constexpr int OD = kGfMaxOwn * DIM / kGfThreads;   // owned DOFs per thread
+  double r[OD], q[OD], p[OD], d[OD];
 };
 template <int DIM, bool COH>
 __device__ __forceinline__ void gf_load_owned(const GfMeta &mt, const double *__restrict__ ro,
                                               const double *__restrict__ qo, const double *__restrict__ po,
                                               const double *__restrict__ Dinv, GfOwned<DIM> &w) {
   const int64_t g0 = (int64_t)mt.node0 * DIM;
+  const int nd = mt.n_own * DIM;
 #pragma unroll
-  for (int u = 0; u < kGfOwnPerThread; ++u) {
-    const int o = threadIdx.x + u * kGfThreads;
-#pragma unroll
-    for (int i = 0; i < DIM; ++i) {
-      w.r[u][i] = w.q[u][i] = w.p[u][i] = w.d[u][i] = 0.0;
-      if (o < mt.n_own) {
-        const int64_t g = g0 + (int64_t)o * DIM + i;
-        w.r[u][i] = gf_ld<COH>(ro + g);
-        w.q[u][i] = gf_ld<COH>(qo + g);
-        w.p[u][i] = gf_ld<COH>(po + g);
-        w.d[u][i] = __ldg(Dinv + g);
-      }
+  for (int v = 0; v < GfOwned<DIM>::OD; ++v) {
+    const int j = threadIdx.x + v * kGfThreads;
+    w.r[v] = w.q[v] = w.p[v] = w.d[v] = 0.0;
+    if (j < nd) {
+      w.r[v] = gf_ld<COH>(ro + g0 + j);
+      w.q[v] = gf_ld<COH>(qo + g0 + j);
+      w.p[v] = gf_ld<COH>(po + g0 + j);
+      w.d[v] = __ldg(Dinv + g0 + j);
     }
   }
 }
 
 // One PCG iteration of one block (steps 1-4 of the header comment); the
-// block's dots (unreduced, per thread) in `dots`.  wait_rec: the record's
-// mbarrier phase is still outstanding (first iteration of the kernel).
+// block's dots (unreduced, per thread) in `dots`.  wait_par >= 0: the
+// record's mbarrier phase of that parity is still outstanding.
 // PRE: the owned r, q, p, Dinv come preloaded in `pre` (CG mode).
 template <int DIM, int MODE, bool COH, bool PRE = false>
-__device__ __forceinline__ void gf_block_iter(const GfView &V, bool wait_rec, const double *__restrict__ ro,
+__device__ __forceinline__ void gf_block_iter(const GfView &V, int wait_par, const double *__restrict__ ro,
                                               const double *__restrict__ qo, const double *__restrict__ po,
                                               const double *__restrict__ Dinv, double *__restrict__ rw,
                                               double *__restrict__ pw, double *__restrict__ qw,
@@ -315,49 +344,33 @@ __device__ __forceinline__ void gf_block_iter(const GfView &V, bool wait_rec, co
   const uint16_t *corner = V.corner, *iptr = V.iptr, *inc = V.inc;
   const int64_t g0 = (int64_t)mt.node0 * DIM;
   double rho = 0.0, rr = 0.0;
-  // 1. owned nodes o = tid + u * kGfThreads (the same nodes as in step 4)
+  // 1. owned DOFs j = tid + v * kGfThreads (DOF-linear, coalesced)
+  if (CG) {
+    GfOwned<DIM> w;
+    if (PRE) w = *pre;
+    else gf_load_owned<DIM, COH>(mt, ro, qo, po, Dinv, w);
 #pragma unroll
-  for (int u = 0; u < OPT; ++u) {
-    const int o = tid + u * kGfThreads;
-    if (o >= nOwn) continue;
-    const int64_t g = g0 + (int64_t)o * DIM;
-    if (CG) {
-      double r_o[DIM], q_o[DIM], p_o[DIM], d_o[DIM];
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) {
-        if (PRE) {
-          r_o[i] = pre->r[u][i];
-          q_o[i] = pre->q[u][i];
-          p_o[i] = pre->p[u][i];
-          d_o[i] = pre->d[u][i];
-        } else {
-          r_o[i] = gf_ld<COH>(ro + g + i);
-          q_o[i] = gf_ld<COH>(qo + g + i);
-          p_o[i] = gf_ld<COH>(po + g + i);
-          d_o[i] = __ldg(Dinv + g + i);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) {
-        const double rn = fma(-alpha, q_o[i], r_o[i]);   // q is 0 on non-free DOFs, so r stays 0 there
-        const double z = d_o[i] * rn;
-        const double pn = fma(beta, p_o[i], z);
-        rw[g + i] = rn;
-        pw[g + i] = pn;
-        if (alpha != 0.0) x[g + i] = fma(alpha, p_o[i], COH ? __ldcg(x + g + i) : x[g + i]);
-        rho = fma(rn, z, rho);
-        rr = fma(rn, rn, rr);
-        P[o * DIM + i] = pn;
-        Zs[o * DIM + i] = z;
-        Ds[o * DIM + i] = d_o[i];
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) P[o * DIM + i] = gf_ld<COH>(po + g + i);
+    for (int v = 0; v < GfOwned<DIM>::OD; ++v) {
+      const int j = tid + v * kGfThreads;
+      if (j >= nOwn * DIM) continue;
+      const int64_t g = g0 + j;
+      const double rn = fma(-alpha, w.q[v], w.r[v]);   // q is 0 on non-free DOFs, so r stays 0 there
+      const double z = w.d[v] * rn;
+      const double pn = fma(beta, w.p[v], z);
+      rw[g] = rn;
+      pw[g] = pn;
+      if (alpha != 0.0) x[g] = fma(alpha, w.p[v], COH ? __ldcg(x + g) : x[g]);
+      rho = fma(rn, z, rho);
+      rr = fma(rn, rn, rr);
+      P[j] = pn;
+      Zs[j] = z;
+      Ds[j] = w.d[v];
     }
+  } else {
+    for (int j = tid; j < nOwn * DIM; j += kGfThreads) P[j] = gf_ld<COH>(po + g0 + j);
   }
   GF_MARK(2);
-  if (wait_rec) mbar_wait(V.bar, 0);
+  if (wait_par >= 0) mbar_wait(V.bar, (unsigned)wait_par);
   // ... and the halo nodes
 #pragma unroll 4
   for (int j = tid; j < nHalo * DIM; j += kGfThreads) {
@@ -395,19 +408,11 @@ __device__ __forceinline__ void gf_block_iter(const GfView &V, bool wait_rec, co
   __syncthreads();
   // 3. elements by chunks of CH (one per thread); then owned nodes sum their
   //    incidences of the chunk in ascending order
-  int cur[OPT], cend[OPT];
   double qa[OPT][DIM];
 #pragma unroll
-  for (int u = 0; u < OPT; ++u) {
-    const int o = tid + u * kGfThreads;
-    cur[u] = cend[u] = 0;
-    if (o < nOwn) {
-      cur[u] = iptr[o];
-      cend[u] = iptr[o + 1];
-    }
+  for (int u = 0; u < OPT; ++u)
 #pragma unroll
     for (int i = 0; i < DIM; ++i) qa[u][i] = 0.0;
-  }
   for (int c0 = 0; c0 < nE; c0 += CH) {
     const int le = c0 + tid;
     if (tid < CH && le < nE) {
@@ -441,22 +446,15 @@ __device__ __forceinline__ void gf_block_iter(const GfView &V, bool wait_rec, co
       for (int a = 0; a < ND; ++a) dst[a] = se * y[a];
     }
     __syncthreads();
-    const int lim = (c0 + CH) * NC;
-#pragma unroll
-    for (int u = 0; u < OPT; ++u) {
-      while (cur[u] < cend[u]) {
-        const unsigned ent = inc[cur[u]];
-        const int lec = (int)(ent & 0x3fffu);
-        if (lec >= lim) break;
-        GF_CHECK(lec >= c0 * NC && lec < nE * NC && (ent >> 14) <= 2);
-        const double w = gf_weight(ent >> 14);
-        const int lr = lec - c0 * NC;
-        const double *src = Y + (size_t)(lr / NC) * YS + (lr % NC) * DIM;
-#pragma unroll
-        for (int i = 0; i < DIM; ++i) qa[u][i] = fma(w, src[i], qa[u][i]);
-        ++cur[u];
-      }
+#ifdef TOMESH_DEBUG_CHECKS
+    for (int o = tid; o < nOwn; o += kGfThreads) {
+      const uint16_t *cp = iptr + (size_t)(c0 / CH) * (nOwn + 1);
+      GF_CHECK(cp[o] <= cp[o + 1] && cp[o + 1] <= mt.n_inc);
+      for (int k = cp[o]; k < cp[o + 1]; ++k)
+        GF_CHECK((inc[k] & 0x3fffu) + DIM <= (unsigned)(min(CH, nE - c0) * YS) && (inc[k] >> 14) <= 2);
     }
+#endif
+    gf_ct_chunk<DIM, OPT, kGfThreads>(iptr, inc, Y, nOwn, c0 / CH, qa);
     __syncthreads();
   }
   GF_MARK(4);
@@ -501,12 +499,13 @@ __device__ __forceinline__ void gf_step_sum(const double *part, int nb, double (
 }
 
 // This block's dots (summed in a fixed order by the next launch / k_gen_step).
-__device__ __forceinline__ void gf_block_dots(double (&dots)[5], double *partials, int nbk, int kit, int step_in) {
+__device__ __forceinline__ void gf_block_dots(double (&dots)[5], double *partials, int nbk, int kit, int step_in,
+                                              int b) {
   block_sum<5>(dots);
   double *pk = partials + (step_in ? (size_t)5 * nbk * (kit & 1) : 0);
   if (threadIdx.x == 0)
 #pragma unroll
-    for (int k = 0; k < 5; ++k) pk[(size_t)5 * blockIdx.x + k] = dots[k];
+    for (int k = 0; k < 5; ++k) pk[(size_t)5 * b + k] = dots[k];
 }
 
 // step_in = 1 (the unsharded solve): the step of iteration kit-1 is evaluated
@@ -515,8 +514,8 @@ __device__ __forceinline__ void gf_block_dots(double (&dots)[5], double *partial
 // everywhere, so every block takes the same alpha, beta and stop decision);
 // block 0 commits it to S.  This launch's dots go to partials[kit & 1].  One
 // launch per iteration; k_gen_step evaluates the last step after the loop.
-// step_in = 0 (the shard group, kernels_gshard.cuh): alpha, beta from S,
-// dots to partials[0..nb).
+// step_in = 0 (large grids, the shard group): alpha, beta from S, dots to
+// partials[0..nb).
 template <int DIM, int MODE>
 __global__ void __launch_bounds__(kGfThreads, TOMESH_GF_MINB)
 k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_loc, const double *__restrict__ ro,
@@ -539,47 +538,49 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
   __syncthreads();
   pdl_wait();
   pdl_release();
-  if (CG && cg_stopped(S)) {
-    mbar_wait(V.bar, 0);   // no bulk copy may still be writing when the CTA exits
-    return;
-  }
-  GF_MARK(1);
-  double alpha = CG ? __ldcg(&S->alpha) : 0.0;
-  double beta = CG ? __ldcg(&S->beta) : 0.0;
-  const int nbk = (int)gridDim.x;
-  if (CG && step_in && kit > 0) {
-    // the owned vectors do not depend on the step: their loads are in flight
-    // while the step is evaluated
+  const int nbk = B.n_blk;
+  if constexpr (CG) {
+    // the owned vectors do not depend on the step or the stop test: their
+    // loads are in flight while S is read and the step is evaluated
     GfOwned<DIM> pre;
     gf_load_owned<DIM, false>(mt, ro, qo, po, Dinv, pre);
-    __shared__ double s_st[3];
-    double d[5];
-    gf_step_sum(partials + (size_t)5 * nbk * ((kit - 1) & 1), nbk, d);
-    if (tid == 0) {
-      CgStepOut so;
-      cg_step_eval(S, kit - 1, d, rtol, so);
-      if (blockIdx.x == 0) cg_step_commit(S, kit - 1, so, hist);
-      s_st[0] = so.alpha;
-      s_st[1] = so.beta;
-      s_st[2] = so.done ? 1.0 : 0.0;
-    }
-    __syncthreads();
-    if (s_st[2] != 0.0) {
-      mbar_wait(V.bar, 0);
+    if (cg_stopped(S)) {
+      mbar_wait(V.bar, 0);   // no bulk copy may still be writing when the CTA exits
       return;
     }
-    alpha = s_st[0];
-    beta = s_st[1];
+    GF_MARK(1);
+    double alpha = __ldcg(&S->alpha);
+    double beta = __ldcg(&S->beta);
+    if (step_in && kit > 0) {
+      __shared__ double s_st[3];
+      double d[5];
+      gf_step_sum(partials + (size_t)5 * nbk * ((kit - 1) & 1), nbk, d);
+      if (tid == 0) {
+        CgStepOut so;
+        cg_step_eval(S, kit - 1, d, rtol, so);
+        if (blockIdx.x == 0) cg_step_commit(S, kit - 1, so, hist);
+        s_st[0] = so.alpha;
+        s_st[1] = so.beta;
+        s_st[2] = so.done ? 1.0 : 0.0;
+      }
+      __syncthreads();
+      if (s_st[2] != 0.0) {
+        mbar_wait(V.bar, 0);
+        return;
+      }
+      alpha = s_st[0];
+      beta = s_st[1];
+    }
     double dots[5];
-    gf_block_iter<DIM, MODE, false, true>(V, true, ro, qo, po, Dinv, rw, pw, qw, x, K2, H, alpha, beta, dots, &pre);
-    gf_block_dots(dots, partials, nbk, kit, step_in);
-    return;
+    gf_block_iter<DIM, MODE, false, true>(V, 0, ro, qo, po, Dinv, rw, pw, qw, x, K2, H, alpha, beta, dots, &pre);
+    GF_MARK(5);
+    gf_block_dots(dots, partials, nbk, kit, step_in, blockIdx.x);
+    GF_MARK(6);
+  } else {
+    GF_MARK(1);
+    double dots[5];
+    gf_block_iter<DIM, MODE, false>(V, 0, ro, qo, po, Dinv, rw, pw, qw, x, K2, H, 0.0, 0.0, dots);
   }
-  double dots[5];
-  gf_block_iter<DIM, MODE, false>(V, true, ro, qo, po, Dinv, rw, pw, qw, x, K2, H, alpha, beta, dots);
-  GF_MARK(5);
-  if (CG) gf_block_dots(dots, partials, nbk, kit, step_in);
-  GF_MARK(6);
 }
 
 // The whole general-path PCG loop in one cooperative kernel, for meshes whose
@@ -613,7 +614,7 @@ k_gen_persist(const __grid_constant__ GenBlocks B, const double *__restrict__ s_
   for (int k = 0; k < max_iter; ++k) {
     const bool odd = k & 1;                           // writes buffer k & 1, reads (k + 1) & 1
     double dots[5];
-    gf_block_iter<DIM, G_CG, true>(V, k == 0, odd ? rb0 : rb1, odd ? qb0 : qb1, odd ? pb0 : pb1, Dinv,
+    gf_block_iter<DIM, G_CG, true>(V, k == 0 ? 0 : -1, odd ? rb0 : rb1, odd ? qb0 : qb1, odd ? pb0 : pb1, Dinv,
                                    odd ? rb1 : rb0, odd ? pb1 : pb0, odd ? qb1 : qb0, x, K2, H, alpha, beta, dots);
     block_sum<5>(dots);
     double *pk = part + (size_t)(k & 1) * 5 * nb;

@@ -320,7 +320,7 @@ struct HostBlocks {
 // max_blocks > 0: stop (return 1) as soon as the cut has more ranges.
 int make_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_hang, const std::vector<int64_t> &iptr,
                     const std::vector<uint32_t> &inc, int64_t N, int own_target, int el_max, int loc_max, int own_max,
-                    int max_blocks, HostBlocks &hb) {
+                    int max_blocks, int ch, HostBlocks &hb) {
   const int nc = 1 << d->dim;
   std::vector<int32_t> el_mark(d->n_elem, -1), nd_mark(d->n_node, -1), el_le(d->n_elem, 0), nd_slot(d->n_node, 0);
   int stamp = 0;
@@ -439,17 +439,38 @@ int make_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_hang
     std::vector<uint16_t> crec((size_t)nE * nc);
     for (int i = 0; i < nE; ++i)
       for (int c = 0; c < nc; ++c) crec[(size_t)i * nc + c] = (uint16_t)slot(d->elem_node[elems[i] * nc + c]);
-    iptr_l.assign(1, 0);
+    // chunk-major incidence CSR: for each chunk of `ch` elements, each owned
+    // node's incidences with that chunk's elements (ascending element order,
+    // as the global list), as offsets into the kernel's chunk buffer
+    const int nch = gf_nchunks(nE, ch), ys = nc * d->dim + 1;
+    if ((ch - 1) * ys + (nc - 1) * d->dim >= (1 << 14)) { set_error("internal: chunk buffer offset range"); return TO_EINVAL; }
+    iptr_l.clear();
     inc_l.clear();
-    for (int64_t n = a; n < b; ++n) {
-      for (int64_t k = iptr[n]; k < iptr[n + 1]; ++k) {
-        const uint32_t t = inc[k];
-        const int64_t e = elem_of(t);
-        const uint32_t c = (t & 0x3fffffffu) % (uint32_t)nc, code = t >> 30;
-        inc_l.push_back((uint16_t)(((uint32_t)el_le[e] * nc + c) | (code << 14)));
+    {
+      std::vector<std::vector<uint16_t>> by_chunk(nch);
+      std::vector<int> cnt((size_t)nch * nOwn, 0);
+      for (int64_t n = a; n < b; ++n)
+        for (int64_t k = iptr[n]; k < iptr[n + 1]; ++k) {
+          const uint32_t t = inc[k];
+          const int le = el_le[elem_of(t)];
+          const uint32_t c = (t & 0x3fffffffu) % (uint32_t)nc, code = t >> 30;
+          const int cix = le / ch;
+          by_chunk[cix].push_back((uint16_t)((uint32_t)((le - cix * ch) * ys + (int)c * d->dim) | (code << 14)));
+          ++cnt[(size_t)cix * nOwn + (n - a)];
+        }
+      // by_chunk[c] holds chunk c's entries node by node (nodes ascending,
+      // each node's entries ascending): concatenate chunk after chunk
+      for (int cix = 0; cix < nch; ++cix) {
+        iptr_l.push_back((uint16_t)inc_l.size());
+        size_t at = 0;
+        for (int o = 0; o < nOwn; ++o) {
+          const int c_o = cnt[(size_t)cix * nOwn + o];
+          inc_l.insert(inc_l.end(), by_chunk[cix].begin() + at, by_chunk[cix].begin() + at + c_o);
+          at += c_o;
+          if (inc_l.size() > 0xffff) { set_error("general-path block with more than 65535 incidences"); return TO_EINVAL; }
+          iptr_l.push_back((uint16_t)inc_l.size());
+        }
       }
-      if (inc_l.size() > 0xffff) { set_error("general-path block with more than 65535 incidences"); return TO_EINVAL; }
-      iptr_l.push_back((uint16_t)inc_l.size());
     }
     GfMeta &mt = meta[bk];
     mt.node0 = (int32_t)a;
@@ -466,8 +487,8 @@ int make_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_hang
     put(crec.data(), 2 * crec.size());
     put(iptr_l.data(), 2 * iptr_l.size());
     put(inc_l.data(), 2 * inc_l.size());
-    const GfSections sec = d->dim == 3 ? gf_sections<3>(nOwn, nHalo, nVirt, nE, mt.n_inc)
-                                       : gf_sections<2>(nOwn, nHalo, nVirt, nE, mt.n_inc);
+    const GfSections sec = d->dim == 3 ? gf_sections<3>(nOwn, nHalo, nVirt, nE, mt.n_inc, ch)
+                                       : gf_sections<2>(nOwn, nHalo, nVirt, nE, mt.n_inc, ch);
     if ((size_t)sec.total != rec.size() - r0) { set_error("internal: block record layout"); return TO_EINVAL; }
     for (int64_t e : elems) el_id.push_back((int32_t)e);
     if (nE & 1) el_id.push_back(-1);   // every block's s_e starts 16-byte aligned
@@ -530,7 +551,7 @@ int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_han
   // (incidence encoding: le * 2^dim < 2^14)
   HostBlocks hb;
   RC(make_gen_blocks(d, node_hang, iptr, inc, N, own_target, std::min(kGfElMax, (1 << 14) / nc - 1), kGfMaxLoc,
-                     kGfMaxOwn, 0, hb));
+                     kGfMaxOwn, 0, d->dim == 3 ? GfChunk<3>::CH : GfChunk<2>::CH, hb));
   GenBlocks &B = m->GB;
   RC(upload_gen_blocks(m, hb, B, &m->gb_el_id, &m->gb_n_loc_el, &m->s_loc, st));
   const int nb = B.n_blk;
@@ -546,6 +567,11 @@ int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_han
     RC(allow_smem(m, (const void *)k_gen_persist<2>, m->gb_smem));
   }
   RC(ensure_partials(m, (size_t)nb * 10));   // dots of two launches (parity)
+  m->gb_local_el = m->gb_local_nodes = 0;
+  for (const GfMeta &mt : hb.meta) {
+    m->gb_local_el += mt.n_el;
+    m->gb_local_nodes += mt.n_own + mt.n_halo + mt.n_virt;
+  }
   m->gen_fused = true;
   return 0;
 }
@@ -581,7 +607,10 @@ int build_gen_cluster(const to_mesh_desc *d, const std::vector<int32_t> &node_ha
   const int T = own_target <= 256 ? 128 : own_target <= 512 ? 256 : 512;
   HostBlocks hb;
   const int rc = make_gen_blocks(d, node_hang, iptr, inc, N, own_target, (1 << 14) / nc - 1, 0xfffe,
-                                 kGcOwnPerThread * T, kGcMaxBlocks, hb);
+                                 kGcOwnPerThread * T, kGcMaxBlocks,
+                                 d->dim == 3 ? (T == 512 ? GcChunk<3, 512>::CH : T == 256 ? GcChunk<3, 256>::CH : GcChunk<3, 128>::CH)
+                                             : (T == 512 ? GcChunk<2, 512>::CH : T == 256 ? GcChunk<2, 256>::CH : GcChunk<2, 128>::CH),
+                                 hb);
   if (rc == 1) return 0;     // the limits split it into more blocks than one cluster holds
   RC(rc);
   // send lists: for every halo node of block b (index i in b's halo list), an
@@ -949,13 +978,14 @@ int op_apply(to_mesh *m, const double *in, double *out, cudaStream_t st) {
 // shard group's exchange and step kernels follow it.
 int op_cg_gen(to_mesh *m, int k, double rtol, cudaStream_t st, bool step_in) {
   const int o = (k + 1) & 1, w = k & 1;
+  const dim3 grid(m->GB.n_blk);
   if (m->dim == 2)
-    RC(launch_pdl(k_gen_fused<2, G_CG>, dim3(m->GB.n_blk), dim3(kGfThreads), m->gb_smem, st, m->GB,
+    RC(launch_pdl(k_gen_fused<2, G_CG>, grid, dim3(kGfThreads), m->gb_smem, st, m->GB,
                   (const double *)m->s_loc, (const double *)m->rb[o], (const double *)m->qb[o],
                   (const double *)m->pb[o], (const double *)m->dinv, m->rb[w], m->pb[w], m->qb[w], m->x, m->K2,
                   m->KS, m->S, m->partials, k, rtol, m->hist, step_in ? 1 : 0));
   else
-    RC(launch_pdl(k_gen_fused<3, G_CG>, dim3(m->GB.n_blk), dim3(kGfThreads), m->gb_smem, st, m->GB,
+    RC(launch_pdl(k_gen_fused<3, G_CG>, grid, dim3(kGfThreads), m->gb_smem, st, m->GB,
                   (const double *)m->s_loc, (const double *)m->rb[o], (const double *)m->qb[o],
                   (const double *)m->pb[o], (const double *)m->dinv, m->rb[w], m->pb[w], m->qb[w], m->x, m->K2,
                   m->KS, m->S, m->partials, k, rtol, m->hist, step_in ? 1 : 0));
@@ -1278,6 +1308,14 @@ extern "C" int tomesh_get_info(const to_mesh *m, to_mesh_info *info) {
   info->kernel_launches = m->last_launches;
   info->matvec_variant = m->structured ? 1 : m->gen_cluster ? 5 : m->gen_persist ? 3 : 4;
   info->launches_total = m->launches_total;
+  if (m->gen_fused) {
+    info->gen_blocks = m->GB.n_blk;
+    info->gen_smem_bytes = (int32_t)m->gb_smem;
+    info->gen_max_loc = m->GB.max_loc;
+    info->gen_max_el = m->GB.max_el;
+    info->gen_local_el = m->gb_local_el;
+    info->gen_local_nodes = m->gb_local_nodes;
+  }
   return 0;
 }
 

@@ -62,6 +62,7 @@ struct to_mesh {
   int64_t gb_n_loc_el = 0;
   double *s_loc = nullptr;             // s_e in block-local element order
   size_t gb_smem = 0;                  // dynamic shared memory of k_gen_fused
+  int64_t gb_local_el = 0, gb_local_nodes = 0;   // staged elements / local node slots over all blocks
   // small meshes: the whole loop in one thread-block cluster (kernels_gencluster.cuh)
   bool gen_cluster = false;
   GenBlocks GC{};                      // its decomposition (at most kGcMaxBlocks blocks)

@@ -39,10 +39,15 @@ struct MeshView {
 //                                 hanging node id
 //   corner  uint16 [n_el][2^dim]  local slot of every corner of the block's
 //                                 elements (ascending element id)
-//   iptr    uint16 [n_own + 1]    owned node o's incidences are inc[iptr[o]
-//                                 .. iptr[o+1])
-//   inc     uint16 [n_inc]        (local element * 2^dim + corner) | weight
-//                                 code << 14 (0: 1, 1: 1/2, 2: 1/4), ascending
+//   iptr    uint16 [nch][n_own+1] chunk-major CSR (nch = ceil(n_el / ch), ch =
+//                                 the reading kernel's elements per chunk):
+//                                 owned node o's incidences with the elements
+//                                 of chunk c are inc[iptr[c][o] .. iptr[c][o+1])
+//   inc     uint16 [n_inc]        double offset of the corner's result in the
+//                                 chunk buffer ((local element - c ch) * YS +
+//                                 corner * dim, YS = 2^dim dim + 1) | weight
+//                                 code << 14 (0: 1, 1: 1/2, 2: 1/4); per node
+//                                 and chunk in ascending element order
 // s_e of the block's elements: s_loc[el_off .. el_off + n_el) (el_off even).
 struct GfMeta {
   int32_t node0, n_own, n_halo, n_virt, n_el, n_inc, el_off, rec_off16;
