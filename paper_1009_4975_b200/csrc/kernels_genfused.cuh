@@ -47,7 +47,10 @@
 
 namespace tomesh {
 
-constexpr int kGfThreads = 256;
+#ifndef TOMESH_GF_THREADS
+#define TOMESH_GF_THREADS 256
+#endif
+constexpr int kGfThreads = TOMESH_GF_THREADS;
 constexpr int kGfOwnPerThread = 1;                       // owned nodes per thread in the C^T sums
 constexpr int kGfMaxOwn = kGfThreads * kGfOwnPerThread;  // (block targets are <= 224 nodes)
 constexpr int kGfMaxLoc = 1536;                          // local node slots per block (uint16 slots)
@@ -74,6 +77,9 @@ constexpr int kGfOwnMin = TOMESH_GF_OWN_MIN;             // smallest block targe
 #endif
 #ifndef TOMESH_GF_MINB
 #define TOMESH_GF_MINB 2
+#endif
+#ifndef TOMESH_GF_HPRE
+#define TOMESH_GF_HPRE 3        // halo DOFs per thread loaded ahead of the owned update (0, 3, 4, 5: c4L 293, 292, 295, 307 us)
 #endif
 #ifndef TOMESH_GF_ELMAX
 #define TOMESH_GF_ELMAX 2047    // capping blocks at one chunk (256) split them too finely: c4 62 -> 92 us
@@ -298,23 +304,25 @@ __device__ __forceinline__ double gf_ld(const double *p) { return COH ? __ldcg(p
 template <int DIM>
 struct GfOwned {
   static constexpr int OD = kGfMaxOwn * DIM / kGfThreads;   // owned DOFs per thread
-  double r[OD], q[OD], p[OD], d[OD];
+  double r[OD], q[OD], p[OD], d[OD], x[OD];
 };
 template <int DIM, bool COH>
 __device__ __forceinline__ void gf_load_owned(const GfMeta &mt, const double *__restrict__ ro,
                                               const double *__restrict__ qo, const double *__restrict__ po,
-                                              const double *__restrict__ Dinv, GfOwned<DIM> &w) {
+                                              const double *__restrict__ Dinv, const double *__restrict__ x,
+                                              GfOwned<DIM> &w) {
   const int64_t g0 = (int64_t)mt.node0 * DIM;
   const int nd = mt.n_own * DIM;
 #pragma unroll
   for (int v = 0; v < GfOwned<DIM>::OD; ++v) {
     const int j = threadIdx.x + v * kGfThreads;
-    w.r[v] = w.q[v] = w.p[v] = w.d[v] = 0.0;
+    w.r[v] = w.q[v] = w.p[v] = w.d[v] = w.x[v] = 0.0;
     if (j < nd) {
       w.r[v] = gf_ld<COH>(ro + g0 + j);
       w.q[v] = gf_ld<COH>(qo + g0 + j);
       w.p[v] = gf_ld<COH>(po + g0 + j);
       w.d[v] = __ldg(Dinv + g0 + j);
+      w.x[v] = __ldcg(x + g0 + j);   // written by this block only (owned DOFs)
     }
   }
 }
@@ -344,11 +352,36 @@ __device__ __forceinline__ void gf_block_iter(const GfView &V, int wait_par, con
   const uint16_t *corner = V.corner, *iptr = V.iptr, *inc = V.inc;
   const int64_t g0 = (int64_t)mt.node0 * DIM;
   double rho = 0.0, rr = 0.0;
+#if TOMESH_GF_HPRE > 0
+  // the first HB halo DOFs of each thread: loads issued before the owned
+  // update, so they are in flight while alpha, beta arrive and the owned
+  // stores go out
+  constexpr int HB = TOMESH_GF_HPRE;
+  double hr[HB], hq[HB], hp[HB], hd[HB];
+  if (CG) {
+    if (wait_par >= 0) mbar_wait(V.bar, (unsigned)wait_par);
+    wait_par = -1;
+#pragma unroll
+    for (int v = 0; v < HB; ++v) {
+      const int j = tid + v * kGfThreads;
+      hr[v] = hq[v] = hp[v] = hd[v] = 0.0;
+      if (j < nHalo * DIM) {
+        const int64_t g = (int64_t)halo[j / DIM] * DIM + (j % DIM);
+        hr[v] = gf_ld<COH>(ro + g);
+        hq[v] = gf_ld<COH>(qo + g);
+        hp[v] = gf_ld<COH>(po + g);
+        hd[v] = __ldg(Dinv + g);
+      }
+    }
+  }
+#else
+  constexpr int HB = 0;
+#endif
   // 1. owned DOFs j = tid + v * kGfThreads (DOF-linear, coalesced)
   if (CG) {
     GfOwned<DIM> w;
     if (PRE) w = *pre;
-    else gf_load_owned<DIM, COH>(mt, ro, qo, po, Dinv, w);
+    else gf_load_owned<DIM, COH>(mt, ro, qo, po, Dinv, x, w);
 #pragma unroll
     for (int v = 0; v < GfOwned<DIM>::OD; ++v) {
       const int j = tid + v * kGfThreads;
@@ -359,7 +392,7 @@ __device__ __forceinline__ void gf_block_iter(const GfView &V, int wait_par, con
       const double pn = fma(beta, w.p[v], z);
       rw[g] = rn;
       pw[g] = pn;
-      if (alpha != 0.0) x[g] = fma(alpha, w.p[v], COH ? __ldcg(x + g) : x[g]);
+      if (alpha != 0.0) x[g] = fma(alpha, w.p[v], w.x[v]);
       rho = fma(rn, z, rho);
       rr = fma(rn, rn, rr);
       P[j] = pn;
@@ -372,8 +405,17 @@ __device__ __forceinline__ void gf_block_iter(const GfView &V, int wait_par, con
   GF_MARK(2);
   if (wait_par >= 0) mbar_wait(V.bar, (unsigned)wait_par);
   // ... and the halo nodes
+#if TOMESH_GF_HPRE > 0
+  if (CG) {
+#pragma unroll
+    for (int v = 0; v < HB; ++v) {
+      const int j = tid + v * kGfThreads;
+      if (j < nHalo * DIM) P[nOwn * DIM + j] = fma(beta, hp[v], hd[v] * fma(-alpha, hq[v], hr[v]));
+    }
+  }
+#endif
 #pragma unroll 4
-  for (int j = tid; j < nHalo * DIM; j += kGfThreads) {
+  for (int j = tid + (CG ? HB : 0) * kGfThreads; j < nHalo * DIM; j += kGfThreads) {
     const int node = halo[j / DIM];
     GF_CHECK(node >= 0 && (node < mt.node0 || node >= mt.node0 + nOwn));
     const int64_t g = (int64_t)node * DIM + (j % DIM);
@@ -543,7 +585,7 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
     // the owned vectors do not depend on the step or the stop test: their
     // loads are in flight while S is read and the step is evaluated
     GfOwned<DIM> pre;
-    gf_load_owned<DIM, false>(mt, ro, qo, po, Dinv, pre);
+    gf_load_owned<DIM, false>(mt, ro, qo, po, Dinv, x, pre);
     if (cg_stopped(S)) {
       mbar_wait(V.bar, 0);   // no bulk copy may still be writing when the CTA exits
       return;

@@ -56,7 +56,9 @@ def run(name):
             "it_per_s_to_tol": round(st.iters / (st.ms / 1e3), 1) if st.ms else None,
             "it_per_s_fixed200": round(200 / (fx.ms / 1e3), 1),
             "us_per_iter_fixed200": round(fx.ms * 1e3 / 200, 2),
-            "sens_plus_filter_ms": round(e0.elapsed_time(e1) / 5, 3), "variant": info["matvec_variant"]}
+            "sens_plus_filter_ms": round(e0.elapsed_time(e1) / 5, 3), "variant": info["matvec_variant"],
+            **{k: info[k] for k in ("gen_blocks", "gen_smem_bytes", "gen_max_loc", "gen_max_el", "gen_local_el",
+                                    "gen_local_nodes")}}
 
 
 if __name__ == "__main__":
