@@ -327,6 +327,34 @@ __device__ __forceinline__ void gf_load_owned(const GfMeta &mt, const double *__
   }
 }
 
+// The first HB halo DOFs of each thread (j = tid + v * kGfThreads of the
+// block's halo DOF list): r, q, p, Dinv loaded before the stop test and the
+// owned update, so they are in flight while S arrives and the owned stores go
+// out (needs the block record: halo ids).
+constexpr int kGfHaloPre = TOMESH_GF_HPRE;
+struct GfHaloPre {
+  double r[kGfHaloPre > 0 ? kGfHaloPre : 1], q[kGfHaloPre > 0 ? kGfHaloPre : 1], p[kGfHaloPre > 0 ? kGfHaloPre : 1],
+      d[kGfHaloPre > 0 ? kGfHaloPre : 1];
+};
+template <int DIM, bool COH>
+__device__ __forceinline__ void gf_load_halo(const GfView &V, const double *__restrict__ ro,
+                                             const double *__restrict__ qo, const double *__restrict__ po,
+                                             const double *__restrict__ Dinv, GfHaloPre &h) {
+  const int nh = V.mt.n_halo * DIM;
+#pragma unroll
+  for (int v = 0; v < kGfHaloPre; ++v) {
+    const int j = threadIdx.x + v * kGfThreads;
+    h.r[v] = h.q[v] = h.p[v] = h.d[v] = 0.0;
+    if (j < nh) {
+      const int64_t g = (int64_t)V.halo[j / DIM] * DIM + (j % DIM);
+      h.r[v] = gf_ld<COH>(ro + g);
+      h.q[v] = gf_ld<COH>(qo + g);
+      h.p[v] = gf_ld<COH>(po + g);
+      h.d[v] = __ldg(Dinv + g);
+    }
+  }
+}
+
 // One PCG iteration of one block (steps 1-4 of the header comment); the
 // block's dots (unreduced, per thread) in `dots`.  wait_par >= 0: the
 // record's mbarrier phase of that parity is still outstanding.
@@ -338,7 +366,7 @@ __device__ __forceinline__ void gf_block_iter(const GfView &V, int wait_par, con
                                               double *__restrict__ pw, double *__restrict__ qw,
                                               double *__restrict__ x, const K0Dense2 &K2, const K0HadSym &H,
                                               double alpha, double beta, double (&dots)[5],
-                                              const GfOwned<DIM> *pre = nullptr) {
+                                              const GfOwned<DIM> *pre = nullptr, const GfHaloPre *hpre = nullptr) {
   constexpr bool CG = MODE == G_CG;
   constexpr int NC = 1 << DIM, ND = NC * DIM, CH = GfChunk<DIM>::CH, YS = GfChunk<DIM>::YS;
   constexpr int OPT = kGfOwnPerThread;
@@ -352,31 +380,17 @@ __device__ __forceinline__ void gf_block_iter(const GfView &V, int wait_par, con
   const uint16_t *corner = V.corner, *iptr = V.iptr, *inc = V.inc;
   const int64_t g0 = (int64_t)mt.node0 * DIM;
   double rho = 0.0, rr = 0.0;
-#if TOMESH_GF_HPRE > 0
-  // the first HB halo DOFs of each thread: loads issued before the owned
-  // update, so they are in flight while alpha, beta arrive and the owned
-  // stores go out
-  constexpr int HB = TOMESH_GF_HPRE;
-  double hr[HB], hq[HB], hp[HB], hd[HB];
-  if (CG) {
-    if (wait_par >= 0) mbar_wait(V.bar, (unsigned)wait_par);
-    wait_par = -1;
-#pragma unroll
-    for (int v = 0; v < HB; ++v) {
-      const int j = tid + v * kGfThreads;
-      hr[v] = hq[v] = hp[v] = hd[v] = 0.0;
-      if (j < nHalo * DIM) {
-        const int64_t g = (int64_t)halo[j / DIM] * DIM + (j % DIM);
-        hr[v] = gf_ld<COH>(ro + g);
-        hq[v] = gf_ld<COH>(qo + g);
-        hp[v] = gf_ld<COH>(po + g);
-        hd[v] = __ldg(Dinv + g);
-      }
+  constexpr int HB = kGfHaloPre;
+  GfHaloPre h;
+  if (CG && HB > 0) {
+    if (hpre) {
+      h = *hpre;
+    } else {
+      if (wait_par >= 0) mbar_wait(V.bar, (unsigned)wait_par);
+      wait_par = -1;
+      gf_load_halo<DIM, COH>(V, ro, qo, po, Dinv, h);
     }
   }
-#else
-  constexpr int HB = 0;
-#endif
   // 1. owned DOFs j = tid + v * kGfThreads (DOF-linear, coalesced)
   if (CG) {
     GfOwned<DIM> w;
@@ -405,15 +419,13 @@ __device__ __forceinline__ void gf_block_iter(const GfView &V, int wait_par, con
   GF_MARK(2);
   if (wait_par >= 0) mbar_wait(V.bar, (unsigned)wait_par);
   // ... and the halo nodes
-#if TOMESH_GF_HPRE > 0
   if (CG) {
 #pragma unroll
     for (int v = 0; v < HB; ++v) {
       const int j = tid + v * kGfThreads;
-      if (j < nHalo * DIM) P[nOwn * DIM + j] = fma(beta, hp[v], hd[v] * fma(-alpha, hq[v], hr[v]));
+      if (j < nHalo * DIM) P[nOwn * DIM + j] = fma(beta, h.p[v], h.d[v] * fma(-alpha, h.q[v], h.r[v]));
     }
   }
-#endif
 #pragma unroll 4
   for (int j = tid + (CG ? HB : 0) * kGfThreads; j < nHalo * DIM; j += kGfThreads) {
     const int node = halo[j / DIM];
@@ -586,13 +598,16 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
     // loads are in flight while S is read and the step is evaluated
     GfOwned<DIM> pre;
     gf_load_owned<DIM, false>(mt, ro, qo, po, Dinv, x, pre);
-    if (cg_stopped(S)) {
-      mbar_wait(V.bar, 0);   // no bulk copy may still be writing when the CTA exits
-      return;
-    }
-    GF_MARK(1);
+    const bool stopped = cg_stopped(S);
     double alpha = __ldcg(&S->alpha);
     double beta = __ldcg(&S->beta);
+    // the halo prefetch needs the record; the stop test is taken after it so
+    // that the S round trip overlaps the halo loads (harmless reads if stopped)
+    mbar_wait(V.bar, 0);   // (also: no bulk copy may still be writing when the CTA exits)
+    GfHaloPre hpre;
+    gf_load_halo<DIM, false>(V, ro, qo, po, Dinv, hpre);
+    if (stopped) return;
+    GF_MARK(1);
     if (step_in && kit > 0) {
       __shared__ double s_st[3];
       double d[5];
@@ -606,15 +621,13 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
         s_st[2] = so.done ? 1.0 : 0.0;
       }
       __syncthreads();
-      if (s_st[2] != 0.0) {
-        mbar_wait(V.bar, 0);
-        return;
-      }
+      if (s_st[2] != 0.0) return;
       alpha = s_st[0];
       beta = s_st[1];
     }
     double dots[5];
-    gf_block_iter<DIM, MODE, false, true>(V, 0, ro, qo, po, Dinv, rw, pw, qw, x, K2, H, alpha, beta, dots, &pre);
+    gf_block_iter<DIM, MODE, false, true>(V, -1, ro, qo, po, Dinv, rw, pw, qw, x, K2, H, alpha, beta, dots, &pre,
+                                          &hpre);
     GF_MARK(5);
     gf_block_dots(dots, partials, nbk, kit, step_in, blockIdx.x);
     GF_MARK(6);
