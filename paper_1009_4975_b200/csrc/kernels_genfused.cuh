@@ -78,6 +78,9 @@ constexpr int kGfOwnMin = TOMESH_GF_OWN_MIN;             // smallest block targe
 #ifndef TOMESH_GF_MINB
 #define TOMESH_GF_MINB 2
 #endif
+#ifndef TOMESH_GF_SMEMMAX
+#define TOMESH_GF_SMEMMAX 0     // > 0: blocks split until their shared memory fits (A/B of 3 CTAs per SM)
+#endif
 #ifndef TOMESH_GF_HPRE
 #define TOMESH_GF_HPRE 3        // halo DOFs per thread loaded ahead of the owned update (0, 3, 4, 5: c4L 293, 292, 295, 307 us)
 #endif

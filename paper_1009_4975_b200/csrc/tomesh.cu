@@ -320,7 +320,7 @@ struct HostBlocks {
 // max_blocks > 0: stop (return 1) as soon as the cut has more ranges.
 int make_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_hang, const std::vector<int64_t> &iptr,
                     const std::vector<uint32_t> &inc, int64_t N, int own_target, int el_max, int loc_max, int own_max,
-                    int max_blocks, int ch, HostBlocks &hb) {
+                    int max_blocks, int ch, HostBlocks &hb, size_t smem_max = 0) {
   const int nc = 1 << d->dim;
   std::vector<int32_t> el_mark(d->n_elem, -1), nd_mark(d->n_node, -1), el_le(d->n_elem, 0), nd_slot(d->n_node, 0);
   int stamp = 0;
@@ -349,7 +349,17 @@ int make_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_hang
           }
         }
       }
-    return nE <= el_max && (b - a) + nOut <= loc_max;
+    if (nE > el_max || (b - a) + nOut > loc_max) return false;
+    if (smem_max) {   // k_gen_fused's shared memory for this block alone (halo / virtual ids bounded by 8 bytes)
+      const int64_t ninc = iptr[b] - iptr[a];
+      const int64_t rec = 2 * gf_pad16((int)(8 * nOut)) + gf_pad16((int)(2 * nc * nE)) +
+                          gf_pad16((int)(2 * gf_nchunks((int)nE, ch) * (b - a + 1))) + gf_pad16((int)(2 * ninc));
+      const int ys = nc * d->dim + 1;
+      const int64_t sm = rec + 8 * ((nE + 1) & ~1) + 8 * (((b - a) + nOut) * d->dim + 2 * (int64_t)own_max * d->dim +
+                                                          (int64_t)ch * ys) + 16;
+      if ((size_t)sm > smem_max) return false;
+    }
+    return true;
   };
   std::vector<int32_t> node0;
   {
@@ -551,7 +561,8 @@ int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_han
   // (incidence encoding: le * 2^dim < 2^14)
   HostBlocks hb;
   RC(make_gen_blocks(d, node_hang, iptr, inc, N, own_target, std::min(kGfElMax, (1 << 14) / nc - 1), kGfMaxLoc,
-                     kGfMaxOwn, 0, d->dim == 3 ? GfChunk<3>::CH : GfChunk<2>::CH, hb));
+                     std::min(kGfMaxOwn, (own_target + 1) & ~1), 0, d->dim == 3 ? GfChunk<3>::CH : GfChunk<2>::CH, hb,
+                     (size_t)TOMESH_GF_SMEMMAX));
   GenBlocks &B = m->GB;
   RC(upload_gen_blocks(m, hb, B, &m->gb_el_id, &m->gb_n_loc_el, &m->s_loc, st));
   const int nb = B.n_blk;
