@@ -53,7 +53,10 @@ namespace tomesh {
 constexpr int kGfThreads = TOMESH_GF_THREADS;
 constexpr int kGfOwnPerThread = 1;                       // owned nodes per thread in the C^T sums
 constexpr int kGfMaxOwn = kGfThreads * kGfOwnPerThread;  // (block targets are <= 224 nodes)
-constexpr int kGfMaxLoc = 1536;                          // local node slots per block (uint16 slots)
+#ifndef TOMESH_GF_LOCMAX
+#define TOMESH_GF_LOCMAX 1536
+#endif
+constexpr int kGfMaxLoc = TOMESH_GF_LOCMAX;              // local node slots per block (uint16 slots)
 constexpr int kGfPersistMaxBlocks = 32;                  // k_gen_persist only up to this many blocks
 // Launched path: every block evaluates the previous step itself (no step
 // kernel) up to this many blocks; beyond, the O(blocks^2) partial reads cost
@@ -61,7 +64,7 @@ constexpr int kGfPersistMaxBlocks = 32;                  // k_gen_persist only u
 // c4, 1,131 blocks: 62.4 -> 78.2; c4L, 7,099 blocks: 320 -> 772)
 constexpr int kGfStepInMaxBlocks = 256;
 #ifndef TOMESH_GF_OWN3
-#define TOMESH_GF_OWN3 224      // A/B on c4 / c4L: 224 < 320 < 448 < 512 (us per iteration)
+#define TOMESH_GF_OWN3 256      // with the 2-CTA shared-memory cap (TOMESH_GF_SMEMMAX): c4L 224 / 240 / 256: 270 / 264 / 259 us
 #endif
 #ifndef TOMESH_GF_OWN2
 #define TOMESH_GF_OWN2 224
@@ -79,7 +82,11 @@ constexpr int kGfOwnMin = TOMESH_GF_OWN_MIN;             // smallest block targe
 #define TOMESH_GF_MINB 2
 #endif
 #ifndef TOMESH_GF_SMEMMAX
-#define TOMESH_GF_SMEMMAX 0     // > 0: blocks split until their shared memory fits (A/B of 3 CTAs per SM)
+// blocks are split until their shared memory fits two CTAs per SM (228 KB
+// less 1 KB reserved and the static shared memory per CTA): one block above
+// it would halve the residency of the whole grid (c4L with 240-node blocks:
+// one CTA per SM, 426 vs 270 us per iteration)
+#define TOMESH_GF_SMEMMAX 113664
 #endif
 #ifndef TOMESH_GF_HPRE
 #define TOMESH_GF_HPRE 3        // halo DOFs per thread loaded ahead of the owned update (0, 3, 4, 5: c4L 293, 292, 295, 307 us)

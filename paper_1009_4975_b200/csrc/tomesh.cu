@@ -560,9 +560,19 @@ int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_han
                                      : kGfOwnTarget2;
   // (incidence encoding: le * 2^dim < 2^14)
   HostBlocks hb;
-  RC(make_gen_blocks(d, node_hang, iptr, inc, N, own_target, std::min(kGfElMax, (1 << 14) / nc - 1), kGfMaxLoc,
-                     std::min(kGfMaxOwn, (own_target + 1) & ~1), 0, d->dim == 3 ? GfChunk<3>::CH : GfChunk<2>::CH, hb,
-                     (size_t)TOMESH_GF_SMEMMAX));
+  // the kernel's shared memory is the sum of per-section maxima over the
+  // blocks (from different blocks), so the per-block cap is tightened until
+  // the total fits as well
+  size_t cap = (size_t)TOMESH_GF_SMEMMAX;
+  for (int attempt = 0;; ++attempt) {
+    RC(make_gen_blocks(d, node_hang, iptr, inc, N, own_target, std::min(kGfElMax, (1 << 14) / nc - 1), kGfMaxLoc,
+                       std::min(kGfMaxOwn, (own_target + 1) & ~1), 0, d->dim == 3 ? GfChunk<3>::CH : GfChunk<2>::CH,
+                       hb, cap));
+    const size_t tot = d->dim == 3 ? gf_smem_bytes<3>(hb.max_rec16, hb.max_el, hb.max_loc, hb.max_own)
+                                   : gf_smem_bytes<2>(hb.max_rec16, hb.max_el, hb.max_loc, hb.max_own);
+    if (!cap || tot <= (size_t)TOMESH_GF_SMEMMAX || attempt == 4) break;
+    cap -= std::min(cap / 2, tot - (size_t)TOMESH_GF_SMEMMAX + 1024);
+  }
   GenBlocks &B = m->GB;
   RC(upload_gen_blocks(m, hb, B, &m->gb_el_id, &m->gb_n_loc_el, &m->s_loc, st));
   const int nb = B.n_blk;
