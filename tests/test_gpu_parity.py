@@ -259,3 +259,20 @@ def test_structured_deferred_x_update():
         assert all(s.iters == k and s.status == 0 for s in sts), (k, [s.iters for s in sts])
         ug = cuda(g.gather_nodes(uss))
         assert abs(true_res(ug) - sts[0].relres) <= 1e-8 * sts[0].relres, k
+
+
+@pytest.mark.parametrize("name", ["c4s", "amr3d", "c2_launched", "c5s_general"])
+def test_general_block_decomposition(name):
+    """The owner-computes decomposition the general kernel runs on
+    (to_mesh_info.gen_*): every element is staged by at least one block and
+    every unconstrained node is owned by exactly one (local slots >= nodes),
+    and the kernel's shared memory fits two CTAs per SM (the block builder
+    splits blocks until it does)."""
+    prob, om, hm, m, x_dev = _setup(name)
+    info = m.info()
+    assert info["structured"] == 0
+    assert info["gen_blocks"] >= 1
+    assert info["gen_local_el"] >= info["n_elem"]
+    assert info["gen_local_nodes"] >= info["n_node"] - info["n_hang"]
+    assert 0 < info["gen_smem_bytes"] <= 113664
+    assert info["gen_max_el"] <= 2047 and info["gen_max_loc"] <= 1536
