@@ -142,8 +142,15 @@ typedef struct {
  *                            kernel).
  *   TO_UPLOAD_NO_CLUSTER     general path: do not use the cluster-resident
  *                            solver (the cooperative kernel, or one kernel
- *                            per iteration, instead). */
-enum { TO_UPLOAD_GENERAL = 1, TO_UPLOAD_LAUNCHED = 2, TO_UPLOAD_NO_CLUSTER = 4 };
+ *                            per iteration, instead).
+ *   TO_UPLOAD_EP             general path: run tosolve_cg's iterations on the
+ *                            element-partitioned blocks (every element once,
+ *                            partial sums of shared nodes in per-block slots,
+ *                            Chronopoulos-Gear form of the same PCG);
+ *                            the default for large meshes where enabled.
+ *   TO_UPLOAD_NO_EP          general path: never use it. */
+enum { TO_UPLOAD_GENERAL = 1, TO_UPLOAD_LAUNCHED = 2, TO_UPLOAD_NO_CLUSTER = 4, TO_UPLOAD_EP = 8,
+       TO_UPLOAD_NO_EP = 16 };
 
 typedef struct {
   int32_t iters;               /* CG iterations performed                        */
@@ -164,7 +171,9 @@ typedef struct {
                                   kernel per iteration), 3 general, whole
                                   loop in one cooperative kernel, 4 general
                                   one kernel per iteration, 5 general, whole
-                                  loop in one thread-block cluster          */
+                                  loop in one thread-block cluster, 6 general
+                                  element-partitioned, one kernel per
+                                  iteration                                    */
   int64_t launches_total;      /* kernels launched by every call on this handle
                                   since upload (monotone counter)               */
   int32_t gen_blocks;          /* general path: owner-computes blocks (CTAs per

@@ -14,7 +14,7 @@ TO_OK, TO_NOT_CONVERGED = 0, 1
 TO_EINVAL, TO_ECUDA, TO_ENOMEM, TO_EMESH, TO_ENAN, TO_EBREAKDOWN, TO_ENONPOS_DIAG = -1, -2, -3, -4, -5, -6, -7
 TO_WARM, TO_FIXED_ITERS, TO_HISTORY, TO_NO_TRUE_RES, TO_PROFILE, TO_PROFILE_LOOP = 1, 2, 4, 8, 16, 32
 TO_FILTER_SENS, TO_FILTER_DENS = 0, 1
-TO_UPLOAD_GENERAL, TO_UPLOAD_LAUNCHED, TO_UPLOAD_NO_CLUSTER = 1, 2, 4
+TO_UPLOAD_GENERAL, TO_UPLOAD_LAUNCHED, TO_UPLOAD_NO_CLUSTER, TO_UPLOAD_EP, TO_UPLOAD_NO_EP = 1, 2, 4, 8, 16
 TO_PC_JACOBI, TO_PC_IC0 = 0, 1
 TOH_LOAD_POINT, TOH_LOAD_LINE, TOH_LOAD_FACE = 0, 1, 2
 

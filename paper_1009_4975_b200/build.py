@@ -22,7 +22,8 @@ LIB = os.path.join(PKG, "libtomesh.so")
 SOURCES = ["tomesh.cu", "tomesh_minres.cu", "tomesh_opt.cu", "tomesh_shard.cu", "host_mesh.cpp", "element.cpp", "errors.cpp"]
 HEADERS = ["common.h", "device_common.cuh", "element.h", "tomesh_types.cuh", "tomesh_impl.cuh", "kernels_cg.cuh",
            "kernels_general.cuh", "kernels_struct3d.cuh", "kernels_oc.cuh", "kernels_minres.cuh", "kernels_ic0.cuh",
-           "kernels_shard.cuh", "kernels_genfused.cuh", "kernels_gencluster.cuh", "kernels_gshard.cuh"]
+           "kernels_shard.cuh", "kernels_genfused.cuh", "kernels_gencluster.cuh", "kernels_gshard.cuh",
+           "kernels_genep.cuh"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

@@ -88,6 +88,52 @@ __device__ __forceinline__ void cg_single_step(CgScalars *S, int k, const double
   S->ab[k & 1][1] = S->beta;
 }
 
+// Element-partitioned general path (kernels_genep.cuh), end of iteration k in
+// the Chronopoulos-Gear form: d = {gamma_k = r_k.u_k, rr_k, delta_k = A u_k .
+// u_k}, u_k = Dinv r_k, all of kernel k's vectors.  x_k is complete.
+//   stop if rr_k <= rtol^2 ||b||^2;
+//   beta_k = gamma_k / gamma_{k-1} (beta_0 = 0),
+//   alpha_k = gamma_k / (delta_k - beta_k gamma_k / alpha_{k-1}) (alpha_0 = gamma_0 / delta_0)
+// (the denominator is p_k . A p_k: <= 0 is a breakdown, status -6).
+__device__ __forceinline__ void cg_cgear_step(CgScalars *S, int k, const double (&d)[5], double rtol, double *hist) {
+  const double gam = d[0], rr = d[1], del = d[2];
+  if (k == 0) {
+    S->thresh2 = rtol * rtol * S->bnorm2;
+    if (S->status != 0) {
+      S->done = 1;
+      return;
+    }
+  }
+  const double gam_prev = S->rho, alpha_prev = S->alpha;
+  S->iter = k;
+  S->rho = gam;
+  S->rr = rr;
+  if (!(gam == gam) || !(rr == rr) || !(del == del)) {
+    cg_fail(S, -5);
+    S->done = 1;
+    return;
+  }
+  if (S->history && hist && k >= 1) hist[k - 1] = sqrt(rr / S->bnorm2);
+  if ((!S->fixed && rr <= S->thresh2) || S->bnorm2 == 0.0) {
+    S->done = 1;
+    return;
+  }
+  double beta = 0.0, den = del;
+  if (k > 0) {
+    beta = gam / gam_prev;
+    den = del - beta * gam / alpha_prev;
+  }
+  if (!(den > 0.0)) {
+    cg_fail(S, -6);
+    S->done = 1;
+    return;
+  }
+  S->alpha = gam / den;
+  S->beta = beta;
+  S->ab[k & 1][0] = S->alpha;
+  S->ab[k & 1][1] = S->beta;
+}
+
 // cg_single_step split for the sharded K1, where EVERY CTA of iteration k+1
 // forms the step of iteration k from the same gathered dots (no separate step
 // kernel): cg_step_eval is the pure decision (reads only fields that are

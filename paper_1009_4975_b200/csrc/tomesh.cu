@@ -7,6 +7,7 @@
 #include "kernels_general.cuh"
 #include "kernels_genfused.cuh"
 #include "kernels_gencluster.cuh"
+#include "kernels_genep.cuh"
 #include "kernels_struct3d.cuh"
 
 using namespace tomesh;
@@ -59,7 +60,8 @@ int validate(const to_mesh_desc *d) {
     if (f < 0 || f >= d->n_node * d->dim || (i > 0 && f <= d->fixed_dof[i - 1])) { set_error("fixed_dof not ascending / out of range"); return TO_EMESH; }
     if (hang[f / d->dim]) { set_error("fixed DOF %lld is on a hanging node", (long long)f); return TO_EMESH; }
   }
-  if ((d->options & ~(uint32_t)(TO_UPLOAD_GENERAL | TO_UPLOAD_LAUNCHED | TO_UPLOAD_NO_CLUSTER)) != 0) {
+  if ((d->options & ~(uint32_t)(TO_UPLOAD_GENERAL | TO_UPLOAD_LAUNCHED | TO_UPLOAD_NO_CLUSTER | TO_UPLOAD_EP |
+                                TO_UPLOAD_NO_EP)) != 0) {
     set_error("unknown upload option bits 0x%x", d->options);
     return TO_EINVAL;
   }
@@ -597,6 +599,270 @@ int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_han
   return 0;
 }
 
+// Element-partitioned decomposition (kernels_genep.cuh): node ranges as in
+// build_gen_blocks; element e is assigned to the block owning its smallest
+// contributed node (non-hanging corner or parent of a hanging corner); node
+// n's operator output is the sum of one partial per contributor block, in
+// ascending block order (slot_ptr[n] .. slot_ptr[n+1]).  Deterministic: every
+// list is built in ascending order from the mesh alone.
+int build_gen_ep(const to_mesh_desc *d, const std::vector<int32_t> &node_hang, cudaStream_t st, to_mesh *m) {
+  const int nc = 1 << d->dim, dim = d->dim;
+  const int64_t N = d->n_node, E = d->n_elem;
+  const int ch = dim == 3 ? GfChunk<3>::CH : GfChunk<2>::CH, ys = nc * dim + 1;
+  if (N >= INT32_MAX / 8) { set_error("mesh too large for the element-partitioned path"); return TO_EINVAL; }
+  auto code = [](double w) -> uint32_t { return w == 1.0 ? 0u : w == 0.5 ? 1u : 2u; };
+  // smallest contributed node of every element; elements bucketed by it
+  std::vector<int32_t> emin(E);
+  for (int64_t e = 0; e < E; ++e) {
+    int32_t mn = INT32_MAX;
+    for (int c = 0; c < nc; ++c) {
+      const int32_t g = d->elem_node[e * nc + c], h = node_hang[g];
+      if (h < 0) mn = std::min(mn, g);
+      else
+        for (int32_t q = d->hang_ptr[h]; q < d->hang_ptr[h + 1]; ++q) mn = std::min(mn, d->hang_parent[q]);
+    }
+    emin[e] = mn;
+  }
+  std::vector<int64_t> bptr(N + 1, 0);
+  for (int64_t e = 0; e < E; ++e) bptr[emin[e] + 1]++;
+  for (int64_t n = 0; n < N; ++n) bptr[n + 1] += bptr[n];
+  std::vector<int32_t> bel(E);
+  {
+    std::vector<int64_t> f(bptr.begin(), bptr.end() - 1);
+    for (int64_t e = 0; e < E; ++e) bel[f[emin[e]]++] = (int32_t)e;
+  }
+  std::vector<int32_t> mark(N, -1), hmark(N, -1);
+  int stamp = 0;
+  // local node counts of a candidate range [a, b)
+  struct Cnt { int64_t nE, nHalo, nVirt, nInc; };
+  auto count = [&](int64_t a, int64_t b) {
+    const int sp = ++stamp;
+    Cnt c{bptr[b] - bptr[a], 0, 0, 0};
+    for (int64_t k = bptr[a]; k < bptr[b]; ++k) {
+      const int64_t e = bel[k];
+      for (int cc = 0; cc < nc; ++cc) {
+        const int32_t g = d->elem_node[e * nc + cc], h = node_hang[g];
+        if (h < 0) {
+          ++c.nInc;
+          if ((g < a || g >= b) && mark[g] != sp) { mark[g] = sp; ++c.nHalo; }
+        } else {
+          if (hmark[g] != sp) { hmark[g] = sp; ++c.nVirt; }
+          for (int32_t q = d->hang_ptr[h]; q < d->hang_ptr[h + 1]; ++q) {
+            const int32_t pn = d->hang_parent[q];
+            ++c.nInc;
+            if ((pn < a || pn >= b) && mark[pn] != sp) { mark[pn] = sp; ++c.nHalo; }
+          }
+        }
+      }
+    }
+    return c;
+  };
+  const size_t cap = (size_t)TOMESH_GF_SMEMMAX;
+  auto fits = [&](int64_t a, int64_t b) {
+    const Cnt c = count(a, b);
+    const int64_t nOwn = b - a, nAcc = nOwn + c.nHalo, nLoc = nAcc + c.nVirt;
+    if (nOwn > kGfMaxOwn || nAcc > kEpMaxAcc || nLoc > kGfMaxLoc || c.nE > kGfElMax || c.nInc > 0xffff) return false;
+    const int64_t rec = gf_pad16((int)(4 * c.nHalo)) + gf_pad16((int)(8 * c.nVirt)) + gf_pad16((int)(2 * nc * c.nE)) +
+                        gf_pad16((int)(2 * gf_nchunks((int)c.nE, ch) * (nAcc + 1))) + gf_pad16((int)(2 * c.nInc)) +
+                        gf_pad16((int)(4 * nAcc)) + gf_pad16((int)(4 * c.nHalo)) + gf_pad16((int)c.nHalo);
+    const size_t sm = (size_t)rec + 8 * (size_t)((c.nE + 1) & ~1) + 8 * ((size_t)nLoc * dim + (size_t)ch * ys) + 16;
+    return sm <= cap;
+  };
+  const int own_target = dim == 3 ? TOMESH_EP_OWN3 : TOMESH_EP_OWN2;
+  std::vector<int32_t> node0;
+  {
+    std::vector<std::pair<int64_t, int64_t>> todo;
+    const int64_t tgt = (own_target + 1) & ~1;
+    for (int64_t a = 0; a < N; a += tgt) todo.push_back({a, std::min<int64_t>(N, a + tgt)});
+    std::reverse(todo.begin(), todo.end());
+    while (!todo.empty()) {
+      auto [a, b] = todo.back();
+      todo.pop_back();
+      if (fits(a, b)) { node0.push_back((int32_t)a); continue; }
+      if (b - a <= 2) { set_error("element-partitioned block of node %lld exceeds the kernel limits", (long long)a); return TO_EINVAL; }
+      const int64_t mid = a + ((b - a) / 2 & ~(int64_t)1);
+      todo.push_back({mid, b});
+      todo.push_back({a, mid});
+    }
+    node0.push_back((int32_t)N);
+  }
+  const int nb = (int)node0.size() - 1;
+  // contributors per node (ascending block): counts, then slot pointers
+  std::vector<int32_t> lastb(N, -1);
+  std::vector<int64_t> sptr(N + 1, 0);
+  auto for_contrib = [&](int64_t e, auto f) {
+    for (int cc = 0; cc < nc; ++cc) {
+      const int32_t g = d->elem_node[e * nc + cc], h = node_hang[g];
+      if (h < 0) f(g);
+      else
+        for (int32_t q = d->hang_ptr[h]; q < d->hang_ptr[h + 1]; ++q) f(d->hang_parent[q]);
+    }
+  };
+  for (int b = 0; b < nb; ++b)
+    for (int64_t k = bptr[node0[b]]; k < bptr[node0[b + 1]]; ++k)
+      for_contrib(bel[k], [&](int32_t g) {
+        if (lastb[g] != b) { lastb[g] = b; sptr[g + 1]++; }
+      });
+  for (int64_t n = 0; n < N; ++n) {
+    if (sptr[n + 1] > 255) { set_error("node %lld has more than 255 contributor blocks", (long long)n); return TO_EINVAL; }
+    sptr[n + 1] += sptr[n];
+  }
+  const int64_t n_slots = sptr[N];
+  if (n_slots * dim >= INT32_MAX) { set_error("too many slots for the element-partitioned path"); return TO_EINVAL; }
+  std::vector<int64_t> sfill(sptr.begin(), sptr.end() - 1);
+  std::vector<GfMeta> meta(nb);
+  std::vector<uint8_t> rec;
+  std::vector<int32_t> el_id;
+  int max_loc = 0, max_rec16 = 0, max_el = 0;
+  int64_t loc_el = 0, loc_nodes = 0;
+  std::vector<int32_t> slot_of(N, 0);
+  auto put = [&](const void *src, size_t bytes) {
+    const size_t at = rec.size();
+    rec.resize(at + ((bytes + 15) & ~(size_t)15), 0);
+    if (bytes) std::memcpy(rec.data() + at, src, bytes);
+  };
+  std::vector<int32_t> elems, hl, vt;
+  for (int bk = 0; bk < nb; ++bk) {
+    const int64_t a = node0[bk], b = node0[bk + 1];
+    const int sp = ++stamp;
+    elems.assign(bel.begin() + bptr[a], bel.begin() + bptr[b]);
+    std::sort(elems.begin(), elems.end());
+    hl.clear();
+    vt.clear();
+    for (int32_t e : elems)
+      for (int cc = 0; cc < nc; ++cc) {
+        const int32_t g = d->elem_node[(int64_t)e * nc + cc], h = node_hang[g];
+        if (h < 0) {
+          if ((g < a || g >= b) && mark[g] != sp) { mark[g] = sp; hl.push_back(g); }
+        } else {
+          if (hmark[g] != sp) { hmark[g] = sp; vt.push_back(g); }
+          for (int32_t q = d->hang_ptr[h]; q < d->hang_ptr[h + 1]; ++q) {
+            const int32_t pn = d->hang_parent[q];
+            if ((pn < a || pn >= b) && mark[pn] != sp) { mark[pn] = sp; hl.push_back(pn); }
+          }
+        }
+      }
+    std::sort(hl.begin(), hl.end());
+    std::sort(vt.begin(), vt.end());
+    const int nOwn = (int)(b - a), nHalo = (int)hl.size(), nVirt = (int)vt.size(), nE = (int)elems.size();
+    const int nAcc = nOwn + nHalo;
+    for (int i = 0; i < nHalo; ++i) slot_of[hl[i]] = nOwn + i;
+    for (int i = 0; i < nVirt; ++i) slot_of[vt[i]] = nAcc + i;
+    auto slot = [&](int32_t g) { return (g >= a && g < b && node_hang[g] < 0) ? (int)(g - a) : slot_of[g]; };
+    std::vector<ushort4> vrec(nVirt);
+    for (int i = 0; i < nVirt; ++i) {
+      const int32_t g = vt[i], h = node_hang[g];
+      const int np = d->hang_ptr[h + 1] - d->hang_ptr[h];
+      if (np != 2 && np != 4) { set_error("hanging node %d has %d parents (2 or 4 expected)", g, np); return TO_EMESH; }
+      uint16_t ps[4] = {0xffff, 0xffff, 0xffff, 0xffff};
+      for (int q = 0; q < np; ++q) {
+        const double w = d->hang_weight[d->hang_ptr[h] + q];
+        if (w != 1.0 / np) { set_error("hanging node %d: weight %g with %d parents", g, w, np); return TO_EMESH; }
+        ps[q] = (uint16_t)slot(d->hang_parent[d->hang_ptr[h] + q]);
+      }
+      vrec[i] = make_ushort4(ps[0], ps[1], ps[2], ps[3]);
+    }
+    std::vector<uint16_t> crec((size_t)nE * nc);
+    // incidences grouped by (chunk, local accumulating node), in (element, corner, parent) order
+    const int nch = gf_nchunks(nE, ch);
+    std::vector<std::vector<uint16_t>> lists((size_t)nch * nAcc);
+    std::vector<uint32_t> wslot(nAcc, 0xffffffffu);
+    for (int le = 0; le < nE; ++le) {
+      const int64_t e = elems[le];
+      const int cix = le / ch;
+      for (int cc = 0; cc < nc; ++cc) {
+        const int32_t g = d->elem_node[e * nc + cc], h = node_hang[g];
+        crec[(size_t)le * nc + cc] = (uint16_t)slot(g);
+        const uint32_t off = (uint32_t)((le - cix * ch) * ys + cc * dim);
+        auto add = [&](int32_t t, uint32_t cd) {
+          const int l = slot(t);
+          lists[(size_t)cix * nAcc + l].push_back((uint16_t)(off | (cd << 14)));
+          if (wslot[l] == 0xffffffffu) wslot[l] = (uint32_t)(sfill[t]++);
+        };
+        if (h < 0) add(g, 0u);
+        else
+          for (int32_t q = d->hang_ptr[h]; q < d->hang_ptr[h + 1]; ++q)
+            add(d->hang_parent[q], code(d->hang_weight[q]));
+      }
+    }
+    std::vector<uint16_t> iptr_l, inc_l;
+    for (int cix = 0; cix < nch; ++cix) {
+      iptr_l.push_back((uint16_t)inc_l.size());
+      for (int l = 0; l < nAcc; ++l) {
+        const auto &L = lists[(size_t)cix * nAcc + l];
+        inc_l.insert(inc_l.end(), L.begin(), L.end());
+        if (inc_l.size() > 0xffff) { set_error("element-partitioned block with more than 65535 incidences"); return TO_EINVAL; }
+        iptr_l.push_back((uint16_t)inc_l.size());
+      }
+    }
+    std::vector<uint32_t> hslot(nHalo);
+    std::vector<uint8_t> hcnt(nHalo);
+    for (int i = 0; i < nHalo; ++i) {
+      hslot[i] = (uint32_t)sptr[hl[i]];
+      hcnt[i] = (uint8_t)(sptr[hl[i] + 1] - sptr[hl[i]]);
+    }
+    GfMeta &mt = meta[bk];
+    mt.node0 = (int32_t)a;
+    mt.n_own = nOwn;
+    mt.n_halo = nHalo;
+    mt.n_virt = nVirt;
+    mt.n_el = nE;
+    mt.n_inc = (int32_t)inc_l.size();
+    mt.el_off = (int32_t)el_id.size();
+    mt.rec_off16 = (int32_t)(rec.size() / 16);
+    const size_t r0 = rec.size();
+    put(hl.data(), 4 * hl.size());
+    put(vrec.data(), 8 * vrec.size());
+    put(crec.data(), 2 * crec.size());
+    put(iptr_l.data(), 2 * iptr_l.size());
+    put(inc_l.data(), 2 * inc_l.size());
+    put(wslot.data(), 4 * wslot.size());
+    put(hslot.data(), 4 * hslot.size());
+    put(hcnt.data(), hcnt.size());
+    const EpSections sec = ep_sections(dim, nOwn, nHalo, nVirt, nE, mt.n_inc, ch);
+    if ((size_t)sec.total != rec.size() - r0) { set_error("internal: element-partitioned record layout"); return TO_EINVAL; }
+    for (int32_t e : elems) el_id.push_back(e);
+    if (nE & 1) el_id.push_back(-1);
+    max_loc = std::max(max_loc, nAcc + nVirt);
+    max_rec16 = std::max(max_rec16, sec.total / 16);
+    max_el = std::max(max_el, nE);
+    loc_el += nE;
+    loc_nodes += nAcc + nVirt;
+  }
+  for (int64_t n = 0; n < N; ++n)
+    if (sfill[n] != sptr[n + 1]) { set_error("internal: element-partitioned slot count"); return TO_EINVAL; }
+  if (rec.size() / 16 >= (size_t)INT32_MAX) { set_error("mesh too large for the element-partitioned records"); return TO_EINVAL; }
+  GenBlocks &B = m->EB;
+  B.n_blk = nb;
+  B.max_loc = max_loc;
+  B.max_own = kGfMaxOwn;
+  B.max_rec16 = max_rec16;
+  B.max_el = max_el;
+  GfMeta *dmeta;
+  uint4 *drec;
+  RC(upload_array(m, &dmeta, meta.data(), meta.size(), st));
+  RC(upload_array(m, &drec, reinterpret_cast<const uint4 *>(rec.data()), rec.size() / 16, st));
+  RC(upload_array(m, &m->ep_el_id, el_id.data(), el_id.size(), st));
+  B.meta = dmeta;
+  B.rec = drec;
+  m->ep_n_loc_el = (int64_t)el_id.size();
+  RC(m->alloc(&m->ep_s_loc, (size_t)std::max<int64_t>(2, m->ep_n_loc_el)));
+  std::vector<int32_t> sp32(sptr.begin(), sptr.end());
+  RC(upload_array(m, &m->ep_slot_ptr, sp32.data(), sp32.size(), st));
+  for (int k = 0; k < 2; ++k) {
+    RC(m->alloc(&m->ep_W[k], (size_t)std::max<int64_t>(1, n_slots * dim)));
+    CK(cudaMemsetAsync(m->ep_W[k], 0, sizeof(double) * (size_t)std::max<int64_t>(1, n_slots * dim), st));
+  }
+  m->ep_smem = dim == 3 ? ep_smem_bytes<3>(max_rec16, max_el, max_loc) : ep_smem_bytes<2>(max_rec16, max_el, max_loc);
+  RC(allow_smem(m, dim == 3 ? (const void *)k_gen_ep<3> : (const void *)k_gen_ep<2>, m->ep_smem));
+  RC(ensure_partials(m, (size_t)nb * 5));
+  m->ep_n_slots = n_slots;
+  m->ep_local_el = loc_el;
+  m->ep_local_nodes = loc_nodes;
+  m->gen_ep = true;
+  return 0;
+}
+
 const void *gc_kernel(int dim, int T) {
   if (dim == 2) return T == 128 ? (const void *)k_gen_cluster<2, 128> : T == 256 ? (const void *)k_gen_cluster<2, 256>
                                                                               : (const void *)k_gen_cluster<2, 512>;
@@ -814,9 +1080,15 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
     std::vector<uint32_t> incv;
     RC(setup_incidence(d, node_hang, st, m, iptr, incv));
     RC(build_gen_blocks(d, node_hang, iptr, incv, st, m));
+    // large meshes (the launched path with a step kernel): the element-
+    // partitioned iteration (kernels_genep.cuh), unless TO_UPLOAD_NO_EP or a
+    // shard's local mesh; TO_UPLOAD_EP forces it
+    const bool ep_auto = TOMESH_EP_AUTO && m->GB.n_blk > kGfStepInMaxBlocks;
+    if (d->n_owned == 0 && !(d->options & TO_UPLOAD_NO_EP) && ((d->options & TO_UPLOAD_EP) || ep_auto))
+      RC(build_gen_ep(d, node_hang, st, m));
     // the smallest meshes: one thread-block cluster holds the whole solve
     // (k_gen_cluster), unless TO_UPLOAD_LAUNCHED / NO_CLUSTER or a shard's local mesh
-    if (!(d->options & (TO_UPLOAD_LAUNCHED | TO_UPLOAD_NO_CLUSTER)) && d->n_owned == 0)
+    if (!(d->options & (TO_UPLOAD_LAUNCHED | TO_UPLOAD_NO_CLUSTER)) && d->n_owned == 0 && !m->gen_ep)
       RC(build_gen_cluster(d, node_hang, iptr, incv, st, m));
     // small meshes (at most kGfPersistMaxBlocks blocks): the whole loop in one
     // cooperative kernel, unless TO_UPLOAD_LAUNCHED.  Measured: c1 (6 blocks)
@@ -825,7 +1097,7 @@ int do_upload(const to_mesh_desc *d, int device, cudaStream_t st, to_mesh *m) {
     // PDL-chained launches once there are more than a few dozen blocks
     int coop = 0;
     CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
-    if (coop && !m->gen_cluster && !(d->options & TO_UPLOAD_LAUNCHED) && d->n_owned == 0 &&
+    if (coop && !m->gen_cluster && !m->gen_ep && !(d->options & TO_UPLOAD_LAUNCHED) && d->n_owned == 0 &&
         m->GB.n_blk <= kGfPersistMaxBlocks) {
       int per_sm = 0;
       const void *fn = d->dim == 2 ? (const void *)k_gen_persist<2> : (const void *)k_gen_persist<3>;
@@ -957,6 +1229,10 @@ int op_scale_and_diag(to_mesh *m, double penal, const double *x, double *d_int, 
       k_gather_s<<<grid_for(m->gc_n_loc_el), kBlock, 0, st>>>(m->gc_n_loc_el, m->gc_el_id, m->s, m->gc_s_loc);
       m->last_launches++;
     }
+    if (m->gen_ep) {
+      k_gather_s<<<grid_for(m->ep_n_loc_el), kBlock, 0, st>>>(m->ep_n_loc_el, m->ep_el_id, m->s, m->ep_s_loc);
+      m->last_launches++;
+    }
     return check_launch();
   }
   k_simp_s3<<<grid_for(m->n_el), kBlock, 0, st>>>(m->n_el, x, m->perm_el, penal, m->E0, m->Emin, m->h_struct,
@@ -1024,6 +1300,43 @@ int op_cg_gen_step(to_mesh *m, int k, double rtol, cudaStream_t st, bool step_in
 }
 
 // General path, x_N and the final residual after N iterations.
+// Element-partitioned path (kernels_genep.cuh): iteration k and its step.
+int op_cg_ep(to_mesh *m, int k, cudaStream_t st) {
+  const int o = (k + 1) & 1, w = k & 1;
+  if (m->dim == 2)
+    RC(launch_pdl(k_gen_ep<2>, dim3(m->EB.n_blk), dim3(kGfThreads), m->ep_smem, st, m->EB,
+                  (const double *)m->ep_s_loc, (const int32_t *)m->ep_slot_ptr, (const double *)m->ep_W[o],
+                  m->ep_W[w], (const double *)m->rb[o], (const double *)m->qb[o], (const double *)m->pb[o],
+                  (const double *)m->dinv, m->rb[w], m->qb[w], m->pb[w], m->x, m->K2, m->KS, m->S, m->partials));
+  else
+    RC(launch_pdl(k_gen_ep<3>, dim3(m->EB.n_blk), dim3(kGfThreads), m->ep_smem, st, m->EB,
+                  (const double *)m->ep_s_loc, (const int32_t *)m->ep_slot_ptr, (const double *)m->ep_W[o],
+                  m->ep_W[w], (const double *)m->rb[o], (const double *)m->qb[o], (const double *)m->pb[o],
+                  (const double *)m->dinv, m->rb[w], m->qb[w], m->pb[w], m->x, m->K2, m->KS, m->S, m->partials));
+  m->last_launches++;
+  return 0;
+}
+int op_cg_ep_step(to_mesh *m, int k, double rtol, cudaStream_t st) {
+  RC(launch_pdl(k_gen_ep_step, dim3(1), dim3(512), 0, st, m->EB.n_blk, (const double *)m->partials, m->S, k, rtol,
+                m->hist));
+  m->last_launches++;
+  return 0;
+}
+// x_N after exactly N element-partitioned iterations (s = A p recurrence).
+int op_final_ep(to_mesh *m, int n_iter, double rtol, cudaStream_t st) {
+  const int o = (n_iter + 1) & 1;
+  if (m->dim == 2)
+    k_final_ep<2><<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->ep_slot_ptr, m->ep_W[o], m->rb[o], m->qb[o],
+                                                         m->pb[o], m->dinv, m->x, m->partials, m->S, n_iter, rtol,
+                                                         m->hist);
+  else
+    k_final_ep<3><<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->ep_slot_ptr, m->ep_W[o], m->rb[o], m->qb[o],
+                                                         m->pb[o], m->dinv, m->x, m->partials, m->S, n_iter, rtol,
+                                                         m->hist);
+  m->last_launches++;
+  return check_launch();
+}
+
 int op_final_gen(to_mesh *m, int n_iter, double rtol, cudaStream_t st) {
   const int o = (n_iter + 1) & 1;
   k_final_gen<false><<<grid_for(m->n_dof), kBlock, 0, st>>>(m->n_dof, m->rb[o], m->qb[o], m->pb[o], m->dinv,
@@ -1107,12 +1420,16 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   // kernel for small meshes): iteration 0 reads r0 = b from rb[1]
   const bool cluster = !m->structured && m->gen_cluster;
   const bool persistent = !m->structured && !cluster && m->gen_persist;
+  // element-partitioned iteration (large general meshes, kernels_genep.cuh)
+  const bool ep = !m->structured && m->gen_ep;
   // launched general path: the step inside the block kernel for small grids
-  const bool step_in = !m->structured && m->GB.n_blk <= kGfStepInMaxBlocks;
+  const bool step_in = !m->structured && !ep && m->GB.n_blk <= kGfStepInMaxBlocks;
   double *r0 = m->rb[1];
   if (!m->structured) {   // q_{-1} = p_{-1} = 0 (finite whatever an earlier solve left)
     CK(cudaMemsetAsync(m->qb[1], 0, sizeof(double) * n, st));
     CK(cudaMemsetAsync(m->pb[1], 0, sizeof(double) * n, st));
+    // element-partitioned: s_{-2} = qb[1] = 0, p_{-2} = 0, w_{-1} = 0 (slots of buffer 1)
+    if (ep) CK(cudaMemsetAsync(m->ep_W[1], 0, sizeof(double) * (size_t)m->ep_n_slots * m->dim, st));
   }
   RC(op_rhs(m, r0, st));
   const int gv = grid_for(n);
@@ -1199,6 +1516,11 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
         RC(op_cg_s3(m, launched + k, rtol, st));
         if (prof) CK(cudaEventRecord(E[1], st));
         if (prof) CK(cudaEventRecord(E[2], st));
+      } else if (ep) {
+        RC(op_cg_ep(m, launched + k, st));
+        if (prof) CK(cudaEventRecord(E[1], st));
+        RC(op_cg_ep_step(m, launched + k, rtol, st));
+        if (prof) CK(cudaEventRecord(E[2], st));
       } else if (step_in) {
         RC(op_cg_gen(m, launched + k, rtol, st, true));
         if (prof) CK(cudaEventRecord(E[1], st));
@@ -1224,6 +1546,7 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
   if (loop_prof) CK(cudaEventRecord(m->loop_ev[1], st));
   // x_N after exactly N iterations (a no-op if an iteration already converged)
   if (m->structured) RC(op_final_s3(m, max_iter, rtol, st));
+  else if (ep) RC(op_final_ep(m, max_iter, rtol, st));
   else RC(op_final_gen(m, max_iter, rtol, st));
   RC(check_launch());
   RC(read_scalars(m, st));
@@ -1327,9 +1650,16 @@ extern "C" int tomesh_get_info(const to_mesh *m, to_mesh_info *info) {
   info->filt_nnz = m->filt_nnz;
   info->device_bytes = m->dev_bytes;
   info->kernel_launches = m->last_launches;
-  info->matvec_variant = m->structured ? 1 : m->gen_cluster ? 5 : m->gen_persist ? 3 : 4;
+  info->matvec_variant = m->structured ? 1 : m->gen_cluster ? 5 : m->gen_persist ? 3 : m->gen_ep ? 6 : 4;
   info->launches_total = m->launches_total;
-  if (m->gen_fused) {
+  if (m->gen_ep) {   // the CG iteration runs on the element-partitioned blocks
+    info->gen_blocks = m->EB.n_blk;
+    info->gen_smem_bytes = (int32_t)m->ep_smem;
+    info->gen_max_loc = m->EB.max_loc;
+    info->gen_max_el = m->EB.max_el;
+    info->gen_local_el = m->ep_local_el;
+    info->gen_local_nodes = m->ep_local_nodes;
+  } else if (m->gen_fused) {
     info->gen_blocks = m->GB.n_blk;
     info->gen_smem_bytes = (int32_t)m->gb_smem;
     info->gen_max_loc = m->GB.max_loc;

@@ -63,6 +63,16 @@ struct to_mesh {
   double *s_loc = nullptr;             // s_e in block-local element order
   size_t gb_smem = 0;                  // dynamic shared memory of k_gen_fused
   int64_t gb_local_el = 0, gb_local_nodes = 0;   // staged elements / local node slots over all blocks
+  // element-partitioned CG iteration (kernels_genep.cuh; large general meshes)
+  bool gen_ep = false;
+  GenBlocks EB{};
+  int32_t *ep_el_id = nullptr;
+  int64_t ep_n_loc_el = 0;
+  double *ep_s_loc = nullptr;
+  int32_t *ep_slot_ptr = nullptr;      // node -> its partial slots [n_node + 1]
+  double *ep_W[2] = {nullptr, nullptr};   // operator output partials (ping-pong)
+  size_t ep_smem = 0;
+  int64_t ep_local_el = 0, ep_local_nodes = 0, ep_n_slots = 0;
   // small meshes: the whole loop in one thread-block cluster (kernels_gencluster.cuh)
   bool gen_cluster = false;
   GenBlocks GC{};                      // its decomposition (at most kGcMaxBlocks blocks)

@@ -31,6 +31,12 @@ CASES = {
     "amr3d": lambda: cantilever3d((3, 2, 2), L=2, leaves=refine_some(3, (3, 2, 2), 2, [(1, 1, 0)]), rmin=0.4),
     "hload2d": hanging_load2d,       # loads on hanging nodes (C8): b = Pi_F C^T f, c = f^T u with them
     "hload3d": hanging_load3d,
+    # the element-partitioned iteration (TO_UPLOAD_EP, kernels_genep.cuh: each element once,
+    # partial sums in per-block slots, Chronopoulos-Gear form of the same PCG)
+    "c2_ep": lambda: config("c2"),
+    "c4s_ep": lambda: config("c4", base=(12, 6, 6), L=2, n_gauss=60),
+    "amr3d_ep": lambda: cantilever3d((3, 2, 2), L=2, leaves=refine_some(3, (3, 2, 2), 2, [(1, 1, 0)]), rmin=0.4),
+    "hload3d_ep": hanging_load3d,
 }
 
 _cache = {}
@@ -43,12 +49,14 @@ def _setup(name):
         import paper_1009_4975_b200 as pb
         opts = (pb.TO_UPLOAD_GENERAL if name.endswith("_general") else 0) | \
                (pb.TO_UPLOAD_LAUNCHED if name.endswith("_launched") else 0) | \
-               (pb.TO_UPLOAD_NO_CLUSTER if name.endswith("_coop") else 0)
+               (pb.TO_UPLOAD_NO_CLUSTER if name.endswith("_coop") else 0) | \
+               (pb.TO_UPLOAD_EP if name.endswith("_ep") else 0)
         hm, m = product_mesh(prob, options=opts)
         if name.startswith(("c3s", "c5s")):
             assert m.info()["structured"] == (0 if name.endswith("_general") else 1)
         # which device path runs the loop (include/tomesh.h matvec_variant)
-        want = {"c1": 5, "c2": 4, "c1_launched": 4, "c2_launched": 4, "c1_coop": 3, "amr2d": 5, "hload2d": 5}
+        want = {"c1": 5, "c2": 4, "c1_launched": 4, "c2_launched": 4, "c1_coop": 3, "amr2d": 5, "hload2d": 5,
+                "c2_ep": 6, "c4s_ep": 6, "amr3d_ep": 6, "hload3d_ep": 6}
         if name in want:
             assert m.info()["matvec_variant"] == want[name], (name, m.info())
         x_dev = product_input_density(prob, hm, m)
@@ -122,7 +130,7 @@ def test_L2_converged_solve(name):
     assert abs(st.iters - ref.cg.iters) <= max(5, 0.05 * ref.cg.iters)
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c1_launched", "c1_coop", "c5s"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c1_launched", "c1_coop", "c5s", "c4s_ep", "c2_ep"])
 def test_warm_start_and_fixed_iterations(name):
     prob, om, hm, m, x_dev = _setup(name)
     u = torch.zeros(om.n_dof, dtype=torch.float64, device="cuda")
@@ -150,7 +158,7 @@ def test_zero_load_gives_zero_solution():
     assert st.iters == 0 and torch.count_nonzero(u) == 0
 
 
-@pytest.mark.parametrize("name", ["c2", "c5s"])
+@pytest.mark.parametrize("name", ["c2", "c5s", "c4s_ep"])
 def test_solver_edge_cases(name):
     """Status codes of include/tomesh.h on both paths: densities outside (0, 1]
     (incl. NaN) -> TO_EINVAL; max_iter = 0 -> no iteration, TO_NOT_CONVERGED, u
@@ -261,7 +269,7 @@ def test_structured_deferred_x_update():
         assert abs(true_res(ug) - sts[0].relres) <= 1e-8 * sts[0].relres, k
 
 
-@pytest.mark.parametrize("name", ["c4s", "amr3d", "c2_launched", "c5s_general"])
+@pytest.mark.parametrize("name", ["c4s", "amr3d", "c2_launched", "c5s_general", "c4s_ep"])
 def test_general_block_decomposition(name):
     """The owner-computes decomposition the general kernel runs on
     (to_mesh_info.gen_*): every element is staged by at least one block and
@@ -276,3 +284,23 @@ def test_general_block_decomposition(name):
     assert info["gen_local_nodes"] >= info["n_node"] - info["n_hang"]
     assert 0 < info["gen_smem_bytes"] <= 113664
     assert info["gen_max_el"] <= 2047 and info["gen_max_loc"] <= 1536
+
+
+@pytest.mark.parametrize("name", ["c4s_ep", "amr3d_ep", "c2_ep"])
+def test_element_partitioned_matches_default_path(name):
+    """The element-partitioned iteration equals the default general path
+    iterate by iterate up to rounding (Chronopoulos-Gear and Hestenes-Stiefel
+    PCG coincide in exact arithmetic): u after 25 fixed iterations at 1e-9,
+    the converged u at 1e-9 with iteration counts within 2."""
+    import paper_1009_4975_b200 as pb
+    prob, om, hm, m, x_dev = _setup(name)
+    _, m0 = product_mesh(prob, options=pb.TO_UPLOAD_LAUNCHED | pb.TO_UPLOAD_NO_EP)
+    assert m0.info()["matvec_variant"] == 4
+    for rtol, n, flags in ((0.0, 25, pb.TO_FIXED_ITERS), (1e-10, 50000, 0)):
+        ua = torch.zeros(om.n_dof, dtype=torch.float64, device="cuda")
+        ub = torch.zeros_like(ua)
+        sa = m.tosolve_cg(prob.penal, x_dev, ua, rtol=rtol, max_iter=n, flags=flags)
+        sb = m0.tosolve_cg(prob.penal, x_dev, ub, rtol=rtol, max_iter=n, flags=flags)
+        assert rel(host(ua), host(ub)) <= 1e-9
+        assert abs(sa.iters - sb.iters) <= 2
+    m0.close()
