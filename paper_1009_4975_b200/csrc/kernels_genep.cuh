@@ -54,6 +54,9 @@ constexpr int kEpMaxAcc = kGfThreads * kEpAccPerThread;            // owned + ha
 #ifndef TOMESH_EP_AUTO
 #define TOMESH_EP_AUTO 0        // 1: meshes with more than kGfStepInMaxBlocks blocks use k_gen_ep by default
 #endif
+#ifndef TOMESH_EP_REDUCE
+#define TOMESH_EP_REDUCE 1      // the shared nodes' partials summed by k_ep_reduce into a w vector
+#endif
 #ifndef TOMESH_EP_OWN3
 #define TOMESH_EP_OWN3 256
 #endif
@@ -123,7 +126,7 @@ k_gen_ep(const __grid_constant__ GenBlocks B, const double *__restrict__ s_loc, 
          const double *__restrict__ so, const double *__restrict__ po, const double *__restrict__ Dinv,
          double *__restrict__ rw, double *__restrict__ sw, double *__restrict__ pw, double *__restrict__ x,
          const __grid_constant__ K0Dense2 K2, const __grid_constant__ K0HadSym H, CgScalars *S,
-         double *partials) {
+         double *partials, const double *__restrict__ wv) {
   constexpr int NC = 1 << DIM, ND = NC * DIM, CH = GfChunk<DIM>::CH, YS = GfChunk<DIM>::YS;
   constexpr int OA = kEpAccPerThread;
   constexpr int OD = kGfMaxOwn * DIM / kGfThreads;   // owned DOFs per thread
@@ -174,8 +177,12 @@ k_gen_ep(const __grid_constant__ GenBlocks B, const double *__restrict__ s_loc, 
       p_o[v] = __ldg(po + g);
       d_o[v] = __ldg(Dinv + g);
       x_o[v] = __ldcg(x + g);
-      const int32_t sa = __ldg(slot_ptr + n), sb = __ldg(slot_ptr + n + 1);
-      w_o[v] = ep_wsum<DIM>(Wo, (uint32_t)sa, sb - sa, j % DIM, d_o[v]);
+      if (TOMESH_EP_REDUCE) {
+        w_o[v] = __ldg(wv + g);   // summed and masked by k_ep_reduce
+      } else {
+        const int32_t sa = __ldg(slot_ptr + n), sb = __ldg(slot_ptr + n + 1);
+        w_o[v] = ep_wsum<DIM>(Wo, (uint32_t)sa, sb - sa, j % DIM, d_o[v]);
+      }
     }
   }
   const bool stopped = cg_stopped(S);
@@ -211,7 +218,7 @@ k_gen_ep(const __grid_constant__ GenBlocks B, const double *__restrict__ s_loc, 
     const int h = j / DIM, i = j % DIM;
     const int64_t g = (int64_t)halo[h] * DIM + i;
     const double d = __ldg(Dinv + g);
-    const double w = ep_wsum<DIM>(Wo, hslot[h], hcnt[h], i, d);
+    const double w = TOMESH_EP_REDUCE ? __ldg(wv + g) : ep_wsum<DIM>(Wo, hslot[h], hcnt[h], i, d);
     const double s = fma(beta, __ldg(so + g), w);
     const double r = fma(-alpha, s, __ldg(ro + g));
     P[nOwn * DIM + j] = d * r;
@@ -301,6 +308,23 @@ k_gen_ep(const __grid_constant__ GenBlocks B, const double *__restrict__ s_loc, 
 #pragma unroll
     for (int k = 0; k < 5; ++k) partials[(size_t)5 * blockIdx.x + k] = dots[k];
   GF_MARK(6);
+}
+
+// w_K = the sum of every node's partial slots (ascending block order, the
+// same arithmetic as ep_wsum everywhere), 0 on non-free DOFs: one coalesced
+// pass between the block kernel of iteration K and the next one, so that the
+// block kernel reads w as a plain vector.
+template <int DIM>
+__global__ void k_ep_reduce(int64_t n, const int32_t *__restrict__ slot_ptr, const double *__restrict__ W,
+                            const double *__restrict__ Dinv, double *__restrict__ wv, const CgScalars *S) {
+  pdl_wait();
+  pdl_release();
+  if (cg_stopped(S)) return;
+  GRID_STRIDE(j, n) {
+    const int64_t node = j / DIM;
+    const int32_t sa = __ldg(slot_ptr + node), sb = __ldg(slot_ptr + node + 1);
+    wv[j] = ep_wsum<DIM>(W, (uint32_t)sa, sb - sa, (int)(j % DIM), __ldg(Dinv + j));
+  }
 }
 
 // After exactly N iterations: r_N, x_N (no operator), rho_N = r_N.Dinv r_N,

@@ -857,6 +857,7 @@ int build_gen_ep(const to_mesh_desc *d, const std::vector<int32_t> &node_hang, c
   RC(allow_smem(m, dim == 3 ? (const void *)k_gen_ep<3> : (const void *)k_gen_ep<2>, m->ep_smem));
   RC(ensure_partials(m, (size_t)nb * 5));
   m->ep_n_slots = n_slots;
+  RC(m->alloc(&m->ep_w, (size_t)std::max<int64_t>(1, m->n_dof)));
   m->ep_local_el = loc_el;
   m->ep_local_nodes = loc_nodes;
   m->gen_ep = true;
@@ -1307,12 +1308,27 @@ int op_cg_ep(to_mesh *m, int k, cudaStream_t st) {
     RC(launch_pdl(k_gen_ep<2>, dim3(m->EB.n_blk), dim3(kGfThreads), m->ep_smem, st, m->EB,
                   (const double *)m->ep_s_loc, (const int32_t *)m->ep_slot_ptr, (const double *)m->ep_W[o],
                   m->ep_W[w], (const double *)m->rb[o], (const double *)m->qb[o], (const double *)m->pb[o],
-                  (const double *)m->dinv, m->rb[w], m->qb[w], m->pb[w], m->x, m->K2, m->KS, m->S, m->partials));
+                  (const double *)m->dinv, m->rb[w], m->qb[w], m->pb[w], m->x, m->K2, m->KS, m->S, m->partials,
+                  (const double *)m->ep_w));
   else
     RC(launch_pdl(k_gen_ep<3>, dim3(m->EB.n_blk), dim3(kGfThreads), m->ep_smem, st, m->EB,
                   (const double *)m->ep_s_loc, (const int32_t *)m->ep_slot_ptr, (const double *)m->ep_W[o],
                   m->ep_W[w], (const double *)m->rb[o], (const double *)m->qb[o], (const double *)m->pb[o],
-                  (const double *)m->dinv, m->rb[w], m->qb[w], m->pb[w], m->x, m->K2, m->KS, m->S, m->partials));
+                  (const double *)m->dinv, m->rb[w], m->qb[w], m->pb[w], m->x, m->K2, m->KS, m->S, m->partials,
+                  (const double *)m->ep_w));
+  m->last_launches++;
+  return 0;
+}
+int op_ep_reduce(to_mesh *m, int k, cudaStream_t st) {
+  if (!TOMESH_EP_REDUCE) return 0;
+  const int w = k & 1;
+  const int g = std::min<int64_t>(grid_for(m->n_dof), (int64_t)4 * kNumSMs);
+  if (m->dim == 2)
+    RC(launch_pdl(k_ep_reduce<2>, dim3(g), dim3(kBlock), 0, st, (int64_t)m->n_dof, (const int32_t *)m->ep_slot_ptr,
+                  (const double *)m->ep_W[w], (const double *)m->dinv, m->ep_w, (const CgScalars *)m->S));
+  else
+    RC(launch_pdl(k_ep_reduce<3>, dim3(g), dim3(kBlock), 0, st, (int64_t)m->n_dof, (const int32_t *)m->ep_slot_ptr,
+                  (const double *)m->ep_W[w], (const double *)m->dinv, m->ep_w, (const CgScalars *)m->S));
   m->last_launches++;
   return 0;
 }
@@ -1430,6 +1446,7 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
     CK(cudaMemsetAsync(m->pb[1], 0, sizeof(double) * n, st));
     // element-partitioned: s_{-2} = qb[1] = 0, p_{-2} = 0, w_{-1} = 0 (slots of buffer 1)
     if (ep) CK(cudaMemsetAsync(m->ep_W[1], 0, sizeof(double) * (size_t)m->ep_n_slots * m->dim, st));
+    if (ep) CK(cudaMemsetAsync(m->ep_w, 0, sizeof(double) * n, st));
   }
   RC(op_rhs(m, r0, st));
   const int gv = grid_for(n);
@@ -1519,6 +1536,7 @@ int solve(to_mesh *m, double penal, const double *x_dev, double *u_dev, double r
       } else if (ep) {
         RC(op_cg_ep(m, launched + k, st));
         if (prof) CK(cudaEventRecord(E[1], st));
+        RC(op_ep_reduce(m, launched + k, st));
         RC(op_cg_ep_step(m, launched + k, rtol, st));
         if (prof) CK(cudaEventRecord(E[2], st));
       } else if (step_in) {

@@ -71,6 +71,7 @@ struct to_mesh {
   double *ep_s_loc = nullptr;
   int32_t *ep_slot_ptr = nullptr;      // node -> its partial slots [n_node + 1]
   double *ep_W[2] = {nullptr, nullptr};   // operator output partials (ping-pong)
+  double *ep_w = nullptr;              // their sums (k_ep_reduce), per DOF
   size_t ep_smem = 0;
   int64_t ep_local_el = 0, ep_local_nodes = 0, ep_n_slots = 0;
   // small meshes: the whole loop in one thread-block cluster (kernels_gencluster.cuh)
