@@ -74,6 +74,11 @@ __device__ __forceinline__ void bulk_load_1d(void *dst, const void *src, unsigne
                : "memory");
 }
 
+// Bulk prefetch of [src, src + bytes) into L2 (src and bytes multiples of 16).
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // 8-byte asynchronous copy global -> shared (LDGSTS), and an mbarrier arrival
 // triggered when all of this thread's prior cp.async copies have completed
 // (.noinc: the arrival is part of the barrier's initial count).

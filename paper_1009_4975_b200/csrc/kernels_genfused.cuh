@@ -91,6 +91,9 @@ constexpr int kGfOwnMin = TOMESH_GF_OWN_MIN;             // smallest block targe
 #ifndef TOMESH_GF_HPRE
 #define TOMESH_GF_HPRE 3        // halo DOFs per thread loaded ahead of the owned update (0, 3, 4, 5: c4L 293, 292, 295, 307 us)
 #endif
+#ifndef TOMESH_GF_PF
+#define TOMESH_GF_PF 1          // next-wave L2 prefetch, in residencies ahead (GenBlocks::pf, set at upload; 0: off)
+#endif
 #ifndef TOMESH_GF_ELMAX
 #define TOMESH_GF_ELMAX 2047    // capping blocks at one chunk (256) split them too finely: c4 62 -> 92 us
 #endif
@@ -300,6 +303,37 @@ __device__ __forceinline__ void gf_issue_record(const GenBlocks &B, const GfView
   mbar_arrive_expect_tx(V.bar, (unsigned)sec.total + s_bytes);
   bulk_load_1d(gsm_raw, B.rec + V.mt.rec_off16, (unsigned)sec.total, V.bar);
   if (s_bytes) bulk_load_1d(V.sl, s_loc + V.mt.el_off, s_bytes, V.bar);
+}
+
+// Lanes 0-6 of warp 0: bulk L2 prefetch of block bn's record, s_e and owned
+// r, q, p, Dinv, x ranges.  bn = blockIdx.x + B.pf is the block that will
+// take over this SM slot about one residency later, so its dependent load
+// chain (meta -> record -> owned/halo loads) starts from L2 instead of HBM;
+// its halo rows are mostly owned rows of the blocks next to it, prefetched
+// by their own predecessors.  Blocks of the last residency prefetch the
+// first ones of the NEXT launch (from the buffers this launch writes, which
+// that launch reads).  Only a cache fill: no effect on results.
+template <int DIM>
+__device__ __forceinline__ void gf_prefetch_block(const GenBlocks &B, int bn, const double *s_loc,
+                                                  const double *ro, const double *qo, const double *po,
+                                                  const double *Dinv, const double *x) {
+  const int lane = threadIdx.x;
+  if (lane >= 7 || bn >= B.n_blk) return;
+  const GfMeta mn = B.meta[bn];
+  uintptr_t a, e;
+  if (lane == 0) {
+    const GfSections sec = gf_sections<DIM>(mn.n_own, mn.n_halo, mn.n_virt, mn.n_el, mn.n_inc, GfChunk<DIM>::CH);
+    a = reinterpret_cast<uintptr_t>(B.rec + mn.rec_off16);
+    e = a + (unsigned)sec.total;
+  } else if (lane == 1) {
+    a = reinterpret_cast<uintptr_t>(s_loc + mn.el_off);
+    e = a + 8u * (unsigned)((mn.n_el + 1) & ~1);
+  } else {
+    const double *v = lane == 2 ? ro : lane == 3 ? qo : lane == 4 ? po : lane == 5 ? Dinv : x;
+    a = reinterpret_cast<uintptr_t>(v + (int64_t)mn.node0 * DIM) & ~(uintptr_t)15;
+    e = (reinterpret_cast<uintptr_t>(v + (int64_t)(mn.node0 + mn.n_own) * DIM) + 15) & ~(uintptr_t)15;
+  }
+  if (e > a) bulk_prefetch_l2(reinterpret_cast<const void *>(a), (unsigned)(e - a));
 }
 
 // Loads of vectors another block may have written in the same kernel (the
@@ -611,6 +645,14 @@ k_gen_fused(const __grid_constant__ GenBlocks B, const double *__restrict__ s_lo
     const bool stopped = cg_stopped(S);
     double alpha = __ldcg(&S->alpha);
     double beta = __ldcg(&S->beta);
+#if TOMESH_GF_PF
+    if (B.pf > 0 && tid < 32) {
+      int bn = blockIdx.x + B.pf;
+      const bool wrap = bn >= B.n_blk;   // the next launch's first wave: it reads this launch's write buffers
+      if (wrap) bn -= B.n_blk;
+      gf_prefetch_block<DIM>(B, bn, s_loc, wrap ? rw : ro, wrap ? qw : qo, wrap ? pw : po, Dinv, x);
+    }
+#endif
     // the halo prefetch needs the record; the stop test is taken after it so
     // that the S round trip overlaps the halo loads (harmless reads if stopped)
     mbar_wait(V.bar, 0);   // (also: no bulk copy may still be writing when the CTA exits)

@@ -589,6 +589,24 @@ int build_gen_blocks(const to_mesh_desc *d, const std::vector<int32_t> &node_han
     RC(allow_smem(m, (const void *)k_gen_fused<2, G_PLAIN>, m->gb_smem));
     RC(allow_smem(m, (const void *)k_gen_persist<2>, m->gb_smem));
   }
+  // next-wave L2 prefetch distance: the CTAs resident at once (a block's
+  // successor in its SM slot is about one full residency later).  Only when
+  // what one iteration streams (records, s_e, the owned r, q, p, Dinv, x)
+  // exceeds the L2: an L2-resident mesh gains nothing (c4: 47.2 -> 48.1 us
+  // with it, c4L: 256-265 -> 241; profiles/r2/general_l2prefetch_ab.txt).  A size rule, not a
+  // timing: the prefetch is a cache fill and never changes a result.
+  B.pf = 0;
+#if TOMESH_GF_PF
+  int l2 = 0;
+  CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, m->device));
+  const size_t streamed = hb.rec.size() + 8 * (size_t)m->gb_n_loc_el + 5 * 8 * (size_t)m->n_owned * d->dim;
+  if (streamed > (size_t)l2) {
+    int per_sm = 0;
+    const void *fn = d->dim == 3 ? (const void *)k_gen_fused<3, G_CG> : (const void *)k_gen_fused<2, G_CG>;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGfThreads, m->gb_smem));
+    if (per_sm > 0 && (int64_t)per_sm * kNumSMs * TOMESH_GF_PF < nb) B.pf = per_sm * kNumSMs * TOMESH_GF_PF;
+  }
+#endif
   RC(ensure_partials(m, (size_t)nb * 10));   // dots of two launches (parity)
   m->gb_local_el = m->gb_local_nodes = 0;
   for (const GfMeta &mt : hb.meta) {

@@ -56,6 +56,7 @@ struct GenBlocks {
   int n_blk, max_loc, max_own, max_rec16, max_el;   // shared-memory sizing: maxima over the blocks
   const GfMeta *meta;
   const uint4 *rec;
+  int pf;   // k_gen_fused: block b prefetches block b + pf's static data and owned vectors into L2 (0: off)
 };
 
 // Send lists of the cluster solver's halo exchange (kernels_gencluster.cuh),
