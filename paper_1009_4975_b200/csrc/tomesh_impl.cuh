@@ -98,10 +98,12 @@ struct to_mesh {
   bool ic_ready = false;
   Ic0View IC{};
   double *ic_kt = nullptr, *ic_L = nullptr, *ic_K0 = nullptr, *ic_y = nullptr;
-  int64_t *ic_lvl_ptr = nullptr, *ic_blvl_ptr = nullptr, *ic_ut_ptr = nullptr, *ic_ut_pos = nullptr;
+  int64_t *ic_ut_ptr = nullptr, *ic_ut_pos = nullptr;
   int32_t *ic_lvl_rows = nullptr, *ic_blvl_rows = nullptr, *ic_ut_row = nullptr;
   std::vector<int64_t> ic_lvl_host;   // level boundaries (host) for the per-level factor launches
   int ic_nlvl = 0, ic_nblvl = 0;
+  int64_t *ic_step_ptr = nullptr, *ic_bstep_ptr = nullptr;   // levels cut into pieces of <= kIc0Warps rows (solves)
+  int ic_nstep = 0, ic_nbstep = 0;
   int *ic_fail = nullptr;
   double ic_setup_ms = 0.0;
   int oc_blocks = 0;

@@ -288,6 +288,18 @@ int ic0_build(to_mesh *m, cudaStream_t st) {
   std::vector<int32_t> lrows, blrows;
   bucket(lv, nl, lptr, lrows);
   bucket(blv, nbl, blptr, blrows);
+  // the solve kernels (k_ic0_tri: 32 warps, a row each) walk "steps": the
+  // levels cut into pieces of at most 32 rows, so that every row goes through
+  // the software pipeline (a barrier between two pieces of one level is
+  // redundant but cheap; arithmetic and order are the level schedule's)
+  auto split = [&](const std::vector<int64_t> &lp, std::vector<int64_t> &sp) {
+    sp.assign(1, 0);
+    for (size_t l = 0; l + 1 < lp.size(); ++l)
+      for (int64_t r = lp[l]; r < lp[l + 1]; r += kIc0Warps) sp.push_back(std::min<int64_t>(r + kIc0Warps, lp[l + 1]));
+  };
+  std::vector<int64_t> slptr, sblptr;
+  split(lptr, slptr);
+  split(blptr, sblptr);
   // device copies
   int64_t *d_ptr, *d_cptr;
   int32_t *d_col, *d_row;
@@ -297,10 +309,12 @@ int ic0_build(to_mesh *m, cudaStream_t st) {
   RC(upload_array(m, &d_row, row.data(), row.size(), st));
   RC(upload_array(m, &d_cptr, cptr.data(), cptr.size(), st));
   RC(upload_array(m, &d_contrib, contrib.data(), std::max<size_t>(1, contrib.size()), st));
-  RC(upload_array(m, &m->ic_lvl_ptr, lptr.data(), lptr.size(), st));
   RC(upload_array(m, &m->ic_lvl_rows, lrows.data(), lrows.size(), st));
-  RC(upload_array(m, &m->ic_blvl_ptr, blptr.data(), blptr.size(), st));
   RC(upload_array(m, &m->ic_blvl_rows, blrows.data(), blrows.size(), st));
+  RC(upload_array(m, &m->ic_step_ptr, slptr.data(), slptr.size(), st));
+  RC(upload_array(m, &m->ic_bstep_ptr, sblptr.data(), sblptr.size(), st));
+  m->ic_nstep = (int)slptr.size() - 1;
+  m->ic_nbstep = (int)sblptr.size() - 1;
   RC(upload_array(m, &m->ic_ut_ptr, ut_ptr.data(), ut_ptr.size(), st));
   RC(upload_array(m, &m->ic_ut_row, ut_row.data(), std::max<size_t>(1, ut_row.size()), st));
   RC(upload_array(m, &m->ic_ut_pos, ut_pos.data(), std::max<size_t>(1, ut_pos.size()), st));
@@ -360,9 +374,10 @@ int op_ic0_setup(to_mesh *m, cudaStream_t st, double *shift) {
 
 // z = (L L^T)^-1 v
 int op_ic0_solve(to_mesh *m, const double *v, double *z, cudaStream_t st) {
-  k_ic0_fwd<<<1, 1024, 0, st>>>(m->IC, m->ic_lvl_ptr, m->ic_nlvl, m->ic_lvl_rows, m->ic_L, v, m->ic_y);
-  k_ic0_bwd<<<1, 1024, 0, st>>>(m->IC, m->ic_ut_ptr, m->ic_ut_row, m->ic_ut_pos, m->ic_blvl_ptr, m->ic_nblvl,
-                                m->ic_blvl_rows, m->ic_L, m->ic_y, z);
+  k_ic0_tri<false><<<1, 32 * kIc0Warps, 0, st>>>(m->IC, nullptr, nullptr, nullptr, m->ic_step_ptr, m->ic_nstep,
+                                                 m->ic_lvl_rows, m->ic_L, v, m->ic_y);
+  k_ic0_tri<true><<<1, 32 * kIc0Warps, 0, st>>>(m->IC, m->ic_ut_ptr, m->ic_ut_row, m->ic_ut_pos, m->ic_bstep_ptr,
+                                                m->ic_nbstep, m->ic_blvl_rows, m->ic_L, m->ic_y, z);
   m->last_launches += 2;
   return check_launch();
 }
