@@ -31,7 +31,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .api import HostMesh
+from .api import HostMesh, Mesh, ipc_close, ipc_open
 
 
 def node_incidence(host: HostMesh):
@@ -173,22 +173,35 @@ def exchange_lists(slabs):
     return slabs
 
 
-def send_entries(slabs, rank):
-    """Rank `rank`'s ghost-store list for to_gshard_attach: (destination rank,
-    local owned node, the destination's local ghost node) per entry."""
-    sl = slabs[rank]
+def send_entries_from(recvs, rank, n0):
+    """Rank `rank`'s ghost-store list for to_gshard_attach from every rank's
+    receive lists: recvs[r] = {source rank: (r's local ghost nodes, their
+    global node ids)}; n0 = this rank's first owned global node.  Returns
+    (destination rank, local owned node, the destination's local ghost node)
+    per entry, destinations in rank order."""
     dst, loc, rem = [], [], []
-    for other in slabs:
-        if other.rank == rank or rank not in other.recv:
+    for r, rv in enumerate(recvs):
+        if r == rank or rank not in rv:
             continue
-        idx = other.recv[rank]                                  # other's ghost slots fed by this rank
-        g = other.node_global[idx]
-        dst.append(np.full(idx.shape[0], other.rank, dtype=np.int32))
-        loc.append((g - sl.n0).astype(np.int32))
+        idx, g = rv[rank]                                       # r's ghost slots fed by this rank
+        idx = np.asarray(idx)
+        dst.append(np.full(idx.shape[0], r, dtype=np.int32))
+        loc.append((np.asarray(g) - n0).astype(np.int32))
         rem.append(idx.astype(np.int32))
     if not dst:
         return np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32)
     return np.concatenate(dst), np.concatenate(loc), np.concatenate(rem)
+
+
+def recv_lists(slab):
+    """What a rank publishes to its peers: per source rank, its local ghost
+    nodes and their global ids (the owner turns them into its send list)."""
+    return {s: (idx, slab.node_global[idx]) for s, idx in slab.recv.items()}
+
+
+def send_entries(slabs, rank):
+    """send_entries_from for a group whose slabs all live in this process."""
+    return send_entries_from([recv_lists(sl) for sl in slabs], rank, slabs[rank].n0)
 
 
 def element_owner(host: HostMesh, ranges):
@@ -215,7 +228,6 @@ class AmrShardGroup:
     device-to-device, the all-reduce the slot / flag protocol)."""
 
     def __init__(self, host: HostMesh, nranks: int, E0=1.0, Emin=1e-9, nu=0.3, device=0):
-        from .api import Mesh
         self.host = host
         inc = node_incidence(host)
         self.ranges = partition(host, nranks, inc[0])
@@ -251,3 +263,83 @@ class AmrShardGroup:
         for sl, v, own in zip(self.slabs, vs, self.elem_owned):
             out[sl.elem_global[own]] = v.detach().cpu().numpy()[own]
         return out
+
+
+class AmrShardRank:
+    """One Morton node range per process and GPU (torchrun), the general-path
+    counterpart of shard.ShardRank: every rank cuts its own local mesh from
+    the global host mesh (the partition is a deterministic function of it),
+    the receive lists and the CUDA IPC handles of the CG vectors, Dinv, x and
+    the all-reduce slots / flags travel through ``dist.all_gather_object``
+    (plumbing), every peer's buffers are mapped (one mapping per IPC handle),
+    and tosolve_cg_group drives this rank's handle alone: the exchanges and
+    the all-reduce are the device-side peer stores and flags."""
+
+    FIELDS = [("rb", 0), ("rb", 1), ("pb", 0), ("pb", 1), ("qb", 0), ("qb", 1), ("x", None), ("slots", None),
+              ("flags", None), ("dinv", None)]
+
+    def __init__(self, host: HostMesh, E0=1.0, Emin=1e-9, nu=0.3, device=0, group=None):
+        import torch.distributed as dist
+        from . import _lib as L
+        single = not (dist.is_available() and dist.is_initialized())
+        rank, nranks = (0, 1) if single else (dist.get_rank(group), dist.get_world_size(group))
+        inc = node_incidence(host)
+        self.ranges = partition(host, nranks, inc[0])
+        self.slab = slice_host(host, nranks, rank, self.ranges, inc)
+        self.device = device
+        self.mesh = Mesh(self.slab.host, E0=E0, Emin=Emin, nu=nu, rmin=0.0, device=device, n_owned=self.slab.n_own)
+        mine = self.mesh.shard_buffers()
+
+        def ptr(b, f, i):
+            v = getattr(b, f)
+            return v[i] if i is not None else v
+
+        exported = {"recv": recv_lists(self.slab),
+                    "ipc": [self.mesh.ipc_export(ptr(mine, f, i)) for f, i in self.FIELDS]}
+        allx = [None] * nranks
+        if single:
+            allx[0] = exported
+        else:
+            dist.all_gather_object(allx, exported, group=group)
+        self._opened = []
+        opened = {}   # one mapping per IPC handle (small buffers may share an allocation block)
+
+        def open_ptr(h, off):
+            if h not in opened:
+                opened[h] = ipc_open(device, h, 0)
+                self._opened.append(opened[h])
+            return opened[h] + off
+
+        peers = []
+        for r, ex in enumerate(allx):
+            if r == rank:
+                peers.append(mine)
+                continue
+            b = L.ToShardBufs()
+            for (f, i), (h, off) in zip(self.FIELDS, ex["ipc"]):
+                p = open_ptr(h, off)
+                if i is not None:
+                    getattr(b, f)[i] = p
+                else:
+                    setattr(b, f, p)
+            peers.append(b)
+        self.mesh.gshard_attach(rank, nranks, peers,
+                                *send_entries_from([ex["recv"] for ex in allx], rank, self.slab.n0))
+        self.elem_owned = element_owner(host, self.ranges)[self.slab.elem_global] == rank
+        if not single:
+            dist.barrier(group=group)
+
+    def solve(self, penal, x, u, rtol=1e-10, max_iter=20000, flags=0, stream=None):
+        from . import _lib as L
+        from .api import tosolve_cg_group
+        return tosolve_cg_group([self.mesh], penal, [x], [u], rtol, max_iter, flags | L.TO_NO_TRUE_RES,
+                                None if stream is None else [stream])[0]
+
+    def close(self):
+        for p in self._opened:
+            try:
+                ipc_close(self.device, p)
+            except Exception:
+                pass
+        self._opened = []
+        self.mesh.close()

@@ -147,3 +147,93 @@ def test_amr_partition_gloo_world2():
         assert p.exitcode == 0
     res = [q.get(timeout=10) for _ in range(2)]
     assert all(ok for _, ok, _ in res) and all(ng > 0 for _, _, ng in res)
+
+
+def _rank_worker(rank, ws, port, out):
+    """AmrShardRank's host plumbing with the device calls replaced by fakes:
+    the receive lists and IPC handles through all_gather_object, every peer
+    buffer mapped once per handle at the right offset, and the send entries it
+    hands to to_gshard_attach equal to the ones the in-process group builds."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(ws))
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    import paper_1009_4975_b200 as pb_
+    from paper_1009_4975_b200 import _lib as L
+    from paper_1009_4975_b200 import amr_shard as ash
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    try:
+        base = 1 << 40 | rank << 32            # fake device addresses of this rank
+        opened, seen = [], {}
+        offs = {("rb", 0): 0x100, ("rb", 1): 0x200, ("pb", 0): 0x300, ("pb", 1): 0x400, ("qb", 0): 0x500,
+                ("qb", 1): 0x600, ("x", None): 0x700, ("dinv", None): 0x800, ("slots", None): 0x10000,
+                ("flags", None): 0x10100}       # slots + flags share one allocation block
+
+        class FakeMesh:
+            def __init__(self, host, **kw):
+                self.host, self.kw = host, kw
+
+            def shard_buffers(self):
+                b = L.ToShardBufs()
+                for (f, i), o in offs.items():
+                    if i is None:
+                        setattr(b, f, base + o)
+                    else:
+                        getattr(b, f)[i] = base + o
+                return b
+
+            def ipc_export(self, ptr):
+                blk = ptr & ~0xFFFF
+                return (f"r{rank}-{blk:x}".encode().ljust(64, b"\0"), ptr - blk)
+
+            def gshard_attach(self, r, n, peers, dst, loc, rem):
+                seen.update(rank=r, n=n, send=(dst.tolist(), loc.tolist(), rem.tolist()),
+                            peers=[{(f, i): ((getattr(p, f)[i] if i is not None else getattr(p, f)) or 0)
+                                    for f, i in offs} for p in peers])
+
+            def close(self):
+                pass
+
+        def fake_open(device, h, off):
+            opened.append(h)
+            owner = int(h.split(b"-")[0][1:])
+            blk = int(h.rstrip(b"\0").split(b"-")[1], 16)
+            assert blk >> 32 == (1 << 8 | owner) and off == 0
+            return blk
+
+        ash.Mesh, ash.ipc_open, ash.ipc_close = FakeMesh, fake_open, lambda d, p: None
+        hm = pb_.prepare(CASES["c4s"]())
+        sr = ash.AmrShardRank(hm)
+        ok = seen["rank"] == rank and seen["n"] == ws and sr.mesh.kw["n_owned"] == sr.slab.n_own
+        ok &= len(set(opened)) == len(opened) == 2 * (ws - 1)   # one mapping per handle: vectors block, slots block
+        for r, p in enumerate(seen["peers"]):
+            ok &= all(p[k] == (1 << 40 | r << 32) + o for k, o in offs.items())
+        # the same entries as the in-process group's (which slices every rank here)
+        slabs = ash.exchange_lists([ash.slice_host(hm, ws, r) for r in range(ws)])
+        dst, loc, rem = ash.send_entries(slabs, rank)
+        ok &= seen["send"] == (dst.tolist(), loc.tolist(), rem.tolist()) and len(seen["send"][0]) > 0
+        ok &= all(0 <= l < sr.slab.n_own for l in seen["send"][1])
+        # every element is reported by exactly one rank
+        allown = [None] * ws
+        dist.all_gather_object(allown, sr.slab.elem_global[sr.elem_owned].tolist())
+        flat = sorted(e for a in allown for e in a)
+        ok &= flat == list(range(hm.n_el))
+        out.put((rank, bool(ok)))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_amr_shard_rank_plumbing_gloo_world3():
+    pytest.importorskip("torch")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(240)
+        assert p.exitcode == 0
+    res = dict(q.get(timeout=10) for _ in range(3))
+    assert res == {0: True, 1: True, 2: True}

@@ -80,3 +80,27 @@ def test_amr_sharded_fixed_iterations_and_errors():
     with pytest.raises(pb.TomeshError) as ei:
         g.solve(prob.penal, xb, us, rtol=1e-8, max_iter=100)
     assert ei.value.code == pb.TO_EINVAL
+
+
+def test_amr_shard_rank_single_process_form():
+    """AmrShardRank (one Morton range per process; here world size 1, no
+    process group): the real IPC export of its buffers, the attach with an
+    empty send list and the group solve of its one handle equal the oracle."""
+    prob = CASES["hload3d"]()
+    hm = pb.prepare(prob)
+    om = omesh.build_mesh(prob)
+    x = density_at(prob, hm.elem_level, hm.elem_anchor)
+    ref = pipeline.run(prob, rtol=1e-10, m=om, x=x)
+    sr = amr_shard.AmrShardRank(hm, E0=prob.E0, Emin=prob.Emin, nu=prob.nu)
+    try:
+        assert sr.slab.n_own == hm.n_node and sr.elem_owned.all()
+        xd = cuda(x)[torch.as_tensor(sr.slab.elem_global, device="cuda")]
+        u = torch.zeros(sr.mesh.n_dof, dtype=torch.float64, device="cuda")
+        st = sr.solve(prob.penal, xd, u, rtol=1e-10, max_iter=50000)
+        assert st.status == 0 and abs(st.iters - ref.cg.iters) <= max(5, 0.05 * ref.cg.iters)
+        un = np.zeros(hm.n_dof)
+        d = hm.dim
+        un.reshape(-1, d)[sr.slab.node_global[:sr.slab.n_own]] = host(u).reshape(-1, d)[:sr.slab.n_own]
+        assert rel(un, ref.u) <= 1e-8
+    finally:
+        sr.close()
