@@ -767,6 +767,118 @@ def run_shard(args):
     return 0
 
 
+def run_amr_shard(args):
+    """--amr-shard: ONE c4L solve (the general / AMR path, reading R26)
+    split into Morton node ranges over the N ranks (SURVEY §8(e);
+    paper_1009_4975_b200/amr_shard.py AmrShardRank): every rank uploads its
+    local mesh, the ghost r, p, q travel by peer stores (CUDA IPC mappings)
+    and the dots by the device-side all-reduce.  Strong scaling: value =
+    iterations/s of the one global solve; a step is 200 fixed PCG iterations
+    plus the sensitivities (the filter is not sharded)."""
+    import torch
+    import paper_1009_4975_b200 as pb
+    from paper_1009_4975_b200 import amr_shard
+    from inputs import density_at
+    from inputs.problems import config_c4L
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")          # plumbing only: receive lists, IPC handles, barriers, the max
+    dev = torch.device("cuda", local)
+    prob = config_c4L()
+    iters = 200
+    hm = pb.prepare(prob)
+    sr = amr_shard.AmrShardRank(hm, E0=prob.E0, Emin=prob.Emin, nu=prob.nu, device=local)
+    sl, m = sr.slab, sr.mesh
+    stream = torch.cuda.Stream(device=dev)
+    x_glob = density_at(prob, hm.elem_level, hm.elem_anchor)
+    x_host = torch.from_numpy(np.ascontiguousarray(x_glob[sl.elem_global])).pin_memory()
+    x = x_host.to(dev)
+    u = torch.zeros(m.n_dof, dtype=torch.float64, device=dev)
+    dc = torch.empty(m.n_el, dtype=torch.float64, device=dev)
+
+    def step(extra=0):
+        st = sr.solve(prob.penal, x, u, rtol=0.0, max_iter=iters, flags=pb.TO_FIXED_ITERS | extra, stream=stream)
+        m.to_sensitivity(prob.penal, x, u, dc, stream=stream)
+        return st
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    l0 = m.info()["launches_total"]
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    launches = m.info()["launches_total"] - l0
+    barrier()
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1), ws)
+    dc_host = torch.empty(m.n_el, dtype=torch.float64).pin_memory()
+    barrier()
+    torch.cuda.synchronize(dev)
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            x.copy_(x_host, non_blocking=True)
+        step()
+        with torch.cuda.stream(stream):
+            dc_host.copy_(dc, non_blocking=True)
+    e3.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = max_over_ranks(e2.elapsed_time(e3), ws)
+    step(pb.TO_PROFILE_LOOP)
+    torch.cuda.synchronize(dev)
+    p = m.profile()
+    it_ms = max_over_ranks(p["loop_ms"] / max(1, p["iters"]), ws)
+    kb = general_bytes(sl.host)                  # §8(d) bytes of this rank's local mesh (ghosts included)
+    hbm, peak_kind = _peaks()
+    if rank == 0:
+        line = {
+            "metric": "pcg_iterations_per_sec", "value": iters * args.steps / (ms / 1000.0), "unit": "iterations/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": prob.name, "n_elem": hm.n_el, "n_dof": hm.n_dof, "iters_per_solve": iters,
+                       "step": "simp+diag+rhs+200 PCG its+recover+sens, Morton node-range sharded general path",
+                       "parallelism": f"morton{ws}", "rank0_nodes": [int(sl.n0), int(sl.n1)],
+                       "rank0_ghosts": int(sl.n_ghost),
+                       "l2": "inputs larger than L2 at N <= 2 (c4L streams ~440 MB per iteration)"},
+            "comm": "device_peer_stores", "gpus_active": ws,
+            "dof_matvecs_per_sec": iters * args.steps / (ms / 1000.0) * hm.n_dof,
+            "e2e": {"value": iters * args.steps / (e2e_ms / 1000.0), "unit": "iterations/s",
+                    "h2d_bytes_per_step": m.n_el * 8, "d2h_bytes_per_step": m.n_el * 8},
+            "roofline": {"bound": "hbm", "achieved": kb / (it_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": kb / (it_ms / 1000.0) / 1e9 / hbm, "traffic": None,
+                         "kernel": "k_gen_fused<3, CG> + k_gshard_xchg + k_shard_step per iteration (rank 0)",
+                         "algorithmic_bytes_per_launch": kb, "avg_launch_ms": it_ms, "peak_source": peak_kind},
+            "cpu_baseline": None, "clocks": clk, "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    sr.close()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -779,6 +891,8 @@ def main():
     ap.add_argument("--no-general", action="store_true", help="skip the c4L general-path sub-record")
     ap.add_argument("--shard", action="store_true",
                     help="split ONE c5 solve into z-slabs over the ranks (strong scaling)")
+    ap.add_argument("--amr-shard", action="store_true",
+                    help="split ONE c4L (general / AMR path) solve into Morton node ranges over the ranks")
     ap.add_argument("--weak", action="store_true", help="the weak-scaled sharded solve even at N = 1")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: N independent c5 solves (no data-path collective) instead of the weak-scaled "
@@ -788,6 +902,8 @@ def main():
         return run_reference(args)
     if args.shard:
         return run_shard(args)
+    if args.amr_shard:
+        return run_amr_shard(args)
     if args.weak or (_dist()[0] > 1 and not args.replicas):
         return run_weak(args)
     return run_ours(args)
