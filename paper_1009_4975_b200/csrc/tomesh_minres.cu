@@ -342,7 +342,7 @@ int ic0_build(to_mesh *m, cudaStream_t st) {
 // K~ (+ a I) assembled and factored; a = 0, then 1e-3 2^t until no pivot fails
 int op_ic0_setup(to_mesh *m, cudaStream_t st, double *shift) {
   if (m->structured) {
-    set_error("IC(0) needs the general (canonical-order) operator path; upload with TOMESH_FORCE_GENERAL=1");
+    set_error("IC(0) needs the general (canonical-order) operator path; upload with the TO_UPLOAD_GENERAL option");
     return TO_EINVAL;
   }
   if (!m->ic_ready) RC(ic0_build(m, st));
