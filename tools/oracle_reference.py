@@ -29,7 +29,24 @@ import numpy as np  # noqa: E402
 
 from inputs import config  # noqa: E402
 from oracle import mesh as omesh, pipeline  # noqa: E402
-from tests.oracle_cache import cache_path, input_key, variant  # noqa: E402
+from tests.oracle_cache import (N_SAMPLE_DOF, N_SAMPLE_EL, cache_path, digest_path, input_key,  # noqa: E402
+                                sample_indices, variant)
+
+
+def write_digest(name, key, path):
+    """tests/golden/oracle_ref_digest_<name>_<key>.npz from the cached oracle
+    solution at `path`: sampled entries of u, dc and the filtered dc (indices a
+    function of the key), the compliance and the solve's meta."""
+    ref = np.load(path)
+    u, dc, dcf = ref["u"], ref["dc"], ref["dcf"]
+    sd = sample_indices(key, u.shape[0], N_SAMPLE_DOF, 1)
+    se = sample_indices(key, dc.shape[0], N_SAMPLE_EL, 2)
+    out = digest_path(name, key)
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    np.savez_compressed(out, u=u[sd], dc=dc[se], dcf=dcf[se], compliance=ref["compliance"], meta=ref["meta"],
+                        n_dof=np.int64(u.shape[0]), n_el=np.int64(dc.shape[0]),
+                        idx_sum=np.int64(sd.sum() + se.sum()))
+    print(f"{name}: digest {os.path.relpath(out, ROOT)} ({os.path.getsize(out) / 1e6:.2f} MB)", flush=True)
 
 
 def main():
@@ -46,6 +63,8 @@ def main():
         path = cache_path(name, key)
         if os.path.exists(path):
             print(f"{name}: {path} exists", flush=True)
+            if not os.path.exists(digest_path(name, key)):
+                write_digest(name, key, path)
             continue
         t_mesh = time.perf_counter() - t0
         print(f"{name}: n_el={om.n_el} n_dof={om.n_dof} n_hang={om.hang_node.shape[0]} "
@@ -60,6 +79,7 @@ def main():
         np.savez(tmp, u=r.u, dc=r.dc, dcf=r.dc_filtered, compliance=np.float64(r.compliance),
                  meta=json.dumps(meta))
         os.replace(tmp, path)
+        write_digest(name, key, path)
         print(json.dumps(meta), flush=True)
 
 
