@@ -25,7 +25,7 @@
 
 namespace tomesh {
 
-constexpr int kIc0Warps = 32;   // warps of the one-CTA triangular solves = rows per step
+constexpr int kIc0Warps = 32;   // most warps of the one-CTA triangular solves (= rows per step); per mesh: to_mesh::ic_warps
 
 template <int DIM>
 __global__ void k_ic0_assemble(Ic0View V, const double *__restrict__ s, const double *__restrict__ msc,
@@ -87,7 +87,7 @@ __global__ void k_ic0_factor(Ic0View V, const int32_t *__restrict__ lvl_rows, in
 // critical path of a level is the gather of the solution entries, the warp
 // sum, the division and the CTA barrier (round 1: four dependent loads per
 // level, ~2.7 us; the arithmetic and its order are unchanged).  The host
-// hands over the levels cut into steps of at most kIc0Warps rows, so every
+// hands over the levels cut into steps of at most blockDim / 32 rows, so every
 // row is a warp's first of its step; entries beyond 64 of a row (and rows
 // beyond the first, if a caller passes whole levels) take the plain loop.
 //   BWD: the rows of L^T through the transposed pattern (ut_ptr, ut_row,

@@ -104,6 +104,7 @@ struct to_mesh {
   int ic_nlvl = 0, ic_nblvl = 0;
   int64_t *ic_step_ptr = nullptr, *ic_bstep_ptr = nullptr;   // levels cut into pieces of <= kIc0Warps rows (solves)
   int ic_nstep = 0, ic_nbstep = 0;
+  int ic_warps = 32;                                         // warps of the solve CTA = rows per step
   int *ic_fail = nullptr;
   double ic_setup_ms = 0.0;
   int oc_blocks = 0;

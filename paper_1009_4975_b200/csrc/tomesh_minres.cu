@@ -288,14 +288,22 @@ int ic0_build(to_mesh *m, cudaStream_t st) {
   std::vector<int32_t> lrows, blrows;
   bucket(lv, nl, lptr, lrows);
   bucket(blv, nbl, blptr, blrows);
-  // the solve kernels (k_ic0_tri: 32 warps, a row each) walk "steps": the
-  // levels cut into pieces of at most 32 rows, so that every row goes through
+  // the solve kernels (k_ic0_tri: ic_warps warps, a row each) walk "steps": the
+  // levels cut into pieces of at most ic_warps rows, so that every row goes through
   // the software pipeline (a barrier between two pieces of one level is
   // redundant but cheap; arithmetic and order are the level schedule's)
+  // warps per CTA: about twice the mean rows per level (idle warps still pay
+  // the per-step bookkeeping and the barrier: c1, 5.6 rows per level, 130 ms
+  // with 32 warps, 112 with 16; c2, 14 rows per level, 3.54 s with 32, 3.65 s
+  // with 16; profiles/r2/ic0_tri_ab.txt)
+  const double mean_rows = (double)n / std::max(1, std::max(nl, nbl));
+  int W = 8;
+  while (W < kIc0Warps && W < 2.0 * mean_rows) W *= 2;
+  m->ic_warps = W;
   auto split = [&](const std::vector<int64_t> &lp, std::vector<int64_t> &sp) {
     sp.assign(1, 0);
     for (size_t l = 0; l + 1 < lp.size(); ++l)
-      for (int64_t r = lp[l]; r < lp[l + 1]; r += kIc0Warps) sp.push_back(std::min<int64_t>(r + kIc0Warps, lp[l + 1]));
+      for (int64_t r = lp[l]; r < lp[l + 1]; r += W) sp.push_back(std::min<int64_t>(r + W, lp[l + 1]));
   };
   std::vector<int64_t> slptr, sblptr;
   split(lptr, slptr);
@@ -374,9 +382,9 @@ int op_ic0_setup(to_mesh *m, cudaStream_t st, double *shift) {
 
 // z = (L L^T)^-1 v
 int op_ic0_solve(to_mesh *m, const double *v, double *z, cudaStream_t st) {
-  k_ic0_tri<false><<<1, 32 * kIc0Warps, 0, st>>>(m->IC, nullptr, nullptr, nullptr, m->ic_step_ptr, m->ic_nstep,
+  k_ic0_tri<false><<<1, 32 * m->ic_warps, 0, st>>>(m->IC, nullptr, nullptr, nullptr, m->ic_step_ptr, m->ic_nstep,
                                                  m->ic_lvl_rows, m->ic_L, v, m->ic_y);
-  k_ic0_tri<true><<<1, 32 * kIc0Warps, 0, st>>>(m->IC, m->ic_ut_ptr, m->ic_ut_row, m->ic_ut_pos, m->ic_bstep_ptr,
+  k_ic0_tri<true><<<1, 32 * m->ic_warps, 0, st>>>(m->IC, m->ic_ut_ptr, m->ic_ut_row, m->ic_ut_pos, m->ic_bstep_ptr,
                                                 m->ic_nbstep, m->ic_blvl_rows, m->ic_L, m->ic_y, z);
   m->last_launches += 2;
   return check_launch();
